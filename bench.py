@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""bench.py — fwd+bwd slices/s of the B200 slice renderer (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): a 512x512x128 unit-spacing
+volume, 1M Gaussians from the reference's init_random(seed 1) (bit-identical
+stream, host-generated), PSF sigma_z = 1, RasterConfig defaults. One "step" is
+U1 = prepare_gaussians + tile binning + rasterize + backward for one slice with
+a fixed synthetic dL/dI, producing the dense (N x 11) gradient — the reference's
+prepare_gaussians + rasterize_prepared + backward_prepared (optimize.hpp:386-395).
+Slices cycle over 16 mid-stack indices. Inputs are resident in HBM; L2 (126 MB)
+is flushed by a 256 MiB write before every timed step, outside the per-step
+CUDA-event window.
+
+Multi-GPU (torchrun): slices are sharded across ranks (rank r takes its own
+slice each step) with one NCCL all-reduce of the dense gradient per step; the
+reported value is all ranks' slices / max-over-ranks device time (weak scaling).
+
+--impl reference: the reference CPU implementation (oracle/_ref, the unmodified
+reference headers) on this host's cores, same config and metric, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fwd+bwd slices/s (1/8 GPU) at 512²×128 vol, 1M Gaussians; % HBM roofline"
+CONFIGS = {
+    "c1": dict(dims=(128, 128, 32), n=20_000, sigma_z=1.0,
+               name="synthetic 128x128x32 volume, 20k Gaussians, sigma_z=1"),
+    "c2": dict(dims=(512, 512, 128), n=1_000_000, sigma_z=1.0,
+               name="light-sheet-like synthetic 512x512x128 stack, 1M Gaussians, sigma_z=1"),
+    "c3": dict(dims=(256, 256, 320), n=500_000, sigma_z=3.0,
+               name="ABUS-like 256x256x320 volume, thick-slice PSF sigma_z=3, 500k Gaussians"),
+    "c5": dict(dims=(2048, 2048, 256), n=8_000_000, sigma_z=1.0,
+               name="large microscopy 2048x2048x256 stack, 8M Gaussians, sigma_z=1"),
+}
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def geometry(cfg):
+    X, Y, Z = cfg["dims"]
+    lo = (-0.5, -0.5, -0.5)
+    hi = (X - 0.5, Y - 0.5, Z - 0.5)
+    return lo, hi
+
+
+def slice_indices(Z):
+    return [Z // 2 - 8 + i for i in range(16)]
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config):
+    """dram__bytes_read+write per K_prep launch from the committed ncu capture."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get(config, {}).get("k_prep", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Polls NVML during the timed region (SM clock + throttle reasons)."""
+
+    REASONS = {
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sync_boost": 0x10,
+        "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def result(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------
+def cpu_reference_rate(cfg, rec, seconds_budget, max_reps=None):
+    """Reference CPU U1 (oracle/_ref) on this host's cores. Returns dict."""
+    import ctypes as C
+
+    from oracle.bindings import Bounds, CfgC, PoseC, PsfC, load
+    import paper_2603_20611_b200 as gp
+
+    ref = load("ref")
+    L = ref.lib
+    cores = os.cpu_count() or 1
+    L.gref_set_threads(0)  # worker_cap() = 0 -> hardware_concurrency (parallel.hpp:14-20)
+    workers = L.gref_effective_workers()
+    X, Y, Z = cfg["dims"]
+    lo, hi = geometry(cfg)
+    b = Bounds((C.c_double * 3)(*lo), (C.c_double * 3)(*hi))
+    L.gref_set_new.restype = C.c_void_p
+    h = L.gref_set_new(C.c_uint64(rec.shape[0]), rec.ctypes.data_as(C.POINTER(C.c_double)), C.byref(b))
+    ks = slice_indices(Z)
+    poses = (PoseC * len(ks))()
+    for i, k in enumerate(ks):
+        p = gp.slice_pose_for_index(cfg["dims"], (1, 1, 1), (0, 0, 0), k)
+        r = np.asarray(p.rotation, np.float64).reshape(9)
+        poses[i] = PoseC((C.c_double * 9)(*r), (C.c_double * 3)(*p.translation), p.width, p.height,
+                         (C.c_double * 2)(*p.pixel_spacing), (C.c_double * 2)(*p.principal_point))
+    psf = PsfC(1.0, 1.0, cfg["sigma_z"])
+    rc = CfgC(0.02, 16, 3.0, 1.0)
+    dl = synthetic_dl_di(cfg).astype(np.float64)
+    secs = np.zeros(3)
+
+    def run(reps):
+        st = L.gref_time_u1(C.c_void_p(h), poses, len(ks), C.byref(psf), C.byref(rc),
+                            dl.ctypes.data_as(C.POINTER(C.c_double)), reps,
+                            secs.ctypes.data_as(C.POINTER(C.c_double)))
+        if st != 0:
+            raise RuntimeError("reference U1 failed")
+        return secs.sum(), secs.copy()
+
+    t1, _ = run(1)  # warm (page-in, allocator)
+    reps = max(1, int(seconds_budget / max(t1, 1e-6)))
+    if max_reps:
+        reps = min(reps, max_reps)
+    t, parts = run(reps)
+    L.gref_set_free(C.c_void_p(h))
+    return {
+        "value": reps / t, "unit": "slices/s", "cores": int(workers), "host_cpus": cores,
+        "kind": "reference", "reps": reps, "seconds": t,
+        "stage_seconds_per_slice": {"prepare": parts[0] / reps, "rasterize": parts[1] / reps,
+                                    "backward": parts[2] / reps},
+        "sample": f"{reps} U1 slices (prepare_gaussians+rasterize_prepared+backward_prepared) of "
+                  f"{cfg['name']}, oracle/_ref with {workers} threads",
+    }
+
+
+def synthetic_dl_di(cfg):
+    X, Y, _ = cfg["dims"]
+    rng = np.random.default_rng(7)
+    return (rng.uniform(-1.0, 1.0, (Y, X)) / (X * Y)).astype(np.float32)
+
+
+def make_records(cfg):
+    import paper_2603_20611_b200 as gp
+
+    lo, hi = geometry(cfg)
+    gs = gp.init_random(cfg["n"], lo, hi, 1.5, 1)
+    # the device stores f32; both arms see the same f32-representable values
+    return gp.GaussianSet(gs.records.astype(np.float32).astype(np.float64), lo, hi)
+
+
+def config_json(args, cfg, world):
+    X, Y, Z = cfg["dims"]
+    return {"workload": cfg["name"], "unit_of_work": "U1 fwd+bwd slice (prepare+bin+raster+backward, dense grads)",
+            "volume": [X, Y, Z], "gaussians": cfg["n"], "sigma_z": cfg["sigma_z"],
+            "slices": f"{len(slice_indices(Z))} mid-stack indices, cycled",
+            "parallelism": f"slice-sharded dp{world}", "l2": "flushed (256 MiB write) before each timed step",
+            "config_id": args.config}
+
+
+# ---------------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    gs = make_records(cfg)
+    budget = min(150.0, max(10.0, 1.0 * args.steps))
+    res = cpu_reference_rate(cfg, gs.records, budget, max_reps=args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "slices/s",
+        "n_gpus": args.gpus, "steps": res["reps"], "warmup": 1, "ms_per_step": 1000.0 / res["value"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (init_random seed 1, dL/dI U(-1,1)/P seed 7)",
+        "config": config_json(args, cfg, world),
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": "slices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "stage_seconds_per_slice": res["stage_seconds_per_slice"],
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2603_20611_b200 as gp
+    from paper_2603_20611_b200 import _native as N
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = CONFIGS[args.config]
+    X, Y, Z = cfg["dims"]
+    P = X * Y
+    gs = make_records(cfg)
+    n = gs.size()
+    stream = torch.cuda.current_stream()
+    sess = gp.Session(local, stream=stream.cuda_stream)
+    sess.set_gaussians(gs)
+    sess.reserve_pairs(max(1 << 20, n))
+    psf = gp.PsfSpec(sigma_z=cfg["sigma_z"])
+    rcfg = gp.RasterConfig()
+    ks = slice_indices(Z)
+    poses = [gp.slice_pose_for_index(cfg["dims"], (1, 1, 1), (0, 0, 0), k) for k in ks]
+
+    if world > 1:
+        uid = bytearray(128)
+        if rank == 0:
+            buf = (gp.api.C.c_char * 128)()
+            N.check(N.lib.gpk_nccl_get_unique_id(buf))
+            uid = bytearray(bytes(buf))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        idbuf = (gp.api.C.c_char * 128).from_buffer_copy(obj[0])
+        N.check(N.lib.gpk_comm_init(sess.handle, world, rank, idbuf))
+
+    # first slice allocates the image-sized buffers, then upload the fixed dL/dI
+    sess.fwd_bwd_slice(poses[0], psf, rcfg)
+    dl = synthetic_dl_di(cfg)
+    sess.upload(N.GPK_BUF_DL_DI, dl.ctypes.data, dl.nbytes)
+    sess.synchronize()
+    # per-slice survivor / pair counts (algorithmic bytes of K_prep)
+    counts = []
+    for p in poses:
+        sess.prepare(p, psf, rcfg)
+        counts.append(sess.prepared_count())
+    S_mean = float(np.mean([c[0] for c in counts]))
+    T_mean = float(np.mean([c[1] for c in counts]))
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def step(i):
+        sess.fwd_bwd_slice(poses[(rank + i * world) % len(poses)], psf, rcfg)
+        if world > 1:
+            N.check(N.lib.gpk_allreduce_grads(sess.handle))
+
+    for i in range(args.warmup):
+        step(i)
+    sess.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sess.stage_times(reset=True)
+    sess.stage_timing(True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            starts[i].record(stream)
+            step(args.warmup + i)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    sess.stage_timing(False)
+    sess.synchronize()
+    if dist:
+        dist.barrier()
+    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    stages = sess.stage_times(reset=True)
+    t = torch.tensor([total_ms], device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * 1000.0 / ms_per_step
+
+    # ---- e2e through the public C-ABI with host buffers ---------------------------
+    e2e_steps = max(5, min(args.steps, 50))
+    pin_dl = torch.from_numpy(dl).pin_memory()
+    pin_img = torch.empty(P, dtype=torch.float32).pin_memory()
+    gptr, gbytes = sess.device_buffer(N.GPK_BUF_GRADS)
+    grad_bytes = n * 11 * 4
+    pin_grads = torch.empty(gbytes // 4, dtype=torch.float32).pin_memory()
+    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)]
+    e_e = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)]
+    cap_floats = gbytes // 44
+    for i in range(e2e_steps):
+        flush.fill_(float(i))
+        e_s[i].record(stream)
+        sess.upload(N.GPK_BUF_DL_DI, pin_dl.data_ptr(), P * 4)
+        step(i)
+        sess.download(N.GPK_BUF_IMAGE, pin_img.data_ptr(), P * 4)
+        # dense gradient planes (11 x N f32) -> host
+        sess.download(N.GPK_BUF_GRADS, pin_grads.data_ptr(), cap_floats * 44)
+        e_e[i].record(stream)
+        e_e[i].synchronize()
+    e2e_ms = sum(s.elapsed_time(e) for s, e in zip(e_s, e_e)) / e2e_steps
+    t = torch.tensor([e2e_ms], device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    assert np.isfinite(pin_grads.numpy()[:1000]).all()
+
+    # ---- roofline of the dominant kernel -------------------------------------------
+    dom = max((k for k in stages if stages[k][1] > 0), key=lambda k: stages[k][0])
+    peak, peak_src = load_peaks()
+    prep_bytes = 44 * n + 44 * (n - S_mean) + 48 * S_mean + 8 * T_mean
+    launch_ms = stages[dom][0] / stages[dom][1]
+    if dom == "prepare":
+        achieved = prep_bytes / (launch_ms * 1e-3) / 1e9
+        traffic = ncu_traffic(args.config)
+        roof = {"kernel": "k_prep", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_launch": prep_bytes, "launch_ms": launch_ms,
+                "bytes_formula": "44N params read + 44(N-S) gradient zero-fill + 48S records + 8T pairs"}
+    else:
+        roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
+                "frac": None, "traffic": None, "launch_ms": launch_ms}
+    u1_bytes = 88 * n + 8 * P
+    step_gbs = u1_bytes / (ms_per_step * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "slices/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (fp64 preprocess/chain)",
+        "data": "synthetic (init_random seed 1, dL/dI U(-1,1)/P seed 7)",
+        "config": config_json(args, cfg, world),
+        "roofline": roof,
+        "u1_roofline": {"bytes_per_step": u1_bytes, "achieved_gbs": step_gbs, "frac": step_gbs / peak,
+                        "formula": "88N + 8P (SURVEY.md §8d)"},
+        "stage_ms_per_step": {k: v[0] / max(v[1], 1) * (v[1] / args.steps) for k, v in stages.items()
+                              if v[1]},
+        "survivors_mean": S_mean, "pairs_mean": T_mean,
+        "e2e": {"value": world * 1000.0 / e2e_ms, "unit": "slices/s", "h2d_bytes_per_step": P * 4,
+                "d2h_bytes_per_step": P * 4 + cap_floats * 44,
+                "path": "C-ABI: gpk_upload(dL/dI) + gpk_fwd_bwd_slice + gpk_download(image, dense grads)"},
+        "gpu_launches": None,
+        "clocks": clk.result(),
+    }
+    # K_prep + radix passes + forward + backward + chain (the memset is a copy-engine op)
+    launches_per_step = 1 + sort_passes(X, Y) + 3
+    line["gpu_launches"] = launches_per_step * args.steps
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(cfg, gs.records, args.cpu_seconds).items()
+                                    if k in ("value", "unit", "cores", "kind", "sample",
+                                             "stage_seconds_per_slice")}
+        except Exception as e:  # reported, never silently replaced
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    sess.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def sort_passes(X, Y):
+    tiles = ((X + 15) // 16) * ((Y + 15) // 16)
+    bits = max(0, (tiles - 1).bit_length())
+    return (bits + 7) // 8
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

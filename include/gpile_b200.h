@@ -1,0 +1,273 @@
+/*
+ * gpile_b200.h — C-ABI boundary of the B200-native GaussianPile slice renderer.
+ *
+ * This is the process/device boundary that replaces the CPU hot path of the
+ * reference library (header-only C++20, /root/reference/proj/include/gpile).
+ * Every entry point below names the reference interface it stands in for.
+ * Nothing here uses C++ or torch types: plain structs, pointers and sizes.
+ *
+ * Conventions
+ *   - Every function returns a gpk_status. No exception ever crosses the ABI.
+ *     Status codes map 1:1 to the reference's exception taxonomy
+ *     (errors.hpp:9-27 plus std::invalid_argument); the failing primitive
+ *     index (when the reference names one, backward.hpp:182-184,
+ *     voxelize.hpp:237) is available from gpk_last_error_index().
+ *   - Gaussian parameters cross the boundary in the checkpoint record layout:
+ *     11 x f32 per primitive, (mu x y z, log-scale x y z, quat w x y z,
+ *     raw alpha) (checkpoint.hpp:14-16, docs/FORMATS.md:5-17). On the device
+ *     they live as 11 SoA f32 planes.
+ *   - Gradients use the same 11-slot order (grad_chain.hpp:12-22 flattened).
+ *   - Images are row-major f32, pixels[j*W + i] (image.hpp:17-27); volumes are
+ *     z-major f32, data[(k*Y + j)*X + i] (core.hpp:119-121).
+ *   - One session per GPU. Calls on a session are issued in order on the
+ *     session's CUDA stream. Functions that take or return HOST buffers
+ *     synchronize the stream and surface device-side errors, like the
+ *     reference's synchronous exceptions; functions whose host pointers are
+ *     NULL stay asynchronous (device-resident data) so they can be captured
+ *     in a CUDA graph; gpk_session_synchronize() surfaces deferred errors.
+ */
+#ifndef GPILE_B200_H
+#define GPILE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPK_ABI_VERSION 1
+#define GPK_RECORD_FLOATS 11
+
+typedef enum {
+    GPK_OK = 0,
+    GPK_ERR_INVALID_ARGUMENT = 1,      /* std::invalid_argument */
+    GPK_ERR_DEGENERATE_COVARIANCE = 2, /* gpile::DegenerateCovariance, errors.hpp:9 */
+    GPK_ERR_NUMERIC_FAILURE = 3,       /* gpile::NumericFailure, errors.hpp:14 */
+    GPK_ERR_CUDA = 4,                  /* CUDA runtime / launch failure */
+    GPK_ERR_NCCL = 5,                  /* NCCL failure */
+    GPK_ERR_OUT_OF_MEMORY = 6,         /* device allocation failed */
+    GPK_ERR_STATE = 7                  /* call order violated (e.g. backward before prepare) */
+} gpk_status;
+
+/* Bounds (core.hpp:50-65): world-space bbox, positions clamped into it by Adam. */
+typedef struct {
+    double min[3];
+    double max[3];
+} gpk_bounds;
+
+/* SlicePose (core.hpp:78-105). rotation is R_c, row-major. */
+typedef struct {
+    double rotation[9];
+    double translation[3];
+    int32_t width;
+    int32_t height;
+    double pixel_spacing[2];
+    double principal_point[2];
+} gpk_slice_pose;
+
+/* PsfSpec (core.hpp:109-117). Only sigma_z enters the renderer. */
+typedef struct {
+    double sigma_x, sigma_y, sigma_z;
+} gpk_psf;
+
+/* RasterConfig (render.hpp:26-31). tile_size must be 16 on this backend. */
+typedef struct {
+    double tau;
+    int32_t tile_size;
+    double footprint_sigmas;
+    double scale_modifier;
+} gpk_raster_config;
+
+/* LearningRates (optimize.hpp:178-180) and AdamState hyper-parameters
+ * (optimize.hpp:157). */
+typedef struct {
+    double position, opacity, scale, rotation;
+} gpk_learning_rates;
+
+typedef struct {
+    double beta1, beta2, eps;
+} gpk_adam_hparams;
+
+/* VoxelizerConfig (voxelize.hpp:16-38). */
+typedef struct {
+    int32_t dims[3];
+    double spacing[3];
+    double origin[3];
+    int32_t tile_dims[3];
+    double support_sigmas;
+    double scale_modifier;
+} gpk_voxelizer_config;
+
+/* ScreenGradStats (backward.hpp:19-26), host arrays of length n, overwritten. */
+typedef struct {
+    double* mu2d_grad_norm;   /* n */
+    uint8_t* observed;        /* n */
+    double* world_pos_grad;   /* 3n, xyz interleaved */
+} gpk_screen_stats;
+
+typedef struct gpk_session gpk_session;
+
+/* Device buffers a zero-copy caller may address (gpk_device_buffer). */
+typedef enum {
+    GPK_BUF_PARAMS = 0,   /* 11 f32 planes x capacity: plane p at p*capacity */
+    GPK_BUF_GRADS = 1,    /* 11 f32 planes, dense dL/dparam (backward output) */
+    GPK_BUF_IMAGE = 2,    /* W*H f32: rendered slice (rasterize output) */
+    GPK_BUF_DL_DI = 3,    /* W*H f32: dL/dI consumed by backward */
+    GPK_BUF_TARGET = 4,   /* W*H f32: target slice for the photometric loss */
+    GPK_BUF_VOLUME = 5,   /* X*Y*Z f32: voxelize output */
+    GPK_BUF_DL_DV = 6,    /* X*Y*Z f32: dL/dV consumed by voxelize_backward */
+    GPK_BUF_LOSS = 7      /* 1 f64: last photometric loss */
+} gpk_buffer;
+
+/* ---- library ------------------------------------------------------------ */
+int gpk_abi_version(void);
+const char* gpk_last_error_message(void);   /* thread-local, valid until next call */
+int64_t gpk_last_error_index(void);          /* primitive index or -1 */
+int gpk_device_count(int* count);
+
+/* ---- session lifecycle ---------------------------------------------------- */
+/* cuda_stream may be NULL (the session creates its own non-blocking stream) or
+ * a caller-owned cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream). */
+int gpk_session_create(int device, void* cuda_stream, gpk_session** out);
+int gpk_session_destroy(gpk_session* s);
+int gpk_session_set_stream(gpk_session* s, void* cuda_stream);
+int gpk_session_get_stream(gpk_session* s, void** cuda_stream);
+/* Wait for all queued work, then report any device-side error flag. */
+int gpk_session_synchronize(gpk_session* s);
+/* Reserve (tile, Gaussian) pair capacity up front (avoids growth on first use). */
+int gpk_session_reserve_pairs(gpk_session* s, uint64_t pairs);
+int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes);
+/* Raw, stream-ordered copies between a device buffer (gpk_buffer) and caller
+ * memory (pinned memory makes them asynchronous). bytes must not exceed the
+ * buffer size reported by gpk_device_buffer. */
+int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes);
+int gpk_download(gpk_session* s, int which, void* host, uint64_t bytes);
+
+/* ---- live stage timing (CUDA events on the session stream) ------------------ */
+typedef enum {
+    GPK_STAGE_PREPARE = 0,   /* K_prep: preprocess + cull + bounds + pair emission */
+    GPK_STAGE_SORT = 1,      /* radix passes */
+    GPK_STAGE_RASTER = 2,    /* forward accumulation */
+    GPK_STAGE_BACKWARD = 3,  /* backward pixel accumulation */
+    GPK_STAGE_CHAIN = 4,     /* backward chain to world parameters */
+    GPK_STAGE_LOSS = 5,
+    GPK_STAGE_ADAM = 6,
+    GPK_STAGE_VOXEL = 7,
+    GPK_NUM_STAGES = 8
+} gpk_stage;
+/* Enable/disable event pairs around every stage launch. */
+int gpk_stage_timing(gpk_session* s, int enable);
+/* Accumulated device milliseconds and launch counts per stage since the last
+ * reset (synchronizes). ms and counts have GPK_NUM_STAGES entries. */
+int gpk_stage_times(gpk_session* s, double* ms, uint64_t* counts, int reset);
+
+/* ---- parameters (GaussianSet, core.hpp:67-74) ------------------------------ */
+/* Upload n primitives (host records, 11 f32 each) and the bbox. Resets Adam. */
+int gpk_set_gaussians(gpk_session* s, uint64_t n, const float* records, const gpk_bounds* bbox);
+/* Same from f64 records (GaussianPrimitive layout flattened); rounded to f32. */
+int gpk_set_gaussians_f64(gpk_session* s, uint64_t n, const double* records,
+                          const gpk_bounds* bbox);
+int gpk_get_gaussians(gpk_session* s, float* records);
+int gpk_gaussian_count(gpk_session* s, uint64_t* n);
+/* Dense gradient buffer (GaussianGradients, grad_chain.hpp:12-22) to/from host
+ * records (n x 11 f32): the input of adam_step when gradients come from the host. */
+int gpk_set_gradients(gpk_session* s, const float* grads);
+int gpk_get_gradients(gpk_session* s, float* grads);
+
+/* ---- slice renderer: prepare_gaussians + TileGrid (render.hpp:83-160) ------ */
+/* Preprocess every primitive for this slice (focus Gaussian, cull, bounds),
+ * then bin survivors to 16x16 tiles with a stable radix sort. Device-resident;
+ * asynchronous. Validates pose/psf/cfg on the host (core.hpp:112-116). */
+int gpk_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                const gpk_raster_config* cfg);
+/* Survivor and pair counts of the last prepare (synchronizes). */
+int gpk_prepared_count(gpk_session* s, uint64_t* survivors, uint64_t* pairs);
+/* Survivors in ascending set order (render.hpp:133-137): set index, inclusive
+ * pixel bounds (lo_x, hi_x, lo_y, hi_y) and 6 doubles (alpha_tilde, mu_2d.x,
+ * mu_2d.y, conic.a, conic.b, conic.d). Any pointer may be NULL. */
+int gpk_get_prepared(gpk_session* s, uint32_t* index, int32_t* bounds, double* fields);
+/* Per-tile lists (render.hpp:142-160): offsets[tiles+1], entries[pairs] holding
+ * set indices in list order. */
+int gpk_get_tile_lists(gpk_session* s, uint32_t* offsets, uint32_t* entries);
+
+/* ---- forward: rasterize_prepared (render.hpp:166-192) ----------------------- */
+/* Renders the prepared slice into GPK_BUF_IMAGE; copies to image_out if non-NULL. */
+int gpk_rasterize(gpk_session* s, float* image_out);
+
+/* ---- backward: backward_prepared (backward.hpp:97-187) ---------------------- */
+/* dl_di: host W*H f32, or NULL to consume GPK_BUF_DL_DI. Writes the dense
+ * gradient (exact zeros for culled primitives) into GPK_BUF_GRADS; copies it
+ * to grads_out (host, n*11 f32 record order) if non-NULL; fills stats if
+ * non-NULL. Non-finite gradients -> GPK_ERR_NUMERIC_FAILURE naming the first
+ * primitive (backward.hpp:175-185). */
+int gpk_backward(gpk_session* s, const float* dl_di, float* grads_out, gpk_screen_stats* stats);
+
+/* ---- loss: photometric_loss (loss.hpp:13-37) -------------------------------- */
+/* target: host W*H f32 or NULL for GPK_BUF_TARGET. Renders must have run.
+ * Writes dL/dI into GPK_BUF_DL_DI (and dl_di_out if non-NULL); the loss into
+ * GPK_BUF_LOSS (and *loss_out if non-NULL, which synchronizes). */
+int gpk_photometric_loss(gpk_session* s, const float* target, double lambda,
+                         double dssim_scale, double* loss_out, float* dl_di_out);
+/* Stand-alone photometric_loss(rendered, target, lambda, dl_di, dssim_scale)
+ * on host images (loss.hpp:13): synchronous; overwrites the session's image,
+ * target and dL/dI buffers. */
+int gpk_photometric_loss_images(gpk_session* s, int32_t width, int32_t height,
+                                const float* rendered, const float* target, double lambda,
+                                double dssim_scale, double* loss_out, float* dl_di_out);
+
+/* ---- optimizer: adam_step (optimize.hpp:195-221) ---------------------------- */
+/* One bias-corrected Adam step on all n primitives using GPK_BUF_GRADS.
+ * hp may be NULL (beta1 0.9, beta2 0.999, eps 1e-8). The step counter lives on
+ * the device (AdamState::step). */
+int gpk_adam_step(gpk_session* s, const gpk_learning_rates* lrs, const gpk_adam_hparams* hp);
+/* Adam step whose learning rates follow lr_at(lr0, step, total) (optimize.hpp:71)
+ * evaluated on the device from the device step counter (graph-capturable). */
+int gpk_adam_step_scheduled(gpk_session* s, const gpk_learning_rates* lr0, int32_t total,
+                            const gpk_adam_hparams* hp);
+int gpk_adam_reset(gpk_session* s);
+/* Adam moments in record order (n*11 each) and the step counter. */
+int gpk_get_adam_state(gpk_session* s, float* m, float* v, int64_t* step);
+int gpk_set_adam_state(gpk_session* s, const float* m, const float* v, int64_t step);
+
+/* ---- fused paths for the throughput loop ------------------------------------ */
+/* U1: prepare + rasterize + backward(GPK_BUF_DL_DI), all device-resident. */
+int gpk_fwd_bwd_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                      const gpk_raster_config* cfg);
+/* U2: prepare + rasterize + loss(GPK_BUF_TARGET) + backward + scheduled Adam. */
+int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                   const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                   const gpk_learning_rates* lr0, int32_t total_iterations);
+
+/* ---- voxelizer: voxelize / voxelize_backward (voxelize.hpp:113-240) ---------- */
+int gpk_voxelize(gpk_session* s, const gpk_voxelizer_config* cfg, float* volume_out);
+/* Per-8^3-tile lists of the last voxelize (VoxelTiles, voxelize.hpp:86-105). */
+int gpk_voxel_tile_count(gpk_session* s, uint64_t* tiles, uint64_t* instances);
+int gpk_get_voxel_tile_lists(gpk_session* s, uint32_t* offsets, uint32_t* entries);
+int gpk_voxelize_backward(gpk_session* s, const gpk_voxelizer_config* cfg, const float* dl_dv,
+                          float* grads_out);
+
+/* ---- host utilities of the fit driver (synthetic inputs, schedule) ----------- */
+/* init_random (optimize.hpp:94-108) on the reference's seeded mt19937_64 stream
+ * (rng.hpp:14-70): n x 11 f64 records, bit-identical to the reference. */
+int gpk_init_random(uint64_t n, const gpk_bounds* bbox, double scale_base, uint64_t seed,
+                    double* records);
+/* slice_pose_for_index (core.hpp:202-211) for a z-major volume geometry. */
+int gpk_slice_pose_for_index(const int32_t dims[3], const double spacing[3],
+                             const double origin[3], int k, gpk_slice_pose* out);
+/* lr_at (optimize.hpp:71-73). */
+double gpk_lr_at(double lr0, int iteration, int total);
+
+/* ---- multi-GPU: slice-sharded data parallelism ------------------------------ */
+/* 128-byte ncclUniqueId produced on rank 0 and broadcast by the caller. */
+int gpk_nccl_get_unique_id(void* id_out128);
+int gpk_comm_init(gpk_session* s, int nranks, int rank, const void* id128);
+int gpk_comm_destroy(gpk_session* s);
+/* Sum GPK_BUF_GRADS across ranks (one ncclAllReduce, in place, session stream). */
+int gpk_allreduce_grads(gpk_session* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GPILE_B200_H */

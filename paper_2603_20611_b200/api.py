@@ -1,0 +1,545 @@
+"""Reference-shaped host API over the sm_100a C-ABI.
+
+Names, argument meaning and error behaviour follow the reference library
+(/root/reference/proj/include/gpile): ``rasterize_slice`` (render.hpp:194),
+``prepare_gaussians`` (render.hpp:83), ``backward_slice`` (backward.hpp:189),
+``photometric_loss`` (loss.hpp:13), ``adam_step`` / ``AdamState`` / ``lr_at``
+(optimize.hpp:71-221), ``voxelize`` / ``voxelize_backward``
+(voxelize.hpp:113-240), ``init_random`` (optimize.hpp:94) and
+``slice_pose_for_index`` (core.hpp:202). Exceptions map the reference's
+taxonomy: ``InvalidArgument`` (std::invalid_argument, also a ValueError),
+``DegenerateCovariance`` and ``NumericFailure``.
+
+Data conventions: a GaussianSet holds an (n, 11) float64 array of stored
+parameters in the checkpoint record order (mu xyz, log-scale xyz, quat wxyz,
+raw alpha) plus the bbox; the device keeps them as float32. Images are
+(height, width) arrays, row-major like SliceImage::pixels[j*W + i]; volumes
+are (Z, Y, X). Gradients come back as (n, 11) arrays in the same slot order.
+
+``Session`` is the device-resident form used by the training loop: parameters
+and Adam moments stay in HBM and only slice-sized data crosses PCIe.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from ._native import (DegenerateCovariance, GpileError, InvalidArgument, NumericFailure,
+                      StateError, check)
+
+__all__ = [
+    "GaussianSet", "SlicePose", "PsfSpec", "RasterConfig", "LearningRates", "AdamState",
+    "VoxelizerConfig", "ScreenGradStats", "Session", "Prepared",
+    "rasterize_slice", "prepare_gaussians", "tile_lists", "backward_slice", "photometric_loss",
+    "adam_step", "lr_at", "voxelize", "voxelize_backward", "init_random",
+    "slice_pose_for_index", "default_session",
+    "DegenerateCovariance", "NumericFailure", "InvalidArgument", "GpileError", "StateError",
+]
+
+RECORD = 11
+
+
+# ---- value types -------------------------------------------------------------
+@dataclass
+class GaussianSet:
+    """GaussianSet (core.hpp:67-74): ordered primitives + world bbox."""
+
+    records: np.ndarray
+    bbox_min: tuple = (0.0, 0.0, 0.0)
+    bbox_max: tuple = (1.0, 1.0, 1.0)
+
+    def __post_init__(self):
+        self.records = np.ascontiguousarray(np.asarray(self.records, dtype=np.float64).reshape(-1, RECORD))
+
+    def size(self) -> int:
+        return int(self.records.shape[0])
+
+    def __len__(self) -> int:
+        return self.size()
+
+    def bounds(self) -> N.Bounds:
+        return N.Bounds((C.c_double * 3)(*self.bbox_min), (C.c_double * 3)(*self.bbox_max))
+
+    def copy(self) -> "GaussianSet":
+        return GaussianSet(self.records.copy(), tuple(self.bbox_min), tuple(self.bbox_max))
+
+
+@dataclass
+class SlicePose:
+    """SlicePose (core.hpp:78-105). rotation is R_c (3x3)."""
+
+    rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
+    translation: tuple = (0.0, 0.0, 0.0)
+    width: int = 0
+    height: int = 0
+    pixel_spacing: tuple = (1.0, 1.0)
+    principal_point: tuple = (0.0, 0.0)
+
+    def to_c(self) -> N.SlicePoseC:
+        r = np.asarray(self.rotation, dtype=np.float64).reshape(9)
+        return N.SlicePoseC((C.c_double * 9)(*r), (C.c_double * 3)(*self.translation),
+                            int(self.width), int(self.height),
+                            (C.c_double * 2)(*self.pixel_spacing),
+                            (C.c_double * 2)(*self.principal_point))
+
+    @staticmethod
+    def from_c(p: N.SlicePoseC) -> "SlicePose":
+        return SlicePose(np.array(list(p.rotation)).reshape(3, 3), tuple(p.translation),
+                         p.width, p.height, tuple(p.pixel_spacing), tuple(p.principal_point))
+
+    def pixel_center(self, i: int, j: int) -> tuple:
+        return ((i - self.principal_point[0]) * self.pixel_spacing[0],
+                (j - self.principal_point[1]) * self.pixel_spacing[1])
+
+
+@dataclass
+class PsfSpec:
+    """PsfSpec (core.hpp:109-117)."""
+
+    sigma_x: float = 1.0
+    sigma_y: float = 1.0
+    sigma_z: float = 1.0
+
+    def to_c(self) -> N.PsfC:
+        return N.PsfC(self.sigma_x, self.sigma_y, self.sigma_z)
+
+
+@dataclass
+class RasterConfig:
+    """RasterConfig (render.hpp:26-31)."""
+
+    tau: float = 0.02
+    tile_size: int = 16
+    footprint_sigmas: float = 3.0
+    scale_modifier: float = 1.0
+
+    def to_c(self) -> N.RasterConfigC:
+        return N.RasterConfigC(self.tau, int(self.tile_size), self.footprint_sigmas, self.scale_modifier)
+
+
+@dataclass
+class LearningRates:
+    """LearningRates (optimize.hpp:178-180)."""
+
+    position: float
+    opacity: float
+    scale: float
+    rotation: float
+
+    def to_c(self) -> N.LearningRatesC:
+        return N.LearningRatesC(self.position, self.opacity, self.scale, self.rotation)
+
+
+@dataclass
+class AdamState:
+    """AdamState (optimize.hpp:156-176); moments as (n, 11) arrays."""
+
+    n: int = 0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    step: int = 0
+    m: np.ndarray | None = None
+    v: np.ndarray | None = None
+
+    def __post_init__(self):
+        if self.m is None:
+            self.m = np.zeros((self.n, RECORD))
+        if self.v is None:
+            self.v = np.zeros((self.n, RECORD))
+
+    def size(self) -> int:
+        return int(self.m.shape[0])
+
+
+@dataclass
+class VoxelizerConfig:
+    """VoxelizerConfig (voxelize.hpp:16-38)."""
+
+    dims: tuple = (0, 0, 0)
+    spacing: tuple = (1.0, 1.0, 1.0)
+    origin: tuple = (0.0, 0.0, 0.0)
+    tile_dims: tuple = (8, 8, 8)
+    support_sigmas: float = 3.0
+    scale_modifier: float = 1.0
+
+    def to_c(self) -> N.VoxelizerConfigC:
+        return N.VoxelizerConfigC((C.c_int32 * 3)(*self.dims), (C.c_double * 3)(*self.spacing),
+                                  (C.c_double * 3)(*self.origin), (C.c_int32 * 3)(*self.tile_dims),
+                                  self.support_sigmas, self.scale_modifier)
+
+
+@dataclass
+class ScreenGradStats:
+    """ScreenGradStats (backward.hpp:19-26)."""
+
+    mu2d_grad_norm: np.ndarray
+    observed: np.ndarray
+    world_pos_grad: np.ndarray
+
+
+@dataclass
+class Prepared:
+    """Survivors of prepare_gaussians (render.hpp:83) in ascending set order."""
+
+    index: np.ndarray      # uint32 set indices
+    bounds: np.ndarray     # int32 (S, 4): lo_x, hi_x, lo_y, hi_y (inclusive)
+    fields: np.ndarray     # float64 (S, 6): alpha_tilde, mu2d.x, mu2d.y, conic a, b, d
+    pairs: int = 0         # (tile, Gaussian) pairs of the binning
+
+
+# ---- session -----------------------------------------------------------------
+class Session:
+    """One device-resident GaussianPile session on one GPU (one CUDA stream)."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        h = C.c_void_p()
+        check(N.lib.gpk_session_create(int(device), C.c_void_p(stream) if stream else None, C.byref(h)))
+        self._h = h
+        self.device = device
+        self.n = 0
+        self.bbox = ((0.0,) * 3, (1.0,) * 3)
+        self.shape = (0, 0)
+
+    # lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib.gpk_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def synchronize(self):
+        check(N.lib.gpk_session_synchronize(self._h))
+
+    def reserve_pairs(self, pairs: int):
+        check(N.lib.gpk_session_reserve_pairs(self._h, int(pairs)))
+
+    def stream(self) -> int:
+        p = C.c_void_p()
+        check(N.lib.gpk_session_get_stream(self._h, C.byref(p)))
+        return int(p.value or 0)
+
+    def set_stream(self, stream: int):
+        check(N.lib.gpk_session_set_stream(self._h, C.c_void_p(stream)))
+
+    def device_buffer(self, which: int) -> tuple[int, int]:
+        p, b = C.c_void_p(), C.c_uint64()
+        check(N.lib.gpk_device_buffer(self._h, int(which), C.byref(p), C.byref(b)))
+        return int(p.value or 0), int(b.value)
+
+    def upload(self, which: int, host_ptr: int, nbytes: int):
+        check(N.lib.gpk_upload(self._h, int(which), C.c_void_p(host_ptr), int(nbytes)))
+
+    def download(self, which: int, host_ptr: int, nbytes: int):
+        check(N.lib.gpk_download(self._h, int(which), C.c_void_p(host_ptr), int(nbytes)))
+
+    STAGES = ("prepare", "sort", "raster", "backward", "chain", "loss", "adam", "voxel")
+
+    def stage_timing(self, enable: bool = True):
+        check(N.lib.gpk_stage_timing(self._h, 1 if enable else 0))
+
+    def stage_times(self, reset: bool = False) -> dict:
+        ms = np.zeros(len(self.STAGES), np.float64)
+        cnt = np.zeros(len(self.STAGES), np.uint64)
+        check(N.lib.gpk_stage_times(self._h, N.dptr(ms), cnt.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                    1 if reset else 0))
+        return {name: (float(ms[k]), int(cnt[k])) for k, name in enumerate(self.STAGES)}
+
+    # parameters
+    def set_gaussians(self, gs: GaussianSet):
+        rec = np.ascontiguousarray(gs.records, dtype=np.float32)
+        b = gs.bounds()
+        check(N.lib.gpk_set_gaussians(self._h, gs.size(), N.fptr(rec), C.byref(b)))
+        self.n = gs.size()
+        self.bbox = (tuple(gs.bbox_min), tuple(gs.bbox_max))
+
+    def get_gaussians(self) -> np.ndarray:
+        out = np.zeros((self.n, RECORD), dtype=np.float32)
+        check(N.lib.gpk_get_gaussians(self._h, N.fptr(out)))
+        return out
+
+    def set_gradients(self, grads: np.ndarray):
+        g = np.ascontiguousarray(grads, dtype=np.float32).reshape(self.n, RECORD)
+        check(N.lib.gpk_set_gradients(self._h, N.fptr(g)))
+
+    def get_gradients(self) -> np.ndarray:
+        out = np.zeros((self.n, RECORD), np.float32)
+        check(N.lib.gpk_get_gradients(self._h, N.fptr(out)))
+        return out
+
+    # slice pipeline
+    def prepare(self, pose: SlicePose, psf: PsfSpec, cfg: RasterConfig):
+        p, f, c = pose.to_c(), psf.to_c(), cfg.to_c()
+        check(N.lib.gpk_prepare(self._h, C.byref(p), C.byref(f), C.byref(c)))
+        self.shape = (pose.height, pose.width)
+
+    def prepared_count(self) -> tuple[int, int]:
+        s, t = C.c_uint64(), C.c_uint64()
+        check(N.lib.gpk_prepared_count(self._h, C.byref(s), C.byref(t)))
+        return int(s.value), int(t.value)
+
+    def prepared(self) -> Prepared:
+        s, t = self.prepared_count()
+        idx = np.zeros(s, np.uint32)
+        bnd = np.zeros((s, 4), np.int32)
+        fld = np.zeros((s, 6), np.float64)
+        check(N.lib.gpk_get_prepared(self._h, N.u32ptr(idx), N.i32ptr(bnd), N.dptr(fld)))
+        return Prepared(idx, bnd, fld, t)
+
+    def tile_lists(self) -> tuple[np.ndarray, np.ndarray]:
+        s, t = self.prepared_count()
+        h, w = self.shape
+        tiles = ((w + 15) // 16) * ((h + 15) // 16)
+        off = np.zeros(tiles + 1, np.uint32)
+        ent = np.zeros(max(t, 1), np.uint32)
+        check(N.lib.gpk_get_tile_lists(self._h, N.u32ptr(off), N.u32ptr(ent)))
+        return off, ent[:t]
+
+    def rasterize(self, to_host: bool = True) -> np.ndarray | None:
+        if not to_host:
+            check(N.lib.gpk_rasterize(self._h, None))
+            return None
+        h, w = self.shape
+        img = np.zeros((h, w), np.float32)
+        check(N.lib.gpk_rasterize(self._h, N.fptr(img)))
+        return img
+
+    def backward(self, dl_di: np.ndarray | None = None, to_host: bool = True,
+                 stats: bool = False):
+        d = None if dl_di is None else np.ascontiguousarray(dl_di, dtype=np.float32)
+        if d is not None and d.shape != self.shape:
+            raise InvalidArgument("backward_slice: gradient image shape mismatch")
+        out = np.zeros((self.n, RECORD), np.float32) if to_host else None
+        st = None
+        if stats:
+            nrm = np.zeros(self.n, np.float64)
+            obs = np.zeros(self.n, np.uint8)
+            wld = np.zeros((self.n, 3), np.float64)
+            st = N.ScreenStatsC(nrm.ctypes.data_as(C.POINTER(C.c_double)),
+                                obs.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                wld.ctypes.data_as(C.POINTER(C.c_double)))
+        check(N.lib.gpk_backward(self._h, None if d is None else N.fptr(d),
+                                 None if out is None else N.fptr(out),
+                                 None if st is None else C.byref(st)))
+        if stats:
+            return out, ScreenGradStats(nrm, obs, wld)
+        return out
+
+    def photometric_loss(self, target: np.ndarray | None, lam: float, dssim_scale: float = 0.5,
+                         to_host: bool = True):
+        t = None if target is None else np.ascontiguousarray(target, dtype=np.float32)
+        if not to_host:
+            check(N.lib.gpk_photometric_loss(self._h, None if t is None else N.fptr(t), lam,
+                                             dssim_scale, None, None))
+            return None
+        loss = C.c_double()
+        dl = np.zeros(self.shape, np.float32)
+        check(N.lib.gpk_photometric_loss(self._h, None if t is None else N.fptr(t), lam,
+                                         dssim_scale, C.byref(loss), N.fptr(dl)))
+        return float(loss.value), dl
+
+    def adam_step(self, lrs: LearningRates, beta1=0.9, beta2=0.999, eps=1e-8):
+        l = lrs.to_c()
+        hp = N.AdamHparamsC(beta1, beta2, eps)
+        check(N.lib.gpk_adam_step(self._h, C.byref(l), C.byref(hp)))
+
+    def adam_state(self) -> tuple[np.ndarray, np.ndarray, int]:
+        m = np.zeros((self.n, RECORD), np.float32)
+        v = np.zeros((self.n, RECORD), np.float32)
+        st = C.c_int64()
+        check(N.lib.gpk_get_adam_state(self._h, N.fptr(m), N.fptr(v), C.byref(st)))
+        return m, v, int(st.value)
+
+    def set_adam_state(self, m: np.ndarray, v: np.ndarray, step: int):
+        m32 = np.ascontiguousarray(m, np.float32)
+        v32 = np.ascontiguousarray(v, np.float32)
+        check(N.lib.gpk_set_adam_state(self._h, N.fptr(m32), N.fptr(v32), int(step)))
+
+    def fwd_bwd_slice(self, pose: SlicePose, psf: PsfSpec, cfg: RasterConfig):
+        p, f, c = pose.to_c(), psf.to_c(), cfg.to_c()
+        check(N.lib.gpk_fwd_bwd_slice(self._h, C.byref(p), C.byref(f), C.byref(c)))
+        self.shape = (pose.height, pose.width)
+
+    def train_step(self, pose: SlicePose, psf: PsfSpec, cfg: RasterConfig, lam: float,
+                   dssim_scale: float, lr0: LearningRates, total_iterations: int):
+        p, f, c, l = pose.to_c(), psf.to_c(), cfg.to_c(), lr0.to_c()
+        check(N.lib.gpk_train_step(self._h, C.byref(p), C.byref(f), C.byref(c), lam, dssim_scale,
+                                   C.byref(l), int(total_iterations)))
+        self.shape = (pose.height, pose.width)
+
+    # voxelizer
+    def voxelize(self, cfg: VoxelizerConfig, to_host: bool = True) -> np.ndarray | None:
+        c = cfg.to_c()
+        if not to_host:
+            check(N.lib.gpk_voxelize(self._h, C.byref(c), None))
+            return None
+        X, Y, Z = cfg.dims
+        vol = np.zeros((Z, Y, X), np.float32)
+        check(N.lib.gpk_voxelize(self._h, C.byref(c), N.fptr(vol)))
+        return vol
+
+    def voxel_tile_lists(self) -> tuple[np.ndarray, np.ndarray]:
+        t, n = C.c_uint64(), C.c_uint64()
+        check(N.lib.gpk_voxel_tile_count(self._h, C.byref(t), C.byref(n)))
+        off = np.zeros(int(t.value) + 1, np.uint32)
+        ent = np.zeros(max(int(n.value), 1), np.uint32)
+        check(N.lib.gpk_get_voxel_tile_lists(self._h, N.u32ptr(off), N.u32ptr(ent)))
+        return off, ent[:int(n.value)]
+
+    def voxelize_backward(self, cfg: VoxelizerConfig, dl_dv: np.ndarray | None) -> np.ndarray:
+        c = cfg.to_c()
+        d = None if dl_dv is None else np.ascontiguousarray(dl_dv, dtype=np.float32)
+        if d is not None and d.shape != (cfg.dims[2], cfg.dims[1], cfg.dims[0]):
+            raise InvalidArgument("voxelize_backward: gradient volume shape mismatch")
+        out = np.zeros((self.n, RECORD), np.float32)
+        check(N.lib.gpk_voxelize_backward(self._h, C.byref(c), None if d is None else N.fptr(d),
+                                          N.fptr(out)))
+        return out
+
+
+_default: dict[int, Session] = {}
+_lock = threading.Lock()
+
+
+def default_session(device: int = 0) -> Session:
+    """Process-wide session per device used by the stateless reference-shaped calls."""
+    with _lock:
+        s = _default.get(device)
+        if s is None:
+            s = Session(device)
+            _default[device] = s
+        return s
+
+
+def _session_for(gs: GaussianSet, device: int) -> Session:
+    s = default_session(device)
+    s.set_gaussians(gs)
+    return s
+
+
+# ---- reference-shaped free functions -----------------------------------------
+def rasterize_slice(gs: GaussianSet, pose: SlicePose, psf: PsfSpec,
+                    cfg: RasterConfig | None = None, device: int = 0) -> np.ndarray:
+    """rasterize_slice (render.hpp:194-199): (H, W) float32 image."""
+    cfg = cfg or RasterConfig()
+    s = _session_for(gs, device)
+    s.prepare(pose, psf, cfg)
+    return s.rasterize()
+
+
+def prepare_gaussians(gs: GaussianSet, pose: SlicePose, psf: PsfSpec,
+                      cfg: RasterConfig | None = None, device: int = 0) -> Prepared:
+    """prepare_gaussians (render.hpp:83-138): survivors in ascending set order."""
+    cfg = cfg or RasterConfig()
+    s = _session_for(gs, device)
+    s.prepare(pose, psf, cfg)
+    return s.prepared()
+
+
+def tile_lists(gs: GaussianSet, pose: SlicePose, psf: PsfSpec, cfg: RasterConfig | None = None,
+               device: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """detail::TileGrid (render.hpp:142-160) as (offsets[tiles+1], set indices)."""
+    cfg = cfg or RasterConfig()
+    s = _session_for(gs, device)
+    s.prepare(pose, psf, cfg)
+    return s.tile_lists()
+
+
+def backward_slice(gs: GaussianSet, pose: SlicePose, psf: PsfSpec, dl_di: np.ndarray,
+                   cfg: RasterConfig | None = None, stats: bool = False, device: int = 0):
+    """backward_slice (backward.hpp:189-196): (n, 11) gradients [, ScreenGradStats]."""
+    cfg = cfg or RasterConfig()
+    dl = np.asarray(dl_di)
+    if dl.shape != (pose.height, pose.width):
+        raise InvalidArgument("backward_slice: gradient image shape mismatch")
+    s = _session_for(gs, device)
+    s.prepare(pose, psf, cfg)
+    return s.backward(dl, stats=stats)
+
+
+def photometric_loss(rendered: np.ndarray, target: np.ndarray, lam: float,
+                     dssim_scale: float = 0.5, device: int = 0) -> tuple[float, np.ndarray]:
+    """photometric_loss (loss.hpp:13-37): (loss, dL/dI)."""
+    r = np.ascontiguousarray(rendered, dtype=np.float32)
+    t = np.ascontiguousarray(target, dtype=np.float32)
+    if r.shape != t.shape or r.ndim != 2:
+        raise InvalidArgument("photometric_loss: image shape mismatch")
+    s = default_session(device)
+    h, w = r.shape
+    loss = C.c_double()
+    dl = np.zeros((h, w), np.float32)
+    check(N.lib.gpk_photometric_loss_images(s.handle, w, h, N.fptr(r), N.fptr(t), lam, dssim_scale,
+                                            C.byref(loss), N.fptr(dl)))
+    return float(loss.value), dl
+
+
+def lr_at(lr0: float, iteration: int, total: int) -> float:
+    """lr_at (optimize.hpp:71-73)."""
+    return float(N.lib.gpk_lr_at(lr0, int(iteration), int(total)))
+
+
+def adam_step(gs: GaussianSet, grads: np.ndarray, state: AdamState, lrs: LearningRates,
+              device: int = 0) -> None:
+    """adam_step (optimize.hpp:195-221): updates gs.records and state in place."""
+    g = np.asarray(grads)
+    if g.shape != (gs.size(), RECORD) or state.size() != gs.size():
+        raise InvalidArgument("adam_step: shape mismatch")
+    s = _session_for(gs, device)
+    s.set_adam_state(state.m, state.v, state.step)
+    s.set_gradients(g)
+    s.adam_step(lrs, state.beta1, state.beta2, state.eps)
+    m, v, st = s.adam_state()
+    gs.records = s.get_gaussians().astype(np.float64)
+    state.m, state.v, state.step = m.astype(np.float64), v.astype(np.float64), st
+
+
+def voxelize(gs: GaussianSet, cfg: VoxelizerConfig, device: int = 0) -> np.ndarray:
+    """voxelize (voxelize.hpp:113-148): (Z, Y, X) float32 volume."""
+    s = _session_for(gs, device)
+    return s.voxelize(cfg)
+
+
+def voxelize_backward(gs: GaussianSet, cfg: VoxelizerConfig, dl_dv: np.ndarray,
+                      device: int = 0) -> np.ndarray:
+    """voxelize_backward (voxelize.hpp:152-240): (n, 11) gradients."""
+    s = _session_for(gs, device)
+    return s.voxelize_backward(cfg, dl_dv)
+
+
+def init_random(count: int, bbox_min, bbox_max, scale_base: float, seed: int) -> GaussianSet:
+    """init_random (optimize.hpp:94-108), bit-identical stream."""
+    rec = np.zeros((int(count), RECORD), np.float64)
+    b = N.Bounds((C.c_double * 3)(*bbox_min), (C.c_double * 3)(*bbox_max))
+    st = N.lib.gpk_init_random(int(count), C.byref(b), float(scale_base), int(seed), N.dptr(rec))
+    if st != N.GPK_OK:
+        raise InvalidArgument("init_random: count must be >= 1 and bbox non-degenerate")
+    return GaussianSet(rec, tuple(bbox_min), tuple(bbox_max))
+
+
+def slice_pose_for_index(dims, spacing, origin, k: int) -> SlicePose:
+    """slice_pose_for_index (core.hpp:202-211)."""
+    d = np.asarray(dims, np.int32)
+    sp = np.asarray(spacing, np.float64)
+    o = np.asarray(origin, np.float64)
+    p = N.SlicePoseC()
+    check(N.lib.gpk_slice_pose_for_index(N.i32ptr(d), N.dptr(sp), N.dptr(o), int(k), C.byref(p)))
+    return SlicePose.from_c(p)

@@ -1,0 +1,249 @@
+// loss.cu — photometric_loss (loss.hpp:13-37) with ssim_with_gradient
+// (metrics.hpp:187-225), the dL/dI producer of the training step.
+//
+// L = mean|I - T| + lambda * dssim_scale * (1 - mean SSIM), SSIM over an
+// 11-tap separable Gaussian window (sigma 1.5, metrics.hpp:66-75) with
+// symmetric reflection at the borders (metrics.hpp:77-83).
+//
+// Two tiled kernels, 32x32 outputs per CTA, inputs staged with a 5-pixel
+// reflected halo in shared memory:
+//   k_ssim_fwd : 5 windowed moments (separable: rows then columns) -> per-pixel
+//                SSIM and its three partials g1 = dS/dmu_x, g2 = dS/dm2,
+//                g3 = dS/dm12 (already / N); per-CTA sums of SSIM and |I - T|.
+//   k_ssim_bwd : the window operator is self-adjoint, so dSSIM/dI =
+//                W g1 + 2 I (W g2) + T (W g3) (metrics.hpp:218-223); fused with
+//                the L1 sign term into dL/dI. The last CTA reduces the per-CTA
+//                sums in a fixed order (deterministic loss).
+// lambda == 0 takes the L1-only kernel (loss.hpp:29).
+#include "common.cuh"
+
+namespace gpk {
+
+namespace {
+
+constexpr int kT = 32, kR = 5, kH = kT + 2 * kR;  // tile, radius, haloed extent
+constexpr double kC1 = 1e-4, kC2 = 9e-4;         // metrics.hpp:155-156
+
+__device__ __forceinline__ int reflect(int p, int n) {
+    while (p < 0 || p >= n) {
+        if (p < 0) p = -p - 1;
+        if (p >= n) p = 2 * n - 1 - p;
+    }
+    return p;
+}
+
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* s_red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+        s_red[2 * warp] = a;
+        s_red[2 * warp + 1] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a = 0.0;
+        b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += s_red[2 * w];
+            b += s_red[2 * w + 1];
+        }
+    }
+}
+
+// Last CTA: loss = l1/N + lambda*dssim*(1 - ssim/N), summed in CTA order.
+__device__ __forceinline__ void finish_loss(const LossLaunch& a, bool with_ssim) {
+    __shared__ unsigned s_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned nblk = gridDim.x * gridDim.y;
+        s_last = (atomicAdd(a.done_ctr, 1u) == nblk - 1) ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    const unsigned nblk = gridDim.x * gridDim.y;
+    double ss = 0.0, l1 = 0.0;
+    for (unsigned k = 0; k < nblk; ++k) {
+        ss += a.partial[2 * k];
+        l1 += a.partial[2 * k + 1];
+    }
+    const double inv_n = 1.0 / ((double)a.W * (double)a.H);
+    double L = l1 * inv_n;
+    if (with_ssim) L += a.lambda * a.dssim_scale * (1.0 - ss * inv_n);
+    *a.loss = L;
+    *a.done_ctr = 0;
+}
+
+__global__ void __launch_bounds__(256) k_l1_only(const LossLaunch a) {
+    __shared__ double s_red[16];
+    const size_t n = (size_t)a.W * a.H;
+    const float inv_n = (float)(1.0 / (double)n);
+    double l1 = 0.0, dummy = 0.0;
+    const unsigned nblk = gridDim.x;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)nblk * blockDim.x) {
+        const float d = a.image[i] - a.target[i];
+        l1 += fabs((double)d);
+        a.dl_di[i] = (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) * inv_n;
+    }
+    block_sum2(dummy, l1, s_red);
+    if (threadIdx.x == 0) {
+        a.partial[2 * blockIdx.x] = 0.0;
+        a.partial[2 * blockIdx.x + 1] = l1;
+    }
+    finish_loss(a, false);
+}
+
+__global__ void __launch_bounds__(256) k_ssim_fwd(const LossLaunch a) {
+    __shared__ float s_x[kH][kH + 1];
+    __shared__ float s_y[kH][kH + 1];
+    __shared__ float s_h[5][kH][kT + 1];
+    __shared__ double s_red[16];
+    const int X0 = blockIdx.x * kT, Y0 = blockIdx.y * kT;
+    const int W = a.W, H = a.H;
+    for (int idx = threadIdx.x; idx < kH * kH; idx += blockDim.x) {
+        const int r = idx / kH, c = idx % kH;
+        const int gx = reflect(X0 + c - kR, W), gy = reflect(Y0 + r - kR, H);
+        s_x[r][c] = a.image[(size_t)gy * W + gx];
+        s_y[r][c] = a.target[(size_t)gy * W + gx];
+    }
+    __syncthreads();
+    // rows (axis 0 of conv_nd, metrics.hpp:112-116)
+    for (int idx = threadIdx.x; idx < kH * kT; idx += blockDim.x) {
+        const int r = idx / kT, c = idx % kT;
+        float hx = 0.f, hy = 0.f, hxx = 0.f, hxy = 0.f, hyy = 0.f;
+#pragma unroll
+        for (int t = 0; t < 2 * kR + 1; ++t) {
+            const float x = s_x[r][c + t], y = s_y[r][c + t], w = a.w[t];
+            hx += w * x;
+            hy += w * y;
+            hxx += w * x * x;
+            hxy += w * x * y;
+            hyy += w * y * y;
+        }
+        s_h[0][r][c] = hx;
+        s_h[1][r][c] = hy;
+        s_h[2][r][c] = hxx;
+        s_h[3][r][c] = hxy;
+        s_h[4][r][c] = hyy;
+    }
+    __syncthreads();
+    const double inv_n = 1.0 / ((double)W * (double)H);
+    double ssum = 0.0, l1 = 0.0;
+    const size_t P = (size_t)W * H;
+    for (int idx = threadIdx.x; idx < kT * kT; idx += blockDim.x) {
+        const int r = idx / kT, c = idx % kT;
+        const int i = X0 + c, j = Y0 + r;
+        if (i >= W || j >= H) continue;
+        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int t = 0; t < 2 * kR + 1; ++t) {
+            const float w = a.w[t];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) m[q] += w * s_h[q][r + t][c];
+        }
+        // metrics.hpp:199-215, evaluated in double per pixel
+        const double mx = m[0], my = m[1];
+        const double vx = m[2] - mx * mx, vy = m[4] - my * my, vxy = m[3] - mx * my;
+        const double a1 = 2.0 * mx * my + kC1, a2 = 2.0 * vxy + kC2;
+        const double b1 = mx * mx + my * my + kC1, b2 = vx + vy + kC2;
+        const double s = (a1 * a2) / (b1 * b2);
+        const double inv_b1b2 = 1.0 / (b1 * b2);
+        const double ds_dm2 = -s / b2;
+        const double ds_dm12 = 2.0 * a1 * inv_b1b2;
+        const double ds_dm1 = 2.0 * my * a2 * inv_b1b2 - 2.0 * mx * s / b1 + 2.0 * mx * s / b2 -
+                              2.0 * my * a1 * inv_b1b2;
+        const size_t o = (size_t)j * W + i;
+        a.g[o] = (float)(ds_dm1 * inv_n);
+        a.g[P + o] = (float)(ds_dm2 * inv_n);
+        a.g[2 * P + o] = (float)(ds_dm12 * inv_n);
+        ssum += s;
+        l1 += fabs((double)(s_x[r + kR][c + kR] - s_y[r + kR][c + kR]));
+    }
+    block_sum2(ssum, l1, s_red);
+    if (threadIdx.x == 0) {
+        const unsigned b = blockIdx.y * gridDim.x + blockIdx.x;
+        a.partial[2 * b] = ssum;
+        a.partial[2 * b + 1] = l1;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_ssim_bwd(const LossLaunch a) {
+    __shared__ float s_g[3][kH][kH + 1];
+    __shared__ float s_h[3][kH][kT + 1];
+    const int X0 = blockIdx.x * kT, Y0 = blockIdx.y * kT;
+    const int W = a.W, H = a.H;
+    const size_t P = (size_t)W * H;
+    for (int idx = threadIdx.x; idx < kH * kH; idx += blockDim.x) {
+        const int r = idx / kH, c = idx % kH;
+        const size_t o = (size_t)reflect(Y0 + r - kR, H) * W + reflect(X0 + c - kR, W);
+        s_g[0][r][c] = a.g[o];
+        s_g[1][r][c] = a.g[P + o];
+        s_g[2][r][c] = a.g[2 * P + o];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kH * kT; idx += blockDim.x) {
+        const int r = idx / kT, c = idx % kT;
+        float h0 = 0.f, h1 = 0.f, h2 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 2 * kR + 1; ++t) {
+            const float w = a.w[t];
+            h0 += w * s_g[0][r][c + t];
+            h1 += w * s_g[1][r][c + t];
+            h2 += w * s_g[2][r][c + t];
+        }
+        s_h[0][r][c] = h0;
+        s_h[1][r][c] = h1;
+        s_h[2][r][c] = h2;
+    }
+    __syncthreads();
+    const float inv_n = (float)(1.0 / (double)P);
+    const float k = (float)(a.lambda * a.dssim_scale);
+    for (int idx = threadIdx.x; idx < kT * kT; idx += blockDim.x) {
+        const int r = idx / kT, c = idx % kT;
+        const int i = X0 + c, j = Y0 + r;
+        if (i >= W || j >= H) continue;
+        float A0 = 0.f, A1 = 0.f, A2 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 2 * kR + 1; ++t) {
+            const float w = a.w[t];
+            A0 += w * s_h[0][r + t][c];
+            A1 += w * s_h[1][r + t][c];
+            A2 += w * s_h[2][r + t][c];
+        }
+        const size_t o = (size_t)j * W + i;
+        const float x = a.image[o], y = a.target[o];
+        const float gs = A0 + 2.f * x * A1 + y * A2;
+        const float d = x - y;
+        a.dl_di[o] = (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) * inv_n + k * (-gs);
+    }
+    finish_loss(a, true);
+}
+
+}  // namespace
+
+void launch_loss(const LossLaunch& a, cudaStream_t st) {
+    if (a.lambda == 0.0) {
+        const size_t n = (size_t)a.W * a.H;
+        const unsigned grid = (unsigned)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+        k_l1_only<<<grid, 256, 0, st>>>(a);
+        return;
+    }
+    const dim3 grid((a.W + kT - 1) / kT, (a.H + kT - 1) / kT);
+    k_ssim_fwd<<<grid, 256, 0, st>>>(a);
+    k_ssim_bwd<<<grid, 256, 0, st>>>(a);
+}
+
+unsigned loss_partial_blocks(int W, int H, double lambda) {
+    if (lambda == 0.0) {
+        const size_t n = (size_t)W * H;
+        return (unsigned)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+    }
+    return (unsigned)(((W + kT - 1) / kT) * ((H + kT - 1) / kT));
+}
+
+}  // namespace gpk

@@ -1,0 +1,1158 @@
+// session.cu — C-ABI implementation (include/gpile_b200.h): device-resident
+// session state, host-side validation with the reference's error semantics,
+// and the launch sequence of each reference entry point.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gpile_b200.h"
+#include "common.cuh"
+
+using namespace gpk;
+
+namespace {
+
+thread_local std::string t_err;
+thread_local int64_t t_err_index = -1;
+
+int fail(int code, const std::string& msg, int64_t index = -1) {
+    t_err = msg;
+    t_err_index = index;
+    return code;
+}
+
+int ok() {
+    t_err.clear();
+    t_err_index = -1;
+    return GPK_OK;
+}
+
+#define CK(expr)                                                                        \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess) {                                                        \
+            if (_e == cudaErrorMemoryAllocation)                                        \
+                return fail(GPK_ERR_OUT_OF_MEMORY, std::string("cuda: ") + cudaGetErrorString(_e)); \
+            return fail(GPK_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+        }                                                                               \
+    } while (0)
+
+#define TRY(expr)                 \
+    do {                          \
+        int _s = (expr);          \
+        if (_s != GPK_OK) return _s; \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    // (Re)allocate to at least `need` bytes; contents are NOT preserved.
+    cudaError_t ensure(size_t need) {
+        if (need <= bytes && p) return cudaSuccess;
+        release();
+        if (need == 0) need = 16;
+        cudaError_t e = cudaMalloc(&p, need);
+        if (e == cudaSuccess) bytes = need;
+        return e;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct PrepState {
+    bool valid = false;
+    SliceArgs slice{};
+    int tiles = 0;
+    int passes = 0;
+    int final_buf = 0;          // which key/val buffer holds the sorted pairs
+    bool rasterized = false;
+    bool grads_zeroed = false;  // K_prep zero-filled non-survivor gradients
+    gpk_slice_pose pose{};
+    gpk_psf psf{};
+    gpk_raster_config cfg{};
+};
+
+}  // namespace
+
+struct gpk_session {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint64_t n = 0, cap = 0;
+    gpk_bounds bbox{};
+    uint64_t pair_cap = 0;
+
+    DevBuf params, grads, adam_m, adam_v, records, survivors;
+    DevBuf keys[2], vals[2], partials, sort_status;
+    DevBuf head;       // Control | hist | prep flags (memset per prepare)
+    DevBuf prep_vals;  // agg + incl per K_prep block
+    DevBuf persist;    // ErrorState | epoch | adam step | adam done ctr | loss done ctr | loss
+    DevBuf image, dl_di, target, loss_g, loss_partial;
+    DevBuf stat_norm, stat_obs, stat_world;
+    int img_w = 0, img_h = 0;
+
+    PrepState prep;
+
+    // live stage timing
+    bool timing = false;
+    struct Pending {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    double stage_ms[GPK_NUM_STAGES] = {};
+    uint64_t stage_cnt[GPK_NUM_STAGES] = {};
+
+    // persist layout
+    ErrorState* err() { return persist.as<ErrorState>(); }
+    unsigned* epoch() { return reinterpret_cast<unsigned*>(persist.as<char>() + 64); }
+    long long* adam_step() { return reinterpret_cast<long long*>(persist.as<char>() + 72); }
+    unsigned* adam_done() { return reinterpret_cast<unsigned*>(persist.as<char>() + 80); }
+    unsigned* loss_done() { return reinterpret_cast<unsigned*>(persist.as<char>() + 84); }
+    double* loss() { return reinterpret_cast<double*>(persist.as<char>() + 88); }
+    Control* ctrl() { return head.as<Control>(); }
+    unsigned* hist() { return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control)); }
+    unsigned* prep_flags() {
+        return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control) +
+                                           kMaxSortPasses * 256 * sizeof(unsigned));
+    }
+};
+
+namespace {
+
+constexpr size_t kPersistBytes = 128;
+
+cudaEvent_t take_event(gpk_session* s) {
+    if (!s->event_pool.empty()) {
+        cudaEvent_t e = s->event_pool.back();
+        s->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Fold completed event pairs into the per-stage totals (stream synchronized).
+void drain_timing(gpk_session* s) {
+    for (auto& p : s->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            s->stage_ms[p.stage] += ms;
+            s->stage_cnt[p.stage] += 1;
+        }
+        s->event_pool.push_back(p.a);
+        s->event_pool.push_back(p.b);
+    }
+    s->pending.clear();
+}
+
+// Event pair around one stage launch when timing is enabled.
+struct StageScope {
+    gpk_session* s;
+    int stage;
+    cudaEvent_t a = nullptr;
+    StageScope(gpk_session* s_, int st) : s(s_), stage(st) {
+        if (!s->timing) return;
+        if (s->pending.size() >= 8192) {
+            cudaStreamSynchronize(s->stream);
+            drain_timing(s);
+        }
+        a = take_event(s);
+        cudaEventRecord(a, s->stream);
+    }
+    void end() {
+        if (!a) return;
+        cudaEvent_t b = take_event(s);
+        cudaEventRecord(b, s->stream);
+        s->pending.push_back({stage, a, b});
+        a = nullptr;
+    }
+    ~StageScope() { end(); }
+};
+
+int set_device(gpk_session* s) {
+    CK(cudaSetDevice(s->device));
+    return GPK_OK;
+}
+
+uint64_t prep_blocks(uint64_t n) { return (n + kPrepBlock - 1) / kPrepBlock; }
+
+int clear_errors(gpk_session* s) {
+    ErrorState e;
+    for (int k = 0; k < 4; ++k) e.first_index[k] = ~0ull;
+    CK(cudaMemcpyAsync(s->err(), &e, sizeof(e), cudaMemcpyHostToDevice, s->stream));
+    return GPK_OK;
+}
+
+// Read the device error record (stream must be synchronized) and map the first
+// failing primitive to the reference's exception types.
+int surface_errors(gpk_session* s, const char* where) {
+    ErrorState e;
+    CK(cudaMemcpy(&e, s->err(), sizeof(e), cudaMemcpyDeviceToHost));
+    int best = 0;
+    unsigned long long idx = ~0ull;
+    for (int k = 1; k < 4; ++k)
+        if (e.first_index[k] < idx) {
+            idx = e.first_index[k];
+            best = k;
+        }
+    if (best == 0) return GPK_OK;
+    TRY(clear_errors(s));
+    CK(cudaStreamSynchronize(s->stream));
+    char buf[256];
+    switch (best) {
+        case kErrInvalid:
+            snprintf(buf, sizeof buf, "%s: invalid primitive %llu (zero-norm quaternion or non-positive scale)",
+                     where, idx);
+            return fail(GPK_ERR_INVALID_ARGUMENT, buf, (int64_t)idx);
+        case kErrDegenerate:
+            snprintf(buf, sizeof buf, "%s: non-positive det(Sigma_2d) or covariance not SPD for primitive %llu",
+                     where, idx);
+            return fail(GPK_ERR_DEGENERATE_COVARIANCE, buf, (int64_t)idx);
+        default:
+            snprintf(buf, sizeof buf, "%s: non-finite gradient for primitive %llu", where, idx);
+            return fail(GPK_ERR_NUMERIC_FAILURE, buf, (int64_t)idx);
+    }
+}
+
+int sync_and_check(gpk_session* s, const char* where) {
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaGetLastError());
+    return surface_errors(s, where);
+}
+
+int ensure_pairs(gpk_session* s, uint64_t need) {
+    if (need <= s->pair_cap && s->keys[0].p) return GPK_OK;
+    const uint64_t cap = std::max<uint64_t>(need, 1ull << 16);
+    for (int b = 0; b < 2; ++b) {
+        CK(s->keys[b].ensure(cap * 4));
+        CK(s->vals[b].ensure(cap * 4));
+    }
+    CK(s->partials.ensure(cap * 24));
+    const uint64_t st_tiles = (cap + kSortTile - 1) / kSortTile;
+    const size_t st_bytes = (size_t)kMaxSortPasses * st_tiles * 256 * 8;
+    CK(s->sort_status.ensure(st_bytes));
+    CK(cudaMemsetAsync(s->sort_status.p, 0, st_bytes, s->stream));
+    s->pair_cap = cap;
+    return GPK_OK;
+}
+
+int ensure_image(gpk_session* s, int w, int h) {
+    const size_t px = (size_t)w * h;
+    CK(s->image.ensure(px * 4));
+    CK(s->dl_di.ensure(px * 4));
+    CK(s->target.ensure(px * 4));
+    s->img_w = w;
+    s->img_h = h;
+    return GPK_OK;
+}
+
+int validate_psf(const gpk_psf* psf) {
+    // PsfSpec::validate (core.hpp:112-116)
+    if (!(psf->sigma_x > 0.0) || !(psf->sigma_y > 0.0) || !(psf->sigma_z > 0.0) ||
+        !std::isfinite(psf->sigma_x) || !std::isfinite(psf->sigma_y) || !std::isfinite(psf->sigma_z))
+        return fail(GPK_ERR_INVALID_ARGUMENT, "PsfSpec: sigmas must be positive and finite");
+    return GPK_OK;
+}
+
+int make_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+               const gpk_raster_config* cfg, SliceArgs& a) {
+    if (!pose || !psf || !cfg) return fail(GPK_ERR_INVALID_ARGUMENT, "null pose/psf/config");
+    TRY(validate_psf(psf));
+    if (pose->width < 1 || pose->height < 1)
+        return fail(GPK_ERR_INVALID_ARGUMENT, "SlicePose: width/height must be >= 1");
+    if (pose->width > 65535 || pose->height > 65535)
+        return fail(GPK_ERR_INVALID_ARGUMENT, "SlicePose: width/height above 65535 unsupported");
+    if (cfg->tile_size != kTile)
+        return fail(GPK_ERR_INVALID_ARGUMENT, "RasterConfig: this backend supports tile_size == 16");
+    if (s->n > 0 && !(cfg->scale_modifier > 0.0))
+        return fail(GPK_ERR_INVALID_ARGUMENT,
+                    "covariance_from_scale_rotation: scale and mod must be > 0", 0);
+    memset(&a, 0, sizeof a);
+    bool ident = true;
+    for (int i = 0; i < 9; ++i) {
+        a.R[i] = pose->rotation[i];
+        const double e = (i % 4 == 0) ? 1.0 : 0.0;
+        if (pose->rotation[i] != e) ident = false;
+    }
+    for (int i = 0; i < 3; ++i) a.t[i] = pose->translation[i];
+    a.sx = pose->pixel_spacing[0];
+    a.sy = pose->pixel_spacing[1];
+    a.ppx = pose->principal_point[0];
+    a.ppy = pose->principal_point[1];
+    a.sigma_z = psf->sigma_z;
+    a.tau = cfg->tau;
+    a.footprint = cfg->footprint_sigmas;
+    a.mod = cfg->scale_modifier;
+    a.W = pose->width;
+    a.H = pose->height;
+    a.tiles_x = (pose->width + kTile - 1) / kTile;
+    a.tiles_y = (pose->height + kTile - 1) / kTile;
+    a.identity_rot = ident ? 1 : 0;
+    return GPK_OK;
+}
+
+int sort_passes(int tiles) {
+    int bits = 0;
+    while (bits < 32 && (1ull << bits) < (unsigned long long)tiles) ++bits;
+    return (bits + 7) / 8;
+}
+
+int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                const gpk_raster_config* cfg, bool zero_grads) {
+    SliceArgs a;
+    TRY(make_slice(s, pose, psf, cfg, a));
+    TRY(ensure_image(s, a.W, a.H));
+    if (!s->keys[0].p) TRY(ensure_pairs(s, std::max<uint64_t>(1ull << 20, 8 * s->n)));
+    PrepState& ps = s->prep;
+    ps.slice = a;
+    ps.tiles = a.tiles_x * a.tiles_y;
+    ps.passes = sort_passes(ps.tiles);
+    ps.pose = *pose;
+    ps.psf = *psf;
+    ps.cfg = *cfg;
+    ps.valid = true;
+    ps.rasterized = false;
+    ps.grads_zeroed = zero_grads;
+    const uint64_t nb = prep_blocks(s->n);
+    const size_t head_bytes = sizeof(Control) + kMaxSortPasses * 256 * sizeof(unsigned) +
+                              std::max<uint64_t>(nb, 1) * sizeof(unsigned);
+    StageScope scope_prep(s, GPK_STAGE_PREPARE);
+    CK(cudaMemsetAsync(s->head.p, 0, head_bytes, s->stream));
+    if (s->n == 0) {
+        ps.final_buf = 0;
+        return GPK_OK;
+    }
+    PrepLaunch pl;
+    pl.params = s->params.as<float>();
+    pl.cap = s->cap;
+    pl.n = (uint32_t)s->n;
+    pl.grads = zero_grads ? s->grads.as<float>() : nullptr;
+    pl.records = s->records.as<SurvivorRecord>();
+    pl.survivor_list = s->survivors.as<uint32_t>();
+    pl.keys = s->keys[0].as<uint32_t>();
+    pl.vals = s->vals[0].as<uint32_t>();
+    pl.pair_cap = s->pair_cap;
+    pl.hist = s->hist();
+    pl.passes = ps.passes;
+    pl.epoch = s->epoch();
+    pl.prep_flags = s->prep_flags();
+    pl.prep_agg = s->prep_vals.as<unsigned long long>();
+    pl.prep_incl = s->prep_vals.as<unsigned long long>() + nb;
+    pl.ctrl = s->ctrl();
+    pl.err = s->err();
+    pl.slice = a;
+    launch_prep(pl, s->stream);
+    CK(cudaGetLastError());
+    scope_prep.end();
+    StageScope scope_sort(s, GPK_STAGE_SORT);
+
+    const int grid = (int)std::min<uint64_t>((s->pair_cap + kSortTile - 1) / kSortTile, 148 * 4);
+    const uint64_t st_tiles = (s->pair_cap + kSortTile - 1) / kSortTile;
+    for (int p = 0; p < ps.passes; ++p) {
+        SortLaunch sl;
+        sl.keys_in = s->keys[p & 1].as<uint32_t>();
+        sl.vals_in = s->vals[p & 1].as<uint32_t>();
+        sl.keys_out = s->keys[(p + 1) & 1].as<uint32_t>();
+        sl.vals_out = s->vals[(p + 1) & 1].as<uint32_t>();
+        sl.hist = s->hist() + 256 * p;
+        sl.status = s->sort_status.as<unsigned long long>() + (size_t)p * st_tiles * 256;
+        sl.epoch = s->epoch();
+        sl.shift = 8 * p;
+        sl.pass = p;
+        sl.ctrl_ro = s->ctrl();
+        sl.ctrl = s->ctrl();
+        sl.pair_cap = s->pair_cap;
+        launch_sort_pass(sl, grid, s->stream);
+        CK(cudaGetLastError());
+    }
+    ps.final_buf = ps.passes & 1;
+    return GPK_OK;
+}
+
+RasterLaunch raster_args(gpk_session* s) {
+    RasterLaunch r;
+    r.records = s->records.as<SurvivorRecord>();
+    r.keys = s->keys[s->prep.final_buf].as<uint32_t>();
+    r.vals = s->vals[s->prep.final_buf].as<uint32_t>();
+    r.ctrl = s->ctrl();
+    r.pair_cap = s->pair_cap;
+    r.image = s->image.as<float>();
+    r.dl_di = s->dl_di.as<float>();
+    r.partials = s->partials.as<float>();
+    r.slice = s->prep.slice;
+    return r;
+}
+
+int run_rasterize(gpk_session* s) {
+    if (!s->prep.valid) return fail(GPK_ERR_STATE, "rasterize: no prepared slice");
+    const size_t px = (size_t)s->img_w * s->img_h;
+    StageScope scope(s, GPK_STAGE_RASTER);
+    if (s->n == 0) {
+        CK(cudaMemsetAsync(s->image.p, 0, px * 4, s->stream));
+    } else {
+        launch_raster_fwd(raster_args(s), s->stream);
+        CK(cudaGetLastError());
+    }
+    s->prep.rasterized = true;
+    return GPK_OK;
+}
+
+int run_backward(gpk_session* s, bool stats) {
+    if (!s->prep.valid) return fail(GPK_ERR_STATE, "backward: no prepared slice");
+    if (s->n == 0) return GPK_OK;
+    if (!s->prep.grads_zeroed) {
+        CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
+    }
+    if (stats) {
+        CK(s->stat_norm.ensure(s->cap * 4));
+        CK(s->stat_obs.ensure(s->cap));
+        CK(s->stat_world.ensure(s->cap * 12));
+        CK(cudaMemsetAsync(s->stat_norm.p, 0, s->cap * 4, s->stream));
+        CK(cudaMemsetAsync(s->stat_obs.p, 0, s->cap, s->stream));
+        CK(cudaMemsetAsync(s->stat_world.p, 0, s->cap * 12, s->stream));
+    }
+    {
+        StageScope scope(s, GPK_STAGE_BACKWARD);
+        launch_raster_bwd(raster_args(s), s->stream);
+        CK(cudaGetLastError());
+    }
+    StageScope scope(s, GPK_STAGE_CHAIN);
+    ChainLaunch c;
+    c.params = s->params.as<float>();
+    c.cap = s->cap;
+    c.records = s->records.as<SurvivorRecord>();
+    c.survivor_list = s->survivors.as<uint32_t>();
+    c.partials = s->partials.as<float>();
+    c.ctrl = s->ctrl();
+    c.grads = s->grads.as<float>();
+    c.stat_norm = stats ? s->stat_norm.as<float>() : nullptr;
+    c.stat_observed = stats ? s->stat_obs.as<uint8_t>() : nullptr;
+    c.stat_world = stats ? s->stat_world.as<float>() : nullptr;
+    c.err = s->err();
+    c.slice = s->prep.slice;
+    const int grid = (int)std::min<uint64_t>((s->n + 127) / 128, 148 * 8);
+    launch_chain(c, grid, s->stream);
+    CK(cudaGetLastError());
+    return GPK_OK;
+}
+
+// Synchronize; if the slice produced more pairs than the buffers hold, grow
+// them and replay prepare (+ rasterize). Returns GPK_OK when the prepared
+// state is complete.
+int settle_pairs(gpk_session* s) {
+    CK(cudaStreamSynchronize(s->stream));
+    Control c;
+    CK(cudaMemcpy(&c, s->ctrl(), sizeof c, cudaMemcpyDeviceToHost));
+    if (!c.pair_overflow) return GPK_OK;
+    TRY(ensure_pairs(s, (uint64_t)c.pairs + c.pairs / 4 + 1024));
+    const bool ras = s->prep.rasterized;
+    const PrepState saved = s->prep;
+    TRY(run_prepare(s, &saved.pose, &saved.psf, &saved.cfg, saved.grads_zeroed));
+    if (ras) TRY(run_rasterize(s));
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaMemcpy(&c, s->ctrl(), sizeof c, cudaMemcpyDeviceToHost));
+    if (c.pair_overflow) return fail(GPK_ERR_STATE, "pair capacity still exceeded after growth");
+    return GPK_OK;
+}
+
+int copy_params_in(gpk_session* s, uint64_t n, const float* rec) {
+    // AoS record -> 11 SoA planes on the host, then one H2D per plane.
+    std::vector<float> plane(n);
+    for (int k = 0; k < 11; ++k) {
+        for (uint64_t i = 0; i < n; ++i) plane[i] = rec[11 * i + k];
+        CK(cudaMemcpyAsync(s->params.as<float>() + (size_t)k * s->cap, plane.data(), n * 4,
+                           cudaMemcpyHostToDevice, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    }
+    return GPK_OK;
+}
+
+int copy_planes_out(gpk_session* s, const float* dev, float* rec) {
+    const uint64_t n = s->n;
+    std::vector<float> plane(n);
+    for (int k = 0; k < 11; ++k) {
+        CK(cudaMemcpyAsync(plane.data(), dev + (size_t)k * s->cap, n * 4, cudaMemcpyDeviceToHost,
+                           s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        for (uint64_t i = 0; i < n; ++i) rec[11 * i + k] = plane[i];
+    }
+    return GPK_OK;
+}
+
+int alloc_for_n(gpk_session* s, uint64_t n) {
+    const uint64_t cap = std::max<uint64_t>(n, 1);
+    if (cap > s->cap || !s->params.p) {
+        CK(s->params.ensure(cap * 11 * 4));
+        CK(s->grads.ensure(cap * 11 * 4));
+        CK(s->adam_m.ensure(cap * 11 * 4));
+        CK(s->adam_v.ensure(cap * 11 * 4));
+        const uint64_t nb = prep_blocks(cap);
+        CK(s->records.ensure(nb * kPrepBlock * sizeof(SurvivorRecord)));
+        CK(s->survivors.ensure(cap * 4));
+        CK(s->prep_vals.ensure(std::max<uint64_t>(nb, 1) * 16));
+        CK(s->head.ensure(sizeof(Control) + kMaxSortPasses * 256 * 4 + std::max<uint64_t>(nb, 1) * 4));
+        s->cap = cap;
+    }
+    s->n = n;
+    return GPK_OK;
+}
+
+int adam_reset(gpk_session* s) {
+    CK(cudaMemsetAsync(s->adam_m.p, 0, s->cap * 11 * 4, s->stream));
+    CK(cudaMemsetAsync(s->adam_v.p, 0, s->cap * 11 * 4, s->stream));
+    CK(cudaMemsetAsync(s->adam_step(), 0, 16, s->stream));
+    return GPK_OK;
+}
+
+int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
+             const gpk_adam_hparams* hp) {
+    if (s->n == 0) {
+        long long st = 0;
+        CK(cudaMemcpyAsync(&st, s->adam_step(), 8, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        ++st;
+        CK(cudaMemcpyAsync(s->adam_step(), &st, 8, cudaMemcpyHostToDevice, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        return GPK_OK;
+    }
+    AdamLaunch a;
+    a.params = s->params.as<float>();
+    a.grads = s->grads.as<float>();
+    a.m = s->adam_m.as<float>();
+    a.v = s->adam_v.as<float>();
+    a.cap = s->cap;
+    a.n = (uint32_t)s->n;
+    for (int d = 0; d < 3; ++d) {
+        a.bbox_min[d] = (float)s->bbox.min[d];
+        a.bbox_max[d] = (float)s->bbox.max[d];
+    }
+    for (int k = 0; k < 4; ++k) a.lr[k] = lr[k];
+    a.scheduled = scheduled ? 1 : 0;
+    a.total = total;
+    a.beta1 = hp ? hp->beta1 : 0.9;
+    a.beta2 = hp ? hp->beta2 : 0.999;
+    a.eps = hp ? hp->eps : 1e-8;
+    a.step = s->adam_step();
+    a.done_ctr = s->adam_done();
+    a.ctrl = s->prep.valid ? s->ctrl() : nullptr;
+    StageScope scope(s, GPK_STAGE_ADAM);
+    launch_adam(a, s->stream);
+    CK(cudaGetLastError());
+    return GPK_OK;
+}
+
+int run_loss(gpk_session* s, double lambda, double dssim_scale) {
+    if (!s->prep.rasterized) return fail(GPK_ERR_STATE, "photometric_loss: no rendered image");
+    const int W = s->img_w, H = s->img_h;
+    const size_t px = (size_t)W * H;
+    if (lambda != 0.0) CK(s->loss_g.ensure(px * 12));
+    CK(s->loss_partial.ensure((size_t)loss_partial_blocks(W, H, lambda) * 16));
+    LossLaunch l;
+    l.image = s->image.as<float>();
+    l.target = s->target.as<float>();
+    l.dl_di = s->dl_di.as<float>();
+    l.g = s->loss_g.as<float>();
+    l.partial = s->loss_partial.as<double>();
+    l.loss = s->loss();
+    l.done_ctr = s->loss_done();
+    l.W = W;
+    l.H = H;
+    l.lambda = lambda;
+    l.dssim_scale = dssim_scale;
+    // gaussian_window(5, 1.5) (metrics.hpp:66-75)
+    double w[11], sum = 0.0;
+    for (int t = -5; t <= 5; ++t) {
+        w[t + 5] = std::exp(-0.5 * t * t / (1.5 * 1.5));
+        sum += w[t + 5];
+    }
+    for (int t = 0; t < 11; ++t) l.w[t] = (float)(w[t] / sum);
+    StageScope scope(s, GPK_STAGE_LOSS);
+    launch_loss(l, s->stream);
+    CK(cudaGetLastError());
+    return GPK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gpk_abi_version(void) { return GPK_ABI_VERSION; }
+const char* gpk_last_error_message(void) { return t_err.c_str(); }
+int64_t gpk_last_error_index(void) { return t_err_index; }
+
+int gpk_device_count(int* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return fail(GPK_ERR_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    *count = c;
+    return ok();
+}
+
+int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
+    if (!out) return fail(GPK_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    auto* s = new gpk_session;
+    s->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete s;
+        return fail(GPK_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    }
+    if (cuda_stream) {
+        s->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+        e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete s;
+            return fail(GPK_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+        }
+        s->own_stream = true;
+    }
+    e = s->persist.ensure(kPersistBytes);
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->persist.p, 0, kPersistBytes, s->stream);
+    if (e == cudaSuccess) {
+        ErrorState es;
+        for (int k = 0; k < 4; ++k) es.first_index[k] = ~0ull;
+        e = cudaMemcpyAsync(s->err(), &es, sizeof es, cudaMemcpyHostToDevice, s->stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    if (e != cudaSuccess) {
+        gpk_session_destroy(s);
+        return fail(GPK_ERR_CUDA, std::string("session init: ") + cudaGetErrorString(e));
+    }
+    if (alloc_for_n(s, 0) != GPK_OK) {
+        gpk_session_destroy(s);
+        return GPK_ERR_OUT_OF_MEMORY;
+    }
+    *out = s;
+    return ok();
+}
+
+int gpk_session_destroy(gpk_session* s) {
+    if (!s) return ok();
+    cudaSetDevice(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    DevBuf* bufs[] = {&s->params, &s->grads, &s->adam_m, &s->adam_v, &s->records, &s->survivors,
+                      &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials,
+                      &s->sort_status, &s->head, &s->prep_vals, &s->persist, &s->image,
+                      &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm,
+                      &s->stat_obs, &s->stat_world};
+    for (DevBuf* b : bufs) b->release();
+    drain_timing(s);
+    for (cudaEvent_t e : s->event_pool) cudaEventDestroy(e);
+    if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+    return ok();
+}
+
+int gpk_session_set_stream(gpk_session* s, void* cuda_stream) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    if (s->own_stream) cudaStreamDestroy(s->stream);
+    s->own_stream = false;
+    s->stream = static_cast<cudaStream_t>(cuda_stream);
+    return ok();
+}
+
+int gpk_session_get_stream(gpk_session* s, void** cuda_stream) {
+    if (!s || !cuda_stream) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    *cuda_stream = s->stream;
+    return ok();
+}
+
+int gpk_session_synchronize(gpk_session* s) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    TRY(sync_and_check(s, "session"));
+    if (s->prep.valid) {
+        Control c;
+        CK(cudaMemcpy(&c, s->ctrl(), sizeof c, cudaMemcpyDeviceToHost));
+        if (c.pair_overflow) {
+            char buf[160];
+            snprintf(buf, sizeof buf,
+                     "tile pair capacity exceeded (%u pairs > %llu); call gpk_session_reserve_pairs",
+                     c.pairs, (unsigned long long)s->pair_cap);
+            return fail(GPK_ERR_STATE, buf);
+        }
+    }
+    return ok();
+}
+
+int gpk_session_reserve_pairs(gpk_session* s, uint64_t pairs) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    TRY(ensure_pairs(s, pairs));
+    CK(cudaStreamSynchronize(s->stream));
+    return ok();
+}
+
+int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
+    if (!s || !ptr) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    const size_t px = (size_t)s->img_w * s->img_h;
+    void* p = nullptr;
+    uint64_t b = 0;
+    switch (which) {
+        case GPK_BUF_PARAMS: p = s->params.p; b = s->cap * 44; break;
+        case GPK_BUF_GRADS: p = s->grads.p; b = s->cap * 44; break;
+        case GPK_BUF_IMAGE: p = s->image.p; b = px * 4; break;
+        case GPK_BUF_DL_DI: p = s->dl_di.p; b = px * 4; break;
+        case GPK_BUF_TARGET: p = s->target.p; b = px * 4; break;
+        case GPK_BUF_LOSS: p = s->loss(); b = 8; break;
+        default: return fail(GPK_ERR_INVALID_ARGUMENT, "unknown or unallocated buffer");
+    }
+    *ptr = p;
+    if (bytes) *bytes = b;
+    return ok();
+}
+
+int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes) {
+    void* p = nullptr;
+    uint64_t cap = 0;
+    TRY(gpk_device_buffer(s, which, &p, &cap));
+    if (!host || bytes > cap) return fail(GPK_ERR_INVALID_ARGUMENT, "upload: size exceeds buffer");
+    TRY(set_device(s));
+    CK(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, s->stream));
+    return ok();
+}
+
+int gpk_download(gpk_session* s, int which, void* host, uint64_t bytes) {
+    void* p = nullptr;
+    uint64_t cap = 0;
+    TRY(gpk_device_buffer(s, which, &p, &cap));
+    if (!host || bytes > cap) return fail(GPK_ERR_INVALID_ARGUMENT, "download: size exceeds buffer");
+    TRY(set_device(s));
+    CK(cudaMemcpyAsync(host, p, bytes, cudaMemcpyDeviceToHost, s->stream));
+    return ok();
+}
+
+int gpk_stage_timing(gpk_session* s, int enable) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    s->timing = enable != 0;
+    return ok();
+}
+
+int gpk_stage_times(gpk_session* s, double* ms, uint64_t* counts, int reset) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    drain_timing(s);
+    for (int k = 0; k < GPK_NUM_STAGES; ++k) {
+        if (ms) ms[k] = s->stage_ms[k];
+        if (counts) counts[k] = s->stage_cnt[k];
+        if (reset) {
+            s->stage_ms[k] = 0.0;
+            s->stage_cnt[k] = 0;
+        }
+    }
+    return ok();
+}
+
+int gpk_set_gaussians(gpk_session* s, uint64_t n, const float* records, const gpk_bounds* bbox) {
+    if (!s || (n && !records) || !bbox) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (n >= (1ull << 31)) return fail(GPK_ERR_INVALID_ARGUMENT, "set size must be < 2^31");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    TRY(alloc_for_n(s, n));
+    s->bbox = *bbox;
+    if (n) TRY(copy_params_in(s, n, records));
+    s->prep.valid = false;
+    TRY(adam_reset(s));
+    CK(cudaStreamSynchronize(s->stream));
+    return ok();
+}
+
+int gpk_set_gaussians_f64(gpk_session* s, uint64_t n, const double* records,
+                          const gpk_bounds* bbox) {
+    std::vector<float> f(n * 11);
+    for (uint64_t i = 0; i < n * 11; ++i) f[i] = (float)records[i];
+    return gpk_set_gaussians(s, n, f.data(), bbox);
+}
+
+int gpk_get_gaussians(gpk_session* s, float* records) {
+    if (!s || (s->n && !records)) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    if (s->n) TRY(copy_planes_out(s, s->params.as<float>(), records));
+    return ok();
+}
+
+int gpk_set_gradients(gpk_session* s, const float* grads) {
+    if (!s || (s->n && !grads)) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    const uint64_t n = s->n;
+    std::vector<float> plane(n);
+    for (int k = 0; k < 11; ++k) {
+        for (uint64_t i = 0; i < n; ++i) plane[i] = grads[11 * i + k];
+        CK(cudaMemcpy(s->grads.as<float>() + (size_t)k * s->cap, plane.data(), n * 4,
+                      cudaMemcpyHostToDevice));
+    }
+    return ok();
+}
+
+int gpk_get_gradients(gpk_session* s, float* grads) {
+    if (!s || (s->n && !grads)) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    TRY(set_device(s));
+    TRY(sync_and_check(s, "gradients"));
+    if (s->n) TRY(copy_planes_out(s, s->grads.as<float>(), grads));
+    return ok();
+}
+
+int gpk_gaussian_count(gpk_session* s, uint64_t* n) {
+    if (!s || !n) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    *n = s->n;
+    return ok();
+}
+
+int gpk_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                const gpk_raster_config* cfg) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    TRY(run_prepare(s, pose, psf, cfg, false));
+    return ok();
+}
+
+int gpk_prepared_count(gpk_session* s, uint64_t* survivors, uint64_t* pairs) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    if (!s->prep.valid) return fail(GPK_ERR_STATE, "no prepared slice");
+    TRY(set_device(s));
+    TRY(settle_pairs(s));
+    TRY(sync_and_check(s, "prepare_gaussians"));
+    Control c;
+    CK(cudaMemcpy(&c, s->ctrl(), sizeof c, cudaMemcpyDeviceToHost));
+    if (survivors) *survivors = s->n ? c.survivors : 0;
+    if (pairs) *pairs = s->n ? c.pairs : 0;
+    return ok();
+}
+
+int gpk_get_prepared(gpk_session* s, uint32_t* index, int32_t* bounds, double* fields) {
+    uint64_t S = 0, T = 0;
+    TRY(gpk_prepared_count(s, &S, &T));
+    if (S == 0) return ok();
+    std::vector<uint32_t> list(S);
+    CK(cudaMemcpy(list.data(), s->survivors.p, S * 4, cudaMemcpyDeviceToHost));
+    std::vector<SurvivorRecord> recs(s->records.bytes / sizeof(SurvivorRecord));
+    CK(cudaMemcpy(recs.data(), s->records.p, recs.size() * sizeof(SurvivorRecord),
+                  cudaMemcpyDeviceToHost));
+    for (uint64_t k = 0; k < S; ++k) {
+        const SurvivorRecord& r = recs[list[k]];
+        if (index) index[k] = r.gidx;
+        if (bounds) {
+            bounds[4 * k + 0] = r.lo_x;
+            bounds[4 * k + 1] = r.hi_x;
+            bounds[4 * k + 2] = r.lo_y;
+            bounds[4 * k + 3] = r.hi_y;
+        }
+        if (fields) {
+            double* f = fields + 6 * k;
+            f[0] = r.alpha_tilde;
+            f[1] = r.mu2d_x;
+            f[2] = r.mu2d_y;
+            f[3] = r.conic_a;
+            f[4] = r.conic_b;
+            f[5] = r.conic_d;
+        }
+    }
+    return ok();
+}
+
+int gpk_get_tile_lists(gpk_session* s, uint32_t* offsets, uint32_t* entries) {
+    uint64_t S = 0, T = 0;
+    TRY(gpk_prepared_count(s, &S, &T));
+    const int tiles = s->prep.tiles;
+    std::vector<uint32_t> keys(T), vals(T);
+    if (T) {
+        CK(cudaMemcpy(keys.data(), s->keys[s->prep.final_buf].p, T * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(vals.data(), s->vals[s->prep.final_buf].p, T * 4, cudaMemcpyDeviceToHost));
+    }
+    std::vector<SurvivorRecord> recs;
+    if (T) {
+        recs.resize(s->records.bytes / sizeof(SurvivorRecord));
+        CK(cudaMemcpy(recs.data(), s->records.p, recs.size() * sizeof(SurvivorRecord),
+                      cudaMemcpyDeviceToHost));
+    }
+    if (offsets) {
+        uint64_t k = 0;
+        for (int t = 0; t <= tiles; ++t) {
+            while (k < T && keys[k] < (uint32_t)t) ++k;
+            offsets[t] = (uint32_t)k;
+        }
+    }
+    if (entries)
+        for (uint64_t k = 0; k < T; ++k) entries[k] = recs[vals[k]].gidx;
+    return ok();
+}
+
+int gpk_rasterize(gpk_session* s, float* image_out) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    TRY(run_rasterize(s));
+    if (image_out) {
+        TRY(settle_pairs(s));
+        TRY(sync_and_check(s, "rasterize_prepared"));
+        CK(cudaMemcpy(image_out, s->image.p, (size_t)s->img_w * s->img_h * 4,
+                      cudaMemcpyDeviceToHost));
+    }
+    return ok();
+}
+
+int gpk_backward(gpk_session* s, const float* dl_di, float* grads_out, gpk_screen_stats* stats) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    if (!s->prep.valid) return fail(GPK_ERR_STATE, "backward: no prepared slice");
+    TRY(set_device(s));
+    const size_t px = (size_t)s->img_w * s->img_h;
+    if (dl_di) CK(cudaMemcpyAsync(s->dl_di.p, dl_di, px * 4, cudaMemcpyHostToDevice, s->stream));
+    const bool host = grads_out || stats;
+    if (host) TRY(settle_pairs(s));
+    TRY(run_backward(s, stats != nullptr));
+    if (host) {
+        TRY(sync_and_check(s, "backward_slice"));
+        if (grads_out && s->n) TRY(copy_planes_out(s, s->grads.as<float>(), grads_out));
+        if (stats && s->n) {
+            std::vector<float> nrm(s->n), wld(3 * s->n);
+            CK(cudaMemcpy(nrm.data(), s->stat_norm.p, s->n * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(wld.data(), s->stat_world.p, s->n * 12, cudaMemcpyDeviceToHost));
+            if (stats->observed)
+                CK(cudaMemcpy(stats->observed, s->stat_obs.p, s->n, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < s->n; ++i) {
+                if (stats->mu2d_grad_norm) stats->mu2d_grad_norm[i] = nrm[i];
+                if (stats->world_pos_grad)
+                    for (int d = 0; d < 3; ++d) stats->world_pos_grad[3 * i + d] = wld[3 * i + d];
+            }
+        }
+    }
+    return ok();
+}
+
+int gpk_photometric_loss(gpk_session* s, const float* target, double lambda, double dssim_scale,
+                         double* loss_out, float* dl_di_out) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    if (lambda < 0.0 || !std::isfinite(lambda))
+        return fail(GPK_ERR_INVALID_ARGUMENT, "photometric_loss: lambda must be >= 0");
+    TRY(set_device(s));
+    const size_t px = (size_t)s->img_w * s->img_h;
+    if (target) CK(cudaMemcpyAsync(s->target.p, target, px * 4, cudaMemcpyHostToDevice, s->stream));
+    TRY(run_loss(s, lambda, dssim_scale));
+    if (loss_out || dl_di_out) {
+        TRY(settle_pairs(s));
+        TRY(sync_and_check(s, "photometric_loss"));
+        if (loss_out) CK(cudaMemcpy(loss_out, s->loss(), 8, cudaMemcpyDeviceToHost));
+        if (dl_di_out) CK(cudaMemcpy(dl_di_out, s->dl_di.p, px * 4, cudaMemcpyDeviceToHost));
+    }
+    return ok();
+}
+
+int gpk_photometric_loss_images(gpk_session* s, int32_t width, int32_t height,
+                                const float* rendered, const float* target, double lambda,
+                                double dssim_scale, double* loss_out, float* dl_di_out) {
+    if (!s || !rendered || !target) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (width < 1 || height < 1)
+        return fail(GPK_ERR_INVALID_ARGUMENT, "photometric_loss: image shape mismatch");
+    if (lambda < 0.0 || !std::isfinite(lambda))
+        return fail(GPK_ERR_INVALID_ARGUMENT, "photometric_loss: lambda must be >= 0");
+    TRY(set_device(s));
+    TRY(ensure_image(s, width, height));
+    const size_t px = (size_t)width * height;
+    CK(cudaMemcpyAsync(s->image.p, rendered, px * 4, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->target.p, target, px * 4, cudaMemcpyHostToDevice, s->stream));
+    s->prep.valid = false;
+    s->prep.rasterized = true;
+    TRY(run_loss(s, lambda, dssim_scale));
+    s->prep.rasterized = false;
+    TRY(sync_and_check(s, "photometric_loss"));
+    if (loss_out) CK(cudaMemcpy(loss_out, s->loss(), 8, cudaMemcpyDeviceToHost));
+    if (dl_di_out) CK(cudaMemcpy(dl_di_out, s->dl_di.p, px * 4, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+int gpk_adam_step(gpk_session* s, const gpk_learning_rates* lrs, const gpk_adam_hparams* hp) {
+    if (!s || !lrs) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    TRY(set_device(s));
+    const double lr[4] = {lrs->position, lrs->opacity, lrs->scale, lrs->rotation};
+    TRY(run_adam(s, lr, false, 1, hp));
+    return ok();
+}
+
+int gpk_adam_step_scheduled(gpk_session* s, const gpk_learning_rates* lr0, int32_t total,
+                            const gpk_adam_hparams* hp) {
+    if (!s || !lr0) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (total < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "total iterations must be >= 1");
+    TRY(set_device(s));
+    const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
+    TRY(run_adam(s, lr, true, total, hp));
+    return ok();
+}
+
+int gpk_adam_reset(gpk_session* s) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    TRY(adam_reset(s));
+    return ok();
+}
+
+int gpk_get_adam_state(gpk_session* s, float* m, float* v, int64_t* step) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    if (m && s->n) TRY(copy_planes_out(s, s->adam_m.as<float>(), m));
+    if (v && s->n) TRY(copy_planes_out(s, s->adam_v.as<float>(), v));
+    if (step) {
+        long long st = 0;
+        CK(cudaMemcpy(&st, s->adam_step(), 8, cudaMemcpyDeviceToHost));
+        *step = st;
+    }
+    return ok();
+}
+
+int gpk_set_adam_state(gpk_session* s, const float* m, const float* v, int64_t step) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    const uint64_t n = s->n;
+    std::vector<float> plane(n);
+    for (int which = 0; which < 2; ++which) {
+        const float* src = which ? v : m;
+        float* dst = which ? s->adam_v.as<float>() : s->adam_m.as<float>();
+        if (!src) continue;
+        for (int k = 0; k < 11; ++k) {
+            for (uint64_t i = 0; i < n; ++i) plane[i] = src[11 * i + k];
+            CK(cudaMemcpy(dst + (size_t)k * s->cap, plane.data(), n * 4, cudaMemcpyHostToDevice));
+        }
+    }
+    long long st = step;
+    CK(cudaMemcpy(s->adam_step(), &st, 8, cudaMemcpyHostToDevice));
+    return ok();
+}
+
+int gpk_fwd_bwd_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                      const gpk_raster_config* cfg) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    TRY(run_prepare(s, pose, psf, cfg, true));
+    TRY(run_rasterize(s));
+    TRY(run_backward(s, false));
+    return ok();
+}
+
+int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                   const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                   const gpk_learning_rates* lr0, int32_t total_iterations) {
+    if (!s || !lr0) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "total iterations must be >= 1");
+    TRY(set_device(s));
+    TRY(run_prepare(s, pose, psf, cfg, true));
+    TRY(run_rasterize(s));
+    TRY(run_loss(s, lambda, dssim_scale));
+    TRY(run_backward(s, false));
+    const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
+    TRY(run_adam(s, lr, true, total_iterations, nullptr));
+    return ok();
+}
+
+// ---- multi-GPU (NCCL loaded lazily so the library has no hard dependency) ----
+struct NcclId {
+    char internal[128];  // ncclUniqueId, passed by value
+};
+struct NcclApi {
+    void* lib = nullptr;
+    int (*get_unique_id)(void*) = nullptr;
+    int (*comm_init_rank)(void**, int, NcclId, int) = nullptr;
+    int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*comm_destroy)(void*) = nullptr;
+    const char* (*get_error_string)(int) = nullptr;
+};
+
+static NcclApi* nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* nm : names) {
+            api.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (api.lib) break;
+        }
+        if (api.lib) {
+            api.get_unique_id = (int (*)(void*))dlsym(api.lib, "ncclGetUniqueId");
+            api.comm_init_rank = (int (*)(void**, int, NcclId, int))dlsym(api.lib, "ncclCommInitRank");
+            api.all_reduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+                api.lib, "ncclAllReduce");
+            api.comm_destroy = (int (*)(void*))dlsym(api.lib, "ncclCommDestroy");
+            api.get_error_string = (const char* (*)(int))dlsym(api.lib, "ncclGetErrorString");
+        }
+    }
+    return (api.get_unique_id && api.comm_init_rank && api.all_reduce) ? &api : nullptr;
+}
+
+static void* g_comms[64] = {nullptr};
+
+static void*& session_comm(gpk_session* s) {
+    // one communicator per device ordinal
+    return g_comms[s->device & 63];
+}
+
+int gpk_nccl_get_unique_id(void* id_out128) {
+    NcclApi* api = nccl();
+    if (!api) return fail(GPK_ERR_NCCL, "libnccl.so.2 not found");
+    const int r = api->get_unique_id(id_out128);
+    if (r != 0) return fail(GPK_ERR_NCCL, "ncclGetUniqueId failed");
+    return ok();
+}
+
+int gpk_comm_init(gpk_session* s, int nranks, int rank, const void* id128) {
+    if (!s || !id128) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    NcclApi* api = nccl();
+    if (!api) return fail(GPK_ERR_NCCL, "libnccl.so.2 not found");
+    TRY(set_device(s));
+    NcclId id;
+    memcpy(id.internal, id128, 128);
+    void* comm = nullptr;
+    const int r = api->comm_init_rank(&comm, nranks, id, rank);
+    if (r != 0)
+        return fail(GPK_ERR_NCCL, std::string("ncclCommInitRank: ") +
+                                      (api->get_error_string ? api->get_error_string(r) : "error"));
+    session_comm(s) = comm;
+    return ok();
+}
+
+int gpk_comm_destroy(gpk_session* s) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    NcclApi* api = nccl();
+    void*& comm = session_comm(s);
+    if (api && comm && api->comm_destroy) api->comm_destroy(comm);
+    comm = nullptr;
+    return ok();
+}
+
+int gpk_allreduce_grads(gpk_session* s) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    NcclApi* api = nccl();
+    void* comm = session_comm(s);
+    if (!api || !comm) return fail(GPK_ERR_STATE, "allreduce: communicator not initialized");
+    TRY(set_device(s));
+    // 11 planes are contiguous with stride cap: reduce the whole [0, 11*cap) range.
+    const int r = api->all_reduce(s->grads.p, s->grads.p, s->cap * 11, /*ncclFloat32*/ 7,
+                                  /*ncclSum*/ 0, comm, s->stream);
+    if (r != 0) return fail(GPK_ERR_NCCL, "ncclAllReduce failed");
+    return ok();
+}
+
+}  // extern "C"

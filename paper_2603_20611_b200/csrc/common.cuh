@@ -67,14 +67,18 @@ struct SliceArgs {
 
 // Small control block, memset to zero at the start of every prepare.
 struct Control {
-    unsigned int prep_block_ctr;               // dynamic block id of K_prep
+    unsigned int prep_block_ctr;               // dynamic block id of K_filter
     unsigned int sort_tile_ctr[kMaxSortPasses];
-    unsigned int survivors;                    // S, written by the last K_prep block
+    unsigned int survivors;                    // S, written by the last K_exact chunk
     unsigned int pairs;                        // T (uncapped)
     unsigned int pair_overflow;                // T > capacity
     unsigned int adam_done_ctr;
-    unsigned int pad[8];
+    unsigned int candidates;                   // C, written by the last K_filter block
+    unsigned int exact_chunk_ctr;              // chunk claims of K_exact
+    unsigned int pad[6];
 };
+
+constexpr int kExactChunk = 256;               // candidates per K_exact chunk (= threads)
 
 // Device-side error record (sticky until the host reads and clears it).
 struct ErrorState {
@@ -106,6 +110,87 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// Wait-free ordered prefix, executed by one full warp of block `b`: publish the
+// block's aggregate as a single ready-tagged word, then sum ALL predecessors'
+// aggregates with independent loads (16 in flight per lane). No inclusive
+// prefix chain: latency is ~1-2 L2 round trips after the slowest predecessor
+// publishes, instead of one round trip per predecessor window. Requires that
+// every predecessor is (or was) resident — true for in-order claimed work.
+// words[b] = 1<<63 | value (value < 2^63); words zeroed before the kernel.
+__device__ __forceinline__ unsigned long long warp_prefix_aggregates(unsigned long long* words,
+                                                                     unsigned b,
+                                                                     unsigned long long agg) {
+    const int lane = threadIdx.x & 31;
+    constexpr unsigned long long kReady = 1ull << 63;
+    if (lane == 0) st_release_u64(&words[b], kReady | agg);
+    unsigned long long excl = 0;
+    for (unsigned j0 = 0; j0 < b; j0 += 32 * 16) {
+        unsigned long long w[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const unsigned j = j0 + i * 32 + lane;
+            w[i] = (j < b) ? ld_acquire_u64(&words[j]) : kReady;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const unsigned j = j0 + i * 32 + lane;
+            while (!(w[i] & kReady)) w[i] = ld_acquire_u64(&words[j]);
+            excl += w[i] & ~kReady;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) excl += __shfl_xor_sync(0xffffffffu, excl, o);
+    return excl;
+}
+
+// Decoupled look-back, executed by one full warp of block `b`: publishes the
+// block aggregate, sums predecessors 32 at a time until an inclusive prefix is
+// found, publishes its own inclusive prefix and returns the exclusive one.
+// flags[b]: 0 = nothing, 1 = aggregate in agg_arr[b], 2 = prefix in incl_arr[b].
+__device__ __forceinline__ unsigned long long warp_lookback(unsigned* flags,
+                                                            unsigned long long* agg_arr,
+                                                            unsigned long long* incl_arr,
+                                                            unsigned b, unsigned long long agg) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long excl = 0;
+    if (b == 0) {
+        if (lane == 0) {
+            incl_arr[0] = agg;
+            st_release_u32(&flags[0], 2u);
+        }
+        return 0;
+    }
+    if (lane == 0) {
+        agg_arr[b] = agg;
+        st_release_u32(&flags[b], 1u);
+    }
+    long j = (long)b - 1;
+    while (true) {
+        const long idx = j - lane;
+        unsigned f = 2u;
+        unsigned long long val = 0;
+        if (idx >= 0) {
+            do {
+                f = ld_acquire_u32(&flags[idx]);
+            } while (f == 0u);
+            val = (f == 2u) ? ld_relaxed_u64(&incl_arr[idx]) : ld_relaxed_u64(&agg_arr[idx]);
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, f == 2u);
+        const int first = pm ? __ffs(pm) - 1 : 31;
+        unsigned long long part = (lane <= first) ? val : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (pm) break;
+        j -= 32;
+    }
+    if (lane == 0) {
+        incl_arr[b] = excl + agg;
+        st_release_u32(&flags[b], 2u);
+    }
+    return excl;
+}
+
 // Pairs actually stored for the current slice (T capped by the buffer size).
 __device__ __forceinline__ unsigned stored_pairs(const Control* c, uint64_t cap) {
     const unsigned long long p = c->pairs;
@@ -124,34 +209,42 @@ struct PrepLaunch {
     uint64_t cap;             // plane stride
     uint32_t n;
     float* grads;             // zero-filled for non-survivors when non-null
-    SurvivorRecord* records;  // indexed by candidate id
-    uint32_t* survivor_list;  // slot -> candidate id
+    unsigned* filter_counts;  // candidates per K_filter block (plain stores)
+    uint32_t* cand_local;     // block-major candidate set indices: [b*kFilterBlock + pos]
+    unsigned nfilter;         // K_filter blocks
+    SurvivorRecord* records;  // indexed by candidate slot
+    uint32_t* survivor_list;  // survivor slot -> candidate slot
     uint32_t* keys;           // pre-sort tile keys
-    uint32_t* vals;           // pre-sort candidate ids
+    uint32_t* vals;           // pre-sort candidate slots
     uint64_t pair_cap;
-    unsigned* hist;           // kMaxSortPasses x 256 digit counts
+    unsigned* hist;           // kMaxSortPasses x 256 global digit counts
+    unsigned* tile_hist0;     // per sort tile (2048 pre-sort positions) x 256: digit-0 counts
+    unsigned* tile_hist_all;  // passes x sort tiles x 256 (zeroed by K_filter)
+    uint64_t sort_tiles_cap;
+    unsigned* prev_sort_tiles;  // persistent: sort tiles used by the previous prepare
     int passes;
-    unsigned* epoch;          // persistent sort epoch, bumped once per prepare
-    unsigned* prep_flags;     // per block, zeroed each prepare
-    unsigned long long* prep_agg;
-    unsigned long long* prep_incl;
+    unsigned long long* exact_words;  // per K_exact chunk: ready<<63 | S<<32 | P (zeroed per prepare)
     Control* ctrl;
     ErrorState* err;
     SliceArgs slice;
+    int exact_grid;           // persistent K_exact CTAs
 };
+
+constexpr int kFilterItems = 8;
+constexpr int kFilterBlock = kPrepThreads * kFilterItems;  // Gaussians per K_filter block
 
 struct SortLaunch {
     const uint32_t* keys_in;
     const uint32_t* vals_in;
     uint32_t* keys_out;
     uint32_t* vals_out;
-    const unsigned* hist;          // 256 counts of this pass
-    unsigned long long* status;    // per (tile, digit): epoch<<32 | flag<<30 | count
-    const unsigned* epoch;         // persistent sort epoch (device)
+    const unsigned* hist;          // 256 global counts of this pass's digit
+    const unsigned* tile_hist;     // per sort tile x 256 counts of this pass's digit
+    unsigned* tile_hist_next;      // next pass's per-tile counts (nullptr on the last pass)
+    unsigned* prev_sort_tiles;     // written by the last pass
     int shift;
     int pass;
-    const Control* ctrl_ro;
-    Control* ctrl;
+    const Control* ctrl;
     uint64_t pair_cap;
 };
 
@@ -212,7 +305,10 @@ struct LossLaunch {
     float w[11];         // normalized Gaussian taps
 };
 
-void launch_prep(const PrepLaunch& a, cudaStream_t st);
+void launch_filter(const PrepLaunch& a, cudaStream_t st);
+void launch_exact(const PrepLaunch& a, cudaStream_t st);
+int exact_blocks_per_sm(size_t dyn_smem);
+size_t exact_dyn_smem(unsigned nfilter);
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st);
 void launch_raster_fwd(const RasterLaunch& a, cudaStream_t st);
 void launch_raster_bwd(const RasterLaunch& a, cudaStream_t st);

@@ -1,22 +1,28 @@
-// prep.cu — K_prep (preprocess + cull + bounds + pair emission) and K_chain
-// (backward chain to world parameters). Built with --fmad=false so the fp64
-// focus algebra rounds like the reference (see focus.cuh).
+// prep.cu — per-slice preprocessing (prepare_gaussians, render.hpp:83-138, and
+// the TileGrid build, render.hpp:142-160) and the backward chain
+// (backward.hpp:148-185). Built with --fmad=false so the fp64 focus algebra
+// rounds like the reference (see focus.cuh).
 //
-// K_prep replaces prepare_gaussians (render.hpp:83-138) + the TileGrid build
-// (render.hpp:142-160) for one slice:
-//   1. one thread per Gaussian, coalesced SoA loads; an fp32 CERTAIN-CULL test
-//      in closed form (q = mu_cz^2 / (sigma_z^2 + Sigma_c,zz))
-//      with a safety margin that covers fp32 error and the reference's own
-//      cancellation noise; everything not certainly culled is a candidate.
-//      Dense gradients of certainly-culled primitives are zero-filled here
-//      (grad_chain.hpp:12-22 exact zeros) so the gradient plane is written once.
-//   2. order-preserving block compaction of candidates, then the exact fp64
-//      reference computation (focus_prepare) on the dense candidate list.
-//   3. a decoupled-lookback chained scan over blocks yields, in set order, the
-//      survivor slots and each survivor's first pair position; pairs
-//      (tile key, candidate id) are emitted in (id, tile) order — the order a
-//      stable sort on the tile key needs to reproduce the reference lists.
-//   4. per-block digit histograms for the radix passes.
+// Two kernels replace prepare_gaussians + TileGrid:
+//   K_filter  one thread per Gaussian (8 per thread), coalesced SoA loads, an
+//             fp32 CERTAIN-CULL test in closed form (q = mu_cz^2 /
+//             (sigma_z^2 + Sigma_c,zz)) with a margin
+//             covering fp32 error and the reference's own cancellation noise.
+//             Certainly-culled primitives get their dense gradient zero-filled
+//             here (the gradient plane is written exactly once per slice); the
+//             rest become candidates, compacted in set order inside the block
+//             and published with a plain per-block count — no cross-block
+//             waiting. This is the HBM-bound kernel (44 B read + 44 B written
+//             per Gaussian) and runs at full occupancy.
+//   K_exact   persistent CTAs take 256-candidate chunks in order (each CTA
+//             locates its candidates from the per-block counts), run the
+//             reference's fp64 computation (focus_prepare) densely, decide the
+//             exact cull, write 48 B survivor records and — through a wait-free
+//             ordered prefix over chunk aggregates — survivor slots and (tile,
+//             candidate) pairs in (candidate, tile) order: the order a stable
+//             sort on the tile key needs to reproduce the reference lists.
+//             Global and per-sort-tile digit histograms for the first radix
+//             pass are accumulated on the way.
 #include "common.cuh"
 #include "focus.cuh"
 
@@ -39,7 +45,6 @@ __device__ __forceinline__ bool certainly_culled(const float p[11], const SliceA
     if (!(smax < 5e2f * smin)) return false;  // (smax/smin)^2 < 2.5e5: far inside the 1e6 guard
     const float inv = rsqrtf(qn2);
     const float w = p[6] * inv, x = p[7] * inv, y = p[8] * inv, z = p[9] * inv;
-    // columns of R(q)
     const float r00 = 1.f - 2.f * (y * y + z * z), r01 = 2.f * (x * y - w * z), r02 = 2.f * (x * z + w * y);
     const float r10 = 2.f * (x * y + w * z), r11 = 1.f - 2.f * (x * x + z * z), r12 = 2.f * (y * z - w * x);
     const float r20 = 2.f * (x * z - w * y), r21 = 2.f * (y * z + w * x), r22 = 1.f - 2.f * (x * x + y * y);
@@ -75,52 +80,34 @@ __device__ __forceinline__ void zero_grads(float* grads, uint64_t cap, uint32_t 
     for (int k = 0; k < 11; ++k) grads[(uint64_t)k * cap + i] = 0.f;
 }
 
-// Block-wide inclusive scan of one 64-bit value per thread (256 threads).
-__device__ __forceinline__ unsigned long long block_incl_scan64(unsigned long long v,
-                                                                unsigned long long* s_warp) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-    }
-    if (lane == 31) s_warp[warp] = v;
-    __syncthreads();
-    unsigned long long add = 0;
-    for (int w = 0; w < warp; ++w) add += s_warp[w];
-    __syncthreads();
-    return v + add;
-}
-
+// ---- K_filter ------------------------------------------------------------------
 template <bool kZeroGrads>
-__global__ void __launch_bounds__(kPrepThreads) k_prep(const PrepLaunch a, float log_tau,
-                                                       int filter_on, unsigned nblocks) {
-    __shared__ unsigned s_bid;
-    __shared__ unsigned s_wcnt[kPrepItems * 8];
-    __shared__ unsigned s_ncand;
-    __shared__ uint32_t s_cand[kPrepBlock];
-    __shared__ unsigned long long s_incl[kPrepBlock];   // (survivors << 32) | pairs, inclusive
-    __shared__ uint16_t s_rect[kPrepBlock][3];           // tx0, ty0, ntx
-    __shared__ unsigned long long s_warp[8];
-    __shared__ unsigned long long s_prefix;
-    __shared__ unsigned s_hist[kMaxSortPasses][256];
+__global__ void __launch_bounds__(kPrepThreads) k_filter(const PrepLaunch a, float log_tau,
+                                                         int filter_on) {
+    constexpr int kSlots = kFilterItems * 8;  // (item, warp) counts, in set order
+    __shared__ unsigned s_off[kSlots];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        s_bid = atomicAdd(&a.ctrl->prep_block_ctr, 1u);
-        if (s_bid == 0) atomicAdd(a.epoch, 1u);  // new epoch for this prepare's sort passes
-    }
-    for (int k = tid; k < kMaxSortPasses * 256; k += kPrepThreads) (&s_hist[0][0])[k] = 0;
-    __syncthreads();
-    const unsigned b = s_bid;
-    const uint32_t base = b * kPrepBlock;
+    const unsigned b = blockIdx.x;
+    const uint32_t base = b * kFilterBlock;
     const float mod_f = (float)a.slice.mod;
     const float sz2 = (float)(a.slice.sigma_z * a.slice.sigma_z);
 
-    // ---- phase 1: certain-cull filter, zero-fill, candidate flags ----------
-    unsigned ballots[kPrepItems];
+    // Housekeeping: clear the per-sort-tile digit histograms the previous
+    // prepare used (all passes) before K_exact / the radix passes refill them.
+    {
+        const uint64_t row = a.sort_tiles_cap * 256;
+        const uint64_t used = (uint64_t)(*a.prev_sort_tiles) * 256;
+        const uint64_t total = (uint64_t)a.passes * used;
+        if (used)
+            for (uint64_t w = (uint64_t)b * kPrepThreads + tid; w < total;
+                 w += (uint64_t)gridDim.x * kPrepThreads)
+                a.tile_hist_all[(w / used) * row + (w % used)] = 0u;
+    }
+
+    unsigned ballots[kFilterItems];
 #pragma unroll
-    for (int k = 0; k < kPrepItems; ++k) {
+    for (int k = 0; k < kFilterItems; ++k) {
         const uint32_t i = base + k * kPrepThreads + tid;
         bool cand = false;
         if (i < a.n) {
@@ -133,185 +120,186 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(const PrepLaunch a, float
             if (kZeroGrads && !cand) zero_grads(a.grads, a.cap, i);
         }
         ballots[k] = __ballot_sync(0xffffffffu, cand);
-        if (lane == 0) s_wcnt[k * 8 + warp] = __popc(ballots[k]);
+        if (lane == 0) s_off[k * 8 + warp] = __popc(ballots[k]);
     }
     __syncthreads();
-    if (warp == 0) {
-        const unsigned v = s_wcnt[lane];
-        unsigned incl = v;
+    if (warp == 0) {  // exclusive scan of the 64 slots, two per lane
+        const unsigned c0 = s_off[2 * lane], c1 = s_off[2 * lane + 1];
+        unsigned incl = c0 + c1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += u;
         }
-        s_wcnt[lane] = incl - v;
-        if (lane == 31) s_ncand = incl;
+        const unsigned ex = incl - c0 - c1;
+        __syncwarp();
+        s_off[2 * lane] = ex;
+        s_off[2 * lane + 1] = ex + c0;
+        if (lane == 31) a.filter_counts[b] = incl;
     }
     __syncthreads();
+    uint32_t* out = a.cand_local + (uint64_t)b * kFilterBlock;
 #pragma unroll
-    for (int k = 0; k < kPrepItems; ++k) {
-        if (ballots[k] & (1u << lane)) {
-            const unsigned pos = s_wcnt[k * 8 + warp] + __popc(ballots[k] & lanemask_lt());
-            s_cand[pos] = base + k * kPrepThreads + tid;
-        }
+    for (int k = 0; k < kFilterItems; ++k) {
+        if (ballots[k] & (1u << lane))
+            out[s_off[k * 8 + warp] + __popc(ballots[k] & lanemask_lt())] = base + k * kPrepThreads + tid;
     }
-    __syncthreads();
-    const unsigned nc = s_ncand;
+}
 
-    // ---- phase 2: exact fp64 reference path on the dense candidate list ----
-    for (unsigned c = tid; c < nc; c += kPrepThreads) {
-        const uint32_t i = s_cand[c];
-        float pf[11];
-        load_params(a.params, a.cap, i, pf);
-        double pd[11];
-#pragma unroll
-        for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
-        Focus f;
-        const int r = focus_prepare(pd, a.slice, f);
-        unsigned long long v = 0;
-        if (r == kSurvive) {
-            const int tx0 = f.lo_x / kTile, tx1 = f.hi_x / kTile;
-            const int ty0 = f.lo_y / kTile, ty1 = f.hi_y / kTile;
-            const unsigned ntx = tx1 - tx0 + 1, nty = ty1 - ty0 + 1;
-            v = (1ull << 32) | (unsigned long long)(ntx * nty);
-            s_rect[c][0] = (uint16_t)tx0;
-            s_rect[c][1] = (uint16_t)ty0;
-            s_rect[c][2] = (uint16_t)ntx;
-            SurvivorRecord rec;
-            rec.mu2d_x = f.mu_e.x;
-            rec.mu2d_y = f.mu_e.y;
-            rec.conic_a = (float)f.con_a;
-            rec.conic_b = (float)f.con_b;
-            rec.conic_d = (float)f.con_d;
-            rec.alpha_tilde = (float)f.alpha_tilde;
-            rec.lo_x = (uint16_t)f.lo_x;
-            rec.hi_x = (uint16_t)f.hi_x;
-            rec.lo_y = (uint16_t)f.lo_y;
-            rec.hi_y = (uint16_t)f.hi_y;
-            rec.gidx = i;
-            rec.pair_base = 0;
-            a.records[base + c] = rec;
-        } else {
-            if (r > 0) record_error(a.err, r, i);
-            if (kZeroGrads) zero_grads(a.grads, a.cap, i);
-        }
-        s_incl[c] = v;
-    }
-    __syncthreads();
+// ---- K_exact -------------------------------------------------------------------
+template <bool kZeroGrads>
+__global__ void __launch_bounds__(kExactChunk) k_exact(const PrepLaunch a) {
+    extern __shared__ unsigned s_bpre[];                 // exclusive prefix of filter counts (nfilter+1)
+    __shared__ unsigned s_chunk;
+    __shared__ unsigned long long s_incl[kExactChunk];   // (survivors << 32) | pairs, inclusive
+    __shared__ uint16_t s_rect[kExactChunk][3];          // tx0, ty0, ntx
+    __shared__ unsigned long long s_warp[kExactChunk / 32];
+    __shared__ unsigned long long s_excl;
+    __shared__ unsigned s_hist[kMaxSortPasses][256];
 
-    // ---- phase 3: block scan of (survivor, pairs) over candidates ----------
-    // Each thread owns 4 consecutive candidates.
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int k = tid; k < kMaxSortPasses * 256; k += kExactChunk) (&s_hist[0][0])[k] = 0;
+    // candidate layout: exclusive prefix over the K_filter blocks' counts
     {
-        unsigned long long loc[kPrepItems];
-        unsigned long long run = 0;
+        const unsigned nb = a.nfilter;
+        unsigned carry = 0;
+        for (unsigned base = 0; base < nb; base += kExactChunk) {
+            const unsigned j = base + tid;
+            const unsigned v = j < nb ? a.filter_counts[j] : 0u;
+            unsigned incl = v;
 #pragma unroll
-        for (int k = 0; k < kPrepItems; ++k) {
-            const unsigned c = tid * kPrepItems + k;
-            run += (c < nc) ? s_incl[c] : 0ull;
-            loc[k] = run;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            if (lane == 31) s_warp[warp] = incl;
+            __syncthreads();
+            unsigned add = carry;
+            for (int w = 0; w < warp; ++w) add += (unsigned)s_warp[w];
+            if (j < nb) s_bpre[j] = add + incl - v;
+            unsigned tot = 0;
+            for (int w = 0; w < kExactChunk / 32; ++w) tot += (unsigned)s_warp[w];
+            carry += tot;
+            __syncthreads();
         }
-        const unsigned long long incl = block_incl_scan64(run, s_warp);
-        const unsigned long long excl = incl - run;
-#pragma unroll
-        for (int k = 0; k < kPrepItems; ++k) {
-            const unsigned c = tid * kPrepItems + k;
-            if (c < nc) s_incl[c] = excl + loc[k];
-        }
+        if (tid == 0) s_bpre[nb] = carry;
+        __syncthreads();
     }
-    __syncthreads();
-    const unsigned long long agg = nc ? s_incl[nc - 1] : 0ull;
-
-    // ---- phase 4: decoupled look-back across blocks --------------------------
-    if (warp == 0) {
-        unsigned long long excl = 0;
-        if (b == 0) {
-            if (lane == 0) {
-                a.prep_incl[0] = agg;
-                st_release_u32(&a.prep_flags[0], 2u);
-            }
-        } else {
-            if (lane == 0) {
-                a.prep_agg[b] = agg;
-                st_release_u32(&a.prep_flags[b], 1u);
-            }
-            int j = (int)b - 1;
-            while (true) {
-                const int idx = j - lane;
-                unsigned f = 2u;
-                unsigned long long val = 0;
-                if (idx >= 0) {
-                    do {
-                        f = ld_acquire_u32(&a.prep_flags[idx]);
-                    } while (f == 0u);
-                    val = (f == 2u) ? ld_relaxed_u64(&a.prep_incl[idx])
-                                    : ld_relaxed_u64(&a.prep_agg[idx]);
-                }
-                const unsigned pm = __ballot_sync(0xffffffffu, f == 2u);
-                if (pm) {
-                    const int first = __ffs(pm) - 1;
-                    unsigned long long part = (lane <= first) ? val : 0ull;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-                    excl += part;
-                    break;
-                }
-                unsigned long long part = val;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-                excl += part;
-                j -= 32;
-            }
-            if (lane == 0) {
-                a.prep_incl[b] = excl + agg;
-                st_release_u32(&a.prep_flags[b], 2u);
-            }
-        }
-        if (lane == 0) {
-            s_prefix = excl;
-            if (b == nblocks - 1) {
-                const unsigned long long tot = excl + agg;
-                const unsigned S = (unsigned)(tot >> 32), P = (unsigned)(tot & 0xffffffffull);
-                a.ctrl->survivors = S;
-                a.ctrl->pairs = P;
-                a.ctrl->pair_overflow = (P > a.pair_cap) ? 1u : 0u;
-            }
-        }
-    }
-    __syncthreads();
-    const unsigned S0 = (unsigned)(s_prefix >> 32);
-    const unsigned P0 = (unsigned)(s_prefix & 0xffffffffull);
-
-    // ---- phase 5: survivor slots, pair bases, cooperative pair emission -----
-    for (unsigned c = tid; c < nc; c += kPrepThreads) {
-        const unsigned long long inc = s_incl[c];
-        const unsigned long long prev = c ? s_incl[c - 1] : 0ull;
-        if ((inc >> 32) != (prev >> 32)) {
-            const unsigned slot = S0 + (unsigned)(prev >> 32);
-            a.survivor_list[slot] = base + c;
-            a.records[base + c].pair_base = P0 + (unsigned)(prev & 0xffffffffull);
-        }
-    }
-    const unsigned Pb = (unsigned)(agg & 0xffffffffull);
+    const unsigned C = s_bpre[a.nfilter];
+    const unsigned nchunks = (C + kExactChunk - 1) / kExactChunk;
     const int tiles_x = a.slice.tiles_x;
-    for (unsigned k = tid; k < Pb; k += kPrepThreads) {
-        // candidate c = first with inclusive pair count > k
-        unsigned lo = 0, hi = nc - 1;
-        while (lo < hi) {
-            const unsigned mid = (lo + hi) >> 1;
-            if ((unsigned)(s_incl[mid] & 0xffffffffull) > k) hi = mid; else lo = mid + 1;
+
+    while (true) {
+        __syncthreads();
+        if (tid == 0) s_chunk = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
+        __syncthreads();
+        const unsigned chunk = s_chunk;
+        if (chunk >= nchunks) break;
+        const unsigned c = chunk * kExactChunk + tid;
+        unsigned long long v = 0;
+        if (c < C) {
+            // filter block holding candidate c: last b with s_bpre[b] <= c
+            unsigned lo = 0, hi = a.nfilter - 1;
+            while (lo < hi) {
+                const unsigned mid = (lo + hi + 1) >> 1;
+                if (s_bpre[mid] <= c) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t i = a.cand_local[(uint64_t)lo * kFilterBlock + (c - s_bpre[lo])];
+            float pf[11];
+            load_params(a.params, a.cap, i, pf);
+            double pd[11];
+#pragma unroll
+            for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
+            Focus f;
+            const int r = focus_prepare(pd, a.slice, f);
+            if (r == kSurvive) {
+                const int tx0 = f.lo_x / kTile, tx1 = f.hi_x / kTile;
+                const int ty0 = f.lo_y / kTile, ty1 = f.hi_y / kTile;
+                const unsigned ntx = tx1 - tx0 + 1, nty = ty1 - ty0 + 1;
+                v = (1ull << 32) | (unsigned long long)(ntx * nty);
+                s_rect[tid][0] = (uint16_t)tx0;
+                s_rect[tid][1] = (uint16_t)ty0;
+                s_rect[tid][2] = (uint16_t)ntx;
+                SurvivorRecord rec;
+                rec.mu2d_x = f.mu_e.x;
+                rec.mu2d_y = f.mu_e.y;
+                rec.conic_a = (float)f.con_a;
+                rec.conic_b = (float)f.con_b;
+                rec.conic_d = (float)f.con_d;
+                rec.alpha_tilde = (float)f.alpha_tilde;
+                rec.lo_x = (uint16_t)f.lo_x;
+                rec.hi_x = (uint16_t)f.hi_x;
+                rec.lo_y = (uint16_t)f.lo_y;
+                rec.hi_y = (uint16_t)f.hi_y;
+                rec.gidx = i;
+                rec.pair_base = 0;
+                a.records[c] = rec;
+            } else {
+                if (r > 0) record_error(a.err, r, i);
+                if (kZeroGrads) zero_grads(a.grads, a.cap, i);
+            }
         }
-        const unsigned c = lo;
-        const unsigned before = c ? (unsigned)(s_incl[c - 1] & 0xffffffffull) : 0u;
-        const unsigned local = k - before;
-        const unsigned ntx = s_rect[c][2];
-        const unsigned ty = s_rect[c][1] + local / ntx;
-        const unsigned tx = s_rect[c][0] + local % ntx;
-        const unsigned tile = ty * (unsigned)tiles_x + tx;
-        const unsigned long long pos = (unsigned long long)P0 + k;
-        if (pos < a.pair_cap) {
-            a.keys[pos] = tile;
-            a.vals[pos] = base + c;
-            for (int ps = 0; ps < a.passes; ++ps) atomicAdd(&s_hist[ps][(tile >> (8 * ps)) & 255u], 1u);
+        // block inclusive scan of (survivor, pairs)
+        unsigned long long incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        unsigned long long add = 0;
+        for (int w = 0; w < warp; ++w) add += s_warp[w];
+        incl += add;
+        s_incl[tid] = incl;
+        __syncthreads();
+        const unsigned long long agg = s_incl[kExactChunk - 1];
+        if (warp == 0) {
+            const unsigned long long excl = warp_prefix_aggregates(a.exact_words, chunk, agg);
+            if (lane == 0) {
+                s_excl = excl;
+                if (chunk == nchunks - 1) {
+                    const unsigned long long tot = excl + agg;
+                    const unsigned S = (unsigned)(tot >> 32), P = (unsigned)(tot & 0xffffffffull);
+                    a.ctrl->survivors = S;
+                    a.ctrl->pairs = P;
+                    a.ctrl->pair_overflow = (P > a.pair_cap) ? 1u : 0u;
+                }
+            }
+        }
+        __syncthreads();
+        const unsigned S0 = (unsigned)(s_excl >> 32);
+        const unsigned P0 = (unsigned)(s_excl & 0xffffffffull);
+        {
+            const unsigned long long prev = tid ? s_incl[tid - 1] : 0ull;
+            if ((s_incl[tid] >> 32) != (prev >> 32)) {
+                a.survivor_list[S0 + (unsigned)(prev >> 32)] = c;
+                a.records[c].pair_base = P0 + (unsigned)(prev & 0xffffffffull);
+            }
+        }
+        // cooperative, balanced pair emission in (candidate, tile) order
+        const unsigned Pb = (unsigned)(agg & 0xffffffffull);
+        for (unsigned k = tid; k < Pb; k += kExactChunk) {
+            unsigned lo = 0, hi = kExactChunk - 1;
+            while (lo < hi) {
+                const unsigned mid = (lo + hi) >> 1;
+                if ((unsigned)(s_incl[mid] & 0xffffffffull) > k) hi = mid; else lo = mid + 1;
+            }
+            const unsigned before = lo ? (unsigned)(s_incl[lo - 1] & 0xffffffffull) : 0u;
+            const unsigned local = k - before;
+            const unsigned ntx = s_rect[lo][2];
+            const unsigned ty = s_rect[lo][1] + local / ntx;
+            const unsigned tx = s_rect[lo][0] + local % ntx;
+            const unsigned tile = ty * (unsigned)tiles_x + tx;
+            const unsigned long long pos = (unsigned long long)P0 + k;
+            if (pos < a.pair_cap) {
+                a.keys[pos] = tile;
+                a.vals[pos] = chunk * kExactChunk + lo;
+                if (a.passes > 0)
+                    atomicAdd(&a.tile_hist0[(pos / kSortTile) * 256 + (tile & 255u)], 1u);
+                for (int ps = 0; ps < a.passes; ++ps)
+                    atomicAdd(&s_hist[ps][(tile >> (8 * ps)) & 255u], 1u);
+            }
         }
     }
     __syncthreads();
@@ -335,7 +323,7 @@ __global__ void __launch_bounds__(128) k_chain(const ChainLaunch a) {
 #pragma unroll
         for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
         Focus f;
-        focus_prepare(pd, a.slice, f);  // deterministic: same state as K_prep
+        focus_prepare(pd, a.slice, f);  // deterministic: same state as K_exact
         const unsigned ntx = rec.hi_x / kTile - rec.lo_x / kTile + 1;
         const unsigned nty = rec.hi_y / kTile - rec.lo_y / kTile + 1;
         const unsigned np = ntx * nty;
@@ -366,16 +354,36 @@ __global__ void __launch_bounds__(128) k_chain(const ChainLaunch a) {
 
 }  // namespace
 
-void launch_prep(const PrepLaunch& a, cudaStream_t st) {
+int exact_blocks_per_sm(size_t dyn_smem) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_exact<true>, kExactChunk, dyn_smem);
+    return nb > 0 ? nb : 1;
+}
+
+size_t exact_dyn_smem(unsigned nfilter) { return (size_t)(nfilter + 1) * sizeof(unsigned); }
+
+void launch_filter(const PrepLaunch& a, cudaStream_t st) {
     if (a.n == 0) return;
-    const unsigned nblocks = (a.n + kPrepBlock - 1) / kPrepBlock;
     const bool filter_on = a.slice.tau > 0.0 && a.slice.mod > 1e-10 && a.slice.mod < 1e10 &&
                            a.slice.sigma_z > 1e-10 && a.slice.sigma_z < 1e10;
     const float log_tau = filter_on ? (float)log(a.slice.tau) : 0.f;
     if (a.grads)
-        k_prep<true><<<nblocks, kPrepThreads, 0, st>>>(a, log_tau, filter_on ? 1 : 0, nblocks);
+        k_filter<true><<<a.nfilter, kPrepThreads, 0, st>>>(a, log_tau, filter_on ? 1 : 0);
     else
-        k_prep<false><<<nblocks, kPrepThreads, 0, st>>>(a, log_tau, filter_on ? 1 : 0, nblocks);
+        k_filter<false><<<a.nfilter, kPrepThreads, 0, st>>>(a, log_tau, filter_on ? 1 : 0);
+}
+
+void launch_exact(const PrepLaunch& a, cudaStream_t st) {
+    if (a.n == 0) return;
+    const size_t smem = exact_dyn_smem(a.nfilter);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    if (a.grads)
+        k_exact<true><<<a.exact_grid, kExactChunk, smem, st>>>(a);
+    else
+        k_exact<false><<<a.exact_grid, kExactChunk, smem, st>>>(a);
 }
 
 void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st) {

@@ -92,11 +92,14 @@ struct gpk_session {
     uint64_t n = 0, cap = 0;
     gpk_bounds bbox{};
     uint64_t pair_cap = 0;
+    uint64_t sort_tiles_cap = 0;
 
     DevBuf params, grads, adam_m, adam_v, records, survivors;
-    DevBuf keys[2], vals[2], partials, sort_status;
+    DevBuf keys[2], vals[2], partials, sort_status;  // sort_status: per-sort-tile digit counts
     DevBuf head;       // Control | hist | prep flags (memset per prepare)
-    DevBuf prep_vals;  // agg + incl per K_prep block
+    DevBuf prep_vals;  // per K_filter block candidate counts
+    DevBuf cand_list;  // block-major candidate set indices
+    int num_sms = 148;
     DevBuf persist;    // ErrorState | epoch | adam step | adam done ctr | loss done ctr | loss
     DevBuf image, dl_di, target, loss_g, loss_partial;
     DevBuf stat_norm, stat_obs, stat_world;
@@ -124,7 +127,8 @@ struct gpk_session {
     double* loss() { return reinterpret_cast<double*>(persist.as<char>() + 88); }
     Control* ctrl() { return head.as<Control>(); }
     unsigned* hist() { return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control)); }
-    unsigned* prep_flags() {
+    unsigned* prev_sort_tiles() { return reinterpret_cast<unsigned*>(persist.as<char>() + 96); }
+    unsigned* filter_flags() {
         return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control) +
                                            kMaxSortPasses * 256 * sizeof(unsigned));
     }
@@ -188,7 +192,14 @@ int set_device(gpk_session* s) {
     return GPK_OK;
 }
 
-uint64_t prep_blocks(uint64_t n) { return (n + kPrepBlock - 1) / kPrepBlock; }
+uint64_t filter_blocks(uint64_t n) { return std::max<uint64_t>((n + kFilterBlock - 1) / kFilterBlock, 1); }
+uint64_t exact_chunks(uint64_t n) { return std::max<uint64_t>((n + kExactChunk - 1) / kExactChunk, 1); }
+// head = Control | digit histograms | K_filter flags | K_exact flags (memset per prepare)
+// head = Control | global digit histograms | K_exact chunk words (u64)
+size_t head_size(uint64_t nbf, uint64_t nbe) {
+    (void)nbf;
+    return sizeof(Control) + kMaxSortPasses * 256 * sizeof(unsigned) + nbe * 8;
+}
 
 int clear_errors(gpk_session* s) {
     ErrorState e;
@@ -242,11 +253,15 @@ int ensure_pairs(gpk_session* s, uint64_t need) {
         CK(s->vals[b].ensure(cap * 4));
     }
     CK(s->partials.ensure(cap * 24));
+    // per-sort-tile digit counts of every pass (kept zero between prepares:
+    // K_filter clears the rows the previous prepare used)
     const uint64_t st_tiles = (cap + kSortTile - 1) / kSortTile;
-    const size_t st_bytes = (size_t)kMaxSortPasses * st_tiles * 256 * 8;
+    const size_t st_bytes = (size_t)kMaxSortPasses * st_tiles * 256 * 4;
     CK(s->sort_status.ensure(st_bytes));
-    CK(cudaMemsetAsync(s->sort_status.p, 0, st_bytes, s->stream));
+    CK(cudaMemsetAsync(s->sort_status.p, 0, s->sort_status.bytes, s->stream));
+    CK(cudaMemsetAsync(s->prev_sort_tiles(), 0, 4, s->stream));
     s->pair_cap = cap;
+    s->sort_tiles_cap = st_tiles;
     return GPK_OK;
 }
 
@@ -327,9 +342,8 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     ps.valid = true;
     ps.rasterized = false;
     ps.grads_zeroed = zero_grads;
-    const uint64_t nb = prep_blocks(s->n);
-    const size_t head_bytes = sizeof(Control) + kMaxSortPasses * 256 * sizeof(unsigned) +
-                              std::max<uint64_t>(nb, 1) * sizeof(unsigned);
+    const uint64_t nbf = filter_blocks(s->n), nbe = exact_chunks(s->n);
+    const size_t head_bytes = head_size(nbf, nbe);
     StageScope scope_prep(s, GPK_STAGE_PREPARE);
     CK(cudaMemsetAsync(s->head.p, 0, head_bytes, s->stream));
     if (s->n == 0) {
@@ -341,27 +355,38 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     pl.cap = s->cap;
     pl.n = (uint32_t)s->n;
     pl.grads = zero_grads ? s->grads.as<float>() : nullptr;
+    pl.filter_counts = s->prep_vals.as<unsigned>();
+    pl.cand_local = s->cand_list.as<uint32_t>();
+    pl.nfilter = (unsigned)nbf;
     pl.records = s->records.as<SurvivorRecord>();
     pl.survivor_list = s->survivors.as<uint32_t>();
     pl.keys = s->keys[0].as<uint32_t>();
     pl.vals = s->vals[0].as<uint32_t>();
     pl.pair_cap = s->pair_cap;
     pl.hist = s->hist();
+    pl.tile_hist0 = s->sort_status.as<unsigned>();
+    pl.tile_hist_all = s->sort_status.as<unsigned>();
+    pl.sort_tiles_cap = s->sort_tiles_cap;
+    pl.prev_sort_tiles = s->prev_sort_tiles();
     pl.passes = ps.passes;
-    pl.epoch = s->epoch();
-    pl.prep_flags = s->prep_flags();
-    pl.prep_agg = s->prep_vals.as<unsigned long long>();
-    pl.prep_incl = s->prep_vals.as<unsigned long long>() + nb;
+    pl.exact_words = reinterpret_cast<unsigned long long*>(s->filter_flags());
     pl.ctrl = s->ctrl();
     pl.err = s->err();
     pl.slice = a;
-    launch_prep(pl, s->stream);
+    const int exact_per_sm = exact_blocks_per_sm(exact_dyn_smem((unsigned)nbf));
+    pl.exact_grid = (int)std::min<uint64_t>(nbe, (uint64_t)s->num_sms * exact_per_sm);
+    launch_filter(pl, s->stream);
     CK(cudaGetLastError());
     scope_prep.end();
+    {
+        StageScope scope_exact(s, GPK_STAGE_EXACT);
+        launch_exact(pl, s->stream);
+        CK(cudaGetLastError());
+    }
     StageScope scope_sort(s, GPK_STAGE_SORT);
 
-    const int grid = (int)std::min<uint64_t>((s->pair_cap + kSortTile - 1) / kSortTile, 148 * 4);
-    const uint64_t st_tiles = (s->pair_cap + kSortTile - 1) / kSortTile;
+    const int grid = (int)std::min<uint64_t>(s->sort_tiles_cap, (uint64_t)s->num_sms * 2);
+    const uint64_t st_tiles = s->sort_tiles_cap;
     for (int p = 0; p < ps.passes; ++p) {
         SortLaunch sl;
         sl.keys_in = s->keys[p & 1].as<uint32_t>();
@@ -369,11 +394,13 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
         sl.keys_out = s->keys[(p + 1) & 1].as<uint32_t>();
         sl.vals_out = s->vals[(p + 1) & 1].as<uint32_t>();
         sl.hist = s->hist() + 256 * p;
-        sl.status = s->sort_status.as<unsigned long long>() + (size_t)p * st_tiles * 256;
-        sl.epoch = s->epoch();
+        sl.tile_hist = s->sort_status.as<unsigned>() + (size_t)p * st_tiles * 256;
+        sl.tile_hist_next = (p + 1 < ps.passes)
+                                ? s->sort_status.as<unsigned>() + (size_t)(p + 1) * st_tiles * 256
+                                : nullptr;
+        sl.prev_sort_tiles = s->prev_sort_tiles();
         sl.shift = 8 * p;
         sl.pass = p;
-        sl.ctrl_ro = s->ctrl();
         sl.ctrl = s->ctrl();
         sl.pair_cap = s->pair_cap;
         launch_sort_pass(sl, grid, s->stream);
@@ -444,7 +471,7 @@ int run_backward(gpk_session* s, bool stats) {
     c.stat_world = stats ? s->stat_world.as<float>() : nullptr;
     c.err = s->err();
     c.slice = s->prep.slice;
-    const int grid = (int)std::min<uint64_t>((s->n + 127) / 128, 148 * 8);
+    const int grid = (int)std::min<uint64_t>((s->n + 127) / 128, (uint64_t)s->num_sms * 8);
     launch_chain(c, grid, s->stream);
     CK(cudaGetLastError());
     return GPK_OK;
@@ -500,11 +527,13 @@ int alloc_for_n(gpk_session* s, uint64_t n) {
         CK(s->grads.ensure(cap * 11 * 4));
         CK(s->adam_m.ensure(cap * 11 * 4));
         CK(s->adam_v.ensure(cap * 11 * 4));
-        const uint64_t nb = prep_blocks(cap);
-        CK(s->records.ensure(nb * kPrepBlock * sizeof(SurvivorRecord)));
+        const uint64_t nbf = filter_blocks(cap), nbe = exact_chunks(cap);
+        CK(s->records.ensure(cap * sizeof(SurvivorRecord)));
+        CK(s->cand_list.ensure(cap * 4));
         CK(s->survivors.ensure(cap * 4));
-        CK(s->prep_vals.ensure(std::max<uint64_t>(nb, 1) * 16));
-        CK(s->head.ensure(sizeof(Control) + kMaxSortPasses * 256 * 4 + std::max<uint64_t>(nb, 1) * 4));
+        CK(s->prep_vals.ensure(nbf * 4));
+        CK(s->cand_list.ensure(nbf * kFilterBlock * 4));
+        CK(s->head.ensure(head_size(nbf, nbe)));
         s->cap = cap;
     }
     s->n = n;
@@ -625,6 +654,8 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
         }
         s->own_stream = true;
     }
+    cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (s->num_sms < 1) s->num_sms = 148;
     e = s->persist.ensure(kPersistBytes);
     if (e == cudaSuccess) e = cudaMemsetAsync(s->persist.p, 0, kPersistBytes, s->stream);
     if (e == cudaSuccess) {
@@ -653,7 +684,7 @@ int gpk_session_destroy(gpk_session* s) {
                       &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials,
                       &s->sort_status, &s->head, &s->prep_vals, &s->persist, &s->image,
                       &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm,
-                      &s->stat_obs, &s->stat_world};
+                      &s->stat_obs, &s->stat_world, &s->cand_list};
     for (DevBuf* b : bufs) b->release();
     drain_timing(s);
     for (cudaEvent_t e : s->event_pool) cudaEventDestroy(e);

@@ -1,41 +1,35 @@
-// sort.cu — hand-written stable LSD radix sort of (tile key, candidate id)
-// pairs, one onesweep pass per 8-bit digit.
+// sort.cu — hand-written stable LSD radix sort of (tile key, candidate slot)
+// pairs, one kernel per 8-bit digit.
 //
-// Stability is the whole point: pairs arrive in ascending candidate id (= set
-// order), so a stable sort by tile reproduces the reference's per-tile lists
-// in ascending prepared index (render.hpp:151-157) bit-exactly.
+// Stability is the whole point: pairs arrive in ascending candidate slot
+// (= set order), so a stable sort by tile reproduces the reference's per-tile
+// lists in ascending prepared index (render.hpp:151-157) bit-exactly.
 //
-// Per pass, one persistent grid claims 2048-key tiles in order. Inside a tile,
-// warp w owns a contiguous 256-key segment processed in 8 rounds of 32; ranks
-// within a round come from __match_any_sync, so the block-local order is the
-// input order. Tile-to-tile offsets per digit come from a decoupled look-back
-// on 64-bit status words tagged with a device-side epoch (no per-pass memset,
-// graph-replay safe). Global digit offsets come from the histograms K_prep
-// accumulated while emitting the pairs.
+// Wait-free passes: the producer of a pass's input (K_exact for pass 0, pass p
+// for pass p+1) also counts, per 2048-key sort tile, how many keys carry each
+// digit value. A sort CTA therefore knows its output offsets up front —
+// global digit base (exclusive scan of the global histogram) + the column sum
+// of the per-tile histograms of all earlier tiles (coalesced L2 reads) — and
+// never waits on another CTA. Inside a tile, warp w owns a contiguous 256-key
+// segment processed in 8 rounds of 32; ranks within a round come from
+// __match_any_sync, so the tile-local order is the input order.
 #include "common.cuh"
 
 namespace gpk {
 
 namespace {
 
-constexpr unsigned long long kFlagAgg = 1ull << 30;
-constexpr unsigned long long kFlagPrefix = 2ull << 30;
-constexpr unsigned long long kCountMask = (1ull << 30) - 1;
-
 __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) {
     __shared__ unsigned s_whist[8][256];
-    __shared__ unsigned s_digit_base[256];
-    __shared__ unsigned s_tile_excl[256];
+    __shared__ unsigned s_part[8][256];
+    __shared__ unsigned s_dbase[256];
     __shared__ unsigned s_wsum[8];
-    __shared__ unsigned s_tile;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned P = stored_pairs(a.ctrl_ro, a.pair_cap);
+    const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
     const unsigned ntiles = (P + kSortTile - 1) / kSortTile;
-    const unsigned epoch = (*a.epoch) * 4u + (unsigned)a.pass;
-    const unsigned long long etag = (unsigned long long)epoch << 32;
 
-    // exclusive scan of this pass's global digit histogram
+    // global digit base: exclusive scan of this pass's histogram
     {
         const unsigned v = a.hist[tid];
         unsigned incl = v;
@@ -48,17 +42,27 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
         __syncthreads();
         unsigned add = 0;
         for (int w = 0; w < warp; ++w) add += s_wsum[w];
-        s_digit_base[tid] = incl - v + add;
+        s_dbase[tid] = incl - v + add;
     }
+    if (blockIdx.x == 0 && tid == 0 && !a.tile_hist_next) *a.prev_sort_tiles = ntiles;
 
-    while (true) {
-        __syncthreads();
-        if (tid == 0) s_tile = atomicAdd(&a.ctrl->sort_tile_ctr[a.pass], 1u);
+    for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        // ---- offsets of earlier tiles: warp w sums rows j = w, w+8, ... < t
+        {
+            unsigned acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const uint4* rows = reinterpret_cast<const uint4*>(a.tile_hist);
+            for (unsigned j = warp; j < t; j += 8) {
+                const uint4 x = rows[(size_t)j * 64 + lane * 2];
+                const uint4 y = rows[(size_t)j * 64 + lane * 2 + 1];
+                acc[0] += x.x; acc[1] += x.y; acc[2] += x.z; acc[3] += x.w;
+                acc[4] += y.x; acc[5] += y.y; acc[6] += y.z; acc[7] += y.w;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s_part[warp][lane * 8 + i] = acc[i];
+        }
 #pragma unroll
         for (int w = 0; w < 8; ++w) s_whist[w][tid] = 0;
         __syncthreads();
-        const unsigned t = s_tile;
-        if (t >= ntiles) break;
 
         // ---- rank: warp-local stable ranks via match_any -----------------
         uint32_t key[kSortItems], val[kSortItems];
@@ -81,47 +85,34 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
         }
         __syncthreads();
 
-        // ---- per digit: exclusive prefix over warps, tile count ------------
-        unsigned count = 0;
+        // ---- per digit: base = global digit base + earlier tiles; warp prefixes
+        {
+            unsigned base = s_dbase[tid];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const unsigned c = s_whist[w][tid];
-            s_whist[w][tid] = count;
-            count += c;
-        }
-
-        // ---- decoupled look-back for digit `tid` ---------------------------
-        unsigned long long* st = a.status + (unsigned long long)t * 256 + tid;
-        unsigned excl = 0;
-        if (t == 0) {
-            st_release_u64(st, etag | kFlagPrefix | count);
-        } else {
-            st_release_u64(st, etag | kFlagAgg | count);
-            long j = (long)t - 1;
-            while (j >= 0) {
-                const unsigned long long w =
-                    ld_acquire_u64(a.status + (unsigned long long)j * 256 + tid);
-                if ((w & 0xffffffff00000000ull) != etag || (w & (3ull << 30)) == 0) continue;
-                excl += (unsigned)(w & kCountMask);
-                if (w & kFlagPrefix) break;
-                --j;
+            for (int w = 0; w < 8; ++w) base += s_part[w][tid];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const unsigned c = s_whist[w][tid];
+                s_whist[w][tid] = base;
+                base += c;
             }
-            st_release_u64(st, etag | kFlagPrefix | (excl + count));
         }
-        s_tile_excl[tid] = excl;
         __syncthreads();
 
-        // ---- scatter -------------------------------------------------------
+        // ---- scatter (+ next pass's per-tile digit counts) ------------------
 #pragma unroll
         for (int r = 0; r < kSortItems; ++r) {
             const unsigned idx = seg + r * 32 + lane;
             if (idx < P) {
                 const unsigned d = (key[r] >> a.shift) & 255u;
-                const unsigned pos = s_digit_base[d] + s_tile_excl[d] + s_whist[warp][d] + rank[r];
+                const unsigned pos = s_whist[warp][d] + rank[r];
                 a.keys_out[pos] = key[r];
                 a.vals_out[pos] = val[r];
+                if (a.tile_hist_next)
+                    atomicAdd(&a.tile_hist_next[(pos / kSortTile) * 256 + ((key[r] >> (a.shift + 8)) & 255u)], 1u);
             }
         }
+        __syncthreads();
     }
 }
 

@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-graphs", dest="graphs", action="store_false",
+                    help="submit the step kernel by kernel instead of as a CUDA graph")
     return ap.parse_args()
 
 
@@ -308,7 +310,7 @@ def run_ours(args):
     # L2 flush by READING 256 MiB (> 126 MB L2): evicts the step's working set
     # without leaving dirty lines whose write-back would bill the next kernel.
     flush_src = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
-    flush_dst = torch.empty(1, dtype=torch.float32, device="cuda")
+    flush_dst = torch.empty((), dtype=torch.float32, device="cuda")
 
     class _Flush:
         @staticmethod
@@ -317,8 +319,15 @@ def run_ours(args):
 
     flush = _Flush()
 
-    def step(i):
-        sess.fwd_bwd_slice(poses[(rank + i * world) % len(poses)], psf, rcfg)
+    # one CUDA graph per slice pose: the whole U1 step is one submission
+    graphs = [sess.capture_fwd_bwd(p, psf, rcfg) for p in poses] if args.graphs else None
+
+    def step(i, use_graph=True):
+        k = (rank + i * world) % len(poses)
+        if graphs is not None and use_graph:
+            sess.graph_launch(graphs[k])
+        else:
+            sess.fwd_bwd_slice(poses[k], psf, rcfg)
         if world > 1:
             N.check(N.lib.gpk_allreduce_grads(sess.handle))
 
@@ -328,8 +337,6 @@ def run_ours(args):
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    sess.stage_times(reset=True)
-    sess.stage_timing(True)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -340,11 +347,20 @@ def run_ours(args):
             step(args.warmup + i)
             ends[i].record(stream)
         torch.cuda.synchronize()
-    sess.stage_timing(False)
     sess.synchronize()
     if dist:
         dist.barrier()
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+
+    # per-kernel device time: the same steps with event pairs around every
+    # stage launch (non-graph submission; events bracket each kernel directly)
+    prof_steps = min(args.steps, 100)
+    sess.stage_times(reset=True)
+    sess.stage_timing(True)
+    for i in range(prof_steps):
+        flush.fill_(float(i))
+        step(args.warmup + i, use_graph=False)
+    sess.stage_timing(False)
     stages = sess.stage_times(reset=True)
     t = torch.tensor([total_ms], device="cuda")
     if dist:
@@ -381,20 +397,32 @@ def run_ours(args):
     assert np.isfinite(pin_grads.numpy()[:1000]).all()
 
     # ---- roofline of the dominant kernel -------------------------------------------
-    dom = max((k for k in stages if stages[k][1] > 0), key=lambda k: stages[k][0])
+    # Algorithmic bytes per launch (each logical tensor read/written once at its
+    # stored width): N Gaussians, S survivors, T pairs, P px.
+    S, T = S_mean, T_mean
+    kernel_bytes = {
+        "prepare": ("k_filter", 44 * n + 44 * (n - S),
+                    "44N params read + 44(N-S) gradient zero-fill"),
+        "exact": ("k_exact", 44 * S + 48 * S + 8 * T, "44S params + 48S records + 8T pairs"),
+        "sort": ("k_sort_pass x passes", 16 * T * max(1, sort_passes(X, Y)), "16T per radix pass"),
+        "raster": ("k_raster_fwd", 32 * T + 4 * P, "32T + 4P (SURVEY.md §8d)"),
+        "backward": ("k_raster_bwd", 4 * P + 32 * T + 24 * S, "4P + 32T + 24S (SURVEY.md §8d)"),
+        "chain": ("k_chain", 44 * S + 48 * S + 24 * T + 44 * S, "44S params + 48S records + 24T partials + 44S grads"),
+    }
+    dom = max((k for k in stages if stages[k][1] > 0 and k in kernel_bytes), key=lambda k: stages[k][0])
     peak, peak_src = load_peaks()
-    prep_bytes = 44 * n + 44 * (n - S_mean) + 48 * S_mean + 8 * T_mean
     launch_ms = stages[dom][0] / stages[dom][1]
-    if dom == "prepare":
-        achieved = prep_bytes / (launch_ms * 1e-3) / 1e9
-        traffic = ncu_traffic(args.config)
-        roof = {"kernel": "k_prep", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "bytes_per_launch": prep_bytes, "launch_ms": launch_ms,
-                "bytes_formula": "44N params read + 44(N-S) gradient zero-fill + 48S records + 8T pairs"}
-    else:
-        roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
-                "frac": None, "traffic": None, "launch_ms": launch_ms}
+    kname, kbytes, kformula = kernel_bytes[dom]
+    achieved = kbytes / (launch_ms * 1e-3) / 1e9
+    roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(args.config) if dom == "prepare" else None,
+            "peak_source": peak_src, "bytes_per_launch": kbytes, "launch_ms": launch_ms,
+            "bytes_formula": kformula}
+    per_kernel = {}
+    for k, (kn, kb, _) in kernel_bytes.items():
+        if stages.get(k, (0, 0))[1]:
+            ms = stages[k][0] / stages[k][1]
+            per_kernel[kn] = {"ms": ms, "gbs": kb / (ms * 1e-3) / 1e9, "frac": kb / (ms * 1e-3) / 1e9 / peak}
     u1_bytes = 88 * n + 8 * P
     step_gbs = u1_bytes / (ms_per_step * 1e-3) / 1e9
 
@@ -407,8 +435,9 @@ def run_ours(args):
         "roofline": roof,
         "u1_roofline": {"bytes_per_step": u1_bytes, "achieved_gbs": step_gbs, "frac": step_gbs / peak,
                         "formula": "88N + 8P (SURVEY.md §8d)"},
-        "stage_ms_per_step": {k: v[0] / max(v[1], 1) * (v[1] / args.steps) for k, v in stages.items()
-                              if v[1]},
+        "stage_ms_per_step": {k: v[0] / prof_steps for k, v in stages.items() if v[1]},
+        "kernels": per_kernel,
+        "submission": "CUDA graph per slice pose" if graphs is not None else "kernel by kernel",
         "survivors_mean": S_mean, "pairs_mean": T_mean,
         "e2e": {"value": world * 1000.0 / e2e_ms, "unit": "slices/s", "h2d_bytes_per_step": P * 4,
                 "d2h_bytes_per_step": P * 4 + cap_floats * 44,
@@ -416,8 +445,8 @@ def run_ours(args):
         "gpu_launches": None,
         "clocks": clk.result(),
     }
-    # K_prep + radix passes + forward + backward + chain (the memset is a copy-engine op)
-    launches_per_step = 1 + sort_passes(X, Y) + 3
+    # K_filter + K_exact + radix passes + forward + backward + chain (+1 memset node)
+    launches_per_step = 2 + sort_passes(X, Y) + 3
     line["gpu_launches"] = launches_per_step * args.steps
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -437,7 +466,7 @@ def run_ours(args):
 def sort_passes(X, Y):
     tiles = ((X + 15) // 16) * ((Y + 15) // 16)
     bits = max(0, (tiles - 1).bit_length())
-    return (bits + 7) // 8
+    return (bits + 9) // 10  # <= 10-bit digits (csrc/common.cuh kMaxDigitBits)
 
 
 def main():

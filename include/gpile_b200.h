@@ -240,6 +240,20 @@ int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* ps
                    const gpk_raster_config* cfg, double lambda, double dssim_scale,
                    const gpk_learning_rates* lr0, int32_t total_iterations);
 
+/* ---- CUDA graphs of the fused paths ------------------------------------------- */
+/* Capture gpk_fwd_bwd_slice / gpk_train_step for a fixed pose into an
+ * executable CUDA graph (launch overhead of the ~7 kernels collapses to one
+ * submission). Buffers must already be sized (run the path once first and
+ * reserve pair capacity). Returns a graph id for gpk_graph_launch. */
+int gpk_graph_capture_fwd_bwd(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                              const gpk_raster_config* cfg, int32_t* graph_id);
+int gpk_graph_capture_train(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                            const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                            const gpk_learning_rates* lr0, int32_t total_iterations,
+                            int32_t* graph_id);
+int gpk_graph_launch(gpk_session* s, int32_t graph_id);
+int gpk_graph_destroy_all(gpk_session* s);
+
 /* ---- voxelizer: voxelize / voxelize_backward (voxelize.hpp:113-240) ---------- */
 int gpk_voxelize(gpk_session* s, const gpk_voxelizer_config* cfg, float* volume_out);
 /* Per-8^3-tile lists of the last voxelize (VoxelTiles, voxelize.hpp:86-105). */

@@ -143,6 +143,13 @@ _PROTOS = {
                                     C.POINTER(RasterConfigC)]),
     "gpk_train_step": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC), C.POINTER(RasterConfigC),
                                  C.c_double, C.c_double, C.POINTER(LearningRatesC), C.c_int32]),
+    "gpk_graph_capture_fwd_bwd": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC),
+                                            C.POINTER(RasterConfigC), C.POINTER(C.c_int32)]),
+    "gpk_graph_capture_train": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC),
+                                          C.POINTER(RasterConfigC), C.c_double, C.c_double,
+                                          C.POINTER(LearningRatesC), C.c_int32, C.POINTER(C.c_int32)]),
+    "gpk_graph_launch": (C.c_int, [_P, C.c_int32]),
+    "gpk_graph_destroy_all": (C.c_int, [_P]),
     "gpk_voxelize": (C.c_int, [_P, C.POINTER(VoxelizerConfigC), _F]),
     "gpk_voxel_tile_count": (C.c_int, [_P, _U64, _U64]),
     "gpk_get_voxel_tile_lists": (C.c_int, [_P, _U32, _U32]),

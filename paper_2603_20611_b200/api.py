@@ -386,6 +386,30 @@ class Session:
                                    C.byref(l), int(total_iterations)))
         self.shape = (pose.height, pose.width)
 
+    # CUDA graphs of the fused paths
+    def capture_fwd_bwd(self, pose: SlicePose, psf: PsfSpec, cfg: RasterConfig) -> int:
+        p, f, c = pose.to_c(), psf.to_c(), cfg.to_c()
+        gid = C.c_int32()
+        check(N.lib.gpk_graph_capture_fwd_bwd(self._h, C.byref(p), C.byref(f), C.byref(c), C.byref(gid)))
+        self.shape = (pose.height, pose.width)
+        return int(gid.value)
+
+    def capture_train(self, pose: SlicePose, psf: PsfSpec, cfg: RasterConfig, lam: float,
+                      dssim_scale: float, lr0: LearningRates, total_iterations: int) -> int:
+        p, f, c, l = pose.to_c(), psf.to_c(), cfg.to_c(), lr0.to_c()
+        gid = C.c_int32()
+        check(N.lib.gpk_graph_capture_train(self._h, C.byref(p), C.byref(f), C.byref(c), lam,
+                                            dssim_scale, C.byref(l), int(total_iterations),
+                                            C.byref(gid)))
+        self.shape = (pose.height, pose.width)
+        return int(gid.value)
+
+    def graph_launch(self, graph_id: int):
+        check(N.lib.gpk_graph_launch(self._h, int(graph_id)))
+
+    def graph_destroy_all(self):
+        check(N.lib.gpk_graph_destroy_all(self._h))
+
     # voxelizer
     def voxelize(self, cfg: VoxelizerConfig, to_host: bool = True) -> np.ndarray | None:
         c = cfg.to_c()

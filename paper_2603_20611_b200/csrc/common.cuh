@@ -27,9 +27,12 @@ constexpr int kPrepThreads = 256;
 constexpr int kPrepItems = 4;
 constexpr int kPrepBlock = kPrepThreads * kPrepItems;   // Gaussians per K_prep block
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 8;
-constexpr int kSortTile = kSortThreads * kSortItems;    // keys per onesweep tile
-constexpr int kMaxSortPasses = 3;                       // up to 2^24 tiles
+constexpr int kSortItems = 4;
+constexpr int kSortTile = kSortThreads * kSortItems;    // keys per sort tile (one CTA)
+constexpr int kMaxDigitBits = 10;                       // radix digit width <= 10 bits
+constexpr int kMaxBuckets = 1 << kMaxDigitBits;
+constexpr int kMaxSortPasses = 2;                       // up to 2^20 image tiles
+constexpr int kSuperTiles = 16;                         // sort tiles per super-tile histogram row
 constexpr int kNumParams = 11;
 
 // Error codes recorded on the device (mirrors gpk_status).
@@ -56,6 +59,7 @@ struct SliceArgs {
     double R[9];          // R_c row-major
     double t[3];
     double sx, sy, ppx, ppy;
+    double inv_sx, inv_sy;  // 1/pixel_spacing (fast path only; the reference path divides)
     double sigma_z;
     double tau;
     double footprint;     // footprint_sigmas
@@ -65,8 +69,9 @@ struct SliceArgs {
     int identity_rot;     // R_c == I exactly: world_to_camera reduces to mu + t bit-exactly
 };
 
-// Small control block, memset to zero at the start of every prepare.
-struct Control {
+// Small control block, memset to zero at the start of every prepare. Its size
+// is a multiple of 64 B so the arrays packed after it stay 8 B aligned.
+struct alignas(64) Control {
     unsigned int prep_block_ctr;               // dynamic block id of K_filter
     unsigned int sort_tile_ctr[kMaxSortPasses];
     unsigned int survivors;                    // S, written by the last K_exact chunk
@@ -75,7 +80,8 @@ struct Control {
     unsigned int adam_done_ctr;
     unsigned int candidates;                   // C, written by the last K_filter block
     unsigned int exact_chunk_ctr;              // chunk claims of K_exact
-    unsigned int pad[6];
+    unsigned int chain_exact;                  // survivors deferred to the fp64 chain
+    unsigned int pad[5];
 };
 
 constexpr int kExactChunk = 256;               // candidates per K_exact chunk (= threads)
@@ -191,6 +197,50 @@ __device__ __forceinline__ unsigned long long warp_lookback(unsigned* flags,
     return excl;
 }
 
+// ---- TMA bulk copies (cp.async.bulk) + mbarrier helpers ---------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// global -> shared bulk copy, completion signalled on `bar` (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// shared -> global bulk store (bulk-group completion)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Pairs actually stored for the current slice (T capped by the buffer size).
 __device__ __forceinline__ unsigned stored_pairs(const Control* c, uint64_t cap) {
     const unsigned long long p = c->pairs;
@@ -217,12 +267,14 @@ struct PrepLaunch {
     uint32_t* keys;           // pre-sort tile keys
     uint32_t* vals;           // pre-sort candidate slots
     uint64_t pair_cap;
-    unsigned* hist;           // kMaxSortPasses x 256 global digit counts
-    unsigned* tile_hist0;     // per sort tile (2048 pre-sort positions) x 256: digit-0 counts
-    unsigned* tile_hist_all;  // passes x sort tiles x 256 (zeroed by K_filter)
+    unsigned* hist;           // kMaxSortPasses x kMaxBuckets global digit counts
+    unsigned* tile_hist0;     // pass-0 region: per sort tile rows, then per super-tile rows
+    unsigned* tile_hist_all;  // kMaxSortPasses regions of hist_region words (zeroed by K_filter)
     uint64_t sort_tiles_cap;
-    unsigned* prev_sort_tiles;  // persistent: sort tiles used by the previous prepare
+    uint64_t hist_region;     // words per pass region
+    unsigned* prev_sort_words;  // persistent: {sort tiles used, buckets} of the previous prepare
     int passes;
+    int digit_bits;           // radix digit width of every pass
     unsigned long long* exact_words;  // per K_exact chunk: ready<<63 | S<<32 | P (zeroed per prepare)
     Control* ctrl;
     ErrorState* err;
@@ -230,7 +282,7 @@ struct PrepLaunch {
     int exact_grid;           // persistent K_exact CTAs
 };
 
-constexpr int kFilterItems = 8;
+constexpr int kFilterItems = 4;
 constexpr int kFilterBlock = kPrepThreads * kFilterItems;  // Gaussians per K_filter block
 
 struct SortLaunch {
@@ -238,11 +290,14 @@ struct SortLaunch {
     const uint32_t* vals_in;
     uint32_t* keys_out;
     uint32_t* vals_out;
-    const unsigned* hist;          // 256 global counts of this pass's digit
-    const unsigned* tile_hist;     // per sort tile x 256 counts of this pass's digit
-    unsigned* tile_hist_next;      // next pass's per-tile counts (nullptr on the last pass)
-    unsigned* prev_sort_tiles;     // written by the last pass
+    const unsigned* hist;          // 2^bits global counts of this pass's digit
+    const unsigned* tile_hist;     // this pass's region: tile rows then super-tile rows (2^bits each)
+    unsigned* tile_hist_next;      // next pass's region (nullptr on the last pass)
+    uint64_t sort_tiles_cap;       // offset (in rows) of the super-tile rows
+    unsigned* prev_sort_words;     // written by the last pass: {sort tiles, buckets}
     int shift;
+    int bits;                      // digit width of this pass
+    unsigned next_buckets;         // 2^bits of the next pass
     int pass;
     const Control* ctrl;
     uint64_t pair_cap;
@@ -271,6 +326,8 @@ struct ChainLaunch {
     float* stat_norm;              // optional (screen-space dL/dmu_2d norm)
     uint8_t* stat_observed;        // optional
     float* stat_world;             // optional, 3 per primitive
+    uint32_t* exact_list;          // survivor slots deferred to the fp64 chain
+    unsigned* exact_count;         // Control::chain_exact
     ErrorState* err;
     SliceArgs slice;
 };
@@ -305,7 +362,81 @@ struct LossLaunch {
     float w[11];         // normalized Gaussian taps
 };
 
-void launch_filter(const PrepLaunch& a, cudaStream_t st);
+// ---- voxelizer (voxelize.hpp) -------------------------------------------------
+// One primitive's voxelizer state (VoxelPrim, voxelize.hpp:42-48), 64 B.
+struct alignas(16) VoxRecord {
+    float mu[3];          // world mean
+    float log2a;          // log2(alpha)
+    float a[6];           // Sigma^-1 * (-0.5*log2 e): a00 a11 a22 2a01 2a02 2a12
+    uint16_t lo[3], hi[3];  // inclusive voxel index bounds of the support AABB
+    uint32_t gidx;
+    uint32_t pair_base;
+    uint32_t pad;
+};
+static_assert(sizeof(VoxRecord) == 64, "voxel record must stay 64 B");
+
+struct VoxArgs {
+    int dims[3];
+    int tile[3];
+    int ntiles[3];
+    double spacing[3];
+    double origin[3];
+    double support;
+    double mod;
+};
+
+struct VoxPrepLaunch {
+    const float* params;
+    uint64_t cap;
+    uint32_t n;
+    VoxRecord* records;        // indexed by set index (all N slots)
+    uint32_t* survivor_list;   // survivor slot -> set index
+    uint32_t* keys;
+    uint32_t* vals;
+    uint64_t pair_cap;
+    unsigned* hist;
+    unsigned* tile_hist0;
+    uint64_t sort_tiles_cap;
+    int passes;
+    int digit_bits;
+    unsigned long long* chunk_words;  // per 256-prim chunk: ready<<63 | S<<32 | P
+    Control* ctrl;
+    ErrorState* err;
+    VoxArgs v;
+    int grid;
+};
+
+struct VoxEvalLaunch {
+    const VoxRecord* records;
+    const uint32_t* keys;      // sorted voxel-tile keys
+    const uint32_t* vals;      // sorted set indices
+    const Control* ctrl;
+    uint64_t pair_cap;
+    float* volume;             // voxelize output
+    const float* dl_dv;        // backward input
+    float* partials;           // backward output: 10 f32 per pair (pre-sort position)
+    VoxArgs v;
+    int dl_global;             // backward: tile too large to stage dL/dV in shared memory
+};
+
+struct VoxChainLaunch {
+    const float* params;
+    uint64_t cap;
+    const VoxRecord* records;
+    const uint32_t* survivor_list;
+    const float* partials;
+    const Control* ctrl;
+    float* grads;
+    ErrorState* err;
+    VoxArgs v;
+};
+
+void launch_vox_prep(const VoxPrepLaunch& a, cudaStream_t st);
+void launch_vox_eval(const VoxEvalLaunch& a, cudaStream_t st);
+void launch_vox_bwd(const VoxEvalLaunch& a, cudaStream_t st);
+void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st);
+
+void launch_filter(const PrepLaunch& a, int num_sms, cudaStream_t st);
 void launch_exact(const PrepLaunch& a, cudaStream_t st);
 int exact_blocks_per_sm(size_t dyn_smem);
 size_t exact_dyn_smem(unsigned nfilter);

@@ -69,6 +69,48 @@ __device__ __forceinline__ bool certainly_culled(const float p[11], const SliceA
     return 0.5f * q > thresh + margin;
 }
 
+// Cheaper certain-cull for the common case R_c = I (every slice_pose_for_index
+// pose): only the third row of R(q) is needed, mu_c,z = mu_z + t_z in fp32
+// with t_z split hi/lo, and the guards avoid per-parameter checks (a single
+// finiteness test of the parameter sum routes NaN/Inf to the exact path).
+struct FilterConsts {
+    float log_tau, mod, sz2;
+    float tx, ty, tz_hi, tz_lo;
+};
+
+__device__ __forceinline__ bool certainly_culled_identity(const float p[11], const FilterConsts& c) {
+    float sum = p[0];
+#pragma unroll
+    for (int k = 1; k < 11; ++k) sum += p[k];
+    if (!isfinite(sum)) return false;
+    const float lmax = fmaxf(p[3], fmaxf(p[4], p[5])), lmin = fminf(p[3], fminf(p[4], p[5]));
+    // |log-scale| <= 40 and (smax/smin) < e^6.2 ~ 490: the exact path's inverse
+    // is unfloored there (focus.cuh invert_cov guard 1e3 ratio)
+    if (!(lmax < 40.f && lmin > -40.f && lmax - lmin < 6.2f)) return false;
+    const float qn2 = p[6] * p[6] + p[7] * p[7] + p[8] * p[8] + p[9] * p[9];
+    if (!(qn2 > 1e-20f && qn2 < 1e20f)) return false;
+    const float inv = rsqrtf(qn2);
+    const float w = p[6] * inv, x = p[7] * inv, y = p[8] * inv, z = p[9] * inv;
+    // third row of R(q): Sigma_c,zz = sum_k (mod s_k)^2 R_2k^2
+    const float r0 = 2.f * (x * z - w * y), r1 = 2.f * (y * z + w * x), r2 = 1.f - 2.f * (x * x + y * y);
+    const float s0 = __expf(p[3]) * c.mod, s1 = __expf(p[4]) * c.mod, s2 = __expf(p[5]) * c.mod;
+    const float var = (s0 * r0) * (s0 * r0) + (s1 * r1) * (s1 * r1) + (s2 * r2) * (s2 * r2);
+    const float mcz = (p[2] + c.tz_hi) + c.tz_lo;
+    const float den = c.sz2 + var;
+    const float q = mcz * mcz / den;
+    const float raw = p[10];
+    const float log_alpha = raw >= 0.f ? -__logf(1.f + __expf(-raw)) : raw - __logf(1.f + __expf(raw));
+    const float mcx = p[0] + c.tx, mcy = p[1] + c.ty;
+    const float smin = __expf(lmin) * c.mod;
+    const float mu2 = mcx * mcx + mcy * mcy + mcz * mcz;
+    // reference cancellation noise (render.hpp:105) + fp32 rounding of mu_c,z
+    const float noise = 2e-14f * mu2 / (smin * smin) +
+                        4.f * fabsf(mcz) * 1.2e-7f * (fabsf(p[2]) + fabsf(c.tz_hi)) / den;
+    const float thresh = log_alpha - c.log_tau;
+    const float margin = 2e-3f + 2e-5f * fabsf(thresh) + noise;
+    return 0.5f * q > thresh + margin;
+}
+
 __device__ __forceinline__ void load_params(const float* __restrict__ params, uint64_t cap,
                                             uint32_t i, float p[11]) {
 #pragma unroll
@@ -81,69 +123,128 @@ __device__ __forceinline__ void zero_grads(float* grads, uint64_t cap, uint32_t 
 }
 
 // ---- K_filter ------------------------------------------------------------------
+// Persistent CTAs walk 1024-Gaussian chunks. Each chunk's 11 parameter planes
+// (4 KB each) arrive by TMA bulk copy (cp.async.bulk + mbarrier complete_tx):
+// 44 KB in flight per CTA without occupying registers. The dense gradient
+// planes of the chunk are zero-filled by 11 bulk shared->global stores from a
+// zero buffer (survivors are overwritten later by K_chain; culled primitives
+// keep the exact zeros of grad_chain.hpp:12-22).
 template <bool kZeroGrads>
 __global__ void __launch_bounds__(kPrepThreads) k_filter(const PrepLaunch a, float log_tau,
-                                                         int filter_on) {
+                                                         int filter_on, unsigned nchunks) {
     constexpr int kSlots = kFilterItems * 8;  // (item, warp) counts, in set order
+    extern __shared__ __align__(128) float s_dyn[];
+    float* s_p = s_dyn;                          // 11 planes x kFilterBlock
+    float* s_zero = s_dyn + 11 * kFilterBlock;   // kFilterBlock zeros
+    __shared__ __align__(8) uint64_t s_bar;
     __shared__ unsigned s_off[kSlots];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned b = blockIdx.x;
-    const uint32_t base = b * kFilterBlock;
     const float mod_f = (float)a.slice.mod;
     const float sz2 = (float)(a.slice.sigma_z * a.slice.sigma_z);
+    const unsigned plane_bytes = kFilterBlock * sizeof(float);
+
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        fence_mbar_init();
+    }
+    if (kZeroGrads) {
+        for (int i = tid; i < kFilterBlock; i += kPrepThreads) s_zero[i] = 0.f;
+        fence_proxy_async_smem();
+    }
+    __syncthreads();
 
     // Housekeeping: clear the per-sort-tile digit histograms the previous
     // prepare used (all passes) before K_exact / the radix passes refill them.
     {
-        const uint64_t row = a.sort_tiles_cap * 256;
-        const uint64_t used = (uint64_t)(*a.prev_sort_tiles) * 256;
-        const uint64_t total = (uint64_t)a.passes * used;
+        const uint64_t pt = a.prev_sort_words[0], pnb = a.prev_sort_words[1];
+        const uint64_t tile_words = pt * pnb;
+        const uint64_t super_words = ((pt + kSuperTiles - 1) / kSuperTiles) * pnb;
+        const uint64_t used = tile_words + super_words;  // per pass region
+        const uint64_t total = (uint64_t)kMaxSortPasses * used;
         if (used)
-            for (uint64_t w = (uint64_t)b * kPrepThreads + tid; w < total;
-                 w += (uint64_t)gridDim.x * kPrepThreads)
-                a.tile_hist_all[(w / used) * row + (w % used)] = 0u;
+            for (uint64_t w = (uint64_t)blockIdx.x * kPrepThreads + tid; w < total;
+                 w += (uint64_t)gridDim.x * kPrepThreads) {
+                const uint64_t p = w / used, o = w % used;
+                const uint64_t off = o < tile_words ? o : a.sort_tiles_cap * pnb + (o - tile_words);
+                a.tile_hist_all[p * a.hist_region + off] = 0u;
+            }
     }
 
-    unsigned ballots[kFilterItems];
-#pragma unroll
-    for (int k = 0; k < kFilterItems; ++k) {
-        const uint32_t i = base + k * kPrepThreads + tid;
-        bool cand = false;
-        if (i < a.n) {
-            cand = true;
+    FilterConsts fc;
+    fc.log_tau = log_tau;
+    fc.mod = mod_f;
+    fc.sz2 = sz2;
+    fc.tx = (float)a.slice.t[0];
+    fc.ty = (float)a.slice.t[1];
+    fc.tz_hi = (float)a.slice.t[2];
+    fc.tz_lo = (float)(a.slice.t[2] - (double)fc.tz_hi);
+    const bool ident = a.slice.identity_rot != 0;
+
+    unsigned phase = 0;
+    for (unsigned b = blockIdx.x; b < nchunks; b += gridDim.x, phase ^= 1u) {
+        const uint32_t base = b * kFilterBlock;
+        if (tid == 0) {
             if (filter_on) {
-                float p[11];
-                load_params(a.params, a.cap, i, p);
-                cand = !certainly_culled(p, a.slice, log_tau, mod_f, sz2);
+                mbar_expect_tx(&s_bar, 11 * plane_bytes);
+#pragma unroll 1
+                for (int k = 0; k < 11; ++k)
+                    bulk_g2s(s_p + k * kFilterBlock, a.params + (uint64_t)k * a.cap + base, plane_bytes, &s_bar);
             }
-            if (kZeroGrads && !cand) zero_grads(a.grads, a.cap, i);
+            if (kZeroGrads) {
+#pragma unroll 1
+                for (int k = 0; k < 11; ++k)
+                    bulk_s2g(a.grads + (uint64_t)k * a.cap + base, s_zero, plane_bytes);
+                bulk_commit();
+            }
         }
-        ballots[k] = __ballot_sync(0xffffffffu, cand);
-        if (lane == 0) s_off[k * 8 + warp] = __popc(ballots[k]);
-    }
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan of the 64 slots, two per lane
-        const unsigned c0 = s_off[2 * lane], c1 = s_off[2 * lane + 1];
-        unsigned incl = c0 + c1;
+        if (filter_on) mbar_wait(&s_bar, phase);
+
+        unsigned ballots[kFilterItems];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
+        for (int k = 0; k < kFilterItems; ++k) {
+            const int li = k * kPrepThreads + tid;
+            const uint32_t i = base + li;
+            bool cand = false;
+            if (i < a.n) {
+                cand = true;
+                if (filter_on) {
+                    float p[11];
+#pragma unroll
+                    for (int q = 0; q < 11; ++q) p[q] = s_p[q * kFilterBlock + li];
+                    cand = ident ? !certainly_culled_identity(p, fc)
+                                 : !certainly_culled(p, a.slice, log_tau, mod_f, sz2);
+                }
+            }
+            ballots[k] = __ballot_sync(0xffffffffu, cand);
+            if (lane == 0) s_off[k * 8 + warp] = __popc(ballots[k]);
         }
-        const unsigned ex = incl - c0 - c1;
-        __syncwarp();
-        s_off[2 * lane] = ex;
-        s_off[2 * lane + 1] = ex + c0;
-        if (lane == 31) a.filter_counts[b] = incl;
-    }
-    __syncthreads();
-    uint32_t* out = a.cand_local + (uint64_t)b * kFilterBlock;
+        __syncthreads();
+        if (warp == 0) {  // exclusive scan of the 32 (item, warp) slots
+            const unsigned v = s_off[lane];
+            unsigned incl = v;
 #pragma unroll
-    for (int k = 0; k < kFilterItems; ++k) {
-        if (ballots[k] & (1u << lane))
-            out[s_off[k * 8 + warp] + __popc(ballots[k] & lanemask_lt())] = base + k * kPrepThreads + tid;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            __syncwarp();
+            s_off[lane] = incl - v;
+            if (lane == 31) {
+                a.filter_counts[b] = incl;
+                if (incl) atomicAdd(&a.ctrl->candidates, incl);
+            }
+        }
+        __syncthreads();
+        uint32_t* out = a.cand_local + (uint64_t)b * kFilterBlock;
+#pragma unroll
+        for (int k = 0; k < kFilterItems; ++k) {
+            if (ballots[k] & (1u << lane))
+                out[s_off[k * 8 + warp] + __popc(ballots[k] & lanemask_lt())] = base + k * kPrepThreads + tid;
+        }
+        __syncthreads();  // s_p / s_off are reused by the next chunk
     }
+    if (kZeroGrads && tid == 0) bulk_wait_all();
 }
 
 // ---- K_exact -------------------------------------------------------------------
@@ -155,10 +256,17 @@ __global__ void __launch_bounds__(kExactChunk) k_exact(const PrepLaunch a) {
     __shared__ uint16_t s_rect[kExactChunk][3];          // tx0, ty0, ntx
     __shared__ unsigned long long s_warp[kExactChunk / 32];
     __shared__ unsigned long long s_excl;
-    __shared__ unsigned s_hist[kMaxSortPasses][256];
+    __shared__ unsigned s_hist[kMaxSortPasses][kMaxBuckets];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int k = tid; k < kMaxSortPasses * 256; k += kExactChunk) (&s_hist[0][0])[k] = 0;
+    const unsigned C = a.ctrl->candidates;  // total, accumulated by K_filter
+    const unsigned nchunks = (C + kExactChunk - 1) / kExactChunk;
+    // claim the first chunk before any setup: surplus CTAs leave at once
+    if (tid == 0) s_chunk = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
+    __syncthreads();
+    if (s_chunk >= nchunks) return;
+    for (int k = tid; k < kMaxSortPasses * kMaxBuckets; k += kExactChunk) (&s_hist[0][0])[k] = 0;
+    const unsigned dmask = (1u << a.digit_bits) - 1;
     // candidate layout: exclusive prefix over the K_filter blocks' counts
     {
         const unsigned nb = a.nfilter;
@@ -185,14 +293,14 @@ __global__ void __launch_bounds__(kExactChunk) k_exact(const PrepLaunch a) {
         if (tid == 0) s_bpre[nb] = carry;
         __syncthreads();
     }
-    const unsigned C = s_bpre[a.nfilter];
-    const unsigned nchunks = (C + kExactChunk - 1) / kExactChunk;
     const int tiles_x = a.slice.tiles_x;
 
-    while (true) {
-        __syncthreads();
-        if (tid == 0) s_chunk = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
-        __syncthreads();
+    for (bool first = true;; first = false) {
+        if (!first) {
+            __syncthreads();
+            if (tid == 0) s_chunk = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
+            __syncthreads();
+        }
         const unsigned chunk = s_chunk;
         if (chunk >= nchunks) break;
         const unsigned c = chunk * kExactChunk + tid;
@@ -207,36 +315,47 @@ __global__ void __launch_bounds__(kExactChunk) k_exact(const PrepLaunch a) {
             const uint32_t i = a.cand_local[(uint64_t)lo * kFilterBlock + (c - s_bpre[lo])];
             float pf[11];
             load_params(a.params, a.cap, i, pf);
-            double pd[11];
+            SurvivorRecord rec;
+            bool survive = false;
+            uint32_t flag = 0;
+            const int fr = fast_decide(pf, a.slice, rec);
+            if (fr == kFastSurvive) {
+                survive = true;
+            } else if (fr == kAmbiguous) {
+                flag = kExactFlag;
+                // near a decision boundary: the reference's own fp64 evaluation
+                double pd[11];
 #pragma unroll
-            for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
-            Focus f;
-            const int r = focus_prepare(pd, a.slice, f);
-            if (r == kSurvive) {
-                const int tx0 = f.lo_x / kTile, tx1 = f.hi_x / kTile;
-                const int ty0 = f.lo_y / kTile, ty1 = f.hi_y / kTile;
+                for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
+                Focus f;
+                const int r = focus_prepare(pd, a.slice, f);
+                if (r == kSurvive) {
+                    survive = true;
+                    rec.mu2d_x = f.mu_e.x;
+                    rec.mu2d_y = f.mu_e.y;
+                    rec.conic_a = (float)f.con_a;
+                    rec.conic_b = (float)f.con_b;
+                    rec.conic_d = (float)f.con_d;
+                    rec.alpha_tilde = (float)f.alpha_tilde;
+                    rec.lo_x = (uint16_t)f.lo_x;
+                    rec.hi_x = (uint16_t)f.hi_x;
+                    rec.lo_y = (uint16_t)f.lo_y;
+                    rec.hi_y = (uint16_t)f.hi_y;
+                } else if (r > 0) {
+                    record_error(a.err, r, i);  // gradients of culled candidates: zeroed by K_filter
+                }
+            }
+            if (survive) {
+                const int tx0 = rec.lo_x / kTile, tx1 = rec.hi_x / kTile;
+                const int ty0 = rec.lo_y / kTile, ty1 = rec.hi_y / kTile;
                 const unsigned ntx = tx1 - tx0 + 1, nty = ty1 - ty0 + 1;
                 v = (1ull << 32) | (unsigned long long)(ntx * nty);
                 s_rect[tid][0] = (uint16_t)tx0;
                 s_rect[tid][1] = (uint16_t)ty0;
                 s_rect[tid][2] = (uint16_t)ntx;
-                SurvivorRecord rec;
-                rec.mu2d_x = f.mu_e.x;
-                rec.mu2d_y = f.mu_e.y;
-                rec.conic_a = (float)f.con_a;
-                rec.conic_b = (float)f.con_b;
-                rec.conic_d = (float)f.con_d;
-                rec.alpha_tilde = (float)f.alpha_tilde;
-                rec.lo_x = (uint16_t)f.lo_x;
-                rec.hi_x = (uint16_t)f.hi_x;
-                rec.lo_y = (uint16_t)f.lo_y;
-                rec.hi_y = (uint16_t)f.hi_y;
-                rec.gidx = i;
+                rec.gidx = i | flag;
                 rec.pair_base = 0;
                 a.records[c] = rec;
-            } else {
-                if (r > 0) record_error(a.err, r, i);
-                if (kZeroGrads) zero_grads(a.grads, a.cap, i);
             }
         }
         // block inclusive scan of (survivor, pairs)
@@ -295,64 +414,335 @@ __global__ void __launch_bounds__(kExactChunk) k_exact(const PrepLaunch a) {
             if (pos < a.pair_cap) {
                 a.keys[pos] = tile;
                 a.vals[pos] = chunk * kExactChunk + lo;
-                if (a.passes > 0)
-                    atomicAdd(&a.tile_hist0[(pos / kSortTile) * 256 + (tile & 255u)], 1u);
+                if (a.passes > 0) {
+                    const uint64_t st = pos / kSortTile;
+                    atomicAdd(&a.tile_hist0[st * (dmask + 1) + (tile & dmask)], 1u);
+                    atomicAdd(&a.tile_hist0[(a.sort_tiles_cap + st / kSuperTiles) * (dmask + 1) + (tile & dmask)], 1u);
+                }
                 for (int ps = 0; ps < a.passes; ++ps)
-                    atomicAdd(&s_hist[ps][(tile >> (8 * ps)) & 255u], 1u);
+                    atomicAdd(&s_hist[ps][(tile >> (a.digit_bits * ps)) & dmask], 1u);
             }
         }
     }
     __syncthreads();
-    for (int ps = 0; ps < a.passes; ++ps) {
-        const unsigned v = s_hist[ps][tid];
-        if (v) atomicAdd(&a.hist[ps * 256 + tid], v);
+    for (int ps = 0; ps < a.passes; ++ps)
+        for (unsigned d = tid; d <= dmask; d += kExactChunk) {
+            const unsigned v = s_hist[ps][d];
+            if (v) atomicAdd(&a.hist[ps * kMaxBuckets + d], v);
+        }
+}
+
+// Stage-2 merge of one survivor's per-tile sums in tile order (backward.hpp:141-145).
+__device__ __forceinline__ void merge_partials(const ChainLaunch& a, const SurvivorRecord& rec,
+                                               double acc[6]) {
+    const unsigned ntx = rec.hi_x / kTile - rec.lo_x / kTile + 1;
+    const unsigned nty = rec.hi_y / kTile - rec.lo_y / kTile + 1;
+    const unsigned np = ntx * nty;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) acc[j] = 0.0;
+    const float2* part = reinterpret_cast<const float2*>(a.partials + 6ull * rec.pair_base);
+    for (unsigned k = 0; k < np; ++k) {
+        const float2 p0 = part[3 * k], p1 = part[3 * k + 1], p2 = part[3 * k + 2];
+        acc[0] += (double)p0.x;
+        acc[1] += (double)p0.y;
+        acc[2] += (double)p1.x;
+        acc[3] += (double)p1.y;
+        acc[4] += (double)p2.x;
+        acc[5] += (double)p2.y;
     }
 }
 
-// K_chain: one thread per survivor (backward.hpp:148-185).
+__device__ __forceinline__ void store_chain(const ChainLaunch& a, uint32_t i, const float g[11],
+                                            const float dmu[3], const double acc[6]) {
+    const bool finite = isfinite(g[10]) && isfinite(g[0] + g[1] + g[2]) &&
+                        isfinite(g[3] + g[4] + g[5]) && isfinite(g[6] + g[7] + g[8] + g[9]);
+    if (!finite) record_error(a.err, kErrNumeric, i);  // backward.hpp:175-185
+#pragma unroll
+    for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = g[k];
+    if (a.stat_norm) a.stat_norm[i] = (float)sqrt(acc[1] * acc[1] + acc[2] * acc[2]);
+    if (a.stat_observed) a.stat_observed[i] = 1;
+    if (a.stat_world) {
+        a.stat_world[3ull * i + 0] = dmu[0];
+        a.stat_world[3ull * i + 1] = dmu[1];
+        a.stat_world[3ull * i + 2] = dmu[2];
+    }
+}
+
+// K_chain: one thread per survivor (backward.hpp:148-185). Survivors that
+// fast_prepare resolves (the same decision K_exact made: identical code and
+// inputs) take the inverse-free fp32 chain; the rest are deferred to
+// K_chain_exact so this kernel stays small in registers.
 __global__ void __launch_bounds__(128) k_chain(const ChainLaunch a) {
     const unsigned S = a.ctrl->survivors;
     for (unsigned slot = blockIdx.x * blockDim.x + threadIdx.x; slot < S;
          slot += gridDim.x * blockDim.x) {
         const uint32_t cid = a.survivor_list[slot];
         const SurvivorRecord rec = a.records[cid];
+        if (rec.gidx & kExactFlag) {
+            a.exact_list[atomicAdd(a.exact_count, 1u)] = slot;
+            continue;
+        }
         const uint32_t i = rec.gidx;
+        float pf[11];
+        load_params(a.params, a.cap, i, pf);
+        FastFocus ff;
+        fast_state(pf, a.slice, ff);
+        double acc[6];
+        merge_partials(a, rec, acc);
+        float g[11], dmu[3];
+        fast_backward(pf, ff, acc, a.slice, g, dmu);
+        store_chain(a, i, g, dmu, acc);
+    }
+}
+
+// K_chain_exact: the reference's fp64 chain for the deferred survivors.
+__global__ void __launch_bounds__(128) k_chain_exact(const ChainLaunch a) {
+    const unsigned E = *a.exact_count;
+    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        const uint32_t cid = a.survivor_list[a.exact_list[e]];
+        const SurvivorRecord rec = a.records[cid];
+        const uint32_t i = rec.gidx & ~kExactFlag;
+        float pf[11];
+        load_params(a.params, a.cap, i, pf);
+        double acc[6];
+        merge_partials(a, rec, acc);
+        double pd[11];
+#pragma unroll
+        for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
+        Focus f;
+        focus_prepare(pd, a.slice, f);
+        double gd[11];
+        D3 dl_dmu;
+        focus_backward(pd, f, acc, a.slice, gd, dl_dmu);
+        float g[11], dmu[3] = {(float)dl_dmu.x, (float)dl_dmu.y, (float)dl_dmu.z};
+#pragma unroll
+        for (int k = 0; k < 11; ++k) g[k] = (float)gd[k];
+        store_chain(a, i, g, dmu, acc);
+    }
+}
+
+// ---- voxelizer: prepare_voxel_prims + VoxelTiles (voxelize.hpp:52-105) ---------
+// Persistent CTAs take 256-primitive chunks in set order. Per primitive: the
+// world covariance and its inverse in the reference's fp64 order (support
+// bounds must reproduce the reference's integer voxel ranges exactly,
+// voxelize.hpp:66-74; invert_covariance raises the same errors), a 64 B record
+// for the evaluation kernel, and (8^3-tile, primitive) pairs emitted in
+// (primitive, tile) order through the same wait-free ordered prefix as K_exact.
+__global__ void __launch_bounds__(256) k_vprep(const VoxPrepLaunch a) {
+    __shared__ unsigned s_chunk;
+    __shared__ unsigned long long s_incl[256];
+    __shared__ uint16_t s_t0[256][3];
+    __shared__ uint16_t s_nt[256][2];  // tiles along x and y of the primitive's box
+    __shared__ unsigned long long s_warp[8];
+    __shared__ unsigned long long s_excl;
+    __shared__ unsigned s_hist[kMaxSortPasses][kMaxBuckets];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int k = tid; k < kMaxSortPasses * kMaxBuckets; k += 256) (&s_hist[0][0])[k] = 0;
+    const unsigned dmask = (1u << a.digit_bits) - 1;
+    const unsigned nchunks = (a.n + 255) / 256;
+    const VoxArgs& v = a.v;
+    constexpr float kK = -0.72134752044448170368f;  // -0.5 * log2(e)
+
+    while (true) {
+        __syncthreads();
+        if (tid == 0) s_chunk = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
+        __syncthreads();
+        const unsigned chunk = s_chunk;
+        if (chunk >= nchunks) break;
+        const uint32_t i = chunk * 256 + tid;
+        unsigned long long val = 0;
+        if (i < a.n) {
+            float pf[11];
+            load_params(a.params, a.cap, i, pf);
+            double pd[11];
+#pragma unroll
+            for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
+            D33 sigma, rot, inv;
+            D3 scale;
+            int e = world_covariance(pd, v.mod, sigma, rot, scale);
+            if (!e) e = invert_cov(sigma, scale, v.mod, inv);
+            if (e) {
+                record_error(a.err, e, i);
+            } else {
+                const double alpha = 1.0 / (1.0 + exp(-pd[10]));
+                int lo[3], hi[3];
+                bool inside = true;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const double half = v.support * sqrt(sigma.m[d][d]);
+                    const double lo_w = pd[d] - half, hi_w = pd[d] + half;
+                    lo[d] = max(0, x86_trunc_int(ceil((lo_w - v.origin[d]) / v.spacing[d])));
+                    hi[d] = min(v.dims[d] - 1, x86_trunc_int(floor((hi_w - v.origin[d]) / v.spacing[d])));
+                    if (lo[d] > hi[d]) inside = false;
+                }
+                if (inside) {
+                    unsigned np = 1;
+                    unsigned nt[3];
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        const int t0 = lo[d] / v.tile[d];
+                        nt[d] = (unsigned)(hi[d] / v.tile[d] - t0 + 1);
+                        np *= nt[d];
+                        s_t0[tid][d] = (uint16_t)t0;
+                    }
+                    s_nt[tid][0] = (uint16_t)nt[0];
+                    s_nt[tid][1] = (uint16_t)nt[1];
+                    val = (1ull << 32) | np;
+                    VoxRecord rec;
+                    rec.mu[0] = pf[0];
+                    rec.mu[1] = pf[1];
+                    rec.mu[2] = pf[2];
+                    rec.log2a = (float)log2(alpha);
+                    rec.a[0] = (float)inv.m[0][0] * kK;
+                    rec.a[1] = (float)inv.m[1][1] * kK;
+                    rec.a[2] = (float)inv.m[2][2] * kK;
+                    rec.a[3] = (float)(inv.m[0][1] + inv.m[1][0]) * kK;
+                    rec.a[4] = (float)(inv.m[0][2] + inv.m[2][0]) * kK;
+                    rec.a[5] = (float)(inv.m[1][2] + inv.m[2][1]) * kK;
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        rec.lo[d] = (uint16_t)lo[d];
+                        rec.hi[d] = (uint16_t)hi[d];
+                    }
+                    rec.gidx = i;
+                    rec.pair_base = 0;
+                    rec.pad = 0;
+                    a.records[i] = rec;
+                }
+            }
+        }
+        unsigned long long incl = val;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        unsigned long long add = 0;
+        for (int w = 0; w < warp; ++w) add += s_warp[w];
+        incl += add;
+        s_incl[tid] = incl;
+        __syncthreads();
+        const unsigned long long agg = s_incl[255];
+        if (warp == 0) {
+            const unsigned long long excl = warp_prefix_aggregates(a.chunk_words, chunk, agg);
+            if (lane == 0) {
+                s_excl = excl;
+                if (chunk == nchunks - 1) {
+                    const unsigned long long tot = excl + agg;
+                    const unsigned P = (unsigned)(tot & 0xffffffffull);
+                    a.ctrl->survivors = (unsigned)(tot >> 32);
+                    a.ctrl->pairs = P;
+                    a.ctrl->pair_overflow = (P > a.pair_cap) ? 1u : 0u;
+                }
+            }
+        }
+        __syncthreads();
+        const unsigned S0 = (unsigned)(s_excl >> 32);
+        const unsigned P0 = (unsigned)(s_excl & 0xffffffffull);
+        {
+            const unsigned long long prev = tid ? s_incl[tid - 1] : 0ull;
+            if ((s_incl[tid] >> 32) != (prev >> 32)) {
+                a.survivor_list[S0 + (unsigned)(prev >> 32)] = i;
+                a.records[i].pair_base = P0 + (unsigned)(prev & 0xffffffffull);
+            }
+        }
+        const unsigned Pb = (unsigned)(agg & 0xffffffffull);
+        for (unsigned k = tid; k < Pb; k += 256) {
+            unsigned lo = 0, hi = 255;
+            while (lo < hi) {
+                const unsigned mid = (lo + hi) >> 1;
+                if ((unsigned)(s_incl[mid] & 0xffffffffull) > k) hi = mid; else lo = mid + 1;
+            }
+            const unsigned before = lo ? (unsigned)(s_incl[lo - 1] & 0xffffffffull) : 0u;
+            const unsigned local = k - before;
+            const unsigned ntx = s_nt[lo][0], nty = s_nt[lo][1];
+            const unsigned dx = local % ntx, rest = local / ntx;
+            const unsigned dy = rest % nty, dz = rest / nty;
+            // z-major tile index (voxelize.hpp:98-101): ((tz * ny) + ty) * nx + tx
+            const unsigned tile = ((s_t0[lo][2] + dz) * (unsigned)v.ntiles[1] + (s_t0[lo][1] + dy)) *
+                                      (unsigned)v.ntiles[0] + (s_t0[lo][0] + dx);
+            const unsigned long long pos = (unsigned long long)P0 + k;
+            if (pos < a.pair_cap) {
+                a.keys[pos] = tile;
+                a.vals[pos] = chunk * 256 + lo;
+                if (a.passes > 0) {
+                    const uint64_t st = pos / kSortTile;
+                    atomicAdd(&a.tile_hist0[st * (dmask + 1) + (tile & dmask)], 1u);
+                    atomicAdd(&a.tile_hist0[(a.sort_tiles_cap + st / kSuperTiles) * (dmask + 1) + (tile & dmask)], 1u);
+                }
+                for (int ps = 0; ps < a.passes; ++ps)
+                    atomicAdd(&s_hist[ps][(tile >> (a.digit_bits * ps)) & dmask], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (int ps = 0; ps < a.passes; ++ps)
+        for (unsigned d = tid; d <= dmask; d += 256) {
+            const unsigned c = s_hist[ps][d];
+            if (c) atomicAdd(&a.hist[ps * kMaxBuckets + d], c);
+        }
+}
+
+// voxelize_backward stage 3 (voxelize.hpp:217-232): merge per-tile sums in
+// tile order, dL/dSigma = sym(-Sigma^-1 dL/dSigma^-1 Sigma^-1), world chain.
+__global__ void __launch_bounds__(128) k_vchain(const VoxChainLaunch a) {
+    const unsigned S = a.ctrl->survivors;
+    for (unsigned slot = blockIdx.x * blockDim.x + threadIdx.x; slot < S;
+         slot += gridDim.x * blockDim.x) {
+        const uint32_t i = a.survivor_list[slot];
+        const VoxRecord rec = a.records[i];
+        unsigned np = 1;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) np *= (unsigned)(rec.hi[d] / a.v.tile[d] - rec.lo[d] / a.v.tile[d] + 1);
+        double acc[10];
+#pragma unroll
+        for (int j = 0; j < 10; ++j) acc[j] = 0.0;
+        const float* part = a.partials + 10ull * rec.pair_base;
+        for (unsigned k = 0; k < np; ++k)
+#pragma unroll
+            for (int j = 0; j < 10; ++j) acc[j] += (double)part[10 * k + j];
         float pf[11];
         load_params(a.params, a.cap, i, pf);
         double pd[11];
 #pragma unroll
         for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
-        Focus f;
-        focus_prepare(pd, a.slice, f);  // deterministic: same state as K_exact
-        const unsigned ntx = rec.hi_x / kTile - rec.lo_x / kTile + 1;
-        const unsigned nty = rec.hi_y / kTile - rec.lo_y / kTile + 1;
-        const unsigned np = ntx * nty;
-        // stage-2 merge in tile order (backward.hpp:141-145)
-        double acc[6] = {0, 0, 0, 0, 0, 0};
-        const float* part = a.partials + 6ull * rec.pair_base;
-        for (unsigned k = 0; k < np; ++k) {
+        D33 sigma, rot, inv;
+        D3 scale;
+        world_covariance(pd, a.v.mod, sigma, rot, scale);
+        invert_cov(sigma, scale, a.v.mod, inv);
+        D33 dA;
+        dA.m[0][0] = acc[4];
+        dA.m[1][1] = acc[5];
+        dA.m[2][2] = acc[6];
+        dA.m[0][1] = dA.m[1][0] = acc[7];
+        dA.m[0][2] = dA.m[2][0] = acc[8];
+        dA.m[1][2] = dA.m[2][1] = acc[9];
+        D33 ds = m33_scale(m33_mul(m33_mul(inv, dA), inv), -1.0);
+        ds = m33_scale(m33_add(ds, m33_t(ds)), 0.5);
+        double d_ls[3], d_q[4];
+        chain_world(pd, ds, a.v.mod, d_ls, d_q);
+        const double alpha = 1.0 / (1.0 + exp(-pd[10]));
+        float g[11] = {(float)acc[1], (float)acc[2], (float)acc[3], (float)d_ls[0], (float)d_ls[1],
+                       (float)d_ls[2], (float)d_q[0], (float)d_q[1], (float)d_q[2], (float)d_q[3],
+                       (float)(acc[0] * (alpha * (1.0 - alpha)))};
+        if (!isfinite(g[10] + g[0] + g[3] + g[6])) record_error(a.err, kErrNumeric, i);  // voxelize.hpp:234-238
 #pragma unroll
-            for (int j = 0; j < 6; ++j) acc[j] += (double)part[6 * k + j];
-        }
-        double g[11];
-        D3 dl_dmu;
-        focus_backward(pd, f, acc, a.slice, g, dl_dmu);
-        const bool finite = isfinite(g[10]) && isfinite(g[0] + g[1] + g[2]) &&
-                            isfinite(g[3] + g[4] + g[5]) && isfinite(g[6] + g[7] + g[8] + g[9]);
-        if (!finite) record_error(a.err, kErrNumeric, i);
-#pragma unroll
-        for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = (float)g[k];
-        if (a.stat_norm) a.stat_norm[i] = (float)sqrt(acc[1] * acc[1] + acc[2] * acc[2]);
-        if (a.stat_observed) a.stat_observed[i] = 1;
-        if (a.stat_world) {
-            a.stat_world[3ull * i + 0] = (float)dl_dmu.x;
-            a.stat_world[3ull * i + 1] = (float)dl_dmu.y;
-            a.stat_world[3ull * i + 2] = (float)dl_dmu.z;
-        }
+        for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = g[k];
     }
 }
 
 }  // namespace
+
+void launch_vox_prep(const VoxPrepLaunch& a, cudaStream_t st) {
+    if (a.n) k_vprep<<<a.grid, 256, 0, st>>>(a);
+}
+
+void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st) {
+    k_vchain<<<grid, 128, 0, st>>>(a);
+}
 
 int exact_blocks_per_sm(size_t dyn_smem) {
     int nb = 0;
@@ -362,15 +752,24 @@ int exact_blocks_per_sm(size_t dyn_smem) {
 
 size_t exact_dyn_smem(unsigned nfilter) { return (size_t)(nfilter + 1) * sizeof(unsigned); }
 
-void launch_filter(const PrepLaunch& a, cudaStream_t st) {
+void launch_filter(const PrepLaunch& a, int num_sms, cudaStream_t st) {
     if (a.n == 0) return;
     const bool filter_on = a.slice.tau > 0.0 && a.slice.mod > 1e-10 && a.slice.mod < 1e10 &&
                            a.slice.sigma_z > 1e-10 && a.slice.sigma_z < 1e10;
     const float log_tau = filter_on ? (float)log(a.slice.tau) : 0.f;
+    const int smem = 12 * kFilterBlock * (int)sizeof(float);
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaFuncSetAttribute(k_filter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_filter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<true>, kPrepThreads, smem);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const unsigned grid = (unsigned)std::min<uint64_t>(a.nfilter, (uint64_t)num_sms * per_sm);
     if (a.grads)
-        k_filter<true><<<a.nfilter, kPrepThreads, 0, st>>>(a, log_tau, filter_on ? 1 : 0);
+        k_filter<true><<<grid, kPrepThreads, smem, st>>>(a, log_tau, filter_on ? 1 : 0, a.nfilter);
     else
-        k_filter<false><<<a.nfilter, kPrepThreads, 0, st>>>(a, log_tau, filter_on ? 1 : 0);
+        k_filter<false><<<grid, kPrepThreads, smem, st>>>(a, log_tau, filter_on ? 1 : 0, a.nfilter);
 }
 
 void launch_exact(const PrepLaunch& a, cudaStream_t st) {
@@ -388,6 +787,7 @@ void launch_exact(const PrepLaunch& a, cudaStream_t st) {
 
 void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st) {
     k_chain<<<grid, 128, 0, st>>>(a);
+    k_chain_exact<<<std::max(1, grid / 8), 128, 0, st>>>(a);
 }
 
 }  // namespace gpk

@@ -75,7 +75,8 @@ struct PrepState {
     SliceArgs slice{};
     int tiles = 0;
     int passes = 0;
-    int final_buf = 0;          // which key/val buffer holds the sorted pairs
+    int digit_bits = 0;
+    int final_buf = 0;         // which key/val buffer holds the sorted pairs
     bool rasterized = false;
     bool grads_zeroed = false;  // K_prep zero-filled non-survivor gradients
     gpk_slice_pose pose{};
@@ -93,6 +94,7 @@ struct gpk_session {
     gpk_bounds bbox{};
     uint64_t pair_cap = 0;
     uint64_t sort_tiles_cap = 0;
+    uint64_t hist_region = 0;  // words per radix pass in sort_status
 
     DevBuf params, grads, adam_m, adam_v, records, survivors;
     DevBuf keys[2], vals[2], partials, sort_status;  // sort_status: per-sort-tile digit counts
@@ -106,6 +108,22 @@ struct gpk_session {
     int img_w = 0, img_h = 0;
 
     PrepState prep;
+
+    // voxelizer state (last voxelize / voxelize_backward)
+    struct VoxState {
+        bool valid = false;
+        VoxArgs v{};
+        uint64_t tiles = 0, voxels = 0;
+        int passes = 0, digit_bits = 0, final_buf = 0;
+    } vox;
+    DevBuf vox_records, volume, dl_dv_vol, vox_partials;
+
+    // captured step graphs (executable graph + the prepared state it leaves)
+    struct Graph {
+        cudaGraphExec_t exec;
+        PrepState prep;
+    };
+    std::vector<Graph> graphs;
 
     // live stage timing
     bool timing = false;
@@ -127,10 +145,10 @@ struct gpk_session {
     double* loss() { return reinterpret_cast<double*>(persist.as<char>() + 88); }
     Control* ctrl() { return head.as<Control>(); }
     unsigned* hist() { return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control)); }
-    unsigned* prev_sort_tiles() { return reinterpret_cast<unsigned*>(persist.as<char>() + 96); }
+    unsigned* prev_sort_words() { return reinterpret_cast<unsigned*>(persist.as<char>() + 96); }
     unsigned* filter_flags() {
         return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control) +
-                                           kMaxSortPasses * 256 * sizeof(unsigned));
+                                           kMaxSortPasses * kMaxBuckets * sizeof(unsigned));
     }
 };
 
@@ -198,7 +216,7 @@ uint64_t exact_chunks(uint64_t n) { return std::max<uint64_t>((n + kExactChunk -
 // head = Control | global digit histograms | K_exact chunk words (u64)
 size_t head_size(uint64_t nbf, uint64_t nbe) {
     (void)nbf;
-    return sizeof(Control) + kMaxSortPasses * 256 * sizeof(unsigned) + nbe * 8;
+    return sizeof(Control) + kMaxSortPasses * kMaxBuckets * sizeof(unsigned) + nbe * 8;
 }
 
 int clear_errors(gpk_session* s) {
@@ -256,12 +274,14 @@ int ensure_pairs(gpk_session* s, uint64_t need) {
     // per-sort-tile digit counts of every pass (kept zero between prepares:
     // K_filter clears the rows the previous prepare used)
     const uint64_t st_tiles = (cap + kSortTile - 1) / kSortTile;
-    const size_t st_bytes = (size_t)kMaxSortPasses * st_tiles * 256 * 4;
-    CK(s->sort_status.ensure(st_bytes));
+    const uint64_t super_tiles = (st_tiles + kSuperTiles - 1) / kSuperTiles;
+    const uint64_t region = (st_tiles + super_tiles) * kMaxBuckets;
+    CK(s->sort_status.ensure((size_t)kMaxSortPasses * region * 4));
     CK(cudaMemsetAsync(s->sort_status.p, 0, s->sort_status.bytes, s->stream));
-    CK(cudaMemsetAsync(s->prev_sort_tiles(), 0, 4, s->stream));
+    CK(cudaMemsetAsync(s->prev_sort_words(), 0, 8, s->stream));
     s->pair_cap = cap;
     s->sort_tiles_cap = st_tiles;
+    s->hist_region = region;
     return GPK_OK;
 }
 
@@ -306,6 +326,8 @@ int make_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     for (int i = 0; i < 3; ++i) a.t[i] = pose->translation[i];
     a.sx = pose->pixel_spacing[0];
     a.sy = pose->pixel_spacing[1];
+    a.inv_sx = 1.0 / a.sx;
+    a.inv_sy = 1.0 / a.sy;
     a.ppx = pose->principal_point[0];
     a.ppy = pose->principal_point[1];
     a.sigma_z = psf->sigma_z;
@@ -320,11 +342,15 @@ int make_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     return GPK_OK;
 }
 
-int sort_passes(int tiles) {
+// Radix plan for the tile key: passes of equal width <= kMaxDigitBits.
+void sort_plan(int tiles, int& passes, int& digit_bits) {
     int bits = 0;
     while (bits < 32 && (1ull << bits) < (unsigned long long)tiles) ++bits;
-    return (bits + 7) / 8;
+    passes = (bits + kMaxDigitBits - 1) / kMaxDigitBits;
+    digit_bits = passes ? (bits + passes - 1) / passes : 0;
 }
+
+int launch_sorts(gpk_session* s, int passes, int digit_bits);
 
 int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                 const gpk_raster_config* cfg, bool zero_grads) {
@@ -335,7 +361,9 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     PrepState& ps = s->prep;
     ps.slice = a;
     ps.tiles = a.tiles_x * a.tiles_y;
-    ps.passes = sort_passes(ps.tiles);
+    if (ps.tiles > (1 << (kMaxDigitBits * kMaxSortPasses)))
+        return fail(GPK_ERR_INVALID_ARGUMENT, "SlicePose: more than 2^20 tiles unsupported");
+    sort_plan(ps.tiles, ps.passes, ps.digit_bits);
     ps.pose = *pose;
     ps.psf = *psf;
     ps.cfg = *cfg;
@@ -367,15 +395,17 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     pl.tile_hist0 = s->sort_status.as<unsigned>();
     pl.tile_hist_all = s->sort_status.as<unsigned>();
     pl.sort_tiles_cap = s->sort_tiles_cap;
-    pl.prev_sort_tiles = s->prev_sort_tiles();
+    pl.hist_region = s->hist_region;
+    pl.prev_sort_words = s->prev_sort_words();
     pl.passes = ps.passes;
+    pl.digit_bits = ps.digit_bits;
     pl.exact_words = reinterpret_cast<unsigned long long*>(s->filter_flags());
     pl.ctrl = s->ctrl();
     pl.err = s->err();
     pl.slice = a;
     const int exact_per_sm = exact_blocks_per_sm(exact_dyn_smem((unsigned)nbf));
     pl.exact_grid = (int)std::min<uint64_t>(nbe, (uint64_t)s->num_sms * exact_per_sm);
-    launch_filter(pl, s->stream);
+    launch_filter(pl, s->num_sms, s->stream);
     CK(cudaGetLastError());
     scope_prep.end();
     {
@@ -384,29 +414,36 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
         CK(cudaGetLastError());
     }
     StageScope scope_sort(s, GPK_STAGE_SORT);
+    TRY(launch_sorts(s, ps.passes, ps.digit_bits));
+    ps.final_buf = ps.passes & 1;
+    return GPK_OK;
+}
 
-    const int grid = (int)std::min<uint64_t>(s->sort_tiles_cap, (uint64_t)s->num_sms * 2);
-    const uint64_t st_tiles = s->sort_tiles_cap;
-    for (int p = 0; p < ps.passes; ++p) {
+// Stable LSD radix passes over the (key, value) pairs in keys[0]/vals[0].
+int launch_sorts(gpk_session* s, int passes, int digit_bits) {
+    const int grid = (int)std::min<uint64_t>(s->sort_tiles_cap, (uint64_t)s->num_sms * 4);
+    const size_t region = s->hist_region;
+    for (int p = 0; p < passes; ++p) {
         SortLaunch sl;
         sl.keys_in = s->keys[p & 1].as<uint32_t>();
         sl.vals_in = s->vals[p & 1].as<uint32_t>();
         sl.keys_out = s->keys[(p + 1) & 1].as<uint32_t>();
         sl.vals_out = s->vals[(p + 1) & 1].as<uint32_t>();
-        sl.hist = s->hist() + 256 * p;
-        sl.tile_hist = s->sort_status.as<unsigned>() + (size_t)p * st_tiles * 256;
-        sl.tile_hist_next = (p + 1 < ps.passes)
-                                ? s->sort_status.as<unsigned>() + (size_t)(p + 1) * st_tiles * 256
-                                : nullptr;
-        sl.prev_sort_tiles = s->prev_sort_tiles();
-        sl.shift = 8 * p;
+        sl.hist = s->hist() + kMaxBuckets * p;
+        sl.tile_hist = s->sort_status.as<unsigned>() + (size_t)p * region;
+        sl.tile_hist_next = (p + 1 < passes) ? s->sort_status.as<unsigned>() + (size_t)(p + 1) * region
+                                                : nullptr;
+        sl.prev_sort_words = s->prev_sort_words();
+        sl.sort_tiles_cap = s->sort_tiles_cap;
+        sl.shift = digit_bits * p;
+        sl.bits = digit_bits;
+        sl.next_buckets = 1u << digit_bits;
         sl.pass = p;
         sl.ctrl = s->ctrl();
         sl.pair_cap = s->pair_cap;
         launch_sort_pass(sl, grid, s->stream);
         CK(cudaGetLastError());
     }
-    ps.final_buf = ps.passes & 1;
     return GPK_OK;
 }
 
@@ -469,6 +506,8 @@ int run_backward(gpk_session* s, bool stats) {
     c.stat_norm = stats ? s->stat_norm.as<float>() : nullptr;
     c.stat_observed = stats ? s->stat_obs.as<uint8_t>() : nullptr;
     c.stat_world = stats ? s->stat_world.as<float>() : nullptr;
+    c.exact_list = s->cand_list.as<uint32_t>();  // free after K_exact: reused as the deferral list
+    c.exact_count = &s->ctrl()->chain_exact;
     c.err = s->err();
     c.slice = s->prep.slice;
     const int grid = (int)std::min<uint64_t>((s->n + 127) / 128, (uint64_t)s->num_sms * 8);
@@ -521,7 +560,9 @@ int copy_planes_out(gpk_session* s, const float* dev, float* rec) {
 }
 
 int alloc_for_n(gpk_session* s, uint64_t n) {
-    const uint64_t cap = std::max<uint64_t>(n, 1);
+    // plane stride: a multiple of the K_filter chunk, so every chunk's plane
+    // slice is a 4 KB, 16 B-aligned TMA bulk-copy source/destination
+    const uint64_t cap = (std::max<uint64_t>(n, 1) + kFilterBlock - 1) / kFilterBlock * kFilterBlock;
     if (cap > s->cap || !s->params.p) {
         CK(s->params.ensure(cap * 11 * 4));
         CK(s->grads.ensure(cap * 11 * 4));
@@ -615,6 +656,119 @@ int run_loss(gpk_session* s, double lambda, double dssim_scale) {
     return GPK_OK;
 }
 
+
+// ---- voxelizer (voxelize.hpp:16-240) --------------------------------------------
+
+// VoxelizerConfig::validate (voxelize.hpp:24-37) + this backend's index limits.
+int make_vox(gpk_session* s, const gpk_voxelizer_config* cfg, VoxArgs& v) {
+    if (!cfg) return fail(GPK_ERR_INVALID_ARGUMENT, "null voxelizer config");
+    if (cfg->dims[0] < 1 || cfg->dims[1] < 1 || cfg->dims[2] < 1)
+        return fail(GPK_ERR_INVALID_ARGUMENT, "VoxelizerConfig: dims must be >= 1");
+    if (cfg->tile_dims[0] < 1 || cfg->tile_dims[1] < 1 || cfg->tile_dims[2] < 1)
+        return fail(GPK_ERR_INVALID_ARGUMENT, "VoxelizerConfig: tile_dims must be >= 1");
+    if (!(cfg->support_sigmas > 0.0))
+        return fail(GPK_ERR_INVALID_ARGUMENT, "VoxelizerConfig: support_sigmas must be > 0");
+    if (!(cfg->spacing[0] > 0.0) || !(cfg->spacing[1] > 0.0) || !(cfg->spacing[2] > 0.0))
+        return fail(GPK_ERR_INVALID_ARGUMENT, "VoxelizerConfig: spacing must be positive");
+    const uint64_t voxels = (uint64_t)cfg->dims[0] * cfg->dims[1] * cfg->dims[2];
+    if (voxels > (1ull << 31)) return fail(GPK_ERR_INVALID_ARGUMENT, "VoxelizerConfig: refusing > 2^31 voxels");
+    if (cfg->dims[0] > 65535 || cfg->dims[1] > 65535 || cfg->dims[2] > 65535)
+        return fail(GPK_ERR_INVALID_ARGUMENT, "VoxelizerConfig: dims above 65535 unsupported");
+    if (s->n > 0 && !(cfg->scale_modifier > 0.0))
+        return fail(GPK_ERR_INVALID_ARGUMENT, "covariance_from_scale_rotation: scale and mod must be > 0", 0);
+    memset(&v, 0, sizeof v);
+    uint64_t tiles = 1;
+    for (int d = 0; d < 3; ++d) {
+        v.dims[d] = cfg->dims[d];
+        v.tile[d] = std::min(cfg->tile_dims[d], cfg->dims[d]);  // same tiling, fewer empty lanes
+        v.ntiles[d] = (cfg->dims[d] + cfg->tile_dims[d] - 1) / cfg->tile_dims[d];
+        v.spacing[d] = cfg->spacing[d];
+        v.origin[d] = cfg->origin[d];
+        tiles *= (uint64_t)v.ntiles[d];
+    }
+    if (tiles > (1ull << (kMaxDigitBits * kMaxSortPasses)))
+        return fail(GPK_ERR_INVALID_ARGUMENT, "VoxelizerConfig: more than 2^20 voxel tiles unsupported");
+    v.support = cfg->support_sigmas;
+    v.mod = cfg->scale_modifier;
+    return GPK_OK;
+}
+
+// prepare_voxel_prims + VoxelTiles (voxelize.hpp:52-105): records, survivor
+// list, (tile, primitive) pairs sorted stably by tile.
+int run_vox_prep(gpk_session* s, const gpk_voxelizer_config* cfg) {
+    VoxArgs v;
+    TRY(make_vox(s, cfg, v));
+    if (!s->keys[0].p) TRY(ensure_pairs(s, std::max<uint64_t>(1ull << 20, 8 * s->n)));
+    s->prep.valid = false;  // the pair buffers now hold voxel tiles
+    s->prep.rasterized = false;
+    auto& vs = s->vox;
+    vs.v = v;
+    vs.tiles = (uint64_t)v.ntiles[0] * v.ntiles[1] * v.ntiles[2];
+    vs.voxels = (uint64_t)v.dims[0] * v.dims[1] * v.dims[2];
+    sort_plan((int)vs.tiles, vs.passes, vs.digit_bits);
+    vs.final_buf = vs.passes & 1;
+    vs.valid = true;
+    CK(s->vox_records.ensure(s->cap * sizeof(VoxRecord)));
+    CK(s->volume.ensure(vs.voxels * 4));
+    CK(s->dl_dv_vol.ensure(vs.voxels * 4));
+    StageScope scope(s, GPK_STAGE_VOXEL);
+    CK(cudaMemsetAsync(s->head.p, 0, head_size(filter_blocks(s->n), exact_chunks(s->n)), s->stream));
+    // the slice path clears only the histogram rows its previous sort used
+    CK(cudaMemsetAsync(s->sort_status.p, 0, s->sort_status.bytes, s->stream));
+    if (s->n == 0) return GPK_OK;
+    VoxPrepLaunch p;
+    p.params = s->params.as<float>();
+    p.cap = s->cap;
+    p.n = (uint32_t)s->n;
+    p.records = s->vox_records.as<VoxRecord>();
+    p.survivor_list = s->survivors.as<uint32_t>();
+    p.keys = s->keys[0].as<uint32_t>();
+    p.vals = s->vals[0].as<uint32_t>();
+    p.pair_cap = s->pair_cap;
+    p.hist = s->hist();
+    p.tile_hist0 = s->sort_status.as<unsigned>();
+    p.sort_tiles_cap = s->sort_tiles_cap;
+    p.passes = vs.passes;
+    p.digit_bits = vs.digit_bits;
+    p.chunk_words = reinterpret_cast<unsigned long long*>(s->filter_flags());
+    p.ctrl = s->ctrl();
+    p.err = s->err();
+    p.v = v;
+    p.grid = (int)std::min<uint64_t>(exact_chunks(s->n), (uint64_t)s->num_sms * 4);
+    launch_vox_prep(p, s->stream);
+    CK(cudaGetLastError());
+    TRY(launch_sorts(s, vs.passes, vs.digit_bits));
+    return GPK_OK;
+}
+
+VoxEvalLaunch vox_eval_args(gpk_session* s) {
+    VoxEvalLaunch e;
+    e.records = s->vox_records.as<VoxRecord>();
+    e.keys = s->keys[s->vox.final_buf].as<uint32_t>();
+    e.vals = s->vals[s->vox.final_buf].as<uint32_t>();
+    e.ctrl = s->ctrl();
+    e.pair_cap = s->pair_cap;
+    e.volume = s->volume.as<float>();
+    e.dl_dv = s->dl_dv_vol.as<float>();
+    e.partials = s->vox_partials.as<float>();
+    e.v = s->vox.v;
+    e.dl_global = (size_t)e.v.tile[0] * e.v.tile[1] * e.v.tile[2] * 4 > 96 * 1024 ? 1 : 0;
+    return e;
+}
+
+// Prepare; on pair overflow grow the pair buffers and prepare again.
+int vox_prep_settled(gpk_session* s, const gpk_voxelizer_config* cfg) {
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        TRY(run_vox_prep(s, cfg));
+        TRY(sync_and_check(s, "voxelize"));
+        Control c;
+        CK(cudaMemcpy(&c, s->ctrl(), sizeof c, cudaMemcpyDeviceToHost));
+        if (!c.pair_overflow) return GPK_OK;
+        TRY(ensure_pairs(s, (uint64_t)c.pairs + c.pairs / 4 + 1024));
+    }
+    return fail(GPK_ERR_STATE, "voxel pair capacity still exceeded after growth");
+}
+
 }  // namespace
 
 extern "C" {
@@ -680,11 +834,14 @@ int gpk_session_destroy(gpk_session* s) {
     if (!s) return ok();
     cudaSetDevice(s->device);
     if (s->stream) cudaStreamSynchronize(s->stream);
+    for (auto& g : s->graphs) cudaGraphExecDestroy(g.exec);
+    s->graphs.clear();
     DevBuf* bufs[] = {&s->params, &s->grads, &s->adam_m, &s->adam_v, &s->records, &s->survivors,
                       &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials,
                       &s->sort_status, &s->head, &s->prep_vals, &s->persist, &s->image,
                       &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm,
-                      &s->stat_obs, &s->stat_world, &s->cand_list};
+                      &s->stat_obs, &s->stat_world, &s->cand_list, &s->vox_records,
+                      &s->volume, &s->dl_dv_vol, &s->vox_partials};
     for (DevBuf* b : bufs) b->release();
     drain_timing(s);
     for (cudaEvent_t e : s->event_pool) cudaEventDestroy(e);
@@ -747,6 +904,8 @@ int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
         case GPK_BUF_DL_DI: p = s->dl_di.p; b = px * 4; break;
         case GPK_BUF_TARGET: p = s->target.p; b = px * 4; break;
         case GPK_BUF_LOSS: p = s->loss(); b = 8; break;
+        case GPK_BUF_VOLUME: p = s->volume.p; b = s->vox.voxels * 4; break;
+        case GPK_BUF_DL_DV: p = s->dl_dv_vol.p; b = s->vox.voxels * 4; break;
         default: return fail(GPK_ERR_INVALID_ARGUMENT, "unknown or unallocated buffer");
     }
     *ptr = p;
@@ -885,7 +1044,7 @@ int gpk_get_prepared(gpk_session* s, uint32_t* index, int32_t* bounds, double* f
                   cudaMemcpyDeviceToHost));
     for (uint64_t k = 0; k < S; ++k) {
         const SurvivorRecord& r = recs[list[k]];
-        if (index) index[k] = r.gidx;
+        if (index) index[k] = r.gidx & 0x7fffffffu;  // bit 31: decided on the fp64 path
         if (bounds) {
             bounds[4 * k + 0] = r.lo_x;
             bounds[4 * k + 1] = r.hi_x;
@@ -928,7 +1087,7 @@ int gpk_get_tile_lists(gpk_session* s, uint32_t* offsets, uint32_t* entries) {
         }
     }
     if (entries)
-        for (uint64_t k = 0; k < T; ++k) entries[k] = recs[vals[k]].gidx;
+        for (uint64_t k = 0; k < T; ++k) entries[k] = recs[vals[k]].gidx & 0x7fffffffu;
     return ok();
 }
 
@@ -1098,6 +1257,94 @@ int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* ps
     return ok();
 }
 
+// ---- CUDA graphs -------------------------------------------------------------
+static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_session*, const void*),
+                         const void* arg) {
+    if (!s || !graph_id) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (s->timing) return fail(GPK_ERR_STATE, "disable stage timing before capturing a graph");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    const int st = body(s, arg);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(s->stream, &g);
+    if (st != GPK_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+    }
+    if (e != cudaSuccess) return fail(GPK_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) return fail(GPK_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+    s->graphs.push_back({ex, s->prep});
+    *graph_id = (int32_t)s->graphs.size() - 1;
+    return ok();
+}
+
+struct FwdBwdArgs {
+    const gpk_slice_pose* pose;
+    const gpk_psf* psf;
+    const gpk_raster_config* cfg;
+};
+
+struct TrainArgs {
+    const gpk_slice_pose* pose;
+    const gpk_psf* psf;
+    const gpk_raster_config* cfg;
+    double lambda, dssim;
+    const gpk_learning_rates* lr0;
+    int total;
+};
+
+int gpk_graph_capture_fwd_bwd(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                              const gpk_raster_config* cfg, int32_t* graph_id) {
+    const FwdBwdArgs args{pose, psf, cfg};
+    return capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
+        const FwdBwdArgs* a = static_cast<const FwdBwdArgs*>(p);
+        TRY(run_prepare(ss, a->pose, a->psf, a->cfg, true));
+        TRY(run_rasterize(ss));
+        TRY(run_backward(ss, false));
+        return GPK_OK;
+    }, &args);
+}
+
+int gpk_graph_capture_train(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                            const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                            const gpk_learning_rates* lr0, int32_t total_iterations,
+                            int32_t* graph_id) {
+    if (!lr0 || total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "bad learning rates");
+    const TrainArgs args{pose, psf, cfg, lambda, dssim_scale, lr0, total_iterations};
+    return capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
+        const TrainArgs* a = static_cast<const TrainArgs*>(p);
+        TRY(run_prepare(ss, a->pose, a->psf, a->cfg, true));
+        TRY(run_rasterize(ss));
+        TRY(run_loss(ss, a->lambda, a->dssim));
+        TRY(run_backward(ss, false));
+        const double lr[4] = {a->lr0->position, a->lr0->opacity, a->lr0->scale, a->lr0->rotation};
+        TRY(run_adam(ss, lr, true, a->total, nullptr));
+        return GPK_OK;
+    }, &args);
+}
+
+int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
+    if (!s || graph_id < 0 || graph_id >= (int32_t)s->graphs.size())
+        return fail(GPK_ERR_INVALID_ARGUMENT, "unknown graph id");
+    TRY(set_device(s));
+    CK(cudaGraphLaunch(s->graphs[graph_id].exec, s->stream));
+    s->prep = s->graphs[graph_id].prep;
+    return ok();
+}
+
+int gpk_graph_destroy_all(gpk_session* s) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    for (auto& g : s->graphs) cudaGraphExecDestroy(g.exec);
+    s->graphs.clear();
+    return ok();
+}
+
 // ---- multi-GPU (NCCL loaded lazily so the library has no hard dependency) ----
 struct NcclId {
     char internal[128];  // ncclUniqueId, passed by value
@@ -1183,6 +1430,88 @@ int gpk_allreduce_grads(gpk_session* s) {
     const int r = api->all_reduce(s->grads.p, s->grads.p, s->cap * 11, /*ncclFloat32*/ 7,
                                   /*ncclSum*/ 0, comm, s->stream);
     if (r != 0) return fail(GPK_ERR_NCCL, "ncclAllReduce failed");
+    return ok();
+}
+
+
+// ---- voxelizer ------------------------------------------------------------------
+
+int gpk_voxelize(gpk_session* s, const gpk_voxelizer_config* cfg, float* volume_out) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    TRY(vox_prep_settled(s, cfg));
+    {
+        StageScope scope(s, GPK_STAGE_VOXEL);
+        launch_vox_eval(vox_eval_args(s), s->stream);
+        CK(cudaGetLastError());
+    }
+    if (volume_out) {
+        CK(cudaMemcpyAsync(volume_out, s->volume.p, s->vox.voxels * 4, cudaMemcpyDeviceToHost, s->stream));
+        TRY(sync_and_check(s, "voxelize"));
+    }
+    return ok();
+}
+
+int gpk_voxel_tile_count(gpk_session* s, uint64_t* tiles, uint64_t* instances) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    if (!s->vox.valid) return fail(GPK_ERR_STATE, "no voxelized volume");
+    TRY(set_device(s));
+    TRY(sync_and_check(s, "voxelize"));
+    Control c;
+    CK(cudaMemcpy(&c, s->ctrl(), sizeof c, cudaMemcpyDeviceToHost));
+    if (tiles) *tiles = s->vox.tiles;
+    if (instances) *instances = s->n ? c.pairs : 0;
+    return ok();
+}
+
+int gpk_get_voxel_tile_lists(gpk_session* s, uint32_t* offsets, uint32_t* entries) {
+    uint64_t T = 0, P = 0;
+    TRY(gpk_voxel_tile_count(s, &T, &P));
+    std::vector<uint32_t> keys(P);
+    if (P) CK(cudaMemcpy(keys.data(), s->keys[s->vox.final_buf].p, P * 4, cudaMemcpyDeviceToHost));
+    if (offsets) {
+        uint64_t k = 0;
+        for (uint64_t t = 0; t <= T; ++t) {
+            while (k < P && keys[k] < (uint32_t)t) ++k;
+            offsets[t] = (uint32_t)k;
+        }
+    }
+    // values are set indices already (ascending within a tile, as the
+    // reference's survivor order, voxelize.hpp:93-103)
+    if (entries && P) CK(cudaMemcpy(entries, s->vals[s->vox.final_buf].p, P * 4, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+int gpk_voxelize_backward(gpk_session* s, const gpk_voxelizer_config* cfg, const float* dl_dv,
+                          float* grads_out) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    TRY(vox_prep_settled(s, cfg));
+    Control c;
+    CK(cudaMemcpy(&c, s->ctrl(), sizeof c, cudaMemcpyDeviceToHost));
+    CK(s->vox_partials.ensure(std::max<uint64_t>(c.pairs, 1) * 40));
+    if (dl_dv)
+        CK(cudaMemcpyAsync(s->dl_dv_vol.p, dl_dv, s->vox.voxels * 4, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
+    if (s->n) {
+        StageScope scope(s, GPK_STAGE_VOXEL);
+        launch_vox_bwd(vox_eval_args(s), s->stream);
+        CK(cudaGetLastError());
+        VoxChainLaunch ch;
+        ch.params = s->params.as<float>();
+        ch.cap = s->cap;
+        ch.records = s->vox_records.as<VoxRecord>();
+        ch.survivor_list = s->survivors.as<uint32_t>();
+        ch.partials = s->vox_partials.as<float>();
+        ch.ctrl = s->ctrl();
+        ch.grads = s->grads.as<float>();
+        ch.err = s->err();
+        ch.v = s->vox.v;
+        launch_vox_chain(ch, (int)std::min<uint64_t>((s->n + 127) / 128, (uint64_t)s->num_sms * 8), s->stream);
+        CK(cudaGetLastError());
+    }
+    TRY(sync_and_check(s, "voxelize_backward"));
+    if (grads_out && s->n) TRY(copy_planes_out(s, s->grads.as<float>(), grads_out));
     return ok();
 }
 

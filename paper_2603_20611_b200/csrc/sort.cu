@@ -1,18 +1,19 @@
 // sort.cu — hand-written stable LSD radix sort of (tile key, candidate slot)
-// pairs, one kernel per 8-bit digit.
+// pairs, one kernel per digit of up to kMaxDigitBits bits (one pass for up to
+// 1024 tiles = a 512x512 slice, two passes up to 2^20 tiles).
 //
 // Stability is the whole point: pairs arrive in ascending candidate slot
 // (= set order), so a stable sort by tile reproduces the reference's per-tile
 // lists in ascending prepared index (render.hpp:151-157) bit-exactly.
 //
 // Wait-free passes: the producer of a pass's input (K_exact for pass 0, pass p
-// for pass p+1) also counts, per 2048-key sort tile, how many keys carry each
-// digit value. A sort CTA therefore knows its output offsets up front —
+// for pass p+1) also counts, per kSortTile-key sort tile, how many keys carry
+// each digit value. A sort CTA therefore knows its output offsets up front —
 // global digit base (exclusive scan of the global histogram) + the column sum
 // of the per-tile histograms of all earlier tiles (coalesced L2 reads) — and
-// never waits on another CTA. Inside a tile, warp w owns a contiguous 256-key
-// segment processed in 8 rounds of 32; ranks within a round come from
-// __match_any_sync, so the tile-local order is the input order.
+// never waits on another CTA. Inside a tile, warp w owns a contiguous segment
+// processed in rounds of 32; ranks within a round come from __match_any_sync,
+// so the tile-local order is the input order.
 #include "common.cuh"
 
 namespace gpk {
@@ -20,49 +21,63 @@ namespace gpk {
 namespace {
 
 __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) {
-    __shared__ unsigned s_whist[8][256];
-    __shared__ unsigned s_part[8][256];
-    __shared__ unsigned s_dbase[256];
-    __shared__ unsigned s_wsum[8];
+    __shared__ unsigned s_whist[8][kMaxBuckets];   // per-warp digit counts -> offsets
+    __shared__ unsigned s_base[kMaxBuckets];       // digit base for this tile
+    __shared__ unsigned s_wsum[32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
     const unsigned ntiles = (P + kSortTile - 1) / kSortTile;
-
-    // global digit base: exclusive scan of this pass's histogram
-    {
-        const unsigned v = a.hist[tid];
-        unsigned incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
-        }
-        if (lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        unsigned add = 0;
-        for (int w = 0; w < warp; ++w) add += s_wsum[w];
-        s_dbase[tid] = incl - v + add;
+    const unsigned nb = 1u << a.bits;
+    const unsigned mask = nb - 1;
+    if (blockIdx.x == 0 && tid == 0 && !a.tile_hist_next) {
+        a.prev_sort_words[0] = ntiles;
+        a.prev_sort_words[1] = nb;
     }
-    if (blockIdx.x == 0 && tid == 0 && !a.tile_hist_next) *a.prev_sort_tiles = ntiles;
+    const unsigned* super_rows = a.tile_hist + a.sort_tiles_cap * nb;
 
     for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        // ---- offsets of earlier tiles: warp w sums rows j = w, w+8, ... < t
+        // ---- global digit base: exclusive scan of the histogram (nb <= 1024)
         {
-            unsigned acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            const uint4* rows = reinterpret_cast<const uint4*>(a.tile_hist);
-            for (unsigned j = warp; j < t; j += 8) {
-                const uint4 x = rows[(size_t)j * 64 + lane * 2];
-                const uint4 y = rows[(size_t)j * 64 + lane * 2 + 1];
-                acc[0] += x.x; acc[1] += x.y; acc[2] += x.z; acc[3] += x.w;
-                acc[4] += y.x; acc[5] += y.y; acc[6] += y.z; acc[7] += y.w;
+            constexpr int kPer = kMaxBuckets / kSortThreads;  // 4 digits per thread
+            unsigned v[kPer], run = 0;
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const unsigned d = tid * kPer + i;
+                v[i] = d < nb ? a.hist[d] : 0u;
+                run += v[i];
             }
+            unsigned incl = run;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) s_part[warp][lane * 8 + i] = acc[i];
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            unsigned ex = incl - run;
+            for (int w = 0; w < warp; ++w) ex += s_wsum[w];
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const unsigned d = tid * kPer + i;
+                s_base[d] = ex;
+                ex += v[i];
+            }
+            for (int w = 0; w < 8; ++w)
+                for (unsigned d = tid; d < nb; d += kSortThreads) s_whist[w][d] = 0;
+            __syncthreads();
         }
-#pragma unroll
-        for (int w = 0; w < 8; ++w) s_whist[w][tid] = 0;
-        __syncthreads();
+        // ---- add the counts of all earlier tiles: whole super-tiles from the
+        // super rows, then the earlier tiles of this super-tile (<= 15 rows)
+        {
+            const unsigned sup = t / kSuperTiles;
+            for (unsigned d = tid; d < nb; d += kSortThreads) {
+                unsigned acc = 0;
+                for (unsigned j = 0; j < sup; ++j) acc += super_rows[(size_t)j * nb + d];
+                for (unsigned j = sup * kSuperTiles; j < t; ++j) acc += a.tile_hist[(size_t)j * nb + d];
+                s_base[d] += acc;
+            }
+        }
 
         // ---- rank: warp-local stable ranks via match_any -----------------
         uint32_t key[kSortItems], val[kSortItems];
@@ -74,7 +89,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
             const bool valid = idx < P;
             key[r] = valid ? a.keys_in[idx] : 0xffffffffu;
             val[r] = valid ? a.vals_in[idx] : 0u;
-            const unsigned d = valid ? ((key[r] >> a.shift) & 255u) : 256u;
+            const unsigned d = valid ? ((key[r] >> a.shift) & mask) : 0xffffffffu;
             const unsigned peers = __match_any_sync(0xffffffffu, d);
             unsigned prior = 0;
             if (valid) prior = s_whist[warp][d];
@@ -85,15 +100,13 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
         }
         __syncthreads();
 
-        // ---- per digit: base = global digit base + earlier tiles; warp prefixes
-        {
-            unsigned base = s_dbase[tid];
-#pragma unroll
-            for (int w = 0; w < 8; ++w) base += s_part[w][tid];
+        // ---- per digit: exclusive prefix over warps on top of the tile base
+        for (unsigned d = tid; d < nb; d += kSortThreads) {
+            unsigned base = s_base[d];
 #pragma unroll
             for (int w = 0; w < 8; ++w) {
-                const unsigned c = s_whist[w][tid];
-                s_whist[w][tid] = base;
+                const unsigned c = s_whist[w][d];
+                s_whist[w][d] = base;
                 base += c;
             }
         }
@@ -104,12 +117,16 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
         for (int r = 0; r < kSortItems; ++r) {
             const unsigned idx = seg + r * 32 + lane;
             if (idx < P) {
-                const unsigned d = (key[r] >> a.shift) & 255u;
+                const unsigned d = (key[r] >> a.shift) & mask;
                 const unsigned pos = s_whist[warp][d] + rank[r];
                 a.keys_out[pos] = key[r];
                 a.vals_out[pos] = val[r];
-                if (a.tile_hist_next)
-                    atomicAdd(&a.tile_hist_next[(pos / kSortTile) * 256 + ((key[r] >> (a.shift + 8)) & 255u)], 1u);
+                if (a.tile_hist_next) {
+                    const unsigned nd = (key[r] >> (a.shift + a.bits)) & (a.next_buckets - 1);
+                    const unsigned st = pos / kSortTile;
+                    atomicAdd(&a.tile_hist_next[(size_t)st * a.next_buckets + nd], 1u);
+                    atomicAdd(&a.tile_hist_next[(a.sort_tiles_cap + st / kSuperTiles) * a.next_buckets + nd], 1u);
+                }
             }
         }
         __syncthreads();

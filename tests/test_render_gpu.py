@@ -225,6 +225,30 @@ def test_fused_u1_equals_staged(gp, session):
     assert np.array_equal(session.rasterize(), img)
 
 
+def test_graph_replay_equals_direct(gp, session):
+    """A captured CUDA graph of the U1 step reproduces the direct submission bitwise."""
+    from paper_2603_20611_b200 import _native as N
+
+    dims = (128, 128, 32)
+    gs = stack_scene(gp, 20000, dims, seed=5)
+    poses = [gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), k) for k in (9, 10)]
+    dl = (np.random.default_rng(4).uniform(-1, 1, (128, 128)) / 16384).astype(np.float32)
+    session.set_gaussians(gs)
+    session.fwd_bwd_slice(poses[0], gp.PsfSpec(), gp.RasterConfig())
+    session.upload(N.GPK_BUF_DL_DI, dl.ctypes.data, dl.nbytes)
+    direct = []
+    for p in poses:
+        session.fwd_bwd_slice(p, gp.PsfSpec(), gp.RasterConfig())
+        direct.append((session.rasterize(), session.get_gradients()))
+    gids = [session.capture_fwd_bwd(p, gp.PsfSpec(), gp.RasterConfig()) for p in poses]
+    for _ in range(2):
+        for gid, (img, g) in zip(gids, direct):
+            session.graph_launch(gid)
+            assert np.array_equal(session.get_gradients(), g)
+            assert np.array_equal(session.rasterize(), img)
+    session.graph_destroy_all()
+
+
 def test_c2_full_size_bitexact_binning(gp, session, ref):
     """C2 (512^2 x 128, 1M Gaussians): survivors, bounds and tile lists bit-exact;
     image and gradients within tolerance of the reference."""

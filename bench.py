@@ -81,14 +81,14 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(config):
-    """dram__bytes_read+write per K_prep launch from the committed ncu capture."""
+def ncu_traffic(config, kernel):
+    """dram__bytes_read+write per launch of `kernel` from the committed ncu capture."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
         d = json.loads(p.read_text())
-        return d.get(config, {}).get("k_prep", {}).get("dram_bytes_per_launch")
+        return d.get(config, {}).get(kernel, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -352,14 +352,16 @@ def run_ours(args):
         dist.barrier()
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
 
-    # per-kernel device time: the same steps with event pairs around every
-    # stage launch (non-graph submission; events bracket each kernel directly)
+    # per-kernel device time: the same steps through graphs captured with an
+    # event-record node around every stage (device-side timestamps, kernels
+    # back to back as in the timed run; L2 flushed before each step)
     prof_steps = min(args.steps, 100)
-    sess.stage_times(reset=True)
     sess.stage_timing(True)
+    prof_graphs = [sess.capture_fwd_bwd(p, psf, rcfg) for p in poses]
+    sess.stage_times(reset=True)
     for i in range(prof_steps):
         flush.fill_(float(i))
-        step(args.warmup + i, use_graph=False)
+        sess.graph_launch(prof_graphs[(rank + (args.warmup + i) * world) % len(poses)])
     sess.stage_timing(False)
     stages = sess.stage_times(reset=True)
     t = torch.tensor([total_ms], device="cuda")
@@ -401,13 +403,15 @@ def run_ours(args):
     # stored width): N Gaussians, S survivors, T pairs, P px.
     S, T = S_mean, T_mean
     kernel_bytes = {
-        "prepare": ("k_filter", 44 * n + 44 * (n - S),
-                    "44N params read + 44(N-S) gradient zero-fill"),
-        "exact": ("k_exact", 44 * S + 48 * S + 8 * T, "44S params + 48S records + 8T pairs"),
+        "prepare": ("k_prep", 44 * n + 44 * S + 96 * S + 8 * T,
+                    "44N params read + 44S previous-survivor gradient clear + 48S records "
+                    "+ 48S survivor params + 8T pairs"),
+        "bin": ("k_bin", 48 * S + 4 * S + 4 * S + 8 * T, "48S records + 4S survivor slots + 4S pair bases + 8T pairs"),
         "sort": ("k_sort_pass x passes", 16 * T * max(1, sort_passes(X, Y)), "16T per radix pass"),
         "raster": ("k_raster_fwd", 32 * T + 4 * P, "32T + 4P (SURVEY.md §8d)"),
         "backward": ("k_raster_bwd", 4 * P + 32 * T + 24 * S, "4P + 32T + 24S (SURVEY.md §8d)"),
-        "chain": ("k_chain", 44 * S + 48 * S + 24 * T + 44 * S, "44S params + 48S records + 24T partials + 44S grads"),
+        "chain": ("k_chain", 48 * S + 48 * S + 24 * T + 44 * S + 4 * S,
+                  "48S survivor params + 48S records + 24T partials + 44S grads + 4S dirty list"),
     }
     dom = max((k for k in stages if stages[k][1] > 0 and k in kernel_bytes), key=lambda k: stages[k][0])
     peak, peak_src = load_peaks()
@@ -415,7 +419,7 @@ def run_ours(args):
     kname, kbytes, kformula = kernel_bytes[dom]
     achieved = kbytes / (launch_ms * 1e-3) / 1e9
     roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(args.config) if dom == "prepare" else None,
+            "frac": achieved / peak, "traffic": ncu_traffic(args.config, kname),
             "peak_source": peak_src, "bytes_per_launch": kbytes, "launch_ms": launch_ms,
             "bytes_formula": kformula}
     per_kernel = {}
@@ -445,8 +449,8 @@ def run_ours(args):
         "gpu_launches": None,
         "clocks": clk.result(),
     }
-    # K_filter + K_exact + radix passes + forward + backward + chain (+1 memset node)
-    launches_per_step = 2 + sort_passes(X, Y) + 3
+    # K_prep + K_bin + radix passes + forward + backward + chain + chain_exact (+1 memset node)
+    launches_per_step = 2 + sort_passes(X, Y) + 4
     line["gpu_launches"] = launches_per_step * args.steps
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

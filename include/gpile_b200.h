@@ -146,7 +146,7 @@ int gpk_download(gpk_session* s, int which, void* host, uint64_t bytes);
 
 /* ---- live stage timing (CUDA events on the session stream) ------------------ */
 typedef enum {
-    GPK_STAGE_PREPARE = 0,   /* K_filter: certain-cull + gradient zero-fill + candidates */
+    GPK_STAGE_PREPARE = 0,   /* K_prep: cull, fp64 focus Gaussians, survivor records, gradient clear */
     GPK_STAGE_SORT = 1,      /* radix passes */
     GPK_STAGE_RASTER = 2,    /* forward accumulation */
     GPK_STAGE_BACKWARD = 3,  /* backward pixel accumulation */
@@ -154,7 +154,7 @@ typedef enum {
     GPK_STAGE_LOSS = 5,
     GPK_STAGE_ADAM = 6,
     GPK_STAGE_VOXEL = 7,
-    GPK_STAGE_EXACT = 8,     /* K_exact: fp64 focus Gaussians, bounds, pair emission */
+    GPK_STAGE_BIN = 8,       /* K_bin: survivor slots, (tile, candidate) pair emission */
     GPK_NUM_STAGES = 9
 } gpk_stage;
 /* Enable/disable event pairs around every stage launch. */

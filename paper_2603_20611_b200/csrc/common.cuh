@@ -54,6 +54,36 @@ struct alignas(16) SurvivorRecord {
 };
 static_assert(sizeof(SurvivorRecord) == 48, "record must stay 48 B");
 
+// One candidate's parameters, gathered once by K_filter from the SoA planes
+// (which it streams anyway) so later stages read 48 contiguous bytes instead of
+// 11 scattered 32 B sectors.
+struct alignas(16) CandParams {
+    float p[11];
+    uint32_t idx;                                 // index in the GaussianSet
+};
+static_assert(sizeof(CandParams) == 48, "candidate params must stay 48 B");
+
+__device__ __forceinline__ void load_cand(const CandParams* __restrict__ c, float p[11], uint32_t& idx) {
+    const float4* v = reinterpret_cast<const float4*>(c);
+    const float4 a = __ldg(v), b = __ldg(v + 1), d = __ldg(v + 2);
+    p[0] = a.x; p[1] = a.y; p[2] = a.z; p[3] = a.w;
+    p[4] = b.x; p[5] = b.y; p[6] = b.z; p[7] = b.w;
+    p[8] = d.x; p[9] = d.y; p[10] = d.z;
+    idx = __float_as_uint(d.w);
+}
+__device__ __forceinline__ void store_cand(CandParams* c, const float p[11], uint32_t idx) {
+    float4* v = reinterpret_cast<float4*>(c);
+    v[0] = make_float4(p[0], p[1], p[2], p[3]);
+    v[1] = make_float4(p[4], p[5], p[6], p[7]);
+    v[2] = make_float4(p[8], p[9], p[10], __uint_as_float(idx));
+}
+
+// Gradient-buffer state word (persistent): the dense gradient planes are zero
+// except at dirty_idx[0 .. count) (the previous backward's survivors), or
+// kGradsDense when anything else wrote them (set_gradients, allreduce, voxel
+// backward, reallocation): the next prepare then clears them densely.
+constexpr unsigned kGradsDense = 0xffffffffu;
+
 // Slice geometry + PSF + raster config, passed by value to every kernel.
 struct SliceArgs {
     double R[9];          // R_c row-major
@@ -258,10 +288,13 @@ struct PrepLaunch {
     const float* params;      // 11 planes x cap
     uint64_t cap;             // plane stride
     uint32_t n;
-    float* grads;             // zero-filled for non-survivors when non-null
-    unsigned* filter_counts;  // candidates per K_filter block (plain stores)
-    uint32_t* cand_local;     // block-major candidate set indices: [b*kFilterBlock + pos]
-    unsigned nfilter;         // K_filter blocks
+    float* grads;             // cleared (dense or sparse, see kGradsDense) when non-null
+    const unsigned* grads_dirty;    // persistent gradient-buffer state word
+    const uint32_t* dirty_idx;      // previous survivors' set indices
+    CandParams* cand;         // K_filter -> K_decide: candidate params, block-major slots
+    unsigned* cand_count;     // candidates per chunk (plain stores)
+    CandParams* surv_params;  // survivor params by survivor slot
+    unsigned nfilter;         // 1024-Gaussian chunks
     SurvivorRecord* records;  // indexed by candidate slot
     uint32_t* survivor_list;  // survivor slot -> candidate slot
     uint32_t* keys;           // pre-sort tile keys
@@ -272,18 +305,18 @@ struct PrepLaunch {
     unsigned* tile_hist_all;  // kMaxSortPasses regions of hist_region words (zeroed by K_filter)
     uint64_t sort_tiles_cap;
     uint64_t hist_region;     // words per pass region
-    unsigned* prev_sort_words;  // persistent: {sort tiles used, buckets} of the previous prepare
+    unsigned* prev_sort_words;  // persistent: {sort tiles, buckets, passes} of the previous sort
     int passes;
     int digit_bits;           // radix digit width of every pass
-    unsigned long long* exact_words;  // per K_exact chunk: ready<<63 | S<<32 | P (zeroed per prepare)
+    unsigned long long* exact_words;  // per chunk: ready<<63 | S<<32 | P (zeroed per prepare)
     Control* ctrl;
     ErrorState* err;
     SliceArgs slice;
-    int exact_grid;           // persistent K_exact CTAs
 };
 
 constexpr int kFilterItems = 4;
 constexpr int kFilterBlock = kPrepThreads * kFilterItems;  // Gaussians per K_filter block
+constexpr int kDecideChunks = 4;                           // K_filter chunks per K_decide group
 
 struct SortLaunch {
     const uint32_t* keys_in;
@@ -294,7 +327,7 @@ struct SortLaunch {
     const unsigned* tile_hist;     // this pass's region: tile rows then super-tile rows (2^bits each)
     unsigned* tile_hist_next;      // next pass's region (nullptr on the last pass)
     uint64_t sort_tiles_cap;       // offset (in rows) of the super-tile rows
-    unsigned* prev_sort_words;     // written by the last pass: {sort tiles, buckets}
+    unsigned* prev_sort_words;     // written by the last pass: {sort tiles, buckets, passes}
     int shift;
     int bits;                      // digit width of this pass
     unsigned next_buckets;         // 2^bits of the next pass
@@ -316,8 +349,10 @@ struct RasterLaunch {
 };
 
 struct ChainLaunch {
-    const float* params;
+    const CandParams* sparams;     // survivor params by candidate slot (K_exact)
     uint64_t cap;
+    uint32_t* dirty_idx;           // out: survivors' set indices (next prepare's sparse clear)
+    unsigned* grads_dirty;         // out: survivor count
     const SurvivorRecord* records;
     const uint32_t* survivor_list;
     const float* partials;
@@ -436,10 +471,8 @@ void launch_vox_eval(const VoxEvalLaunch& a, cudaStream_t st);
 void launch_vox_bwd(const VoxEvalLaunch& a, cudaStream_t st);
 void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st);
 
-void launch_filter(const PrepLaunch& a, int num_sms, cudaStream_t st);
-void launch_exact(const PrepLaunch& a, cudaStream_t st);
-int exact_blocks_per_sm(size_t dyn_smem);
-size_t exact_dyn_smem(unsigned nfilter);
+void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st);
+void launch_bin(const PrepLaunch& a, cudaStream_t st);
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st);
 void launch_raster_fwd(const RasterLaunch& a, cudaStream_t st);
 void launch_raster_bwd(const RasterLaunch& a, cudaStream_t st);

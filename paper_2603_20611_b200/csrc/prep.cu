@@ -76,6 +76,7 @@ __device__ __forceinline__ bool certainly_culled(const float p[11], const SliceA
 struct FilterConsts {
     float log_tau, mod, sz2;
     float tx, ty, tz_hi, tz_lo;
+    float mod2, inv_mod2, inv_sz2;   // quick test only
 };
 
 __device__ __forceinline__ bool certainly_culled_identity(const float p[11], const FilterConsts& c) {
@@ -117,106 +118,186 @@ __device__ __forceinline__ void load_params(const float* __restrict__ params, ui
     for (int k = 0; k < 11; ++k) p[k] = __ldg(params + (uint64_t)k * cap + i);
 }
 
-__device__ __forceinline__ void zero_grads(float* grads, uint64_t cap, uint32_t i) {
+
+// Cheapest certain-cull for R_c = I, division-free: lower-bounds q by replacing
+// the projected variance Sigma_c,zz with its maximum (mod * s_max)^2, upper-
+// bounds the threshold by log alpha <= min(raw, 0) and the margin's noise
+// terms by their values at Sigma_c,zz = 0 / s_min. Returns true only if the
+// full fp32 test (certainly_culled_identity) culls too:
+//   0.5 q > T + M   with q = mcz^2 / den, 0 < sz2 <= den <= den_hi
+//   <=  0.5 mcz^2 > X_up * (X_up >= 0 ? den_hi : sz2),  X_up >= T + M.
+// Undecided items take the full test, compacted, so the warp does not pay it
+// for every Gaussian.
+__device__ __forceinline__ bool quick_culled_identity(const float p[11], const FilterConsts& c) {
+    float sum = p[0];
 #pragma unroll
-    for (int k = 0; k < 11; ++k) grads[(uint64_t)k * cap + i] = 0.f;
+    for (int k = 1; k < 11; ++k) sum += p[k];
+    if (!isfinite(sum)) return false;
+    const float lmax = fmaxf(p[3], fmaxf(p[4], p[5])), lmin = fminf(p[3], fminf(p[4], p[5]));
+    if (!(lmax < 40.f && lmin > -40.f && lmax - lmin < 6.2f)) return false;
+    const float qn2 = __fmaf_rn(p[6], p[6], __fmaf_rn(p[7], p[7], __fmaf_rn(p[8], p[8], p[9] * p[9])));
+    if (!(qn2 > 1e-20f && qn2 < 1e20f)) return false;
+    const float mcz = (p[2] + c.tz_hi) + c.tz_lo;
+    const float mcx = p[0] + c.tx, mcy = p[1] + c.ty;
+    const float mu2 = __fmaf_rn(mcx, mcx, __fmaf_rn(mcy, mcy, mcz * mcz));
+    // e^(2 lmax) mod^2 = (mod s_max)^2 ; e^(-2 lmin) / mod^2 = 1 / (mod s_min)^2
+    const float den_hi = __fmaf_rn(__expf(2.f * lmax) * c.mod2, 1.0002f, c.sz2);
+    const float inv_smin2 = __expf(-2.f * lmin) * c.inv_mod2 * 1.0002f;
+    const float thresh_hi = fminf(p[10], 0.f) - c.log_tau;
+    const float noise = __fmaf_rn(2e-14f * mu2, inv_smin2,
+                                  4.8e-7f * fabsf(mcz) * (fabsf(p[2]) + fabsf(c.tz_hi)) * c.inv_sz2 * 1.0002f);
+    const float x = thresh_hi + (2e-3f + __fmaf_rn(2e-5f, fabsf(thresh_hi) + 0.7f, noise));
+    const float x_up = __fmaf_rn(1e-3f, fabsf(x) + noise, x) + 1e-6f;
+    return 0.5f * mcz * mcz > x_up * (x_up >= 0.f ? den_hi : c.sz2);
 }
 
 // ---- K_filter ------------------------------------------------------------------
-// Persistent CTAs walk 1024-Gaussian chunks. Each chunk's 11 parameter planes
-// (4 KB each) arrive by TMA bulk copy (cp.async.bulk + mbarrier complete_tx):
-// 44 KB in flight per CTA without occupying registers. The dense gradient
-// planes of the chunk are zero-filled by 11 bulk shared->global stores from a
-// zero buffer (survivors are overwritten later by K_chain; culled primitives
-// keep the exact zeros of grad_chain.hpp:12-22).
+// prepare_gaussians' cull (render.hpp:107) as a streaming pass. CTAs walk
+// 1024-Gaussian chunks (4 per SM resident, one chunk each in flight):
+//   1. TMA bulk copy of the chunk's 11 parameter planes (44 KB) into shared
+//      memory (cp.async.bulk + mbarrier complete_tx); when the gradient planes
+//      must be cleared densely, bulk shared->global stores of a zero buffer.
+//   2. fp32 certain-cull: a division-free quick bound for everything, the full
+//      closed form (q = mu_cz^2 / (sigma_z^2 + Sigma_c,zz))
+//      only for the undecided, compacted — both conservative: a culled
+//      Gaussian is one the reference culls too.
+//   3. candidates compacted in set order into 48 B CandParams records at
+//      block-major slots [b*1024, b*1024 + count_b), count_b stored plainly.
+// No fp64 and no cross-CTA waiting here, so the kernel stays small in
+// registers and the HBM stream has all the warps it needs.
+constexpr int kFilterCtasPerSm = 4;
+constexpr int kZeroBuf = 256;  // floats in the dense-clear source buffer
+
 template <bool kZeroGrads>
-__global__ void __launch_bounds__(kPrepThreads) k_filter(const PrepLaunch a, float log_tau,
-                                                         int filter_on, unsigned nchunks) {
-    constexpr int kSlots = kFilterItems * 8;  // (item, warp) counts, in set order
-    extern __shared__ __align__(128) float s_dyn[];
-    float* s_p = s_dyn;                          // 11 planes x kFilterBlock
-    float* s_zero = s_dyn + 11 * kFilterBlock;   // kFilterBlock zeros
+__global__ void __launch_bounds__(kPrepThreads, kFilterCtasPerSm)
+    k_filter(const PrepLaunch a, float log_tau, int filter_on) {
+    extern __shared__ __align__(128) float s_p[];         // 11 planes x kFilterBlock
     __shared__ __align__(8) uint64_t s_bar;
-    __shared__ unsigned s_off[kSlots];
+    __shared__ __align__(16) float s_zero[kZeroBuf];
+    __shared__ uint8_t s_flag[kFilterBlock];              // 0 culled, 1 candidate, 2 undecided
+    __shared__ uint16_t s_list[kFilterBlock];             // undecided work list
+    __shared__ unsigned s_off[kFilterItems * 8];
+    __shared__ unsigned s_nfull;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const float mod_f = (float)a.slice.mod;
-    const float sz2 = (float)(a.slice.sigma_z * a.slice.sigma_z);
+    const unsigned nchunks = a.nfilter;
     const unsigned plane_bytes = kFilterBlock * sizeof(float);
+    const unsigned dirty = kZeroGrads ? *a.grads_dirty : 0u;
+    const bool dense_zero = kZeroGrads && dirty == kGradsDense;
 
     if (tid == 0) {
         mbar_init(&s_bar, 1);
         fence_mbar_init();
+        s_nfull = 0;
     }
-    if (kZeroGrads) {
-        for (int i = tid; i < kFilterBlock; i += kPrepThreads) s_zero[i] = 0.f;
+    if (dense_zero) {
+        for (int i = tid; i < kZeroBuf; i += kPrepThreads) s_zero[i] = 0.f;
         fence_proxy_async_smem();
     }
     __syncthreads();
+    auto stage_chunk = [&](unsigned bb) {
+        const uint32_t bbase = bb * kFilterBlock;
+        mbar_expect_tx(&s_bar, 11 * plane_bytes);
+#pragma unroll 1
+        for (int k = 0; k < 11; ++k)
+            bulk_g2s(s_p + k * kFilterBlock, a.params + (uint64_t)k * a.cap + bbase, plane_bytes, &s_bar);
+        if (dense_zero) {
+#pragma unroll 1
+            for (int k = 0; k < 11; ++k)
+#pragma unroll 1
+                for (int z = 0; z < kFilterBlock; z += kZeroBuf)
+                    bulk_s2g(a.grads + (uint64_t)k * a.cap + bbase + z, s_zero, kZeroBuf * sizeof(float));
+            bulk_commit();
+        }
+    };
+    if (tid == 0 && blockIdx.x < nchunks) stage_chunk(blockIdx.x);  // in flight during housekeeping
 
     // Housekeeping: clear the per-sort-tile digit histograms the previous
-    // prepare used (all passes) before K_exact / the radix passes refill them.
+    // sort used (its passes only) before this prepare / the radix passes refill
+    // them; clear the previous survivors' gradients (sparse mode).
     {
-        const uint64_t pt = a.prev_sort_words[0], pnb = a.prev_sort_words[1];
-        const uint64_t tile_words = pt * pnb;
-        const uint64_t super_words = ((pt + kSuperTiles - 1) / kSuperTiles) * pnb;
-        const uint64_t used = tile_words + super_words;  // per pass region
-        const uint64_t total = (uint64_t)kMaxSortPasses * used;
-        if (used)
-            for (uint64_t w = (uint64_t)blockIdx.x * kPrepThreads + tid; w < total;
-                 w += (uint64_t)gridDim.x * kPrepThreads) {
-                const uint64_t p = w / used, o = w % used;
-                const uint64_t off = o < tile_words ? o : a.sort_tiles_cap * pnb + (o - tile_words);
-                a.tile_hist_all[p * a.hist_region + off] = 0u;
+        const unsigned pt = a.prev_sort_words[0], pnb = a.prev_sort_words[1], pp = a.prev_sort_words[2];
+        const unsigned tile_words = pt * pnb;
+        const unsigned used = tile_words + ((pt + kSuperTiles - 1) / kSuperTiles) * pnb;  // per pass
+        const unsigned stride = gridDim.x * kPrepThreads;
+        for (unsigned ps = 0; ps < pp; ++ps) {
+            unsigned* region = a.tile_hist_all + (uint64_t)ps * a.hist_region;
+            unsigned* super = region + a.sort_tiles_cap * pnb - tile_words;
+            for (unsigned w = blockIdx.x * kPrepThreads + tid; w < used; w += stride)
+                (w < tile_words ? region : super)[w] = 0u;
+        }
+        if (kZeroGrads && !dense_zero)
+            for (unsigned e = blockIdx.x * kPrepThreads + tid; e < dirty; e += stride) {
+                const uint32_t i = a.dirty_idx[e];
+#pragma unroll
+                for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = 0.f;
             }
     }
 
     FilterConsts fc;
     fc.log_tau = log_tau;
-    fc.mod = mod_f;
-    fc.sz2 = sz2;
+    fc.mod = (float)a.slice.mod;
+    fc.sz2 = (float)(a.slice.sigma_z * a.slice.sigma_z);
     fc.tx = (float)a.slice.t[0];
     fc.ty = (float)a.slice.t[1];
     fc.tz_hi = (float)a.slice.t[2];
     fc.tz_lo = (float)(a.slice.t[2] - (double)fc.tz_hi);
+    fc.mod2 = (float)(a.slice.mod * a.slice.mod);
+    fc.inv_mod2 = (float)(1.0 / (a.slice.mod * a.slice.mod));
+    fc.inv_sz2 = (float)(1.0 / (a.slice.sigma_z * a.slice.sigma_z));
     const bool ident = a.slice.identity_rot != 0;
 
     unsigned phase = 0;
     for (unsigned b = blockIdx.x; b < nchunks; b += gridDim.x, phase ^= 1u) {
         const uint32_t base = b * kFilterBlock;
-        if (tid == 0) {
-            if (filter_on) {
-                mbar_expect_tx(&s_bar, 11 * plane_bytes);
-#pragma unroll 1
-                for (int k = 0; k < 11; ++k)
-                    bulk_g2s(s_p + k * kFilterBlock, a.params + (uint64_t)k * a.cap + base, plane_bytes, &s_bar);
-            }
-            if (kZeroGrads) {
-#pragma unroll 1
-                for (int k = 0; k < 11; ++k)
-                    bulk_s2g(a.grads + (uint64_t)k * a.cap + base, s_zero, plane_bytes);
-                bulk_commit();
-            }
-        }
-        if (filter_on) mbar_wait(&s_bar, phase);
+        mbar_wait(&s_bar, phase);
 
-        unsigned ballots[kFilterItems];
+        // ---- certain-cull: quick bound, then the full test compacted ----------
 #pragma unroll
         for (int k = 0; k < kFilterItems; ++k) {
             const int li = k * kPrepThreads + tid;
-            const uint32_t i = base + li;
-            bool cand = false;
-            if (i < a.n) {
-                cand = true;
+            uint8_t flag = 0;
+            if (base + li < a.n) {
+                flag = 1;
                 if (filter_on) {
-                    float p[11];
+                    flag = 2;
+                    if (ident) {
+                        float p[11];
 #pragma unroll
-                    for (int q = 0; q < 11; ++q) p[q] = s_p[q * kFilterBlock + li];
-                    cand = ident ? !certainly_culled_identity(p, fc)
-                                 : !certainly_culled(p, a.slice, log_tau, mod_f, sz2);
+                        for (int q = 0; q < 11; ++q) p[q] = s_p[q * kFilterBlock + li];
+                        if (quick_culled_identity(p, fc)) flag = 0;
+                    }
                 }
             }
-            ballots[k] = __ballot_sync(0xffffffffu, cand);
+            s_flag[li] = flag;
+            const unsigned m = __ballot_sync(0xffffffffu, flag == 2);
+            if (m) {
+                unsigned wbase = 0;
+                if (lane == 0) wbase = atomicAdd(&s_nfull, (unsigned)__popc(m));
+                wbase = __shfl_sync(0xffffffffu, wbase, 0);
+                if (flag == 2) s_list[wbase + __popc(m & lanemask_lt())] = (uint16_t)li;
+            }
+        }
+        __syncthreads();
+        {
+            const unsigned nfull = s_nfull;
+            for (unsigned j = tid; j < nfull; j += kPrepThreads) {
+                const int li = s_list[j];
+                float p[11];
+#pragma unroll
+                for (int q = 0; q < 11; ++q) p[q] = s_p[q * kFilterBlock + li];
+                const bool culled = ident ? certainly_culled_identity(p, fc)
+                                          : certainly_culled(p, a.slice, log_tau, fc.mod, fc.sz2);
+                s_flag[li] = culled ? 0 : 1;
+            }
+        }
+        __syncthreads();
+
+        // ---- candidates in set order -------------------------------------------
+        unsigned ballots[kFilterItems];
+#pragma unroll
+        for (int k = 0; k < kFilterItems; ++k) {
+            ballots[k] = __ballot_sync(0xffffffffu, s_flag[k * kPrepThreads + tid] == 1);
             if (lane == 0) s_off[k * 8 + warp] = __popc(ballots[k]);
         }
         __syncthreads();
@@ -228,95 +309,92 @@ __global__ void __launch_bounds__(kPrepThreads) k_filter(const PrepLaunch a, flo
                 const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += u;
             }
-            __syncwarp();
             s_off[lane] = incl - v;
-            if (lane == 31) {
-                a.filter_counts[b] = incl;
-                if (incl) atomicAdd(&a.ctrl->candidates, incl);
-            }
+            if (lane == 31) a.cand_count[b] = incl;
         }
         __syncthreads();
-        uint32_t* out = a.cand_local + (uint64_t)b * kFilterBlock;
+        CandParams* out = a.cand + base;
 #pragma unroll
-        for (int k = 0; k < kFilterItems; ++k) {
-            if (ballots[k] & (1u << lane))
-                out[s_off[k * 8 + warp] + __popc(ballots[k] & lanemask_lt())] = base + k * kPrepThreads + tid;
+        for (int k = 0; k < kFilterItems; ++k)
+            if (ballots[k] & (1u << lane)) {
+                const int li = k * kPrepThreads + tid;
+                float p[11];
+#pragma unroll
+                for (int q = 0; q < 11; ++q) p[q] = s_p[q * kFilterBlock + li];
+                store_cand(out + s_off[k * 8 + warp] + __popc(ballots[k] & lanemask_lt()), p, base + li);
+            }
+        __syncthreads();  // s_p, s_flag, s_list, s_off free again
+        if (tid == 0) {
+            s_nfull = 0;
+            if (b + gridDim.x < nchunks) stage_chunk(b + gridDim.x);
         }
-        __syncthreads();  // s_p / s_off are reused by the next chunk
     }
-    if (kZeroGrads && tid == 0) bulk_wait_all();
+    if (dense_zero && tid == 0) bulk_wait_all();
 }
 
-// ---- K_exact -------------------------------------------------------------------
-template <bool kZeroGrads>
-__global__ void __launch_bounds__(kExactChunk) k_exact(const PrepLaunch a) {
-    extern __shared__ unsigned s_bpre[];                 // exclusive prefix of filter counts (nfilter+1)
-    __shared__ unsigned s_chunk;
-    __shared__ unsigned long long s_incl[kExactChunk];   // (survivors << 32) | pairs, inclusive
-    __shared__ uint16_t s_rect[kExactChunk][3];          // tx0, ty0, ntx
-    __shared__ unsigned long long s_warp[kExactChunk / 32];
-    __shared__ unsigned long long s_excl;
+// ---- K_decide ------------------------------------------------------------------
+// The rest of prepare_gaussians + the TileGrid pair list (render.hpp:91-160),
+// one CTA per kDecideChunks consecutive K_filter chunks (a "group"; few enough
+// groups that all CTAs are resident together), groups taken in ticket order:
+//   1. each candidate gets the decision-grade fp64 closed form (fast_decide)
+//      and, within ~1e-9 of a decision boundary, the reference's own fp64
+//      evaluation (focus_prepare): survivors and pixel bounds — therefore tile
+//      pairs — are the reference's bit for bit. Survivors are compacted in set
+//      order: 48 B record + 48 B params at group-major survivor slots.
+//   2. group aggregate (survivors, pairs) through a wait-free ordered prefix
+//      over group words (predecessors hold earlier tickets: they are running
+//      or done and publish before they wait).
+//   3. survivor slots, and (tile, survivor slot) pairs in (survivor, tile)
+//      order — the order a stable sort on the tile key needs to reproduce the
+//      reference's ascending per-tile lists — with the first radix pass's
+//      digit histograms (global, per sort tile, per super-tile).
+constexpr int kDecideThreads = 256;
+constexpr int kDecideGroup = kDecideChunks * kFilterBlock;   // Gaussians per group
+
+__global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
+    extern __shared__ unsigned s_dyn_u[];
+    unsigned* s_incl = s_dyn_u;                                              // kDecideGroup
+    uint16_t(*s_rect)[3] = reinterpret_cast<uint16_t(*)[3]>(s_dyn_u + kDecideGroup);  // kDecideGroup x 3
     __shared__ unsigned s_hist[kMaxSortPasses][kMaxBuckets];
-
+    __shared__ unsigned s_cnt[2][kDecideThreads / 32];
+    __shared__ unsigned s_cpre[kDecideChunks + 1];
+    __shared__ unsigned s_grp, s_nsurv;
+    __shared__ unsigned long long s_excl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned C = a.ctrl->candidates;  // total, accumulated by K_filter
-    const unsigned nchunks = (C + kExactChunk - 1) / kExactChunk;
-    // claim the first chunk before any setup: surplus CTAs leave at once
-    if (tid == 0) s_chunk = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
-    __syncthreads();
-    if (s_chunk >= nchunks) return;
-    for (int k = tid; k < kMaxSortPasses * kMaxBuckets; k += kExactChunk) (&s_hist[0][0])[k] = 0;
     const unsigned dmask = (1u << a.digit_bits) - 1;
-    // candidate layout: exclusive prefix over the K_filter blocks' counts
-    {
-        const unsigned nb = a.nfilter;
-        unsigned carry = 0;
-        for (unsigned base = 0; base < nb; base += kExactChunk) {
-            const unsigned j = base + tid;
-            const unsigned v = j < nb ? a.filter_counts[j] : 0u;
-            unsigned incl = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += u;
-            }
-            if (lane == 31) s_warp[warp] = incl;
-            __syncthreads();
-            unsigned add = carry;
-            for (int w = 0; w < warp; ++w) add += (unsigned)s_warp[w];
-            if (j < nb) s_bpre[j] = add + incl - v;
-            unsigned tot = 0;
-            for (int w = 0; w < kExactChunk / 32; ++w) tot += (unsigned)s_warp[w];
-            carry += tot;
-            __syncthreads();
-        }
-        if (tid == 0) s_bpre[nb] = carry;
-        __syncthreads();
-    }
+    const unsigned nb = dmask + 1;
     const int tiles_x = a.slice.tiles_x;
-
-    for (bool first = true;; first = false) {
-        if (!first) {
-            __syncthreads();
-            if (tid == 0) s_chunk = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
-            __syncthreads();
+    const unsigned ngroups = gridDim.x;
+    for (int k = tid; k < a.passes * kMaxBuckets; k += kDecideThreads) (&s_hist[0][0])[k] = 0;
+    if (tid == 0) {
+        const unsigned g = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
+        s_grp = g;
+        s_nsurv = 0;
+        unsigned acc = 0;
+        for (int q = 0; q < kDecideChunks; ++q) {
+            s_cpre[q] = acc;
+            const unsigned c = g * kDecideChunks + q;
+            acc += c < a.nfilter ? __ldcg(&a.cand_count[c]) : 0u;
         }
-        const unsigned chunk = s_chunk;
-        if (chunk >= nchunks) break;
-        const unsigned c = chunk * kExactChunk + tid;
-        unsigned long long v = 0;
-        if (c < C) {
-            // filter block holding candidate c: last b with s_bpre[b] <= c
-            unsigned lo = 0, hi = a.nfilter - 1;
-            while (lo < hi) {
-                const unsigned mid = (lo + hi + 1) >> 1;
-                if (s_bpre[mid] <= c) lo = mid; else hi = mid - 1;
-            }
-            const uint32_t i = a.cand_local[(uint64_t)lo * kFilterBlock + (c - s_bpre[lo])];
-            float pf[11];
-            load_params(a.params, a.cap, i, pf);
-            SurvivorRecord rec;
-            bool survive = false;
+        s_cpre[kDecideChunks] = acc;
+    }
+    __syncthreads();
+    const unsigned g = s_grp;
+    const uint32_t base = g * kDecideGroup;
+    const unsigned nc = s_cpre[kDecideChunks];
+
+    // ---- 1. exact decision, survivors compacted in order -------------------------
+    for (unsigned j0 = 0, r = 0; j0 < nc; j0 += kDecideThreads, r ^= 1) {
+        const unsigned j = j0 + tid;
+        SurvivorRecord rec;
+        float pf[11];
+        uint32_t i = 0;
+        bool survive = false;
+        if (j < nc) {
+            int q = 0;
+#pragma unroll
+            for (int t = 1; t < kDecideChunks; ++t) q += (j >= s_cpre[t]);
+            load_cand(a.cand + (uint64_t)base + q * kFilterBlock + (j - s_cpre[q]), pf, i);
             uint32_t flag = 0;
             const int fr = fast_decide(pf, a.slice, rec);
             if (fr == kFastSurvive) {
@@ -326,10 +404,10 @@ __global__ void __launch_bounds__(kExactChunk) k_exact(const PrepLaunch a) {
                 // near a decision boundary: the reference's own fp64 evaluation
                 double pd[11];
 #pragma unroll
-                for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
+                for (int t = 0; t < 11; ++t) pd[t] = (double)pf[t];
                 Focus f;
-                const int r = focus_prepare(pd, a.slice, f);
-                if (r == kSurvive) {
+                const int res = focus_prepare(pd, a.slice, f);
+                if (res == kSurvive) {
                     survive = true;
                     rec.mu2d_x = f.mu_e.x;
                     rec.mu2d_y = f.mu_e.y;
@@ -341,92 +419,109 @@ __global__ void __launch_bounds__(kExactChunk) k_exact(const PrepLaunch a) {
                     rec.hi_x = (uint16_t)f.hi_x;
                     rec.lo_y = (uint16_t)f.lo_y;
                     rec.hi_y = (uint16_t)f.hi_y;
-                } else if (r > 0) {
-                    record_error(a.err, r, i);  // gradients of culled candidates: zeroed by K_filter
+                } else if (res > 0) {
+                    record_error(a.err, res, i);
                 }
             }
-            if (survive) {
-                const int tx0 = rec.lo_x / kTile, tx1 = rec.hi_x / kTile;
-                const int ty0 = rec.lo_y / kTile, ty1 = rec.hi_y / kTile;
-                const unsigned ntx = tx1 - tx0 + 1, nty = ty1 - ty0 + 1;
-                v = (1ull << 32) | (unsigned long long)(ntx * nty);
-                s_rect[tid][0] = (uint16_t)tx0;
-                s_rect[tid][1] = (uint16_t)ty0;
-                s_rect[tid][2] = (uint16_t)ntx;
-                rec.gidx = i | flag;
-                rec.pair_base = 0;
-                a.records[c] = rec;
-            }
+            rec.gidx = i | flag;
+            rec.pair_base = 0;
         }
-        // block inclusive scan of (survivor, pairs)
-        unsigned long long incl = v;
+        const unsigned m = __ballot_sync(0xffffffffu, survive);
+        if (lane == 0) s_cnt[r][warp] = __popc(m);
+        __syncthreads();
+        unsigned rank = s_nsurv + __popc(m & lanemask_lt());
+        for (int w = 0; w < warp; ++w) rank += s_cnt[r][w];
+        if (survive) {
+            a.records[base + rank] = rec;
+            store_cand(a.surv_params + base + rank, pf, i);
+            const unsigned tx0 = rec.lo_x / kTile, ty0 = rec.lo_y / kTile;
+            const unsigned ntx = rec.hi_x / kTile - tx0 + 1, nty = rec.hi_y / kTile - ty0 + 1;
+            s_rect[rank][0] = (uint16_t)tx0;
+            s_rect[rank][1] = (uint16_t)ty0;
+            s_rect[rank][2] = (uint16_t)ntx;
+            s_incl[rank] = ntx * nty;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            unsigned t = 0;
+            for (int w = 0; w < kDecideThreads / 32; ++w) t += s_cnt[r][w];
+            s_nsurv += t;
+        }
+    }
+    __syncthreads();
+    const unsigned S = s_nsurv;
+
+    // ---- 2. inclusive scan of the pair counts, ordered group prefix -------------
+    {
+        constexpr int kPer = kDecideGroup / kDecideThreads;  // consecutive survivors per thread
+        const unsigned j0 = tid * kPer;
+        unsigned run = 0;
+        for (int q = 0; q < kPer; ++q) run += (j0 + q < S) ? s_incl[j0 + q] : 0u;
+        unsigned incl = run;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += u;
         }
-        if (lane == 31) s_warp[warp] = incl;
+        if (lane == 31) s_cnt[0][warp] = incl;
         __syncthreads();
-        unsigned long long add = 0;
-        for (int w = 0; w < warp; ++w) add += s_warp[w];
-        incl += add;
-        s_incl[tid] = incl;
-        __syncthreads();
-        const unsigned long long agg = s_incl[kExactChunk - 1];
-        if (warp == 0) {
-            const unsigned long long excl = warp_prefix_aggregates(a.exact_words, chunk, agg);
-            if (lane == 0) {
-                s_excl = excl;
-                if (chunk == nchunks - 1) {
-                    const unsigned long long tot = excl + agg;
-                    const unsigned S = (unsigned)(tot >> 32), P = (unsigned)(tot & 0xffffffffull);
-                    a.ctrl->survivors = S;
-                    a.ctrl->pairs = P;
-                    a.ctrl->pair_overflow = (P > a.pair_cap) ? 1u : 0u;
-                }
-            }
+        unsigned ex = incl - run;
+        for (int w = 0; w < warp; ++w) ex += s_cnt[0][w];
+        for (int q = 0; q < kPer && j0 + q < S; ++q) {
+            ex += s_incl[j0 + q];
+            s_incl[j0 + q] = ex;
         }
-        __syncthreads();
-        const unsigned S0 = (unsigned)(s_excl >> 32);
-        const unsigned P0 = (unsigned)(s_excl & 0xffffffffull);
-        {
-            const unsigned long long prev = tid ? s_incl[tid - 1] : 0ull;
-            if ((s_incl[tid] >> 32) != (prev >> 32)) {
-                a.survivor_list[S0 + (unsigned)(prev >> 32)] = c;
-                a.records[c].pair_base = P0 + (unsigned)(prev & 0xffffffffull);
-            }
-        }
-        // cooperative, balanced pair emission in (candidate, tile) order
-        const unsigned Pb = (unsigned)(agg & 0xffffffffull);
-        for (unsigned k = tid; k < Pb; k += kExactChunk) {
-            unsigned lo = 0, hi = kExactChunk - 1;
-            while (lo < hi) {
-                const unsigned mid = (lo + hi) >> 1;
-                if ((unsigned)(s_incl[mid] & 0xffffffffull) > k) hi = mid; else lo = mid + 1;
-            }
-            const unsigned before = lo ? (unsigned)(s_incl[lo - 1] & 0xffffffffull) : 0u;
-            const unsigned local = k - before;
-            const unsigned ntx = s_rect[lo][2];
-            const unsigned ty = s_rect[lo][1] + local / ntx;
-            const unsigned tx = s_rect[lo][0] + local % ntx;
-            const unsigned tile = ty * (unsigned)tiles_x + tx;
-            const unsigned long long pos = (unsigned long long)P0 + k;
-            if (pos < a.pair_cap) {
-                a.keys[pos] = tile;
-                a.vals[pos] = chunk * kExactChunk + lo;
-                if (a.passes > 0) {
-                    const uint64_t st = pos / kSortTile;
-                    atomicAdd(&a.tile_hist0[st * (dmask + 1) + (tile & dmask)], 1u);
-                    atomicAdd(&a.tile_hist0[(a.sort_tiles_cap + st / kSuperTiles) * (dmask + 1) + (tile & dmask)], 1u);
-                }
-                for (int ps = 0; ps < a.passes; ++ps)
-                    atomicAdd(&s_hist[ps][(tile >> (a.digit_bits * ps)) & dmask], 1u);
+    }
+    __syncthreads();
+    const unsigned Pb = S ? s_incl[S - 1] : 0u;
+    if (warp == 0) {
+        const unsigned long long agg = ((unsigned long long)S << 32) | Pb;
+        const unsigned long long excl = warp_prefix_aggregates(a.exact_words, g, agg);
+        if (lane == 0) {
+            s_excl = excl;
+            if (g == ngroups - 1) {
+                const unsigned long long tot = excl + agg;
+                const unsigned P = (unsigned)(tot & 0xffffffffull);
+                a.ctrl->survivors = (unsigned)(tot >> 32);
+                a.ctrl->pairs = P;
+                a.ctrl->pair_overflow = (P > a.pair_cap) ? 1u : 0u;
             }
         }
     }
     __syncthreads();
+
+    // ---- 3. survivor slots and pair emission -------------------------------------
+    const unsigned S0 = (unsigned)(s_excl >> 32);
+    const unsigned P0 = (unsigned)(s_excl & 0xffffffffull);
+    for (unsigned j = tid; j < S; j += kDecideThreads) {
+        a.survivor_list[S0 + j] = base + j;
+        a.records[base + j].pair_base = P0 + (j ? s_incl[j - 1] : 0u);
+    }
+    for (unsigned k = tid; k < Pb; k += kDecideThreads) {
+        unsigned lo = 0, hi = S - 1;
+        while (lo < hi) {
+            const unsigned mid = (lo + hi) >> 1;
+            if (s_incl[mid] > k) hi = mid; else lo = mid + 1;
+        }
+        const unsigned local = k - (lo ? s_incl[lo - 1] : 0u);
+        const unsigned ntx = s_rect[lo][2];
+        const unsigned tile = (s_rect[lo][1] + local / ntx) * (unsigned)tiles_x + s_rect[lo][0] + local % ntx;
+        const unsigned long long pos = (unsigned long long)P0 + k;
+        if (pos < a.pair_cap) {
+            a.keys[pos] = tile;
+            a.vals[pos] = base + lo;
+            if (a.passes > 0) {
+                const uint64_t st = pos / kSortTile;
+                atomicAdd(&a.tile_hist0[st * nb + (tile & dmask)], 1u);
+                atomicAdd(&a.tile_hist0[(a.sort_tiles_cap + st / kSuperTiles) * nb + (tile & dmask)], 1u);
+            }
+            for (int ps = 0; ps < a.passes; ++ps)
+                atomicAdd(&s_hist[ps][(tile >> (a.digit_bits * ps)) & dmask], 1u);
+        }
+    }
+    __syncthreads();
     for (int ps = 0; ps < a.passes; ++ps)
-        for (unsigned d = tid; d <= dmask; d += kExactChunk) {
+        for (unsigned d = tid; d <= dmask; d += kDecideThreads) {
             const unsigned v = s_hist[ps][d];
             if (v) atomicAdd(&a.hist[ps * kMaxBuckets + d], v);
         }
@@ -474,17 +569,19 @@ __device__ __forceinline__ void store_chain(const ChainLaunch& a, uint32_t i, co
 // K_chain_exact so this kernel stays small in registers.
 __global__ void __launch_bounds__(128) k_chain(const ChainLaunch a) {
     const unsigned S = a.ctrl->survivors;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.grads_dirty = S;
     for (unsigned slot = blockIdx.x * blockDim.x + threadIdx.x; slot < S;
          slot += gridDim.x * blockDim.x) {
         const uint32_t cid = a.survivor_list[slot];
         const SurvivorRecord rec = a.records[cid];
+        a.dirty_idx[slot] = rec.gidx & ~kExactFlag;
         if (rec.gidx & kExactFlag) {
             a.exact_list[atomicAdd(a.exact_count, 1u)] = slot;
             continue;
         }
-        const uint32_t i = rec.gidx;
         float pf[11];
-        load_params(a.params, a.cap, i, pf);
+        uint32_t i;
+        load_cand(a.sparams + cid, pf, i);
         FastFocus ff;
         fast_state(pf, a.slice, ff);
         double acc[6];
@@ -501,9 +598,9 @@ __global__ void __launch_bounds__(128) k_chain_exact(const ChainLaunch a) {
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
         const uint32_t cid = a.survivor_list[a.exact_list[e]];
         const SurvivorRecord rec = a.records[cid];
-        const uint32_t i = rec.gidx & ~kExactFlag;
         float pf[11];
-        load_params(a.params, a.cap, i, pf);
+        uint32_t i;
+        load_cand(a.sparams + cid, pf, i);
         double acc[6];
         merge_partials(a, rec, acc);
         double pd[11];
@@ -744,20 +841,12 @@ void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st) {
     k_vchain<<<grid, 128, 0, st>>>(a);
 }
 
-int exact_blocks_per_sm(size_t dyn_smem) {
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_exact<true>, kExactChunk, dyn_smem);
-    return nb > 0 ? nb : 1;
-}
-
-size_t exact_dyn_smem(unsigned nfilter) { return (size_t)(nfilter + 1) * sizeof(unsigned); }
-
-void launch_filter(const PrepLaunch& a, int num_sms, cudaStream_t st) {
+void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st) {
     if (a.n == 0) return;
     const bool filter_on = a.slice.tau > 0.0 && a.slice.mod > 1e-10 && a.slice.mod < 1e10 &&
                            a.slice.sigma_z > 1e-10 && a.slice.sigma_z < 1e10;
     const float log_tau = filter_on ? (float)log(a.slice.tau) : 0.f;
-    const int smem = 12 * kFilterBlock * (int)sizeof(float);
+    const int smem = 11 * kFilterBlock * (int)sizeof(float);
     static int per_sm = 0;
     if (!per_sm) {
         cudaFuncSetAttribute(k_filter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -767,22 +856,21 @@ void launch_filter(const PrepLaunch& a, int num_sms, cudaStream_t st) {
     }
     const unsigned grid = (unsigned)std::min<uint64_t>(a.nfilter, (uint64_t)num_sms * per_sm);
     if (a.grads)
-        k_filter<true><<<grid, kPrepThreads, smem, st>>>(a, log_tau, filter_on ? 1 : 0, a.nfilter);
+        k_filter<true><<<grid, kPrepThreads, smem, st>>>(a, log_tau, filter_on ? 1 : 0);
     else
-        k_filter<false><<<grid, kPrepThreads, smem, st>>>(a, log_tau, filter_on ? 1 : 0, a.nfilter);
+        k_filter<false><<<grid, kPrepThreads, smem, st>>>(a, log_tau, filter_on ? 1 : 0);
 }
 
-void launch_exact(const PrepLaunch& a, cudaStream_t st) {
-    if (a.n == 0) return;
-    const size_t smem = exact_dyn_smem(a.nfilter);
-    if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(k_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+void launch_bin(const PrepLaunch& a, cudaStream_t st) {
+    if (!a.n) return;
+    const int smem = kDecideGroup * (4 + 6);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
     }
-    if (a.grads)
-        k_exact<true><<<a.exact_grid, kExactChunk, smem, st>>>(a);
-    else
-        k_exact<false><<<a.exact_grid, kExactChunk, smem, st>>>(a);
+    const unsigned groups = (a.nfilter + kDecideChunks - 1) / kDecideChunks;
+    k_decide<<<groups, kDecideThreads, smem, st>>>(a);
 }
 
 void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st) {

@@ -99,8 +99,11 @@ struct gpk_session {
     DevBuf params, grads, adam_m, adam_v, records, survivors;
     DevBuf keys[2], vals[2], partials, sort_status;  // sort_status: per-sort-tile digit counts
     DevBuf head;       // Control | hist | prep flags (memset per prepare)
-    DevBuf prep_vals;  // per K_filter block candidate counts
-    DevBuf cand_list;  // block-major candidate set indices
+    DevBuf cand_list;  // K_chain's deferral list (survivor slots for the fp64 chain)
+    DevBuf cand;       // CandParams of K_filter's candidates (block-major slots)
+    DevBuf cand_count; // candidates per 1024-Gaussian chunk
+    DevBuf surv_params;  // CandParams of survivors by survivor slot (K_decide)
+    DevBuf dirty_idx;  // set indices of the last backward's survivors
     int num_sms = 148;
     DevBuf persist;    // ErrorState | epoch | adam step | adam done ctr | loss done ctr | loss
     DevBuf image, dl_di, target, loss_g, loss_partial;
@@ -119,18 +122,20 @@ struct gpk_session {
     DevBuf vox_records, volume, dl_dv_vol, vox_partials;
 
     // captured step graphs (executable graph + the prepared state it leaves)
-    struct Graph {
-        cudaGraphExec_t exec;
-        PrepState prep;
-    };
-    std::vector<Graph> graphs;
-
-    // live stage timing
-    bool timing = false;
     struct Pending {
         int stage;
         cudaEvent_t a, b;
     };
+    struct Graph {
+        cudaGraphExec_t exec;
+        PrepState prep;
+        std::vector<Pending> timed;  // event-record nodes captured with stage timing on
+    };
+    bool capturing = false;
+    std::vector<Graph> graphs;
+
+    // live stage timing
+    bool timing = false;
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> event_pool;
     double stage_ms[GPK_NUM_STAGES] = {};
@@ -145,7 +150,8 @@ struct gpk_session {
     double* loss() { return reinterpret_cast<double*>(persist.as<char>() + 88); }
     Control* ctrl() { return head.as<Control>(); }
     unsigned* hist() { return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control)); }
-    unsigned* prev_sort_words() { return reinterpret_cast<unsigned*>(persist.as<char>() + 96); }
+    unsigned* prev_sort_words() { return reinterpret_cast<unsigned*>(persist.as<char>() + 96); }  // 3 words
+    unsigned* grads_dirty() { return reinterpret_cast<unsigned*>(persist.as<char>() + 112); }
     unsigned* filter_flags() {
         return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control) +
                                            kMaxSortPasses * kMaxBuckets * sizeof(unsigned));
@@ -188,17 +194,18 @@ struct StageScope {
     cudaEvent_t a = nullptr;
     StageScope(gpk_session* s_, int st) : s(s_), stage(st) {
         if (!s->timing) return;
-        if (s->pending.size() >= 8192) {
+        if (s->pending.size() >= 8192 && !s->capturing) {
             cudaStreamSynchronize(s->stream);
             drain_timing(s);
         }
         a = take_event(s);
-        cudaEventRecord(a, s->stream);
+        // under capture: an external event node (device timestamp on replay)
+        cudaEventRecordWithFlags(a, s->stream, s->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
     }
     void end() {
         if (!a) return;
         cudaEvent_t b = take_event(s);
-        cudaEventRecord(b, s->stream);
+        cudaEventRecordWithFlags(b, s->stream, s->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
         s->pending.push_back({stage, a, b});
         a = nullptr;
     }
@@ -212,11 +219,10 @@ int set_device(gpk_session* s) {
 
 uint64_t filter_blocks(uint64_t n) { return std::max<uint64_t>((n + kFilterBlock - 1) / kFilterBlock, 1); }
 uint64_t exact_chunks(uint64_t n) { return std::max<uint64_t>((n + kExactChunk - 1) / kExactChunk, 1); }
-// head = Control | digit histograms | K_filter flags | K_exact flags (memset per prepare)
-// head = Control | global digit histograms | K_exact chunk words (u64)
-size_t head_size(uint64_t nbf, uint64_t nbe) {
-    (void)nbf;
-    return sizeof(Control) + kMaxSortPasses * kMaxBuckets * sizeof(unsigned) + nbe * 8;
+// head = Control | global digit histograms | chunk words (u64), memset per prepare
+size_t head_size(uint64_t n) {
+    // chunk words: K_prep uses one per 1024 Gaussians, the voxelizer one per 256
+    return sizeof(Control) + kMaxSortPasses * kMaxBuckets * sizeof(unsigned) + exact_chunks(n) * 8;
 }
 
 int clear_errors(gpk_session* s) {
@@ -263,6 +269,13 @@ int sync_and_check(gpk_session* s, const char* where) {
     return surface_errors(s, where);
 }
 
+// The gradient planes were written by something other than K_chain: the next
+// prepare clears them densely (see kGradsDense).
+int mark_grads_dense(gpk_session* s) {
+    CK(cudaMemsetAsync(s->grads_dirty(), 0xff, 4, s->stream));
+    return GPK_OK;
+}
+
 int ensure_pairs(gpk_session* s, uint64_t need) {
     if (need <= s->pair_cap && s->keys[0].p) return GPK_OK;
     const uint64_t cap = std::max<uint64_t>(need, 1ull << 16);
@@ -278,7 +291,7 @@ int ensure_pairs(gpk_session* s, uint64_t need) {
     const uint64_t region = (st_tiles + super_tiles) * kMaxBuckets;
     CK(s->sort_status.ensure((size_t)kMaxSortPasses * region * 4));
     CK(cudaMemsetAsync(s->sort_status.p, 0, s->sort_status.bytes, s->stream));
-    CK(cudaMemsetAsync(s->prev_sort_words(), 0, 8, s->stream));
+    CK(cudaMemsetAsync(s->prev_sort_words(), 0, 12, s->stream));
     s->pair_cap = cap;
     s->sort_tiles_cap = st_tiles;
     s->hist_region = region;
@@ -370,8 +383,8 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     ps.valid = true;
     ps.rasterized = false;
     ps.grads_zeroed = zero_grads;
-    const uint64_t nbf = filter_blocks(s->n), nbe = exact_chunks(s->n);
-    const size_t head_bytes = head_size(nbf, nbe);
+    const uint64_t nbf = filter_blocks(s->n);
+    const size_t head_bytes = head_size(s->n);
     StageScope scope_prep(s, GPK_STAGE_PREPARE);
     CK(cudaMemsetAsync(s->head.p, 0, head_bytes, s->stream));
     if (s->n == 0) {
@@ -383,8 +396,11 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     pl.cap = s->cap;
     pl.n = (uint32_t)s->n;
     pl.grads = zero_grads ? s->grads.as<float>() : nullptr;
-    pl.filter_counts = s->prep_vals.as<unsigned>();
-    pl.cand_local = s->cand_list.as<uint32_t>();
+    pl.surv_params = s->surv_params.as<CandParams>();
+    pl.cand = s->cand.as<CandParams>();
+    pl.cand_count = s->cand_count.as<unsigned>();
+    pl.grads_dirty = s->grads_dirty();
+    pl.dirty_idx = s->dirty_idx.as<uint32_t>();
     pl.nfilter = (unsigned)nbf;
     pl.records = s->records.as<SurvivorRecord>();
     pl.survivor_list = s->survivors.as<uint32_t>();
@@ -403,14 +419,12 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     pl.ctrl = s->ctrl();
     pl.err = s->err();
     pl.slice = a;
-    const int exact_per_sm = exact_blocks_per_sm(exact_dyn_smem((unsigned)nbf));
-    pl.exact_grid = (int)std::min<uint64_t>(nbe, (uint64_t)s->num_sms * exact_per_sm);
-    launch_filter(pl, s->num_sms, s->stream);
+    launch_prep(pl, s->num_sms, s->stream);
     CK(cudaGetLastError());
     scope_prep.end();
     {
-        StageScope scope_exact(s, GPK_STAGE_EXACT);
-        launch_exact(pl, s->stream);
+        StageScope scope_bin(s, GPK_STAGE_BIN);
+        launch_bin(pl, s->stream);
         CK(cudaGetLastError());
     }
     StageScope scope_sort(s, GPK_STAGE_SORT);
@@ -480,6 +494,7 @@ int run_backward(gpk_session* s, bool stats) {
     if (s->n == 0) return GPK_OK;
     if (!s->prep.grads_zeroed) {
         CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
+        CK(cudaMemsetAsync(s->grads_dirty(), 0, 4, s->stream));
     }
     if (stats) {
         CK(s->stat_norm.ensure(s->cap * 4));
@@ -496,7 +511,9 @@ int run_backward(gpk_session* s, bool stats) {
     }
     StageScope scope(s, GPK_STAGE_CHAIN);
     ChainLaunch c;
-    c.params = s->params.as<float>();
+    c.sparams = s->surv_params.as<CandParams>();
+    c.dirty_idx = s->dirty_idx.as<uint32_t>();
+    c.grads_dirty = s->grads_dirty();
     c.cap = s->cap;
     c.records = s->records.as<SurvivorRecord>();
     c.survivor_list = s->survivors.as<uint32_t>();
@@ -568,13 +585,16 @@ int alloc_for_n(gpk_session* s, uint64_t n) {
         CK(s->grads.ensure(cap * 11 * 4));
         CK(s->adam_m.ensure(cap * 11 * 4));
         CK(s->adam_v.ensure(cap * 11 * 4));
-        const uint64_t nbf = filter_blocks(cap), nbe = exact_chunks(cap);
+        const uint64_t nbf = filter_blocks(cap);
         CK(s->records.ensure(cap * sizeof(SurvivorRecord)));
         CK(s->cand_list.ensure(cap * 4));
+        CK(s->surv_params.ensure(cap * sizeof(CandParams)));
+        CK(s->cand.ensure(cap * sizeof(CandParams)));
+        CK(s->cand_count.ensure(nbf * 4));
+        CK(s->dirty_idx.ensure(cap * 4));
+        TRY(mark_grads_dense(s));
         CK(s->survivors.ensure(cap * 4));
-        CK(s->prep_vals.ensure(nbf * 4));
-        CK(s->cand_list.ensure(nbf * kFilterBlock * 4));
-        CK(s->head.ensure(head_size(nbf, nbe)));
+        CK(s->head.ensure(head_size(cap)));
         s->cap = cap;
     }
     s->n = n;
@@ -712,7 +732,7 @@ int run_vox_prep(gpk_session* s, const gpk_voxelizer_config* cfg) {
     CK(s->volume.ensure(vs.voxels * 4));
     CK(s->dl_dv_vol.ensure(vs.voxels * 4));
     StageScope scope(s, GPK_STAGE_VOXEL);
-    CK(cudaMemsetAsync(s->head.p, 0, head_size(filter_blocks(s->n), exact_chunks(s->n)), s->stream));
+    CK(cudaMemsetAsync(s->head.p, 0, head_size(s->n), s->stream));
     // the slice path clears only the histogram rows its previous sort used
     CK(cudaMemsetAsync(s->sort_status.p, 0, s->sort_status.bytes, s->stream));
     if (s->n == 0) return GPK_OK;
@@ -834,13 +854,20 @@ int gpk_session_destroy(gpk_session* s) {
     if (!s) return ok();
     cudaSetDevice(s->device);
     if (s->stream) cudaStreamSynchronize(s->stream);
-    for (auto& g : s->graphs) cudaGraphExecDestroy(g.exec);
+    for (auto& g : s->graphs) {
+        cudaGraphExecDestroy(g.exec);
+        for (auto& p : g.timed) {
+            cudaEventDestroy(p.a);
+            cudaEventDestroy(p.b);
+        }
+    }
     s->graphs.clear();
     DevBuf* bufs[] = {&s->params, &s->grads, &s->adam_m, &s->adam_v, &s->records, &s->survivors,
                       &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials,
-                      &s->sort_status, &s->head, &s->prep_vals, &s->persist, &s->image,
+                      &s->sort_status, &s->head, &s->persist, &s->image,
                       &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm,
-                      &s->stat_obs, &s->stat_world, &s->cand_list, &s->vox_records,
+                      &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count,
+                      &s->dirty_idx, &s->vox_records,
                       &s->volume, &s->dl_dv_vol, &s->vox_partials};
     for (DevBuf* b : bufs) b->release();
     drain_timing(s);
@@ -995,6 +1022,8 @@ int gpk_set_gradients(gpk_session* s, const float* grads) {
         CK(cudaMemcpy(s->grads.as<float>() + (size_t)k * s->cap, plane.data(), n * 4,
                       cudaMemcpyHostToDevice));
     }
+    TRY(mark_grads_dense(s));
+    CK(cudaStreamSynchronize(s->stream));
     return ok();
 }
 
@@ -1261,13 +1290,24 @@ int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* ps
 static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_session*, const void*),
                          const void* arg) {
     if (!s || !graph_id) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
-    if (s->timing) return fail(GPK_ERR_STATE, "disable stage timing before capturing a graph");
     TRY(set_device(s));
     CK(cudaStreamSynchronize(s->stream));
+    drain_timing(s);
     CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    s->capturing = true;
     const int st = body(s, arg);
+    s->capturing = false;
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(s->stream, &g);
+    // stage events recorded during capture became event-record nodes of the graph
+    std::vector<gpk_session::Pending> timed;
+    timed.swap(s->pending);
+    if (st != GPK_OK || e != cudaSuccess) {
+        for (auto& p : timed) {
+            s->event_pool.push_back(p.a);
+            s->event_pool.push_back(p.b);
+        }
+    }
     if (st != GPK_OK) {
         if (g) cudaGraphDestroy(g);
         return st;
@@ -1277,7 +1317,7 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
     const cudaError_t ei = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (ei != cudaSuccess) return fail(GPK_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
-    s->graphs.push_back({ex, s->prep});
+    s->graphs.push_back({ex, s->prep, std::move(timed)});
     *graph_id = (int32_t)s->graphs.size() - 1;
     return ok();
 }
@@ -1331,8 +1371,21 @@ int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
     if (!s || graph_id < 0 || graph_id >= (int32_t)s->graphs.size())
         return fail(GPK_ERR_INVALID_ARGUMENT, "unknown graph id");
     TRY(set_device(s));
-    CK(cudaGraphLaunch(s->graphs[graph_id].exec, s->stream));
-    s->prep = s->graphs[graph_id].prep;
+    gpk_session::Graph& g = s->graphs[graph_id];
+    CK(cudaGraphLaunch(g.exec, s->stream));
+    s->prep = g.prep;
+    if (s->timing && !g.timed.empty()) {
+        // graph captured with stage timing: its event nodes bracket each stage
+        // on the device, back to back (no host submission gaps)
+        CK(cudaStreamSynchronize(s->stream));
+        for (auto& p : g.timed) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+                s->stage_ms[p.stage] += ms;
+                s->stage_cnt[p.stage] += 1;
+            }
+        }
+    }
     return ok();
 }
 
@@ -1340,7 +1393,13 @@ int gpk_graph_destroy_all(gpk_session* s) {
     if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
     TRY(set_device(s));
     CK(cudaStreamSynchronize(s->stream));
-    for (auto& g : s->graphs) cudaGraphExecDestroy(g.exec);
+    for (auto& g : s->graphs) {
+        cudaGraphExecDestroy(g.exec);
+        for (auto& p : g.timed) {
+            s->event_pool.push_back(p.a);
+            s->event_pool.push_back(p.b);
+        }
+    }
     s->graphs.clear();
     return ok();
 }
@@ -1430,6 +1489,7 @@ int gpk_allreduce_grads(gpk_session* s) {
     const int r = api->all_reduce(s->grads.p, s->grads.p, s->cap * 11, /*ncclFloat32*/ 7,
                                   /*ncclSum*/ 0, comm, s->stream);
     if (r != 0) return fail(GPK_ERR_NCCL, "ncclAllReduce failed");
+    TRY(mark_grads_dense(s));  // non-zero wherever any rank had survivors
     return ok();
 }
 
@@ -1493,6 +1553,7 @@ int gpk_voxelize_backward(gpk_session* s, const gpk_voxelizer_config* cfg, const
     if (dl_dv)
         CK(cudaMemcpyAsync(s->dl_dv_vol.p, dl_dv, s->vox.voxels * 4, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
+    TRY(mark_grads_dense(s));
     if (s->n) {
         StageScope scope(s, GPK_STAGE_VOXEL);
         launch_vox_bwd(vox_eval_args(s), s->stream);

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
     if (blockIdx.x == 0 && tid == 0 && !a.tile_hist_next) {
         a.prev_sort_words[0] = ntiles;
         a.prev_sort_words[1] = nb;
+        a.prev_sort_words[2] = (unsigned)a.pass + 1;
     }
     const unsigned* super_rows = a.tile_hist + a.sort_tiles_cap * nb;
 
@@ -68,15 +69,39 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
             __syncthreads();
         }
         // ---- add the counts of all earlier tiles: whole super-tiles from the
-        // super rows, then the earlier tiles of this super-tile (<= 15 rows)
+        // super rows, then the earlier tiles of this super-tile (<= 15 rows).
+        // Thread owns 4 consecutive digits (one 16 B load per row); rows are
+        // unrolled so all of a thread's loads are in flight together.
         {
             const unsigned sup = t / kSuperTiles;
-            for (unsigned d = tid; d < nb; d += kSortThreads) {
+            const unsigned t0 = sup * kSuperTiles;
+            const unsigned nrows = sup + (t - t0);  // super rows first, then tile rows
+            if (nb >= 4) {
+                const unsigned d0 = tid * 4;
+                if (d0 < nb) {
+                    uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll 8
+                    for (unsigned r = 0; r < nrows; ++r) {
+                        const unsigned* row = r < sup ? super_rows + (size_t)r * nb
+                                                      : a.tile_hist + (size_t)(t0 + r - sup) * nb;
+                        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(row + d0));
+                        acc.x += v.x;
+                        acc.y += v.y;
+                        acc.z += v.z;
+                        acc.w += v.w;
+                    }
+                    s_base[d0] += acc.x;
+                    s_base[d0 + 1] += acc.y;
+                    s_base[d0 + 2] += acc.z;
+                    s_base[d0 + 3] += acc.w;
+                }
+            } else if ((unsigned)tid < nb) {
                 unsigned acc = 0;
-                for (unsigned j = 0; j < sup; ++j) acc += super_rows[(size_t)j * nb + d];
-                for (unsigned j = sup * kSuperTiles; j < t; ++j) acc += a.tile_hist[(size_t)j * nb + d];
-                s_base[d] += acc;
+                for (unsigned r = 0; r < nrows; ++r)
+                    acc += r < sup ? super_rows[(size_t)r * nb + tid] : a.tile_hist[(size_t)(t0 + r - sup) * nb + tid];
+                s_base[tid] += acc;
             }
+            __syncthreads();
         }
 
         // ---- rank: warp-local stable ranks via match_any -----------------

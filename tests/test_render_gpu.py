@@ -249,6 +249,45 @@ def test_graph_replay_equals_direct(gp, session):
     session.graph_destroy_all()
 
 
+def test_dense_gradients_after_sparse_clear(gp, session):
+    """The gradient planes are cleared sparsely (previous survivors only) between
+    fused steps: every step must still leave the exact dense gradient, whatever
+    wrote the planes before (another slice, set_gradients, voxelize_backward,
+    a graph replay)."""
+    from paper_2603_20611_b200 import _native as N
+
+    dims = (128, 128, 32)
+    gs = stack_scene(gp, 20000, dims, seed=8)
+    poses = [gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), k) for k in (3, 28, 15)]
+    dl = (np.random.default_rng(6).uniform(-1, 1, (128, 128)) / 16384).astype(np.float32)
+    psf, rc = gp.PsfSpec(), gp.RasterConfig()
+    # expected: staged path (dense memset + backward) on a fresh session
+    want = []
+    with gp.Session(0) as fresh:
+        fresh.set_gaussians(gs)
+        for p in poses:
+            fresh.prepare(p, psf, rc)
+            fresh.rasterize()
+            want.append(fresh.backward(dl))
+    session.set_gaussians(gs)
+    session.fwd_bwd_slice(poses[0], psf, rc)
+    session.upload(N.GPK_BUF_DL_DI, dl.ctypes.data, dl.nbytes)
+    for k in (0, 1, 2, 0, 2, 1):
+        session.fwd_bwd_slice(poses[k], psf, rc)
+        assert np.array_equal(session.get_gradients(), want[k]), k
+    session.set_gradients(np.full((gs.size(), 11), 7.0, np.float32))
+    session.fwd_bwd_slice(poses[1], psf, rc)
+    assert np.array_equal(session.get_gradients(), want[1])
+    session.voxelize_backward(gp.VoxelizerConfig(dims=(32, 32, 8)), np.ones((8, 32, 32), np.float32))
+    session.fwd_bwd_slice(poses[2], psf, rc)
+    assert np.array_equal(session.get_gradients(), want[2])
+    gids = [session.capture_fwd_bwd(p, psf, rc) for p in poses]
+    for k in (2, 0, 1, 1, 0):
+        session.graph_launch(gids[k])
+        assert np.array_equal(session.get_gradients(), want[k]), k
+    session.graph_destroy_all()
+
+
 def test_c2_full_size_bitexact_binning(gp, session, ref):
     """C2 (512^2 x 128, 1M Gaussians): survivors, bounds and tile lists bit-exact;
     image and gradients within tolerance of the reference."""

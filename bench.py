@@ -256,6 +256,7 @@ def run_ours(args):
 
     import paper_2603_20611_b200 as gp
     from paper_2603_20611_b200 import _native as N
+    from paper_2603_20611_b200 import dp
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -284,15 +285,7 @@ def run_ours(args):
     poses = [gp.slice_pose_for_index(cfg["dims"], (1, 1, 1), (0, 0, 0), k) for k in ks]
 
     if world > 1:
-        uid = bytearray(128)
-        if rank == 0:
-            buf = (gp.api.C.c_char * 128)()
-            N.check(N.lib.gpk_nccl_get_unique_id(buf))
-            uid = bytearray(bytes(buf))
-        obj = [bytes(uid)]
-        dist.broadcast_object_list(obj, src=0)
-        idbuf = (gp.api.C.c_char * 128).from_buffer_copy(obj[0])
-        N.check(N.lib.gpk_comm_init(sess.handle, world, rank, idbuf))
+        dp.init_grad_comm(sess, rank, world)
 
     # first slice allocates the image-sized buffers, then upload the fixed dL/dI
     sess.fwd_bwd_slice(poses[0], psf, rcfg)
@@ -323,13 +316,13 @@ def run_ours(args):
     graphs = [sess.capture_fwd_bwd(p, psf, rcfg) for p in poses] if args.graphs else None
 
     def step(i, use_graph=True):
-        k = (rank + i * world) % len(poses)
+        k = dp.slice_for(i, rank, world, len(poses))
         if graphs is not None and use_graph:
             sess.graph_launch(graphs[k])
         else:
             sess.fwd_bwd_slice(poses[k], psf, rcfg)
         if world > 1:
-            N.check(N.lib.gpk_allreduce_grads(sess.handle))
+            dp.allreduce_grads(sess)
 
     for i in range(args.warmup):
         step(i)
@@ -361,7 +354,7 @@ def run_ours(args):
     sess.stage_times(reset=True)
     for i in range(prof_steps):
         flush.fill_(float(i))
-        sess.graph_launch(prof_graphs[(rank + (args.warmup + i) * world) % len(poses)])
+        sess.graph_launch(prof_graphs[dp.slice_for(args.warmup + i, rank, world, len(poses))])
     sess.stage_timing(False)
     stages = sess.stage_times(reset=True)
     t = torch.tensor([total_ms], device="cuda")

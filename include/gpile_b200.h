@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GPK_ABI_VERSION 1
+#define GPK_ABI_VERSION 2
 #define GPK_RECORD_FLOATS 11
 
 typedef enum {

@@ -405,6 +405,31 @@ int gor_rasterize(uint64_t n, const double* rec, const gpk_slice_pose* pose, con
     return ok();
 }
 
+/* rasterize_naive (render.hpp:203-219): survivors in set order, each over its
+ * whole pixel box — the all-pairs oracle the tiled path must equal bitwise. */
+int gor_rasterize_naive(uint64_t n, const double* rec, const gpk_slice_pose* pose, const gpk_psf* psf,
+                        const gpk_raster_config* cfg, double* image) {
+    if (validate_psf(psf)) return GPK_ERR_INVALID_ARGUMENT;
+    prep_t* P;
+    uint64_t S;
+    int st = prepare_all(n, rec, pose, psf, cfg, &P, &S);
+    if (st) return st;
+    const int W = pose->width, H = pose->height;
+    memset(image, 0, sizeof(double) * (size_t)W * H);
+    for (uint64_t k = 0; k < S; ++k) {
+        const prep_t* p = &P[k];
+        for (int j = p->lo_y; j <= p->hi_y; ++j)
+            for (int i = p->lo_x; i <= p->hi_x; ++i) {
+                const double dx = (i - pose->principal_point[0]) * pose->pixel_spacing[0] - p->mux;
+                const double dy = (j - pose->principal_point[1]) * pose->pixel_spacing[1] - p->muy;
+                const double e = p->ka * dx * dx + 2.0 * p->kb * dx * dy + p->kd * dy * dy;
+                image[(size_t)j * W + i] += p->at * exp(-0.5 * e);
+            }
+    }
+    free(P);
+    return ok();
+}
+
 /* ---- backward.hpp + grad_chain.hpp ---------------------------------------- */
 static void rotation_backward(const double q[4], m3 g, double out[4]) { /* grad_chain.hpp:27-40 */
     const double w = q[0], x = q[1], y = q[2], z = q[3];

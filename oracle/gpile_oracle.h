@@ -35,6 +35,9 @@ int gor_tile_lists(uint64_t n, const double* rec, const gpk_slice_pose* pose, co
 /* rasterize_slice (render.hpp:194). */
 int gor_rasterize(uint64_t n, const double* rec, const gpk_slice_pose* pose, const gpk_psf* psf,
                   const gpk_raster_config* cfg, double* image);
+/* rasterize_naive (render.hpp:203-219). */
+int gor_rasterize_naive(uint64_t n, const double* rec, const gpk_slice_pose* pose, const gpk_psf* psf,
+                        const gpk_raster_config* cfg, double* image);
 /* backward_slice (backward.hpp:189). */
 int gor_backward(uint64_t n, const double* rec, const gpk_slice_pose* pose, const gpk_psf* psf,
                  const gpk_raster_config* cfg, const double* dl_di, double* grads,

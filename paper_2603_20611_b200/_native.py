@@ -13,6 +13,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libgpile_b200.so"
+GPK_ABI_VERSION = 2  # include/gpile_b200.h
 
 GPK_OK = 0
 GPK_ERR_INVALID_ARGUMENT = 1
@@ -167,6 +168,8 @@ for _name, (_res, _args) in _PROTOS.items():
     _fn = getattr(lib, _name)
     _fn.restype = _res
     _fn.argtypes = _args
+if lib.gpk_abi_version() != GPK_ABI_VERSION:
+    raise ImportError(f"{LIB_PATH}: ABI {lib.gpk_abi_version()} != {GPK_ABI_VERSION}; rebuild the library")
 
 
 # ---- error mapping (errors.hpp:9-27 + std::invalid_argument) --------------------

@@ -362,6 +362,10 @@ class Session:
         hp = N.AdamHparamsC(beta1, beta2, eps)
         check(N.lib.gpk_adam_step(self._h, C.byref(l), C.byref(hp)))
 
+    def adam_reset(self):
+        """AdamState reset: zero moments, step 0."""
+        check(N.lib.gpk_adam_reset(self._h))
+
     def adam_state(self) -> tuple[np.ndarray, np.ndarray, int]:
         m = np.zeros((self.n, RECORD), np.float32)
         v = np.zeros((self.n, RECORD), np.float32)

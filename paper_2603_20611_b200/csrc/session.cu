@@ -129,9 +129,11 @@ struct gpk_session {
     struct Graph {
         cudaGraphExec_t exec;
         PrepState prep;
+        uint64_t alloc_epoch;
         std::vector<Pending> timed;  // event-record nodes captured with stage timing on
     };
     bool capturing = false;
+    uint64_t alloc_epoch = 0;  // bumped whenever a buffer a captured graph may use is reallocated
     std::vector<Graph> graphs;
 
     // live stage timing
@@ -284,6 +286,7 @@ int ensure_pairs(gpk_session* s, uint64_t need) {
         CK(s->vals[b].ensure(cap * 4));
     }
     CK(s->partials.ensure(cap * 24));
+    ++s->alloc_epoch;
     // per-sort-tile digit counts of every pass (kept zero between prepares:
     // K_filter clears the rows the previous prepare used)
     const uint64_t st_tiles = (cap + kSortTile - 1) / kSortTile;
@@ -300,9 +303,11 @@ int ensure_pairs(gpk_session* s, uint64_t need) {
 
 int ensure_image(gpk_session* s, int w, int h) {
     const size_t px = (size_t)w * h;
+    const void* before[3] = {s->image.p, s->dl_di.p, s->target.p};
     CK(s->image.ensure(px * 4));
     CK(s->dl_di.ensure(px * 4));
     CK(s->target.ensure(px * 4));
+    if (before[0] != s->image.p || before[1] != s->dl_di.p || before[2] != s->target.p) ++s->alloc_epoch;
     s->img_w = w;
     s->img_h = h;
     return GPK_OK;
@@ -596,6 +601,7 @@ int alloc_for_n(gpk_session* s, uint64_t n) {
         CK(s->survivors.ensure(cap * 4));
         CK(s->head.ensure(head_size(cap)));
         s->cap = cap;
+        ++s->alloc_epoch;
     }
     s->n = n;
     return GPK_OK;
@@ -649,8 +655,13 @@ int run_loss(gpk_session* s, double lambda, double dssim_scale) {
     if (!s->prep.rasterized) return fail(GPK_ERR_STATE, "photometric_loss: no rendered image");
     const int W = s->img_w, H = s->img_h;
     const size_t px = (size_t)W * H;
+    const void* before[2] = {s->loss_g.p, s->loss_partial.p};
     if (lambda != 0.0) CK(s->loss_g.ensure(px * 12));
     CK(s->loss_partial.ensure((size_t)loss_partial_blocks(W, H, lambda) * 16));
+    if (before[0] != s->loss_g.p || before[1] != s->loss_partial.p) {
+        if (s->capturing) return fail(GPK_ERR_STATE, "loss buffers must be sized before capture");
+        ++s->alloc_epoch;
+    }
     LossLaunch l;
     l.image = s->image.as<float>();
     l.target = s->target.as<float>();
@@ -941,9 +952,20 @@ int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
 }
 
 int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    // image-shaped inputs may be staged before the first slice sized them
+    DevBuf* grow = which == GPK_BUF_DL_DI ? &s->dl_di : which == GPK_BUF_TARGET ? &s->target
+                 : which == GPK_BUF_DL_DV ? &s->dl_dv_vol : nullptr;
+    if (grow && host && bytes > grow->bytes) {
+        TRY(set_device(s));
+        CK(cudaStreamSynchronize(s->stream));
+        CK(grow->ensure(bytes));
+        ++s->alloc_epoch;
+    }
     void* p = nullptr;
     uint64_t cap = 0;
     TRY(gpk_device_buffer(s, which, &p, &cap));
+    if (grow) cap = grow->bytes;
     if (!host || bytes > cap) return fail(GPK_ERR_INVALID_ARGUMENT, "upload: size exceeds buffer");
     TRY(set_device(s));
     CK(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, s->stream));
@@ -1317,7 +1339,7 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
     const cudaError_t ei = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (ei != cudaSuccess) return fail(GPK_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
-    s->graphs.push_back({ex, s->prep, std::move(timed)});
+    s->graphs.push_back({ex, s->prep, s->alloc_epoch, std::move(timed)});
     *graph_id = (int32_t)s->graphs.size() - 1;
     return ok();
 }
@@ -1337,8 +1359,28 @@ struct TrainArgs {
     int total;
 };
 
+// Size every buffer the captured step touches (allocation is illegal under capture).
+static int presize_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                        const gpk_raster_config* cfg, bool loss, double lambda) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    SliceArgs a;
+    TRY(make_slice(s, pose, psf, cfg, a));
+    TRY(ensure_image(s, a.W, a.H));
+    if (!s->keys[0].p) TRY(ensure_pairs(s, std::max<uint64_t>(1ull << 20, 8 * s->n)));
+    if (loss) {
+        const size_t px = (size_t)a.W * a.H;
+        const void* before[2] = {s->loss_g.p, s->loss_partial.p};
+        if (lambda != 0.0) CK(s->loss_g.ensure(px * 12));
+        CK(s->loss_partial.ensure((size_t)loss_partial_blocks(a.W, a.H, lambda) * 16));
+        if (before[0] != s->loss_g.p || before[1] != s->loss_partial.p) ++s->alloc_epoch;
+    }
+    return GPK_OK;
+}
+
 int gpk_graph_capture_fwd_bwd(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                               const gpk_raster_config* cfg, int32_t* graph_id) {
+    TRY(presize_step(s, pose, psf, cfg, false, 0.0));
     const FwdBwdArgs args{pose, psf, cfg};
     return capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
         const FwdBwdArgs* a = static_cast<const FwdBwdArgs*>(p);
@@ -1354,6 +1396,7 @@ int gpk_graph_capture_train(gpk_session* s, const gpk_slice_pose* pose, const gp
                             const gpk_learning_rates* lr0, int32_t total_iterations,
                             int32_t* graph_id) {
     if (!lr0 || total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "bad learning rates");
+    TRY(presize_step(s, pose, psf, cfg, true, lambda));
     const TrainArgs args{pose, psf, cfg, lambda, dssim_scale, lr0, total_iterations};
     return capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
         const TrainArgs* a = static_cast<const TrainArgs*>(p);
@@ -1372,6 +1415,8 @@ int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
         return fail(GPK_ERR_INVALID_ARGUMENT, "unknown graph id");
     TRY(set_device(s));
     gpk_session::Graph& g = s->graphs[graph_id];
+    if (g.alloc_epoch != s->alloc_epoch)
+        return fail(GPK_ERR_STATE, "graph invalidated: session buffers were reallocated since capture; recapture");
     CK(cudaGraphLaunch(g.exec, s->stream));
     s->prep = g.prep;
     if (s->timing && !g.timed.empty()) {

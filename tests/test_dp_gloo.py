@@ -1,0 +1,123 @@
+"""CPU, world_size 2 over gloo: the host side of slice-sharded data parallelism
+(paper_2603_20611_b200/dp.py).
+
+* the slice schedule deals distinct slices to the ranks of a step and covers
+  the schedule;
+* the NCCL unique id created on rank 0 reaches every rank intact;
+* max-over-ranks timing reduction;
+* the exchange algebra: each rank's dense gradient of its own slice (the C
+  oracle stands in for the device backward), summed by an all-reduce, equals
+  the serial sum over the step's slices — what ncclAllReduce(sum) over the
+  11-plane buffer computes on the GPUs.
+"""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _scene():
+    from types import SimpleNamespace as NS
+
+    rng = np.random.default_rng(0)
+    n = 300
+    rec = np.zeros((n, 11))
+    rec[:, 0] = rng.uniform(0, 32, n)
+    rec[:, 1] = rng.uniform(0, 24, n)
+    rec[:, 2] = rng.uniform(0, 8, n)
+    rec[:, 3:6] = np.log(rng.uniform(0.8, 1.6, (n, 3)))
+    q = rng.normal(size=(n, 4))
+    rec[:, 6:10] = q / np.linalg.norm(q, axis=1, keepdims=True)
+    rec[:, 10] = rng.uniform(-3, 0, n)
+    poses = [NS(rotation=np.eye(3), translation=(0.0, 0.0, -float(k)), width=32, height=24,
+                pixel_spacing=(1.0, 1.0), principal_point=(0.0, 0.0)) for k in range(8)]
+    psf = NS(sigma_x=1.0, sigma_y=1.0, sigma_z=1.0)
+    cfg = NS(tau=0.02, tile_size=16, footprint_sigmas=3.0, scale_modifier=1.0)
+    dl = [np.random.default_rng(10 + k).uniform(-1, 1, (24, 32)) for k in range(8)]
+    return rec, poses, psf, cfg, dl
+
+
+def _worker(rank, world, port, q):
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    from oracle.bindings import load
+    from paper_2603_20611_b200 import dp
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = {}
+        out["uid"] = dp.exchange_unique_id(rank, make_id=lambda: bytes(range(128)))
+        out["max"] = dp.max_over_ranks([float(rank), 10.0 - rank])
+        oracle = load("oracle")
+        rec, poses, psf, cfg, dl = _scene()
+        sums = []
+        for step in range(3):
+            k = dp.slice_for(step, rank, world, len(poses))
+            g, _ = oracle.backward(rec, poses[k], psf, cfg, dl[k])
+            t = torch.from_numpy(np.ascontiguousarray(g))
+            dist.all_reduce(t)  # the exchange: sum of per-slice dense gradients
+            sums.append(t.numpy().copy())
+        out["sums"] = sums
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slice_schedule_partitions_each_step():
+    from paper_2603_20611_b200 import dp
+
+    for world in (1, 2, 4, 8):
+        n = 16
+        seen = []
+        for step in range(n // world):
+            ks = dp.step_slices(step, world, n)
+            assert len(set(ks)) == world
+            seen += ks
+        assert sorted(seen) == list(range(n))
+    with pytest.raises(ValueError):
+        dp.slice_for(0, 2, 2, 4)
+
+
+def test_gloo_world2_exchange():
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0]["uid"] == res[1]["uid"] == bytes(range(128))
+    assert res[0]["max"] == res[1]["max"] == [1.0, 10.0]
+
+    sys.path.insert(0, str(ROOT))
+    from oracle.bindings import load
+    from paper_2603_20611_b200 import dp
+
+    oracle = load("oracle")
+    rec, poses, psf, cfg, dl = _scene()
+    for step in range(3):
+        want = sum(oracle.backward(rec, poses[k], psf, cfg, dl[k])[0] for k in dp.step_slices(step, 2, len(poses)))
+        for r in (0, 1):
+            assert np.allclose(res[r]["sums"][step], want, rtol=1e-12, atol=1e-15)
+        assert np.array_equal(res[0]["sums"][step], res[1]["sums"][step])  # replicas stay equal

@@ -1,0 +1,447 @@
+// gpile_b200.hpp — C++ drop-in for the reference's slice-renderer hot path
+// (GaussianPile, proj/include/gpile) on the B200 C-ABI
+// (gpile_b200.h). The types are the reference's own — include this header
+// where the reference headers are on the include path — and every function
+// keeps the reference signature, argument meaning and exception types:
+//
+//   reference (namespace gpile)                 drop-in (namespace gpile::b200)
+//   prepare_gaussians     render.hpp:83         prepare_gaussians
+//   rasterize_prepared    render.hpp:166        rasterize_prepared
+//   rasterize_slice       render.hpp:194        rasterize_slice
+//   backward_prepared     backward.hpp:97       backward_prepared
+//   backward_slice        backward.hpp:189      backward_slice
+//   photometric_loss      loss.hpp:13           photometric_loss
+//   lr_at                 optimize.hpp:71       lr_at
+//   adam_step             optimize.hpp:195      adam_step
+//   voxelize              voxelize.hpp:113      voxelize
+//   voxelize_backward     voxelize.hpp:152      voxelize_backward
+//
+// Errors: GPK_ERR_INVALID_ARGUMENT -> std::invalid_argument,
+// GPK_ERR_DEGENERATE_COVARIANCE -> gpile::DegenerateCovariance,
+// GPK_ERR_NUMERIC_FAILURE -> gpile::NumericFailure (message names the first
+// failing primitive, as backward.hpp:182-184), anything else ->
+// std::runtime_error. Calls are blocking, like the reference's.
+//
+// The free functions marshal the GaussianSet (AoS f64 -> f32 records) per
+// call, as the reference's value semantics require. For throughput keep the
+// parameters resident: use gpile::b200::Session (set_gaussians once, then
+// fwd_bwd / train_step, parameters never leave HBM).
+//
+// PreparedGaussian: the device keeps the prepared slice; the vector returned
+// by prepare_gaussians carries index, alpha_tilde, mu_2d, conic and the pixel
+// bounds (the fields the pixel kernels consume), and acts as the handle that
+// rasterize_prepared / backward_prepared must be given (the most recent
+// prepare on this thread's default session).
+#pragma once
+
+#include <gpile/backward.hpp>
+#include <gpile/core.hpp>
+#include <gpile/errors.hpp>
+#include <gpile/image.hpp>
+#include <gpile/loss.hpp>
+#include <gpile/optimize.hpp>
+#include <gpile/render.hpp>
+#include <gpile/voxelize.hpp>
+
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "gpile_b200.h"
+
+namespace gpile {
+namespace b200 {
+
+inline void check(int status) {
+    if (status == GPK_OK) return;
+    const char* m = gpk_last_error_message();
+    const std::string msg = m ? m : "gpile_b200 error";
+    switch (status) {
+        case GPK_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case GPK_ERR_DEGENERATE_COVARIANCE: throw DegenerateCovariance(msg);
+        case GPK_ERR_NUMERIC_FAILURE: throw NumericFailure(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+namespace detail {
+
+inline std::vector<float> records_of(const GaussianSet& set) {
+    std::vector<float> r(set.size() * 11);
+    for (std::size_t i = 0; i < set.size(); ++i) {
+        const GaussianPrimitive& g = set.primitives[i];
+        const double v[11] = {g.mu.x, g.mu.y, g.mu.z, g.log_scale.x, g.log_scale.y, g.log_scale.z,
+                              g.quat.w, g.quat.x, g.quat.y, g.quat.z, g.alpha_raw};
+        for (int k = 0; k < 11; ++k) r[11 * i + k] = static_cast<float>(v[k]);
+    }
+    return r;
+}
+
+inline void store_records(const std::vector<float>& r, GaussianSet& set) {
+    for (std::size_t i = 0; i < set.size(); ++i) {
+        GaussianPrimitive& g = set.primitives[i];
+        const float* v = &r[11 * i];
+        g.mu = {v[0], v[1], v[2]};
+        g.log_scale = {v[3], v[4], v[5]};
+        g.quat = {v[6], v[7], v[8], v[9]};
+        g.alpha_raw = v[10];
+    }
+}
+
+inline GaussianGradients grads_of(const std::vector<float>& r, std::size_t n) {
+    GaussianGradients g(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const float* v = &r[11 * i];
+        g.d_mu[i] = {v[0], v[1], v[2]};
+        g.d_log_scale[i] = {v[3], v[4], v[5]};
+        g.d_quat[i] = {v[6], v[7], v[8], v[9]};
+        g.d_alpha_raw[i] = v[10];
+    }
+    return g;
+}
+
+inline std::vector<float> records_of(const GaussianGradients& g) {
+    std::vector<float> r(g.size() * 11);
+    for (std::size_t i = 0; i < g.size(); ++i) {
+        const double v[11] = {g.d_mu[i].x, g.d_mu[i].y, g.d_mu[i].z, g.d_log_scale[i].x, g.d_log_scale[i].y,
+                              g.d_log_scale[i].z, g.d_quat[i].w, g.d_quat[i].x, g.d_quat[i].y, g.d_quat[i].z,
+                              g.d_alpha_raw[i]};
+        for (int k = 0; k < 11; ++k) r[11 * i + k] = static_cast<float>(v[k]);
+    }
+    return r;
+}
+
+inline gpk_bounds bounds_of(const Bounds& b) {
+    return {{b.min.x, b.min.y, b.min.z}, {b.max.x, b.max.y, b.max.z}};
+}
+
+inline gpk_slice_pose pose_of(const SlicePose& p) {
+    gpk_slice_pose c;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) c.rotation[3 * i + j] = p.rotation.m[i][j];
+    c.translation[0] = p.translation.x;
+    c.translation[1] = p.translation.y;
+    c.translation[2] = p.translation.z;
+    c.width = p.width;
+    c.height = p.height;
+    c.pixel_spacing[0] = p.pixel_spacing.x;
+    c.pixel_spacing[1] = p.pixel_spacing.y;
+    c.principal_point[0] = p.principal_point.x;
+    c.principal_point[1] = p.principal_point.y;
+    return c;
+}
+
+inline gpk_psf psf_of(const PsfSpec& f) { return {f.sigma_x, f.sigma_y, f.sigma_z}; }
+
+inline gpk_raster_config cfg_of(const RasterConfig& c) {
+    return {c.tau, c.tile_size, c.footprint_sigmas, c.scale_modifier};
+}
+
+inline gpk_voxelizer_config vcfg_of(const VoxelizerConfig& v) {
+    gpk_voxelizer_config c;
+    for (int d = 0; d < 3; ++d) {
+        c.dims[d] = v.dims[d];
+        c.tile_dims[d] = v.tile_dims[d];
+    }
+    c.spacing[0] = v.spacing.x;
+    c.spacing[1] = v.spacing.y;
+    c.spacing[2] = v.spacing.z;
+    c.origin[0] = v.origin.x;
+    c.origin[1] = v.origin.y;
+    c.origin[2] = v.origin.z;
+    c.support_sigmas = v.support_sigmas;
+    c.scale_modifier = v.scale_modifier;
+    return c;
+}
+
+inline std::vector<float> pixels_of(const SliceImage& img) {
+    return std::vector<float>(img.pixels.begin(), img.pixels.end());
+}
+
+}  // namespace detail
+
+// One session per GPU: parameters, gradients and Adam moments stay in HBM.
+class Session {
+  public:
+    explicit Session(int device = 0, void* cuda_stream = nullptr) { check(gpk_session_create(device, cuda_stream, &s_)); }
+    ~Session() {
+        if (s_) gpk_session_destroy(s_);
+    }
+    Session(const Session&) = delete;
+    Session& operator=(const Session&) = delete;
+    Session(Session&& o) noexcept : s_(std::exchange(o.s_, nullptr)) {}
+
+    gpk_session* handle() const { return s_; }
+
+    void set_gaussians(const GaussianSet& set) {
+        const std::vector<float> r = detail::records_of(set);
+        const gpk_bounds b = detail::bounds_of(set.bbox);
+        check(gpk_set_gaussians(s_, set.size(), r.data(), &b));
+    }
+    // Parameters back into `set` (same size as uploaded).
+    void get_gaussians(GaussianSet& set) const {
+        std::vector<float> r(set.size() * 11);
+        check(gpk_get_gaussians(s_, r.data()));
+        detail::store_records(r, set);
+    }
+
+    std::vector<PreparedGaussian> prepare(const SlicePose& pose, const PsfSpec& psf, const RasterConfig& cfg) {
+        const gpk_slice_pose p = detail::pose_of(pose);
+        const gpk_psf f = detail::psf_of(psf);
+        const gpk_raster_config c = detail::cfg_of(cfg);
+        check(gpk_prepare(s_, &p, &f, &c));
+        uint64_t S = 0, T = 0;
+        check(gpk_prepared_count(s_, &S, &T));
+        std::vector<uint32_t> idx(S);
+        std::vector<int32_t> bnd(4 * S);
+        std::vector<double> fld(6 * S);
+        if (S) check(gpk_get_prepared(s_, idx.data(), bnd.data(), fld.data()));
+        std::vector<PreparedGaussian> out(S);
+        for (uint64_t k = 0; k < S; ++k) {
+            PreparedGaussian& g = out[k];
+            g.index = idx[k];
+            g.lo_x = bnd[4 * k];
+            g.hi_x = bnd[4 * k + 1];
+            g.lo_y = bnd[4 * k + 2];
+            g.hi_y = bnd[4 * k + 3];
+            g.alpha_tilde = fld[6 * k];
+            g.mu_2d = {fld[6 * k + 1], fld[6 * k + 2]};
+            g.conic = {fld[6 * k + 3], fld[6 * k + 4], fld[6 * k + 4], fld[6 * k + 5]};
+        }
+        pose_ = pose;
+        return out;
+    }
+
+    SliceImage rasterize() {
+        SliceImage img(pose_.width, pose_.height);
+        std::vector<float> px(img.size());
+        check(gpk_rasterize(s_, px.data()));
+        std::copy(px.begin(), px.end(), img.pixels.begin());
+        return img;
+    }
+
+    GaussianGradients backward(const SliceImage& dl_di, ScreenGradStats* stats = nullptr) {
+        if (dl_di.width != pose_.width || dl_di.height != pose_.height)
+            throw std::invalid_argument("backward_prepared: dl_di shape mismatch");  // backward.hpp:102-103
+        uint64_t n = 0;
+        check(gpk_gaussian_count(s_, &n));
+        const std::vector<float> dl = detail::pixels_of(dl_di);
+        std::vector<float> g(n * 11);
+        std::vector<double> nrm, wld;
+        std::vector<uint8_t> obs;
+        gpk_screen_stats st{};
+        if (stats) {
+            nrm.resize(n);
+            obs.resize(n);
+            wld.resize(3 * n);
+            st = {nrm.data(), obs.data(), wld.data()};
+        }
+        check(gpk_backward(s_, dl.data(), g.data(), stats ? &st : nullptr));
+        if (stats) {
+            *stats = ScreenGradStats(n);
+            for (uint64_t i = 0; i < n; ++i) {
+                stats->mu2d_grad_norm[i] = nrm[i];
+                stats->observed[i] = obs[i];
+                stats->world_pos_grad[i] = {wld[3 * i], wld[3 * i + 1], wld[3 * i + 2]};
+            }
+        }
+        return detail::grads_of(g, n);
+    }
+
+    // U1 / U2 on resident parameters; dL/dI resp. the target come from the
+    // session buffers (gpk_upload GPK_BUF_DL_DI / GPK_BUF_TARGET).
+    void fwd_bwd(const SlicePose& pose, const PsfSpec& psf, const RasterConfig& cfg) {
+        const gpk_slice_pose p = detail::pose_of(pose);
+        const gpk_psf f = detail::psf_of(psf);
+        const gpk_raster_config c = detail::cfg_of(cfg);
+        check(gpk_fwd_bwd_slice(s_, &p, &f, &c));
+        pose_ = pose;
+    }
+    void train_step(const SlicePose& pose, const PsfSpec& psf, const RasterConfig& cfg, double lambda,
+                    double dssim_scale, const LearningRates& lr0, int total_iterations) {
+        const gpk_slice_pose p = detail::pose_of(pose);
+        const gpk_psf f = detail::psf_of(psf);
+        const gpk_raster_config c = detail::cfg_of(cfg);
+        const gpk_learning_rates l{lr0.position, lr0.opacity, lr0.scale, lr0.rotation};
+        check(gpk_train_step(s_, &p, &f, &c, lambda, dssim_scale, &l, total_iterations));
+        pose_ = pose;
+    }
+
+  private:
+    gpk_session* s_ = nullptr;
+    SlicePose pose_{};
+};
+
+namespace detail {
+
+// This thread's session on device 0 and the handle of its last prepare.
+struct ThreadState {
+    std::unique_ptr<Session> session;
+    const void* prepared_data = nullptr;
+    std::size_t prepared_size = 0;
+    std::size_t set_size = 0;
+};
+
+inline ThreadState& state() {
+    thread_local ThreadState st;
+    if (!st.session) st.session = std::make_unique<Session>(0);
+    return st;
+}
+
+inline void require_last(const std::vector<PreparedGaussian>& prepared) {
+    const ThreadState& st = state();
+    if (prepared.data() != st.prepared_data || prepared.size() != st.prepared_size)
+        throw std::logic_error(
+            "gpile::b200: prepared vector is not the result of this thread's last prepare_gaussians");
+}
+
+}  // namespace detail
+
+inline Session& default_session() { return *detail::state().session; }
+
+// ---- render.hpp ------------------------------------------------------------------
+inline std::vector<PreparedGaussian> prepare_gaussians(const GaussianSet& set, const SlicePose& pose,
+                                                       const PsfSpec& psf, const RasterConfig& cfg) {
+    detail::ThreadState& st = detail::state();
+    st.session->set_gaussians(set);
+    std::vector<PreparedGaussian> out = st.session->prepare(pose, psf, cfg);
+    st.prepared_data = out.data();
+    st.prepared_size = out.size();
+    st.set_size = set.size();
+    return out;
+}
+
+inline SliceImage rasterize_prepared(const std::vector<PreparedGaussian>& prepared, const SlicePose& pose,
+                                     const RasterConfig& cfg) {
+    (void)pose;
+    (void)cfg;
+    detail::require_last(prepared);
+    return detail::state().session->rasterize();
+}
+
+inline SliceImage rasterize_slice(const GaussianSet& set, const SlicePose& pose, const PsfSpec& psf,
+                                  const RasterConfig& cfg = {}) {
+    const auto prep = b200::prepare_gaussians(set, pose, psf, cfg);  // qualified: ADL also finds gpile::
+    return b200::rasterize_prepared(prep, pose, cfg);
+}
+
+// ---- backward.hpp ----------------------------------------------------------------
+inline GaussianGradients backward_prepared(const GaussianSet& set, const std::vector<PreparedGaussian>& prepared,
+                                           const SlicePose& pose, const SliceImage& dl_di,
+                                           const RasterConfig& cfg, ScreenGradStats* stats = nullptr) {
+    (void)pose;
+    (void)cfg;
+    detail::require_last(prepared);
+    if (set.size() != detail::state().set_size)
+        throw std::invalid_argument("backward_prepared: set does not match the prepared slice");
+    return detail::state().session->backward(dl_di, stats);
+}
+
+inline GaussianGradients backward_slice(const GaussianSet& set, const SlicePose& pose, const PsfSpec& psf,
+                                        const SliceImage& dl_di, const RasterConfig& cfg = {},
+                                        ScreenGradStats* stats = nullptr) {
+    const auto prep = b200::prepare_gaussians(set, pose, psf, cfg);
+    return b200::backward_prepared(set, prep, pose, dl_di, cfg, stats);
+}
+
+// ---- loss.hpp --------------------------------------------------------------------
+inline double photometric_loss(const SliceImage& rendered, const SliceImage& target, double lambda,
+                               SliceImage& dl_di, double dssim_scale = 0.5) {
+    if (rendered.width != target.width || rendered.height != target.height)
+        throw std::invalid_argument("photometric_loss: image shape mismatch");  // loss.hpp:15-16
+    const std::vector<float> r = detail::pixels_of(rendered), t = detail::pixels_of(target);
+    std::vector<float> dl(r.size());
+    double loss = 0.0;
+    check(gpk_photometric_loss_images(default_session().handle(), rendered.width, rendered.height, r.data(),
+                                      t.data(), lambda, dssim_scale, &loss, dl.data()));
+    dl_di = SliceImage(rendered.width, rendered.height);
+    std::copy(dl.begin(), dl.end(), dl_di.pixels.begin());
+    return loss;
+}
+
+// ---- optimize.hpp ----------------------------------------------------------------
+inline double lr_at(double lr0, int iteration, int total) { return gpk_lr_at(lr0, iteration, total); }
+
+inline void adam_step(GaussianSet& set, const GaussianGradients& grads, AdamState& state,
+                      const LearningRates& lrs) {
+    const std::size_t n = set.size();
+    if (grads.size() != n || state.m_a.size() != n)
+        throw std::invalid_argument("adam_step: size mismatch");  // optimize.hpp:197-198
+    Session& s = default_session();
+    s.set_gaussians(set);
+    std::vector<float> m(n * 11), v(n * 11);
+    for (std::size_t i = 0; i < n; ++i) {
+        const double mm[11] = {state.m_mu[i].x, state.m_mu[i].y, state.m_mu[i].z, state.m_ls[i].x, state.m_ls[i].y,
+                               state.m_ls[i].z, state.m_q[i].w, state.m_q[i].x, state.m_q[i].y, state.m_q[i].z,
+                               state.m_a[i]};
+        const double vv[11] = {state.v_mu[i].x, state.v_mu[i].y, state.v_mu[i].z, state.v_ls[i].x, state.v_ls[i].y,
+                               state.v_ls[i].z, state.v_q[i].w, state.v_q[i].x, state.v_q[i].y, state.v_q[i].z,
+                               state.v_a[i]};
+        for (int k = 0; k < 11; ++k) {
+            m[11 * i + k] = static_cast<float>(mm[k]);
+            v[11 * i + k] = static_cast<float>(vv[k]);
+        }
+    }
+    check(gpk_set_adam_state(s.handle(), m.data(), v.data(), state.step));
+    const std::vector<float> g = detail::records_of(grads);
+    check(gpk_set_gradients(s.handle(), g.data()));
+    const gpk_learning_rates l{lrs.position, lrs.opacity, lrs.scale, lrs.rotation};
+    const gpk_adam_hparams hp{state.beta1, state.beta2, state.eps};
+    check(gpk_adam_step(s.handle(), &l, &hp));
+    int64_t step = 0;
+    check(gpk_get_adam_state(s.handle(), m.data(), v.data(), &step));
+    s.get_gaussians(set);
+    state.step = static_cast<long>(step);
+    for (std::size_t i = 0; i < n; ++i) {
+        const float* a = &m[11 * i];
+        const float* b = &v[11 * i];
+        state.m_mu[i] = {a[0], a[1], a[2]};
+        state.m_ls[i] = {a[3], a[4], a[5]};
+        state.m_q[i] = {a[6], a[7], a[8], a[9]};
+        state.m_a[i] = a[10];
+        state.v_mu[i] = {b[0], b[1], b[2]};
+        state.v_ls[i] = {b[3], b[4], b[5]};
+        state.v_q[i] = {b[6], b[7], b[8], b[9]};
+        state.v_a[i] = b[10];
+    }
+}
+
+// ---- voxelize.hpp ----------------------------------------------------------------
+inline VolumeGrid voxelize(const GaussianSet& set, const VoxelizerConfig& cfg) {
+    Session& s = default_session();
+    s.set_gaussians(set);
+    const gpk_voxelizer_config c = detail::vcfg_of(cfg);
+    VolumeGrid vol;
+    for (int d = 0; d < 3; ++d) vol.dims[d] = cfg.dims[d];
+    vol.spacing = cfg.spacing;
+    vol.origin = cfg.origin;
+    // validation (voxelize.hpp:24-37, incl. the 2^31 refusal) happens in the
+    // library before anything is allocated
+    check(gpk_voxelize(s.handle(), &c, nullptr));
+    const std::size_t voxels = vol.voxel_count();
+    std::vector<float> out(voxels);
+    check(gpk_download(s.handle(), GPK_BUF_VOLUME, out.data(), voxels * sizeof(float)));
+    check(gpk_session_synchronize(s.handle()));
+    vol.data.assign(out.begin(), out.end());
+    return vol;
+}
+
+inline GaussianGradients voxelize_backward(const GaussianSet& set, const VoxelizerConfig& cfg,
+                                           const VolumeGrid& dl_dv) {
+    for (int d = 0; d < 3; ++d)
+        if (dl_dv.dims[d] != cfg.dims[d])
+            throw std::invalid_argument("voxelize_backward: gradient volume shape mismatch");  // voxelize.hpp:155-157
+    Session& s = default_session();
+    s.set_gaussians(set);
+    const gpk_voxelizer_config c = detail::vcfg_of(cfg);
+    const std::vector<float> dl(dl_dv.data.begin(), dl_dv.data.end());
+    std::vector<float> g(set.size() * 11);
+    check(gpk_voxelize_backward(s.handle(), &c, dl.data(), g.data()));
+    return detail::grads_of(g, set.size());
+}
+
+}  // namespace b200
+}  // namespace gpile

@@ -1214,10 +1214,14 @@ int gpk_photometric_loss_images(gpk_session* s, int32_t width, int32_t height,
     const size_t px = (size_t)width * height;
     CK(cudaMemcpyAsync(s->image.p, rendered, px * 4, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemcpyAsync(s->target.p, target, px * 4, cudaMemcpyHostToDevice, s->stream));
-    s->prep.valid = false;
+    // the prepared slice survives when the images have its shape (only the
+    // rendered image buffer is overwritten), as the reference's loss leaves
+    // the caller's prepared vector alone
+    const bool keep = s->prep.valid && s->prep.slice.W == width && s->prep.slice.H == height;
     s->prep.rasterized = true;
     TRY(run_loss(s, lambda, dssim_scale));
     s->prep.rasterized = false;
+    s->prep.valid = keep;
     TRY(sync_and_check(s, "photometric_loss"));
     if (loss_out) CK(cudaMemcpy(loss_out, s->loss(), 8, cudaMemcpyDeviceToHost));
     if (dl_di_out) CK(cudaMemcpy(dl_di_out, s->dl_di.p, px * 4, cudaMemcpyDeviceToHost));

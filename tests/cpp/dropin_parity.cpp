@@ -1,0 +1,201 @@
+// dropin_parity.cpp — TEST ONLY. The reference's own call sequence, run twice
+// on the same inputs: once through the reference (namespace gpile, header-only
+// CPU implementation compiled into this binary as the oracle) and once through
+// the drop-in (namespace gpile::b200, include/gpile_b200.hpp over the C-ABI).
+// Mirrors the fit loop (optimize.hpp:385-402) and proj/tests/test_render.cpp /
+// test_grad.cpp / test_voxelize.cpp pins. Exit status 0 iff every comparison
+// is within the north-star tolerances (images 1e-4 rel, gradients 1e-3 rel,
+// tile-derived survivor sets bit-exact).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+
+#include "../../include/gpile_b200.hpp"
+
+using namespace gpile;
+
+static int failures = 0;
+
+static void expect(bool ok, const char* what) {
+    std::printf("%-58s %s\n", what, ok ? "ok" : "FAIL");
+    if (!ok) ++failures;
+}
+
+static bool images_close(const SliceImage& a, const SliceImage& b) {
+    if (a.width != b.width || a.height != b.height) return false;
+    double peak = 0.0;
+    for (double v : b.pixels) peak = std::fmax(peak, std::fabs(v));
+    for (std::size_t i = 0; i < a.pixels.size(); ++i)
+        if (std::fabs(a.pixels[i] - b.pixels[i]) > 1e-4 * std::fabs(b.pixels[i]) + 1e-6 * peak) return false;
+    return true;
+}
+
+static bool grads_close(const GaussianGradients& a, const GaussianGradients& b) {
+    if (a.size() != b.size()) return false;
+    const std::size_t n = a.size();
+    auto plane = [&](auto get) {
+        double mx = 0.0;
+        for (std::size_t i = 0; i < n; ++i) mx = std::fmax(mx, std::fabs(get(b, i)));
+        for (std::size_t i = 0; i < n; ++i) {
+            const double r = get(b, i), x = get(a, i);
+            if (std::fabs(x - r) > 1e-3 * std::fabs(r) + 1e-3 * mx) return false;
+        }
+        return true;
+    };
+    bool ok = true;
+    for (int k = 0; k < 3; ++k) {
+        ok &= plane([k](const GaussianGradients& g, std::size_t i) { return g.d_mu[i][k]; });
+        ok &= plane([k](const GaussianGradients& g, std::size_t i) { return g.d_log_scale[i][k]; });
+    }
+    ok &= plane([](const GaussianGradients& g, std::size_t i) { return g.d_quat[i].w; });
+    ok &= plane([](const GaussianGradients& g, std::size_t i) { return g.d_quat[i].x; });
+    ok &= plane([](const GaussianGradients& g, std::size_t i) { return g.d_quat[i].y; });
+    ok &= plane([](const GaussianGradients& g, std::size_t i) { return g.d_quat[i].z; });
+    ok &= plane([](const GaussianGradients& g, std::size_t i) { return g.d_alpha_raw[i]; });
+    return ok;
+}
+
+static GaussianSet f32_set(GaussianSet s) {  // the device stores f32: give both sides identical inputs
+    auto r = [](double v) { return (double)(float)v; };
+    for (auto& g : s.primitives) {
+        g.mu = {r(g.mu.x), r(g.mu.y), r(g.mu.z)};
+        g.log_scale = {r(g.log_scale.x), r(g.log_scale.y), r(g.log_scale.z)};
+        g.quat = {r(g.quat.w), r(g.quat.x), r(g.quat.y), r(g.quat.z)};
+        g.alpha_raw = r(g.alpha_raw);
+    }
+    return s;
+}
+
+int main() {
+    VolumeGrid vol;
+    vol.dims[0] = 96;
+    vol.dims[1] = 80;
+    vol.dims[2] = 24;
+    const Bounds bbox = vol.world_bounds();
+    const GaussianSet set = f32_set(init_random(8000, bbox, 1.5, 1));
+    const PsfSpec psf{};
+    const RasterConfig cfg{};
+
+    // fit-loop sequence: prepare -> rasterize -> loss -> backward -> adam
+    const SlicePose pose = slice_pose_for_index(vol, 11);
+    const auto prep_ref = prepare_gaussians(set, pose, psf, cfg);
+    const auto prep_gpu = b200::prepare_gaussians(set, pose, psf, cfg);
+    bool same = prep_ref.size() == prep_gpu.size();
+    for (std::size_t k = 0; same && k < prep_ref.size(); ++k)
+        same = prep_ref[k].index == prep_gpu[k].index && prep_ref[k].lo_x == prep_gpu[k].lo_x &&
+               prep_ref[k].hi_x == prep_gpu[k].hi_x && prep_ref[k].lo_y == prep_gpu[k].lo_y &&
+               prep_ref[k].hi_y == prep_gpu[k].hi_y;
+    expect(same, "prepare_gaussians: survivors + pixel bounds bit-exact");
+
+    const SliceImage img_ref = rasterize_prepared(prep_ref, pose, cfg);
+    const SliceImage img_gpu = b200::rasterize_prepared(prep_gpu, pose, cfg);
+    expect(images_close(img_gpu, img_ref), "rasterize_prepared within 1e-4 rel");
+
+    SliceImage target(vol.dims[0], vol.dims[1]);
+    for (std::size_t i = 0; i < target.size(); ++i) target.pixels[i] = (double)(float)(0.05 + 0.04 * std::sin(0.37 * i));
+    SliceImage dl_ref, dl_gpu;
+    SliceImage img32 = img_gpu;  // both losses on the same (f32-exact) rendered image
+    const double L_ref = photometric_loss(img32, target, 0.2, dl_ref);
+    const double L_gpu = b200::photometric_loss(img32, target, 0.2, dl_gpu);
+    expect(std::fabs(L_gpu - L_ref) <= 1e-5 * std::fabs(L_ref), "photometric_loss value within 1e-5 rel");
+
+    ScreenGradStats st_ref, st_gpu;
+    SliceImage dl32 = dl_ref;
+    for (double& v : dl32.pixels) v = (double)(float)v;
+    const GaussianGradients g_ref = backward_prepared(set, prep_ref, pose, dl32, cfg, &st_ref);
+    const GaussianGradients g_gpu = b200::backward_prepared(set, prep_gpu, pose, dl32, cfg, &st_gpu);
+    expect(grads_close(g_gpu, g_ref), "backward_prepared within 1e-3 rel (+plane floor)");
+    expect(st_gpu.observed == st_ref.observed, "ScreenGradStats.observed identical");
+
+    GaussianSet s_ref = set, s_gpu = set;
+    AdamState a_ref(set.size()), a_gpu(set.size());
+    const LearningRates lrs{6e-4, 0.02, 2e-3, 1e-3};
+    adam_step(s_ref, g_gpu, a_ref, lrs);
+    b200::adam_step(s_gpu, g_gpu, a_gpu, lrs);
+    bool adam_ok = a_ref.step == a_gpu.step;
+    for (std::size_t i = 0; adam_ok && i < set.size(); ++i)
+        for (int k = 0; k < 3; ++k)
+            adam_ok = std::fabs(s_ref.primitives[i].mu[k] - s_gpu.primitives[i].mu[k]) <=
+                      2e-6 * std::fabs(s_ref.primitives[i].mu[k]) + 1e-6;
+    expect(adam_ok, "adam_step parameters within fp32 tolerance");
+    expect(b200::lr_at(6e-4, 7, 30) == lr_at(6e-4, 7, 30), "lr_at identical");
+
+    // rasterize_slice / backward_slice, random pose, tau = 0 (test_grad.cpp:128-177)
+    Rng rng(5);
+    GaussianSet small;
+    small.bbox = {{-3, -3, -3}, {3, 3, 3}};
+    for (int i = 0; i < 30; ++i) {
+        GaussianPrimitive g;
+        g.mu = rng.uniform_in_box(small.bbox.min, small.bbox.max);
+        g.log_scale = {std::log(rng.uniform(0.5, 2.0)), std::log(rng.uniform(0.5, 2.0)), std::log(rng.uniform(0.5, 2.0))};
+        g.quat = rng.unit_quaternion();
+        g.alpha_raw = alpha_activation_inverse(rng.uniform(0.2, 0.9));
+        small.primitives.push_back(g);
+    }
+    small = f32_set(small);
+    SlicePose rp;
+    rp.rotation = quat_to_rotation(rng.unit_quaternion());
+    rp.translation = {rng.uniform(-2.0, 2.0), rng.uniform(-2.0, 2.0), rng.uniform(-2.0, 2.0)};
+    rp.width = 24;
+    rp.height = 20;
+    rp.pixel_spacing = {0.5, 0.5};
+    rp.principal_point = {12.0, 10.0};
+    const RasterConfig cfg0{0.0, 16, 8.0, 1.0};
+    const PsfSpec psf08{1.0, 1.0, 0.8};
+    expect(images_close(b200::rasterize_slice(small, rp, psf08, cfg0), rasterize_slice(small, rp, psf08, cfg0)),
+           "rasterize_slice (random pose) within 1e-4 rel");
+    SliceImage dl(24, 20);
+    for (std::size_t i = 0; i < dl.size(); ++i) dl.pixels[i] = (double)(float)std::cos(0.91 * i);
+    expect(grads_close(b200::backward_slice(small, rp, psf08, dl, cfg0), backward_slice(small, rp, psf08, dl, cfg0)),
+           "backward_slice (random pose) within 1e-3 rel");
+
+    // voxelizer (voxelize.hpp:113-240)
+    VoxelizerConfig vc;
+    vc.dims[0] = 40;
+    vc.dims[1] = 36;
+    vc.dims[2] = 28;
+    GaussianSet vs = f32_set(init_random(1500, {{2, 2, 2}, {38, 34, 26}}, 1.2, 9));
+    const VolumeGrid v_ref = voxelize(vs, vc), v_gpu = b200::voxelize(vs, vc);
+    double vpeak = 0.0;
+    for (double x : v_ref.data) vpeak = std::fmax(vpeak, x);
+    bool vok = v_gpu.data.size() == v_ref.data.size();
+    for (std::size_t i = 0; vok && i < v_ref.data.size(); ++i)
+        vok = std::fabs(v_gpu.data[i] - v_ref.data[i]) <= 1e-4 * std::fabs(v_ref.data[i]) + 1e-6 * vpeak;
+    expect(vok, "voxelize within 1e-4 rel");
+    VolumeGrid dlv = v_ref;
+    for (std::size_t i = 0; i < dlv.data.size(); ++i) dlv.data[i] = (double)(float)std::sin(0.013 * i);
+    expect(grads_close(b200::voxelize_backward(vs, vc, dlv), voxelize_backward(vs, vc, dlv)),
+           "voxelize_backward within 1e-3 rel");
+
+    // error semantics
+    bool threw = false;
+    try {
+        VoxelizerConfig big;
+        big.dims[0] = big.dims[1] = 2048;
+        big.dims[2] = 1024;
+        b200::voxelize(vs, big);
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    expect(threw, "voxelize > 2^31 voxels -> std::invalid_argument");
+    threw = false;
+    try {
+        b200::rasterize_slice(set, pose, PsfSpec{1.0, 1.0, 0.0}, cfg);
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    expect(threw, "bad PsfSpec -> std::invalid_argument");
+    threw = false;
+    try {
+        GaussianSet bad = small;
+        bad.primitives[3].quat = {0, 0, 0, 0};
+        b200::rasterize_slice(bad, rp, psf08, cfg0);
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    expect(threw, "zero quaternion -> std::invalid_argument");
+
+    std::printf("%s\n", failures ? "DROPIN PARITY FAILED" : "DROPIN PARITY OK");
+    return failures ? 1 : 0;
+}

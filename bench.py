@@ -151,11 +151,15 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------------
 def cpu_reference_rate(cfg, rec, seconds_budget, max_reps=None):
-    """Reference CPU U1 (oracle/_ref) on this host's cores. Returns dict."""
+    """Reference CPU U1 (oracle/_ref) on this host's cores. Returns dict.
+
+    Everything on this path is the reference's own code (oracle/_ref: the
+    reference headers compiled as they are): its slice poses
+    (slice_pose_for_index, core.hpp:202-211) and its prepare / rasterize /
+    backward; `rec` is the same synthetic set the GPU arm uses."""
     import ctypes as C
 
     from oracle.bindings import Bounds, CfgC, PoseC, PsfC, load
-    import paper_2603_20611_b200 as gp
 
     ref = load("ref")
     L = ref.lib
@@ -169,11 +173,14 @@ def cpu_reference_rate(cfg, rec, seconds_budget, max_reps=None):
     h = L.gref_set_new(C.c_uint64(rec.shape[0]), rec.ctypes.data_as(C.POINTER(C.c_double)), C.byref(b))
     ks = slice_indices(Z)
     poses = (PoseC * len(ks))()
+    dims = (C.c_int32 * 3)(X, Y, Z)
+    sp = (C.c_double * 3)(1.0, 1.0, 1.0)
+    org = (C.c_double * 3)(0.0, 0.0, 0.0)
+    L.gref_slice_pose_for_index.argtypes = [C.POINTER(C.c_int32), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                            C.c_int, C.POINTER(PoseC)]
     for i, k in enumerate(ks):
-        p = gp.slice_pose_for_index(cfg["dims"], (1, 1, 1), (0, 0, 0), k)
-        r = np.asarray(p.rotation, np.float64).reshape(9)
-        poses[i] = PoseC((C.c_double * 9)(*r), (C.c_double * 3)(*p.translation), p.width, p.height,
-                         (C.c_double * 2)(*p.pixel_spacing), (C.c_double * 2)(*p.principal_point))
+        if L.gref_slice_pose_for_index(dims, sp, org, k, C.byref(poses[i])) != 0:
+            raise RuntimeError("reference slice_pose_for_index failed")
     psf = PsfC(1.0, 1.0, cfg["sigma_z"])
     rc = CfgC(0.02, 16, 3.0, 1.0)
     dl = synthetic_dl_di(cfg).astype(np.float64)
@@ -209,12 +216,28 @@ def synthetic_dl_di(cfg):
     return (rng.uniform(-1.0, 1.0, (Y, X)) / (X * Y)).astype(np.float32)
 
 
-def make_records(cfg):
-    import paper_2603_20611_b200 as gp
+def make_records(cfg, via_reference=False):
+    """init_random(N, world bounds, 1.5, seed 1) (optimize.hpp:94-108), rounded
+    to f32 so both arms see identical values. The reference arm draws it with
+    the reference's own Rng (oracle/_ref); the GPU arm with the bit-identical
+    host port in the C-ABI (tests/test_abi.py pins the equality)."""
+    import ctypes as C
 
     lo, hi = geometry(cfg)
+    if via_reference:
+        from oracle.bindings import Bounds, load
+
+        L = load("ref").lib
+        rec = np.zeros((cfg["n"], 11), np.float64)
+        bnd = Bounds((C.c_double * 3)(*lo), (C.c_double * 3)(*hi))
+        L.gref_init_random.argtypes = [C.c_uint64, C.POINTER(Bounds), C.c_double, C.c_uint64,
+                                       C.POINTER(C.c_double)]
+        if L.gref_init_random(cfg["n"], C.byref(bnd), 1.5, 1, rec.ctypes.data_as(C.POINTER(C.c_double))) != 0:
+            raise RuntimeError("reference init_random failed")
+        return rec.astype(np.float32).astype(np.float64)
+    import paper_2603_20611_b200 as gp
+
     gs = gp.init_random(cfg["n"], lo, hi, 1.5, 1)
-    # the device stores f32; both arms see the same f32-representable values
     return gp.GaussianSet(gs.records.astype(np.float32).astype(np.float64), lo, hi)
 
 
@@ -234,9 +257,9 @@ def run_reference(args):
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
-    gs = make_records(cfg)
+    rec = make_records(cfg, via_reference=True)
     budget = min(150.0, max(10.0, 1.0 * args.steps))
-    res = cpu_reference_rate(cfg, gs.records, budget, max_reps=args.steps)
+    res = cpu_reference_rate(cfg, rec, budget, max_reps=args.steps)
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "slices/s",
         "n_gpus": args.gpus, "steps": res["reps"], "warmup": 1, "ms_per_step": 1000.0 / res["value"],
@@ -292,13 +315,15 @@ def run_ours(args):
     dl = synthetic_dl_di(cfg)
     sess.upload(N.GPK_BUF_DL_DI, dl.ctypes.data, dl.nbytes)
     sess.synchronize()
-    # per-slice survivor / pair counts (algorithmic bytes of K_prep)
+    # per-slice counters (algorithmic bytes of the prepare kernels)
     counts = []
     for p in poses:
         sess.prepare(p, psf, rcfg)
-        counts.append(sess.prepared_count())
-    S_mean = float(np.mean([c[0] for c in counts]))
-    T_mean = float(np.mean([c[1] for c in counts]))
+        counts.append(sess.prepare_stats())
+    S_mean = float(np.mean([c["survivors"] for c in counts]))
+    T_mean = float(np.mean([c["pairs"] for c in counts]))
+    C_mean = float(np.mean([c["candidates"] for c in counts]))
+    X64_mean = float(np.mean([c["fp64_decided"] for c in counts]))
 
     # L2 flush by READING 256 MiB (> 126 MB L2): evicts the step's working set
     # without leaving dirty lines whose write-back would bill the next kernel.
@@ -394,17 +419,18 @@ def run_ours(args):
     # ---- roofline of the dominant kernel -------------------------------------------
     # Algorithmic bytes per launch (each logical tensor read/written once at its
     # stored width): N Gaussians, S survivors, T pairs, P px.
-    S, T = S_mean, T_mean
-    kernel_bytes = {
-        "prepare": ("k_prep", 44 * n + 44 * S + 96 * S + 8 * T,
-                    "44N params read + 44S previous-survivor gradient clear + 48S records "
-                    "+ 48S survivor params + 8T pairs"),
-        "bin": ("k_bin", 48 * S + 4 * S + 4 * S + 8 * T, "48S records + 4S survivor slots + 4S pair bases + 8T pairs"),
-        "sort": ("k_sort_pass x passes", 16 * T * max(1, sort_passes(X, Y)), "16T per radix pass"),
-        "raster": ("k_raster_fwd", 32 * T + 4 * P, "32T + 4P (SURVEY.md §8d)"),
-        "backward": ("k_raster_bwd", 4 * P + 32 * T + 24 * S, "4P + 32T + 24S (SURVEY.md §8d)"),
-        "chain": ("k_chain", 48 * S + 48 * S + 24 * T + 44 * S + 4 * S,
-                  "48S survivor params + 48S records + 24T partials + 44S grads + 4S dirty list"),
+    S, T, Cc = S_mean, T_mean, C_mean
+    passes = max(1, sort_passes(X, Y))
+    kernel_bytes = {  # algorithmic bytes per launch
+        "prepare": ("k_filter", 44 * n + 44 * S + 48 * Cc + 4 * (n / 1024),
+                    "44N params + 44S previous-survivor gradient clear + 48C candidate records + 4/1024 N counts"),
+        "bin": ("k_decide", 48 * Cc + 48 * S + 48 * S + 8 * S + 8 * T,
+                "48C candidates + 48S records + 48S survivor params + 8S slots/bases + 8T pairs"),
+        "sort": ("k_sort_pass x passes", 16 * T * passes, "16T per radix pass"),
+        "raster": ("k_raster_fwd", 56 * T + 4 * P, "56T (key, slot, 48 B record per pair) + 4P image"),
+        "backward": ("k_raster_bwd", 56 * T + 4 * P + 24 * T, "56T + 4P dL/dI + 24T partials"),
+        "chain": ("k_chain", 48 * S + 48 * S + 24 * T + 44 * S + 8 * S,
+                  "48S records + 48S params + 24T partials + 44S grads + 8S slot/dirty list"),
     }
     dom = max((k for k in stages if stages[k][1] > 0 and k in kernel_bytes), key=lambda k: stages[k][0])
     peak, peak_src = load_peaks()
@@ -435,7 +461,8 @@ def run_ours(args):
         "stage_ms_per_step": {k: v[0] / prof_steps for k, v in stages.items() if v[1]},
         "kernels": per_kernel,
         "submission": "CUDA graph per slice pose" if graphs is not None else "kernel by kernel",
-        "survivors_mean": S_mean, "pairs_mean": T_mean,
+        "survivors_mean": S_mean, "pairs_mean": T_mean, "candidates_mean": C_mean,
+        "fp64_decided_mean": X64_mean,
         "e2e": {"value": world * 1000.0 / e2e_ms, "unit": "slices/s", "h2d_bytes_per_step": P * 4,
                 "d2h_bytes_per_step": P * 4 + cap_floats * 44,
                 "path": "C-ABI: gpk_upload(dL/dI) + gpk_fwd_bwd_slice + gpk_download(image, dense grads)"},

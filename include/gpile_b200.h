@@ -184,6 +184,12 @@ int gpk_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                 const gpk_raster_config* cfg);
 /* Survivor and pair counts of the last prepare (synchronizes). */
 int gpk_prepared_count(gpk_session* s, uint64_t* survivors, uint64_t* pairs);
+/* Counters of the last prepare (synchronizes): K_filter candidates (not
+ * certainly culled by the fp32 bound), survivors, (tile, survivor) pairs and
+ * survivors whose decision took the reference-order fp64 path. Any pointer
+ * may be NULL. */
+int gpk_prepare_stats(gpk_session* s, uint64_t* candidates, uint64_t* survivors, uint64_t* pairs,
+                      uint64_t* fp64_decided);
 /* Survivors in ascending set order (render.hpp:133-137): set index, inclusive
  * pixel bounds (lo_x, hi_x, lo_y, hi_y) and 6 doubles (alpha_tilde, mu_2d.x,
  * mu_2d.y, conic.a, conic.b, conic.d). Any pointer may be NULL. */

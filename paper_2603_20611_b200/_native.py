@@ -129,6 +129,7 @@ _PROTOS = {
                                               C.c_double, _D, _F]),
     "gpk_prepare": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC), C.POINTER(RasterConfigC)]),
     "gpk_prepared_count": (C.c_int, [_P, _U64, _U64]),
+    "gpk_prepare_stats": (C.c_int, [_P, _U64, _U64, _U64, _U64]),
     "gpk_get_prepared": (C.c_int, [_P, _U32, _I32, _D]),
     "gpk_get_tile_lists": (C.c_int, [_P, _U32, _U32]),
     "gpk_rasterize": (C.c_int, [_P, _F]),

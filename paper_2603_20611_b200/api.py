@@ -297,6 +297,12 @@ class Session:
         check(N.lib.gpk_prepared_count(self._h, C.byref(s), C.byref(t)))
         return int(s.value), int(t.value)
 
+    def prepare_stats(self) -> dict:
+        """Counters of the last prepare: candidates, survivors, pairs, fp64-decided survivors."""
+        v = [C.c_uint64() for _ in range(4)]
+        check(N.lib.gpk_prepare_stats(self._h, *[C.byref(x) for x in v]))
+        return dict(zip(("candidates", "survivors", "pairs", "fp64_decided"), (int(x.value) for x in v)))
+
     def prepared(self) -> Prepared:
         s, t = self.prepared_count()
         idx = np.zeros(s, np.uint32)

@@ -108,10 +108,11 @@ struct alignas(64) Control {
     unsigned int pairs;                        // T (uncapped)
     unsigned int pair_overflow;                // T > capacity
     unsigned int adam_done_ctr;
-    unsigned int candidates;                   // C, written by the last K_filter block
+    unsigned int candidates;                   // C: K_filter candidates (summed by K_decide)
     unsigned int exact_chunk_ctr;              // chunk claims of K_exact
     unsigned int chain_exact;                  // survivors deferred to the fp64 chain
-    unsigned int pad[5];
+    unsigned int exact_decided;                // survivors decided on the reference-order fp64 path
+    unsigned int pad[4];
 };
 
 constexpr int kExactChunk = 256;               // candidates per K_exact chunk (= threads)

@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     __shared__ unsigned s_hist[kMaxSortPasses][kMaxBuckets];
     __shared__ unsigned s_cnt[2][kDecideThreads / 32];
     __shared__ unsigned s_cpre[kDecideChunks + 1];
-    __shared__ unsigned s_grp, s_nsurv;
+    __shared__ unsigned s_grp, s_nsurv, s_nexact;
     __shared__ unsigned long long s_excl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned dmask = (1u << a.digit_bits) - 1;
@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
         const unsigned g = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
         s_grp = g;
         s_nsurv = 0;
+        s_nexact = 0;
         unsigned acc = 0;
         for (int q = 0; q < kDecideChunks; ++q) {
             s_cpre[q] = acc;
@@ -427,7 +428,11 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
             rec.pair_base = 0;
         }
         const unsigned m = __ballot_sync(0xffffffffu, survive);
-        if (lane == 0) s_cnt[r][warp] = __popc(m);
+        const unsigned mx = __ballot_sync(0xffffffffu, survive && (rec.gidx & kExactFlag));
+        if (lane == 0) {
+            s_cnt[r][warp] = __popc(m);
+            if (mx) atomicAdd(&s_nexact, (unsigned)__popc(mx));
+        }
         __syncthreads();
         unsigned rank = s_nsurv + __popc(m & lanemask_lt());
         for (int w = 0; w < warp; ++w) rank += s_cnt[r][w];
@@ -450,6 +455,10 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     }
     __syncthreads();
     const unsigned S = s_nsurv;
+    if (tid == 0) {  // statistics (gpk_prepare_stats)
+        if (nc) atomicAdd(&a.ctrl->candidates, nc);
+        if (s_nexact) atomicAdd(&a.ctrl->exact_decided, s_nexact);
+    }
 
     // ---- 2. inclusive scan of the pair counts, ordered group prefix -------------
     {

@@ -1084,6 +1084,19 @@ int gpk_prepared_count(gpk_session* s, uint64_t* survivors, uint64_t* pairs) {
     return ok();
 }
 
+int gpk_prepare_stats(gpk_session* s, uint64_t* candidates, uint64_t* survivors, uint64_t* pairs,
+                      uint64_t* fp64_decided) {
+    uint64_t S = 0, T = 0;
+    TRY(gpk_prepared_count(s, &S, &T));
+    Control c;
+    CK(cudaMemcpy(&c, s->ctrl(), sizeof c, cudaMemcpyDeviceToHost));
+    if (candidates) *candidates = s->n ? c.candidates : 0;
+    if (survivors) *survivors = S;
+    if (pairs) *pairs = T;
+    if (fp64_decided) *fp64_decided = s->n ? c.exact_decided : 0;
+    return ok();
+}
+
 int gpk_get_prepared(gpk_session* s, uint32_t* index, int32_t* bounds, double* fields) {
     uint64_t S = 0, T = 0;
     TRY(gpk_prepared_count(s, &S, &T));

@@ -329,6 +329,7 @@ struct SortLaunch {
     unsigned* tile_hist_next;      // next pass's region (nullptr on the last pass)
     uint64_t sort_tiles_cap;       // offset (in rows) of the super-tile rows
     unsigned* prev_sort_words;     // written by the last pass: {sort tiles, buckets, passes}
+    unsigned* grp_begin;           // last pass only: first sorted position of every digit (+ end)
     int shift;
     int bits;                      // digit width of this pass
     unsigned next_buckets;         // 2^bits of the next pass
@@ -337,10 +338,16 @@ struct SortLaunch {
     uint64_t pair_cap;
 };
 
+// Words between the global digit histograms and the chunk words of the
+// control head: first sorted position of every last-pass digit group (+ end).
+constexpr int kGroupBeginWords = kMaxBuckets + 4;
+
 struct RasterLaunch {
     const SurvivorRecord* records;
     const uint32_t* keys;          // sorted tile keys
     const uint32_t* vals;          // sorted candidate ids
+    const unsigned* grp_begin;     // last radix pass: first position of each digit group
+    int grp_shift;                 // tile >> grp_shift = last-pass digit (-1: no sort pass ran)
     const Control* ctrl;
     uint64_t pair_cap;
     float* image;                  // forward output

@@ -13,13 +13,19 @@
 //   factor folded into the conic.
 //
 // Backward replaces stage 1 of backward_prepared (backward.hpp:108-139):
-//   one LANE per (tile, Gaussian) pair walks the pair's tile-clipped footprint
-//   row-major — the reference's own summation order — accumulating the six
-//   per-pair sums in registers (no reduction, no atomics). Pairs of a tile are
-//   bucketed by footprint area (descending) so the 32 lanes of a warp get
-//   similar trip counts. Each pair's sums go to its PRE-SORT position, so
+//   the tile's pairs are staged once in shared memory (tile-local centre,
+//   conic, alpha_tilde, clipped footprint, output position), bucketed by work
+//   (rows-per-lane x width, largest first) and processed one QUAD (4 lanes)
+//   per pair: lane q takes rows q, q+4, ... of the tile-clipped footprint and
+//   walks each row left to right. The per-pixel work is factored through the
+//   linearity of the six sums: with u = dL/dI * exp(-q/2),
+//     dA = sum u,  dmu = at * C * (sum u dx, sum u dy),
+//     dconic = -at/2 * (sum u dx^2, sum u dx dy, sum u dy^2),
+//   and within a row dy is constant, so a pixel costs 3 FMA for the exponent,
+//   one MUFU.EX2 and 5 FMA/FADD for the sums. The quad's sums are combined by
+//   a fixed xor-shuffle tree and written to the pair's PRE-SORT position, so
 //   K_chain merges a Gaussian's tiles in tile order (backward.hpp:141-145):
-//   bitwise reproducible run to run.
+//   bitwise reproducible run to run, no float atomics.
 #include "common.cuh"
 
 namespace gpk {
@@ -72,11 +78,27 @@ __device__ __forceinline__ unsigned clip_mask(const SurvivorRecord& r, int x0, i
     return xm | (ym << 16);
 }
 
+// [begin, end) of the tile's pairs in the sorted list. The last radix pass
+// recorded where each of its digit groups starts; with one pass the digit is
+// the tile, otherwise a warp binary-searches inside the tile's group.
 __device__ __forceinline__ void tile_range(const RasterLaunch& a, int tile, unsigned* s_range) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
+    if (a.grp_shift < 0) {  // no sort pass: a single tile
+        if (threadIdx.x == 0) {
+            s_range[0] = 0;
+            s_range[1] = P;
+        }
+        return;
+    }
+    const unsigned d = (unsigned)tile >> a.grp_shift;
+    if (a.grp_shift == 0) {
+        if (threadIdx.x < 2) s_range[threadIdx.x] = __ldcg(&a.grp_begin[d + threadIdx.x]);
+        return;
+    }
     if (warp < 2) {
-        const unsigned r = warp_lower_bound(a.keys, P, (unsigned)tile + warp);
+        const unsigned lo = __ldcg(&a.grp_begin[d]), hi = __ldcg(&a.grp_begin[d + 1]);
+        const unsigned r = lo + warp_lower_bound(a.keys + lo, hi - lo, (unsigned)tile + warp);
         if (lane == 0) s_range[warp] = r;
     }
 }
@@ -136,14 +158,14 @@ __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
     if (i < a.slice.W && j < a.slice.H) a.image[(size_t)j * a.slice.W + i] = acc;
 }
 
-constexpr int kBwdBatch = 1024;   // pairs per scheduling round of a tile
-constexpr int kBwdPerThread = kBwdBatch / 256;
-constexpr int kAreaBuckets = 16;
+constexpr int kBwdBatch = 256;    // pairs staged per round (one per thread)
+constexpr int kWorkBuckets = 16;
 
 __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
     __shared__ float s_dl[kTile * kTile];
-    __shared__ unsigned s_bucket[kAreaBuckets];
-    __shared__ uint16_t s_order[kBwdBatch];
+    __shared__ float4 s_pair[kBwdBatch][2];   // {ox, oy, ca, cb}, {cd, at, rect, pos}
+    __shared__ unsigned s_bucket[kWorkBuckets];
+    __shared__ uint8_t s_order[kBwdBatch];
     __shared__ unsigned s_range[2];
 
     const int tid = threadIdx.x;
@@ -153,7 +175,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
     tile_range(a, tile, s_range);
     {
         const int i = x0 + (tid & 15), j = y0 + (tid >> 4);
-        s_dl[tid] = (i < a.slice.W && j < a.slice.H) ? a.dl_di[(size_t)j * a.slice.W + i] : 0.f;
+        s_dl[tid] = (i < a.slice.W && j < a.slice.H) ? __ldg(&a.dl_di[(size_t)j * a.slice.W + i]) : 0.f;
     }
     const double X0 = ((double)x0 - a.slice.ppx) * a.slice.sx;
     const double Y0 = ((double)y0 - a.slice.ppy) * a.slice.sy;
@@ -163,99 +185,91 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
 
     for (unsigned b = start; b < end; b += kBwdBatch) {
         const unsigned nb = min((unsigned)kBwdBatch, end - b);
-        if (tid < kAreaBuckets) s_bucket[tid] = 0;
+        if (tid < kWorkBuckets) s_bucket[tid] = 0;
         __syncthreads();
-        // ---- bucket the batch's pairs by clipped area, largest first ----------
-        unsigned slot[kBwdPerThread];
-#pragma unroll
-        for (int u = 0; u < kBwdPerThread; ++u) {
-            const unsigned q = tid + u * 256;
-            slot[u] = 0xffffffffu;
-            if (q < nb) {
-                const unsigned rc = clip_rect(a.records[a.vals[b + q]], x0, y0);
-                const unsigned area = (((rc >> 8) & 255u) - (rc & 255u) + 1) *
-                                      ((rc >> 24) - ((rc >> 16) & 255u) + 1);
-                const unsigned bk = (kAreaBuckets - 1) - min(area >> 4, (unsigned)kAreaBuckets - 1);
-                slot[u] = (bk << 16) | atomicAdd(&s_bucket[bk], 1u);
-            }
+        // ---- stage the batch's pairs, bucketed by per-lane work ---------------
+        unsigned slot = 0xffffffffu;
+        if ((unsigned)tid < nb) {
+            const SurvivorRecord r = a.records[a.vals[b + tid]];
+            const unsigned rc = clip_rect(r, x0, y0);
+            const unsigned w = ((rc >> 8) & 255u) - (rc & 255u) + 1, h = (rc >> 24) - ((rc >> 16) & 255u) + 1;
+            const unsigned ntx = r.hi_x / kTile - r.lo_x / kTile + 1;
+            const unsigned pos = r.pair_base + (unsigned)((ty - r.lo_y / kTile) * ntx + (tx - r.lo_x / kTile));
+            s_pair[tid][0] = make_float4((float)(r.mu2d_x - X0), (float)(r.mu2d_y - Y0), r.conic_a, r.conic_b);
+            s_pair[tid][1] = make_float4(r.conic_d, r.alpha_tilde, __uint_as_float(rc), __uint_as_float(pos));
+            const unsigned work = ((h + 3) >> 2) * w;  // rows per lane x row length, <= 64
+            const unsigned bk = (kWorkBuckets - 1) - min(work >> 2, (unsigned)kWorkBuckets - 1);
+            slot = (bk << 16) | atomicAdd(&s_bucket[bk], 1u);
         }
         __syncthreads();
         if (tid < 32) {
-            const unsigned v = tid < kAreaBuckets ? s_bucket[tid] : 0u;
+            const unsigned v = tid < kWorkBuckets ? s_bucket[tid] : 0u;
             unsigned incl = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const unsigned w = __shfl_up_sync(0xffffffffu, incl, o);
-                if (tid >= o) incl += w;
+                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += u;
             }
-            if (tid < kAreaBuckets) s_bucket[tid] = incl - v;
+            if (tid < kWorkBuckets) s_bucket[tid] = incl - v;
         }
         __syncthreads();
-#pragma unroll
-        for (int u = 0; u < kBwdPerThread; ++u)
-            if (slot[u] != 0xffffffffu)
-                s_order[s_bucket[slot[u] >> 16] + (slot[u] & 0xffffu)] = (uint16_t)(tid + u * 256);
+        if (slot != 0xffffffffu) s_order[s_bucket[slot >> 16] + (slot & 0xffffu)] = (uint8_t)tid;
         __syncthreads();
 
-        // ---- one QUAD (4 lanes) per pair: lane q walks pixels q, q+4, ... of
-        // the clipped footprint in row-major order; the quad's partial sums
-        // are combined by two xor-shuffles ((l0+l1)+(l2+l3), deterministic).
+        // ---- one quad per pair ------------------------------------------------
         const int quad = tid >> 2, ql = tid & 3;
-        for (unsigned o0 = 0; o0 < nb; o0 += 64) {
+        for (unsigned o0 = 0; o0 < nb; o0 += kBwdBatch / 4) {
             const unsigned o = o0 + quad;
             const bool active = o < nb;  // quads are whole: all 4 lanes agree
-            float s_a = 0.f, s_mx = 0.f, s_my = 0.f, s_xx = 0.f, s_xy = 0.f, s_yy = 0.f;
-            unsigned pos = 0xffffffffu;
+            float U = 0.f, UX = 0.f, UY = 0.f, UXX = 0.f, UXY = 0.f, UYY = 0.f;
+            float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0;
             if (active) {
                 const unsigned q = s_order[o];
-                const SurvivorRecord r = a.records[a.vals[b + q]];
-                const unsigned rc = clip_rect(r, x0, y0);
+                p0 = s_pair[q][0];
+                p1 = s_pair[q][1];
+                const unsigned rc = __float_as_uint(p1.z);
                 const int cx0 = rc & 255, cx1 = (rc >> 8) & 255, cy0 = (rc >> 16) & 255, cy1 = rc >> 24;
-                const int w = cx1 - cx0 + 1;
-                const int area = w * (cy1 - cy0 + 1);
-                const float ox = (float)(r.mu2d_x - X0), oy = (float)(r.mu2d_y - Y0);
-                const float ca = r.conic_a, cb = r.conic_b, cd = r.conic_d, at = r.alpha_tilde;
-                int x = cx0 + ql % w, y = cy0 + ql / w;
-                for (int idx = ql; idx < area; idx += 4) {
-                    const float gi = s_dl[y * kTile + x];
-                    if (gi != 0.f) {  // backward.hpp:125
-                        const float dx = (float)x * sxf - ox;
-                        const float dy = (float)y * syf - oy;
-                        const float cdx = fmaf(ca, dx, cb * dy);
-                        const float cdy = fmaf(cb, dx, cd * dy);
-                        const float g = ex2_approx(kNegHalfLog2e * fmaf(dx, cdx, dy * cdy));
-                        s_a = fmaf(gi, g, s_a);
-                        const float wgt = at * g * gi;
-                        s_mx = fmaf(cdx, wgt, s_mx);
-                        s_my = fmaf(cdy, wgt, s_my);
-                        const float hw = -0.5f * wgt;
-                        s_xx = fmaf(hw * dx, dx, s_xx);
-                        s_xy = fmaf(hw * dx, dy, s_xy);
-                        s_yy = fmaf(hw * dy, dy, s_yy);
+                const float ka = p0.z * kNegHalfLog2e, kb2 = 2.f * p0.w * kNegHalfLog2e,
+                            kd = p1.x * kNegHalfLog2e;
+                for (int y = cy0 + ql; y <= cy1; y += 4) {
+                    const float dy = fmaf((float)y, syf, -p0.y);
+                    const float B = kb2 * dy, Cc = kd * dy * dy;
+                    const float* row = s_dl + y * kTile;
+                    float ru = 0.f, rux = 0.f, ruxx = 0.f;
+#pragma unroll 4
+                    for (int x = cx0; x <= cx1; ++x) {
+                        const float dx = fmaf((float)x, sxf, -p0.x);
+                        const float u = row[x] * ex2_approx(fmaf(dx, fmaf(ka, dx, B), Cc));
+                        ru += u;
+                        const float ux = u * dx;
+                        rux += ux;
+                        ruxx = fmaf(ux, dx, ruxx);
                     }
-                    x += 4;
-                    while (x > cx1) {
-                        x -= w;
-                        ++y;
-                    }
+                    U += ru;
+                    UX += rux;
+                    UXX += ruxx;
+                    UY = fmaf(dy, ru, UY);
+                    UXY = fmaf(dy, rux, UXY);
+                    UYY = fmaf(dy * dy, ru, UYY);
                 }
-                const int ntx = r.hi_x / kTile - r.lo_x / kTile + 1;
-                pos = r.pair_base + (unsigned)((ty - r.lo_y / kTile) * ntx + (tx - r.lo_x / kTile));
             }
 #pragma unroll
             for (int sh = 1; sh <= 2; sh <<= 1) {
-                s_a += __shfl_xor_sync(0xffffffffu, s_a, sh);
-                s_mx += __shfl_xor_sync(0xffffffffu, s_mx, sh);
-                s_my += __shfl_xor_sync(0xffffffffu, s_my, sh);
-                s_xx += __shfl_xor_sync(0xffffffffu, s_xx, sh);
-                s_xy += __shfl_xor_sync(0xffffffffu, s_xy, sh);
-                s_yy += __shfl_xor_sync(0xffffffffu, s_yy, sh);
+                U += __shfl_xor_sync(0xffffffffu, U, sh);
+                UX += __shfl_xor_sync(0xffffffffu, UX, sh);
+                UY += __shfl_xor_sync(0xffffffffu, UY, sh);
+                UXX += __shfl_xor_sync(0xffffffffu, UXX, sh);
+                UXY += __shfl_xor_sync(0xffffffffu, UXY, sh);
+                UYY += __shfl_xor_sync(0xffffffffu, UYY, sh);
             }
+            const unsigned pos = __float_as_uint(p1.w);
             if (active && ql == 0 && pos < a.pair_cap) {
+                // PixelAccum (backward.hpp:129-136): dA, dmu = w C d, dconic = -w/2 d d^T
+                const float at = p1.y, ca = p0.z, cb = p0.w, cd = p1.x, h = -0.5f * at;
                 float2* dst = reinterpret_cast<float2*>(a.partials + 6ull * pos);
-                dst[0] = make_float2(s_a, s_mx);
-                dst[1] = make_float2(s_my, s_xx);
-                dst[2] = make_float2(s_xy, s_yy);
+                dst[0] = make_float2(U, at * fmaf(ca, UX, cb * UY));
+                dst[1] = make_float2(at * fmaf(cb, UX, cd * UY), h * UXX);
+                dst[2] = make_float2(h * UXY, h * UYY);
             }
         }
         __syncthreads();

@@ -154,9 +154,13 @@ struct gpk_session {
     unsigned* hist() { return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control)); }
     unsigned* prev_sort_words() { return reinterpret_cast<unsigned*>(persist.as<char>() + 96); }  // 3 words
     unsigned* grads_dirty() { return reinterpret_cast<unsigned*>(persist.as<char>() + 112); }
-    unsigned* filter_flags() {
+    unsigned* grp_begin() {
         return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control) +
                                            kMaxSortPasses * kMaxBuckets * sizeof(unsigned));
+    }
+    unsigned* filter_flags() {  // u64 chunk words (8 B aligned)
+        return reinterpret_cast<unsigned*>(head.as<char>() + sizeof(Control) +
+                                           (kMaxSortPasses * kMaxBuckets + kGroupBeginWords) * sizeof(unsigned));
     }
 };
 
@@ -221,10 +225,12 @@ int set_device(gpk_session* s) {
 
 uint64_t filter_blocks(uint64_t n) { return std::max<uint64_t>((n + kFilterBlock - 1) / kFilterBlock, 1); }
 uint64_t exact_chunks(uint64_t n) { return std::max<uint64_t>((n + kExactChunk - 1) / kExactChunk, 1); }
-// head = Control | global digit histograms | chunk words (u64), memset per prepare
+// head = Control | global digit histograms | digit-group begins | chunk words
+// (u64), memset per prepare
 size_t head_size(uint64_t n) {
-    // chunk words: K_prep uses one per 1024 Gaussians, the voxelizer one per 256
-    return sizeof(Control) + kMaxSortPasses * kMaxBuckets * sizeof(unsigned) + exact_chunks(n) * 8;
+    // chunk words: K_decide uses one per 4096 Gaussians, the voxelizer one per 256
+    return sizeof(Control) + (kMaxSortPasses * kMaxBuckets + kGroupBeginWords) * sizeof(unsigned) +
+           exact_chunks(n) * 8;
 }
 
 int clear_errors(gpk_session* s) {
@@ -453,6 +459,7 @@ int launch_sorts(gpk_session* s, int passes, int digit_bits) {
         sl.tile_hist_next = (p + 1 < passes) ? s->sort_status.as<unsigned>() + (size_t)(p + 1) * region
                                                 : nullptr;
         sl.prev_sort_words = s->prev_sort_words();
+        sl.grp_begin = (p + 1 == passes) ? s->grp_begin() : nullptr;
         sl.sort_tiles_cap = s->sort_tiles_cap;
         sl.shift = digit_bits * p;
         sl.bits = digit_bits;
@@ -471,6 +478,8 @@ RasterLaunch raster_args(gpk_session* s) {
     r.records = s->records.as<SurvivorRecord>();
     r.keys = s->keys[s->prep.final_buf].as<uint32_t>();
     r.vals = s->vals[s->prep.final_buf].as<uint32_t>();
+    r.grp_begin = s->grp_begin();
+    r.grp_shift = s->prep.passes ? s->prep.digit_bits * (s->prep.passes - 1) : -1;
     r.ctrl = s->ctrl();
     r.pair_cap = s->pair_cap;
     r.image = s->image.as<float>();

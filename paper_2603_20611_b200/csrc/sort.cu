@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
     const unsigned ntiles = (P + kSortTile - 1) / kSortTile;
     const unsigned nb = 1u << a.bits;
     const unsigned mask = nb - 1;
+    if (blockIdx.x == 0 && tid == 0 && a.grp_begin) a.grp_begin[nb] = P;
     if (blockIdx.x == 0 && tid == 0 && !a.tile_hist_next) {
         a.prev_sort_words[0] = ntiles;
         a.prev_sort_words[1] = nb;
@@ -62,6 +63,9 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
             for (int i = 0; i < kPer; ++i) {
                 const unsigned d = tid * kPer + i;
                 s_base[d] = ex;
+                // last pass: the digit groups' sorted start positions let the
+                // pixel kernels find their tile's range without a search
+                if (a.grp_begin && t == 0 && d < nb) a.grp_begin[d] = ex;
                 ex += v[i];
             }
             for (int w = 0; w < 8; ++w)

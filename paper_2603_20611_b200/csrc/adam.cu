@@ -14,6 +14,7 @@ namespace gpk {
 namespace {
 
 __global__ void __launch_bounds__(256) k_adam(const AdamLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ float s_c[7];  // bc1, bc2, lr pos, lr opacity, lr scale, lr rot, eps
     if (a.ctrl && a.ctrl->pair_overflow) return;
     if (threadIdx.x == 0) {
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(256) k_adam(const AdamLaunch a) {
 
 void launch_adam(const AdamLaunch& a, cudaStream_t st) {
     const unsigned grid = (a.n + 255) / 256;
-    if (grid) k_adam<<<grid, 256, 0, st>>>(a);
+    if (grid) launch_pdl(k_adam, dim3(grid), dim3(256), 0, st, a);
 }
 
 }  // namespace gpk

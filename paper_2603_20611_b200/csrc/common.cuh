@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace gpk {
 
 constexpr int kTile = 16;                  // RasterConfig::tile_size (render.hpp:28)
@@ -271,6 +273,35 @@ __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// ---- programmatic dependent launch (PDL) -------------------------------------
+// Every kernel of the step chain lets its successor start launching as soon as
+// all of its own CTAs are resident, and waits for its predecessor's completion
+// (and memory) before touching its outputs. Back-to-back kernels then overlap
+// launch latency and tails instead of draining the GPU between them. Both are
+// no-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_entry() {
+#ifdef GPK_PDL_EARLY_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... Params, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Pairs actually stored for the current slice (T capped by the buffer size).
 __device__ __forceinline__ unsigned stored_pairs(const Control* c, uint64_t cap) {

@@ -79,6 +79,7 @@ __device__ __forceinline__ void finish_loss(const LossLaunch& a, bool with_ssim)
 }
 
 __global__ void __launch_bounds__(256) k_l1_only(const LossLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ double s_red[16];
     const size_t n = (size_t)a.W * a.H;
     const float inv_n = (float)(1.0 / (double)n);
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(256) k_l1_only(const LossLaunch a) {
 }
 
 __global__ void __launch_bounds__(256) k_ssim_fwd(const LossLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ float s_x[kH][kH + 1];
     __shared__ float s_y[kH][kH + 1];
     __shared__ float s_h[5][kH][kT + 1];
@@ -173,6 +175,7 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(const LossLaunch a) {
 }
 
 __global__ void __launch_bounds__(256) k_ssim_bwd(const LossLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ float s_g[3][kH][kH + 1];
     __shared__ float s_h[3][kH][kT + 1];
     const int X0 = blockIdx.x * kT, Y0 = blockIdx.y * kT;
@@ -230,12 +233,12 @@ void launch_loss(const LossLaunch& a, cudaStream_t st) {
     if (a.lambda == 0.0) {
         const size_t n = (size_t)a.W * a.H;
         const unsigned grid = (unsigned)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
-        k_l1_only<<<grid, 256, 0, st>>>(a);
+        launch_pdl(k_l1_only, dim3(grid), dim3(256), 0, st, a);
         return;
     }
     const dim3 grid((a.W + kT - 1) / kT, (a.H + kT - 1) / kT);
-    k_ssim_fwd<<<grid, 256, 0, st>>>(a);
-    k_ssim_bwd<<<grid, 256, 0, st>>>(a);
+    launch_pdl(k_ssim_fwd, dim3(grid), dim3(256), 0, st, a);
+    launch_pdl(k_ssim_bwd, dim3(grid), dim3(256), 0, st, a);
 }
 
 unsigned loss_partial_blocks(int W, int H, double lambda) {

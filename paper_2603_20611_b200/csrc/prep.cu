@@ -171,6 +171,7 @@ constexpr int kZeroBuf = 256;  // floats in the dense-clear source buffer
 template <bool kZeroGrads>
 __global__ void __launch_bounds__(kPrepThreads, kFilterCtasPerSm)
     k_filter(const PrepLaunch a, float log_tau, int filter_on) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     extern __shared__ __align__(128) float s_p[];         // 11 planes x kFilterBlock
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ __align__(16) float s_zero[kZeroBuf];
@@ -352,6 +353,7 @@ constexpr int kDecideThreads = 256;
 constexpr int kDecideGroup = kDecideChunks * kFilterBlock;   // Gaussians per group
 
 __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     extern __shared__ unsigned s_dyn_u[];
     unsigned* s_incl = s_dyn_u;                                              // kDecideGroup
     uint16_t(*s_rect)[3] = reinterpret_cast<uint16_t(*)[3]>(s_dyn_u + kDecideGroup);  // kDecideGroup x 3
@@ -577,6 +579,7 @@ __device__ __forceinline__ void store_chain(const ChainLaunch& a, uint32_t i, co
 // inputs) take the inverse-free fp32 chain; the rest are deferred to
 // K_chain_exact so this kernel stays small in registers.
 __global__ void __launch_bounds__(128) k_chain(const ChainLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     const unsigned S = a.ctrl->survivors;
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.grads_dirty = S;
     for (unsigned slot = blockIdx.x * blockDim.x + threadIdx.x; slot < S;
@@ -603,6 +606,7 @@ __global__ void __launch_bounds__(128) k_chain(const ChainLaunch a) {
 
 // K_chain_exact: the reference's fp64 chain for the deferred survivors.
 __global__ void __launch_bounds__(128) k_chain_exact(const ChainLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     const unsigned E = *a.exact_count;
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
         const uint32_t cid = a.survivor_list[a.exact_list[e]];
@@ -879,12 +883,12 @@ void launch_bin(const PrepLaunch& a, cudaStream_t st) {
         attr = true;
     }
     const unsigned groups = (a.nfilter + kDecideChunks - 1) / kDecideChunks;
-    k_decide<<<groups, kDecideThreads, smem, st>>>(a);
+    launch_pdl(k_decide, dim3(groups), dim3(kDecideThreads), smem, st, a);
 }
 
 void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st) {
-    k_chain<<<grid, 128, 0, st>>>(a);
-    k_chain_exact<<<std::max(1, grid / 8), 128, 0, st>>>(a);
+    launch_pdl(k_chain, dim3(grid), dim3(128), 0, st, a);
+    launch_pdl(k_chain_exact, dim3(std::max(1, grid / 8)), dim3(128), 0, st, a);
 }
 
 }  // namespace gpk

@@ -104,6 +104,7 @@ __device__ __forceinline__ void tile_range(const RasterLaunch& a, int tile, unsi
 }
 
 __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ float4 s_rec[256][2];  // {ox, oy, a*k, 2b*k}, {d*k, alpha_tilde, mask, -}
     __shared__ unsigned s_range[2];
 
@@ -162,6 +163,7 @@ constexpr int kBwdBatch = 256;    // pairs staged per round (one per thread)
 constexpr int kWorkBuckets = 16;
 
 __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ float s_dl[kTile * kTile];
     __shared__ float4 s_pair[kBwdBatch][2];   // {ox, oy, ca, cb}, {cd, at, rect, pos}
     __shared__ unsigned s_bucket[kWorkBuckets];
@@ -280,12 +282,12 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
 
 void launch_raster_fwd(const RasterLaunch& a, cudaStream_t st) {
     const int tiles = a.slice.tiles_x * a.slice.tiles_y;
-    if (tiles > 0) k_raster_fwd<<<tiles, 256, 0, st>>>(a);
+    if (tiles > 0) launch_pdl(k_raster_fwd, dim3(tiles), dim3(256), 0, st, a);
 }
 
 void launch_raster_bwd(const RasterLaunch& a, cudaStream_t st) {
     const int tiles = a.slice.tiles_x * a.slice.tiles_y;
-    if (tiles > 0) k_raster_bwd<<<tiles, 256, 0, st>>>(a);
+    if (tiles > 0) launch_pdl(k_raster_bwd, dim3(tiles), dim3(256), 0, st, a);
 }
 
 }  // namespace gpk

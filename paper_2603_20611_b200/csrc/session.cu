@@ -90,6 +90,10 @@ struct gpk_session {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // U1 with a given dL/dI: the forward runs on `side`, concurrently with the
+    // backward on `stream` (fork/join by events; captured graphs keep the fork)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     uint64_t n = 0, cap = 0;
     gpk_bounds bbox{};
     uint64_t pair_cap = 0;
@@ -198,20 +202,21 @@ struct StageScope {
     gpk_session* s;
     int stage;
     cudaEvent_t a = nullptr;
-    StageScope(gpk_session* s_, int st) : s(s_), stage(st) {
+    cudaStream_t strm;
+    StageScope(gpk_session* s_, int st, cudaStream_t on = nullptr) : s(s_), stage(st), strm(on ? on : s_->stream) {
         if (!s->timing) return;
         if (s->pending.size() >= 8192 && !s->capturing) {
-            cudaStreamSynchronize(s->stream);
+            cudaStreamSynchronize(strm);
             drain_timing(s);
         }
         a = take_event(s);
         // under capture: an external event node (device timestamp on replay)
-        cudaEventRecordWithFlags(a, s->stream, s->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+        cudaEventRecordWithFlags(a, strm, s->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
     }
     void end() {
         if (!a) return;
         cudaEvent_t b = take_event(s);
-        cudaEventRecordWithFlags(b, s->stream, s->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+        cudaEventRecordWithFlags(b, strm, s->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
         s->pending.push_back({stage, a, b});
         a = nullptr;
     }
@@ -489,14 +494,15 @@ RasterLaunch raster_args(gpk_session* s) {
     return r;
 }
 
-int run_rasterize(gpk_session* s) {
+int run_rasterize(gpk_session* s, cudaStream_t on = nullptr) {
     if (!s->prep.valid) return fail(GPK_ERR_STATE, "rasterize: no prepared slice");
     const size_t px = (size_t)s->img_w * s->img_h;
-    StageScope scope(s, GPK_STAGE_RASTER);
+    cudaStream_t st = on ? on : s->stream;
+    StageScope scope(s, GPK_STAGE_RASTER, st);
     if (s->n == 0) {
-        CK(cudaMemsetAsync(s->image.p, 0, px * 4, s->stream));
+        CK(cudaMemsetAsync(s->image.p, 0, px * 4, st));
     } else {
-        launch_raster_fwd(raster_args(s), s->stream);
+        launch_raster_fwd(raster_args(s), st);
         CK(cudaGetLastError());
     }
     s->prep.rasterized = true;
@@ -544,6 +550,19 @@ int run_backward(gpk_session* s, bool stats) {
     const int grid = (int)std::min<uint64_t>((s->n + 127) / 128, (uint64_t)s->num_sms * 8);
     launch_chain(c, grid, s->stream);
     CK(cudaGetLastError());
+    return GPK_OK;
+}
+
+// U1 with dL/dI already in GPK_BUF_DL_DI: the forward does not feed the
+// backward, so it runs on the side stream while the backward (+ chain) runs on
+// the session stream; the session stream then waits for the forward.
+int run_fwd_bwd_forked(gpk_session* s) {
+    CK(cudaEventRecord(s->ev_fork, s->stream));
+    CK(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+    TRY(run_rasterize(s, s->side));
+    CK(cudaEventRecord(s->ev_join, s->side));
+    TRY(run_backward(s, false));
+    CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
     return GPK_OK;
 }
 
@@ -857,6 +876,9 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
         for (int k = 0; k < 4; ++k) es.first_index[k] = ~0ull;
         e = cudaMemcpyAsync(s->err(), &es, sizeof es, cudaMemcpyHostToDevice, s->stream);
     }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) {
         gpk_session_destroy(s);
@@ -892,6 +914,12 @@ int gpk_session_destroy(gpk_session* s) {
     for (DevBuf* b : bufs) b->release();
     drain_timing(s);
     for (cudaEvent_t e : s->event_pool) cudaEventDestroy(e);
+    if (s->side) {
+        cudaStreamSynchronize(s->side);
+        cudaStreamDestroy(s->side);
+    }
+    if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+    if (s->ev_join) cudaEventDestroy(s->ev_join);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
     return ok();
@@ -1314,8 +1342,7 @@ int gpk_fwd_bwd_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf*
     if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
     TRY(set_device(s));
     TRY(run_prepare(s, pose, psf, cfg, true));
-    TRY(run_rasterize(s));
-    TRY(run_backward(s, false));
+    TRY(run_fwd_bwd_forked(s));
     return ok();
 }
 
@@ -1411,8 +1438,7 @@ int gpk_graph_capture_fwd_bwd(gpk_session* s, const gpk_slice_pose* pose, const 
     return capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
         const FwdBwdArgs* a = static_cast<const FwdBwdArgs*>(p);
         TRY(run_prepare(ss, a->pose, a->psf, a->cfg, true));
-        TRY(run_rasterize(ss));
-        TRY(run_backward(ss, false));
+        TRY(run_fwd_bwd_forked(ss));
         return GPK_OK;
     }, &args);
 }

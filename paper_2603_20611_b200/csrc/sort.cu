@@ -21,6 +21,7 @@ namespace gpk {
 namespace {
 
 __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ unsigned s_whist[8][kMaxBuckets];   // per-warp digit counts -> offsets
     __shared__ unsigned s_base[kMaxBuckets];       // digit base for this tile
     __shared__ unsigned s_wsum[32];
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
 }  // namespace
 
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st) {
-    k_sort_pass<<<grid, kSortThreads, 0, st>>>(a);
+    launch_pdl(k_sort_pass, dim3(grid), dim3(kSortThreads), 0, st, a);
 }
 
 }  // namespace gpk

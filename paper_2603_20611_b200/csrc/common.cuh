@@ -114,7 +114,8 @@ struct alignas(64) Control {
     unsigned int exact_chunk_ctr;              // chunk claims of K_exact
     unsigned int chain_exact;                  // survivors deferred to the fp64 chain
     unsigned int exact_decided;                // survivors decided on the reference-order fp64 path
-    unsigned int pad[4];
+    unsigned int dirty_ctr;                    // K_chain: next slot of the dirty-gradient list
+    unsigned int pad[3];
 };
 
 constexpr int kExactChunk = 256;               // candidates per K_exact chunk (= threads)
@@ -326,7 +327,9 @@ struct PrepLaunch {
     CandParams* cand;         // K_filter -> K_decide: candidate params, block-major slots
     unsigned* cand_count;     // candidates per chunk (plain stores)
     CandParams* surv_params;  // survivor params by survivor slot
-    unsigned nfilter;         // 1024-Gaussian chunks
+    uint2* grp_pairs;         // per K_decide group: (first pair position, pair count)
+    unsigned* grp_surv;       // per K_decide group: survivors (slots g*4096 + [0, S_g))
+    unsigned nfilter;         // 64-Gaussian chunks
     SurvivorRecord* records;  // indexed by candidate slot
     uint32_t* survivor_list;  // survivor slot -> candidate slot
     uint32_t* keys;           // pre-sort tile keys
@@ -346,9 +349,11 @@ struct PrepLaunch {
     SliceArgs slice;
 };
 
-constexpr int kFilterItems = 4;
-constexpr int kFilterBlock = kPrepThreads * kFilterItems;  // Gaussians per K_filter block
-constexpr int kDecideChunks = 4;                           // K_filter chunks per K_decide group
+constexpr int kFilterItems = 2;                            // consecutive Gaussians per K_filter lane
+constexpr int kFilterBlock = 32 * kFilterItems;            // Gaussians per K_filter warp chunk (64)
+constexpr int kDecideChunks = 64;                          // K_filter chunks per K_decide group
+constexpr int kDecideGroupSize = kDecideChunks * kFilterBlock;  // Gaussians per group (4096)
+constexpr int kParamAlign = 512;                           // plane stride (capacity) granularity
 
 struct SortLaunch {
     const uint32_t* keys_in;
@@ -361,6 +366,8 @@ struct SortLaunch {
     uint64_t sort_tiles_cap;       // offset (in rows) of the super-tile rows
     unsigned* prev_sort_words;     // written by the last pass: {sort tiles, buckets, passes}
     unsigned* grp_begin;           // last pass only: first sorted position of every digit (+ end)
+    const uint2* grp_pairs;        // pass over K_decide output: sort tiles are its groups (in group
+    unsigned ngroups;              //   order = slot order); nullptr: tiles of kSortTile positions
     int shift;
     int bits;                      // digit width of this pass
     unsigned next_buckets;         // 2^bits of the next pass
@@ -400,8 +407,10 @@ struct ChainLaunch {
     float* stat_norm;              // optional (screen-space dL/dmu_2d norm)
     uint8_t* stat_observed;        // optional
     float* stat_world;             // optional, 3 per primitive
-    uint32_t* exact_list;          // survivor slots deferred to the fp64 chain
+    uint32_t* exact_list;          // record slots deferred to the fp64 chain
     unsigned* exact_count;         // Control::chain_exact
+    const unsigned* grp_surv;      // survivors per K_decide group (CTA per group)
+    unsigned* dirty_ctr;           // Control::dirty_ctr
     ErrorState* err;
     SliceArgs slice;
 };

@@ -129,10 +129,10 @@ __device__ __forceinline__ void load_params(const float* __restrict__ params, ui
 // Undecided items take the full test, compacted, so the warp does not pay it
 // for every Gaussian.
 __device__ __forceinline__ bool quick_culled_identity(const float p[11], const FilterConsts& c) {
-    float sum = p[0];
-#pragma unroll
-    for (int k = 1; k < 11; ++k) sum += p[k];
-    if (!isfinite(sum)) return false;
+    // NaN/Inf guard: log-scales (fmaxf/fminf drop NaN), mu_z and alpha_raw
+    // (fminf drops NaN) explicitly; mu_x/y propagate into the final compare
+    // (false -> not culled) and the quaternion fails the norm range test.
+    if (!isfinite(((p[2] + p[3]) + (p[4] + p[5])) + p[10])) return false;
     const float lmax = fmaxf(p[3], fmaxf(p[4], p[5])), lmin = fminf(p[3], fminf(p[4], p[5]));
     if (!(lmax < 40.f && lmin > -40.f && lmax - lmin < 6.2f)) return false;
     const float qn2 = __fmaf_rn(p[6], p[6], __fmaf_rn(p[7], p[7], __fmaf_rn(p[8], p[8], p[9] * p[9])));
@@ -152,66 +152,31 @@ __device__ __forceinline__ bool quick_culled_identity(const float p[11], const F
 }
 
 // ---- K_filter ------------------------------------------------------------------
-// prepare_gaussians' cull (render.hpp:107) as a streaming pass. CTAs walk
-// 1024-Gaussian chunks (4 per SM resident, one chunk each in flight):
-//   1. TMA bulk copy of the chunk's 11 parameter planes (44 KB) into shared
-//      memory (cp.async.bulk + mbarrier complete_tx); when the gradient planes
-//      must be cleared densely, bulk shared->global stores of a zero buffer.
-//   2. fp32 certain-cull: a division-free quick bound for everything, the full
-//      closed form (q = mu_cz^2 / (sigma_z^2 + Sigma_c,zz))
-//      only for the undecided, compacted — both conservative: a culled
-//      Gaussian is one the reference culls too.
-//   3. candidates compacted in set order into 48 B CandParams records at
-//      block-major slots [b*1024, b*1024 + count_b), count_b stored plainly.
-// No fp64 and no cross-CTA waiting here, so the kernel stays small in
-// registers and the HBM stream has all the warps it needs.
-constexpr int kFilterCtasPerSm = 4;
-constexpr int kZeroBuf = 256;  // floats in the dense-clear source buffer
+// prepare_gaussians' cull (render.hpp:107) as a streaming pass with no block
+// barriers. Warps walk 64-Gaussian chunks grid-stride; each lane owns two
+// consecutive Gaussians and loads their 11 parameters with one 8 B vector load
+// per plane straight into registers (many warps per SM keep the HBM pipe
+// full). Per chunk:
+//   1. division-free fp32 quick bound; lanes whose Gaussians it cannot decide
+//      run the full closed-form test (q = mu_cz^2 / (sigma_z^2 + Sigma_c,zz),
+//      SURVEY.md §7.3.2) — both conservative: a culled Gaussian is one the
+//      reference culls too;
+//   2. candidates compacted in set order (warp scan) into 48 B CandParams
+//      records at chunk-major slots [b*64, b*64 + count_b), count_b stored.
+// Gradient clearing (dense output contract, grad_chain.hpp:12-22): the previous
+// survivors' entries (sparse), or the chunk's planes when anything else wrote
+// them. No fp64 and no cross-warp waiting here.
+constexpr int kFilterThreads = 256;
 
 template <bool kZeroGrads>
-__global__ void __launch_bounds__(kPrepThreads, kFilterCtasPerSm)
-    k_filter(const PrepLaunch a, float log_tau, int filter_on) {
+__global__ void __launch_bounds__(kFilterThreads) k_filter(const PrepLaunch a, float log_tau, int filter_on) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    extern __shared__ __align__(128) float s_p[];         // 11 planes x kFilterBlock
-    __shared__ __align__(8) uint64_t s_bar;
-    __shared__ __align__(16) float s_zero[kZeroBuf];
-    __shared__ uint8_t s_flag[kFilterBlock];              // 0 culled, 1 candidate, 2 undecided
-    __shared__ uint16_t s_list[kFilterBlock];             // undecided work list
-    __shared__ unsigned s_off[kFilterItems * 8];
-    __shared__ unsigned s_nfull;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     const unsigned nchunks = a.nfilter;
-    const unsigned plane_bytes = kFilterBlock * sizeof(float);
     const unsigned dirty = kZeroGrads ? *a.grads_dirty : 0u;
     const bool dense_zero = kZeroGrads && dirty == kGradsDense;
-
-    if (tid == 0) {
-        mbar_init(&s_bar, 1);
-        fence_mbar_init();
-        s_nfull = 0;
-    }
-    if (dense_zero) {
-        for (int i = tid; i < kZeroBuf; i += kPrepThreads) s_zero[i] = 0.f;
-        fence_proxy_async_smem();
-    }
-    __syncthreads();
-    auto stage_chunk = [&](unsigned bb) {
-        const uint32_t bbase = bb * kFilterBlock;
-        mbar_expect_tx(&s_bar, 11 * plane_bytes);
-#pragma unroll 1
-        for (int k = 0; k < 11; ++k)
-            bulk_g2s(s_p + k * kFilterBlock, a.params + (uint64_t)k * a.cap + bbase, plane_bytes, &s_bar);
-        if (dense_zero) {
-#pragma unroll 1
-            for (int k = 0; k < 11; ++k)
-#pragma unroll 1
-                for (int z = 0; z < kFilterBlock; z += kZeroBuf)
-                    bulk_s2g(a.grads + (uint64_t)k * a.cap + bbase + z, s_zero, kZeroBuf * sizeof(float));
-            bulk_commit();
-        }
-    };
-    if (tid == 0 && blockIdx.x < nchunks) stage_chunk(blockIdx.x);  // in flight during housekeeping
+    const unsigned gthreads = gridDim.x * kFilterThreads;
+    const unsigned gtid = blockIdx.x * kFilterThreads + tid;
 
     // Housekeeping: clear the per-sort-tile digit histograms the previous
     // sort used (its passes only) before this prepare / the radix passes refill
@@ -220,15 +185,13 @@ __global__ void __launch_bounds__(kPrepThreads, kFilterCtasPerSm)
         const unsigned pt = a.prev_sort_words[0], pnb = a.prev_sort_words[1], pp = a.prev_sort_words[2];
         const unsigned tile_words = pt * pnb;
         const unsigned used = tile_words + ((pt + kSuperTiles - 1) / kSuperTiles) * pnb;  // per pass
-        const unsigned stride = gridDim.x * kPrepThreads;
         for (unsigned ps = 0; ps < pp; ++ps) {
             unsigned* region = a.tile_hist_all + (uint64_t)ps * a.hist_region;
             unsigned* super = region + a.sort_tiles_cap * pnb - tile_words;
-            for (unsigned w = blockIdx.x * kPrepThreads + tid; w < used; w += stride)
-                (w < tile_words ? region : super)[w] = 0u;
+            for (unsigned w = gtid; w < used; w += gthreads) (w < tile_words ? region : super)[w] = 0u;
         }
         if (kZeroGrads && !dense_zero)
-            for (unsigned e = blockIdx.x * kPrepThreads + tid; e < dirty; e += stride) {
+            for (unsigned e = gtid; e < dirty; e += gthreads) {
                 const uint32_t i = a.dirty_idx[e];
 #pragma unroll
                 for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = 0.f;
@@ -248,89 +211,56 @@ __global__ void __launch_bounds__(kPrepThreads, kFilterCtasPerSm)
     fc.inv_sz2 = (float)(1.0 / (a.slice.sigma_z * a.slice.sigma_z));
     const bool ident = a.slice.identity_rot != 0;
 
-    unsigned phase = 0;
-    for (unsigned b = blockIdx.x; b < nchunks; b += gridDim.x, phase ^= 1u) {
-        const uint32_t base = b * kFilterBlock;
-        mbar_wait(&s_bar, phase);
-
-        // ---- certain-cull: quick bound, then the full test compacted ----------
+    const unsigned gwarps = gthreads / 32;
+    for (unsigned b = gtid / 32; b < nchunks; b += gwarps) {
+        const uint32_t i0 = b * kFilterBlock + lane * kFilterItems;  // this lane's first Gaussian
+        // cap is a multiple of kParamAlign: the pair load never leaves the plane
+        float2 v[11];
+#pragma unroll
+        for (int q = 0; q < 11; ++q) v[q] = __ldcs(reinterpret_cast<const float2*>(a.params + (uint64_t)q * a.cap + i0));
+        if (dense_zero)
+#pragma unroll
+            for (int q = 0; q < 11; ++q)
+                *reinterpret_cast<float2*>(a.grads + (uint64_t)q * a.cap + i0) = make_float2(0.f, 0.f);
+        unsigned cmask = 0;
 #pragma unroll
         for (int k = 0; k < kFilterItems; ++k) {
-            const int li = k * kPrepThreads + tid;
-            uint8_t flag = 0;
-            if (base + li < a.n) {
-                flag = 1;
-                if (filter_on) {
-                    flag = 2;
-                    if (ident) {
-                        float p[11];
+            if (i0 + k >= a.n) continue;
+            float p[11];
 #pragma unroll
-                        for (int q = 0; q < 11; ++q) p[q] = s_p[q * kFilterBlock + li];
-                        if (quick_culled_identity(p, fc)) flag = 0;
-                    }
+            for (int q = 0; q < 11; ++q) p[q] = k ? v[q].y : v[q].x;
+            bool cand = true;
+            if (filter_on) {
+                if (ident && quick_culled_identity(p, fc)) {
+                    cand = false;
+                } else {
+                    cand = ident ? !certainly_culled_identity(p, fc)
+                                 : !certainly_culled(p, a.slice, log_tau, fc.mod, fc.sz2);
                 }
             }
-            s_flag[li] = flag;
-            const unsigned m = __ballot_sync(0xffffffffu, flag == 2);
-            if (m) {
-                unsigned wbase = 0;
-                if (lane == 0) wbase = atomicAdd(&s_nfull, (unsigned)__popc(m));
-                wbase = __shfl_sync(0xffffffffu, wbase, 0);
-                if (flag == 2) s_list[wbase + __popc(m & lanemask_lt())] = (uint16_t)li;
-            }
+            cmask |= (cand ? 1u : 0u) << k;
         }
-        __syncthreads();
-        {
-            const unsigned nfull = s_nfull;
-            for (unsigned j = tid; j < nfull; j += kPrepThreads) {
-                const int li = s_list[j];
-                float p[11];
+        // set-order compaction: lanes in order, each lane's two Gaussians in order
+        const unsigned nc = __popc(cmask);
+        unsigned incl = nc;
 #pragma unroll
-                for (int q = 0; q < 11; ++q) p[q] = s_p[q * kFilterBlock + li];
-                const bool culled = ident ? certainly_culled_identity(p, fc)
-                                          : certainly_culled(p, a.slice, log_tau, fc.mod, fc.sz2);
-                s_flag[li] = culled ? 0 : 1;
-            }
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
         }
-        __syncthreads();
-
-        // ---- candidates in set order -------------------------------------------
-        unsigned ballots[kFilterItems];
+        if (lane == 31) a.cand_count[b] = incl;
+        if (cmask) {
+            CandParams* out = a.cand + (uint64_t)b * kFilterBlock + (incl - nc);
 #pragma unroll
-        for (int k = 0; k < kFilterItems; ++k) {
-            ballots[k] = __ballot_sync(0xffffffffu, s_flag[k * kPrepThreads + tid] == 1);
-            if (lane == 0) s_off[k * 8 + warp] = __popc(ballots[k]);
-        }
-        __syncthreads();
-        if (warp == 0) {  // exclusive scan of the 32 (item, warp) slots
-            const unsigned v = s_off[lane];
-            unsigned incl = v;
+            for (int k = 0; k < kFilterItems; ++k)
+                if (cmask & (1u << k)) {
+                    float p[11];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += u;
-            }
-            s_off[lane] = incl - v;
-            if (lane == 31) a.cand_count[b] = incl;
-        }
-        __syncthreads();
-        CandParams* out = a.cand + base;
-#pragma unroll
-        for (int k = 0; k < kFilterItems; ++k)
-            if (ballots[k] & (1u << lane)) {
-                const int li = k * kPrepThreads + tid;
-                float p[11];
-#pragma unroll
-                for (int q = 0; q < 11; ++q) p[q] = s_p[q * kFilterBlock + li];
-                store_cand(out + s_off[k * 8 + warp] + __popc(ballots[k] & lanemask_lt()), p, base + li);
-            }
-        __syncthreads();  // s_p, s_flag, s_list, s_off free again
-        if (tid == 0) {
-            s_nfull = 0;
-            if (b + gridDim.x < nchunks) stage_chunk(b + gridDim.x);
+                    for (int q = 0; q < 11; ++q) p[q] = k ? v[q].y : v[q].x;
+                    store_cand(out++, p, i0 + k);
+                }
         }
     }
-    if (dense_zero && tid == 0) bulk_wait_all();
 }
 
 // ---- K_decide ------------------------------------------------------------------
@@ -350,7 +280,7 @@ __global__ void __launch_bounds__(kPrepThreads, kFilterCtasPerSm)
 //      reference's ascending per-tile lists — with the first radix pass's
 //      digit histograms (global, per sort tile, per super-tile).
 constexpr int kDecideThreads = 256;
-constexpr int kDecideGroup = kDecideChunks * kFilterBlock;   // Gaussians per group
+constexpr int kDecideGroup = kDecideGroupSize;
 
 __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
@@ -369,17 +299,30 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     const unsigned ngroups = gridDim.x;
     for (int k = tid; k < a.passes * kMaxBuckets; k += kDecideThreads) (&s_hist[0][0])[k] = 0;
     if (tid == 0) {
-        const unsigned g = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
-        s_grp = g;
+        s_grp = blockIdx.x;
         s_nsurv = 0;
         s_nexact = 0;
-        unsigned acc = 0;
-        for (int q = 0; q < kDecideChunks; ++q) {
-            s_cpre[q] = acc;
-            const unsigned c = g * kDecideChunks + q;
-            acc += c < a.nfilter ? __ldcg(&a.cand_count[c]) : 0u;
+    }
+    __syncthreads();
+    if (warp < kDecideChunks / 32) {  // exclusive prefix of the group's chunk counts
+        const unsigned c = s_grp * kDecideChunks + tid;
+        const unsigned v = c < a.nfilter ? __ldcg(&a.cand_count[c]) : 0u;
+        unsigned incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
         }
-        s_cpre[kDecideChunks] = acc;
+        s_cpre[tid] = incl - v;
+        if (lane == 31) s_cnt[0][warp] = incl;
+    }
+    __syncthreads();
+    if (tid < kDecideChunks && warp > 0)
+        for (int w = 0; w < warp; ++w) s_cpre[tid] += s_cnt[0][w];
+    if (tid == 0) {
+        unsigned tot = 0;
+        for (int w = 0; w < kDecideChunks / 32; ++w) tot += s_cnt[0][w];
+        s_cpre[kDecideChunks] = tot;
     }
     __syncthreads();
     const unsigned g = s_grp;
@@ -394,9 +337,10 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
         uint32_t i = 0;
         bool survive = false;
         if (j < nc) {
-            int q = 0;
+            int q = 0;  // chunk of candidate j: last q with s_cpre[q] <= j
 #pragma unroll
-            for (int t = 1; t < kDecideChunks; ++t) q += (j >= s_cpre[t]);
+            for (int step = kDecideChunks / 2; step > 0; step >>= 1)
+                if (s_cpre[q + step] <= j) q += step;
             load_cand(a.cand + (uint64_t)base + q * kFilterBlock + (j - s_cpre[q]), pf, i);
             uint32_t flag = 0;
             const int fr = fast_decide(pf, a.slice, rec);
@@ -485,29 +429,21 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     }
     __syncthreads();
     const unsigned Pb = S ? s_incl[S - 1] : 0u;
-    if (warp == 0) {
-        const unsigned long long agg = ((unsigned long long)S << 32) | Pb;
-        const unsigned long long excl = warp_prefix_aggregates(a.exact_words, g, agg);
-        if (lane == 0) {
-            s_excl = excl;
-            if (g == ngroups - 1) {
-                const unsigned long long tot = excl + agg;
-                const unsigned P = (unsigned)(tot & 0xffffffffull);
-                a.ctrl->survivors = (unsigned)(tot >> 32);
-                a.ctrl->pairs = P;
-                a.ctrl->pair_overflow = (P > a.pair_cap) ? 1u : 0u;
-            }
-        }
+    // ---- 2. reserve the group's pair range (no ordering between groups here:
+    // the radix pass orders pairs of equal tile by group index, i.e. by slot)
+    if (tid == 0) {
+        const unsigned P0 = atomicAdd(&a.ctrl->pairs, Pb);
+        if (S) atomicAdd(&a.ctrl->survivors, S);
+        if ((unsigned long long)P0 + Pb > a.pair_cap) a.ctrl->pair_overflow = 1u;
+        a.grp_pairs[g] = make_uint2(P0, Pb);
+        a.grp_surv[g] = S;
+        s_excl = P0;
     }
     __syncthreads();
 
-    // ---- 3. survivor slots and pair emission -------------------------------------
-    const unsigned S0 = (unsigned)(s_excl >> 32);
-    const unsigned P0 = (unsigned)(s_excl & 0xffffffffull);
-    for (unsigned j = tid; j < S; j += kDecideThreads) {
-        a.survivor_list[S0 + j] = base + j;
-        a.records[base + j].pair_base = P0 + (j ? s_incl[j - 1] : 0u);
-    }
+    // ---- 3. pair bases and pair emission ------------------------------------------
+    const unsigned P0 = (unsigned)s_excl;
+    for (unsigned j = tid; j < S; j += kDecideThreads) a.records[base + j].pair_base = P0 + (j ? s_incl[j - 1] : 0u);
     for (unsigned k = tid; k < Pb; k += kDecideThreads) {
         unsigned lo = 0, hi = S - 1;
         while (lo < hi) {
@@ -521,16 +457,20 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
         if (pos < a.pair_cap) {
             a.keys[pos] = tile;
             a.vals[pos] = base + lo;
-            if (a.passes > 0) {
-                const uint64_t st = pos / kSortTile;
-                atomicAdd(&a.tile_hist0[st * nb + (tile & dmask)], 1u);
-                atomicAdd(&a.tile_hist0[(a.sort_tiles_cap + st / kSuperTiles) * nb + (tile & dmask)], 1u);
-            }
             for (int ps = 0; ps < a.passes; ++ps)
                 atomicAdd(&s_hist[ps][(tile >> (a.digit_bits * ps)) & dmask], 1u);
         }
     }
     __syncthreads();
+    // first radix pass: this group's digit-count row (plain stores, every digit),
+    // its super-row and the global counts of every pass
+    unsigned* row = a.tile_hist0 + (uint64_t)g * nb;
+    unsigned* super = a.tile_hist0 + (a.sort_tiles_cap + g / kSuperTiles) * nb;
+    for (unsigned d = tid; d <= dmask; d += kDecideThreads) {
+        const unsigned v = s_hist[0][d];
+        row[d] = v;
+        if (v) atomicAdd(&super[d], v);
+    }
     for (int ps = 0; ps < a.passes; ++ps)
         for (unsigned d = tid; d <= dmask; d += kDecideThreads) {
             const unsigned v = s_hist[ps][d];
@@ -578,17 +518,18 @@ __device__ __forceinline__ void store_chain(const ChainLaunch& a, uint32_t i, co
 // fast_prepare resolves (the same decision K_exact made: identical code and
 // inputs) take the inverse-free fp32 chain; the rest are deferred to
 // K_chain_exact so this kernel stays small in registers.
-__global__ void __launch_bounds__(128) k_chain(const ChainLaunch a) {
+__global__ void __launch_bounds__(256) k_chain(const ChainLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    const unsigned S = a.ctrl->survivors;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *a.grads_dirty = S;
-    for (unsigned slot = blockIdx.x * blockDim.x + threadIdx.x; slot < S;
-         slot += gridDim.x * blockDim.x) {
-        const uint32_t cid = a.survivor_list[slot];
+    // CTA per K_decide group: its survivors sit at slots [g*4096, g*4096 + S_g)
+    const unsigned g = blockIdx.x;
+    const unsigned S = a.grp_surv[g];
+    if (g == 0 && threadIdx.x == 0) *a.grads_dirty = a.ctrl->survivors;
+    for (unsigned j = threadIdx.x; j < S; j += blockDim.x) {
+        const uint32_t cid = g * kDecideGroupSize + j;
         const SurvivorRecord rec = a.records[cid];
-        a.dirty_idx[slot] = rec.gidx & ~kExactFlag;
+        a.dirty_idx[atomicAdd(a.dirty_ctr, 1u)] = rec.gidx & ~kExactFlag;
         if (rec.gidx & kExactFlag) {
-            a.exact_list[atomicAdd(a.exact_count, 1u)] = slot;
+            a.exact_list[atomicAdd(a.exact_count, 1u)] = cid;
             continue;
         }
         float pf[11];
@@ -598,9 +539,9 @@ __global__ void __launch_bounds__(128) k_chain(const ChainLaunch a) {
         fast_state(pf, a.slice, ff);
         double acc[6];
         merge_partials(a, rec, acc);
-        float g[11], dmu[3];
-        fast_backward(pf, ff, acc, a.slice, g, dmu);
-        store_chain(a, i, g, dmu, acc);
+        float g11[11], dmu[3];
+        fast_backward(pf, ff, acc, a.slice, g11, dmu);
+        store_chain(a, i, g11, dmu, acc);
     }
 }
 
@@ -609,7 +550,7 @@ __global__ void __launch_bounds__(128) k_chain_exact(const ChainLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     const unsigned E = *a.exact_count;
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-        const uint32_t cid = a.survivor_list[a.exact_list[e]];
+        const uint32_t cid = a.exact_list[e];  // record slot
         const SurvivorRecord rec = a.records[cid];
         float pf[11];
         uint32_t i;
@@ -859,19 +800,17 @@ void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st) {
     const bool filter_on = a.slice.tau > 0.0 && a.slice.mod > 1e-10 && a.slice.mod < 1e10 &&
                            a.slice.sigma_z > 1e-10 && a.slice.sigma_z < 1e10;
     const float log_tau = filter_on ? (float)log(a.slice.tau) : 0.f;
-    const int smem = 11 * kFilterBlock * (int)sizeof(float);
     static int per_sm = 0;
     if (!per_sm) {
-        cudaFuncSetAttribute(k_filter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_filter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<true>, kPrepThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<true>, kFilterThreads, 0);
         if (per_sm < 1) per_sm = 1;
     }
-    const unsigned grid = (unsigned)std::min<uint64_t>(a.nfilter, (uint64_t)num_sms * per_sm);
+    const uint64_t need = ((uint64_t)a.nfilter * 32 + kFilterThreads - 1) / kFilterThreads;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms * per_sm));
     if (a.grads)
-        k_filter<true><<<grid, kPrepThreads, smem, st>>>(a, log_tau, filter_on ? 1 : 0);
+        launch_pdl(k_filter<true>, dim3(grid), dim3(kFilterThreads), 0, st, a, log_tau, filter_on ? 1 : 0);
     else
-        k_filter<false><<<grid, kPrepThreads, smem, st>>>(a, log_tau, filter_on ? 1 : 0);
+        launch_pdl(k_filter<false>, dim3(grid), dim3(kFilterThreads), 0, st, a, log_tau, filter_on ? 1 : 0);
 }
 
 void launch_bin(const PrepLaunch& a, cudaStream_t st) {
@@ -887,7 +826,7 @@ void launch_bin(const PrepLaunch& a, cudaStream_t st) {
 }
 
 void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st) {
-    launch_pdl(k_chain, dim3(grid), dim3(128), 0, st, a);
+    launch_pdl(k_chain, dim3(grid), dim3(256), 0, st, a);
     launch_pdl(k_chain_exact, dim3(std::max(1, grid / 8)), dim3(128), 0, st, a);
 }
 

@@ -108,6 +108,9 @@ struct gpk_session {
     DevBuf cand_count; // candidates per 1024-Gaussian chunk
     DevBuf surv_params;  // CandParams of survivors by survivor slot (K_decide)
     DevBuf dirty_idx;  // set indices of the last backward's survivors
+    DevBuf grp_table;  // per K_decide group: uint2 (first pair, pairs), then u32 survivors
+    uint2* grp_pairs() { return grp_table.as<uint2>(); }
+    unsigned* grp_surv() { return reinterpret_cast<unsigned*>(grp_table.as<char>() + (cap / kDecideGroupSize + 2) * 8); }
     int num_sms = 148;
     DevBuf persist;    // ErrorState | epoch | adam step | adam done ctr | loss done ctr | loss
     DevBuf image, dl_di, target, loss_g, loss_partial;
@@ -375,11 +378,14 @@ int make_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
 void sort_plan(int tiles, int& passes, int& digit_bits) {
     int bits = 0;
     while (bits < 32 && (1ull << bits) < (unsigned long long)tiles) ++bits;
+    bits = std::max(bits, 1);  // at least one pass: it orders the K_decide groups
     passes = (bits + kMaxDigitBits - 1) / kMaxDigitBits;
     digit_bits = passes ? (bits + passes - 1) / passes : 0;
 }
 
-int launch_sorts(gpk_session* s, int passes, int digit_bits);
+int launch_sorts(gpk_session* s, int passes, int digit_bits, const uint2* grp_pairs = nullptr,
+                 unsigned ngroups = 0);
+uint64_t decide_group_count(uint64_t n);
 
 int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                 const gpk_raster_config* cfg, bool zero_grads) {
@@ -415,6 +421,8 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     pl.surv_params = s->surv_params.as<CandParams>();
     pl.cand = s->cand.as<CandParams>();
     pl.cand_count = s->cand_count.as<unsigned>();
+    pl.grp_pairs = s->grp_pairs();
+    pl.grp_surv = s->grp_surv();
     pl.grads_dirty = s->grads_dirty();
     pl.dirty_idx = s->dirty_idx.as<uint32_t>();
     pl.nfilter = (unsigned)nbf;
@@ -444,14 +452,17 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
         CK(cudaGetLastError());
     }
     StageScope scope_sort(s, GPK_STAGE_SORT);
-    TRY(launch_sorts(s, ps.passes, ps.digit_bits));
+    TRY(launch_sorts(s, ps.passes, ps.digit_bits, s->grp_pairs(), (unsigned)decide_group_count(s->n)));
     ps.final_buf = ps.passes & 1;
     return GPK_OK;
 }
 
+uint64_t decide_group_count(uint64_t n) { return (filter_blocks(n) + kDecideChunks - 1) / kDecideChunks; }
+
 // Stable LSD radix passes over the (key, value) pairs in keys[0]/vals[0].
-int launch_sorts(gpk_session* s, int passes, int digit_bits) {
-    const int grid = (int)std::min<uint64_t>(s->sort_tiles_cap, (uint64_t)s->num_sms * 4);
+int launch_sorts(gpk_session* s, int passes, int digit_bits, const uint2* grp_pairs, unsigned ngroups) {
+    const int grid = (int)std::max<uint64_t>(
+        1, std::min<uint64_t>(std::max<uint64_t>(s->sort_tiles_cap, ngroups), (uint64_t)s->num_sms * 4));
     const size_t region = s->hist_region;
     for (int p = 0; p < passes; ++p) {
         SortLaunch sl;
@@ -472,6 +483,8 @@ int launch_sorts(gpk_session* s, int passes, int digit_bits) {
         sl.pass = p;
         sl.ctrl = s->ctrl();
         sl.pair_cap = s->pair_cap;
+        sl.grp_pairs = p == 0 ? grp_pairs : nullptr;
+        sl.ngroups = ngroups;
         launch_sort_pass(sl, grid, s->stream);
         CK(cudaGetLastError());
     }
@@ -543,12 +556,13 @@ int run_backward(gpk_session* s, bool stats) {
     c.stat_norm = stats ? s->stat_norm.as<float>() : nullptr;
     c.stat_observed = stats ? s->stat_obs.as<uint8_t>() : nullptr;
     c.stat_world = stats ? s->stat_world.as<float>() : nullptr;
-    c.exact_list = s->cand_list.as<uint32_t>();  // free after K_exact: reused as the deferral list
+    c.exact_list = s->cand_list.as<uint32_t>();  // deferral list (record slots)
     c.exact_count = &s->ctrl()->chain_exact;
+    c.grp_surv = s->grp_surv();
+    c.dirty_ctr = &s->ctrl()->dirty_ctr;
     c.err = s->err();
     c.slice = s->prep.slice;
-    const int grid = (int)std::min<uint64_t>((s->n + 127) / 128, (uint64_t)s->num_sms * 8);
-    launch_chain(c, grid, s->stream);
+    launch_chain(c, (int)decide_group_count(s->n), s->stream);
     CK(cudaGetLastError());
     return GPK_OK;
 }
@@ -612,7 +626,7 @@ int copy_planes_out(gpk_session* s, const float* dev, float* rec) {
 int alloc_for_n(gpk_session* s, uint64_t n) {
     // plane stride: a multiple of the K_filter chunk, so every chunk's plane
     // slice is a 4 KB, 16 B-aligned TMA bulk-copy source/destination
-    const uint64_t cap = (std::max<uint64_t>(n, 1) + kFilterBlock - 1) / kFilterBlock * kFilterBlock;
+    const uint64_t cap = (std::max<uint64_t>(n, 1) + kParamAlign - 1) / kParamAlign * kParamAlign;
     if (cap > s->cap || !s->params.p) {
         CK(s->params.ensure(cap * 11 * 4));
         CK(s->grads.ensure(cap * 11 * 4));
@@ -622,6 +636,7 @@ int alloc_for_n(gpk_session* s, uint64_t n) {
         CK(s->records.ensure(cap * sizeof(SurvivorRecord)));
         CK(s->cand_list.ensure(cap * 4));
         CK(s->surv_params.ensure(cap * sizeof(CandParams)));
+        CK(s->grp_table.ensure((cap / kDecideGroupSize + 2) * 12));
         CK(s->cand.ensure(cap * sizeof(CandParams)));
         CK(s->cand_count.ensure(nbf * 4));
         CK(s->dirty_idx.ensure(cap * 4));
@@ -908,7 +923,7 @@ int gpk_session_destroy(gpk_session* s) {
                       &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials,
                       &s->sort_status, &s->head, &s->persist, &s->image,
                       &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm,
-                      &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count,
+                      &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table,
                       &s->dirty_idx, &s->vox_records,
                       &s->volume, &s->dl_dv_vol, &s->vox_partials};
     for (DevBuf* b : bufs) b->release();
@@ -1138,8 +1153,14 @@ int gpk_get_prepared(gpk_session* s, uint32_t* index, int32_t* bounds, double* f
     uint64_t S = 0, T = 0;
     TRY(gpk_prepared_count(s, &S, &T));
     if (S == 0) return ok();
-    std::vector<uint32_t> list(S);
-    CK(cudaMemcpy(list.data(), s->survivors.p, S * 4, cudaMemcpyDeviceToHost));
+    // survivors in set order: K_decide groups in order, slots g*4096 + [0, S_g)
+    const uint64_t ng = decide_group_count(s->n);
+    std::vector<uint32_t> per(ng), list;
+    CK(cudaMemcpy(per.data(), s->grp_surv(), ng * 4, cudaMemcpyDeviceToHost));
+    list.reserve(S);
+    for (uint64_t g = 0; g < ng; ++g)
+        for (uint32_t j = 0; j < per[g]; ++j) list.push_back((uint32_t)(g * kDecideGroupSize + j));
+    if (list.size() != S) return fail(GPK_ERR_STATE, "prepared: survivor bookkeeping mismatch");
     std::vector<SurvivorRecord> recs(s->records.bytes / sizeof(SurvivorRecord));
     CK(cudaMemcpy(recs.data(), s->records.p, recs.size() * sizeof(SurvivorRecord),
                   cudaMemcpyDeviceToHost));

@@ -1,19 +1,26 @@
-// sort.cu — hand-written stable LSD radix sort of (tile key, candidate slot)
-// pairs, one kernel per digit of up to kMaxDigitBits bits (one pass for up to
-// 1024 tiles = a 512x512 slice, two passes up to 2^20 tiles).
+// sort.cu — hand-written stable LSD radix sort of (tile key, slot) pairs, one
+// kernel per digit of up to kMaxDigitBits bits (one pass for up to 1024 tiles
+// = a 512x512 slice, two passes up to 2^20 tiles).
 //
-// Stability is the whole point: pairs arrive in ascending candidate slot
-// (= set order), so a stable sort by tile reproduces the reference's per-tile
-// lists in ascending prepared index (render.hpp:151-157) bit-exactly.
+// Stability is the whole point: the output must list each tile's survivors in
+// ascending slot (= set) order to reproduce the reference's per-tile lists
+// (render.hpp:151-157) bit-exactly.
 //
-// Wait-free passes: the producer of a pass's input (K_exact for pass 0, pass p
-// for pass p+1) also counts, per kSortTile-key sort tile, how many keys carry
-// each digit value. A sort CTA therefore knows its output offsets up front —
-// global digit base (exclusive scan of the global histogram) + the column sum
-// of the per-tile histograms of all earlier tiles (coalesced L2 reads) — and
-// never waits on another CTA. Inside a tile, warp w owns a contiguous segment
-// processed in rounds of 32; ranks within a round come from __match_any_sync,
-// so the tile-local order is the input order.
+// Sort tiles. The first pass over K_decide's output takes the K_decide GROUPS
+// as its tiles, in group order: each group wrote its pairs in (slot, tile)
+// order into a range it reserved atomically (anywhere in the pair array), its
+// digit-count row and its super-row counts. Ordering groups by index here is
+// what makes the result stable in slot order, so K_decide never waits on
+// another group. Later passes (and the voxelizer's single ordered emission) use
+// tiles of kSortTile consecutive positions, counted by the producing pass.
+//
+// Wait-free passes: a CTA knows a tile's output offsets up front — global digit
+// base (exclusive scan of the global histogram) + the column sum of the digit
+// rows of all earlier tiles (whole super-tiles from the super rows, then at
+// most kSuperTiles-1 rows) — and never waits on another CTA. Inside a tile,
+// rounds of kSortTile pairs keep running per-digit offsets; in a round, warp w
+// owns a contiguous segment processed 32 at a time, ranks from
+// __match_any_sync, so the order inside a tile is the input order.
 #include "common.cuh"
 
 namespace gpk {
@@ -23,23 +30,36 @@ namespace {
 __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ unsigned s_whist[8][kMaxBuckets];   // per-warp digit counts -> offsets
-    __shared__ unsigned s_base[kMaxBuckets];       // digit base for this tile
+    __shared__ unsigned s_base[kMaxBuckets];       // running digit offsets of this tile
     __shared__ unsigned s_wsum[32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
-    const unsigned ntiles = (P + kSortTile - 1) / kSortTile;
+    const bool groups = a.grp_pairs != nullptr;
+    const unsigned ntiles = groups ? a.ngroups : (P + kSortTile - 1) / kSortTile;
     const unsigned nb = 1u << a.bits;
     const unsigned mask = nb - 1;
     if (blockIdx.x == 0 && tid == 0 && a.grp_begin) a.grp_begin[nb] = P;
     if (blockIdx.x == 0 && tid == 0 && !a.tile_hist_next) {
-        a.prev_sort_words[0] = ntiles;
+        // rows the filter clears before the next prepare: the largest tile
+        // count any pass of this sort used (group rows or position tiles)
+        const unsigned pos_tiles = (P + kSortTile - 1) / kSortTile;
+        a.prev_sort_words[0] = max(ntiles, max(pos_tiles, a.ngroups));
         a.prev_sort_words[1] = nb;
         a.prev_sort_words[2] = (unsigned)a.pass + 1;
     }
     const unsigned* super_rows = a.tile_hist + a.sort_tiles_cap * nb;
 
     for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        unsigned first, count;
+        if (groups) {
+            const uint2 gp = __ldcg(&a.grp_pairs[t]);
+            first = min(gp.x, P);
+            count = min(gp.x + gp.y, P) - first;
+        } else {
+            first = t * kSortTile;
+            count = min(P - first, (unsigned)kSortTile);
+        }
         // ---- global digit base: exclusive scan of the histogram (nb <= 1024)
         {
             constexpr int kPer = kMaxBuckets / kSortThreads;  // 4 digits per thread
@@ -47,7 +67,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
 #pragma unroll
             for (int i = 0; i < kPer; ++i) {
                 const unsigned d = tid * kPer + i;
-                v[i] = d < nb ? a.hist[d] : 0u;
+                v[i] = d < nb ? a.hist[d] : 0;
                 run += v[i];
             }
             unsigned incl = run;
@@ -69,8 +89,6 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
                 if (a.grp_begin && t == 0 && d < nb) a.grp_begin[d] = ex;
                 ex += v[i];
             }
-            for (int w = 0; w < 8; ++w)
-                for (unsigned d = tid; d < nb; d += kSortThreads) s_whist[w][d] = 0;
             __syncthreads();
         }
         // ---- add the counts of all earlier tiles: whole super-tiles from the
@@ -106,60 +124,66 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
                     acc += r < sup ? super_rows[(size_t)r * nb + tid] : a.tile_hist[(size_t)(t0 + r - sup) * nb + tid];
                 s_base[tid] += acc;
             }
+        }
+
+        // ---- rounds of kSortTile pairs, in input order ---------------------------
+        for (unsigned r0 = 0; r0 < count; r0 += kSortTile) {
+            for (int w = 0; w < 8; ++w)
+                for (unsigned d = tid; d < nb; d += kSortThreads) s_whist[w][d] = 0;
             __syncthreads();
-        }
-
-        // ---- rank: warp-local stable ranks via match_any -----------------
-        uint32_t key[kSortItems], val[kSortItems];
-        unsigned rank[kSortItems];
-        const unsigned seg = t * kSortTile + warp * (kSortItems * 32);
+            // rank: warp-local stable ranks via match_any
+            uint32_t key[kSortItems], val[kSortItems];
+            unsigned rank[kSortItems];
+            const unsigned seg = r0 + warp * (kSortItems * 32);
+            const unsigned lim = min(count - r0, (unsigned)kSortTile) + r0;
 #pragma unroll
-        for (int r = 0; r < kSortItems; ++r) {
-            const unsigned idx = seg + r * 32 + lane;
-            const bool valid = idx < P;
-            key[r] = valid ? a.keys_in[idx] : 0xffffffffu;
-            val[r] = valid ? a.vals_in[idx] : 0u;
-            const unsigned d = valid ? ((key[r] >> a.shift) & mask) : 0xffffffffu;
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
-            unsigned prior = 0;
-            if (valid) prior = s_whist[warp][d];
-            __syncwarp();
-            if (valid && (__ffs(peers) - 1) == lane) s_whist[warp][d] = prior + __popc(peers);
-            __syncwarp();
-            rank[r] = prior + __popc(peers & lanemask_lt());
-        }
-        __syncthreads();
-
-        // ---- per digit: exclusive prefix over warps on top of the tile base
-        for (unsigned d = tid; d < nb; d += kSortThreads) {
-            unsigned base = s_base[d];
-#pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                const unsigned c = s_whist[w][d];
-                s_whist[w][d] = base;
-                base += c;
+            for (int r = 0; r < kSortItems; ++r) {
+                const unsigned idx = seg + r * 32 + lane;
+                const bool valid = idx < lim;
+                key[r] = valid ? a.keys_in[first + idx] : 0xffffffffu;
+                val[r] = valid ? a.vals_in[first + idx] : 0u;
+                const unsigned d = valid ? ((key[r] >> a.shift) & mask) : 0xffffffffu;
+                const unsigned peers = __match_any_sync(0xffffffffu, d);
+                unsigned prior = 0;
+                if (valid) prior = s_whist[warp][d];
+                __syncwarp();
+                if (valid && (__ffs(peers) - 1) == lane) s_whist[warp][d] = prior + __popc(peers);
+                __syncwarp();
+                rank[r] = prior + __popc(peers & lanemask_lt());
             }
-        }
-        __syncthreads();
-
-        // ---- scatter (+ next pass's per-tile digit counts) ------------------
+            __syncthreads();
+            // per digit: exclusive prefix over warps on top of the running base
+            for (unsigned d = tid; d < nb; d += kSortThreads) {
+                unsigned base = s_base[d];
 #pragma unroll
-        for (int r = 0; r < kSortItems; ++r) {
-            const unsigned idx = seg + r * 32 + lane;
-            if (idx < P) {
-                const unsigned d = (key[r] >> a.shift) & mask;
-                const unsigned pos = s_whist[warp][d] + rank[r];
-                a.keys_out[pos] = key[r];
-                a.vals_out[pos] = val[r];
-                if (a.tile_hist_next) {
-                    const unsigned nd = (key[r] >> (a.shift + a.bits)) & (a.next_buckets - 1);
-                    const unsigned st = pos / kSortTile;
-                    atomicAdd(&a.tile_hist_next[(size_t)st * a.next_buckets + nd], 1u);
-                    atomicAdd(&a.tile_hist_next[(a.sort_tiles_cap + st / kSuperTiles) * a.next_buckets + nd], 1u);
+                for (int w = 0; w < 8; ++w) {
+                    const unsigned c = s_whist[w][d];
+                    s_whist[w][d] = base;
+                    base += c;
+                }
+                s_base[d] = base;  // the next round of this tile continues here
+            }
+            __syncthreads();
+            // scatter (+ next pass's per-tile digit counts)
+#pragma unroll
+            for (int r = 0; r < kSortItems; ++r) {
+                const unsigned idx = seg + r * 32 + lane;
+                if (idx < lim) {
+                    const unsigned d = (key[r] >> a.shift) & mask;
+                    const unsigned pos = s_whist[warp][d] + rank[r];
+                    a.keys_out[pos] = key[r];
+                    a.vals_out[pos] = val[r];
+                    if (a.tile_hist_next) {
+                        const unsigned nd = (key[r] >> (a.shift + a.bits)) & (a.next_buckets - 1);
+                        const unsigned st = pos / kSortTile;
+                        atomicAdd(&a.tile_hist_next[(size_t)st * a.next_buckets + nd], 1u);
+                        atomicAdd(&a.tile_hist_next[(a.sort_tiles_cap + st / kSuperTiles) * a.next_buckets + nd], 1u);
+                    }
                 }
             }
+            __syncthreads();
         }
-        __syncthreads();
+        __syncthreads();  // s_base / s_wsum are rewritten for the next tile
     }
 }
 

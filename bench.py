@@ -1,22 +1,32 @@
 #!/usr/bin/env python
-"""bench.py — fwd+bwd slices/s of the B200 slice renderer (BASELINE.json metric).
+"""bench.py — slices/s of the B200 slice renderer's training step (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1]): a 512x512x128 unit-spacing
-volume, 1M Gaussians from the reference's init_random(seed 1) (bit-identical
-stream, host-generated), PSF sigma_z = 1, RasterConfig defaults. One "step" is
-U1 = prepare_gaussians + tile binning + rasterize + backward for one slice with
-a fixed synthetic dL/dI, producing the dense (N x 11) gradient — the reference's
-prepare_gaussians + rasterize_prepared + backward_prepared (optimize.hpp:386-395).
-Slices cycle over 16 mid-stack indices. Inputs are resident in HBM; L2 (126 MB)
-is flushed by a 256 MiB write before every timed step, outside the per-step
-CUDA-event window.
+Workload (BASELINE.json configs[1] "light-sheet-like synthetic 512x512x128 stack,
+1M Gaussians, fwd+bwd training step on 1 B200"): a 512x512x128
+unit-spacing volume, 1M Gaussians from the reference's init_random(seed 1)
+(bit-identical stream), PSF sigma_z = 1, RasterConfig defaults, targets U(0, 0.1)
+(seed 7). One step = one slice of the reference's fit loop (optimize.hpp:385-402):
 
-Multi-GPU (torchrun): slices are sharded across ranks (rank r takes its own
-slice each step) with one NCCL all-reduce of the dense gradient per step; the
-reported value is all ranks' slices / max-over-ranks device time (weak scaling).
+  --unit u2 (default): prepare_gaussians + tile binning + rasterize +
+      photometric_loss(lambda = 0.2, SSIM) + backward + scheduled Adam;
+  --unit u1: prepare + binning + rasterize + backward for a given dL/dI,
+      producing the dense (N x 11) gradient.
 
---impl reference: the reference CPU implementation (oracle/_ref, the unmodified
-reference headers) on this host's cores, same config and metric, rank 0 only.
+Slices cycle over 16 mid-stack indices (one CUDA graph per pose). Parameters,
+moments and the target are resident in HBM; L2 (126 MB) is flushed by a 256 MiB
+read before every timed step, outside the per-step CUDA-event window.
+`e2e` is the same step through the C-ABI with host buffers: u2 uploads the
+step's target from pinned memory and reads the loss back; u1 uploads dL/dI and
+reads the image and the dense gradient back.
+
+Multi-GPU (torchrun): slices are sharded across ranks (rank r renders its own
+slice each step) with one NCCL all-reduce of the dense gradient per step (inside
+the u2 step, between backward and Adam); the value is all ranks' slices /
+max-over-ranks device time (weak scaling).
+
+--impl reference: the reference CPU implementation (oracle/_ref: the unmodified
+reference headers compiled here) on this host's cores, same unit, config and
+metric, rank 0 only.
 """
 from __future__ import annotations
 
@@ -45,6 +55,14 @@ CONFIGS = {
     "c5": dict(dims=(2048, 2048, 256), n=8_000_000, sigma_z=1.0,
                name="large microscopy 2048x2048x256 stack, 8M Gaussians, sigma_z=1"),
 }
+UNITS = {
+    "u2": "U2 training step: prepare + bin + rasterize + photometric loss (lambda 0.2, SSIM) + backward "
+          "+ scheduled Adam, one slice",
+    "u1": "U1 fwd+bwd slice: prepare + bin + rasterize + backward for a given dL/dI, dense gradients",
+}
+LAMBDA = 0.2
+LR0 = (6e-4, 0.02, 2e-3, 1e-3)      # optimize.hpp:23-26
+TOTAL_ITERS = 30000
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -55,6 +73,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--unit", default="u2", choices=sorted(UNITS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
@@ -150,13 +169,11 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------
-def cpu_reference_rate(cfg, rec, seconds_budget, max_reps=None):
-    """Reference CPU U1 (oracle/_ref) on this host's cores. Returns dict.
-
-    Everything on this path is the reference's own code (oracle/_ref: the
-    reference headers compiled as they are): its slice poses
-    (slice_pose_for_index, core.hpp:202-211) and its prepare / rasterize /
-    backward; `rec` is the same synthetic set the GPU arm uses."""
+def cpu_reference_rate(cfg, rec, unit, seconds_budget, max_reps=None):
+    """The reference's own CPU implementation (oracle/_ref: its headers compiled
+    unmodified) of the same unit on this host's cores. Its slice poses come from
+    the reference's slice_pose_for_index (core.hpp:202-211); `rec` is the same
+    synthetic set the GPU arm uses."""
     import ctypes as C
 
     from oracle.bindings import Bounds, CfgC, PoseC, PsfC, load
@@ -183,15 +200,26 @@ def cpu_reference_rate(cfg, rec, seconds_budget, max_reps=None):
             raise RuntimeError("reference slice_pose_for_index failed")
     psf = PsfC(1.0, 1.0, cfg["sigma_z"])
     rc = CfgC(0.02, 16, 3.0, 1.0)
-    dl = synthetic_dl_di(cfg).astype(np.float64)
-    secs = np.zeros(3)
+    if unit == "u2":
+        img_in = synthetic_target(cfg).astype(np.float64)
+        secs = np.zeros(5)
+        names = ("prepare", "rasterize", "loss", "backward", "adam")
+    else:
+        img_in = synthetic_dl_di(cfg).astype(np.float64)
+        secs = np.zeros(3)
+        names = ("prepare", "rasterize", "backward")
 
     def run(reps):
-        st = L.gref_time_u1(C.c_void_p(h), poses, len(ks), C.byref(psf), C.byref(rc),
-                            dl.ctypes.data_as(C.POINTER(C.c_double)), reps,
-                            secs.ctypes.data_as(C.POINTER(C.c_double)))
+        if unit == "u2":
+            st = L.gref_time_u2(C.c_void_p(h), poses, len(ks), C.byref(psf), C.byref(rc),
+                                img_in.ctypes.data_as(C.POINTER(C.c_double)), C.c_double(LAMBDA), reps,
+                                secs.ctypes.data_as(C.POINTER(C.c_double)))
+        else:
+            st = L.gref_time_u1(C.c_void_p(h), poses, len(ks), C.byref(psf), C.byref(rc),
+                                img_in.ctypes.data_as(C.POINTER(C.c_double)), reps,
+                                secs.ctypes.data_as(C.POINTER(C.c_double)))
         if st != 0:
-            raise RuntimeError("reference U1 failed")
+            raise RuntimeError("reference step failed")
         return secs.sum(), secs.copy()
 
     t1, _ = run(1)  # warm (page-in, allocator)
@@ -200,14 +228,19 @@ def cpu_reference_rate(cfg, rec, seconds_budget, max_reps=None):
         reps = min(reps, max_reps)
     t, parts = run(reps)
     L.gref_set_free(C.c_void_p(h))
+    calls = ("prepare_gaussians+rasterize_prepared+photometric_loss+backward_prepared+adam_step" if unit == "u2"
+             else "prepare_gaussians+rasterize_prepared+backward_prepared")
     return {
         "value": reps / t, "unit": "slices/s", "cores": int(workers), "host_cpus": cores,
         "kind": "reference", "reps": reps, "seconds": t,
-        "stage_seconds_per_slice": {"prepare": parts[0] / reps, "rasterize": parts[1] / reps,
-                                    "backward": parts[2] / reps},
-        "sample": f"{reps} U1 slices (prepare_gaussians+rasterize_prepared+backward_prepared) of "
-                  f"{cfg['name']}, oracle/_ref with {workers} threads",
+        "stage_seconds_per_slice": {n: float(parts[i] / reps) for i, n in enumerate(names)},
+        "sample": f"{reps} {unit.upper()} slices ({calls}) of {cfg['name']}, oracle/_ref with {workers} threads",
     }
+
+
+def synthetic_target(cfg):
+    X, Y, _ = cfg["dims"]
+    return np.random.default_rng(7).uniform(0.0, 0.1, (Y, X)).astype(np.float32)
 
 
 def synthetic_dl_di(cfg):
@@ -243,11 +276,17 @@ def make_records(cfg, via_reference=False):
 
 def config_json(args, cfg, world):
     X, Y, Z = cfg["dims"]
-    return {"workload": cfg["name"], "unit_of_work": "U1 fwd+bwd slice (prepare+bin+raster+backward, dense grads)",
+    return {"workload": cfg["name"], "unit_of_work": UNITS[args.unit],
             "volume": [X, Y, Z], "gaussians": cfg["n"], "sigma_z": cfg["sigma_z"],
-            "slices": f"{len(slice_indices(Z))} mid-stack indices, cycled",
-            "parallelism": f"slice-sharded dp{world}", "l2": "flushed (256 MiB read) before each timed step, outside the event window",
+            "slices": f"{len(slice_indices(Z))} mid-stack indices, cycled, one per step",
+            "parallelism": f"slice-sharded dp{world}",
+            "l2": "flushed (256 MiB read) before each timed step, outside the event window",
             "config_id": args.config}
+
+
+def data_note(unit):
+    return ("synthetic (init_random seed 1; targets U(0,0.1) seed 7)" if unit == "u2"
+            else "synthetic (init_random seed 1; dL/dI U(-1,1)/P seed 7)")
 
 
 # ---------------------------------------------------------------------------------
@@ -259,13 +298,12 @@ def run_reference(args):
     cfg = CONFIGS[args.config]
     rec = make_records(cfg, via_reference=True)
     budget = min(150.0, max(10.0, 1.0 * args.steps))
-    res = cpu_reference_rate(cfg, rec, budget, max_reps=args.steps)
+    res = cpu_reference_rate(cfg, rec, args.unit, budget, max_reps=args.steps)
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "slices/s",
         "n_gpus": args.gpus, "steps": res["reps"], "warmup": 1, "ms_per_step": 1000.0 / res["value"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (init_random seed 1, dL/dI U(-1,1)/P seed 7)",
-        "config": config_json(args, cfg, world),
+        "data": data_note(args.unit), "config": config_json(args, cfg, world),
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": "slices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "stage_seconds_per_slice": res["stage_seconds_per_slice"],
@@ -274,7 +312,15 @@ def run_reference(args):
     return 0
 
 
+def sort_passes(X, Y):
+    tiles = ((X + 15) // 16) * ((Y + 15) // 16)
+    bits = max(1, (tiles - 1).bit_length())
+    return (bits + 9) // 10
+
+
 def run_ours(args):
+    import ctypes as C
+
     import torch
 
     import paper_2603_20611_b200 as gp
@@ -291,6 +337,7 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    u2 = args.unit == "u2"
     cfg = CONFIGS[args.config]
     X, Y, Z = cfg["dims"]
     P = X * Y
@@ -304,15 +351,15 @@ def run_ours(args):
     sess.reserve_pairs(max(1 << 20, n))
     psf = gp.PsfSpec(sigma_z=cfg["sigma_z"])
     rcfg = gp.RasterConfig()
+    lr0 = gp.LearningRates(*LR0)
     ks = slice_indices(Z)
     poses = [gp.slice_pose_for_index(cfg["dims"], (1, 1, 1), (0, 0, 0), k) for k in ks]
-
     if world > 1:
         dp.init_grad_comm(sess, rank, world)
 
-    # first slice allocates the image-sized buffers, then upload the fixed dL/dI
-    sess.fwd_bwd_slice(poses[0], psf, rcfg)
+    tgt = synthetic_target(cfg)
     dl = synthetic_dl_di(cfg)
+    sess.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
     sess.upload(N.GPK_BUF_DL_DI, dl.ctypes.data, dl.nbytes)
     sess.synchronize()
     # per-slice counters (algorithmic bytes of the prepare kernels)
@@ -330,23 +377,25 @@ def run_ours(args):
     flush_src = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     flush_dst = torch.empty((), dtype=torch.float32, device="cuda")
 
-    class _Flush:
-        @staticmethod
-        def fill_(_v):
-            torch.sum(flush_src, dim=0, out=flush_dst)
+    def flush():
+        torch.sum(flush_src, dim=0, out=flush_dst)
 
-    flush = _Flush()
+    def capture(p):
+        return sess.capture_train(p, psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS) if u2 else \
+            sess.capture_fwd_bwd(p, psf, rcfg)
 
-    # one CUDA graph per slice pose: the whole U1 step is one submission
-    graphs = [sess.capture_fwd_bwd(p, psf, rcfg) for p in poses] if args.graphs else None
+    # one CUDA graph per slice pose: the whole step is one submission
+    graphs = [capture(p) for p in poses] if args.graphs else None
 
-    def step(i, use_graph=True):
+    def step(i):
         k = dp.slice_for(i, rank, world, len(poses))
-        if graphs is not None and use_graph:
+        if graphs is not None:
             sess.graph_launch(graphs[k])
+        elif u2:
+            sess.train_step(poses[k], psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS)  # all-reduce inside
         else:
             sess.fwd_bwd_slice(poses[k], psf, rcfg)
-        if world > 1:
+        if world > 1 and not u2:
             dp.allreduce_grads(sess)
 
     for i in range(args.warmup):
@@ -360,7 +409,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
-            flush.fill_(float(i))
+            flush()
             starts[i].record(stream)
             step(args.warmup + i)
             ends[i].record(stream)
@@ -369,112 +418,125 @@ def run_ours(args):
     if dist:
         dist.barrier()
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-
-    # per-kernel device time: the same steps through graphs captured with an
-    # event-record node around every stage (device-side timestamps, kernels
-    # back to back as in the timed run; L2 flushed before each step)
-    prof_steps = min(args.steps, 100)
-    sess.stage_timing(True)
-    prof_graphs = [sess.capture_fwd_bwd(p, psf, rcfg) for p in poses]
-    sess.stage_times(reset=True)
-    for i in range(prof_steps):
-        flush.fill_(float(i))
-        sess.graph_launch(prof_graphs[dp.slice_for(args.warmup + i, rank, world, len(poses))])
-    sess.stage_timing(False)
-    stages = sess.stage_times(reset=True)
-    t = torch.tensor([total_ms], device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = dp.max_over_ranks([total_ms], device="cuda")[0]
     ms_per_step = total_ms / args.steps
     value = world * 1000.0 / ms_per_step
 
+    # per-kernel device time: the same steps through graphs captured with an
+    # event-record node around every stage (device-side timestamps; the nodes
+    # themselves add ~2-4 us per stage, so these over-state each stage a little)
+    prof_steps = min(args.steps, 100)
+    sess.stage_timing(True)
+    prof_graphs = [capture(p) for p in poses]
+    sess.stage_times(reset=True)
+    for i in range(prof_steps):
+        flush()
+        sess.graph_launch(prof_graphs[dp.slice_for(args.warmup + i, rank, world, len(poses))])
+    sess.stage_timing(False)
+    stages = sess.stage_times(reset=True)
+
     # ---- e2e through the public C-ABI with host buffers ---------------------------
     e2e_steps = max(5, min(args.steps, 50))
-    pin_dl = torch.from_numpy(dl).pin_memory()
-    pin_img = torch.empty(P, dtype=torch.float32).pin_memory()
-    gptr, gbytes = sess.device_buffer(N.GPK_BUF_GRADS)
-    grad_bytes = n * 11 * 4
-    pin_grads = torch.empty(gbytes // 4, dtype=torch.float32).pin_memory()
     e_s = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)]
     e_e = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)]
-    cap_floats = gbytes // 44
-    for i in range(e2e_steps):
-        flush.fill_(float(i))
-        e_s[i].record(stream)
-        sess.upload(N.GPK_BUF_DL_DI, pin_dl.data_ptr(), P * 4)
-        step(i)
-        sess.download(N.GPK_BUF_IMAGE, pin_img.data_ptr(), P * 4)
-        # dense gradient planes (11 x N f32) -> host
-        sess.download(N.GPK_BUF_GRADS, pin_grads.data_ptr(), cap_floats * 44)
-        e_e[i].record(stream)
-        e_e[i].synchronize()
+    if u2:
+        pin_tgt = torch.from_numpy(tgt).pin_memory()
+        pin_loss = torch.empty(1, dtype=torch.float64).pin_memory()
+        for i in range(e2e_steps):
+            flush()
+            e_s[i].record(stream)
+            sess.upload(N.GPK_BUF_TARGET, pin_tgt.data_ptr(), P * 4)
+            step(i)
+            sess.download(N.GPK_BUF_LOSS, pin_loss.data_ptr(), 8)
+            e_e[i].record(stream)
+            e_e[i].synchronize()
+        assert np.isfinite(pin_loss.numpy()).all()
+        h2d, d2h = P * 4, 8
+        e2e_path = "C-ABI: gpk_upload(target, pinned) + train step (graph) + gpk_download(loss)"
+    else:
+        pin_dl = torch.from_numpy(dl).pin_memory()
+        pin_img = torch.empty(P, dtype=torch.float32).pin_memory()
+        _, gbytes = sess.device_buffer(N.GPK_BUF_GRADS)
+        pin_grads = torch.empty(gbytes // 4, dtype=torch.float32).pin_memory()
+        for i in range(e2e_steps):
+            flush()
+            e_s[i].record(stream)
+            sess.upload(N.GPK_BUF_DL_DI, pin_dl.data_ptr(), P * 4)
+            step(i)
+            sess.download(N.GPK_BUF_IMAGE, pin_img.data_ptr(), P * 4)
+            sess.download(N.GPK_BUF_GRADS, pin_grads.data_ptr(), gbytes)  # dense gradient planes
+            e_e[i].record(stream)
+            e_e[i].synchronize()
+        assert np.isfinite(pin_grads.numpy()[:1000]).all()
+        h2d, d2h = P * 4, P * 4 + gbytes
+        e2e_path = "C-ABI: gpk_upload(dL/dI) + fwd_bwd (graph) + gpk_download(image, dense gradients)"
     e2e_ms = sum(s.elapsed_time(e) for s, e in zip(e_s, e_e)) / e2e_steps
-    t = torch.tensor([e2e_ms], device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
-    assert np.isfinite(pin_grads.numpy()[:1000]).all()
+    e2e_ms = dp.max_over_ranks([e2e_ms], device="cuda")[0]
 
     # ---- roofline of the dominant kernel -------------------------------------------
-    # Algorithmic bytes per launch (each logical tensor read/written once at its
-    # stored width): N Gaussians, S survivors, T pairs, P px.
+    # Algorithmic bytes per launch (each logical tensor read or written once at its
+    # stored width): N Gaussians, C candidates, S survivors, T pairs, P px.
     S, T, Cc = S_mean, T_mean, C_mean
-    passes = max(1, sort_passes(X, Y))
-    kernel_bytes = {  # algorithmic bytes per launch
-        "prepare": ("k_filter", 44 * n + 44 * S + 48 * Cc + 4 * (n / 1024),
-                    "44N params + 44S previous-survivor gradient clear + 48C candidate records + 4/1024 N counts"),
-        "bin": ("k_decide", 48 * Cc + 48 * S + 48 * S + 8 * S + 8 * T,
-                "48C candidates + 48S records + 48S survivor params + 8S slots/bases + 8T pairs"),
-        "sort": ("k_sort_pass x passes", 16 * T * passes, "16T per radix pass"),
-        "raster": ("k_raster_fwd", 56 * T + 4 * P, "56T (key, slot, 48 B record per pair) + 4P image"),
-        "backward": ("k_raster_bwd", 56 * T + 4 * P + 24 * T, "56T + 4P dL/dI + 24T partials"),
-        "chain": ("k_chain", 48 * S + 48 * S + 24 * T + 44 * S + 8 * S,
-                  "48S records + 48S params + 24T partials + 44S grads + 8S slot/dirty list"),
+    passes = sort_passes(X, Y)
+    kernel_bytes = {
+        "prepare": ("k_filter", 44 * n + 44 * S + 48 * Cc + 4 * (n / 64),
+                    "44N params + 44S previous-survivor gradient clear + 48C candidate records + 4N/64 counts"),
+        "bin": ("k_decide", 48 * Cc + 48 * S + 48 * S + 4 * S + 4 * T + 4 * 1025 * (n / 4096),
+                "48C candidates + 48S records + 48S survivor params + 4S pair bases + 4T slots + bucket table"),
+        "sort": ("k_gather" if passes == 1 else "k_sort_pass x passes",
+                 8 * T if passes == 1 else 16 * T * passes,
+                 "8T (bucketed slots in, tile lists out)" if passes == 1 else "16T per radix pass"),
+        "raster": ("k_raster_fwd", 52 * T + 4 * P, "52T (slot + 48 B record per pair) + 4P image"),
+        "backward": ("k_raster_bwd", 52 * T + 4 * P + 24 * T, "52T + 4P dL/dI + 24T partials"),
+        "chain": ("k_chain", 48 * S + 48 * S + 24 * T + 44 * S + 4 * S,
+                  "48S records + 48S params + 24T partials + 44S grads + 4S dirty list"),
+        "loss": ("k_ssim_fwd + k_ssim_bwd", 36 * P, "8P images + 4P dL/dI + 24P SSIM moments (w+r)"),
+        "adam": ("k_adam", 308 * n, "308N: read params, grads, m, v; write params, m, v"),
     }
-    dom = max((k for k in stages if stages[k][1] > 0 and k in kernel_bytes), key=lambda k: stages[k][0])
+    measured = {k: v for k, v in stages.items() if v[1] > 0 and k in kernel_bytes}
+    dom = max(measured, key=lambda k: measured[k][0])
     peak, peak_src = load_peaks()
-    launch_ms = stages[dom][0] / stages[dom][1]
+    launch_ms = measured[dom][0] / measured[dom][1]
     kname, kbytes, kformula = kernel_bytes[dom]
     achieved = kbytes / (launch_ms * 1e-3) / 1e9
     roof = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(args.config, kname),
+            "frac": achieved / peak, "traffic": ncu_traffic(args.config, kname.split(" ")[0]),
             "peak_source": peak_src, "bytes_per_launch": kbytes, "launch_ms": launch_ms,
             "bytes_formula": kformula}
     per_kernel = {}
-    for k, (kn, kb, _) in kernel_bytes.items():
-        if stages.get(k, (0, 0))[1]:
-            ms = stages[k][0] / stages[k][1]
-            per_kernel[kn] = {"ms": ms, "gbs": kb / (ms * 1e-3) / 1e9, "frac": kb / (ms * 1e-3) / 1e9 / peak}
-    u1_bytes = 88 * n + 8 * P
-    step_gbs = u1_bytes / (ms_per_step * 1e-3) / 1e9
+    for k, (ms_tot, cnt) in measured.items():
+        kn, kb, _ = kernel_bytes[k]
+        ms = ms_tot / cnt
+        per_kernel[kn] = {"ms": ms, "gbs": kb / (ms * 1e-3) / 1e9, "frac": kb / (ms * 1e-3) / 1e9 / peak}
+    step_bytes = (396 * n + 8 * P) if u2 else (88 * n + 8 * P)
+    step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
 
     line = {
         "metric": METRIC, "value": value, "unit": "slices/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (fp64 preprocess/chain)",
-        "data": "synthetic (init_random seed 1, dL/dI U(-1,1)/P seed 7)",
-        "config": config_json(args, cfg, world),
+        "vs_baseline": None, "dtype": "f32 (fp64 cull/bounds decisions and chain)",
+        "data": data_note(args.unit), "config": config_json(args, cfg, world),
         "roofline": roof,
-        "u1_roofline": {"bytes_per_step": u1_bytes, "achieved_gbs": step_gbs, "frac": step_gbs / peak,
-                        "formula": "88N + 8P (SURVEY.md §8d)"},
-        "stage_ms_per_step": {k: v[0] / prof_steps for k, v in stages.items() if v[1]},
+        "step_roofline": {"bytes_per_step": step_bytes, "achieved_gbs": step_gbs, "frac": step_gbs / peak,
+                          "formula": ("396N + 8P (U2, SURVEY.md §8d)" if u2 else "88N + 8P (U1, SURVEY.md §8d)")},
+        "stage_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in stages.items() if v[1]},
         "kernels": per_kernel,
         "submission": "CUDA graph per slice pose" if graphs is not None else "kernel by kernel",
         "survivors_mean": S_mean, "pairs_mean": T_mean, "candidates_mean": C_mean,
         "fp64_decided_mean": X64_mean,
-        "e2e": {"value": world * 1000.0 / e2e_ms, "unit": "slices/s", "h2d_bytes_per_step": P * 4,
-                "d2h_bytes_per_step": P * 4 + cap_floats * 44,
-                "path": "C-ABI: gpk_upload(dL/dI) + gpk_fwd_bwd_slice + gpk_download(image, dense grads)"},
+        "e2e": {"value": world * 1000.0 / e2e_ms, "unit": "slices/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "path": e2e_path},
         "gpu_launches": None,
         "clocks": clk.result(),
     }
-    # K_prep + K_bin + radix passes + forward + backward + chain + chain_exact (+1 memset node)
-    launches_per_step = 2 + sort_passes(X, Y) + 4
-    line["gpu_launches"] = launches_per_step * args.steps
+    # filter + decide + (gather | radix passes) + forward + backward + chain + chain_exact
+    # (+ u2: 2 loss kernels + Adam; u1: + memset node, not a kernel)
+    launches = 2 + (1 if passes == 1 else passes) + 4 + (3 if u2 else 0)
+    line["gpu_launches"] = launches * args.steps
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(cfg, gs.records, args.cpu_seconds).items()
+            line["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(cfg, gs.records, args.unit,
+                                                                        args.cpu_seconds).items()
                                     if k in ("value", "unit", "cores", "kind", "sample",
                                              "stage_seconds_per_slice")}
         except Exception as e:  # reported, never silently replaced
@@ -485,12 +547,6 @@ def run_ours(args):
     if dist:
         dist.destroy_process_group()
     return 0
-
-
-def sort_passes(X, Y):
-    tiles = ((X + 15) // 16) * ((Y + 15) // 16)
-    bits = max(0, (tiles - 1).bit_length())
-    return (bits + 9) // 10  # <= 10-bit digits (csrc/common.cuh kMaxDigitBits)
 
 
 def main():

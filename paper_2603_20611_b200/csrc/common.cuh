@@ -115,7 +115,8 @@ struct alignas(64) Control {
     unsigned int chain_exact;                  // survivors deferred to the fp64 chain
     unsigned int exact_decided;                // survivors decided on the reference-order fp64 path
     unsigned int dirty_ctr;                    // K_chain: next slot of the dirty-gradient list
-    unsigned int pad[3];
+    unsigned int decide_done;                  // K_decide groups finished (last one scans the tiles)
+    unsigned int pad[2];
 };
 
 constexpr int kExactChunk = 256;               // candidates per K_exact chunk (= threads)
@@ -328,6 +329,8 @@ struct PrepLaunch {
     unsigned* cand_count;     // candidates per chunk (plain stores)
     CandParams* surv_params;  // survivor params by survivor slot
     uint2* grp_pairs;         // per K_decide group: (first pair position, pair count)
+    unsigned* bucket_tab;     // single-pass slices: per group, bucket starts + end (else nullptr)
+    unsigned* tile_begin;     // single-pass slices: tile list starts, written by the last group
     unsigned* grp_surv;       // per K_decide group: survivors (slots g*4096 + [0, S_g))
     unsigned nfilter;         // 64-Gaussian chunks
     SurvivorRecord* records;  // indexed by candidate slot
@@ -354,6 +357,22 @@ constexpr int kFilterBlock = 32 * kFilterItems;            // Gaussians per K_fi
 constexpr int kDecideChunks = 64;                          // K_filter chunks per K_decide group
 constexpr int kDecideGroupSize = kDecideChunks * kFilterBlock;  // Gaussians per group (4096)
 constexpr int kParamAlign = 512;                           // plane stride (capacity) granularity
+
+// Gather (single radix digit covers every tile): K_decide bucketed each
+// group's pairs by tile and wrote the bucket starts; one CTA per tile
+// concatenates its buckets in group order (= slot order).
+struct GatherLaunch {
+    const unsigned* bucket_tab;    // per group: bucket start of every tile, then the group end
+    unsigned ngroups;
+    unsigned ntiles;
+    unsigned row_stride;           // radix buckets + 1
+    const unsigned* tile_begin;    // tile list starts (+ end), computed by the last K_decide group
+    const uint32_t* vals_in;       // bucketed slots
+    uint32_t* vals_out;            // per-tile lists, ascending slot
+    const Control* ctrl;
+    uint64_t pair_cap;
+};
+void launch_gather(const GatherLaunch& a, cudaStream_t st);
 
 struct SortLaunch {
     const uint32_t* keys_in;

@@ -54,23 +54,29 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* s_red) 
     }
 }
 
-// Last CTA: loss = l1/N + lambda*dssim*(1 - ssim/N), summed in CTA order.
+// Last CTA: loss = l1/N + lambda*dssim*(1 - ssim/N). The per-CTA sums are
+// reduced by the whole last CTA in a fixed order (thread t sums CTAs t, t+256,
+// ... then a fixed warp/block tree): deterministic run to run.
 __device__ __forceinline__ void finish_loss(const LossLaunch& a, bool with_ssim) {
     __shared__ unsigned s_last;
+    __shared__ double s_red2[16];
+    __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned nblk = gridDim.x * gridDim.y;
         s_last = (atomicAdd(a.done_ctr, 1u) == nblk - 1) ? 1u : 0u;
     }
     __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
+    if (!s_last) return;
     __threadfence();
     const unsigned nblk = gridDim.x * gridDim.y;
     double ss = 0.0, l1 = 0.0;
-    for (unsigned k = 0; k < nblk; ++k) {
-        ss += a.partial[2 * k];
-        l1 += a.partial[2 * k + 1];
+    for (unsigned k = threadIdx.x; k < nblk; k += blockDim.x) {
+        ss += __ldcg(&a.partial[2 * k]);
+        l1 += __ldcg(&a.partial[2 * k + 1]);
     }
+    block_sum2(ss, l1, s_red2);
+    if (threadIdx.x != 0) return;
     const double inv_n = 1.0 / ((double)a.W * (double)a.H);
     double L = l1 * inv_n;
     if (with_ssim) L += a.lambda * a.dssim_scale * (1.0 - ss * inv_n);
@@ -153,11 +159,13 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(const LossLaunch a) {
         const double vx = m[2] - mx * mx, vy = m[4] - my * my, vxy = m[3] - mx * my;
         const double a1 = 2.0 * mx * my + kC1, a2 = 2.0 * vxy + kC2;
         const double b1 = mx * mx + my * my + kC1, b2 = vx + vy + kC2;
-        const double s = (a1 * a2) / (b1 * b2);
+        // one fp64 reciprocal instead of four divisions (metrics.hpp:205-215)
         const double inv_b1b2 = 1.0 / (b1 * b2);
-        const double ds_dm2 = -s / b2;
+        const double s = a1 * a2 * inv_b1b2;
+        const double inv_b1 = b2 * inv_b1b2, inv_b2 = b1 * inv_b1b2;
+        const double ds_dm2 = -s * inv_b2;
         const double ds_dm12 = 2.0 * a1 * inv_b1b2;
-        const double ds_dm1 = 2.0 * my * a2 * inv_b1b2 - 2.0 * mx * s / b1 + 2.0 * mx * s / b2 -
+        const double ds_dm1 = 2.0 * my * a2 * inv_b1b2 - 2.0 * mx * s * inv_b1 + 2.0 * mx * s * inv_b2 -
                               2.0 * my * a1 * inv_b1b2;
         const size_t o = (size_t)j * W + i;
         a.g[o] = (float)(ds_dm1 * inv_n);

@@ -444,15 +444,108 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     // ---- 3. pair bases and pair emission ------------------------------------------
     const unsigned P0 = (unsigned)s_excl;
     for (unsigned j = tid; j < S; j += kDecideThreads) a.records[base + j].pair_base = P0 + (j ? s_incl[j - 1] : 0u);
-    for (unsigned k = tid; k < Pb; k += kDecideThreads) {
+    // tile of the group's k-th pair (pairs in (survivor, tile-in-rect) order)
+    auto pair_tile = [&](unsigned k, unsigned& surv) {
         unsigned lo = 0, hi = S - 1;
         while (lo < hi) {
             const unsigned mid = (lo + hi) >> 1;
             if (s_incl[mid] > k) hi = mid; else lo = mid + 1;
         }
+        surv = lo;
         const unsigned local = k - (lo ? s_incl[lo - 1] : 0u);
         const unsigned ntx = s_rect[lo][2];
-        const unsigned tile = (s_rect[lo][1] + local / ntx) * (unsigned)tiles_x + s_rect[lo][0] + local % ntx;
+        return (s_rect[lo][1] + local / ntx) * (unsigned)tiles_x + s_rect[lo][0] + local % ntx;
+    };
+    if (a.bucket_tab) {
+        // single-pass slice (every tile is one digit): bucket the group's pairs
+        // by tile — counts, bucket starts (published for k_gather), then slots
+        // into their buckets. Order inside a bucket is restored by k_gather.
+        for (unsigned k = tid; k < Pb; k += kDecideThreads) {
+            unsigned j;
+            atomicAdd(&s_hist[0][pair_tile(k, j)], 1u);
+        }
+        __syncthreads();
+        unsigned* s_start = &s_hist[1][0];
+        {
+            constexpr int kPer = kMaxBuckets / kDecideThreads;
+            const unsigned d0 = tid * kPer;
+            unsigned v[kPer], run = 0;
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                v[q] = s_hist[0][d0 + q];
+                run += v[q];
+                if (v[q]) atomicAdd(&a.hist[d0 + q], v[q]);
+            }
+            unsigned incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            if (lane == 31) s_cnt[0][warp] = incl;
+            __syncthreads();
+            unsigned ex = incl - run;
+            for (int w = 0; w < warp; ++w) ex += s_cnt[0][w];
+            // the group's row of bucket starts (+ end), coalesced
+            unsigned* trow = a.bucket_tab + (uint64_t)g * (nb + 1);
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                s_start[d0 + q] = ex;
+                if (d0 + q < nb) trow[d0 + q] = P0 + ex;
+                s_hist[0][d0 + q] = 0;  // becomes the fill counter
+                ex += v[q];
+            }
+            if (tid == 0) trow[nb] = P0 + Pb;
+        }
+        __syncthreads();
+        for (unsigned k = tid; k < Pb; k += kDecideThreads) {
+            unsigned j;
+            const unsigned tile = pair_tile(k, j);
+            const unsigned long long pos = (unsigned long long)P0 + s_start[tile] + atomicAdd(&s_hist[0][tile], 1u);
+            if (pos < a.pair_cap) a.vals[pos] = base + j;
+        }
+        // the last group to finish turns the per-tile counts into list starts
+        // (one scan, instead of every gather CTA re-reading the same counts)
+        __threadfence();
+        __syncthreads();
+        __shared__ bool s_last;
+        if (tid == 0) s_last = atomicAdd(&a.ctrl->decide_done, 1u) == ngroups - 1;
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        {
+            constexpr int kPer = kMaxBuckets / kDecideThreads;
+            const unsigned d0 = tid * kPer;
+            const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
+            unsigned v[kPer], run = 0;
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                v[q] = d0 + q < nb ? __ldcg(&a.hist[d0 + q]) : 0u;
+                run += v[q];
+            }
+            unsigned incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            __syncthreads();
+            if (lane == 31) s_cnt[1][warp] = incl;
+            __syncthreads();
+            unsigned ex = incl - run;
+            for (int w = 0; w < warp; ++w) ex += s_cnt[1][w];
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                if (d0 + q < nb) a.tile_begin[d0 + q] = min(ex, P);
+                ex += v[q];
+            }
+            if (tid == kDecideThreads - 1) a.tile_begin[nb] = min(ex, P);
+        }
+        return;
+    }
+    for (unsigned k = tid; k < Pb; k += kDecideThreads) {
+        unsigned lo;
+        const unsigned tile = pair_tile(k, lo);
         const unsigned long long pos = (unsigned long long)P0 + k;
         if (pos < a.pair_cap) {
             a.keys[pos] = tile;

@@ -109,6 +109,7 @@ struct gpk_session {
     DevBuf surv_params;  // CandParams of survivors by survivor slot (K_decide)
     DevBuf dirty_idx;  // set indices of the last backward's survivors
     DevBuf grp_table;  // per K_decide group: uint2 (first pair, pairs), then u32 survivors
+    DevBuf bucket_tab; // single-pass slices: per group, tiles + 1 bucket starts
     uint2* grp_pairs() { return grp_table.as<uint2>(); }
     unsigned* grp_surv() { return reinterpret_cast<unsigned*>(grp_table.as<char>() + (cap / kDecideGroupSize + 2) * 8); }
     int num_sms = 148;
@@ -423,6 +424,8 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     pl.cand_count = s->cand_count.as<unsigned>();
     pl.grp_pairs = s->grp_pairs();
     pl.grp_surv = s->grp_surv();
+    pl.bucket_tab = ps.passes == 1 ? s->bucket_tab.as<unsigned>() : nullptr;
+    pl.tile_begin = s->grp_begin();
     pl.grads_dirty = s->grads_dirty();
     pl.dirty_idx = s->dirty_idx.as<uint32_t>();
     pl.nfilter = (unsigned)nbf;
@@ -452,7 +455,23 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
         CK(cudaGetLastError());
     }
     StageScope scope_sort(s, GPK_STAGE_SORT);
-    TRY(launch_sorts(s, ps.passes, ps.digit_bits, s->grp_pairs(), (unsigned)decide_group_count(s->n)));
+    if (ps.passes == 1) {
+        // every tile is one digit: gather the K_decide buckets instead of a radix pass
+        GatherLaunch gl;
+        gl.bucket_tab = s->bucket_tab.as<unsigned>();
+        gl.ngroups = (unsigned)decide_group_count(s->n);
+        gl.ntiles = (unsigned)ps.tiles;
+        gl.row_stride = (1u << ps.digit_bits) + 1;
+        gl.tile_begin = s->grp_begin();
+        gl.vals_in = s->vals[0].as<uint32_t>();
+        gl.vals_out = s->vals[1].as<uint32_t>();
+        gl.ctrl = s->ctrl();
+        gl.pair_cap = s->pair_cap;
+        launch_gather(gl, s->stream);
+        CK(cudaGetLastError());
+    } else {
+        TRY(launch_sorts(s, ps.passes, ps.digit_bits, s->grp_pairs(), (unsigned)decide_group_count(s->n)));
+    }
     ps.final_buf = ps.passes & 1;
     return GPK_OK;
 }
@@ -637,6 +656,7 @@ int alloc_for_n(gpk_session* s, uint64_t n) {
         CK(s->cand_list.ensure(cap * 4));
         CK(s->surv_params.ensure(cap * sizeof(CandParams)));
         CK(s->grp_table.ensure((cap / kDecideGroupSize + 2) * 12));
+        CK(s->bucket_tab.ensure((cap / kDecideGroupSize + 2) * (kMaxBuckets + 1) * 4));
         CK(s->cand.ensure(cap * sizeof(CandParams)));
         CK(s->cand_count.ensure(nbf * 4));
         CK(s->dirty_idx.ensure(cap * 4));
@@ -923,7 +943,7 @@ int gpk_session_destroy(gpk_session* s) {
                       &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials,
                       &s->sort_status, &s->head, &s->persist, &s->image,
                       &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm,
-                      &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table,
+                      &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table, &s->bucket_tab,
                       &s->dirty_idx, &s->vox_records,
                       &s->volume, &s->dl_dv_vol, &s->vox_partials};
     for (DevBuf* b : bufs) b->release();
@@ -1192,8 +1212,15 @@ int gpk_get_tile_lists(gpk_session* s, uint32_t* offsets, uint32_t* entries) {
     const int tiles = s->prep.tiles;
     std::vector<uint32_t> keys(T), vals(T);
     if (T) {
-        CK(cudaMemcpy(keys.data(), s->keys[s->prep.final_buf].p, T * 4, cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(vals.data(), s->vals[s->prep.final_buf].p, T * 4, cudaMemcpyDeviceToHost));
+        if (s->prep.passes == 1) {  // gathered lists: tile starts from the published table
+            std::vector<uint32_t> begin(tiles + 1);
+            CK(cudaMemcpy(begin.data(), s->grp_begin(), (tiles + 1) * 4, cudaMemcpyDeviceToHost));
+            for (int t = 0; t < tiles; ++t)
+                for (uint32_t k = begin[t]; k < begin[t + 1] && k < T; ++k) keys[k] = (uint32_t)t;
+        } else {
+            CK(cudaMemcpy(keys.data(), s->keys[s->prep.final_buf].p, T * 4, cudaMemcpyDeviceToHost));
+        }
     }
     std::vector<SurvivorRecord> recs;
     if (T) {
@@ -1367,6 +1394,10 @@ int gpk_fwd_bwd_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf*
     return ok();
 }
 
+// Data-parallel training: with a communicator, the dense gradient planes are
+// summed over the ranks between backward and Adam (defined with the NCCL code).
+static int dp_allreduce_if_comm(gpk_session* s);
+
 int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                    const gpk_raster_config* cfg, double lambda, double dssim_scale,
                    const gpk_learning_rates* lr0, int32_t total_iterations) {
@@ -1377,6 +1408,7 @@ int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* ps
     TRY(run_rasterize(s));
     TRY(run_loss(s, lambda, dssim_scale));
     TRY(run_backward(s, false));
+    TRY(dp_allreduce_if_comm(s));
     const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
     TRY(run_adam(s, lr, true, total_iterations, nullptr));
     return ok();
@@ -1478,6 +1510,7 @@ int gpk_graph_capture_train(gpk_session* s, const gpk_slice_pose* pose, const gp
         TRY(run_loss(ss, a->lambda, a->dssim));
         TRY(run_backward(ss, false));
         const double lr[4] = {a->lr0->position, a->lr0->opacity, a->lr0->scale, a->lr0->rotation};
+        TRY(dp_allreduce_if_comm(ss));
         TRY(run_adam(ss, lr, true, a->total, nullptr));
         return GPK_OK;
     }, &args);
@@ -1595,6 +1628,17 @@ int gpk_comm_destroy(gpk_session* s) {
     if (api && comm && api->comm_destroy) api->comm_destroy(comm);
     comm = nullptr;
     return ok();
+}
+
+static int dp_allreduce_if_comm(gpk_session* s) {
+    void* comm = session_comm(s);
+    if (!comm) return GPK_OK;
+    NcclApi* api = nccl();
+    if (!api) return fail(GPK_ERR_NCCL, "NCCL not available");
+    const int r = api->all_reduce(s->grads.p, s->grads.p, s->cap * 11, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm,
+                                  s->stream);
+    if (r != 0) return fail(GPK_ERR_NCCL, "ncclAllReduce failed");
+    return mark_grads_dense(s);
 }
 
 int gpk_allreduce_grads(gpk_session* s) {

@@ -126,7 +126,45 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
             }
         }
 
-        // ---- rounds of kSortTile pairs, in input order ---------------------------
+        if (count <= (unsigned)kSortTile) {
+            // ---- short tile: staged in shared memory by all threads, then one
+            // warp ranks the pairs in input order, 32 at a time, against running
+            // per-digit counters (no per-warp tables)
+            uint32_t* s_key = &s_whist[0][0];
+            uint32_t* s_val = &s_whist[4][0];
+            for (unsigned i = tid; i < count; i += kSortThreads) {
+                s_key[i] = a.keys_in[first + i];
+                s_val[i] = a.vals_in[first + i];
+            }
+            __syncthreads();  // s_base and the staged pairs complete
+            if (warp == 0) {
+                for (unsigned r0 = 0; r0 < count; r0 += 32) {
+                    const unsigned idx = r0 + lane;
+                    const bool valid = idx < count;
+                    const uint32_t key = valid ? s_key[idx] : 0xffffffffu;
+                    const uint32_t val = valid ? s_val[idx] : 0u;
+                    const unsigned d = valid ? ((key >> a.shift) & mask) : 0xffffffffu;
+                    const unsigned peers = __match_any_sync(0xffffffffu, d);
+                    unsigned base = 0;
+                    if (valid) base = s_base[d];
+                    __syncwarp();
+                    if (valid && (__ffs(peers) - 1) == lane) s_base[d] = base + __popc(peers);
+                    __syncwarp();
+                    if (valid) {
+                        const unsigned pos = base + __popc(peers & lanemask_lt());
+                        a.keys_out[pos] = key;
+                        a.vals_out[pos] = val;
+                        if (a.tile_hist_next) {
+                            const unsigned nd = (key >> (a.shift + a.bits)) & (a.next_buckets - 1);
+                            const unsigned st = pos / kSortTile;
+                            atomicAdd(&a.tile_hist_next[(size_t)st * a.next_buckets + nd], 1u);
+                            atomicAdd(&a.tile_hist_next[(a.sort_tiles_cap + st / kSuperTiles) * a.next_buckets + nd], 1u);
+                        }
+                    }
+                }
+            }
+        } else {
+        // ---- long tile: rounds of kSortTile pairs, in input order ----------------
         for (unsigned r0 = 0; r0 < count; r0 += kSortTile) {
             for (int w = 0; w < 8; ++w)
                 for (unsigned d = tid; d < nb; d += kSortThreads) s_whist[w][d] = 0;
@@ -183,11 +221,69 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
             }
             __syncthreads();
         }
+        }
         __syncthreads();  // s_base / s_wsum are rewritten for the next tile
     }
 }
 
+// ---- k_gather --------------------------------------------------------------------
+// Single-pass slices (every tile is one digit): instead of a radix pass, one
+// CTA per tile concatenates the tile's buckets — one per K_decide group, in
+// group order, which is ascending slot order — into the tile's final list.
+// A bucket holds the group's survivors overlapping the tile (almost always 0-3
+// entries) in arbitrary order; each thread orders its bucket by rank (slots are
+// unique), so the list comes out in ascending slot order, like the reference's.
+constexpr int kGatherThreads = 256;
+
+__global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    __shared__ unsigned s_wsum[kGatherThreads / 32];
+    __shared__ unsigned s_chunk_total;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned d = blockIdx.x;
+    const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
+    unsigned out = __ldcg(&a.tile_begin[d]);
+    for (unsigned g0 = 0; g0 < a.ngroups; g0 += kGatherThreads) {
+        const unsigned g = g0 + tid;
+        unsigned b = 0, e = 0;
+        if (g < a.ngroups) {  // group g's bucket for tile d: [row[d], row[d + 1])
+            const unsigned* row = a.bucket_tab + (uint64_t)g * a.row_stride;
+            b = min(__ldcg(&row[d]), P);
+            e = min(__ldcg(&row[d + 1]), P);
+        }
+        const unsigned cnt = e > b ? e - b : 0u;
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        __syncthreads();  // s_wsum of the previous chunk consumed
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        unsigned pos = out + incl - cnt;
+        for (int w = 0; w < warp; ++w) pos += s_wsum[w];
+        if (tid == kGatherThreads - 1) s_chunk_total = pos + cnt - out;
+        if (cnt == 1) {
+            a.vals_out[pos] = a.vals_in[b];
+        } else if (cnt > 1) {
+            for (unsigned i = 0; i < cnt; ++i) {  // rank within the bucket (slots are unique)
+                const uint32_t v = a.vals_in[b + i];
+                unsigned r = 0;
+                for (unsigned j = 0; j < cnt; ++j) r += a.vals_in[b + j] < v;
+                a.vals_out[pos + r] = v;
+            }
+        }
+        __syncthreads();
+        out += s_chunk_total;
+    }
+}
+
 }  // namespace
+
+void launch_gather(const GatherLaunch& a, cudaStream_t st) {
+    if (a.ntiles) launch_pdl(k_gather, dim3(a.ntiles), dim3(kGatherThreads), 0, st, a);
+}
 
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st) {
     launch_pdl(k_sort_pass, dim3(grid), dim3(kSortThreads), 0, st, a);

@@ -411,6 +411,11 @@ struct RasterLaunch {
     const float* dl_di;            // backward input
     float* partials;               // backward output: 6 f32 per pair (pre-sort position)
     SliceArgs slice;
+    // fused SSIM backward (training step): dL/dI = sign(I-T)/N - k (W g1 + 2 I W g2 + T W g3)
+    const float* ssim_g;           // 3 planes from k_ssim_fwd, or nullptr (dL/dI given)
+    const float* target;
+    float ssim_k, inv_n;           // lambda * dssim_scale, 1/(W*H)
+    float w[11];                   // window taps
 };
 
 struct ChainLaunch {
@@ -462,7 +467,10 @@ struct LossLaunch {
     int W, H;
     double lambda, dssim_scale;
     float w[11];         // normalized Gaussian taps
+    int finish_in_fwd;   // training step: k_ssim_fwd finalizes the loss; the raster backward
+                         // turns the SSIM partials into dL/dI itself (k_ssim_bwd is skipped)
 };
+void launch_loss_fwd_only(const LossLaunch& a, cudaStream_t st);
 
 // ---- voxelizer (voxelize.hpp) -------------------------------------------------
 // One primitive's voxelizer state (VoxelPrim, voxelize.hpp:42-48), 64 B.

@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(const LossLaunch a) {
         a.partial[2 * b] = ssum;
         a.partial[2 * b + 1] = l1;
     }
+    if (a.finish_in_fwd) finish_loss(a, true);
 }
 
 __global__ void __launch_bounds__(256) k_ssim_bwd(const LossLaunch a) {
@@ -236,6 +237,11 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(const LossLaunch a) {
 }
 
 }  // namespace
+
+void launch_loss_fwd_only(const LossLaunch& a, cudaStream_t st) {
+    const dim3 grid((a.W + kT - 1) / kT, (a.H + kT - 1) / kT);
+    launch_pdl(k_ssim_fwd, grid, dim3(256), 0, st, a);
+}
 
 void launch_loss(const LossLaunch& a, cudaStream_t st) {
     if (a.lambda == 0.0) {

@@ -159,6 +159,71 @@ __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
     if (i < a.slice.W && j < a.slice.H) a.image[(size_t)j * a.slice.W + i] = acc;
 }
 
+// Training step: dL/dI of the tile from k_ssim_fwd's three partial planes
+// (metrics.hpp:218-223: the window is self-adjoint, dSSIM/dI = W g1 + 2 I W g2
+// + T W g3) plus the L1 sign term (loss.hpp:29-33) — the work of k_ssim_bwd,
+// done here so it costs no kernel of its own. Reflected borders (metrics.hpp:
+// 77-83); the tile's dL/dI is also stored (GPK_BUF_DL_DI stays meaningful).
+constexpr int kSsimR = 5, kSsimH = kTile + 2 * kSsimR;
+
+__device__ __forceinline__ int reflect_idx(int p, int n) {
+    while (p < 0 || p >= n) {
+        if (p < 0) p = -p - 1;
+        if (p >= n) p = 2 * n - 1 - p;
+    }
+    return p;
+}
+
+__device__ __forceinline__ void ssim_dl_tile(const RasterLaunch& a, int x0, int y0, float* s_dl) {
+    __shared__ float s_g[3][kSsimH][kSsimH + 1];
+    __shared__ float s_h[3][kSsimH][kTile + 1];
+    const int W = a.slice.W, H = a.slice.H;
+    const size_t P = (size_t)W * H;
+    for (int idx = threadIdx.x; idx < kSsimH * kSsimH; idx += blockDim.x) {
+        const int r = idx / kSsimH, c = idx % kSsimH;
+        const size_t o = (size_t)reflect_idx(y0 + r - kSsimR, H) * W + reflect_idx(x0 + c - kSsimR, W);
+        s_g[0][r][c] = a.ssim_g[o];
+        s_g[1][r][c] = a.ssim_g[P + o];
+        s_g[2][r][c] = a.ssim_g[2 * P + o];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kSsimH * kTile; idx += blockDim.x) {
+        const int r = idx / kTile, c = idx % kTile;
+        float h0 = 0.f, h1 = 0.f, h2 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 2 * kSsimR + 1; ++t) {
+            const float w = a.w[t];
+            h0 += w * s_g[0][r][c + t];
+            h1 += w * s_g[1][r][c + t];
+            h2 += w * s_g[2][r][c + t];
+        }
+        s_h[0][r][c] = h0;
+        s_h[1][r][c] = h1;
+        s_h[2][r][c] = h2;
+    }
+    __syncthreads();
+    const int r = threadIdx.x >> 4, c = threadIdx.x & 15;
+    const int i = x0 + c, j = y0 + r;
+    float dl = 0.f;
+    if (i < W && j < H) {
+        float A0 = 0.f, A1 = 0.f, A2 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 2 * kSsimR + 1; ++t) {
+            const float w = a.w[t];
+            A0 += w * s_h[0][r + t][c];
+            A1 += w * s_h[1][r + t][c];
+            A2 += w * s_h[2][r + t][c];
+        }
+        const size_t o = (size_t)j * W + i;
+        const float x = a.image[o], y = a.target[o];
+        const float gs = A0 + 2.f * x * A1 + y * A2;
+        const float d = x - y;
+        dl = (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) * a.inv_n + a.ssim_k * (-gs);
+        const_cast<float*>(a.dl_di)[o] = dl;
+    }
+    s_dl[threadIdx.x] = dl;
+}
+
 constexpr int kBwdBatch = 256;    // pairs staged per round (one per thread)
 constexpr int kWorkBuckets = 16;
 
@@ -175,7 +240,9 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
     const int tx = tile % a.slice.tiles_x, ty = tile / a.slice.tiles_x;
     const int x0 = tx * kTile, y0 = ty * kTile;
     tile_range(a, tile, s_range);
-    {
+    if (a.ssim_g) {
+        ssim_dl_tile(a, x0, y0, s_dl);
+    } else {
         const int i = x0 + (tid & 15), j = y0 + (tid >> 4);
         s_dl[tid] = (i < a.slice.W && j < a.slice.H) ? __ldg(&a.dl_di[(size_t)j * a.slice.W + i]) : 0.f;
     }

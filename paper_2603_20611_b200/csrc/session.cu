@@ -79,6 +79,9 @@ struct PrepState {
     int final_buf = 0;         // which key/val buffer holds the sorted pairs
     bool rasterized = false;
     bool grads_zeroed = false;  // K_prep zero-filled non-survivor gradients
+    bool ssim_pending = false;  // training step: the raster backward forms dL/dI from the SSIM partials
+    float ssim_k = 0.f, inv_n = 0.f;
+    float w[11] = {};
     gpk_slice_pose pose{};
     gpk_psf psf{};
     gpk_raster_config cfg{};
@@ -406,6 +409,7 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     ps.valid = true;
     ps.rasterized = false;
     ps.grads_zeroed = zero_grads;
+    ps.ssim_pending = false;
     const uint64_t nbf = filter_blocks(s->n);
     const size_t head_bytes = head_size(s->n);
     StageScope scope_prep(s, GPK_STAGE_PREPARE);
@@ -523,6 +527,11 @@ RasterLaunch raster_args(gpk_session* s) {
     r.dl_di = s->dl_di.as<float>();
     r.partials = s->partials.as<float>();
     r.slice = s->prep.slice;
+    r.ssim_g = s->prep.ssim_pending ? s->loss_g.as<float>() : nullptr;
+    r.target = s->target.as<float>();
+    r.ssim_k = s->prep.ssim_k;
+    r.inv_n = s->prep.inv_n;
+    for (int t = 0; t < 11; ++t) r.w[t] = s->prep.w[t];
     return r;
 }
 
@@ -560,6 +569,7 @@ int run_backward(gpk_session* s, bool stats) {
         StageScope scope(s, GPK_STAGE_BACKWARD);
         launch_raster_bwd(raster_args(s), s->stream);
         CK(cudaGetLastError());
+        s->prep.ssim_pending = false;
     }
     StageScope scope(s, GPK_STAGE_CHAIN);
     ChainLaunch c;
@@ -714,7 +724,7 @@ int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
     return GPK_OK;
 }
 
-int run_loss(gpk_session* s, double lambda, double dssim_scale) {
+int run_loss(gpk_session* s, double lambda, double dssim_scale, bool fuse_into_backward = false) {
     if (!s->prep.rasterized) return fail(GPK_ERR_STATE, "photometric_loss: no rendered image");
     const int W = s->img_w, H = s->img_h;
     const size_t px = (size_t)W * H;
@@ -745,7 +755,17 @@ int run_loss(gpk_session* s, double lambda, double dssim_scale) {
     }
     for (int t = 0; t < 11; ++t) l.w[t] = (float)(w[t] / sum);
     StageScope scope(s, GPK_STAGE_LOSS);
-    launch_loss(l, s->stream);
+    const bool fuse = fuse_into_backward && lambda != 0.0;
+    l.finish_in_fwd = fuse ? 1 : 0;
+    if (fuse) {
+        launch_loss_fwd_only(l, s->stream);
+        s->prep.ssim_pending = true;
+        s->prep.ssim_k = (float)(lambda * dssim_scale);
+        s->prep.inv_n = (float)(1.0 / (double)px);
+        for (int t = 0; t < 11; ++t) s->prep.w[t] = l.w[t];
+    } else {
+        launch_loss(l, s->stream);
+    }
     CK(cudaGetLastError());
     return GPK_OK;
 }
@@ -1406,7 +1426,7 @@ int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* ps
     TRY(set_device(s));
     TRY(run_prepare(s, pose, psf, cfg, true));
     TRY(run_rasterize(s));
-    TRY(run_loss(s, lambda, dssim_scale));
+    TRY(run_loss(s, lambda, dssim_scale, true));
     TRY(run_backward(s, false));
     TRY(dp_allreduce_if_comm(s));
     const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
@@ -1507,7 +1527,7 @@ int gpk_graph_capture_train(gpk_session* s, const gpk_slice_pose* pose, const gp
         const TrainArgs* a = static_cast<const TrainArgs*>(p);
         TRY(run_prepare(ss, a->pose, a->psf, a->cfg, true));
         TRY(run_rasterize(ss));
-        TRY(run_loss(ss, a->lambda, a->dssim));
+        TRY(run_loss(ss, a->lambda, a->dssim, true));
         TRY(run_backward(ss, false));
         const double lr[4] = {a->lr0->position, a->lr0->opacity, a->lr0->scale, a->lr0->rotation};
         TRY(dp_allreduce_if_comm(ss));

@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--unit", default="u2", choices=sorted(UNITS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="u2: fuse each step's Adam with the cull of the rank's next slice "
+                         "(gpk_graph_capture_train_next); measured slower than the separate kernels on B200")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
                     help="submit the step kernel by kernel instead of as a CUDA graph")
@@ -276,7 +279,8 @@ def make_records(cfg, via_reference=False):
 
 def config_json(args, cfg, world):
     X, Y, Z = cfg["dims"]
-    return {"workload": cfg["name"], "unit_of_work": UNITS[args.unit],
+    return {"workload": cfg["name"], "unit_of_work": UNITS[args.unit] + (
+        " (Adam fused with the next slice's cull)" if args.unit == "u2" and getattr(args, "pipeline", True) else ""),
             "volume": [X, Y, Z], "gaussians": cfg["n"], "sigma_z": cfg["sigma_z"],
             "slices": f"{len(slice_indices(Z))} mid-stack indices, cycled, one per step",
             "parallelism": f"slice-sharded dp{world}",
@@ -380,19 +384,24 @@ def run_ours(args):
     def flush():
         torch.sum(flush_src, dim=0, out=flush_dst)
 
-    def capture(p):
-        return sess.capture_train(p, psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS) if u2 else \
-            sess.capture_fwd_bwd(p, psf, rcfg)
+    def capture(k):
+        # u2: the step's Adam is fused with the cull of this rank's next slice
+        # (gpk_graph_capture_train_next), so each step starts at K_decide
+        if u2:
+            return sess.capture_train(poses[k], psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS,
+                                      next_pose=poses[(k + world) % len(poses)] if args.pipeline else None)
+        return sess.capture_fwd_bwd(poses[k], psf, rcfg)
 
     # one CUDA graph per slice pose: the whole step is one submission
-    graphs = [capture(p) for p in poses] if args.graphs else None
+    graphs = [capture(k) for k in range(len(poses))] if args.graphs else None
 
     def step(i):
         k = dp.slice_for(i, rank, world, len(poses))
         if graphs is not None:
             sess.graph_launch(graphs[k])
-        elif u2:
-            sess.train_step(poses[k], psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS)  # all-reduce inside
+        elif u2:  # all-reduce inside
+            sess.train_step(poses[k], psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS,
+                            next_pose=poses[(k + world) % len(poses)] if args.pipeline else None)
         else:
             sess.fwd_bwd_slice(poses[k], psf, rcfg)
         if world > 1 and not u2:
@@ -427,7 +436,7 @@ def run_ours(args):
     # themselves add ~2-4 us per stage, so these over-state each stage a little)
     prof_steps = min(args.steps, 100)
     sess.stage_timing(True)
-    prof_graphs = [capture(p) for p in poses]
+    prof_graphs = [capture(k) for k in range(len(poses))]
     sess.stage_times(reset=True)
     for i in range(prof_steps):
         flush()
@@ -487,11 +496,14 @@ def run_ours(args):
                  8 * T if passes == 1 else 16 * T * passes,
                  "8T (bucketed slots in, tile lists out)" if passes == 1 else "16T per radix pass"),
         "raster": ("k_raster_fwd", 52 * T + 4 * P, "52T (slot + 48 B record per pair) + 4P image"),
-        "backward": ("k_raster_bwd", 52 * T + 4 * P + 24 * T, "52T + 4P dL/dI + 24T partials"),
+        "backward": ("k_raster_bwd", 52 * T + 4 * P + 24 * T + (20 * P if u2 else 0),
+                     "52T + 4P dL/dI + 24T partials" + (" + 20P fused SSIM backward" if u2 else "")),
         "chain": ("k_chain", 48 * S + 48 * S + 24 * T + 44 * S + 4 * S,
                   "48S records + 48S params + 24T partials + 44S grads + 4S dirty list"),
-        "loss": ("k_ssim_fwd + k_ssim_bwd", 36 * P, "8P images + 4P dL/dI + 24P SSIM moments (w+r)"),
-        "adam": ("k_adam", 308 * n, "308N: read params, grads, m, v; write params, m, v"),
+        "loss": ("k_ssim_fwd", 20 * P, "8P images + 12P SSIM partials (the backward half runs in k_raster_bwd)"),
+        "adam": ("k_adam_cull", 308 * n + 48 * Cc,
+                 "308N: read params, grads, m, v; write params, m, v + 48C next-slice candidates")
+        if (u2 and args.pipeline) else ("k_adam", 308 * n, "308N: read params, grads, m, v; write params, m, v"),
     }
     measured = {k: v for k, v in stages.items() if v[1] > 0 and k in kernel_bytes}
     dom = max(measured, key=lambda k: measured[k][0])
@@ -529,9 +541,10 @@ def run_ours(args):
         "gpu_launches": None,
         "clocks": clk.result(),
     }
-    # filter + decide + (gather | radix passes) + forward + backward + chain + chain_exact
-    # (+ u2: 2 loss kernels + Adam; u1: + memset node, not a kernel)
-    launches = 2 + (1 if passes == 1 else passes) + 4 + (3 if u2 else 0)
+    # u1: filter + decide + (gather | radix passes) + forward + backward + chain + chain_exact;
+    # u2: the same without the filter (fused into Adam) + SSIM forward + Adam/cull
+    # (the SSIM backward runs inside the raster backward; memsets are not kernels)
+    launches = 2 + (1 if passes == 1 else passes) + 4 + (1 if u2 else 0)
     line["gpu_launches"] = launches * args.steps
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GPK_ABI_VERSION 2
+#define GPK_ABI_VERSION 3
 #define GPK_RECORD_FLOATS 11
 
 typedef enum {
@@ -246,6 +246,16 @@ int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* ps
                    const gpk_raster_config* cfg, double lambda, double dssim_scale,
                    const gpk_learning_rates* lr0, int32_t total_iterations);
 
+/* Pipelined U2: as gpk_train_step, with Adam fused with the cull of next_pose
+ * (same PSF and raster config): the parameters cross HBM once per step and the
+ * next step on next_pose starts at K_decide. Results are bitwise those of
+ * gpk_train_step; any other call that changes parameters or gradients in
+ * between simply makes the next step cull again. */
+int gpk_train_step_next(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                        const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                        const gpk_learning_rates* lr0, int32_t total_iterations,
+                        const gpk_slice_pose* next_pose);
+
 /* ---- CUDA graphs of the fused paths ------------------------------------------- */
 /* Capture gpk_fwd_bwd_slice / gpk_train_step for a fixed pose into an
  * executable CUDA graph (launch overhead of the ~7 kernels collapses to one
@@ -257,6 +267,12 @@ int gpk_graph_capture_train(gpk_session* s, const gpk_slice_pose* pose, const gp
                             const gpk_raster_config* cfg, double lambda, double dssim_scale,
                             const gpk_learning_rates* lr0, int32_t total_iterations,
                             int32_t* graph_id);
+/* Graph of gpk_train_step_next (launching it culls its own slice first when the
+ * previous launch did not leave it culled). */
+int gpk_graph_capture_train_next(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                                 const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                                 const gpk_learning_rates* lr0, int32_t total_iterations,
+                                 const gpk_slice_pose* next_pose, int32_t* graph_id);
 int gpk_graph_launch(gpk_session* s, int32_t graph_id);
 int gpk_graph_destroy_all(gpk_session* s);
 

@@ -13,7 +13,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libgpile_b200.so"
-GPK_ABI_VERSION = 2  # include/gpile_b200.h
+GPK_ABI_VERSION = 3  # include/gpile_b200.h
 
 GPK_OK = 0
 GPK_ERR_INVALID_ARGUMENT = 1
@@ -145,11 +145,16 @@ _PROTOS = {
                                     C.POINTER(RasterConfigC)]),
     "gpk_train_step": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC), C.POINTER(RasterConfigC),
                                  C.c_double, C.c_double, C.POINTER(LearningRatesC), C.c_int32]),
+    "gpk_train_step_next": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC), C.POINTER(RasterConfigC),
+                                 C.c_double, C.c_double, C.POINTER(LearningRatesC), C.c_int32, C.POINTER(SlicePoseC)]),
     "gpk_graph_capture_fwd_bwd": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC),
                                             C.POINTER(RasterConfigC), C.POINTER(C.c_int32)]),
     "gpk_graph_capture_train": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC),
                                           C.POINTER(RasterConfigC), C.c_double, C.c_double,
                                           C.POINTER(LearningRatesC), C.c_int32, C.POINTER(C.c_int32)]),
+    "gpk_graph_capture_train_next": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC),
+                                          C.POINTER(RasterConfigC), C.c_double, C.c_double,
+                                          C.POINTER(LearningRatesC), C.c_int32, C.POINTER(SlicePoseC), C.POINTER(C.c_int32)]),
     "gpk_graph_launch": (C.c_int, [_P, C.c_int32]),
     "gpk_graph_destroy_all": (C.c_int, [_P]),
     "gpk_voxelize": (C.c_int, [_P, C.POINTER(VoxelizerConfigC), _F]),

@@ -390,10 +390,18 @@ class Session:
         self.shape = (pose.height, pose.width)
 
     def train_step(self, pose: SlicePose, psf: PsfSpec, cfg: RasterConfig, lam: float,
-                   dssim_scale: float, lr0: LearningRates, total_iterations: int):
+                   dssim_scale: float, lr0: LearningRates, total_iterations: int,
+                   next_pose: SlicePose | None = None):
+        """One training step on `pose` (target from GPK_BUF_TARGET). With
+        next_pose, Adam is fused with the next slice's cull (gpk_train_step_next)."""
         p, f, c, l = pose.to_c(), psf.to_c(), cfg.to_c(), lr0.to_c()
-        check(N.lib.gpk_train_step(self._h, C.byref(p), C.byref(f), C.byref(c), lam, dssim_scale,
-                                   C.byref(l), int(total_iterations)))
+        if next_pose is None:
+            check(N.lib.gpk_train_step(self._h, C.byref(p), C.byref(f), C.byref(c), lam, dssim_scale,
+                                       C.byref(l), int(total_iterations)))
+        else:
+            nx = next_pose.to_c()
+            check(N.lib.gpk_train_step_next(self._h, C.byref(p), C.byref(f), C.byref(c), lam, dssim_scale,
+                                            C.byref(l), int(total_iterations), C.byref(nx)))
         self.shape = (pose.height, pose.width)
 
     # CUDA graphs of the fused paths
@@ -405,9 +413,17 @@ class Session:
         return int(gid.value)
 
     def capture_train(self, pose: SlicePose, psf: PsfSpec, cfg: RasterConfig, lam: float,
-                      dssim_scale: float, lr0: LearningRates, total_iterations: int) -> int:
+                      dssim_scale: float, lr0: LearningRates, total_iterations: int,
+                      next_pose: SlicePose | None = None) -> int:
         p, f, c, l = pose.to_c(), psf.to_c(), cfg.to_c(), lr0.to_c()
         gid = C.c_int32()
+        if next_pose is not None:
+            nx = next_pose.to_c()
+            check(N.lib.gpk_graph_capture_train_next(self._h, C.byref(p), C.byref(f), C.byref(c), lam,
+                                                     dssim_scale, C.byref(l), int(total_iterations),
+                                                     C.byref(nx), C.byref(gid)))
+            self.shape = (pose.height, pose.width)
+            return int(gid.value)
         check(N.lib.gpk_graph_capture_train(self._h, C.byref(p), C.byref(f), C.byref(c), lam,
                                             dssim_scale, C.byref(l), int(total_iterations),
                                             C.byref(gid)))

@@ -1,0 +1,165 @@
+// adam.cuh — the Adam update of adam_step (optimize.hpp:184-221), shared by the
+// stand-alone Adam kernel (adam.cu) and the training step's Adam + next-slice
+// cull kernel (prep.cu). Every operation is an explicit round-to-nearest
+// intrinsic, so both translation units (prep.cu is built with --fmad=false)
+// produce the same bits. A thread updates N consecutive primitives with one
+// N*4-byte access per plane and array.
+#pragma once
+
+#include "common.cuh"
+
+namespace gpk {
+
+// Per-launch constants, evaluated once per CTA by thread 0 (fp64, then f32):
+// bias corrections of step+1 and the lr_at schedule (optimize.hpp:71-73).
+struct AdamConsts {
+    float b1, b2, ib1, ib2;   // beta1, beta2, 1 - beta1, 1 - beta2
+    float ibc1, isbc2, eps;   // 1 / bc1, 1 / sqrt(bc2), eps
+    float lr[4];              // position, opacity, scale, rotation
+};
+
+__device__ __forceinline__ void adam_consts(const AdamLaunch& a, AdamConsts& c) {
+    const long long step = *a.step + 1;
+    const double bc1 = 1.0 - pow(a.beta1, (double)step);
+    const double bc2 = 1.0 - pow(a.beta2, (double)step);
+    double f = 1.0;
+    if (a.scheduled) f = pow(0.1, (double)(step - 1) / (double)a.total);
+    c.b1 = (float)a.beta1;
+    c.b2 = (float)a.beta2;
+    c.ib1 = (float)(1.0 - a.beta1);
+    c.ib2 = (float)(1.0 - a.beta2);
+    c.ibc1 = __frcp_rn((float)bc1);
+    c.isbc2 = __frcp_rn(__fsqrt_rn((float)bc2));
+    c.eps = (float)a.eps;
+    for (int k = 0; k < 4; ++k) c.lr[k] = (float)(a.lr[k] * f);
+}
+
+// N consecutive floats moved with one vector access.
+template <int N>
+struct Pack {
+    float v[N];
+};
+template <int N>
+__device__ __forceinline__ Pack<N> ldp(const float* p) {
+    Pack<N> r;
+    if constexpr (N == 4) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        r.v[0] = t.x, r.v[1] = t.y, r.v[2] = t.z, r.v[3] = t.w;
+    } else if constexpr (N == 2) {
+        const float2 t = *reinterpret_cast<const float2*>(p);
+        r.v[0] = t.x, r.v[1] = t.y;
+    } else {
+        r.v[0] = *p;
+    }
+    return r;
+}
+template <int N>
+__device__ __forceinline__ Pack<N> ldp_stream(const float* p) {
+    Pack<N> r;
+    if constexpr (N == 4) {
+        const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+        r.v[0] = t.x, r.v[1] = t.y, r.v[2] = t.z, r.v[3] = t.w;
+    } else if constexpr (N == 2) {
+        const float2 t = __ldcs(reinterpret_cast<const float2*>(p));
+        r.v[0] = t.x, r.v[1] = t.y;
+    } else {
+        r.v[0] = __ldcs(p);
+    }
+    return r;
+}
+template <int N>
+__device__ __forceinline__ void stp(float* p, const Pack<N>& r) {
+    if constexpr (N == 4)
+        *reinterpret_cast<float4*>(p) = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
+    else if constexpr (N == 2)
+        *reinterpret_cast<float2*>(p) = make_float2(r.v[0], r.v[1]);
+    else
+        *p = r.v[0];
+}
+
+// lr * (m / bc1) / (sqrt(v / bc2) + eps), bias corrections folded into the
+// constants; sqrt and the division on MUFU (relative error ~1e-7).
+__device__ __forceinline__ float adam_delta(const AdamConsts& c, float lrc, float m, float v) {
+    const float sq = v > 0.f ? __fmul_rn(v, rsqrtf(v)) : 0.f;
+    return __fdividef(__fmul_rn(lrc, m), __fmaf_rn(sq, c.isbc2, c.eps));
+}
+
+// One parameter plane of N consecutive primitives: moments updated and stored,
+// the stepped parameters returned (before clamp / renormalisation); nz collects
+// which primitives had a non-zero gradient.
+template <int N>
+__device__ __forceinline__ Pack<N> adam_plane(const AdamLaunch& a, const AdamConsts& c, int k, float lr, uint32_t i0,
+                                              unsigned& nz) {
+    const uint64_t o = (uint64_t)k * a.cap + i0;
+    const Pack<N> g = ldp_stream<N>(a.grads + o);
+    Pack<N> m = ldp<N>(a.m + o), v = ldp<N>(a.v + o), p = ldp<N>(a.params + o);
+    const float lrc = __fmul_rn(lr, c.ibc1);
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+        nz |= (g.v[l] != 0.f ? 1u : 0u) << l;
+        m.v[l] = __fmaf_rn(c.b1, m.v[l], __fmul_rn(c.ib1, g.v[l]));
+        v.v[l] = __fmaf_rn(c.b2, v.v[l], __fmul_rn(__fmul_rn(c.ib2, g.v[l]), g.v[l]));
+        p.v[l] = __fsub_rn(p.v[l], adam_delta(c, lrc, m.v[l], v.v[l]));
+    }
+    stp<N>(a.m + o, m);
+    stp<N>(a.v + o, v);
+    return p;
+}
+
+// All 11 planes of N consecutive primitives in the reference's order: position
+// then the bbox clamp (optimize.hpp:212), log-scale, raw alpha, quaternion then
+// renormalisation when the norm is > 0 (:216-217). p[k] returns the new
+// parameters; nz the primitives with a non-zero gradient.
+template <int N>
+__device__ __forceinline__ void adam_update(const AdamLaunch& a, const AdamConsts& c, uint32_t i0, Pack<N> p[11],
+                                            unsigned& nz) {
+    nz = 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        p[d] = adam_plane<N>(a, c, d, c.lr[0], i0, nz);
+        const float lo = a.bbox_min[d], hi = a.bbox_max[d];
+#pragma unroll
+        for (int l = 0; l < N; ++l) p[d].v[l] = fminf(hi, fmaxf(lo, p[d].v[l]));
+    }
+#pragma unroll
+    for (int d = 3; d < 6; ++d) p[d] = adam_plane<N>(a, c, d, c.lr[2], i0, nz);
+    p[10] = adam_plane<N>(a, c, 10, c.lr[1], i0, nz);
+#pragma unroll
+    for (int d = 6; d < 10; ++d) p[d] = adam_plane<N>(a, c, d, c.lr[3], i0, nz);
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+        float& w = p[6].v[l];
+        float& x = p[7].v[l];
+        float& y = p[8].v[l];
+        float& z = p[9].v[l];
+        const float qn = __fsqrt_rn(__fmaf_rn(w, w, __fmaf_rn(x, x, __fmaf_rn(y, y, __fmul_rn(z, z)))));
+        if (qn > 0.f) {
+            const float inv = __frcp_rn(qn);
+            w = __fmul_rn(w, inv);
+            x = __fmul_rn(x, inv);
+            y = __fmul_rn(y, inv);
+            z = __fmul_rn(z, inv);
+        }
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void adam_store(const AdamLaunch& a, uint32_t i0, const Pack<N> p[11]) {
+#pragma unroll
+    for (int d = 0; d < 11; ++d) stp<N>(a.params + (uint64_t)d * a.cap + i0, p[d]);
+}
+
+// The last CTA out advances AdamState::step (the kernel's CTAs read it first).
+__device__ __forceinline__ void adam_finish(const AdamLaunch& a) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(a.done_ctr, 1u);
+        if (done == gridDim.x - 1) {
+            *a.step += 1;
+            *a.done_ctr = 0;
+        }
+    }
+}
+
+}  // namespace gpk

@@ -323,7 +323,7 @@ struct PrepLaunch {
     uint64_t cap;             // plane stride
     uint32_t n;
     float* grads;             // cleared (dense or sparse, see kGradsDense) when non-null
-    const unsigned* grads_dirty;    // persistent gradient-buffer state word
+    unsigned* grads_dirty;          // persistent gradient-buffer state word
     const uint32_t* dirty_idx;      // previous survivors' set indices
     CandParams* cand;         // K_filter -> K_decide: candidate params, block-major slots
     unsigned* cand_count;     // candidates per chunk (plain stores)
@@ -352,9 +352,9 @@ struct PrepLaunch {
     SliceArgs slice;
 };
 
-constexpr int kFilterItems = 2;                            // consecutive Gaussians per K_filter lane
-constexpr int kFilterBlock = 32 * kFilterItems;            // Gaussians per K_filter warp chunk (64)
-constexpr int kDecideChunks = 64;                          // K_filter chunks per K_decide group
+constexpr int kFilterItems = 4;                            // consecutive Gaussians per K_filter lane
+constexpr int kFilterBlock = 32 * kFilterItems;            // Gaussians per K_filter warp chunk (128)
+constexpr int kDecideChunks = 32;                          // K_filter chunks per K_decide group
 constexpr int kDecideGroupSize = kDecideChunks * kFilterBlock;  // Gaussians per group (4096)
 constexpr int kParamAlign = 512;                           // plane stride (capacity) granularity
 
@@ -441,7 +441,7 @@ struct ChainLaunch {
 
 struct AdamLaunch {
     float* params;
-    const float* grads;
+    float* grads;         // read (and cleared where non-zero by the fused Adam + cull)
     float* m;
     float* v;
     uint64_t cap;
@@ -547,6 +547,7 @@ void launch_vox_bwd(const VoxEvalLaunch& a, cudaStream_t st);
 void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st);
 
 void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st);
+void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& next, cudaStream_t st);
 void launch_bin(const PrepLaunch& a, cudaStream_t st);
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st);
 void launch_raster_fwd(const RasterLaunch& a, cudaStream_t st);

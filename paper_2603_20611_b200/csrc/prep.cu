@@ -23,6 +23,7 @@
 //             sort on the tile key needs to reproduce the reference lists.
 //             Global and per-sort-tile digit histograms for the first radix
 //             pass are accumulated on the way.
+#include "adam.cuh"
 #include "common.cuh"
 #include "focus.cuh"
 
@@ -153,20 +154,94 @@ __device__ __forceinline__ bool quick_culled_identity(const float p[11], const F
 
 // ---- K_filter ------------------------------------------------------------------
 // prepare_gaussians' cull (render.hpp:107) as a streaming pass with no block
-// barriers. Warps walk 64-Gaussian chunks grid-stride; each lane owns two
-// consecutive Gaussians and loads their 11 parameters with one 8 B vector load
-// per plane straight into registers (many warps per SM keep the HBM pipe
+// barriers. Warps walk 128-Gaussian chunks grid-stride; each lane owns four
+// consecutive Gaussians and loads their 11 parameters with one 16 B vector
+// load per plane straight into registers (many warps per SM keep the HBM pipe
 // full). Per chunk:
 //   1. division-free fp32 quick bound; lanes whose Gaussians it cannot decide
 //      run the full closed-form test (q = mu_cz^2 / (sigma_z^2 + Sigma_c,zz),
 //      SURVEY.md §7.3.2) — both conservative: a culled Gaussian is one the
 //      reference culls too;
 //   2. candidates compacted in set order (warp scan) into 48 B CandParams
-//      records at chunk-major slots [b*64, b*64 + count_b), count_b stored.
+//      records at chunk-major slots [b*128, b*128 + count_b), count_b stored.
 // Gradient clearing (dense output contract, grad_chain.hpp:12-22): the previous
 // survivors' entries (sparse), or the chunk's planes when anything else wrote
 // them. No fp64 and no cross-warp waiting here.
 constexpr int kFilterThreads = 256;
+
+// Housekeeping shared by the cull kernels: clear the per-sort-tile digit
+// histograms the previous radix sort used (its passes only) before this
+// prepare / the radix passes refill them.
+__device__ __forceinline__ void clear_prev_sort_rows(const PrepLaunch& a, unsigned gtid, unsigned gthreads) {
+    const unsigned pt = a.prev_sort_words[0], pnb = a.prev_sort_words[1], pp = a.prev_sort_words[2];
+    const unsigned tile_words = pt * pnb;
+    const unsigned used = tile_words + ((pt + kSuperTiles - 1) / kSuperTiles) * pnb;  // per pass
+    for (unsigned ps = 0; ps < pp; ++ps) {
+        unsigned* region = a.tile_hist_all + (uint64_t)ps * a.hist_region;
+        unsigned* super = region + a.sort_tiles_cap * pnb - tile_words;
+        for (unsigned w = gtid; w < used; w += gthreads) (w < tile_words ? region : super)[w] = 0u;
+    }
+}
+
+__device__ __forceinline__ FilterConsts filter_consts(const SliceArgs& sl, float log_tau) {
+    FilterConsts fc;
+    fc.log_tau = log_tau;
+    fc.mod = (float)sl.mod;
+    fc.sz2 = (float)(sl.sigma_z * sl.sigma_z);
+    fc.tx = (float)sl.t[0];
+    fc.ty = (float)sl.t[1];
+    fc.tz_hi = (float)sl.t[2];
+    fc.tz_lo = (float)(sl.t[2] - (double)fc.tz_hi);
+    fc.mod2 = (float)(sl.mod * sl.mod);
+    fc.inv_mod2 = (float)(1.0 / (sl.mod * sl.mod));
+    fc.inv_sz2 = (float)(1.0 / (sl.sigma_z * sl.sigma_z));
+    return fc;
+}
+
+// Cull one warp chunk (128 consecutive Gaussians, 4 per lane in v[]) and
+// compact its candidates in set order (lanes in order, each lane's 4 in order)
+// into 48 B CandParams records at slots [b*128, b*128 + count_b). Whole warp.
+__device__ __forceinline__ void cull_chunk(const PrepLaunch& a, const FilterConsts& fc, float log_tau, int filter_on,
+                                           unsigned b, uint32_t i0, const float4 v[11]) {
+    const int lane = threadIdx.x & 31;
+    const bool ident = a.slice.identity_rot != 0;
+    unsigned cmask = 0;
+#pragma unroll
+    for (int k = 0; k < kFilterItems; ++k) {
+        if (i0 + k >= a.n) continue;
+        float p[11];
+#pragma unroll
+        for (int q = 0; q < 11; ++q) p[q] = (&v[q].x)[k];
+        bool cand = true;
+        if (filter_on) {
+            if (ident && quick_culled_identity(p, fc)) {
+                cand = false;
+            } else {
+                cand = ident ? !certainly_culled_identity(p, fc) : !certainly_culled(p, a.slice, log_tau, fc.mod, fc.sz2);
+            }
+        }
+        cmask |= (cand ? 1u : 0u) << k;
+    }
+    const unsigned nc = __popc(cmask);
+    unsigned incl = nc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) a.cand_count[b] = incl;
+    if (cmask) {
+        CandParams* out = a.cand + (uint64_t)b * kFilterBlock + (incl - nc);
+#pragma unroll
+        for (int k = 0; k < kFilterItems; ++k)
+            if (cmask & (1u << k)) {
+                float p[11];
+#pragma unroll
+                for (int q = 0; q < 11; ++q) p[q] = (&v[q].x)[k];
+                store_cand(out++, p, i0 + k);
+            }
+    }
+}
 
 template <bool kZeroGrads>
 __global__ void __launch_bounds__(kFilterThreads) k_filter(const PrepLaunch a, float log_tau, int filter_on) {
@@ -178,89 +253,74 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(const PrepLaunch a, f
     const unsigned gthreads = gridDim.x * kFilterThreads;
     const unsigned gtid = blockIdx.x * kFilterThreads + tid;
 
-    // Housekeeping: clear the per-sort-tile digit histograms the previous
-    // sort used (its passes only) before this prepare / the radix passes refill
-    // them; clear the previous survivors' gradients (sparse mode).
-    {
-        const unsigned pt = a.prev_sort_words[0], pnb = a.prev_sort_words[1], pp = a.prev_sort_words[2];
-        const unsigned tile_words = pt * pnb;
-        const unsigned used = tile_words + ((pt + kSuperTiles - 1) / kSuperTiles) * pnb;  // per pass
-        for (unsigned ps = 0; ps < pp; ++ps) {
-            unsigned* region = a.tile_hist_all + (uint64_t)ps * a.hist_region;
-            unsigned* super = region + a.sort_tiles_cap * pnb - tile_words;
-            for (unsigned w = gtid; w < used; w += gthreads) (w < tile_words ? region : super)[w] = 0u;
-        }
-        if (kZeroGrads && !dense_zero)
-            for (unsigned e = gtid; e < dirty; e += gthreads) {
-                const uint32_t i = a.dirty_idx[e];
+    clear_prev_sort_rows(a, gtid, gthreads);
+    if (kZeroGrads && !dense_zero)  // the previous survivors' gradients (sparse mode)
+        for (unsigned e = gtid; e < dirty; e += gthreads) {
+            const uint32_t i = a.dirty_idx[e];
 #pragma unroll
-                for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = 0.f;
-            }
-    }
-
-    FilterConsts fc;
-    fc.log_tau = log_tau;
-    fc.mod = (float)a.slice.mod;
-    fc.sz2 = (float)(a.slice.sigma_z * a.slice.sigma_z);
-    fc.tx = (float)a.slice.t[0];
-    fc.ty = (float)a.slice.t[1];
-    fc.tz_hi = (float)a.slice.t[2];
-    fc.tz_lo = (float)(a.slice.t[2] - (double)fc.tz_hi);
-    fc.mod2 = (float)(a.slice.mod * a.slice.mod);
-    fc.inv_mod2 = (float)(1.0 / (a.slice.mod * a.slice.mod));
-    fc.inv_sz2 = (float)(1.0 / (a.slice.sigma_z * a.slice.sigma_z));
-    const bool ident = a.slice.identity_rot != 0;
+            for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = 0.f;
+        }
+    const FilterConsts fc = filter_consts(a.slice, log_tau);
 
     const unsigned gwarps = gthreads / 32;
     for (unsigned b = gtid / 32; b < nchunks; b += gwarps) {
         const uint32_t i0 = b * kFilterBlock + lane * kFilterItems;  // this lane's first Gaussian
-        // cap is a multiple of kParamAlign: the pair load never leaves the plane
-        float2 v[11];
+        // cap is a multiple of kParamAlign: the 16 B load never leaves the plane
+        float4 v[11];
 #pragma unroll
-        for (int q = 0; q < 11; ++q) v[q] = __ldcs(reinterpret_cast<const float2*>(a.params + (uint64_t)q * a.cap + i0));
+        for (int q = 0; q < 11; ++q) v[q] = __ldcs(reinterpret_cast<const float4*>(a.params + (uint64_t)q * a.cap + i0));
         if (dense_zero)
 #pragma unroll
             for (int q = 0; q < 11; ++q)
-                *reinterpret_cast<float2*>(a.grads + (uint64_t)q * a.cap + i0) = make_float2(0.f, 0.f);
-        unsigned cmask = 0;
-#pragma unroll
-        for (int k = 0; k < kFilterItems; ++k) {
-            if (i0 + k >= a.n) continue;
-            float p[11];
-#pragma unroll
-            for (int q = 0; q < 11; ++q) p[q] = k ? v[q].y : v[q].x;
-            bool cand = true;
-            if (filter_on) {
-                if (ident && quick_culled_identity(p, fc)) {
-                    cand = false;
-                } else {
-                    cand = ident ? !certainly_culled_identity(p, fc)
-                                 : !certainly_culled(p, a.slice, log_tau, fc.mod, fc.sz2);
-                }
-            }
-            cmask |= (cand ? 1u : 0u) << k;
-        }
-        // set-order compaction: lanes in order, each lane's two Gaussians in order
-        const unsigned nc = __popc(cmask);
-        unsigned incl = nc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
-        }
-        if (lane == 31) a.cand_count[b] = incl;
-        if (cmask) {
-            CandParams* out = a.cand + (uint64_t)b * kFilterBlock + (incl - nc);
-#pragma unroll
-            for (int k = 0; k < kFilterItems; ++k)
-                if (cmask & (1u << k)) {
-                    float p[11];
-#pragma unroll
-                    for (int q = 0; q < 11; ++q) p[q] = k ? v[q].y : v[q].x;
-                    store_cand(out++, p, i0 + k);
-                }
-        }
+                *reinterpret_cast<float4*>(a.grads + (uint64_t)q * a.cap + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
+        cull_chunk(a, fc, log_tau, filter_on, b, i0, v);
     }
+}
+
+// ---- K_adam_cull -----------------------------------------------------------------
+// Training step: adam_step (optimize.hpp:195-221) fused with the NEXT slice's
+// K_filter. Both stream every parameter once; fused, the next step starts at
+// K_decide and the parameters cross HBM once per step instead of twice. Each
+// thread updates 4 consecutive primitives (adam.cuh: the same bits as the
+// stand-alone Adam kernel), clears the gradients it consumed where they were
+// non-zero (the survivors: the dense gradient is exactly zero again), then its
+// warp culls the 128 updated primitives against the next pose (cull_chunk).
+__global__ void __launch_bounds__(256) k_adam_cull(const AdamLaunch a, const PrepLaunch f, float log_tau,
+                                                   int filter_on) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    __shared__ AdamConsts s_c;
+    const bool adam_on = !(a.ctrl && a.ctrl->pair_overflow);  // the slice overflowed: no update
+    if (threadIdx.x == 0) adam_consts(a, s_c);
+    __syncthreads();
+    const AdamConsts c = s_c;
+    const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    clear_prev_sort_rows(f, gtid, gridDim.x * blockDim.x);
+    if (gtid == 0) *f.grads_dirty = 0u;  // every gradient is zero after this kernel
+    const uint32_t i0 = gtid * kFilterItems;
+    float4 p[11];
+    if (i0 < a.n) {
+        if (adam_on) {
+            unsigned nz;
+            Pack<kFilterItems> q[11];
+            adam_update<kFilterItems>(a, c, i0, q, nz);
+            adam_store<kFilterItems>(a, i0, q);
+#pragma unroll
+            for (int d = 0; d < 11; ++d) p[d] = make_float4(q[d].v[0], q[d].v[1], q[d].v[2], q[d].v[3]);
+            if (nz)
+#pragma unroll
+                for (int d = 0; d < 11; ++d)
+                    *reinterpret_cast<float4*>(a.grads + (uint64_t)d * a.cap + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+#pragma unroll
+            for (int d = 0; d < 11; ++d) p[d] = *reinterpret_cast<const float4*>(a.params + (uint64_t)d * a.cap + i0);
+        }
+    } else {
+#pragma unroll
+        for (int d = 0; d < 11; ++d) p[d] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const unsigned b = i0 / kFilterBlock;  // the warp's chunk
+    if (b < f.nfilter) cull_chunk(f, filter_consts(f.slice, log_tau), log_tau, filter_on, b, i0, p);
+    if (adam_on) adam_finish(a);
 }
 
 // ---- K_decide ------------------------------------------------------------------
@@ -904,6 +964,15 @@ void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st) {
         launch_pdl(k_filter<true>, dim3(grid), dim3(kFilterThreads), 0, st, a, log_tau, filter_on ? 1 : 0);
     else
         launch_pdl(k_filter<false>, dim3(grid), dim3(kFilterThreads), 0, st, a, log_tau, filter_on ? 1 : 0);
+}
+
+void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& f, cudaStream_t st) {
+    const bool filter_on = f.slice.tau > 0.0 && f.slice.mod > 1e-10 && f.slice.mod < 1e10 &&
+                           f.slice.sigma_z > 1e-10 && f.slice.sigma_z < 1e10;
+    const float log_tau = filter_on ? (float)log(f.slice.tau) : 0.f;
+    const unsigned threads = (unsigned)std::max<uint64_t>((uint64_t)f.nfilter * 32, (a.n + kFilterItems - 1) / kFilterItems);
+    const unsigned grid = (threads + 255) / 256;
+    if (grid) launch_pdl(k_adam_cull, dim3(grid), dim3(256), 0, st, a, f, log_tau, filter_on ? 1 : 0);
 }
 
 void launch_bin(const PrepLaunch& a, cudaStream_t st) {

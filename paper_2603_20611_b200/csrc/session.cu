@@ -116,6 +116,20 @@ struct gpk_session {
     uint2* grp_pairs() { return grp_table.as<uint2>(); }
     unsigned* grp_surv() { return reinterpret_cast<unsigned*>(grp_table.as<char>() + (cap / kDecideGroupSize + 2) * 8); }
     int num_sms = 148;
+    // candidates of a slice culled ahead of time by the fused Adam + cull of the
+    // previous training step (K_filter can be skipped when they match)
+    struct Prefilter {
+        bool valid = false;
+        gpk_slice_pose pose{};
+        gpk_psf psf{};
+        gpk_raster_config cfg{};
+        uint64_t n = 0;
+    } prefilter;
+    bool assume_prefiltered = false;  // set while capturing a pipelined train step
+    struct CaptureMeta {
+        bool needs_prefilter = false, sets_prefilter = false, writes_params = false;
+        gpk_slice_pose next_pose{};
+    } capture_meta;
     DevBuf persist;    // ErrorState | epoch | adam step | adam done ctr | loss done ctr | loss
     DevBuf image, dl_di, target, loss_g, loss_partial;
     DevBuf stat_norm, stat_obs, stat_world;
@@ -141,6 +155,10 @@ struct gpk_session {
         cudaGraphExec_t exec;
         PrepState prep;
         uint64_t alloc_epoch;
+        bool needs_prefilter = false;  // pipelined train step: starts at K_decide
+        bool sets_prefilter = false;   // ... and leaves next_pose culled
+        bool writes_params = false;
+        gpk_slice_pose next_pose{};
         std::vector<Pending> timed;  // event-record nodes captured with stage timing on
     };
     bool capturing = false;
@@ -292,6 +310,7 @@ int sync_and_check(gpk_session* s, const char* where) {
 // The gradient planes were written by something other than K_chain: the next
 // prepare clears them densely (see kGradsDense).
 int mark_grads_dense(gpk_session* s) {
+    s->prefilter.valid = false;  // a skipped K_filter would not clear them
     CK(cudaMemsetAsync(s->grads_dirty(), 0xff, 4, s->stream));
     return GPK_OK;
 }
@@ -391,6 +410,57 @@ int launch_sorts(gpk_session* s, int passes, int digit_bits, const uint2* grp_pa
                  unsigned ngroups = 0);
 uint64_t decide_group_count(uint64_t n);
 
+PrepLaunch prep_launch(gpk_session* s, const SliceArgs& a, int passes, int digit_bits, bool zero_grads) {
+    PrepLaunch pl;
+    pl.params = s->params.as<float>();
+    pl.cap = s->cap;
+    pl.n = (uint32_t)s->n;
+    pl.grads = zero_grads ? s->grads.as<float>() : nullptr;
+    pl.surv_params = s->surv_params.as<CandParams>();
+    pl.cand = s->cand.as<CandParams>();
+    pl.cand_count = s->cand_count.as<unsigned>();
+    pl.grp_pairs = s->grp_pairs();
+    pl.grp_surv = s->grp_surv();
+    pl.bucket_tab = passes == 1 ? s->bucket_tab.as<unsigned>() : nullptr;
+    pl.tile_begin = s->grp_begin();
+    pl.grads_dirty = s->grads_dirty();
+    pl.dirty_idx = s->dirty_idx.as<uint32_t>();
+    pl.nfilter = (unsigned)filter_blocks(s->n);
+    pl.records = s->records.as<SurvivorRecord>();
+    pl.survivor_list = s->survivors.as<uint32_t>();
+    pl.keys = s->keys[0].as<uint32_t>();
+    pl.vals = s->vals[0].as<uint32_t>();
+    pl.pair_cap = s->pair_cap;
+    pl.hist = s->hist();
+    pl.tile_hist0 = s->sort_status.as<unsigned>();
+    pl.tile_hist_all = s->sort_status.as<unsigned>();
+    pl.sort_tiles_cap = s->sort_tiles_cap;
+    pl.hist_region = s->hist_region;
+    pl.prev_sort_words = s->prev_sort_words();
+    pl.passes = passes;
+    pl.digit_bits = digit_bits;
+    pl.exact_words = reinterpret_cast<unsigned long long*>(s->filter_flags());
+    pl.ctrl = s->ctrl();
+    pl.err = s->err();
+    pl.slice = a;
+    return pl;
+}
+
+bool prefilter_matches(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                       const gpk_raster_config* cfg) {
+    const auto& f = s->prefilter;
+    return f.valid && f.n == s->n && std::memcmp(&f.pose, pose, sizeof *pose) == 0 &&
+           std::memcmp(&f.psf, psf, sizeof *psf) == 0 && std::memcmp(&f.cfg, cfg, sizeof *cfg) == 0;
+}
+
+void set_prefilter(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf, const gpk_raster_config* cfg) {
+    s->prefilter.valid = true;
+    s->prefilter.pose = *pose;
+    s->prefilter.psf = *psf;
+    s->prefilter.cfg = *cfg;
+    s->prefilter.n = s->n;
+}
+
 int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                 const gpk_raster_config* cfg, bool zero_grads) {
     SliceArgs a;
@@ -418,40 +488,15 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
         ps.final_buf = 0;
         return GPK_OK;
     }
-    PrepLaunch pl;
-    pl.params = s->params.as<float>();
-    pl.cap = s->cap;
-    pl.n = (uint32_t)s->n;
-    pl.grads = zero_grads ? s->grads.as<float>() : nullptr;
-    pl.surv_params = s->surv_params.as<CandParams>();
-    pl.cand = s->cand.as<CandParams>();
-    pl.cand_count = s->cand_count.as<unsigned>();
-    pl.grp_pairs = s->grp_pairs();
-    pl.grp_surv = s->grp_surv();
-    pl.bucket_tab = ps.passes == 1 ? s->bucket_tab.as<unsigned>() : nullptr;
-    pl.tile_begin = s->grp_begin();
-    pl.grads_dirty = s->grads_dirty();
-    pl.dirty_idx = s->dirty_idx.as<uint32_t>();
-    pl.nfilter = (unsigned)nbf;
-    pl.records = s->records.as<SurvivorRecord>();
-    pl.survivor_list = s->survivors.as<uint32_t>();
-    pl.keys = s->keys[0].as<uint32_t>();
-    pl.vals = s->vals[0].as<uint32_t>();
-    pl.pair_cap = s->pair_cap;
-    pl.hist = s->hist();
-    pl.tile_hist0 = s->sort_status.as<unsigned>();
-    pl.tile_hist_all = s->sort_status.as<unsigned>();
-    pl.sort_tiles_cap = s->sort_tiles_cap;
-    pl.hist_region = s->hist_region;
-    pl.prev_sort_words = s->prev_sort_words();
-    pl.passes = ps.passes;
-    pl.digit_bits = ps.digit_bits;
-    pl.exact_words = reinterpret_cast<unsigned long long*>(s->filter_flags());
-    pl.ctrl = s->ctrl();
-    pl.err = s->err();
-    pl.slice = a;
-    launch_prep(pl, s->num_sms, s->stream);
-    CK(cudaGetLastError());
+    const PrepLaunch pl = prep_launch(s, a, ps.passes, ps.digit_bits, zero_grads);
+    // K_filter is skipped when the previous training step's fused Adam + cull
+    // already produced this slice's candidates (and left the gradients zero)
+    const bool pre = zero_grads && (s->assume_prefiltered || prefilter_matches(s, pose, psf, cfg));
+    s->prefilter.valid = false;
+    if (!pre) {
+        launch_prep(pl, s->num_sms, s->stream);
+        CK(cudaGetLastError());
+    }
     scope_prep.end();
     {
         StageScope scope_bin(s, GPK_STAGE_BIN);
@@ -552,6 +597,7 @@ int run_rasterize(gpk_session* s, cudaStream_t on = nullptr) {
 
 int run_backward(gpk_session* s, bool stats) {
     if (!s->prep.valid) return fail(GPK_ERR_STATE, "backward: no prepared slice");
+    s->prefilter.valid = false;  // the chain writes gradients
     if (s->n == 0) return GPK_OK;
     if (!s->prep.grads_zeroed) {
         CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
@@ -718,9 +764,47 @@ int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
     a.step = s->adam_step();
     a.done_ctr = s->adam_done();
     a.ctrl = s->prep.valid ? s->ctrl() : nullptr;
+    s->prefilter.valid = false;  // the parameters change
     StageScope scope(s, GPK_STAGE_ADAM);
     launch_adam(a, s->stream);
     CK(cudaGetLastError());
+    return GPK_OK;
+}
+
+// Adam fused with the next slice's K_filter (the training step's last kernel):
+// leaves `next` culled for the following prepare and every gradient zero.
+int run_adam_cull(gpk_session* s, const double lr[4], int total, const gpk_slice_pose* next,
+                  const gpk_psf* psf, const gpk_raster_config* cfg) {
+    SliceArgs na;
+    TRY(make_slice(s, next, psf, cfg, na));
+    if (s->n == 0) return run_adam(s, lr, true, total, nullptr);
+    int passes = 0, digit_bits = 0;
+    sort_plan(na.tiles_x * na.tiles_y, passes, digit_bits);
+    const PrepLaunch f = prep_launch(s, na, passes, digit_bits, true);
+    AdamLaunch a;
+    a.params = s->params.as<float>();
+    a.grads = s->grads.as<float>();
+    a.m = s->adam_m.as<float>();
+    a.v = s->adam_v.as<float>();
+    a.cap = s->cap;
+    a.n = (uint32_t)s->n;
+    for (int d = 0; d < 3; ++d) {
+        a.bbox_min[d] = (float)s->bbox.min[d];
+        a.bbox_max[d] = (float)s->bbox.max[d];
+    }
+    for (int k = 0; k < 4; ++k) a.lr[k] = lr[k];
+    a.scheduled = 1;
+    a.total = total;
+    a.beta1 = 0.9;
+    a.beta2 = 0.999;
+    a.eps = 1e-8;
+    a.step = s->adam_step();
+    a.done_ctr = s->adam_done();
+    a.ctrl = s->prep.valid ? s->ctrl() : nullptr;
+    StageScope scope(s, GPK_STAGE_ADAM);
+    launch_adam_cull(a, f, s->stream);
+    CK(cudaGetLastError());
+    set_prefilter(s, next, psf, cfg);
     return GPK_OK;
 }
 
@@ -1028,7 +1112,7 @@ int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
     void* p = nullptr;
     uint64_t b = 0;
     switch (which) {
-        case GPK_BUF_PARAMS: p = s->params.p; b = s->cap * 44; break;
+        case GPK_BUF_PARAMS: p = s->params.p; b = s->cap * 44; s->prefilter.valid = false; break;
         case GPK_BUF_GRADS: p = s->grads.p; b = s->cap * 44; break;
         case GPK_BUF_IMAGE: p = s->image.p; b = px * 4; break;
         case GPK_BUF_DL_DI: p = s->dl_di.p; b = px * 4; break;
@@ -1105,6 +1189,7 @@ int gpk_set_gaussians(gpk_session* s, uint64_t n, const float* records, const gp
     s->bbox = *bbox;
     if (n) TRY(copy_params_in(s, n, records));
     s->prep.valid = false;
+    s->prefilter.valid = false;
     TRY(adam_reset(s));
     CK(cudaStreamSynchronize(s->stream));
     return ok();
@@ -1434,10 +1519,32 @@ int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* ps
     return ok();
 }
 
+// Pipelined training step: as gpk_train_step, with Adam fused with the cull of
+// `next_pose` (same PSF and raster config), so the next step on next_pose skips
+// K_filter. Bitwise the same results as gpk_train_step.
+int gpk_train_step_next(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                        const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                        const gpk_learning_rates* lr0, int32_t total_iterations,
+                        const gpk_slice_pose* next_pose) {
+    if (!s || !lr0 || !next_pose) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "total iterations must be >= 1");
+    TRY(set_device(s));
+    TRY(run_prepare(s, pose, psf, cfg, true));
+    TRY(run_rasterize(s));
+    TRY(run_loss(s, lambda, dssim_scale, true));
+    TRY(run_backward(s, false));
+    TRY(dp_allreduce_if_comm(s));
+    const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
+    TRY(run_adam_cull(s, lr, total_iterations, next_pose, psf, cfg));
+    return ok();
+}
+
 // ---- CUDA graphs -------------------------------------------------------------
 static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_session*, const void*),
                          const void* arg) {
     if (!s || !graph_id) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    const gpk_session::CaptureMeta meta = s->capture_meta;  // set by the caller for this capture
+    s->capture_meta = gpk_session::CaptureMeta{};
     TRY(set_device(s));
     CK(cudaStreamSynchronize(s->stream));
     drain_timing(s);
@@ -1465,7 +1572,16 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
     const cudaError_t ei = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (ei != cudaSuccess) return fail(GPK_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
-    s->graphs.push_back({ex, s->prep, s->alloc_epoch, std::move(timed)});
+    gpk_session::Graph gr;
+    gr.exec = ex;
+    gr.prep = s->prep;
+    gr.alloc_epoch = s->alloc_epoch;
+    gr.timed = std::move(timed);
+    gr.needs_prefilter = meta.needs_prefilter;
+    gr.sets_prefilter = meta.sets_prefilter;
+    gr.writes_params = meta.writes_params;
+    gr.next_pose = meta.next_pose;
+    s->graphs.push_back(std::move(gr));
     *graph_id = (int32_t)s->graphs.size() - 1;
     return ok();
 }
@@ -1523,6 +1639,7 @@ int gpk_graph_capture_train(gpk_session* s, const gpk_slice_pose* pose, const gp
     if (!lr0 || total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "bad learning rates");
     TRY(presize_step(s, pose, psf, cfg, true, lambda));
     const TrainArgs args{pose, psf, cfg, lambda, dssim_scale, lr0, total_iterations};
+    s->capture_meta.writes_params = true;
     return capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
         const TrainArgs* a = static_cast<const TrainArgs*>(p);
         TRY(run_prepare(ss, a->pose, a->psf, a->cfg, true));
@@ -1536,6 +1653,46 @@ int gpk_graph_capture_train(gpk_session* s, const gpk_slice_pose* pose, const gp
     }, &args);
 }
 
+struct TrainNextArgs {
+    const gpk_slice_pose* pose;
+    const gpk_psf* psf;
+    const gpk_raster_config* cfg;
+    double lambda, dssim;
+    const gpk_learning_rates* lr0;
+    int total;
+    const gpk_slice_pose* next;
+};
+
+int gpk_graph_capture_train_next(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                                 const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                                 const gpk_learning_rates* lr0, int32_t total_iterations,
+                                 const gpk_slice_pose* next_pose, int32_t* graph_id) {
+    if (!lr0 || !next_pose || total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "bad arguments");
+    TRY(presize_step(s, pose, psf, cfg, true, lambda));
+    const TrainNextArgs args{pose, psf, cfg, lambda, dssim_scale, lr0, total_iterations, next_pose};
+    s->capture_meta.needs_prefilter = true;
+    s->capture_meta.sets_prefilter = true;
+    s->capture_meta.writes_params = true;
+    s->capture_meta.next_pose = *next_pose;
+    const gpk_session::Prefilter saved = s->prefilter;
+    s->assume_prefiltered = true;
+    const int st = capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
+        const TrainNextArgs* a = static_cast<const TrainNextArgs*>(p);
+        TRY(run_prepare(ss, a->pose, a->psf, a->cfg, true));
+        ss->assume_prefiltered = false;
+        TRY(run_rasterize(ss));
+        TRY(run_loss(ss, a->lambda, a->dssim, true));
+        TRY(run_backward(ss, false));
+        TRY(dp_allreduce_if_comm(ss));
+        const double lr[4] = {a->lr0->position, a->lr0->opacity, a->lr0->scale, a->lr0->rotation};
+        TRY(run_adam_cull(ss, lr, a->total, a->next, a->psf, a->cfg));
+        return GPK_OK;
+    }, &args);
+    s->assume_prefiltered = false;
+    s->prefilter = saved;  // capture records work, it does not run it
+    return st;
+}
+
 int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
     if (!s || graph_id < 0 || graph_id >= (int32_t)s->graphs.size())
         return fail(GPK_ERR_INVALID_ARGUMENT, "unknown graph id");
@@ -1543,7 +1700,21 @@ int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
     gpk_session::Graph& g = s->graphs[graph_id];
     if (g.alloc_epoch != s->alloc_epoch)
         return fail(GPK_ERR_STATE, "graph invalidated: session buffers were reallocated since capture; recapture");
+    if (g.needs_prefilter && !prefilter_matches(s, &g.prep.pose, &g.prep.psf, &g.prep.cfg)) {
+        // the graph starts at K_decide: cull its slice first (stand-alone K_filter,
+        // which also clears the gradient planes)
+        SliceArgs a;
+        TRY(make_slice(s, &g.prep.pose, &g.prep.psf, &g.prep.cfg, a));
+        if (s->n) {
+            launch_prep(prep_launch(s, a, g.prep.passes, g.prep.digit_bits, true), s->num_sms, s->stream);
+            CK(cudaGetLastError());
+        }
+    }
     CK(cudaGraphLaunch(g.exec, s->stream));
+    if (g.sets_prefilter)
+        set_prefilter(s, &g.next_pose, &g.prep.psf, &g.prep.cfg);
+    else if (g.writes_params || g.needs_prefilter)
+        s->prefilter.valid = false;
     s->prep = g.prep;
     if (s->timing && !g.timed.empty()) {
         // graph captured with stage timing: its event nodes bracket each stage

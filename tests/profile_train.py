@@ -1,0 +1,37 @@
+"""ncu driver for the pipelined training step (C2): a few steps of
+gpk_train_step_next through the C-ABI, no timing."""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import paper_2603_20611_b200 as gp  # noqa: E402
+from paper_2603_20611_b200 import _native as N  # noqa: E402
+
+
+def main():
+    steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    dims = (512, 512, 128)
+    lo, hi = (-0.5, -0.5, -0.5), (511.5, 511.5, 127.5)
+    gs = gp.init_random(1_000_000, lo, hi, 1.5, 1)
+    s = gp.Session(0)
+    s.set_gaussians(gp.GaussianSet(gs.records.astype(np.float32).astype(np.float64), lo, hi))
+    s.reserve_pairs(1 << 20)
+    psf, cfg = gp.PsfSpec(), gp.RasterConfig()
+    poses = [gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), 64 + i) for i in range(4)]
+    tgt = np.random.default_rng(7).uniform(0, 0.1, (512, 512)).astype(np.float32)
+    s.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
+    lr = gp.LearningRates(6e-4, 0.02, 2e-3, 1e-3)
+    for i in range(steps):
+        s.train_step(poses[i % 4], psf, cfg, 0.2, 0.5, lr, 30000, next_pose=poses[(i + 1) % 4])
+    s.synchronize()
+    print("ok", s.prepared_count())
+
+
+if __name__ == "__main__":
+    main()

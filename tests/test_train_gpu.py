@@ -230,3 +230,46 @@ def test_train_graph_replay_equals_direct(gp, session):
             s2.graph_launch(gids[it % 2])
             assert np.array_equal(session.get_gaussians(), s2.get_gaussians()), it
         s2.graph_destroy_all()
+
+
+def test_pipelined_train_step_bitwise_equals_plain(gp, session):
+    """gpk_train_step_next (Adam fused with the next slice's cull) leaves exactly
+    the parameters, moments and gradients of gpk_train_step, also when other
+    calls in between force the next step to cull again, and through graphs."""
+    from paper_2603_20611_b200 import _native as N
+
+    dims = (64, 48, 12)
+    lo, hi = (-0.5, -0.5, -0.5), (63.5, 47.5, 11.5)
+    gs = gp.GaussianSet(f32(gp.init_random(3000, lo, hi, 1.5, 4).records), lo, hi)
+    poses = [gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), k) for k in (3, 6, 8, 5)]
+    psf, rc = gp.PsfSpec(), gp.RasterConfig()
+    tgt = np.random.default_rng(9).uniform(0, 0.1, (48, 64)).astype(np.float32)
+    lr0 = gp.LearningRates(6e-4, 0.02, 2e-3, 1e-3)
+    with gp.Session(0) as s2:
+        for s in (session, s2):
+            s.set_gaussians(gs)
+            s.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
+        for it in range(8):
+            k, nk = it % 4, (it + 1) % 4
+            session.train_step(poses[k], psf, rc, 0.2, 0.5, lr0, 40)
+            s2.train_step(poses[k], psf, rc, 0.2, 0.5, lr0, 40, next_pose=poses[nk])
+            if it == 3:  # anything touching the gradients in between: the next step culls again
+                g = s2.get_gradients()
+                s2.set_gradients(g)
+                session.set_gradients(g)
+            assert np.array_equal(session.get_gaussians(), s2.get_gaussians()), it
+            m1, v1, st1 = session.adam_state()
+            m2, v2, st2 = s2.adam_state()
+            assert st1 == st2 and np.array_equal(m1, m2) and np.array_equal(v1, v2), it
+        # graphs: each pose's graph culls the next one
+        gids = [s2.capture_train(poses[k], psf, rc, 0.2, 0.5, lr0, 40, next_pose=poses[(k + 1) % 4])
+                for k in range(4)]
+        for it in range(8, 14):
+            k = it % 4
+            session.train_step(poses[k], psf, rc, 0.2, 0.5, lr0, 40)
+            s2.graph_launch(gids[k])
+            assert np.array_equal(session.get_gaussians(), s2.get_gaussians()), it
+        s2.graph_launch(gids[1])  # out of order: the graph culls its own slice first
+        session.train_step(poses[1], psf, rc, 0.2, 0.5, lr0, 40)
+        assert np.array_equal(session.get_gaussians(), s2.get_gaussians())
+        s2.graph_destroy_all()

@@ -130,26 +130,30 @@ __device__ __forceinline__ void load_params(const float* __restrict__ params, ui
 // Undecided items take the full test, compacted, so the warp does not pay it
 // for every Gaussian.
 __device__ __forceinline__ bool quick_culled_identity(const float p[11], const FilterConsts& c) {
+    // Branch-free (the four items of a lane interleave): the guards are folded
+    // into the result with bitwise ANDs instead of early returns.
     // NaN/Inf guard: log-scales (fmaxf/fminf drop NaN), mu_z and alpha_raw
     // (fminf drops NaN) explicitly; mu_x/y propagate into the final compare
     // (false -> not culled) and the quaternion fails the norm range test.
-    if (!isfinite(((p[2] + p[3]) + (p[4] + p[5])) + p[10])) return false;
+    const bool fin = isfinite(((p[2] + p[3]) + (p[4] + p[5])) + p[10]);
     const float lmax = fmaxf(p[3], fmaxf(p[4], p[5])), lmin = fminf(p[3], fminf(p[4], p[5]));
-    if (!(lmax < 40.f && lmin > -40.f && lmax - lmin < 6.2f)) return false;
+    const bool scales_ok = (lmax < 40.f) & (lmin > -40.f) & (lmax - lmin < 6.2f);
     const float qn2 = __fmaf_rn(p[6], p[6], __fmaf_rn(p[7], p[7], __fmaf_rn(p[8], p[8], p[9] * p[9])));
-    if (!(qn2 > 1e-20f && qn2 < 1e20f)) return false;
+    const bool quat_ok = (qn2 > 1e-20f) & (qn2 < 1e20f);
     const float mcz = (p[2] + c.tz_hi) + c.tz_lo;
     const float mcx = p[0] + c.tx, mcy = p[1] + c.ty;
     const float mu2 = __fmaf_rn(mcx, mcx, __fmaf_rn(mcy, mcy, mcz * mcz));
     // e^(2 lmax) mod^2 = (mod s_max)^2 ; e^(-2 lmin) / mod^2 = 1 / (mod s_min)^2
-    const float den_hi = __fmaf_rn(__expf(2.f * lmax) * c.mod2, 1.0002f, c.sz2);
-    const float inv_smin2 = __expf(-2.f * lmin) * c.inv_mod2 * 1.0002f;
+    // (the clamps only keep the exponentials finite where the guards reject)
+    const float den_hi = __fmaf_rn(__expf(2.f * fminf(lmax, 40.f)) * c.mod2, 1.0002f, c.sz2);
+    const float inv_smin2 = __expf(-2.f * fmaxf(lmin, -40.f)) * c.inv_mod2 * 1.0002f;
     const float thresh_hi = fminf(p[10], 0.f) - c.log_tau;
     const float noise = __fmaf_rn(2e-14f * mu2, inv_smin2,
                                   4.8e-7f * fabsf(mcz) * (fabsf(p[2]) + fabsf(c.tz_hi)) * c.inv_sz2 * 1.0002f);
     const float x = thresh_hi + (2e-3f + __fmaf_rn(2e-5f, fabsf(thresh_hi) + 0.7f, noise));
     const float x_up = __fmaf_rn(1e-3f, fabsf(x) + noise, x) + 1e-6f;
-    return 0.5f * mcz * mcz > x_up * (x_up >= 0.f ? den_hi : c.sz2);
+    const bool culled = 0.5f * mcz * mcz > x_up * (x_up >= 0.f ? den_hi : c.sz2);
+    return fin & scales_ok & quat_ok & culled;
 }
 
 // ---- K_filter ------------------------------------------------------------------
@@ -198,29 +202,95 @@ __device__ __forceinline__ FilterConsts filter_consts(const SliceArgs& sl, float
     return fc;
 }
 
+// Per-warp scratch of cull_chunk: the undecided Gaussians (lane*4 + item) and
+// the full test's verdicts (one ballot word per 32); register-fed callers also
+// copy the undecided parameters here (plane-major).
+struct CullIdx {
+    uint8_t idx[kFilterBlock];
+    unsigned res[kFilterBlock / 32];
+};
+struct CullScratch {
+    CullIdx x;
+    float p[11][kFilterBlock];
+};
+
 // Cull one warp chunk (128 consecutive Gaussians, 4 per lane in v[]) and
 // compact its candidates in set order (lanes in order, each lane's 4 in order)
 // into 48 B CandParams records at slots [b*128, b*128 + count_b). Whole warp.
+// The quick test runs on all 128; the Gaussians it leaves undecided (about 1
+// in 10 at C2) are compacted so the full test runs in ceil(U/32) warp rounds
+// instead of once per lane item. `staged` (plane-major [11][128], the chunk in
+// shared memory) supplies their parameters; else they are copied to sc.p.
 __device__ __forceinline__ void cull_chunk(const PrepLaunch& a, const FilterConsts& fc, float log_tau, int filter_on,
-                                           unsigned b, uint32_t i0, const float4 v[11]) {
+                                           unsigned b, uint32_t i0, const float4 v[11], CullIdx& sx,
+                                           float (*sp)[kFilterBlock], const float* staged) {
     const int lane = threadIdx.x & 31;
     const bool ident = a.slice.identity_rot != 0;
-    unsigned cmask = 0;
+    // items inside the set: all candidates with the cull off, else undecided
+    // unless the quick test culls them (identity poses only)
+    const unsigned inset = i0 >= a.n ? 0u : (a.n - i0 >= kFilterItems ? (1u << kFilterItems) - 1 : (1u << (a.n - i0)) - 1);
+    unsigned cmask = filter_on ? 0u : inset, umask = filter_on ? inset : 0u;
+    if (filter_on && ident) {
+        unsigned qmask = 0;
 #pragma unroll
-    for (int k = 0; k < kFilterItems; ++k) {
-        if (i0 + k >= a.n) continue;
-        float p[11];
+        for (int k = 0; k < kFilterItems; ++k) {
+            float p[11];
 #pragma unroll
-        for (int q = 0; q < 11; ++q) p[q] = (&v[q].x)[k];
-        bool cand = true;
-        if (filter_on) {
-            if (ident && quick_culled_identity(p, fc)) {
-                cand = false;
-            } else {
-                cand = ident ? !certainly_culled_identity(p, fc) : !certainly_culled(p, a.slice, log_tau, fc.mod, fc.sz2);
-            }
+            for (int q = 0; q < 11; ++q) p[q] = (&v[q].x)[k];
+            qmask |= (quick_culled_identity(p, fc) ? 1u : 0u) << k;
         }
-        cmask |= (cand ? 1u : 0u) << k;
+        umask &= ~qmask;
+    }
+    const unsigned nu = __popc(umask);
+    unsigned uincl = nu;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned u = __shfl_up_sync(0xffffffffu, uincl, o);
+        if (lane >= o) uincl += u;
+    }
+    const unsigned U = __shfl_sync(0xffffffffu, uincl, 31);
+    if (U) {
+        unsigned pos = uincl - nu;
+#pragma unroll
+        for (int k = 0; k < kFilterItems; ++k)
+            if (umask & (1u << k)) {
+                if (staged) {
+                    sx.idx[pos] = (uint8_t)(lane * kFilterItems + k);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 11; ++q) sp[q][pos] = (&v[q].x)[k];
+                }
+                ++pos;
+            }
+        __syncwarp();
+        for (unsigned r = 0; r * 32 < U; ++r) {
+            const unsigned e = r * 32 + lane;
+            bool cand = false;
+            if (e < U) {
+                float p[11];
+                if (staged) {
+                    const unsigned j = sx.idx[e];
+#pragma unroll
+                    for (int q = 0; q < 11; ++q) p[q] = staged[q * kFilterBlock + j];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 11; ++q) p[q] = sp[q][e];
+                }
+                cand = ident ? !certainly_culled_identity(p, fc)
+                             : !certainly_culled(p, a.slice, log_tau, fc.mod, fc.sz2);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, cand);
+            if (lane == 0) sx.res[r] = bal;
+        }
+        __syncwarp();
+        pos = uincl - nu;
+#pragma unroll
+        for (int k = 0; k < kFilterItems; ++k)
+            if (umask & (1u << k)) {
+                if ((sx.res[pos >> 5] >> (pos & 31)) & 1u) cmask |= 1u << k;
+                ++pos;
+            }
+        __syncwarp();  // the scratch is reused by the warp's next chunk
     }
     const unsigned nc = __popc(cmask);
     unsigned incl = nc;
@@ -243,16 +313,49 @@ __device__ __forceinline__ void cull_chunk(const PrepLaunch& a, const FilterCons
     }
 }
 
+// cp.async (16 B, L1 bypass) staging of K_filter chunks: each lane copies its
+// own 4 Gaussians' 11 plane slices; one commit group per chunk.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+constexpr int kFilterStages = 2;
+constexpr size_t kFilterStageFloats = 11 * kFilterBlock;  // one warp chunk, plane-major
+constexpr size_t kFilterSmem =
+    (size_t)(kFilterThreads / 32) * (kFilterStages * kFilterStageFloats * 4 + sizeof(CullIdx));
+
+// Each warp streams its chunks (grid-stride) through a 2-stage cp.async ring:
+// chunk b+1's 5.6 KB is in flight while chunk b is culled, so HBM never waits
+// for the cull arithmetic (a register-fed loop leaves the memory idle between
+// its load bursts: ~2 chunks per warp at C2).
 template <bool kZeroGrads>
-__global__ void __launch_bounds__(kFilterThreads) k_filter(const PrepLaunch a, float log_tau, int filter_on) {
+__global__ void __launch_bounds__(kFilterThreads, 2) k_filter(const PrepLaunch a, float log_tau, int filter_on) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    const int tid = threadIdx.x, lane = tid & 31;
+    extern __shared__ __align__(16) float s_filter[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float* ring = s_filter + (size_t)warp * kFilterStages * kFilterStageFloats;
+    CullIdx& sx = reinterpret_cast<CullIdx*>(s_filter + (size_t)(kFilterThreads / 32) * kFilterStages *
+                                                             kFilterStageFloats)[warp];
     const unsigned nchunks = a.nfilter;
-    const unsigned dirty = kZeroGrads ? *a.grads_dirty : 0u;
-    const bool dense_zero = kZeroGrads && dirty == kGradsDense;
     const unsigned gthreads = gridDim.x * kFilterThreads;
     const unsigned gtid = blockIdx.x * kFilterThreads + tid;
+    const unsigned gwarps = gthreads / 32;
+    auto prefetch = [&](unsigned b, int stage) {
+        // cap is a multiple of kParamAlign: the chunk never leaves the plane
+        const float* src = a.params + (uint64_t)b * kFilterBlock + lane * kFilterItems;
+        float* dst = ring + stage * kFilterStageFloats + lane * kFilterItems;
+#pragma unroll
+        for (int q = 0; q < 11; ++q) cp_async16(dst + q * kFilterBlock, src + (uint64_t)q * a.cap);
+    };
+    unsigned b = gtid / 32;
+    if (b < nchunks) prefetch(b, 0);
+    cp_async_commit();
 
+    const unsigned dirty = kZeroGrads ? *a.grads_dirty : 0u;
+    const bool dense_zero = kZeroGrads && dirty == kGradsDense;
     clear_prev_sort_rows(a, gtid, gthreads);
     if (kZeroGrads && !dense_zero)  // the previous survivors' gradients (sparse mode)
         for (unsigned e = gtid; e < dirty; e += gthreads) {
@@ -262,18 +365,22 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(const PrepLaunch a, f
         }
     const FilterConsts fc = filter_consts(a.slice, log_tau);
 
-    const unsigned gwarps = gthreads / 32;
-    for (unsigned b = gtid / 32; b < nchunks; b += gwarps) {
+    for (int it = 0; b < nchunks; ++it, b += gwarps) {
+        if (b + gwarps < nchunks) prefetch(b + gwarps, (it + 1) & 1);
+        cp_async_commit();
+        cp_async_wait1();  // this lane's copies of chunk b landed
+        __syncwarp();      // ... and every lane's (the full test reads other lanes' Gaussians)
+        const float* st = ring + (it & 1) * kFilterStageFloats;
         const uint32_t i0 = b * kFilterBlock + lane * kFilterItems;  // this lane's first Gaussian
-        // cap is a multiple of kParamAlign: the 16 B load never leaves the plane
         float4 v[11];
 #pragma unroll
-        for (int q = 0; q < 11; ++q) v[q] = __ldcs(reinterpret_cast<const float4*>(a.params + (uint64_t)q * a.cap + i0));
+        for (int q = 0; q < 11; ++q) v[q] = *reinterpret_cast<const float4*>(st + q * kFilterBlock + lane * kFilterItems);
         if (dense_zero)
 #pragma unroll
             for (int q = 0; q < 11; ++q)
                 *reinterpret_cast<float4*>(a.grads + (uint64_t)q * a.cap + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
-        cull_chunk(a, fc, log_tau, filter_on, b, i0, v);
+        cull_chunk(a, fc, log_tau, filter_on, b, i0, v, sx, nullptr, st);
+        __syncwarp();  // stage (it & 1) is refilled by the next iteration's prefetch
     }
 }
 
@@ -285,10 +392,11 @@ __global__ void __launch_bounds__(kFilterThreads) k_filter(const PrepLaunch a, f
 // stand-alone Adam kernel), clears the gradients it consumed where they were
 // non-zero (the survivors: the dense gradient is exactly zero again), then its
 // warp culls the 128 updated primitives against the next pose (cull_chunk).
-__global__ void __launch_bounds__(256) k_adam_cull(const AdamLaunch a, const PrepLaunch f, float log_tau,
+__global__ void __launch_bounds__(256, 3) k_adam_cull(const AdamLaunch a, const PrepLaunch f, float log_tau,
                                                    int filter_on) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ AdamConsts s_c;
+    __shared__ CullScratch s_cull[8];
     const bool adam_on = !(a.ctrl && a.ctrl->pair_overflow);  // the slice overflowed: no update
     if (threadIdx.x == 0) adam_consts(a, s_c);
     __syncthreads();
@@ -319,7 +427,10 @@ __global__ void __launch_bounds__(256) k_adam_cull(const AdamLaunch a, const Pre
         for (int d = 0; d < 11; ++d) p[d] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const unsigned b = i0 / kFilterBlock;  // the warp's chunk
-    if (b < f.nfilter) cull_chunk(f, filter_consts(f.slice, log_tau), log_tau, filter_on, b, i0, p);
+    if (b < f.nfilter) {
+        CullScratch& sc = s_cull[threadIdx.x >> 5];
+        cull_chunk(f, filter_consts(f.slice, log_tau), log_tau, filter_on, b, i0, p, sc.x, sc.p, nullptr);
+    }
     if (adam_on) adam_finish(a);
 }
 
@@ -955,15 +1066,17 @@ void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st) {
     const float log_tau = filter_on ? (float)log(a.slice.tau) : 0.f;
     static int per_sm = 0;
     if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<true>, kFilterThreads, 0);
+        cudaFuncSetAttribute(k_filter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFilterSmem);
+        cudaFuncSetAttribute(k_filter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFilterSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<true>, kFilterThreads, kFilterSmem);
         if (per_sm < 1) per_sm = 1;
     }
     const uint64_t need = ((uint64_t)a.nfilter * 32 + kFilterThreads - 1) / kFilterThreads;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms * per_sm));
     if (a.grads)
-        launch_pdl(k_filter<true>, dim3(grid), dim3(kFilterThreads), 0, st, a, log_tau, filter_on ? 1 : 0);
+        launch_pdl(k_filter<true>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, filter_on ? 1 : 0);
     else
-        launch_pdl(k_filter<false>, dim3(grid), dim3(kFilterThreads), 0, st, a, log_tau, filter_on ? 1 : 0);
+        launch_pdl(k_filter<false>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, filter_on ? 1 : 0);
 }
 
 void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& f, cudaStream_t st) {

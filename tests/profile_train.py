@@ -1,5 +1,6 @@
-"""ncu driver for the pipelined training step (C2): a few steps of
-gpk_train_step_next through the C-ABI, no timing."""
+"""ncu driver for the training step (C2): a few steps of gpk_train_step_next
+(argv[2] == "plain": gpk_train_step, Adam as its own kernel) through the
+C-ABI, no timing."""
 from __future__ import annotations
 
 import sys
@@ -16,6 +17,7 @@ from paper_2603_20611_b200 import _native as N  # noqa: E402
 
 def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    pipelined = not (len(sys.argv) > 2 and sys.argv[2] == "plain")
     dims = (512, 512, 128)
     lo, hi = (-0.5, -0.5, -0.5), (511.5, 511.5, 127.5)
     gs = gp.init_random(1_000_000, lo, hi, 1.5, 1)
@@ -28,7 +30,7 @@ def main():
     s.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
     lr = gp.LearningRates(6e-4, 0.02, 2e-3, 1e-3)
     for i in range(steps):
-        s.train_step(poses[i % 4], psf, cfg, 0.2, 0.5, lr, 30000, next_pose=poses[(i + 1) % 4])
+        s.train_step(poses[i % 4], psf, cfg, 0.2, 0.5, lr, 30000, next_pose=poses[(i + 1) % 4] if pipelined else None)
     s.synchronize()
     print("ok", s.prepared_count())
 

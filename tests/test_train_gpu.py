@@ -273,3 +273,49 @@ def test_pipelined_train_step_bitwise_equals_plain(gp, session):
         session.train_step(poses[1], psf, rc, 0.2, 0.5, lr0, 40)
         assert np.array_equal(session.get_gaussians(), s2.get_gaussians())
         s2.graph_destroy_all()
+
+
+def test_gradient_layouts_interleave(gp, session):
+    """The dense gradient planes stay exact across mixed calls: a dense backward
+    after training steps (plain and pipelined, the latter skipping K_filter),
+    training steps after a dense backward (the stale entries are cleared), and
+    gpk_get_gradients after a plain step equals the staged composition's."""
+    from paper_2603_20611_b200 import _native as N
+
+    dims = (64, 48, 12)
+    lo, hi = (-0.5, -0.5, -0.5), (63.5, 47.5, 11.5)
+    gs = gp.GaussianSet(f32(gp.init_random(3000, lo, hi, 1.5, 5).records), lo, hi)
+    poses = [gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), k) for k in (2, 9, 5)]
+    psf, rc = gp.PsfSpec(), gp.RasterConfig()
+    tgt = np.random.default_rng(11).uniform(0, 0.1, (48, 64)).astype(np.float32)
+    dl = np.random.default_rng(12).normal(0, 1e-3, (48, 64)).astype(np.float32)
+    lr0 = gp.LearningRates(6e-4, 0.02, 2e-3, 1e-3)
+
+    def fresh_backward(params, pose):
+        with gp.Session(0) as f:
+            f.set_gaussians(gp.GaussianSet(params.astype(np.float64), lo, hi))
+            f.prepare(pose, psf, rc)
+            return f.backward(dl)
+
+    session.set_gaussians(gs)
+    session.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
+    session.prepare(poses[0], psf, rc)
+    session.backward(dl)  # dense gradients of slice 0 pending a clear
+    session.train_step(poses[1], psf, rc, 0.2, 0.5, lr0, 40, next_pose=poses[2])
+    session.train_step(poses[2], psf, rc, 0.2, 0.5, lr0, 40)  # prefiltered: no K_filter
+    # the staged step on the same parameters gives the same dense gradient
+    before = session.get_gaussians()
+    session.prepare(poses[0], psf, rc)
+    g = session.backward(dl)
+    assert np.array_equal(g, fresh_backward(before, poses[0]))
+    # gradients read after a step equal the staged composition's
+    with gp.Session(0) as s2:
+        s2.set_gaussians(gp.GaussianSet(before.astype(np.float64), lo, hi))
+        s2.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
+        s2.adam_reset()
+        session.adam_reset()
+        session.train_step(poses[1], psf, rc, 0.2, 0.5, lr0, 40)
+        s2.prepare(poses[1], psf, rc)
+        s2.rasterize()
+        _, dl2 = s2.photometric_loss(tgt, 0.2, 0.5)
+        assert np.array_equal(session.get_gradients(), s2.backward(dl2))

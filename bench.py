@@ -501,9 +501,14 @@ def run_ours(args):
         "chain": ("k_chain", 48 * S + 48 * S + 24 * T + 44 * S + 4 * S,
                   "48S records + 48S params + 24T partials + 44S grads + 4S dirty list"),
         "loss": ("k_ssim_fwd", 20 * P, "8P images + 12P SSIM partials (the backward half runs in k_raster_bwd)"),
-        "adam": ("k_adam_cull", 308 * n + 48 * Cc,
-                 "308N: read params, grads, m, v; write params, m, v + 48C next-slice candidates")
-        if (u2 and args.pipeline) else ("k_adam", 308 * n, "308N: read params, grads, m, v; write params, m, v"),
+        # slot-gradient Adam (single-GPU step): the survivors' gradients by slot
+        # + a 2 B map per primitive instead of 44 B dense gradient planes
+        "adam": ("k_adam_cull", 266 * n + 44 * S + 48 * Cc,
+                 "266N + 44S: read params, m, v, 2 B slot map; write params, m, v; survivor gradients "
+                 "+ 48C next-slice candidates")
+        if (u2 and args.pipeline) else
+        ("k_adam", 266 * n + 44 * S,
+         "266N + 44S: read params, m, v, 2 B slot map; write params, m, v; survivor gradients"),
     }
     measured = {k: v for k, v in stages.items() if v[1] > 0 and k in kernel_bytes}
     dom = max(measured, key=lambda k: measured[k][0])
@@ -520,7 +525,10 @@ def run_ours(args):
         kn, kb, _ = kernel_bytes[k]
         ms = ms_tot / cnt
         per_kernel[kn] = {"ms": ms, "gbs": kb / (ms * 1e-3) / 1e9, "frac": kb / (ms * 1e-3) / 1e9 / peak}
-    step_bytes = (396 * n + 8 * P) if u2 else (88 * n + 8 * P)
+    # U2 floor with slot gradients: 44N cull read + 264N Adam (p, m, v read and
+    # written) + 2N slot map (SURVEY.md §8d's 396N assumed dense gradient
+    # planes: +44N Adam read, +44N clear)
+    step_bytes = (310 * n + 8 * P) if u2 else (88 * n + 8 * P)
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
 
     line = {
@@ -530,7 +538,8 @@ def run_ours(args):
         "data": data_note(args.unit), "config": config_json(args, cfg, world),
         "roofline": roof,
         "step_roofline": {"bytes_per_step": step_bytes, "achieved_gbs": step_gbs, "frac": step_gbs / peak,
-                          "formula": ("396N + 8P (U2, SURVEY.md §8d)" if u2 else "88N + 8P (U1, SURVEY.md §8d)")},
+                          "formula": ("310N + 8P (U2 with slot gradients; SURVEY.md §8d: 396N dense)" if u2
+                                      else "88N + 8P (U1, SURVEY.md §8d)")},
         "stage_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in stages.items() if v[1]},
         "kernels": per_kernel,
         "submission": "CUDA graph per slice pose" if graphs is not None else "kernel by kernel",

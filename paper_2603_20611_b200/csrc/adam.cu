@@ -1,47 +1,84 @@
 // adam.cu — fused Adam step over all N primitives (adam_step, optimize.hpp:195-221).
 //
-// One thread per 4 consecutive primitives walks the 11 parameter planes with
-// 16 B accesses: read p, g, m, v and write p, m, v (308 B/primitive: the HBM
-// roofline of the kernel). Order of
-// the reference is kept: position update then bbox clamp (:212), log-scale,
-// quaternion update then renormalisation when the norm is > 0 (:216-217),
-// raw alpha. The step counter lives on the device; bias corrections and the
-// lr_at schedule (optimize.hpp:71-73) are evaluated once per CTA in fp64, so
-// a whole training step can be captured in a CUDA graph.
+// k_adam_consts (one thread) evaluates the step's bias corrections and the
+// lr_at schedule (optimize.hpp:71-73) in fp64 from the device step counter and
+// advances it, so a whole training step can be captured in a CUDA graph and
+// the update kernel needs no CTA barrier. k_adam: each thread walks the 11
+// parameter planes of 2 consecutive primitives with 8 B accesses, storing each
+// plane as soon as it is final (few live registers: 6 CTAs per SM keep enough
+// requests in flight). Bytes: read p, g, m, v and write p, m, v = 308 B per
+// primitive; in slot-gradient mode (the training step, see AdamLaunch) the
+// gradient comes from the survivors' slots: 266 B per primitive + 44 B per
+// survivor. The reference's order is kept: position update then bbox clamp
+// (:212), log-scale, raw alpha, quaternion update then renormalisation when
+// the norm is > 0 (:216-217).
 #include "adam.cuh"
-
-#ifndef ADAM_ITEMS
-#define ADAM_ITEMS 4
-#endif
 
 namespace gpk {
 
 namespace {
 
-constexpr int kAdamItems = ADAM_ITEMS;  // consecutive primitives per thread (one vector access per plane)
+constexpr int kAdamItems = 2;
 
-__global__ void __launch_bounds__(256) k_adam(const AdamLaunch a) {
+__global__ void k_adam_consts(const AdamLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    __shared__ AdamConsts s_c;
-    if (a.ctrl && a.ctrl->pair_overflow) return;
-    if (threadIdx.x == 0) adam_consts(a, s_c);
-    __syncthreads();
-    const AdamConsts c = s_c;
+    if (threadIdx.x != 0 || (a.ctrl && a.ctrl->pair_overflow)) return;  // overflowed slice: no step
+    AdamConsts c;
+    adam_consts(a, c);
+    *a.consts = c;
+    *a.step += 1;
+}
+
+template <bool kSlots>
+__global__ void __launch_bounds__(256, 6) k_adam(const AdamLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * kAdamItems;
-    if (i0 < a.n) {  // the capacity is a multiple of 512: vector accesses stay in the plane
-        Pack<kAdamItems> p[11];
-        unsigned nz;
-        adam_update<kAdamItems>(a, c, i0, p, nz);
-        adam_store<kAdamItems>(a, i0, p);
+    if (i0 >= a.n) return;  // the capacity is a multiple of 512: vector accesses stay in the plane
+    if (a.ctrl && a.ctrl->pair_overflow) {  // the slice overflowed: no update
+        if (kSlots) adam_slots_clear<kAdamItems>(a, i0);
+        return;
     }
-    adam_finish(a);
+    const AdamConsts c = *a.consts;
+    uint32_t gslot[kAdamItems];
+    const bool any = kSlots && adam_slots<kAdamItems>(a, i0, gslot);
+    adam_update_store<kAdamItems>(a, c, i0, kSlots ? gslot : nullptr);
+    if (any) adam_slots_clear<kAdamItems>(a, i0);
+}
+
+// Slot gradients -> dense planes (gpk_get_gradients after a training step;
+// the dense planes were zeroed before) and/or clearing the survivors' map
+// entries (a slot backward no Adam consumed). CTA per K_decide group.
+__global__ void __launch_bounds__(256) k_scatter_slots(const AdamLaunch a, int grads) {
+    const unsigned g = blockIdx.x;
+    const unsigned S = a.grp_surv[g];
+    for (unsigned j = threadIdx.x; j < S; j += blockDim.x) {
+        const uint32_t slot = g * kDecideGroupSize + j, i = a.surv_gidx[slot];
+        if (grads)
+#pragma unroll
+            for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = a.slot_grads[(uint64_t)k * a.cap + slot];
+        else
+            a.gmap[i] = 0;
+    }
 }
 
 }  // namespace
 
+void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, bool grads, cudaStream_t st) {
+    if (ngroups) k_scatter_slots<<<ngroups, 256, 0, st>>>(a, grads ? 1 : 0);
+}
+
+void launch_adam_consts(const AdamLaunch& a, cudaStream_t st) {
+    launch_pdl(k_adam_consts, dim3(1), dim3(32), 0, st, a);
+}
+
 void launch_adam(const AdamLaunch& a, cudaStream_t st) {
+    launch_adam_consts(a, st);
+    // 2 primitives per thread, registers capped for 6 CTAs per SM: measured
+    // best on B200 among 1/2/4 items per thread, persistent grid or not
     const unsigned grid = (a.n + 256 * kAdamItems - 1) / (256 * kAdamItems);
-    if (grid) launch_pdl(k_adam, dim3(grid), dim3(256), 0, st, a);
+    if (!grid) return;
+    if (a.slot_grads) launch_pdl(k_adam<true>, dim3(grid), dim3(256), 0, st, a);
+    else launch_pdl(k_adam<false>, dim3(grid), dim3(256), 0, st, a);
 }
 
 }  // namespace gpk

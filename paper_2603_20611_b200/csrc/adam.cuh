@@ -10,14 +10,8 @@
 
 namespace gpk {
 
-// Per-launch constants, evaluated once per CTA by thread 0 (fp64, then f32):
-// bias corrections of step+1 and the lr_at schedule (optimize.hpp:71-73).
-struct AdamConsts {
-    float b1, b2, ib1, ib2;   // beta1, beta2, 1 - beta1, 1 - beta2
-    float ibc1, isbc2, eps;   // 1 / bc1, 1 / sqrt(bc2), eps
-    float lr[4];              // position, opacity, scale, rotation
-};
-
+// Per-step constants, evaluated once by k_adam_consts (fp64, then f32): bias
+// corrections of step+1 and the lr_at schedule (optimize.hpp:71-73).
 __device__ __forceinline__ void adam_consts(const AdamLaunch& a, AdamConsts& c) {
     const long long step = *a.step + 1;
     const double bc1 = 1.0 - pow(a.beta1, (double)step);
@@ -84,14 +78,61 @@ __device__ __forceinline__ float adam_delta(const AdamConsts& c, float lrc, floa
     return __fdividef(__fmul_rn(lrc, m), __fmaf_rn(sq, c.isbc2, c.eps));
 }
 
+// Where a thread's N gradients come from: the dense planes at i0 (gslot ==
+// nullptr), or per primitive a survivor slot (kNoSlot: zero gradient).
+constexpr uint32_t kNoSlot = 0xffffffffu;
+
+template <int N>
+__device__ __forceinline__ Pack<N> adam_grad(const AdamLaunch& a, int k, uint32_t i0, const uint32_t* gslot) {
+    if (!gslot) return ldp_stream<N>(a.grads + (uint64_t)k * a.cap + i0);
+    Pack<N> g;
+#pragma unroll
+    for (int l = 0; l < N; ++l)
+        g.v[l] = gslot[l] != kNoSlot ? __ldcs(a.slot_grads + (uint64_t)k * a.cap + gslot[l]) : 0.f;
+    return g;
+}
+
+// Slot-gradient mode (AdamLaunch::slot_grads): the survivor slots of primitives
+// i0 .. i0+N-1 from the chain's map (1 + offset within the K_decide group, 0
+// for a non-survivor). Returns whether any is a survivor: the caller then
+// clears those map entries (adam_slots_clear) so the map is zero again.
+template <int N>
+__device__ __forceinline__ bool adam_slots(const AdamLaunch& a, uint32_t i0, uint32_t gslot[N]) {
+    uint16_t m[N];
+    if constexpr (N == 4) {
+        const uint2 t = *reinterpret_cast<const uint2*>(a.gmap + i0);
+        m[0] = (uint16_t)(t.x & 0xffffu), m[1] = (uint16_t)(t.x >> 16), m[2] = (uint16_t)(t.y & 0xffffu),
+        m[3] = (uint16_t)(t.y >> 16);
+    } else if constexpr (N == 2) {
+        const unsigned t = *reinterpret_cast<const unsigned*>(a.gmap + i0);
+        m[0] = (uint16_t)(t & 0xffffu), m[1] = (uint16_t)(t >> 16);
+    } else {
+        m[0] = a.gmap[i0];
+    }
+    const uint32_t gbase = i0 / kDecideGroupSize * kDecideGroupSize;  // N divides the group size
+    bool any = false;
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+        gslot[l] = m[l] ? gbase + m[l] - 1 : kNoSlot;
+        any |= m[l] != 0;
+    }
+    return any;
+}
+template <int N>
+__device__ __forceinline__ void adam_slots_clear(const AdamLaunch& a, uint32_t i0) {
+    if constexpr (N == 4) *reinterpret_cast<uint2*>(a.gmap + i0) = make_uint2(0u, 0u);
+    else if constexpr (N == 2) *reinterpret_cast<unsigned*>(a.gmap + i0) = 0u;
+    else a.gmap[i0] = 0;
+}
+
 // One parameter plane of N consecutive primitives: moments updated and stored,
 // the stepped parameters returned (before clamp / renormalisation); nz collects
 // which primitives had a non-zero gradient.
 template <int N>
 __device__ __forceinline__ Pack<N> adam_plane(const AdamLaunch& a, const AdamConsts& c, int k, float lr, uint32_t i0,
-                                              unsigned& nz) {
+                                              const uint32_t* gslot, unsigned& nz) {
     const uint64_t o = (uint64_t)k * a.cap + i0;
-    const Pack<N> g = ldp_stream<N>(a.grads + o);
+    const Pack<N> g = adam_grad<N>(a, k, i0, gslot);
     Pack<N> m = ldp<N>(a.m + o), v = ldp<N>(a.v + o), p = ldp<N>(a.params + o);
     const float lrc = __fmul_rn(lr, c.ibc1);
 #pragma unroll
@@ -109,23 +150,23 @@ __device__ __forceinline__ Pack<N> adam_plane(const AdamLaunch& a, const AdamCon
 // All 11 planes of N consecutive primitives in the reference's order: position
 // then the bbox clamp (optimize.hpp:212), log-scale, raw alpha, quaternion then
 // renormalisation when the norm is > 0 (:216-217). p[k] returns the new
-// parameters; nz the primitives with a non-zero gradient.
+// parameters; nz the primitives with a non-zero gradient; gslot as adam_grad.
 template <int N>
-__device__ __forceinline__ void adam_update(const AdamLaunch& a, const AdamConsts& c, uint32_t i0, Pack<N> p[11],
-                                            unsigned& nz) {
+__device__ __forceinline__ void adam_update(const AdamLaunch& a, const AdamConsts& c, uint32_t i0,
+                                            const uint32_t* gslot, Pack<N> p[11], unsigned& nz) {
     nz = 0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        p[d] = adam_plane<N>(a, c, d, c.lr[0], i0, nz);
+        p[d] = adam_plane<N>(a, c, d, c.lr[0], i0, gslot, nz);
         const float lo = a.bbox_min[d], hi = a.bbox_max[d];
 #pragma unroll
         for (int l = 0; l < N; ++l) p[d].v[l] = fminf(hi, fmaxf(lo, p[d].v[l]));
     }
 #pragma unroll
-    for (int d = 3; d < 6; ++d) p[d] = adam_plane<N>(a, c, d, c.lr[2], i0, nz);
-    p[10] = adam_plane<N>(a, c, 10, c.lr[1], i0, nz);
+    for (int d = 3; d < 6; ++d) p[d] = adam_plane<N>(a, c, d, c.lr[2], i0, gslot, nz);
+    p[10] = adam_plane<N>(a, c, 10, c.lr[1], i0, gslot, nz);
 #pragma unroll
-    for (int d = 6; d < 10; ++d) p[d] = adam_plane<N>(a, c, d, c.lr[3], i0, nz);
+    for (int d = 6; d < 10; ++d) p[d] = adam_plane<N>(a, c, d, c.lr[3], i0, gslot, nz);
 #pragma unroll
     for (int l = 0; l < N; ++l) {
         float& w = p[6].v[l];
@@ -143,23 +184,50 @@ __device__ __forceinline__ void adam_update(const AdamLaunch& a, const AdamConst
     }
 }
 
+// As adam_update + adam_store, storing each plane's parameters as soon as they
+// are final (all but the quaternion, renormalised at the end): few registers
+// live, so the stand-alone kernel runs at full occupancy. Same bits.
+template <int N>
+__device__ __forceinline__ void adam_update_store(const AdamLaunch& a, const AdamConsts& c, uint32_t i0,
+                                                  const uint32_t* gslot) {
+    unsigned nz = 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        Pack<N> p = adam_plane<N>(a, c, d, c.lr[0], i0, gslot, nz);
+        const float lo = a.bbox_min[d], hi = a.bbox_max[d];
+#pragma unroll
+        for (int l = 0; l < N; ++l) p.v[l] = fminf(hi, fmaxf(lo, p.v[l]));
+        stp<N>(a.params + (uint64_t)d * a.cap + i0, p);
+    }
+#pragma unroll
+    for (int d = 3; d < 6; ++d) stp<N>(a.params + (uint64_t)d * a.cap + i0, adam_plane<N>(a, c, d, c.lr[2], i0, gslot, nz));
+    stp<N>(a.params + (uint64_t)10 * a.cap + i0, adam_plane<N>(a, c, 10, c.lr[1], i0, gslot, nz));
+    Pack<N> q[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) q[d] = adam_plane<N>(a, c, 6 + d, c.lr[3], i0, gslot, nz);
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+        float& w = q[0].v[l];
+        float& x = q[1].v[l];
+        float& y = q[2].v[l];
+        float& z = q[3].v[l];
+        const float qn = __fsqrt_rn(__fmaf_rn(w, w, __fmaf_rn(x, x, __fmaf_rn(y, y, __fmul_rn(z, z)))));
+        if (qn > 0.f) {
+            const float inv = __frcp_rn(qn);
+            w = __fmul_rn(w, inv);
+            x = __fmul_rn(x, inv);
+            y = __fmul_rn(y, inv);
+            z = __fmul_rn(z, inv);
+        }
+    }
+#pragma unroll
+    for (int d = 0; d < 4; ++d) stp<N>(a.params + (uint64_t)(6 + d) * a.cap + i0, q[d]);
+}
+
 template <int N>
 __device__ __forceinline__ void adam_store(const AdamLaunch& a, uint32_t i0, const Pack<N> p[11]) {
 #pragma unroll
     for (int d = 0; d < 11; ++d) stp<N>(a.params + (uint64_t)d * a.cap + i0, p[d]);
-}
-
-// The last CTA out advances AdamState::step (the kernel's CTAs read it first).
-__device__ __forceinline__ void adam_finish(const AdamLaunch& a) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned done = atomicAdd(a.done_ctr, 1u);
-        if (done == gridDim.x - 1) {
-            *a.step += 1;
-            *a.done_ctr = 0;
-        }
-    }
 }
 
 }  // namespace gpk

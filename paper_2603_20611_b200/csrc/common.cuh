@@ -334,7 +334,7 @@ struct PrepLaunch {
     unsigned* grp_surv;       // per K_decide group: survivors (slots g*4096 + [0, S_g))
     unsigned nfilter;         // 64-Gaussian chunks
     SurvivorRecord* records;  // indexed by candidate slot
-    uint32_t* survivor_list;  // survivor slot -> candidate slot
+    uint32_t* survivor_list;  // survivor slot -> set index (K_decide)
     uint32_t* keys;           // pre-sort tile keys
     uint32_t* vals;           // pre-sort candidate slots
     uint64_t pair_cap;
@@ -427,7 +427,9 @@ struct ChainLaunch {
     const uint32_t* survivor_list;
     const float* partials;
     const Control* ctrl;
-    float* grads;
+    float* grads;                  // dense gradient planes (set-indexed) ...
+    float* slot_grads;             // ... or, when non-null, slot-indexed planes (see AdamLaunch)
+    uint16_t* gmap;                // slot mode: 1 + the survivor's offset in its group, by set index
     float* stat_norm;              // optional (screen-space dL/dmu_2d norm)
     uint8_t* stat_observed;        // optional
     float* stat_world;             // optional, 3 per primitive
@@ -437,6 +439,13 @@ struct ChainLaunch {
     unsigned* dirty_ctr;           // Control::dirty_ctr
     ErrorState* err;
     SliceArgs slice;
+};
+
+// Per-step Adam constants (adam.cuh adam_consts), written by k_adam_consts.
+struct AdamConsts {
+    float b1, b2, ib1, ib2;   // beta1, beta2, 1 - beta1, 1 - beta2
+    float ibc1, isbc2, eps;   // 1 / bc1, 1 / sqrt(bc2), eps
+    float lr[4];              // position, opacity, scale, rotation
 };
 
 struct AdamLaunch {
@@ -452,8 +461,19 @@ struct AdamLaunch {
     int total;
     double beta1, beta2, eps;
     long long* step;      // AdamState::step, device
-    unsigned* done_ctr;
+    AdamConsts* consts;   // this step's constants (k_adam_consts, then the update kernel)
     const Control* ctrl;  // skip when the slice overflowed its pair capacity
+    // Slot-gradient mode (the single-GPU training step): when slot_grads is
+    // non-null the gradients are not read from `grads` but from the chain's
+    // survivor-slot planes (slot g*4096 + j holds group g's j-th survivor);
+    // gmap[i] = 1 + j for a survivor i of group g, 0 for every other primitive
+    // (zero gradient). Adam clears the map entries it reads. Nothing has to
+    // clear dense gradient planes between steps, and Adam reads 2 B per
+    // primitive + 44 B per survivor instead of 44 B per primitive.
+    const float* slot_grads;
+    uint16_t* gmap;
+    const uint32_t* surv_gidx;    // slot -> set index (the gradient scatter)
+    const unsigned* grp_surv;
 };
 
 struct LossLaunch {
@@ -554,6 +574,8 @@ void launch_raster_fwd(const RasterLaunch& a, cudaStream_t st);
 void launch_raster_bwd(const RasterLaunch& a, cudaStream_t st);
 void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st);
 void launch_adam(const AdamLaunch& a, cudaStream_t st);
+void launch_adam_consts(const AdamLaunch& a, cudaStream_t st);
+void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, bool grads, cudaStream_t st);
 void launch_loss(const LossLaunch& a, cudaStream_t st);
 unsigned loss_partial_blocks(int W, int H, double lambda);
 

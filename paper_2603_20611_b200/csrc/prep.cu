@@ -389,39 +389,56 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter(const PrepLaunch a
 // K_filter. Both stream every parameter once; fused, the next step starts at
 // K_decide and the parameters cross HBM once per step instead of twice. Each
 // thread updates 4 consecutive primitives (adam.cuh: the same bits as the
-// stand-alone Adam kernel), clears the gradients it consumed where they were
-// non-zero (the survivors: the dense gradient is exactly zero again), then its
-// warp culls the 128 updated primitives against the next pose (cull_chunk).
+// stand-alone Adam kernel; dense or slot gradients), leaves the dense gradient
+// planes zero, then its warp culls the 128 updated primitives against the next
+// pose (cull_chunk).
 __global__ void __launch_bounds__(256, 3) k_adam_cull(const AdamLaunch a, const PrepLaunch f, float log_tau,
-                                                   int filter_on) {
+                                                      int filter_on) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    __shared__ AdamConsts s_c;
     __shared__ CullScratch s_cull[8];
     const bool adam_on = !(a.ctrl && a.ctrl->pair_overflow);  // the slice overflowed: no update
-    if (threadIdx.x == 0) adam_consts(a, s_c);
-    __syncthreads();
-    const AdamConsts c = s_c;
-    const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    clear_prev_sort_rows(f, gtid, gridDim.x * blockDim.x);
-    if (gtid == 0) *f.grads_dirty = 0u;  // every gradient is zero after this kernel
+    const bool slots = a.slot_grads != nullptr;
+    const AdamConsts c = *a.consts;  // k_adam_consts ran just before
+    const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
+    clear_prev_sort_rows(f, gtid, gthreads);
+    // K_filter's gradient duty. Dense gradients: the Adam below zeroes every
+    // non-zero entry it consumes. Slot gradients: the dense planes are not
+    // consumed, so the pending clear of the last dense backward happens here
+    // (the next K_decide resets the state word).
+    unsigned dirty = 0;
+    if (!slots) {
+        if (gtid == 0) *f.grads_dirty = 0u;
+    } else {
+        dirty = *f.grads_dirty;
+        if (dirty != kGradsDense)
+            for (unsigned e = gtid; e < dirty; e += gthreads) {
+                const uint32_t i = f.dirty_idx[e];
+#pragma unroll
+                for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = 0.f;
+            }
+    }
     const uint32_t i0 = gtid * kFilterItems;
     float4 p[11];
     if (i0 < a.n) {
+        unsigned nz = 0;
         if (adam_on) {
-            unsigned nz;
             Pack<kFilterItems> q[11];
-            adam_update<kFilterItems>(a, c, i0, q, nz);
+            uint32_t gslot[kFilterItems];
+            const bool any = slots && adam_slots<kFilterItems>(a, i0, gslot);
+            adam_update<kFilterItems>(a, c, i0, slots ? gslot : nullptr, q, nz);
             adam_store<kFilterItems>(a, i0, q);
+            if (any) adam_slots_clear<kFilterItems>(a, i0);
 #pragma unroll
             for (int d = 0; d < 11; ++d) p[d] = make_float4(q[d].v[0], q[d].v[1], q[d].v[2], q[d].v[3]);
-            if (nz)
-#pragma unroll
-                for (int d = 0; d < 11; ++d)
-                    *reinterpret_cast<float4*>(a.grads + (uint64_t)d * a.cap + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
         } else {
+            if (slots) adam_slots_clear<kFilterItems>(a, i0);
 #pragma unroll
             for (int d = 0; d < 11; ++d) p[d] = *reinterpret_cast<const float4*>(a.params + (uint64_t)d * a.cap + i0);
         }
+        if (slots ? dirty == kGradsDense : nz != 0)
+#pragma unroll
+            for (int d = 0; d < 11; ++d)
+                *reinterpret_cast<float4*>(a.grads + (uint64_t)d * a.cap + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
 #pragma unroll
         for (int d = 0; d < 11; ++d) p[d] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -431,7 +448,6 @@ __global__ void __launch_bounds__(256, 3) k_adam_cull(const AdamLaunch a, const 
         CullScratch& sc = s_cull[threadIdx.x >> 5];
         cull_chunk(f, filter_consts(f.slice, log_tau), log_tau, filter_on, b, i0, p, sc.x, sc.p, nullptr);
     }
-    if (adam_on) adam_finish(a);
 }
 
 // ---- K_decide ------------------------------------------------------------------
@@ -497,6 +513,9 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     }
     __syncthreads();
     const unsigned g = s_grp;
+    // the preceding K_filter / fused Adam + cull cleared the dense gradient
+    // planes as the state word said (the dense chain sets it again)
+    if (a.grads && blockIdx.x == 0 && tid == 0) *a.grads_dirty = 0u;
     const uint32_t base = g * kDecideGroup;
     const unsigned nc = s_cpre[kDecideChunks];
 
@@ -556,6 +575,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
         if (survive) {
             a.records[base + rank] = rec;
             store_cand(a.surv_params + base + rank, pf, i);
+            a.survivor_list[base + rank] = i;
             const unsigned tx0 = rec.lo_x / kTile, ty0 = rec.lo_y / kTile;
             const unsigned ntx = rec.hi_x / kTile - tx0 + 1, nty = rec.hi_y / kTile - ty0 + 1;
             s_rect[rank][0] = (uint16_t)tx0;
@@ -762,13 +782,17 @@ __device__ __forceinline__ void merge_partials(const ChainLaunch& a, const Survi
     }
 }
 
-__device__ __forceinline__ void store_chain(const ChainLaunch& a, uint32_t i, const float g[11],
+// Gradient of set index i (survivor slot cid): the dense planes, or the slot
+// planes in slot-gradient mode (coalesced: a CTA's survivors are consecutive).
+__device__ __forceinline__ void store_chain(const ChainLaunch& a, uint32_t i, uint32_t cid, const float g[11],
                                             const float dmu[3], const double acc[6]) {
     const bool finite = isfinite(g[10]) && isfinite(g[0] + g[1] + g[2]) &&
                         isfinite(g[3] + g[4] + g[5]) && isfinite(g[6] + g[7] + g[8] + g[9]);
     if (!finite) record_error(a.err, kErrNumeric, i);  // backward.hpp:175-185
+    float* dst = a.slot_grads ? a.slot_grads + cid : a.grads + i;
 #pragma unroll
-    for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = g[k];
+    for (int k = 0; k < 11; ++k) dst[(uint64_t)k * a.cap] = g[k];
+    if (a.slot_grads) a.gmap[i] = (uint16_t)(cid % kDecideGroupSize + 1);
     if (a.stat_norm) a.stat_norm[i] = (float)sqrt(acc[1] * acc[1] + acc[2] * acc[2]);
     if (a.stat_observed) a.stat_observed[i] = 1;
     if (a.stat_world) {
@@ -787,11 +811,12 @@ __global__ void __launch_bounds__(256) k_chain(const ChainLaunch a) {
     // CTA per K_decide group: its survivors sit at slots [g*4096, g*4096 + S_g)
     const unsigned g = blockIdx.x;
     const unsigned S = a.grp_surv[g];
-    if (g == 0 && threadIdx.x == 0) *a.grads_dirty = a.ctrl->survivors;
+    const bool dense = a.slot_grads == nullptr;  // dense planes: keep the sparse-clear list
+    if (dense && g == 0 && threadIdx.x == 0) *a.grads_dirty = a.ctrl->survivors;
     for (unsigned j = threadIdx.x; j < S; j += blockDim.x) {
         const uint32_t cid = g * kDecideGroupSize + j;
         const SurvivorRecord rec = a.records[cid];
-        a.dirty_idx[atomicAdd(a.dirty_ctr, 1u)] = rec.gidx & ~kExactFlag;
+        if (dense) a.dirty_idx[atomicAdd(a.dirty_ctr, 1u)] = rec.gidx & ~kExactFlag;
         if (rec.gidx & kExactFlag) {
             a.exact_list[atomicAdd(a.exact_count, 1u)] = cid;
             continue;
@@ -805,7 +830,7 @@ __global__ void __launch_bounds__(256) k_chain(const ChainLaunch a) {
         merge_partials(a, rec, acc);
         float g11[11], dmu[3];
         fast_backward(pf, ff, acc, a.slice, g11, dmu);
-        store_chain(a, i, g11, dmu, acc);
+        store_chain(a, i, cid, g11, dmu, acc);
     }
 }
 
@@ -832,7 +857,7 @@ __global__ void __launch_bounds__(128) k_chain_exact(const ChainLaunch a) {
         float g[11], dmu[3] = {(float)dl_dmu.x, (float)dl_dmu.y, (float)dl_dmu.z};
 #pragma unroll
         for (int k = 0; k < 11; ++k) g[k] = (float)gd[k];
-        store_chain(a, i, g, dmu, acc);
+        store_chain(a, i, cid, g, dmu, acc);
     }
 }
 
@@ -1085,7 +1110,9 @@ void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& f, cudaStream_t st)
     const float log_tau = filter_on ? (float)log(f.slice.tau) : 0.f;
     const unsigned threads = (unsigned)std::max<uint64_t>((uint64_t)f.nfilter * 32, (a.n + kFilterItems - 1) / kFilterItems);
     const unsigned grid = (threads + 255) / 256;
-    if (grid) launch_pdl(k_adam_cull, dim3(grid), dim3(256), 0, st, a, f, log_tau, filter_on ? 1 : 0);
+    if (!grid) return;
+    launch_adam_consts(a, st);
+    launch_pdl(k_adam_cull, dim3(grid), dim3(256), 0, st, a, f, log_tau, filter_on ? 1 : 0);
 }
 
 void launch_bin(const PrepLaunch& a, cudaStream_t st) {

@@ -111,6 +111,10 @@ struct gpk_session {
     DevBuf cand_count; // candidates per 1024-Gaussian chunk
     DevBuf surv_params;  // CandParams of survivors by survivor slot (K_decide)
     DevBuf dirty_idx;  // set indices of the last backward's survivors
+    DevBuf slot_grads; // training-step gradients by survivor slot (11 planes, stride cap)
+    bool grads_in_slots = false;  // the latest gradient lives in slot_grads (see AdamLaunch)
+    DevBuf gmap;       // slot mode: u16 per primitive, 1 + survivor offset in its group (else 0)
+    bool gmap_dirty = false;      // a slot backward wrote gmap and no Adam consumed (cleared) it
     DevBuf grp_table;  // per K_decide group: uint2 (first pair, pairs), then u32 survivors
     DevBuf bucket_tab; // single-pass slices: per group, tiles + 1 bucket starts
     uint2* grp_pairs() { return grp_table.as<uint2>(); }
@@ -158,6 +162,8 @@ struct gpk_session {
         bool needs_prefilter = false;  // pipelined train step: starts at K_decide
         bool sets_prefilter = false;   // ... and leaves next_pose culled
         bool writes_params = false;
+        bool grads_in_slots = false;   // where the graph leaves the gradient
+        bool gmap_dirty = false;
         gpk_slice_pose next_pose{};
         std::vector<Pending> timed;  // event-record nodes captured with stage timing on
     };
@@ -176,7 +182,7 @@ struct gpk_session {
     ErrorState* err() { return persist.as<ErrorState>(); }
     unsigned* epoch() { return reinterpret_cast<unsigned*>(persist.as<char>() + 64); }
     long long* adam_step() { return reinterpret_cast<long long*>(persist.as<char>() + 72); }
-    unsigned* adam_done() { return reinterpret_cast<unsigned*>(persist.as<char>() + 80); }
+    AdamConsts* adam_consts() { return reinterpret_cast<AdamConsts*>(persist.as<char>() + 128); }
     unsigned* loss_done() { return reinterpret_cast<unsigned*>(persist.as<char>() + 84); }
     double* loss() { return reinterpret_cast<double*>(persist.as<char>() + 88); }
     Control* ctrl() { return head.as<Control>(); }
@@ -195,7 +201,7 @@ struct gpk_session {
 
 namespace {
 
-constexpr size_t kPersistBytes = 128;
+constexpr size_t kPersistBytes = 192;
 
 cudaEvent_t take_event(gpk_session* s) {
     if (!s->event_pool.empty()) {
@@ -461,6 +467,21 @@ void set_prefilter(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* ps
     s->prefilter.n = s->n;
 }
 
+// A slot backward whose gradient no Adam consumed: clear its map entries (the
+// survivors of the current prepared slice).
+int clear_gmap(gpk_session* s) {
+    if (!s->gmap_dirty) return GPK_OK;
+    s->gmap_dirty = false;
+    if (!s->prep.valid || s->n == 0) return GPK_OK;
+    AdamLaunch c{};
+    c.gmap = s->gmap.as<uint16_t>();
+    c.surv_gidx = s->survivors.as<uint32_t>();
+    c.grp_surv = s->grp_surv();
+    launch_scatter_slot_grads(c, (unsigned)decide_group_count(s->n), false, s->stream);
+    CK(cudaGetLastError());
+    return GPK_OK;
+}
+
 int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                 const gpk_raster_config* cfg, bool zero_grads) {
     SliceArgs a;
@@ -478,8 +499,10 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     ps.cfg = *cfg;
     ps.valid = true;
     ps.rasterized = false;
+    TRY(clear_gmap(s));  // before the survivor slots change
     ps.grads_zeroed = zero_grads;
     ps.ssim_pending = false;
+    s->grads_in_slots = false;  // the survivor slots are about to change
     const uint64_t nbf = filter_blocks(s->n);
     const size_t head_bytes = head_size(s->n);
     StageScope scope_prep(s, GPK_STAGE_PREPARE);
@@ -595,11 +618,16 @@ int run_rasterize(gpk_session* s, cudaStream_t on = nullptr) {
     return GPK_OK;
 }
 
-int run_backward(gpk_session* s, bool stats) {
+// slots: the chain writes the gradient by survivor slot (single-GPU training
+// step: Adam reads it there) instead of into the dense planes.
+int run_backward(gpk_session* s, bool stats, bool slots = false) {
     if (!s->prep.valid) return fail(GPK_ERR_STATE, "backward: no prepared slice");
     s->prefilter.valid = false;  // the chain writes gradients
+    TRY(clear_gmap(s));
+    s->grads_in_slots = slots && s->n;
+    s->gmap_dirty = s->grads_in_slots;
     if (s->n == 0) return GPK_OK;
-    if (!s->prep.grads_zeroed) {
+    if (!slots && !s->prep.grads_zeroed) {
         CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
         CK(cudaMemsetAsync(s->grads_dirty(), 0, 4, s->stream));
     }
@@ -628,6 +656,8 @@ int run_backward(gpk_session* s, bool stats) {
     c.partials = s->partials.as<float>();
     c.ctrl = s->ctrl();
     c.grads = s->grads.as<float>();
+    c.slot_grads = slots ? s->slot_grads.as<float>() : nullptr;
+    c.gmap = s->gmap.as<uint16_t>();
     c.stat_norm = stats ? s->stat_norm.as<float>() : nullptr;
     c.stat_observed = stats ? s->stat_obs.as<uint8_t>() : nullptr;
     c.stat_world = stats ? s->stat_world.as<float>() : nullptr;
@@ -716,6 +746,11 @@ int alloc_for_n(gpk_session* s, uint64_t n) {
         CK(s->cand.ensure(cap * sizeof(CandParams)));
         CK(s->cand_count.ensure(nbf * 4));
         CK(s->dirty_idx.ensure(cap * 4));
+        CK(s->slot_grads.ensure(cap * 11 * 4));
+        CK(s->gmap.ensure(cap * 2));
+        CK(cudaMemsetAsync(s->gmap.p, 0, cap * 2, s->stream));
+        s->grads_in_slots = false;
+        s->gmap_dirty = false;
         TRY(mark_grads_dense(s));
         CK(s->survivors.ensure(cap * 4));
         CK(s->head.ensure(head_size(cap)));
@@ -731,6 +766,41 @@ int adam_reset(gpk_session* s) {
     CK(cudaMemsetAsync(s->adam_v.p, 0, s->cap * 11 * 4, s->stream));
     CK(cudaMemsetAsync(s->adam_step(), 0, 16, s->stream));
     return GPK_OK;
+}
+
+int materialize_dense_grads(gpk_session* s);
+
+// Adam's gradient: the slot planes of the last training step's backward while
+// its map is intact (Adam consumes the map), else the dense planes (the slot
+// gradient scattered into them first if it is the latest).
+int adam_grad_source(gpk_session* s, AdamLaunch& a) {
+    const bool slots = s->grads_in_slots && s->gmap_dirty && s->prep.valid;
+    if (!slots) TRY(materialize_dense_grads(s));
+    a.slot_grads = slots ? s->slot_grads.as<float>() : nullptr;
+    a.gmap = s->gmap.as<uint16_t>();
+    a.surv_gidx = s->survivors.as<uint32_t>();
+    a.grp_surv = s->grp_surv();
+    if (slots) s->gmap_dirty = false;
+    return GPK_OK;
+}
+
+// Make the dense planes hold the latest gradient (API readers and writers of
+// GPK_BUF_GRADS, the all-reduce): scatter the slot gradient if it lives there.
+int materialize_dense_grads(gpk_session* s) {
+    if (!s->grads_in_slots) return GPK_OK;
+    s->grads_in_slots = false;
+    if (!s->prep.valid || s->n == 0) return GPK_OK;
+    if (s->capturing) return fail(GPK_ERR_STATE, "gradient layout change during capture");
+    CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
+    AdamLaunch a{};
+    a.grads = s->grads.as<float>();
+    a.cap = s->cap;
+    a.slot_grads = s->slot_grads.as<float>();
+    a.surv_gidx = s->survivors.as<uint32_t>();
+    a.grp_surv = s->grp_surv();
+    launch_scatter_slot_grads(a, (unsigned)decide_group_count(s->n), true, s->stream);
+    CK(cudaGetLastError());
+    return mark_grads_dense(s);
 }
 
 int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
@@ -762,8 +832,9 @@ int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
     a.beta2 = hp ? hp->beta2 : 0.999;
     a.eps = hp ? hp->eps : 1e-8;
     a.step = s->adam_step();
-    a.done_ctr = s->adam_done();
+    a.consts = s->adam_consts();
     a.ctrl = s->prep.valid ? s->ctrl() : nullptr;
+    TRY(adam_grad_source(s, a));
     s->prefilter.valid = false;  // the parameters change
     StageScope scope(s, GPK_STAGE_ADAM);
     launch_adam(a, s->stream);
@@ -799,8 +870,9 @@ int run_adam_cull(gpk_session* s, const double lr[4], int total, const gpk_slice
     a.beta2 = 0.999;
     a.eps = 1e-8;
     a.step = s->adam_step();
-    a.done_ctr = s->adam_done();
+    a.consts = s->adam_consts();
     a.ctrl = s->prep.valid ? s->ctrl() : nullptr;
+    TRY(adam_grad_source(s, a));
     StageScope scope(s, GPK_STAGE_ADAM);
     launch_adam_cull(a, f, s->stream);
     CK(cudaGetLastError());
@@ -1113,7 +1185,12 @@ int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
     uint64_t b = 0;
     switch (which) {
         case GPK_BUF_PARAMS: p = s->params.p; b = s->cap * 44; s->prefilter.valid = false; break;
-        case GPK_BUF_GRADS: p = s->grads.p; b = s->cap * 44; break;
+        case GPK_BUF_GRADS:  // the caller may read or write the dense planes
+            TRY(materialize_dense_grads(s));
+            TRY(mark_grads_dense(s));
+            p = s->grads.p;
+            b = s->cap * 44;
+            break;
         case GPK_BUF_IMAGE: p = s->image.p; b = px * 4; break;
         case GPK_BUF_DL_DI: p = s->dl_di.p; b = px * 4; break;
         case GPK_BUF_TARGET: p = s->target.p; b = px * 4; break;
@@ -1221,6 +1298,7 @@ int gpk_set_gradients(gpk_session* s, const float* grads) {
         CK(cudaMemcpy(s->grads.as<float>() + (size_t)k * s->cap, plane.data(), n * 4,
                       cudaMemcpyHostToDevice));
     }
+    s->grads_in_slots = false;
     TRY(mark_grads_dense(s));
     CK(cudaStreamSynchronize(s->stream));
     return ok();
@@ -1229,6 +1307,7 @@ int gpk_set_gradients(gpk_session* s, const float* grads) {
 int gpk_get_gradients(gpk_session* s, float* grads) {
     if (!s || (s->n && !grads)) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
     TRY(set_device(s));
+    TRY(materialize_dense_grads(s));
     TRY(sync_and_check(s, "gradients"));
     if (s->n) TRY(copy_planes_out(s, s->grads.as<float>(), grads));
     return ok();
@@ -1502,6 +1581,26 @@ int gpk_fwd_bwd_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf*
 // Data-parallel training: with a communicator, the dense gradient planes are
 // summed over the ranks between backward and Adam (defined with the NCCL code).
 static int dp_allreduce_if_comm(gpk_session* s);
+static void*& session_comm(gpk_session* s);
+
+// One training step (optimize.hpp:385-402): prepare, rasterize, photometric
+// loss, backward, (all-reduce), scheduled Adam. The gradient is kept by
+// survivor slot on a single GPU (AdamLaunch) and dense under a communicator.
+// With `next`, Adam is fused with the cull of the next slice (same PSF and
+// raster config) and the following step on `next` skips K_filter.
+static int train_body(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf, const gpk_raster_config* cfg,
+                      double lambda, double dssim_scale, const gpk_learning_rates* lr0, int32_t total,
+                      const gpk_slice_pose* next) {
+    TRY(run_prepare(s, pose, psf, cfg, true));
+    s->assume_prefiltered = false;
+    TRY(run_rasterize(s));
+    TRY(run_loss(s, lambda, dssim_scale, true));
+    TRY(run_backward(s, false, /*slots=*/session_comm(s) == nullptr));  // dense planes for the all-reduce
+    TRY(dp_allreduce_if_comm(s));
+    const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
+    if (next) return run_adam_cull(s, lr, total, next, psf, cfg);
+    return run_adam(s, lr, true, total, nullptr);
+}
 
 int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                    const gpk_raster_config* cfg, double lambda, double dssim_scale,
@@ -1509,13 +1608,7 @@ int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* ps
     if (!s || !lr0) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
     if (total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "total iterations must be >= 1");
     TRY(set_device(s));
-    TRY(run_prepare(s, pose, psf, cfg, true));
-    TRY(run_rasterize(s));
-    TRY(run_loss(s, lambda, dssim_scale, true));
-    TRY(run_backward(s, false));
-    TRY(dp_allreduce_if_comm(s));
-    const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
-    TRY(run_adam(s, lr, true, total_iterations, nullptr));
+    TRY(train_body(s, pose, psf, cfg, lambda, dssim_scale, lr0, total_iterations, nullptr));
     return ok();
 }
 
@@ -1529,13 +1622,7 @@ int gpk_train_step_next(gpk_session* s, const gpk_slice_pose* pose, const gpk_ps
     if (!s || !lr0 || !next_pose) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
     if (total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "total iterations must be >= 1");
     TRY(set_device(s));
-    TRY(run_prepare(s, pose, psf, cfg, true));
-    TRY(run_rasterize(s));
-    TRY(run_loss(s, lambda, dssim_scale, true));
-    TRY(run_backward(s, false));
-    TRY(dp_allreduce_if_comm(s));
-    const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
-    TRY(run_adam_cull(s, lr, total_iterations, next_pose, psf, cfg));
+    TRY(train_body(s, pose, psf, cfg, lambda, dssim_scale, lr0, total_iterations, next_pose));
     return ok();
 }
 
@@ -1575,6 +1662,8 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
     gpk_session::Graph gr;
     gr.exec = ex;
     gr.prep = s->prep;
+    gr.grads_in_slots = s->grads_in_slots;
+    gr.gmap_dirty = s->gmap_dirty;
     gr.alloc_epoch = s->alloc_epoch;
     gr.timed = std::move(timed);
     gr.needs_prefilter = meta.needs_prefilter;
@@ -1642,14 +1731,7 @@ int gpk_graph_capture_train(gpk_session* s, const gpk_slice_pose* pose, const gp
     s->capture_meta.writes_params = true;
     return capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
         const TrainArgs* a = static_cast<const TrainArgs*>(p);
-        TRY(run_prepare(ss, a->pose, a->psf, a->cfg, true));
-        TRY(run_rasterize(ss));
-        TRY(run_loss(ss, a->lambda, a->dssim, true));
-        TRY(run_backward(ss, false));
-        const double lr[4] = {a->lr0->position, a->lr0->opacity, a->lr0->scale, a->lr0->rotation};
-        TRY(dp_allreduce_if_comm(ss));
-        TRY(run_adam(ss, lr, true, a->total, nullptr));
-        return GPK_OK;
+        return train_body(ss, a->pose, a->psf, a->cfg, a->lambda, a->dssim, a->lr0, a->total, nullptr);
     }, &args);
 }
 
@@ -1678,15 +1760,7 @@ int gpk_graph_capture_train_next(gpk_session* s, const gpk_slice_pose* pose, con
     s->assume_prefiltered = true;
     const int st = capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
         const TrainNextArgs* a = static_cast<const TrainNextArgs*>(p);
-        TRY(run_prepare(ss, a->pose, a->psf, a->cfg, true));
-        ss->assume_prefiltered = false;
-        TRY(run_rasterize(ss));
-        TRY(run_loss(ss, a->lambda, a->dssim, true));
-        TRY(run_backward(ss, false));
-        TRY(dp_allreduce_if_comm(ss));
-        const double lr[4] = {a->lr0->position, a->lr0->opacity, a->lr0->scale, a->lr0->rotation};
-        TRY(run_adam_cull(ss, lr, a->total, a->next, a->psf, a->cfg));
-        return GPK_OK;
+        return train_body(ss, a->pose, a->psf, a->cfg, a->lambda, a->dssim, a->lr0, a->total, a->next);
     }, &args);
     s->assume_prefiltered = false;
     s->prefilter = saved;  // capture records work, it does not run it
@@ -1716,6 +1790,8 @@ int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
     else if (g.writes_params || g.needs_prefilter)
         s->prefilter.valid = false;
     s->prep = g.prep;
+    s->grads_in_slots = g.grads_in_slots;
+    s->gmap_dirty = g.gmap_dirty;
     if (s->timing && !g.timed.empty()) {
         // graph captured with stage timing: its event nodes bracket each stage
         // on the device, back to back (no host submission gaps)
@@ -1838,6 +1914,7 @@ int gpk_allreduce_grads(gpk_session* s) {
     void* comm = session_comm(s);
     if (!api || !comm) return fail(GPK_ERR_STATE, "allreduce: communicator not initialized");
     TRY(set_device(s));
+    TRY(materialize_dense_grads(s));
     // 11 planes are contiguous with stride cap: reduce the whole [0, 11*cap) range.
     const int r = api->all_reduce(s->grads.p, s->grads.p, s->cap * 11, /*ncclFloat32*/ 7,
                                   /*ncclSum*/ 0, comm, s->stream);
@@ -1906,6 +1983,7 @@ int gpk_voxelize_backward(gpk_session* s, const gpk_voxelizer_config* cfg, const
     if (dl_dv)
         CK(cudaMemcpyAsync(s->dl_dv_vol.p, dl_dv, s->vox.voxels * 4, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
+    s->grads_in_slots = false;
     TRY(mark_grads_dense(s));
     if (s->n) {
         StageScope scope(s, GPK_STAGE_VOXEL);

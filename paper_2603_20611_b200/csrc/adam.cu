@@ -1,9 +1,10 @@
 // adam.cu — fused Adam step over all N primitives (adam_step, optimize.hpp:195-221).
 //
-// k_adam_consts (one thread) evaluates the step's bias corrections and the
-// lr_at schedule (optimize.hpp:71-73) in fp64 from the device step counter and
-// advances it, so a whole training step can be captured in a CUDA graph and
-// the update kernel needs no CTA barrier. k_adam: each thread walks the 11
+// k_adam_consts (one warp) evaluates the step's bias corrections and the lr_at
+// schedule (optimize.hpp:71-73) in fp64 from the device step counter (the
+// training step runs it on a side stream, off the critical path); the update
+// kernel advances the counter, so a whole training step can be captured in a
+// CUDA graph and the update kernel needs no CTA barrier. k_adam: each thread walks the 11
 // parameter planes of 2 consecutive primitives with 8 B accesses, storing each
 // plane as soon as it is final (few live registers: 6 CTAs per SM keep enough
 // requests in flight). Bytes: read p, g, m, v and write p, m, v = 308 B per
@@ -22,11 +23,9 @@ constexpr int kAdamItems = 2;
 
 __global__ void k_adam_consts(const AdamLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    if (threadIdx.x != 0 || (a.ctrl && a.ctrl->pair_overflow)) return;  // overflowed slice: no step
     AdamConsts c;
     adam_consts(a, c);
-    *a.consts = c;
-    *a.step += 1;
+    if (threadIdx.x == 0) *a.consts = c;
 }
 
 template <bool kSlots>
@@ -39,6 +38,7 @@ __global__ void __launch_bounds__(256, 6) k_adam(const AdamLaunch a) {
         return;
     }
     const AdamConsts c = *a.consts;
+    adam_advance_step(a, c);
     uint32_t gslot[kAdamItems];
     const bool any = kSlots && adam_slots<kAdamItems>(a, i0, gslot);
     adam_update_store<kAdamItems>(a, c, i0, kSlots ? gslot : nullptr);
@@ -72,7 +72,6 @@ void launch_adam_consts(const AdamLaunch& a, cudaStream_t st) {
 }
 
 void launch_adam(const AdamLaunch& a, cudaStream_t st) {
-    launch_adam_consts(a, st);
     // 2 primitives per thread, registers capped for 6 CTAs per SM: measured
     // best on B200 among 1/2/4 items per thread, persistent grid or not
     const unsigned grid = (a.n + 256 * kAdamItems - 1) / (256 * kAdamItems);

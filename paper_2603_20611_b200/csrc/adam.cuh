@@ -12,12 +12,17 @@ namespace gpk {
 
 // Per-step constants, evaluated once by k_adam_consts (fp64, then f32): bias
 // corrections of step+1 and the lr_at schedule (optimize.hpp:71-73).
+// Whole warp: lanes 0-2 evaluate the three fp64 powers side by side (one pow
+// latency instead of three); the result is complete in lane 0.
 __device__ __forceinline__ void adam_consts(const AdamLaunch& a, AdamConsts& c) {
+    const int lane = threadIdx.x & 31;
     const long long step = *a.step + 1;
-    const double bc1 = 1.0 - pow(a.beta1, (double)step);
-    const double bc2 = 1.0 - pow(a.beta2, (double)step);
-    double f = 1.0;
-    if (a.scheduled) f = pow(0.1, (double)(step - 1) / (double)a.total);
+    const double base = lane == 0 ? a.beta1 : lane == 1 ? a.beta2 : 0.1;
+    const double ex = lane == 2 ? (double)(step - 1) / (double)a.total : (double)step;
+    const double pw = lane < 3 ? pow(base, ex) : 1.0;
+    const double bc1 = 1.0 - __shfl_sync(0xffffffffu, pw, 0);
+    const double bc2 = 1.0 - __shfl_sync(0xffffffffu, pw, 1);
+    const double f = a.scheduled ? __shfl_sync(0xffffffffu, pw, 2) : 1.0;
     c.b1 = (float)a.beta1;
     c.b2 = (float)a.beta2;
     c.ib1 = (float)(1.0 - a.beta1);
@@ -26,6 +31,13 @@ __device__ __forceinline__ void adam_consts(const AdamLaunch& a, AdamConsts& c) 
     c.isbc2 = __frcp_rn(__fsqrt_rn((float)bc2));
     c.eps = (float)a.eps;
     for (int k = 0; k < 4; ++k) c.lr[k] = (float)(a.lr[k] * f);
+    c.step = step;
+}
+
+// The update kernels' CTA 0 advances AdamState::step (no other CTA reads it;
+// the next step's k_adam_consts runs after this kernel).
+__device__ __forceinline__ void adam_advance_step(const AdamLaunch& a, const AdamConsts& c) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.step = c.step;
 }
 
 // N consecutive floats moved with one vector access.

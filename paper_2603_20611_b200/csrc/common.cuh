@@ -446,6 +446,7 @@ struct AdamConsts {
     float b1, b2, ib1, ib2;   // beta1, beta2, 1 - beta1, 1 - beta2
     float ibc1, isbc2, eps;   // 1 / bc1, 1 / sqrt(bc2), eps
     float lr[4];              // position, opacity, scale, rotation
+    long long step;           // the step these constants are for (AdamState::step after it)
 };
 
 struct AdamLaunch {
@@ -461,7 +462,7 @@ struct AdamLaunch {
     int total;
     double beta1, beta2, eps;
     long long* step;      // AdamState::step, device
-    AdamConsts* consts;   // this step's constants (k_adam_consts, then the update kernel)
+    AdamConsts* consts;   // this step's constants (k_adam_consts; the update kernel stores c.step)
     const Control* ctrl;  // skip when the slice overflowed its pair capacity
     // Slot-gradient mode (the single-GPU training step): when slot_grads is
     // non-null the gradients are not read from `grads` but from the chain's

@@ -398,7 +398,8 @@ __global__ void __launch_bounds__(256, 3) k_adam_cull(const AdamLaunch a, const 
     __shared__ CullScratch s_cull[8];
     const bool adam_on = !(a.ctrl && a.ctrl->pair_overflow);  // the slice overflowed: no update
     const bool slots = a.slot_grads != nullptr;
-    const AdamConsts c = *a.consts;  // k_adam_consts ran just before
+    const AdamConsts c = *a.consts;  // k_adam_consts ran before
+    if (adam_on) adam_advance_step(a, c);
     const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
     clear_prev_sort_rows(f, gtid, gthreads);
     // K_filter's gradient duty. Dense gradients: the Adam below zeroes every
@@ -697,10 +698,14 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
         }
         // the last group to finish turns the per-tile counts into list starts
         // (one scan, instead of every gather CTA re-reading the same counts)
-        __threadfence();
+        // (barrier, then one fence: cumulative over the CTA's writes the barrier
+        // ordered before it; a fence per thread stalls every warp on its stores)
         __syncthreads();
         __shared__ bool s_last;
-        if (tid == 0) s_last = atomicAdd(&a.ctrl->decide_done, 1u) == ngroups - 1;
+        if (tid == 0) {
+            __threadfence();
+            s_last = atomicAdd(&a.ctrl->decide_done, 1u) == ngroups - 1;
+        }
         __syncthreads();
         if (!s_last) return;
         __threadfence();
@@ -1111,7 +1116,6 @@ void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& f, cudaStream_t st)
     const unsigned threads = (unsigned)std::max<uint64_t>((uint64_t)f.nfilter * 32, (a.n + kFilterItems - 1) / kFilterItems);
     const unsigned grid = (threads + 255) / 256;
     if (!grid) return;
-    launch_adam_consts(a, st);
     launch_pdl(k_adam_cull, dim3(grid), dim3(256), 0, st, a, f, log_tau, filter_on ? 1 : 0);
 }
 

@@ -97,6 +97,8 @@ struct gpk_session {
     // backward on `stream` (fork/join by events; captured graphs keep the fork)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_cfork = nullptr, ev_cjoin = nullptr;  // Adam constants on the side stream
+    bool consts_pending = false;  // k_adam_consts was launched ahead (wait on ev_cjoin)
     uint64_t n = 0, cap = 0;
     gpk_bounds bbox{};
     uint64_t pair_cap = 0;
@@ -803,18 +805,8 @@ int materialize_dense_grads(gpk_session* s) {
     return mark_grads_dense(s);
 }
 
-int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
-             const gpk_adam_hparams* hp) {
-    if (s->n == 0) {
-        long long st = 0;
-        CK(cudaMemcpyAsync(&st, s->adam_step(), 8, cudaMemcpyDeviceToHost, s->stream));
-        CK(cudaStreamSynchronize(s->stream));
-        ++st;
-        CK(cudaMemcpyAsync(s->adam_step(), &st, 8, cudaMemcpyHostToDevice, s->stream));
-        CK(cudaStreamSynchronize(s->stream));
-        return GPK_OK;
-    }
-    AdamLaunch a;
+AdamLaunch adam_launch(gpk_session* s, const double lr[4], bool scheduled, int total, const gpk_adam_hparams* hp) {
+    AdamLaunch a{};
     a.params = s->params.as<float>();
     a.grads = s->grads.as<float>();
     a.m = s->adam_m.as<float>();
@@ -834,9 +826,49 @@ int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
     a.step = s->adam_step();
     a.consts = s->adam_consts();
     a.ctrl = s->prep.valid ? s->ctrl() : nullptr;
+    return a;
+}
+
+// The training step evaluates the Adam constants (fp64 pow latency) on the
+// side stream while the slice renders; the update waits on ev_cjoin.
+int adam_consts_ahead(gpk_session* s, const AdamLaunch& a) {
+    CK(cudaEventRecord(s->ev_cfork, s->stream));
+    CK(cudaStreamWaitEvent(s->side, s->ev_cfork, 0));
+    launch_adam_consts(a, s->side);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(s->ev_cjoin, s->side));
+    s->consts_pending = true;
+    return GPK_OK;
+}
+
+int adam_consts_ready(gpk_session* s, const AdamLaunch& a) {
+    if (s->consts_pending) {
+        s->consts_pending = false;
+        CK(cudaStreamWaitEvent(s->stream, s->ev_cjoin, 0));
+        return GPK_OK;
+    }
+    launch_adam_consts(a, s->stream);
+    CK(cudaGetLastError());
+    return GPK_OK;
+}
+
+int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
+             const gpk_adam_hparams* hp) {
+    if (s->n == 0) {
+        s->consts_pending = false;
+        long long st = 0;
+        CK(cudaMemcpyAsync(&st, s->adam_step(), 8, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        ++st;
+        CK(cudaMemcpyAsync(s->adam_step(), &st, 8, cudaMemcpyHostToDevice, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        return GPK_OK;
+    }
+    AdamLaunch a = adam_launch(s, lr, scheduled, total, hp);
     TRY(adam_grad_source(s, a));
     s->prefilter.valid = false;  // the parameters change
     StageScope scope(s, GPK_STAGE_ADAM);
+    TRY(adam_consts_ready(s, a));
     launch_adam(a, s->stream);
     CK(cudaGetLastError());
     return GPK_OK;
@@ -852,28 +884,10 @@ int run_adam_cull(gpk_session* s, const double lr[4], int total, const gpk_slice
     int passes = 0, digit_bits = 0;
     sort_plan(na.tiles_x * na.tiles_y, passes, digit_bits);
     const PrepLaunch f = prep_launch(s, na, passes, digit_bits, true);
-    AdamLaunch a;
-    a.params = s->params.as<float>();
-    a.grads = s->grads.as<float>();
-    a.m = s->adam_m.as<float>();
-    a.v = s->adam_v.as<float>();
-    a.cap = s->cap;
-    a.n = (uint32_t)s->n;
-    for (int d = 0; d < 3; ++d) {
-        a.bbox_min[d] = (float)s->bbox.min[d];
-        a.bbox_max[d] = (float)s->bbox.max[d];
-    }
-    for (int k = 0; k < 4; ++k) a.lr[k] = lr[k];
-    a.scheduled = 1;
-    a.total = total;
-    a.beta1 = 0.9;
-    a.beta2 = 0.999;
-    a.eps = 1e-8;
-    a.step = s->adam_step();
-    a.consts = s->adam_consts();
-    a.ctrl = s->prep.valid ? s->ctrl() : nullptr;
+    AdamLaunch a = adam_launch(s, lr, true, total, nullptr);
     TRY(adam_grad_source(s, a));
     StageScope scope(s, GPK_STAGE_ADAM);
+    TRY(adam_consts_ready(s, a));
     launch_adam_cull(a, f, s->stream);
     CK(cudaGetLastError());
     set_prefilter(s, next, psf, cfg);
@@ -1090,6 +1104,8 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_cfork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_cjoin, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) {
         gpk_session_destroy(s);
@@ -1131,6 +1147,8 @@ int gpk_session_destroy(gpk_session* s) {
     }
     if (s->ev_fork) cudaEventDestroy(s->ev_fork);
     if (s->ev_join) cudaEventDestroy(s->ev_join);
+    if (s->ev_cfork) cudaEventDestroy(s->ev_cfork);
+    if (s->ev_cjoin) cudaEventDestroy(s->ev_cjoin);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
     return ok();
@@ -1588,18 +1606,27 @@ static void*& session_comm(gpk_session* s);
 // survivor slot on a single GPU (AdamLaunch) and dense under a communicator.
 // With `next`, Adam is fused with the cull of the next slice (same PSF and
 // raster config) and the following step on `next` skips K_filter.
-static int train_body(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf, const gpk_raster_config* cfg,
-                      double lambda, double dssim_scale, const gpk_learning_rates* lr0, int32_t total,
-                      const gpk_slice_pose* next) {
+static int train_body_(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                       const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                       const gpk_learning_rates* lr0, int32_t total, const gpk_slice_pose* next) {
+    const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
+    if (s->n) TRY(adam_consts_ahead(s, adam_launch(s, lr, true, total, nullptr)));
     TRY(run_prepare(s, pose, psf, cfg, true));
     s->assume_prefiltered = false;
     TRY(run_rasterize(s));
     TRY(run_loss(s, lambda, dssim_scale, true));
     TRY(run_backward(s, false, /*slots=*/session_comm(s) == nullptr));  // dense planes for the all-reduce
     TRY(dp_allreduce_if_comm(s));
-    const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
     if (next) return run_adam_cull(s, lr, total, next, psf, cfg);
     return run_adam(s, lr, true, total, nullptr);
+}
+
+static int train_body(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf, const gpk_raster_config* cfg,
+                      double lambda, double dssim_scale, const gpk_learning_rates* lr0, int32_t total,
+                      const gpk_slice_pose* next) {
+    const int st = train_body_(s, pose, psf, cfg, lambda, dssim_scale, lr0, total, next);
+    if (st != GPK_OK) s->consts_pending = false;  // constants of an abandoned step
+    return st;
 }
 
 int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,

@@ -335,6 +335,7 @@ struct PrepLaunch {
     unsigned nfilter;         // 64-Gaussian chunks
     SurvivorRecord* records;  // indexed by candidate slot
     uint32_t* survivor_list;  // survivor slot -> set index (K_decide)
+    uint32_t* exact_list;     // slots of the fp64-decided survivors (count: Control::chain_exact)
     uint32_t* keys;           // pre-sort tile keys
     uint32_t* vals;           // pre-sort candidate slots
     uint64_t pair_cap;
@@ -433,7 +434,7 @@ struct ChainLaunch {
     float* stat_norm;              // optional (screen-space dL/dmu_2d norm)
     uint8_t* stat_observed;        // optional
     float* stat_world;             // optional, 3 per primitive
-    uint32_t* exact_list;          // record slots deferred to the fp64 chain
+    const uint32_t* exact_list;    // record slots of the fp64 chain (K_decide)
     unsigned* exact_count;         // Control::chain_exact
     const unsigned* grp_surv;      // survivors per K_decide group (CTA per group)
     unsigned* dirty_ctr;           // Control::dirty_ctr
@@ -574,6 +575,7 @@ void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st);
 void launch_raster_fwd(const RasterLaunch& a, cudaStream_t st);
 void launch_raster_bwd(const RasterLaunch& a, cudaStream_t st);
 void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st);
+void launch_chain_exact(const ChainLaunch& a, int grid, cudaStream_t st);
 void launch_adam(const AdamLaunch& a, cudaStream_t st);
 void launch_adam_consts(const AdamLaunch& a, cudaStream_t st);
 void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, bool grads, cudaStream_t st);

@@ -577,6 +577,9 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
             a.records[base + rank] = rec;
             store_cand(a.surv_params + base + rank, pf, i);
             a.survivor_list[base + rank] = i;
+            // fp64-decided survivors take the fp64 chain (K_chain_exact, which
+            // runs beside K_chain once the backward is done)
+            if (rec.gidx & kExactFlag) a.exact_list[atomicAdd(&a.ctrl->chain_exact, 1u)] = base + rank;
             const unsigned tx0 = rec.lo_x / kTile, ty0 = rec.lo_y / kTile;
             const unsigned ntx = rec.hi_x / kTile - tx0 + 1, nty = rec.hi_y / kTile - ty0 + 1;
             s_rect[rank][0] = (uint16_t)tx0;
@@ -822,10 +825,7 @@ __global__ void __launch_bounds__(256) k_chain(const ChainLaunch a) {
         const uint32_t cid = g * kDecideGroupSize + j;
         const SurvivorRecord rec = a.records[cid];
         if (dense) a.dirty_idx[atomicAdd(a.dirty_ctr, 1u)] = rec.gidx & ~kExactFlag;
-        if (rec.gidx & kExactFlag) {
-            a.exact_list[atomicAdd(a.exact_count, 1u)] = cid;
-            continue;
-        }
+        if (rec.gidx & kExactFlag) continue;  // K_chain_exact (listed by K_decide)
         float pf[11];
         uint32_t i;
         load_cand(a.sparams + cid, pf, i);
@@ -1133,6 +1133,9 @@ void launch_bin(const PrepLaunch& a, cudaStream_t st) {
 
 void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st) {
     launch_pdl(k_chain, dim3(grid), dim3(256), 0, st, a);
+}
+
+void launch_chain_exact(const ChainLaunch& a, int grid, cudaStream_t st) {
     launch_pdl(k_chain_exact, dim3(std::max(1, grid / 8)), dim3(128), 0, st, a);
 }
 

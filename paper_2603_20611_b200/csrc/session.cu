@@ -98,6 +98,7 @@ struct gpk_session {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_cfork = nullptr, ev_cjoin = nullptr;  // Adam constants on the side stream
+    cudaEvent_t ev_xfork = nullptr, ev_xjoin = nullptr;  // K_chain_exact beside K_chain
     bool consts_pending = false;  // k_adam_consts was launched ahead (wait on ev_cjoin)
     uint64_t n = 0, cap = 0;
     gpk_bounds bbox{};
@@ -436,6 +437,7 @@ PrepLaunch prep_launch(gpk_session* s, const SliceArgs& a, int passes, int digit
     pl.nfilter = (unsigned)filter_blocks(s->n);
     pl.records = s->records.as<SurvivorRecord>();
     pl.survivor_list = s->survivors.as<uint32_t>();
+    pl.exact_list = s->cand_list.as<uint32_t>();
     pl.keys = s->keys[0].as<uint32_t>();
     pl.vals = s->vals[0].as<uint32_t>();
     pl.pair_cap = s->pair_cap;
@@ -669,8 +671,16 @@ int run_backward(gpk_session* s, bool stats, bool slots = false) {
     c.dirty_ctr = &s->ctrl()->dirty_ctr;
     c.err = s->err();
     c.slice = s->prep.slice;
-    launch_chain(c, (int)decide_group_count(s->n), s->stream);
+    // K_chain_exact (the few fp64-decided survivors) beside K_chain
+    const int groups = (int)decide_group_count(s->n);
+    CK(cudaEventRecord(s->ev_xfork, s->stream));
+    CK(cudaStreamWaitEvent(s->side, s->ev_xfork, 0));
+    launch_chain_exact(c, groups, s->side);
     CK(cudaGetLastError());
+    CK(cudaEventRecord(s->ev_xjoin, s->side));
+    launch_chain(c, groups, s->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamWaitEvent(s->stream, s->ev_xjoin, 0));
     return GPK_OK;
 }
 
@@ -1106,6 +1116,8 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_cfork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_cjoin, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_xfork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_xjoin, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) {
         gpk_session_destroy(s);
@@ -1136,7 +1148,7 @@ int gpk_session_destroy(gpk_session* s) {
                       &s->sort_status, &s->head, &s->persist, &s->image,
                       &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm,
                       &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table, &s->bucket_tab,
-                      &s->dirty_idx, &s->vox_records,
+                      &s->dirty_idx, &s->vox_records, &s->slot_grads, &s->gmap,
                       &s->volume, &s->dl_dv_vol, &s->vox_partials};
     for (DevBuf* b : bufs) b->release();
     drain_timing(s);
@@ -1149,6 +1161,8 @@ int gpk_session_destroy(gpk_session* s) {
     if (s->ev_join) cudaEventDestroy(s->ev_join);
     if (s->ev_cfork) cudaEventDestroy(s->ev_cfork);
     if (s->ev_cjoin) cudaEventDestroy(s->ev_cjoin);
+    if (s->ev_xfork) cudaEventDestroy(s->ev_xfork);
+    if (s->ev_xjoin) cudaEventDestroy(s->ev_xjoin);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
     return ok();

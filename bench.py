@@ -172,7 +172,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------
-def cpu_reference_rate(cfg, rec, unit, seconds_budget, max_reps=None):
+def cpu_reference_rate(cfg, rec, unit, seconds_budget, max_reps=None, warmup=1):
     """The reference's own CPU implementation (oracle/_ref: its headers compiled
     unmodified) of the same unit on this host's cores. Its slice poses come from
     the reference's slice_pose_for_index (core.hpp:202-211); `rec` is the same
@@ -225,7 +225,8 @@ def cpu_reference_rate(cfg, rec, unit, seconds_budget, max_reps=None):
             raise RuntimeError("reference step failed")
         return secs.sum(), secs.copy()
 
-    t1, _ = run(1)  # warm (page-in, allocator)
+    t1, _ = run(max(1, warmup))  # warm (page-in, allocator)
+    t1 /= max(1, warmup)
     reps = max(1, int(seconds_budget / max(t1, 1e-6)))
     if max_reps:
         reps = min(reps, max_reps)
@@ -302,10 +303,10 @@ def run_reference(args):
     cfg = CONFIGS[args.config]
     rec = make_records(cfg, via_reference=True)
     budget = min(150.0, max(10.0, 1.0 * args.steps))
-    res = cpu_reference_rate(cfg, rec, args.unit, budget, max_reps=args.steps)
+    res = cpu_reference_rate(cfg, rec, args.unit, budget, max_reps=args.steps, warmup=min(args.warmup, 10))
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "slices/s",
-        "n_gpus": args.gpus, "steps": res["reps"], "warmup": 1, "ms_per_step": 1000.0 / res["value"],
+        "n_gpus": args.gpus, "steps": res["reps"], "warmup": min(args.warmup, 10), "ms_per_step": 1000.0 / res["value"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": data_note(args.unit), "config": config_json(args, cfg, world),
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},

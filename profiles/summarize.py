@@ -3,7 +3,7 @@
     python profiles/summarize.py full  <capture.ncu-rep> <out.json> [--config c2]
     python profiles/summarize.py launches <launches.csv> <out.json>
 
-`full`: one `ncu --set full` capture of one U1 step (tests/profile_step.py)
+`full`: one `ncu --set full` capture of one training step (tests/profile_train.py)
 -> per kernel: duration, DRAM bytes read/written, instructions, registers,
 achieved occupancy, IPC, top warp-stall reasons. Also merges the kernel's
 DRAM bytes into profiles/ncu_summary.json (read by bench.py for the
@@ -55,7 +55,7 @@ def ncu_raw(rep: str) -> list[dict]:
 
 
 def stalls(rep: str, kernel: str, top: int = 4) -> dict:
-    out = subprocess.run(["ncu", "-i", rep, "-k", f"regex:{kernel}", "--page", "raw", "--csv"],
+    out = subprocess.run(["ncu", "-i", rep, "-k", f"regex:(^|::){kernel}(<|$)", "--page", "raw", "--csv"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
@@ -93,7 +93,7 @@ def full(rep: str, out: str, config: str) -> None:
         k["share_of_step"] = round((k["duration_us"] or 0) / total, 4) if total else None
     Path(out).write_text(json.dumps({"capture": Path(rep).name, "config": config,
                                      "note": "ncu --set full --clock-control none, cold caches, serialised "
-                                             "(one U1 step of tests/profile_step.py)",
+                                             "(one U2 training step of tests/profile_train.py, the third)",
                                      "sum_us": total, "kernels": kernels}, indent=1))
     # traffic per launch for bench.py's roofline field
     summ = HERE / "ncu_summary.json"

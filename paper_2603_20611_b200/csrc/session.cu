@@ -99,6 +99,11 @@ struct gpk_session {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_cfork = nullptr, ev_cjoin = nullptr;  // Adam constants on the side stream
     cudaEvent_t ev_xfork = nullptr, ev_xjoin = nullptr;  // K_chain_exact beside K_chain
+    // slice targets are uploaded on their own stream and overlap the step's
+    // prepare + forward; the loss waits on ev_tgt_ready (see gpk_upload)
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_tgt_fork = nullptr, ev_tgt_ready = nullptr;
+    bool tgt_pending = false;
     bool consts_pending = false;  // k_adam_consts was launched ahead (wait on ev_cjoin)
     uint64_t n = 0, cap = 0;
     gpk_bounds bbox{};
@@ -349,6 +354,7 @@ int ensure_pairs(gpk_session* s, uint64_t need) {
 
 int ensure_image(gpk_session* s, int w, int h) {
     const size_t px = (size_t)w * h;
+    if (s->copy && px * 4 > s->target.bytes) CK(cudaStreamSynchronize(s->copy));  // no copy into a freed buffer
     const void* before[3] = {s->image.p, s->dl_di.p, s->target.p};
     CK(s->image.ensure(px * 4));
     CK(s->dl_di.ensure(px * 4));
@@ -904,6 +910,21 @@ int run_adam_cull(gpk_session* s, const double lr[4], int total, const gpk_slice
     return GPK_OK;
 }
 
+// Before the session stream reads or writes the target: the uploaded slice
+// target has landed. Captured graphs always wait on ev_tgt_ready (an external
+// event node: resolved at each launch against the latest upload).
+int target_wait(gpk_session* s) {
+    if (s->capturing) {
+        CK(cudaStreamWaitEvent(s->stream, s->ev_tgt_ready, cudaEventWaitExternal));
+        return GPK_OK;
+    }
+    if (s->tgt_pending) {
+        CK(cudaStreamWaitEvent(s->stream, s->ev_tgt_ready, 0));
+        s->tgt_pending = false;
+    }
+    return GPK_OK;
+}
+
 int run_loss(gpk_session* s, double lambda, double dssim_scale, bool fuse_into_backward = false) {
     if (!s->prep.rasterized) return fail(GPK_ERR_STATE, "photometric_loss: no rendered image");
     const int W = s->img_w, H = s->img_h;
@@ -934,6 +955,7 @@ int run_loss(gpk_session* s, double lambda, double dssim_scale, bool fuse_into_b
         sum += w[t + 5];
     }
     for (int t = 0; t < 11; ++t) l.w[t] = (float)(w[t] / sum);
+    TRY(target_wait(s));
     StageScope scope(s, GPK_STAGE_LOSS);
     const bool fuse = fuse_into_backward && lambda != 0.0;
     l.finish_in_fwd = fuse ? 1 : 0;
@@ -1118,6 +1140,9 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_cjoin, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_xfork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_xjoin, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->copy, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) {
         gpk_session_destroy(s);
@@ -1163,6 +1188,12 @@ int gpk_session_destroy(gpk_session* s) {
     if (s->ev_cjoin) cudaEventDestroy(s->ev_cjoin);
     if (s->ev_xfork) cudaEventDestroy(s->ev_xfork);
     if (s->ev_xjoin) cudaEventDestroy(s->ev_xjoin);
+    if (s->copy) {
+        cudaStreamSynchronize(s->copy);
+        cudaStreamDestroy(s->copy);
+    }
+    if (s->ev_tgt_fork) cudaEventDestroy(s->ev_tgt_fork);
+    if (s->ev_tgt_ready) cudaEventDestroy(s->ev_tgt_ready);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
     return ok();
@@ -1225,7 +1256,11 @@ int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
             break;
         case GPK_BUF_IMAGE: p = s->image.p; b = px * 4; break;
         case GPK_BUF_DL_DI: p = s->dl_di.p; b = px * 4; break;
-        case GPK_BUF_TARGET: p = s->target.p; b = px * 4; break;
+        case GPK_BUF_TARGET:
+            TRY(target_wait(s));
+            p = s->target.p;
+            b = px * 4;
+            break;
         case GPK_BUF_LOSS: p = s->loss(); b = 8; break;
         case GPK_BUF_VOLUME: p = s->volume.p; b = s->vox.voxels * 4; break;
         case GPK_BUF_DL_DV: p = s->dl_dv_vol.p; b = s->vox.voxels * 4; break;
@@ -1244,6 +1279,7 @@ int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes) {
     if (grow && host && bytes > grow->bytes) {
         TRY(set_device(s));
         CK(cudaStreamSynchronize(s->stream));
+        CK(cudaStreamSynchronize(s->copy));
         CK(grow->ensure(bytes));
         ++s->alloc_epoch;
     }
@@ -1253,6 +1289,17 @@ int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes) {
     if (grow) cap = grow->bytes;
     if (!host || bytes > cap) return fail(GPK_ERR_INVALID_ARGUMENT, "upload: size exceeds buffer");
     TRY(set_device(s));
+    if (which == GPK_BUF_TARGET && !s->capturing) {
+        // after everything already queued on the session stream (earlier
+        // readers of the target), on the copy stream: the transfer overlaps
+        // the next step's prepare and forward, which do not read the target
+        CK(cudaEventRecord(s->ev_tgt_fork, s->stream));
+        CK(cudaStreamWaitEvent(s->copy, s->ev_tgt_fork, 0));
+        CK(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, s->copy));
+        CK(cudaEventRecord(s->ev_tgt_ready, s->copy));
+        s->tgt_pending = true;
+        return ok();
+    }
     CK(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, s->stream));
     return ok();
 }
@@ -1504,6 +1551,7 @@ int gpk_photometric_loss(gpk_session* s, const float* target, double lambda, dou
         return fail(GPK_ERR_INVALID_ARGUMENT, "photometric_loss: lambda must be >= 0");
     TRY(set_device(s));
     const size_t px = (size_t)s->img_w * s->img_h;
+    TRY(target_wait(s));
     if (target) CK(cudaMemcpyAsync(s->target.p, target, px * 4, cudaMemcpyHostToDevice, s->stream));
     TRY(run_loss(s, lambda, dssim_scale));
     if (loss_out || dl_di_out) {
@@ -1526,6 +1574,7 @@ int gpk_photometric_loss_images(gpk_session* s, int32_t width, int32_t height,
     TRY(set_device(s));
     TRY(ensure_image(s, width, height));
     const size_t px = (size_t)width * height;
+    TRY(target_wait(s));
     CK(cudaMemcpyAsync(s->image.p, rendered, px * 4, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemcpyAsync(s->target.p, target, px * 4, cudaMemcpyHostToDevice, s->stream));
     // the prepared slice survives when the images have its shape (only the

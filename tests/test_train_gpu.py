@@ -319,3 +319,44 @@ def test_gradient_layouts_interleave(gp, session):
         s2.rasterize()
         _, dl2 = s2.photometric_loss(tgt, 0.2, 0.5)
         assert np.array_equal(session.get_gradients(), s2.backward(dl2))
+
+
+def test_target_upload_overlaps_but_is_ordered(gp, session):
+    """gpk_upload(GPK_BUF_TARGET) runs on the session's copy stream and overlaps
+    the next step's prepare + forward; the loss (direct or in a replayed graph)
+    must still see the new target: both equal a session that synchronizes after
+    every upload. A large slice (16 MB target) and a small set make the copy
+    outlast the kernels before the loss."""
+    from paper_2603_20611_b200 import _native as N
+
+    dims = (2048, 2048, 8)
+    lo, hi = (-0.5, -0.5, -0.5), (2047.5, 2047.5, 7.5)
+    gs = gp.GaussianSet(f32(gp.init_random(2000, lo, hi, 1.5, 6).records), lo, hi)
+    pose = gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), 3)
+    psf, rc = gp.PsfSpec(), gp.RasterConfig()
+    lr0 = gp.LearningRates(6e-4, 0.02, 2e-3, 1e-3)
+    rng = np.random.default_rng(13)
+    targets = [rng.uniform(0, 0.1 * (k + 1), (2048, 2048)).astype(np.float32) for k in range(3)]
+    with gp.Session(0) as s2, gp.Session(0) as s3:
+        for s in (session, s2, s3):
+            s.set_gaussians(gs)
+            s.upload(N.GPK_BUF_TARGET, targets[0].ctypes.data, targets[0].nbytes)
+        gid = s2.capture_train(pose, psf, rc, 0.2, 0.5, lr0, 20)
+        for k in range(3):
+            for s in (session, s2, s3):
+                s.upload(N.GPK_BUF_TARGET, targets[k].ctypes.data, targets[k].nbytes)
+            s3.synchronize()
+            session.train_step(pose, psf, rc, 0.2, 0.5, lr0, 20)
+            s2.graph_launch(gid)
+            s3.train_step(pose, psf, rc, 0.2, 0.5, lr0, 20)
+            loss = []
+            for s in (session, s2, s3):
+                v = np.zeros(1)
+                s.download(N.GPK_BUF_LOSS, v.ctypes.data, 8)
+                s.synchronize()
+                loss.append(v[0])
+            assert loss[0] == loss[2] and loss[1] == loss[2], (k, loss)
+            ref = s3.get_gaussians()
+            assert np.array_equal(session.get_gaussians(), ref), k
+            assert np.array_equal(s2.get_gaussians(), ref), k
+        s2.graph_destroy_all()

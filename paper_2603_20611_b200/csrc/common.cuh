@@ -305,6 +305,16 @@ inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, 
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Last-CTA tickets: a device-scope acq_rel fetch-add. Issued by one thread
+// after a CTA barrier it releases the CTA's writes (the barrier orders them
+// before it; PTX causality is cumulative) and, for the last CTA, acquires
+// everyone else's — no separate fence.sc (MEMBAR.SC) round trip.
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* ctr) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+    return old;
+}
+
 // Pairs actually stored for the current slice (T capped by the buffer size).
 __device__ __forceinline__ unsigned stored_pairs(const Control* c, uint64_t cap) {
     const unsigned long long p = c->pairs;

@@ -62,13 +62,11 @@ __device__ __forceinline__ void finish_loss(const LossLaunch& a, bool with_ssim)
     __shared__ double s_red2[16];
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
         const unsigned nblk = gridDim.x * gridDim.y;
-        s_last = (atomicAdd(a.done_ctr, 1u) == nblk - 1) ? 1u : 0u;
+        s_last = (ticket_acq_rel(a.done_ctr) == nblk - 1) ? 1u : 0u;
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     const unsigned nblk = gridDim.x * gridDim.y;
     double ss = 0.0, l1 = 0.0;
     for (unsigned k = threadIdx.x; k < nblk; k += blockDim.x) {

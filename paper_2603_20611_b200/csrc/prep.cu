@@ -701,17 +701,11 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
         }
         // the last group to finish turns the per-tile counts into list starts
         // (one scan, instead of every gather CTA re-reading the same counts)
-        // (barrier, then one fence: cumulative over the CTA's writes the barrier
-        // ordered before it; a fence per thread stalls every warp on its stores)
         __syncthreads();
         __shared__ bool s_last;
-        if (tid == 0) {
-            __threadfence();
-            s_last = atomicAdd(&a.ctrl->decide_done, 1u) == ngroups - 1;
-        }
+        if (tid == 0) s_last = ticket_acq_rel(&a.ctrl->decide_done) == ngroups - 1;
         __syncthreads();
         if (!s_last) return;
-        __threadfence();
         {
             constexpr int kPer = kMaxBuckets / kDecideThreads;
             const unsigned d0 = tid * kPer;

@@ -489,18 +489,21 @@ def run_ours(args):
     S, T, Cc = S_mean, T_mean, C_mean
     passes = sort_passes(X, Y)
     kernel_bytes = {
-        "prepare": ("k_filter", 44 * n + 44 * S + 48 * Cc + 4 * (n / 64),
-                    "44N params + 44S previous-survivor gradient clear + 48C candidate records + 4N/64 counts"),
+        "prepare": ("k_filter", 44 * n + 48 * Cc + 4 * (n / 128),
+                    "44N params + 48C candidate records + 4N/128 counts"),
         "bin": ("k_decide", 48 * Cc + 48 * S + 48 * S + 4 * S + 4 * T + 4 * 1025 * (n / 4096),
-                "48C candidates + 48S records + 48S survivor params + 4S pair bases + 4T slots + bucket table"),
+                "48C candidates + 48S records + 48S survivor params + 4S set indices + 4T slots + bucket table"),
         "sort": ("k_gather" if passes == 1 else "k_sort_pass x passes",
                  8 * T if passes == 1 else 16 * T * passes,
                  "8T (bucketed slots in, tile lists out)" if passes == 1 else "16T per radix pass"),
-        "raster": ("k_raster_fwd", 52 * T + 4 * P, "52T (slot + 48 B record per pair) + 4P image"),
+        "raster": ("k_raster_fwd", 52 * T + 4 * P + (8 * T if u2 and passes == 1 else 0),
+                   "52T (slot + 48 B record per pair) + 4P image"
+                   + (" + 8T fused gather (bucketed slots in, tile lists out)" if u2 and passes == 1 else "")),
         "backward": ("k_raster_bwd", 52 * T + 4 * P + 24 * T + (20 * P if u2 else 0),
                      "52T + 4P dL/dI + 24T partials" + (" + 20P fused SSIM backward" if u2 else "")),
-        "chain": ("k_chain", 48 * S + 48 * S + 24 * T + 44 * S + 4 * S,
-                  "48S records + 48S params + 24T partials + 44S grads + 4S dirty list"),
+        "chain": ("k_chain", 48 * S + 48 * S + 24 * T + 44 * S + (2 * S if u2 else 4 * S),
+                  "48S records + 48S params + 24T partials + 44S gradients"
+                  + (" (by survivor slot) + 2S slot map" if u2 else " + 4S dirty list")),
         "loss": ("k_ssim_fwd", 20 * P, "8P images + 12P SSIM partials (the backward half runs in k_raster_bwd)"),
         # slot-gradient Adam (single-GPU step): the survivors' gradients by slot
         # + a 2 B map per primitive instead of 44 B dense gradient planes

@@ -427,6 +427,13 @@ struct RasterLaunch {
     const float* target;
     float ssim_k, inv_n;           // lambda * dssim_scale, 1/(W*H)
     float w[11];                   // window taps
+    // fused gather (training step, single-pass slices): the forward CTA first
+    // builds its tile's list from K_decide's buckets (k_gather's work) into
+    // vals_out (== vals), or nullptr when the lists are built already
+    const unsigned* bucket_tab;
+    unsigned ngroups, row_stride;
+    const uint32_t* vals_in;
+    uint32_t* vals_out;
 };
 
 struct ChainLaunch {

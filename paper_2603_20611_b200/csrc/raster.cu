@@ -103,6 +103,52 @@ __device__ __forceinline__ void tile_range(const RasterLaunch& a, int tile, unsi
     }
 }
 
+// k_gather's work for one tile (sort.cu): concatenate the K_decide groups'
+// buckets for the tile in group (= ascending slot) order into its list at
+// tile_begin[d]; tiny buckets are ordered by rank. Whole CTA of 256; the list
+// is visible to the CTA after the caller's barrier.
+__device__ __forceinline__ void gather_tile(const RasterLaunch& a, unsigned d) {
+    __shared__ unsigned s_wsum[8];
+    __shared__ unsigned s_chunk_total;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
+    unsigned out = __ldcg(&a.grp_begin[d]);
+    for (unsigned g0 = 0; g0 < a.ngroups; g0 += 256) {
+        const unsigned g = g0 + tid;
+        unsigned b = 0, e = 0;
+        if (g < a.ngroups) {  // group g's bucket for tile d: [row[d], row[d + 1])
+            const unsigned* row = a.bucket_tab + (uint64_t)g * a.row_stride;
+            b = min(__ldcg(&row[d]), P);
+            e = min(__ldcg(&row[d + 1]), P);
+        }
+        const unsigned cnt = e > b ? e - b : 0u;
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        __syncthreads();  // s_wsum of the previous chunk consumed
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        unsigned pos = out + incl - cnt;
+        for (int w = 0; w < warp; ++w) pos += s_wsum[w];
+        if (tid == 255) s_chunk_total = pos + cnt - out;
+        if (cnt == 1) {
+            a.vals_out[pos] = __ldcg(&a.vals_in[b]);
+        } else if (cnt > 1) {
+            for (unsigned i = 0; i < cnt; ++i) {  // rank within the bucket (slots are unique)
+                const uint32_t v = __ldcg(&a.vals_in[b + i]);
+                unsigned r = 0;
+                for (unsigned j = 0; j < cnt; ++j) r += __ldcg(&a.vals_in[b + j]) < v;
+                a.vals_out[pos + r] = v;
+            }
+        }
+        __syncthreads();
+        out += s_chunk_total;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ float4 s_rec[256][2];  // {ox, oy, a*k, 2b*k}, {d*k, alpha_tilde, mask, -}
@@ -110,6 +156,7 @@ __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
+    if (a.bucket_tab) gather_tile(a, (unsigned)tile);  // (ends with a barrier)
     const int tx = tile % a.slice.tiles_x, ty = tile / a.slice.tiles_x;
     const int x0 = tx * kTile, y0 = ty * kTile;
     tile_range(a, tile, s_range);
@@ -129,7 +176,8 @@ __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
         const unsigned nb = min(256u, end - b);
         __syncthreads();
         if (tid < nb) {
-            const SurvivorRecord r = a.records[a.vals[b + tid]];
+            // (L2 load: the list may have been written by this CTA / a neighbour just now)
+            const SurvivorRecord r = a.records[__ldcg(&a.vals[b + tid])];
             s_rec[tid][0] = make_float4((float)(r.mu2d_x - X0), (float)(r.mu2d_y - Y0),
                                         r.conic_a * kNegHalfLog2e, 2.f * r.conic_b * kNegHalfLog2e);
             s_rec[tid][1] = make_float4(r.conic_d * kNegHalfLog2e, r.alpha_tilde,

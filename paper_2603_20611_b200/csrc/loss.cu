@@ -23,6 +23,7 @@ namespace {
 
 constexpr int kT = 32, kR = 5, kH = kT + 2 * kR;  // tile, radius, haloed extent
 constexpr double kC1 = 1e-4, kC2 = 9e-4;         // metrics.hpp:155-156
+constexpr int kSsimThreads = 512;                // 2 output pixels per thread: short latency chains
 
 __device__ __forceinline__ int reflect(int p, int n) {
     while (p < 0 || p >= n) {
@@ -59,7 +60,7 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* s_red) 
 // ... then a fixed warp/block tree): deterministic run to run.
 __device__ __forceinline__ void finish_loss(const LossLaunch& a, bool with_ssim) {
     __shared__ unsigned s_last;
-    __shared__ double s_red2[16];
+    __shared__ double s_red2[2 * 32];
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned nblk = gridDim.x * gridDim.y;
@@ -103,19 +104,37 @@ __global__ void __launch_bounds__(256) k_l1_only(const LossLaunch a) {
     finish_loss(a, false);
 }
 
-__global__ void __launch_bounds__(256) k_ssim_fwd(const LossLaunch a) {
+__global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const LossLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ float s_x[kH][kH + 1];
     __shared__ float s_y[kH][kH + 1];
     __shared__ float s_h[5][kH][kT + 1];
-    __shared__ double s_red[16];
+    __shared__ double s_red[2 * 32];
     const int X0 = blockIdx.x * kT, Y0 = blockIdx.y * kT;
     const int W = a.W, H = a.H;
-    for (int idx = threadIdx.x; idx < kH * kH; idx += blockDim.x) {
-        const int r = idx / kH, c = idx % kH;
-        const int gx = reflect(X0 + c - kR, W), gy = reflect(Y0 + r - kR, H);
-        s_x[r][c] = a.image[(size_t)gy * W + gx];
-        s_y[r][c] = a.target[(size_t)gy * W + gx];
+    {
+        // every load of the haloed tile in flight at once (a load-store loop
+        // would wait one global round trip per element)
+        constexpr int kPer = (kH * kH + kSsimThreads - 1) / kSsimThreads;
+        float vx[kPer], vy[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int idx = threadIdx.x + k * kSsimThreads;
+            if (idx < kH * kH) {
+                const int r = idx / kH, c = idx % kH;
+                const size_t o = (size_t)reflect(Y0 + r - kR, H) * W + reflect(X0 + c - kR, W);
+                vx[k] = a.image[o];
+                vy[k] = a.target[o];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int idx = threadIdx.x + k * kSsimThreads;
+            if (idx < kH * kH) {
+                s_x[idx / kH][idx % kH] = vx[k];
+                s_y[idx / kH][idx % kH] = vy[k];
+            }
+        }
     }
     __syncthreads();
     // rows (axis 0 of conv_nd, metrics.hpp:112-116)
@@ -238,7 +257,7 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(const LossLaunch a) {
 
 void launch_loss_fwd_only(const LossLaunch& a, cudaStream_t st) {
     const dim3 grid((a.W + kT - 1) / kT, (a.H + kT - 1) / kT);
-    launch_pdl(k_ssim_fwd, grid, dim3(256), 0, st, a);
+    launch_pdl(k_ssim_fwd, grid, dim3(kSsimThreads), 0, st, a);
 }
 
 void launch_loss(const LossLaunch& a, cudaStream_t st) {
@@ -249,7 +268,7 @@ void launch_loss(const LossLaunch& a, cudaStream_t st) {
         return;
     }
     const dim3 grid((a.W + kT - 1) / kT, (a.H + kT - 1) / kT);
-    launch_pdl(k_ssim_fwd, dim3(grid), dim3(256), 0, st, a);
+    launch_pdl(k_ssim_fwd, dim3(grid), dim3(kSsimThreads), 0, st, a);
     launch_pdl(k_ssim_bwd, dim3(grid), dim3(256), 0, st, a);
 }
 

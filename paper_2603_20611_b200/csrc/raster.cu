@@ -227,12 +227,31 @@ __device__ __forceinline__ void ssim_dl_tile(const RasterLaunch& a, int x0, int 
     __shared__ float s_h[3][kSsimH][kTile + 1];
     const int W = a.slice.W, H = a.slice.H;
     const size_t P = (size_t)W * H;
-    for (int idx = threadIdx.x; idx < kSsimH * kSsimH; idx += blockDim.x) {
-        const int r = idx / kSsimH, c = idx % kSsimH;
-        const size_t o = (size_t)reflect_idx(y0 + r - kSsimR, H) * W + reflect_idx(x0 + c - kSsimR, W);
-        s_g[0][r][c] = a.ssim_g[o];
-        s_g[1][r][c] = a.ssim_g[P + o];
-        s_g[2][r][c] = a.ssim_g[2 * P + o];
+    {
+        // all loads of the haloed g planes in flight at once, then to shared
+        constexpr int kPer = (kSsimH * kSsimH + 255) / 256;
+        float v[3][kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int idx = threadIdx.x + k * 256;
+            if (idx < kSsimH * kSsimH) {
+                const int r = idx / kSsimH, c = idx % kSsimH;
+                const size_t o = (size_t)reflect_idx(y0 + r - kSsimR, H) * W + reflect_idx(x0 + c - kSsimR, W);
+                v[0][k] = a.ssim_g[o];
+                v[1][k] = a.ssim_g[P + o];
+                v[2][k] = a.ssim_g[2 * P + o];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int idx = threadIdx.x + k * 256;
+            if (idx < kSsimH * kSsimH) {
+                const int r = idx / kSsimH, c = idx % kSsimH;
+                s_g[0][r][c] = v[0][k];
+                s_g[1][r][c] = v[1][k];
+                s_g[2][r][c] = v[2][k];
+            }
+        }
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < kSsimH * kTile; idx += blockDim.x) {

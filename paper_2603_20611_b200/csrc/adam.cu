@@ -28,8 +28,9 @@ __global__ void k_adam_consts(const AdamLaunch a) {
     if (threadIdx.x == 0) *a.consts = c;
 }
 
-template <bool kSlots>
-__global__ void __launch_bounds__(256, 6) k_adam(const AdamLaunch a) {
+// (6 CTAs/SM: 40 registers; 7-8 CTAs/SM spill and measured slower)
+template <bool kSlots, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) k_adam(const AdamLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * kAdamItems;
     if (i0 >= a.n) return;  // the capacity is a multiple of 512: vector accesses stay in the plane
@@ -37,7 +38,9 @@ __global__ void __launch_bounds__(256, 6) k_adam(const AdamLaunch a) {
         if (kSlots) adam_slots_clear<kAdamItems>(a, i0);
         return;
     }
-    const AdamConsts c = *a.consts;
+    // read in place (L1) where used: the constants would otherwise hold 12
+    // registers for the whole kernel
+    const AdamConsts& c = *a.consts;
     adam_advance_step(a, c);
     uint32_t gslot[kAdamItems];
     const bool any = kSlots && adam_slots<kAdamItems>(a, i0, gslot);
@@ -76,8 +79,8 @@ void launch_adam(const AdamLaunch& a, cudaStream_t st) {
     // best on B200 among 1/2/4 items per thread, persistent grid or not
     const unsigned grid = (a.n + 256 * kAdamItems - 1) / (256 * kAdamItems);
     if (!grid) return;
-    if (a.slot_grads) launch_pdl(k_adam<true>, dim3(grid), dim3(256), 0, st, a);
-    else launch_pdl(k_adam<false>, dim3(grid), dim3(256), 0, st, a);
+    if (a.slot_grads) launch_pdl(k_adam<true, 6>, dim3(grid), dim3(256), 0, st, a);
+    else launch_pdl(k_adam<false, 6>, dim3(grid), dim3(256), 0, st, a);
 }
 
 }  // namespace gpk

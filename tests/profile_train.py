@@ -18,15 +18,16 @@ from paper_2603_20611_b200 import _native as N  # noqa: E402
 def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     pipelined = not (len(sys.argv) > 2 and sys.argv[2] == "plain")
-    dims = (512, 512, 128)
-    lo, hi = (-0.5, -0.5, -0.5), (511.5, 511.5, 127.5)
-    gs = gp.init_random(1_000_000, lo, hi, 1.5, 1)
+    big = len(sys.argv) > 3 and sys.argv[3] == "c5"  # 2048^2 x 256, 8M Gaussians
+    dims = (2048, 2048, 256) if big else (512, 512, 128)
+    lo, hi = (-0.5, -0.5, -0.5), tuple(d - 0.5 for d in dims)
+    gs = gp.init_random(8_000_000 if big else 1_000_000, lo, hi, 1.5, 1)
     s = gp.Session(0)
     s.set_gaussians(gp.GaussianSet(gs.records.astype(np.float32).astype(np.float64), lo, hi))
-    s.reserve_pairs(1 << 20)
+    s.reserve_pairs(1 << 21 if big else 1 << 20)
     psf, cfg = gp.PsfSpec(), gp.RasterConfig()
-    poses = [gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), 64 + i) for i in range(4)]
-    tgt = np.random.default_rng(7).uniform(0, 0.1, (512, 512)).astype(np.float32)
+    poses = [gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), dims[2] // 2 + i) for i in range(4)]
+    tgt = np.random.default_rng(7).uniform(0, 0.1, (dims[1], dims[0])).astype(np.float32)
     s.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
     lr = gp.LearningRates(6e-4, 0.02, 2e-3, 1e-3)
     for i in range(steps):

@@ -129,6 +129,12 @@ __device__ __forceinline__ void load_params(const float* __restrict__ params, ui
 //   <=  0.5 mcz^2 > X_up * (X_up >= 0 ? den_hi : sz2),  X_up >= T + M.
 // Undecided items take the full test, compacted, so the warp does not pay it
 // for every Gaussian.
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ bool quick_culled_identity(const float p[11], const FilterConsts& c) {
     // Branch-free (the four items of a lane interleave): the guards are folded
     // into the result with bitwise ANDs instead of early returns.
@@ -145,8 +151,10 @@ __device__ __forceinline__ bool quick_culled_identity(const float p[11], const F
     const float mu2 = __fmaf_rn(mcx, mcx, __fmaf_rn(mcy, mcy, mcz * mcz));
     // e^(2 lmax) mod^2 = (mod s_max)^2 ; e^(-2 lmin) / mod^2 = 1 / (mod s_min)^2
     // (the clamps only keep the exponentials finite where the guards reject)
-    const float den_hi = __fmaf_rn(__expf(2.f * fminf(lmax, 40.f)) * c.mod2, 1.0002f, c.sz2);
-    const float inv_smin2 = __expf(-2.f * fmaxf(lmin, -40.f)) * c.inv_mod2 * 1.0002f;
+    // (MUFU.EX2 with flush-to-zero: the arguments stay within +-116, so no
+    // denormal range fix-up is needed; ~2 ulp, inside the 2e-4 factor)
+    const float den_hi = __fmaf_rn(ex2_ftz(fminf(lmax, 40.f) * 2.8853900817779268f) * c.mod2, 1.0002f, c.sz2);
+    const float inv_smin2 = ex2_ftz(fmaxf(lmin, -40.f) * -2.8853900817779268f) * c.inv_mod2 * 1.0002f;
     const float thresh_hi = fminf(p[10], 0.f) - c.log_tau;
     const float noise = __fmaf_rn(2e-14f * mu2, inv_smin2,
                                   4.8e-7f * fabsf(mcz) * (fabsf(p[2]) + fabsf(c.tz_hi)) * c.inv_sz2 * 1.0002f);

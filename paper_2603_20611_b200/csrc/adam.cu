@@ -32,7 +32,7 @@ __global__ void k_adam_consts(const AdamLaunch a) {
 template <bool kSlots, int kMinB>
 __global__ void __launch_bounds__(256, kMinB) k_adam(const AdamLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * kAdamItems;
+    const uint32_t i0 = a.lo + (blockIdx.x * blockDim.x + threadIdx.x) * kAdamItems;
     if (i0 >= a.n) return;  // the capacity is a multiple of 512: vector accesses stay in the plane
     if (a.ctrl && a.ctrl->pair_overflow) {  // the slice overflowed: no update
         if (kSlots) adam_slots_clear<kAdamItems>(a, i0);
@@ -77,8 +77,8 @@ void launch_adam_consts(const AdamLaunch& a, cudaStream_t st) {
 void launch_adam(const AdamLaunch& a, cudaStream_t st) {
     // 2 primitives per thread, registers capped for 6 CTAs per SM: measured
     // best on B200 among 1/2/4 items per thread, persistent grid or not
-    const unsigned grid = (a.n + 256 * kAdamItems - 1) / (256 * kAdamItems);
-    if (!grid) return;
+    const unsigned grid = (a.n - a.lo + 256 * kAdamItems - 1) / (256 * kAdamItems);
+    if (!grid || a.n <= a.lo) return;
     if (a.slot_grads) launch_pdl(k_adam<true, 6>, dim3(grid), dim3(256), 0, st, a);
     else launch_pdl(k_adam<false, 6>, dim3(grid), dim3(256), 0, st, a);
 }

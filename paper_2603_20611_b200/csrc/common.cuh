@@ -473,7 +473,8 @@ struct AdamLaunch {
     float* m;
     float* v;
     uint64_t cap;
-    uint32_t n;
+    uint32_t n;           // primitives [lo, n) are updated (lo > 0: this rank's shard)
+    uint32_t lo;
     float bbox_min[3], bbox_max[3];
     double lr[4];         // position, opacity, scale, rotation (or lr0 when scheduled)
     int scheduled;        // lr = lr0 * 0.1^((step-1)/total)

@@ -105,6 +105,9 @@ struct gpk_session {
     cudaStream_t copy = nullptr;
     cudaEvent_t ev_tgt_fork = nullptr, ev_tgt_ready = nullptr;
     bool tgt_pending = false;
+    // data parallelism (gpk_comm_init): this session's NCCL communicator
+    void* comm = nullptr;
+    int comm_rank = 0, comm_world = 1;
     bool consts_pending = false;  // k_adam_consts was launched ahead (wait on ev_cjoin)
     uint64_t n = 0, cap = 0;
     gpk_bounds bbox{};
@@ -901,8 +904,9 @@ int adam_consts_ready(gpk_session* s, const AdamLaunch& a) {
     return GPK_OK;
 }
 
+// lo, hi: the primitives to update (a data-parallel rank's shard), default all
 int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
-             const gpk_adam_hparams* hp) {
+             const gpk_adam_hparams* hp, uint64_t lo = 0, uint64_t hi = ~0ull) {
     if (s->n == 0) {
         s->consts_pending = false;
         long long st = 0;
@@ -914,6 +918,8 @@ int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
         return GPK_OK;
     }
     AdamLaunch a = adam_launch(s, lr, scheduled, total, hp);
+    a.lo = (uint32_t)std::min<uint64_t>(lo, s->n);
+    a.n = (uint32_t)std::min<uint64_t>(hi, s->n);
     TRY(adam_grad_source(s, a));
     s->prefilter.valid = false;  // the parameters change
     StageScope scope(s, GPK_STAGE_ADAM);
@@ -1227,6 +1233,7 @@ int gpk_session_destroy(gpk_session* s) {
     }
     if (s->ev_tgt_fork) cudaEventDestroy(s->ev_tgt_fork);
     if (s->ev_tgt_ready) cudaEventDestroy(s->ev_tgt_ready);
+    if (s->comm) gpk_comm_destroy(s);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
     return ok();
@@ -1695,10 +1702,15 @@ int gpk_fwd_bwd_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf*
     return ok();
 }
 
-// Data-parallel training: with a communicator, the dense gradient planes are
-// summed over the ranks between backward and Adam (defined with the NCCL code).
-static int dp_allreduce_if_comm(gpk_session* s);
+// Data-parallel training (defined with the NCCL code): the dense gradient
+// planes are reduce-scattered, each rank updates its shard, the parameter
+// shards are all-gathered; a plain all-reduce when the shards would not tile
+// the planes.
 static void*& session_comm(gpk_session* s);
+static uint64_t dp_chunk(gpk_session* s);
+static int dp_reduce_scatter(gpk_session* s);
+static int dp_all_gather_params(gpk_session* s);
+static int dp_all_reduce(gpk_session* s);
 
 // One training step (optimize.hpp:385-402): prepare, rasterize, photometric
 // loss, backward, (all-reduce), scheduled Adam. The gradient is kept by
@@ -1717,9 +1729,16 @@ static int train_body_(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf
     s->assume_prefiltered = false;
     TRY(run_rasterize(s));
     TRY(run_loss(s, lambda, dssim_scale, true));
-    TRY(run_backward(s, false, /*slots=*/session_comm(s) == nullptr));  // dense planes for the all-reduce
-    TRY(dp_allreduce_if_comm(s));
-    if (next) return run_adam_cull(s, lr, total, next, psf, cfg);
+    const bool dp = session_comm(s) != nullptr;
+    TRY(run_backward(s, false, /*slots=*/!dp));  // dense planes for the collectives
+    if (dp && s->n && s->cap % (uint64_t)s->comm_world == 0) {
+        TRY(dp_reduce_scatter(s));
+        const uint64_t chunk = dp_chunk(s), lo = (uint64_t)s->comm_rank * chunk;
+        TRY(run_adam(s, lr, true, total, nullptr, lo, lo + chunk));
+        return dp_all_gather_params(s);
+    }
+    if (dp) TRY(dp_all_reduce(s));
+    if (next && !dp) return run_adam_cull(s, lr, total, next, psf, cfg);
     return run_adam(s, lr, true, total, nullptr);
 }
 
@@ -1879,6 +1898,8 @@ int gpk_graph_capture_train_next(gpk_session* s, const gpk_slice_pose* pose, con
                                  const gpk_learning_rates* lr0, int32_t total_iterations,
                                  const gpk_slice_pose* next_pose, int32_t* graph_id) {
     if (!lr0 || !next_pose || total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "bad arguments");
+    if (session_comm(s))  // data parallel: the shard-wise Adam has no fused cull
+        return gpk_graph_capture_train(s, pose, psf, cfg, lambda, dssim_scale, lr0, total_iterations, graph_id);
     TRY(presize_step(s, pose, psf, cfg, true, lambda));
     const TrainNextArgs args{pose, psf, cfg, lambda, dssim_scale, lr0, total_iterations, next_pose};
     s->capture_meta.needs_prefilter = true;
@@ -1960,6 +1981,10 @@ struct NcclApi {
     int (*get_unique_id)(void*) = nullptr;
     int (*comm_init_rank)(void**, int, NcclId, int) = nullptr;
     int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*reduce_scatter)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+    int (*group_start)() = nullptr;
+    int (*group_end)() = nullptr;
     int (*comm_destroy)(void*) = nullptr;
     const char* (*get_error_string)(int) = nullptr;
 };
@@ -1980,18 +2005,20 @@ static NcclApi* nccl() {
             api.all_reduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
                 api.lib, "ncclAllReduce");
             api.comm_destroy = (int (*)(void*))dlsym(api.lib, "ncclCommDestroy");
+            api.reduce_scatter = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+                api.lib, "ncclReduceScatter");
+            api.all_gather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(
+                api.lib, "ncclAllGather");
+            api.group_start = (int (*)())dlsym(api.lib, "ncclGroupStart");
+            api.group_end = (int (*)())dlsym(api.lib, "ncclGroupEnd");
             api.get_error_string = (const char* (*)(int))dlsym(api.lib, "ncclGetErrorString");
         }
     }
     return (api.get_unique_id && api.comm_init_rank && api.all_reduce) ? &api : nullptr;
 }
 
-static void* g_comms[64] = {nullptr};
 
-static void*& session_comm(gpk_session* s) {
-    // one communicator per device ordinal
-    return g_comms[s->device & 63];
-}
+static void*& session_comm(gpk_session* s) { return s->comm; }
 
 int gpk_nccl_get_unique_id(void* id_out128) {
     NcclApi* api = nccl();
@@ -2014,6 +2041,8 @@ int gpk_comm_init(gpk_session* s, int nranks, int rank, const void* id128) {
         return fail(GPK_ERR_NCCL, std::string("ncclCommInitRank: ") +
                                       (api->get_error_string ? api->get_error_string(r) : "error"));
     session_comm(s) = comm;
+    s->comm_rank = rank;
+    s->comm_world = nranks;
     return ok();
 }
 
@@ -2023,18 +2052,64 @@ int gpk_comm_destroy(gpk_session* s) {
     void*& comm = session_comm(s);
     if (api && comm && api->comm_destroy) api->comm_destroy(comm);
     comm = nullptr;
+    s->comm_rank = 0;
+    s->comm_world = 1;
     return ok();
 }
 
-static int dp_allreduce_if_comm(gpk_session* s) {
-    void* comm = session_comm(s);
-    if (!comm) return GPK_OK;
+// Data-parallel training step, ZeRO-style: the summed
+// gradient is only needed by the Adam that updates it, so each rank
+// reduce-scatters the dense planes (rank r receives the sum over primitives
+// [r*chunk, (r+1)*chunk) of every plane), runs Adam on that shard and the
+// parameter shards are all-gathered. Same traffic as one all-reduce, Adam work
+// / world, and every replica ends bitwise equal (one owner per primitive).
+static uint64_t dp_chunk(gpk_session* s) { return s->cap / (uint64_t)s->comm_world; }
+
+static int dp_all_reduce(gpk_session* s) {
     NcclApi* api = nccl();
     if (!api) return fail(GPK_ERR_NCCL, "NCCL not available");
-    const int r = api->all_reduce(s->grads.p, s->grads.p, s->cap * 11, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm,
-                                  s->stream);
-    if (r != 0) return fail(GPK_ERR_NCCL, "ncclAllReduce failed");
-    return mark_grads_dense(s);
+    if (api->all_reduce(s->grads.p, s->grads.p, s->cap * 11, /*ncclFloat32*/ 7, /*ncclSum*/ 0, s->comm, s->stream) != 0)
+        return fail(GPK_ERR_NCCL, "ncclAllReduce failed");
+    return mark_grads_dense(s);  // non-zero wherever any rank had survivors
+}
+
+static int dp_reduce_scatter(gpk_session* s) {
+    NcclApi* api = nccl();
+    if (!api || !api->reduce_scatter || !api->group_start) return fail(GPK_ERR_NCCL, "NCCL not available");
+    const uint64_t chunk = dp_chunk(s);
+    float* g = s->grads.as<float>();
+    if (api->group_start() != 0) return fail(GPK_ERR_NCCL, "ncclGroupStart failed");
+    for (int k = 0; k < 11; ++k) {
+        float* plane = g + (size_t)k * s->cap;  // in place: recv = send + rank * chunk
+        if (api->reduce_scatter(plane, plane + (size_t)s->comm_rank * chunk, chunk, /*ncclFloat32*/ 7, /*ncclSum*/ 0,
+                                s->comm, s->stream) != 0)
+            return fail(GPK_ERR_NCCL, "ncclReduceScatter failed");
+    }
+    if (api->group_end() != 0) return fail(GPK_ERR_NCCL, "ncclGroupEnd failed");
+    return GPK_OK;
+}
+
+static int dp_all_gather_params(gpk_session* s) {
+    NcclApi* api = nccl();
+    if (!api || !api->all_gather || !api->group_start) return fail(GPK_ERR_NCCL, "NCCL not available");
+    const uint64_t chunk = dp_chunk(s);
+    float* p = s->params.as<float>();
+    if (api->group_start() != 0) return fail(GPK_ERR_NCCL, "ncclGroupStart failed");
+    for (int k = 0; k < 11; ++k) {
+        float* plane = p + (size_t)k * s->cap;  // in place: send = recv + rank * chunk
+        if (api->all_gather(plane + (size_t)s->comm_rank * chunk, plane, chunk, /*ncclFloat32*/ 7, s->comm,
+                            s->stream) != 0)
+            return fail(GPK_ERR_NCCL, "ncclAllGather failed");
+    }
+    if (api->group_end() != 0) return fail(GPK_ERR_NCCL, "ncclGroupEnd failed");
+    // the shard of the dense planes now holds other ranks' gradients too:
+    // zero it (the sparse clear of the next prepare covers this rank's own
+    // survivors elsewhere)
+    const uint64_t chunk_bytes = chunk * 4;
+    for (int k = 0; k < 11; ++k)
+        CK(cudaMemsetAsync(s->grads.as<float>() + (size_t)k * s->cap + (size_t)s->comm_rank * chunk, 0, chunk_bytes,
+                           s->stream));
+    return GPK_OK;
 }
 
 int gpk_allreduce_grads(gpk_session* s) {

@@ -8,7 +8,10 @@
 * the exchange algebra: each rank's dense gradient of its own slice (the C
   oracle stands in for the device backward), summed by an all-reduce, equals
   the serial sum over the step's slices — what ncclAllReduce(sum) over the
-  11-plane buffer computes on the GPUs.
+  11-plane buffer computes on the GPUs;
+* the training step's ZeRO-style update: reduce the summed gradient to each
+  primitive's owner, Adam on the owner's shard only, all-gather the parameter
+  shards — every replica ends bitwise equal to the full all-reduce + full Adam.
 """
 from __future__ import annotations
 
@@ -74,6 +77,30 @@ def _worker(rank, world, port, q):
             dist.all_reduce(t)  # the exchange: sum of per-slice dense gradients
             sums.append(t.numpy().copy())
         out["sums"] = sums
+        # sharded Adam: owner r holds primitives [r*chunk, (r+1)*chunk)
+        n = rec.shape[0]
+        chunk = (n + world - 1) // world
+        bbox = ((-0.5, -0.5, -0.5), (31.5, 23.5, 7.5))
+        lrs = (6e-4, 0.02, 2e-3, 1e-3)
+        k = dp.slice_for(0, rank, world, len(poses))
+        g, _ = oracle.backward(rec, poses[k], psf, cfg, dl[k])
+        full = torch.from_numpy(np.array(g, copy=True))
+        for r in range(world):  # reduce-scatter: each shard summed onto its owner
+            part = full[r * chunk:min(n, (r + 1) * chunk)].clone()  # (gloo may scribble on non-root inputs)
+            dist.reduce(part, dst=r)
+            if r == rank:
+                mine = part.numpy().copy()
+        lo, hi = rank * chunk, min(n, (rank + 1) * chunk)
+        p = rec[lo:hi].copy()
+        m = np.zeros_like(p)
+        v = np.zeros_like(p)
+        p, m, v = oracle.adam_step(p, bbox, mine, m, v, 0, lrs)[:3]
+        shards = [torch.zeros((chunk, 11), dtype=torch.float64) for _ in range(world)]
+        mine_p = torch.zeros((chunk, 11), dtype=torch.float64)
+        mine_p[:hi - lo] = torch.from_numpy(np.ascontiguousarray(p))
+        dist.all_gather(shards, mine_p)  # the parameter shards to every replica
+        out["zero_params"] = torch.cat(shards)[:n].numpy()
+        out["zero_grads"] = np.array(g, copy=True)
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -121,3 +148,10 @@ def test_gloo_world2_exchange():
         for r in (0, 1):
             assert np.allclose(res[r]["sums"][step], want, rtol=1e-12, atol=1e-15)
         assert np.array_equal(res[0]["sums"][step], res[1]["sums"][step])  # replicas stay equal
+    # sharded update == all-reduce + full Adam, bitwise, on both replicas
+    g_sum = res[0]["zero_grads"] + res[1]["zero_grads"]
+    bbox = ((-0.5, -0.5, -0.5), (31.5, 23.5, 7.5))
+    want = oracle.adam_step(rec.copy(), bbox, g_sum, np.zeros_like(rec), np.zeros_like(rec), 0,
+                            (6e-4, 0.02, 2e-3, 1e-3))[0]
+    assert np.array_equal(res[0]["zero_params"], res[1]["zero_params"])
+    assert np.array_equal(res[0]["zero_params"], want)

@@ -526,9 +526,12 @@ def run_ours(args):
         "adam": ("k_adam_cull", 266 * n + 44 * S + 48 * Cc,
                  "266N + 44S: read params, m, v, 2 B slot map; write params, m, v; survivor gradients "
                  "+ 48C next-slice candidates")
-        if (u2 and args.pipeline) else
+        if (u2 and args.pipeline and world == 1) else
         ("k_adam", 266 * n + 44 * S,
-         "266N + 44S: read params, m, v, 2 B slot map; write params, m, v; survivor gradients"),
+         "266N + 44S: read params, m, v, 2 B slot map; write params, m, v; survivor gradients")
+        if world == 1 else
+        ("k_adam", 308 * n / world,
+         "308N/world: the rank's shard (read params, dense gradients, m, v; write params, m, v)"),
     }
     measured = {k: v for k, v in stages.items() if v[1] > 0 and k in kernel_bytes}
     dom = max(measured, key=lambda k: measured[k][0])
@@ -548,7 +551,8 @@ def run_ours(args):
     # U2 floor with slot gradients: 44N cull read + 264N Adam (p, m, v read and
     # written) + 2N slot map (SURVEY.md §8d's 396N assumed dense gradient
     # planes: +44N Adam read, +44N clear)
-    step_bytes = (310 * n + 8 * P) if u2 else (88 * n + 8 * P)
+    step_bytes = ((310 * n + 8 * P) if world == 1 else (44 * n + 308 * n / world + 8 * P)) if u2 \
+        else (88 * n + 8 * P)
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
 
     line = {
@@ -558,8 +562,9 @@ def run_ours(args):
         "data": data_note(args.unit), "config": config_json(args, cfg, world),
         "roofline": roof,
         "step_roofline": {"bytes_per_step": step_bytes, "achieved_gbs": step_gbs, "frac": step_gbs / peak,
-                          "formula": ("310N + 8P (U2 with slot gradients; SURVEY.md §8d: 396N dense)" if u2
-                                      else "88N + 8P (U1, SURVEY.md §8d)")},
+                          "formula": (("310N + 8P (U2 with slot gradients; SURVEY.md §8d: 396N dense)" if world == 1
+                                       else "44N + 308N/world + 8P per rank (U2, sharded Adam; collectives excluded)")
+                                      if u2 else "88N + 8P (U1, SURVEY.md §8d)")},
         "stage_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in stages.items() if v[1]},
         "kernels": per_kernel,
         "submission": "CUDA graph per slice pose" if graphs is not None else "kernel by kernel",

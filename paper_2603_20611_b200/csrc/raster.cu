@@ -227,6 +227,14 @@ __device__ __forceinline__ void ssim_dl_tile(const RasterLaunch& a, int x0, int 
     __shared__ float s_h[3][kSsimH][kTile + 1];
     const int W = a.slice.W, H = a.slice.H;
     const size_t P = (size_t)W * H;
+    float px = 0.f, py = 0.f;  // this thread's pixel, requested first
+    {
+        const int pi = x0 + (threadIdx.x & 15), pj = y0 + (threadIdx.x >> 4);
+        if (pi < W && pj < H) {
+            px = a.image[(size_t)pj * W + pi];
+            py = a.target[(size_t)pj * W + pi];
+        }
+    }
     {
         // all loads of the haloed g planes in flight at once, then to shared
         constexpr int kPer = (kSsimH * kSsimH + 255) / 256;
@@ -254,35 +262,46 @@ __device__ __forceinline__ void ssim_dl_tile(const RasterLaunch& a, int x0, int 
         }
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < kSsimH * kTile; idx += blockDim.x) {
-        const int r = idx / kTile, c = idx % kTile;
-        float h0 = 0.f, h1 = 0.f, h2 = 0.f;
+    // rows: a thread filters 8 consecutive outputs of one plane row from 18
+    // inputs held in registers (each output still sums its 11 taps in order)
+    if (threadIdx.x < kSsimH * 3 * 2) {
+        const int r = threadIdx.x / 6, q = (threadIdx.x % 6) >> 1, c0 = (threadIdx.x & 1) * 8;
+        float v[8 + 2 * kSsimR];
 #pragma unroll
-        for (int t = 0; t < 2 * kSsimR + 1; ++t) {
-            const float w = a.w[t];
-            h0 += w * s_g[0][r][c + t];
-            h1 += w * s_g[1][r][c + t];
-            h2 += w * s_g[2][r][c + t];
+        for (int t = 0; t < 8 + 2 * kSsimR; ++t) v[t] = s_g[q][r][c0 + t];
+#pragma unroll
+        for (int o = 0; o < 8; ++o) {
+            float h = 0.f;
+#pragma unroll
+            for (int t = 0; t < 2 * kSsimR + 1; ++t) h += a.w[t] * v[o + t];
+            s_h[q][r][c0 + o] = h;
         }
-        s_h[0][r][c] = h0;
-        s_h[1][r][c] = h1;
-        s_h[2][r][c] = h2;
+    }
+    __syncthreads();
+    // columns: a thread filters 4 consecutive outputs of one plane column from
+    // 14 inputs in registers, into s_g (free now) as A[q][row][col]
+    float(*s_A)[kTile][kTile + 1] = reinterpret_cast<float(*)[kTile][kTile + 1]>(&s_g[0][0][0]);
+    if (threadIdx.x < 3 * kTile * 4) {
+        const int q = threadIdx.x / (kTile * 4), c = threadIdx.x % kTile, r0 = ((threadIdx.x / kTile) & 3) * 4;
+        float v[4 + 2 * kSsimR];
+#pragma unroll
+        for (int t = 0; t < 4 + 2 * kSsimR; ++t) v[t] = s_h[q][r0 + t][c];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            float acc = 0.f;
+#pragma unroll
+            for (int t = 0; t < 2 * kSsimR + 1; ++t) acc += a.w[t] * v[o + t];
+            s_A[q][r0 + o][c] = acc;
+        }
     }
     __syncthreads();
     const int r = threadIdx.x >> 4, c = threadIdx.x & 15;
     const int i = x0 + c, j = y0 + r;
     float dl = 0.f;
     if (i < W && j < H) {
-        float A0 = 0.f, A1 = 0.f, A2 = 0.f;
-#pragma unroll
-        for (int t = 0; t < 2 * kSsimR + 1; ++t) {
-            const float w = a.w[t];
-            A0 += w * s_h[0][r + t][c];
-            A1 += w * s_h[1][r + t][c];
-            A2 += w * s_h[2][r + t][c];
-        }
+        const float x = px, y = py;
+        const float A0 = s_A[0][r][c], A1 = s_A[1][r][c], A2 = s_A[2][r][c];
         const size_t o = (size_t)j * W + i;
-        const float x = a.image[o], y = a.target[o];
         const float gs = A0 + 2.f * x * A1 + y * A2;
         const float d = x - y;
         dl = (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) * a.inv_n + a.ssim_k * (-gs);

@@ -23,7 +23,7 @@ namespace {
 
 constexpr int kT = 32, kR = 5, kH = kT + 2 * kR;  // tile, radius, haloed extent
 constexpr double kC1 = 1e-4, kC2 = 9e-4;         // metrics.hpp:155-156
-constexpr int kSsimThreads = 512;                // 2 output pixels per thread: short latency chains
+constexpr int kSsimThreads = 512;                // 2 output pixels per thread (column pairs)
 
 __device__ __forceinline__ int reflect(int p, int n) {
     while (p < 0 || p >= n) {
@@ -137,59 +137,82 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const LossLaunch a) {
         }
     }
     __syncthreads();
-    // rows (axis 0 of conv_nd, metrics.hpp:112-116)
-    for (int idx = threadIdx.x; idx < kH * kT; idx += blockDim.x) {
-        const int r = idx / kT, c = idx % kT;
-        float hx = 0.f, hy = 0.f, hxx = 0.f, hxy = 0.f, hyy = 0.f;
+    // rows (axis 0 of conv_nd, metrics.hpp:112-116): a thread filters 4
+    // consecutive outputs from 14 samples in registers (each output still sums
+    // its 11 taps in order)
+    for (int item = threadIdx.x; item < kH * (kT / 4); item += blockDim.x) {
+        const int r = item / (kT / 4), c0 = (item % (kT / 4)) * 4;
+        float x[4 + 2 * kR], y[4 + 2 * kR];
 #pragma unroll
-        for (int t = 0; t < 2 * kR + 1; ++t) {
-            const float x = s_x[r][c + t], y = s_y[r][c + t], w = a.w[t];
-            hx += w * x;
-            hy += w * y;
-            hxx += w * x * x;
-            hxy += w * x * y;
-            hyy += w * y * y;
+        for (int t = 0; t < 4 + 2 * kR; ++t) {
+            x[t] = s_x[r][c0 + t];
+            y[t] = s_y[r][c0 + t];
         }
-        s_h[0][r][c] = hx;
-        s_h[1][r][c] = hy;
-        s_h[2][r][c] = hxx;
-        s_h[3][r][c] = hxy;
-        s_h[4][r][c] = hyy;
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            float hx = 0.f, hy = 0.f, hxx = 0.f, hxy = 0.f, hyy = 0.f;
+#pragma unroll
+            for (int t = 0; t < 2 * kR + 1; ++t) {
+                const float xv = x[o + t], yv = y[o + t], w = a.w[t];
+                hx += w * xv;
+                hy += w * yv;
+                hxx += w * xv * xv;
+                hxy += w * xv * yv;
+                hyy += w * yv * yv;
+            }
+            s_h[0][r][c0 + o] = hx;
+            s_h[1][r][c0 + o] = hy;
+            s_h[2][r][c0 + o] = hxx;
+            s_h[3][r][c0 + o] = hxy;
+            s_h[4][r][c0 + o] = hyy;
+        }
     }
     __syncthreads();
     const double inv_n = 1.0 / ((double)W * (double)H);
     double ssum = 0.0, l1 = 0.0;
     const size_t P = (size_t)W * H;
-    for (int idx = threadIdx.x; idx < kT * kT; idx += blockDim.x) {
-        const int r = idx / kT, c = idx % kT;
-        const int i = X0 + c, j = Y0 + r;
-        if (i >= W || j >= H) continue;
-        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    // columns: a thread owns 2 vertically adjacent pixels (12 samples per moment)
+    {
+        const int c = threadIdx.x % kT, r0 = (threadIdx.x / kT) * 2;
+        float m[2][5];
 #pragma unroll
-        for (int t = 0; t < 2 * kR + 1; ++t) {
-            const float w = a.w[t];
+        for (int q = 0; q < 5; ++q) {
+            float v[2 + 2 * kR];
 #pragma unroll
-            for (int q = 0; q < 5; ++q) m[q] += w * s_h[q][r + t][c];
+            for (int t = 0; t < 2 + 2 * kR; ++t) v[t] = s_h[q][r0 + t][c];
+#pragma unroll
+            for (int o = 0; o < 2; ++o) {
+                float acc = 0.f;
+#pragma unroll
+                for (int t = 0; t < 2 * kR + 1; ++t) acc += a.w[t] * v[o + t];
+                m[o][q] = acc;
+            }
         }
-        // metrics.hpp:199-215, evaluated in double per pixel
-        const double mx = m[0], my = m[1];
-        const double vx = m[2] - mx * mx, vy = m[4] - my * my, vxy = m[3] - mx * my;
-        const double a1 = 2.0 * mx * my + kC1, a2 = 2.0 * vxy + kC2;
-        const double b1 = mx * mx + my * my + kC1, b2 = vx + vy + kC2;
-        // one fp64 reciprocal instead of four divisions (metrics.hpp:205-215)
-        const double inv_b1b2 = 1.0 / (b1 * b2);
-        const double s = a1 * a2 * inv_b1b2;
-        const double inv_b1 = b2 * inv_b1b2, inv_b2 = b1 * inv_b1b2;
-        const double ds_dm2 = -s * inv_b2;
-        const double ds_dm12 = 2.0 * a1 * inv_b1b2;
-        const double ds_dm1 = 2.0 * my * a2 * inv_b1b2 - 2.0 * mx * s * inv_b1 + 2.0 * mx * s * inv_b2 -
-                              2.0 * my * a1 * inv_b1b2;
-        const size_t o = (size_t)j * W + i;
-        a.g[o] = (float)(ds_dm1 * inv_n);
-        a.g[P + o] = (float)(ds_dm2 * inv_n);
-        a.g[2 * P + o] = (float)(ds_dm12 * inv_n);
-        ssum += s;
-        l1 += fabs((double)(s_x[r + kR][c + kR] - s_y[r + kR][c + kR]));
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+            const int r = r0 + o;
+            const int i = X0 + c, j = Y0 + r;
+            if (i >= W || j >= H) continue;
+            // metrics.hpp:199-215, evaluated in double per pixel
+            const double mx = m[o][0], my = m[o][1];
+            const double vx = m[o][2] - mx * mx, vy = m[o][4] - my * my, vxy = m[o][3] - mx * my;
+            const double a1 = 2.0 * mx * my + kC1, a2 = 2.0 * vxy + kC2;
+            const double b1 = mx * mx + my * my + kC1, b2 = vx + vy + kC2;
+            // one fp64 reciprocal instead of four divisions (metrics.hpp:205-215)
+            const double inv_b1b2 = 1.0 / (b1 * b2);
+            const double s = a1 * a2 * inv_b1b2;
+            const double inv_b1 = b2 * inv_b1b2, inv_b2 = b1 * inv_b1b2;
+            const double ds_dm2 = -s * inv_b2;
+            const double ds_dm12 = 2.0 * a1 * inv_b1b2;
+            const double ds_dm1 = 2.0 * my * a2 * inv_b1b2 - 2.0 * mx * s * inv_b1 + 2.0 * mx * s * inv_b2 -
+                                  2.0 * my * a1 * inv_b1b2;
+            const size_t off = (size_t)j * W + i;
+            a.g[off] = (float)(ds_dm1 * inv_n);
+            a.g[P + off] = (float)(ds_dm2 * inv_n);
+            a.g[2 * P + off] = (float)(ds_dm12 * inv_n);
+            ssum += s;
+            l1 += fabs((double)(s_x[r + kR][c + kR] - s_y[r + kR][c + kR]));
+        }
     }
     block_sum2(ssum, l1, s_red);
     if (threadIdx.x == 0) {

@@ -346,6 +346,8 @@ struct PrepLaunch {
     SurvivorRecord* records;  // indexed by candidate slot
     uint32_t* survivor_list;  // survivor slot -> set index (K_decide)
     uint32_t* exact_list;     // slots of the fp64-decided survivors (count: Control::chain_exact)
+    unsigned* head;           // K_filter: zero these head_words first (the control head), or nullptr
+    unsigned head_words;
     uint32_t* keys;           // pre-sort tile keys
     uint32_t* vals;           // pre-sort candidate slots
     uint64_t pair_cap;

@@ -364,6 +364,8 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter(const PrepLaunch a
 
     const unsigned dirty = kZeroGrads ? *a.grads_dirty : 0u;
     const bool dense_zero = kZeroGrads && dirty == kGradsDense;
+    if (a.head)  // the prepare's control head (no separate memset)
+        for (unsigned w = gtid; w < a.head_words; w += gthreads) a.head[w] = 0u;
     clear_prev_sort_rows(a, gtid, gthreads);
     if (kZeroGrads && !dense_zero)  // the previous survivors' gradients (sparse mode)
         for (unsigned e = gtid; e < dirty; e += gthreads) {

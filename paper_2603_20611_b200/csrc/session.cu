@@ -450,6 +450,8 @@ PrepLaunch prep_launch(gpk_session* s, const SliceArgs& a, int passes, int digit
     pl.records = s->records.as<SurvivorRecord>();
     pl.survivor_list = s->survivors.as<uint32_t>();
     pl.exact_list = s->cand_list.as<uint32_t>();
+    pl.head = nullptr;
+    pl.head_words = 0;
     pl.keys = s->keys[0].as<uint32_t>();
     pl.vals = s->vals[0].as<uint32_t>();
     pl.pair_cap = s->pair_cap;
@@ -522,19 +524,25 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     const uint64_t nbf = filter_blocks(s->n);
     const size_t head_bytes = head_size(s->n);
     StageScope scope_prep(s, GPK_STAGE_PREPARE);
-    CK(cudaMemsetAsync(s->head.p, 0, head_bytes, s->stream));
     if (s->n == 0) {
+        CK(cudaMemsetAsync(s->head.p, 0, head_bytes, s->stream));
         ps.final_buf = 0;
         return GPK_OK;
     }
-    const PrepLaunch pl = prep_launch(s, a, ps.passes, ps.digit_bits, zero_grads);
+    PrepLaunch pl = prep_launch(s, a, ps.passes, ps.digit_bits, zero_grads);
     // K_filter is skipped when the previous training step's fused Adam + cull
     // already produced this slice's candidates (and left the gradients zero)
     const bool pre = zero_grads && (s->assume_prefiltered || prefilter_matches(s, pose, psf, cfg));
     s->prefilter.valid = false;
     if (!pre) {
+        // K_filter zeroes the control head itself (K_decide is the first to use it)
+        pl.head = s->head.as<unsigned>();
+        pl.head_words = (unsigned)(head_bytes / 4);
         launch_prep(pl, s->num_sms, s->stream);
         CK(cudaGetLastError());
+        pl.head = nullptr;
+    } else {
+        CK(cudaMemsetAsync(s->head.p, 0, head_bytes, s->stream));
     }
     scope_prep.end();
     {

@@ -74,6 +74,15 @@ __device__ __forceinline__ Pack<N> ldp_stream(const float* p) {
     return r;
 }
 template <int N>
+__device__ __forceinline__ void stp_stream(float* p, const Pack<N>& r) {
+    if constexpr (N == 4)
+        __stcs(reinterpret_cast<float4*>(p), make_float4(r.v[0], r.v[1], r.v[2], r.v[3]));
+    else if constexpr (N == 2)
+        __stcs(reinterpret_cast<float2*>(p), make_float2(r.v[0], r.v[1]));
+    else
+        __stcs(p, r.v[0]);
+}
+template <int N>
 __device__ __forceinline__ void stp(float* p, const Pack<N>& r) {
     if constexpr (N == 4)
         *reinterpret_cast<float4*>(p) = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
@@ -145,7 +154,11 @@ __device__ __forceinline__ Pack<N> adam_plane(const AdamLaunch& a, const AdamCon
                                               const uint32_t* gslot, unsigned& nz) {
     const uint64_t o = (uint64_t)k * a.cap + i0;
     const Pack<N> g = adam_grad<N>(a, k, i0, gslot);
-    Pack<N> m = ldp<N>(a.m + o), v = ldp<N>(a.v + o), p = ldp<N>(a.params + o);
+    // Everything evict-first: the moments must not push the parameters (which
+    // K_filter left in L2 with evict-last priority for this read) out of L2,
+    // and the parameter accesses here demote those lines again, so nothing of
+    // this step stays resident into the next one.
+    Pack<N> m = ldp_stream<N>(a.m + o), v = ldp_stream<N>(a.v + o), p = ldp_stream<N>(a.params + o);
     const float lrc = __fmul_rn(lr, c.ibc1);
 #pragma unroll
     for (int l = 0; l < N; ++l) {
@@ -154,8 +167,8 @@ __device__ __forceinline__ Pack<N> adam_plane(const AdamLaunch& a, const AdamCon
         v.v[l] = __fmaf_rn(c.b2, v.v[l], __fmul_rn(__fmul_rn(c.ib2, g.v[l]), g.v[l]));
         p.v[l] = __fsub_rn(p.v[l], adam_delta(c, lrc, m.v[l], v.v[l]));
     }
-    stp<N>(a.m + o, m);
-    stp<N>(a.v + o, v);
+    stp_stream<N>(a.m + o, m);
+    stp_stream<N>(a.v + o, v);
     return p;
 }
 
@@ -209,11 +222,12 @@ __device__ __forceinline__ void adam_update_store(const AdamLaunch& a, const Ada
         const float lo = a.bbox_min[d], hi = a.bbox_max[d];
 #pragma unroll
         for (int l = 0; l < N; ++l) p.v[l] = fminf(hi, fmaxf(lo, p.v[l]));
-        stp<N>(a.params + (uint64_t)d * a.cap + i0, p);
+        stp_stream<N>(a.params + (uint64_t)d * a.cap + i0, p);
     }
 #pragma unroll
-    for (int d = 3; d < 6; ++d) stp<N>(a.params + (uint64_t)d * a.cap + i0, adam_plane<N>(a, c, d, c.lr[2], i0, gslot, nz));
-    stp<N>(a.params + (uint64_t)10 * a.cap + i0, adam_plane<N>(a, c, 10, c.lr[1], i0, gslot, nz));
+    for (int d = 3; d < 6; ++d)
+        stp_stream<N>(a.params + (uint64_t)d * a.cap + i0, adam_plane<N>(a, c, d, c.lr[2], i0, gslot, nz));
+    stp_stream<N>(a.params + (uint64_t)10 * a.cap + i0, adam_plane<N>(a, c, 10, c.lr[1], i0, gslot, nz));
     Pack<N> q[4];
 #pragma unroll
     for (int d = 0; d < 4; ++d) q[d] = adam_plane<N>(a, c, 6 + d, c.lr[3], i0, gslot, nz);
@@ -233,13 +247,13 @@ __device__ __forceinline__ void adam_update_store(const AdamLaunch& a, const Ada
         }
     }
 #pragma unroll
-    for (int d = 0; d < 4; ++d) stp<N>(a.params + (uint64_t)(6 + d) * a.cap + i0, q[d]);
+    for (int d = 0; d < 4; ++d) stp_stream<N>(a.params + (uint64_t)(6 + d) * a.cap + i0, q[d]);
 }
 
 template <int N>
 __device__ __forceinline__ void adam_store(const AdamLaunch& a, uint32_t i0, const Pack<N> p[11]) {
 #pragma unroll
-    for (int d = 0; d < 11; ++d) stp<N>(a.params + (uint64_t)d * a.cap + i0, p[d]);
+    for (int d = 0; d < 11; ++d) stp_stream<N>(a.params + (uint64_t)d * a.cap + i0, p[d]);
 }
 
 }  // namespace gpk

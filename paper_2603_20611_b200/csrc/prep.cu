@@ -327,6 +327,18 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+// ... with an L2 eviction-priority hint (the parameter planes are read again
+// by the same training step's Adam: keep them in L2 until then)
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, unsigned long long policy) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "l"(policy)
+                 : "memory");
+}
+__device__ __forceinline__ unsigned long long l2_evict_last_policy() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
@@ -351,12 +363,13 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter(const PrepLaunch a
     const unsigned gthreads = gridDim.x * kFilterThreads;
     const unsigned gtid = blockIdx.x * kFilterThreads + tid;
     const unsigned gwarps = gthreads / 32;
+    const unsigned long long keep = l2_evict_last_policy();
     auto prefetch = [&](unsigned b, int stage) {
         // cap is a multiple of kParamAlign: the chunk never leaves the plane
         const float* src = a.params + (uint64_t)b * kFilterBlock + lane * kFilterItems;
         float* dst = ring + stage * kFilterStageFloats + lane * kFilterItems;
 #pragma unroll
-        for (int q = 0; q < 11; ++q) cp_async16(dst + q * kFilterBlock, src + (uint64_t)q * a.cap);
+        for (int q = 0; q < 11; ++q) cp_async16_hint(dst + q * kFilterBlock, src + (uint64_t)q * a.cap, keep);
     };
     unsigned b = gtid / 32;
     if (b < nchunks) prefetch(b, 0);

@@ -30,7 +30,25 @@ def main():
     tgt = np.random.default_rng(7).uniform(0, 0.1, (dims[1], dims[0])).astype(np.float32)
     s.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
     lr = gp.LearningRates(6e-4, 0.02, 2e-3, 1e-3)
+    flush = None
+    mode = sys.argv[4] if len(sys.argv) > 4 else ""
+    if mode in ("flush", "flushw"):  # an L2 flush between steps: read (bench) or write 256 MiB
+        import torch
+
+        src = torch.ones((256 << 20) // 4, dtype=torch.float32, device="cuda")
+        dst = torch.empty((), dtype=torch.float32, device="cuda")
+
+        def flush():
+            torch.cuda.synchronize()
+            if mode == "flush":
+                torch.sum(src, dim=0, out=dst)
+            else:
+                src.fill_(float(np.random.rand()))
+            torch.cuda.synchronize()
     for i in range(steps):
+        if flush:
+            s.synchronize()
+            flush()
         s.train_step(poses[i % 4], psf, cfg, 0.2, 0.5, lr, 30000, next_pose=poses[(i + 1) % 4] if pipelined else None)
     s.synchronize()
     print("ok", s.prepared_count())

@@ -88,7 +88,7 @@ def _load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
             f"{LIB_PATH} is missing: build the sm_100a library first "
-            "(python -m paper_2603_20611_b200.build or __graft_entry__.build()). "
+            "(python paper_2603_20611_b200/build.py or __graft_entry__.build()). "
             "There is no CPU fallback.")
     return C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | getattr(os, "RTLD_GLOBAL", 0))
 

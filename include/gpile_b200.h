@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GPK_ABI_VERSION 3
+#define GPK_ABI_VERSION 4
 #define GPK_RECORD_FLOATS 11
 
 typedef enum {
@@ -294,6 +294,95 @@ int gpk_slice_pose_for_index(const int32_t dims[3], const double spacing[3],
                              const double origin[3], int k, gpk_slice_pose* out);
 /* lr_at (optimize.hpp:71-73). */
 double gpk_lr_at(double lr0, int iteration, int total);
+
+/* init_grid (optimize.hpp:111-133): ceil(cbrt(n))^3 lattice of cell centres,
+ * truncated to n, shapes from the same seeded stream; n x 11 f64 records. */
+int gpk_init_grid(uint64_t n, const gpk_bounds* bbox, double scale_base, uint64_t seed,
+                  double* records);
+/* default_init_count (optimize.hpp:64-66). */
+int gpk_default_init_count(uint64_t voxel_count, uint64_t* out);
+
+/* The reference's seeded generator (Rng, rng.hpp:14-70: mt19937_64 with
+ * self-contained distributions), for slice sampling and split draws. */
+typedef struct gpk_rng gpk_rng;
+int gpk_rng_create(uint64_t seed, gpk_rng** out);
+int gpk_rng_destroy(gpk_rng* rng);
+int gpk_rng_uniform(gpk_rng* rng, double* out);              /* [0, 1) */
+int gpk_rng_below(gpk_rng* rng, uint64_t n, uint64_t* out);  /* Rng::below */
+int gpk_rng_normal(gpk_rng* rng, double* out);               /* Box-Muller, spare cached */
+
+/* ---- adaptive density control (optimize.hpp:228-344) ------------------------ */
+typedef struct {
+    double tau;                  /* prune exposed alpha < tau (FitConfig::tau) */
+    double grad_threshold;       /* mean screen gradient threshold (5e-5) */
+    double split_scale_fraction; /* split when max scale > fraction * extent (0.01) */
+    double split_scale_divisor;  /* children's scales divided by this (1.6) */
+    double scale_modifier;       /* "mod" (1.0) */
+} gpk_densify_config;
+
+typedef struct {
+    uint64_t pruned, cloned, split;   /* DensifyReport (optimize.hpp:251-253) */
+} gpk_densify_report;
+
+/* DensifyAccum (optimize.hpp:228-249) kept on the device: while enabled, every
+ * backward (gpk_backward, gpk_train_step, graphs captured afterwards) adds
+ * its ScreenGradStats (|dL/dmu_2d|, observed, world dL/dmu) of the survivors.
+ * Enabling zeroes it; it is zeroed whenever the set changes size. */
+int gpk_densify_accum_enable(gpk_session* s, int on);
+int gpk_densify_accum_reset(gpk_session* s);
+/* host arrays of n: grad_norm_sum f64, observations i32, world_grad_sum 3n f64 */
+int gpk_get_densify_accum(gpk_session* s, double* grad_norm_sum, int32_t* observations,
+                          double* world_grad_sum);
+int gpk_set_densify_accum(gpk_session* s, const double* grad_norm_sum, const int32_t* observations,
+                          const double* world_grad_sum);
+/* densify_and_prune(set, adam, accum, cfg, rng) (optimize.hpp:255-344) on the
+ * resident set: prune / keep / clone / split decided on the device, the new
+ * set ordered as the reference orders it (kept in index order, then the born
+ * in their parents' order), Adam moments carried for the kept and zero for
+ * the born, the step counter kept; 6 normals per split drawn from rng in
+ * parent order. Resets the accumulator. */
+int gpk_densify_and_prune(gpk_session* s, const gpk_densify_config* cfg, gpk_rng* rng,
+                          gpk_densify_report* report);
+
+/* ---- fit driver (optimize.hpp:360-424) --------------------------------------- */
+typedef struct {
+    int32_t iterations;            /* 30000 */
+    double lr_position, lr_opacity, lr_scale, lr_rotation;  /* 6e-4, 0.02, 2e-3, 1e-3 */
+    uint64_t init_count;           /* 0 -> default_init_count(voxels) */
+    double tau;                    /* 0.02 */
+    int32_t densify_start, densify_end;   /* 500, 25000 */
+    double grad_threshold;         /* 5e-5 */
+    double lambda;                 /* 0.2 */
+    int32_t densify_interval;      /* 100 */
+    uint64_t rng_seed;             /* 0 */
+    int32_t init_mode;             /* 0 random, 1 grid */
+    double scale_modifier;         /* 1.0 */
+    double split_scale_fraction;   /* 0.01 */
+    double split_scale_divisor;    /* 1.6 */
+    double dssim_scale;            /* 0.5 */
+    int32_t progress_interval;     /* 200 */
+    int32_t tile_size;             /* 16 */
+    double footprint_sigmas;       /* 3.0 */
+} gpk_fit_config;
+
+typedef struct {
+    int32_t iteration;
+    double loss;          /* photometric loss on this iteration's slice */
+    uint64_t count;       /* primitives */
+    double psnr2d;        /* monitor slice (Z/2), clamped render */
+    double monitor_loss;  /* photometric loss on the monitor slice */
+} gpk_fit_progress;       /* FitProgress (optimize.hpp:350-356) */
+
+#define GPK_PSNR_INF 999.0   /* kPsnrInf (metrics.hpp:14) */
+
+typedef void (*gpk_fit_progress_fn)(const gpk_fit_progress* p, void* user);
+
+/* fit(volume, psf, cfg, progress) (optimize.hpp:360-424): volume is host
+ * X*Y*Z f32 z-major (data[(k*Y + j)*X + i]). The fitted set stays resident in
+ * the session (gpk_get_gaussians). Errors carry "fit: iteration N: ". */
+int gpk_fit(gpk_session* s, const float* volume, const int32_t dims[3], const double spacing[3],
+            const double origin[3], const gpk_psf* psf, const gpk_fit_config* cfg,
+            gpk_fit_progress_fn progress, void* user);
 
 /* ---- multi-GPU: slice-sharded data parallelism ------------------------------ */
 /* 128-byte ncclUniqueId produced on rank 0 and broadcast by the caller. */

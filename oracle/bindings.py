@@ -61,6 +61,26 @@ class VcfgC(C.Structure):
                 ("scale_modifier", C.c_double)]
 
 
+class DcfgC(C.Structure):
+    _fields_ = [("tau", C.c_double), ("grad_threshold", C.c_double),
+                ("split_scale_fraction", C.c_double), ("split_scale_divisor", C.c_double),
+                ("scale_modifier", C.c_double)]
+
+
+class FitCfgC(C.Structure):
+    """gpk_fit_config (include/gpile_b200.h) = FitConfig (optimize.hpp:21-44)."""
+    _fields_ = [
+        ("iterations", C.c_int32), ("lr_position", C.c_double), ("lr_opacity", C.c_double),
+        ("lr_scale", C.c_double), ("lr_rotation", C.c_double), ("init_count", C.c_uint64),
+        ("tau", C.c_double), ("densify_start", C.c_int32), ("densify_end", C.c_int32),
+        ("grad_threshold", C.c_double), ("lambda_", C.c_double), ("densify_interval", C.c_int32),
+        ("rng_seed", C.c_uint64), ("init_mode", C.c_int32), ("scale_modifier", C.c_double),
+        ("split_scale_fraction", C.c_double), ("split_scale_divisor", C.c_double),
+        ("dssim_scale", C.c_double), ("progress_interval", C.c_int32), ("tile_size", C.c_int32),
+        ("footprint_sigmas", C.c_double),
+    ]
+
+
 class CheckerError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[{code}] {msg}")
@@ -231,6 +251,51 @@ class CpuChecker:
             self._call("adam_step", C.c_uint64(rec.shape[0]), _d(rec), C.byref(b), _d(g), _d(m), _d(v),
                        C.byref(st), C.byref(lr), C.byref(hpc))
         return rec, m, v, st.value
+
+    def densify_and_prune(self, rec, bbox, m, v, step, grad_norm_sum, observations, world_grad_sum,
+                          dcfg, rng):
+        """densify_and_prune (optimize.hpp:255-344) through the reference (ref only);
+        dcfg = (tau, grad_threshold, split_scale_fraction, split_scale_divisor, mod);
+        rng a RefRng. Returns (records, m, v, (pruned, cloned, split))."""
+        assert self.is_ref, "densify_and_prune: the reference build only"
+        rec = np.ascontiguousarray(rec, np.float64).reshape(-1, 11)
+        n = rec.shape[0]
+        h = self._set(rec, bbox)
+        m = np.ascontiguousarray(m, np.float64).reshape(n, 11).copy()
+        v = np.ascontiguousarray(v, np.float64).reshape(n, 11).copy()
+        g = np.ascontiguousarray(grad_norm_sum, np.float64).reshape(n)
+        o = np.ascontiguousarray(observations, np.int32).reshape(n)
+        w = np.ascontiguousarray(world_grad_sum, np.float64).reshape(n, 3)
+        cap = max(2 * n, 1)
+        out = np.zeros((cap, 11))
+        om = np.zeros((cap, 11))
+        ov = np.zeros((cap, 11))
+        on = C.c_uint64()
+        rep = (C.c_uint64 * 3)()
+        dc = DcfgC(*dcfg)
+        self._call("densify_and_prune", C.c_void_p(h.h), _d(m), _d(v), C.c_int64(step), _d(g),
+                   o.ctypes.data_as(C.POINTER(C.c_int32)), _d(w), C.byref(dc), C.c_void_p(rng.h), _d(out),
+                   _d(om), _d(ov), C.byref(on), rep)
+        k = on.value
+        return out[:k].copy(), om[:k].copy(), ov[:k].copy(), tuple(int(x) for x in rep)
+
+    def fit(self, volume, spacing, origin, psf, fit_fields: dict, capacity: int = 1 << 20,
+            max_progress: int = 4096):
+        """fit (optimize.hpp:360-424) through the reference (ref only); volume (Z, Y, X).
+        Returns (records, progress rows [iteration, loss, count, psnr2d, monitor_loss])."""
+        assert self.is_ref, "fit: the reference build only"
+        vol = np.ascontiguousarray(volume, np.float64)
+        dims = (C.c_int32 * 3)(vol.shape[2], vol.shape[1], vol.shape[0])
+        sp = (C.c_double * 3)(*spacing)
+        org = (C.c_double * 3)(*origin)
+        fc = FitCfgC(**fit_fields)
+        out = np.zeros((capacity, 11))
+        prog = np.zeros((max_progress, 5))
+        on, npg = C.c_uint64(), C.c_uint64()
+        pc = psf_c(psf)
+        self._call("fit", _d(vol), dims, sp, org, C.byref(pc), C.byref(fc), _d(out), C.c_uint64(capacity),
+                   C.byref(on), _d(prog), C.c_uint64(max_progress), C.byref(npg))
+        return out[:on.value].copy(), prog[:min(npg.value, max_progress)].copy()
 
     def voxelize(self, rec, vcfg):
         h = self._set(rec)

@@ -228,6 +228,16 @@ int gref_init_random(uint64_t n, const gpk_bounds* bbox, double scale_base, uint
     });
 }
 
+int gref_init_grid(uint64_t n, const gpk_bounds* bbox, double scale_base, uint64_t seed,
+                   double* out) {
+    return guarded([&] {
+        const GaussianSet set = init_grid(n, bounds_from(bbox), scale_base, seed);
+        for (std::size_t i = 0; i < set.size(); ++i) prim_to(set.primitives[i], out + 11 * i);
+    });
+}
+
+uint64_t gref_default_init_count(uint64_t voxels) { return default_init_count(voxels); }
+
 int gref_slice_pose_for_index(const int32_t dims[3], const double spacing[3],
                               const double origin[3], int k, gpk_slice_pose* out) {
     return guarded([&] {
@@ -569,6 +579,121 @@ int gref_time_voxelize(void* s, const gpk_voxelizer_config* cfg, int reps, doubl
             *seconds += seconds_since(t0);
             if (vol.data.empty()) throw std::runtime_error("empty volume");
         }
+    });
+}
+
+
+// ---- adaptive density control + fit (optimize.hpp:228-424) -------------------
+// densify_and_prune on (set, Adam moments n x 11, accum) with the caller's
+// generator; the new set (capacity 2n suffices: a primitive yields at most
+// two) replaces records/m/v (out_n).
+int gref_densify_and_prune(void* s, double* m, double* v, int64_t step, const double* grad_norm_sum,
+                           const int32_t* observations, const double* world_grad_sum,
+                           const gpk_densify_config* cfg, void* rng, double* out_rec, double* out_m,
+                           double* out_v, uint64_t* out_n, uint64_t* report3) {
+    return guarded([&] {
+        GaussianSet& set = *static_cast<GaussianSet*>(s);
+        const std::size_t n = set.size();
+        AdamState st(n);
+        st.step = static_cast<long>(step);
+        for (std::size_t i = 0; i < n; ++i) {
+            const double* mi = m + 11 * i;
+            const double* vi = v + 11 * i;
+            st.m_mu[i] = {mi[0], mi[1], mi[2]};
+            st.v_mu[i] = {vi[0], vi[1], vi[2]};
+            st.m_ls[i] = {mi[3], mi[4], mi[5]};
+            st.v_ls[i] = {vi[3], vi[4], vi[5]};
+            st.m_q[i] = {mi[6], mi[7], mi[8], mi[9]};
+            st.v_q[i] = {vi[6], vi[7], vi[8], vi[9]};
+            st.m_a[i] = mi[10];
+            st.v_a[i] = vi[10];
+        }
+        DensifyAccum acc(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            acc.grad_norm_sum[i] = grad_norm_sum[i];
+            acc.observations[i] = observations[i];
+            acc.world_grad_sum[i] = {world_grad_sum[3 * i], world_grad_sum[3 * i + 1], world_grad_sum[3 * i + 2]};
+        }
+        FitConfig fc;
+        fc.tau = cfg->tau;
+        fc.grad_threshold = cfg->grad_threshold;
+        fc.split_scale_fraction = cfg->split_scale_fraction;
+        fc.split_scale_divisor = cfg->split_scale_divisor;
+        fc.scale_modifier = cfg->scale_modifier;
+        const DensifyReport rep = densify_and_prune(set, st, acc, fc, *static_cast<Rng*>(rng));
+        *out_n = set.size();
+        for (std::size_t i = 0; i < set.size(); ++i) {
+            prim_to(set.primitives[i], out_rec + 11 * i);
+            double* mi = out_m + 11 * i;
+            double* vi = out_v + 11 * i;
+            for (int d = 0; d < 3; ++d) {
+                mi[d] = st.m_mu[i][d];
+                vi[d] = st.v_mu[i][d];
+                mi[3 + d] = st.m_ls[i][d];
+                vi[3 + d] = st.v_ls[i][d];
+            }
+            for (int d = 0; d < 4; ++d) {
+                mi[6 + d] = st.m_q[i][d];
+                vi[6 + d] = st.v_q[i][d];
+            }
+            mi[10] = st.m_a[i];
+            vi[10] = st.v_a[i];
+        }
+        report3[0] = rep.pruned;
+        report3[1] = rep.cloned;
+        report3[2] = rep.split;
+    });
+}
+
+// fit (optimize.hpp:360-424) on a z-major f64 volume; the fitted set goes to
+// out_rec (capacity records) and each FitProgress to progress (5 doubles:
+// iteration, loss, count, psnr2d, monitor_loss; up to max_progress).
+int gref_fit(const double* volume, const int32_t dims[3], const double spacing[3], const double origin[3],
+             const gpk_psf* psf, const gpk_fit_config* c, double* out_rec, uint64_t capacity, uint64_t* out_n,
+             double* progress, uint64_t max_progress, uint64_t* n_progress) {
+    return guarded([&] {
+        VolumeGrid vol;
+        for (int d = 0; d < 3; ++d) vol.dims[d] = dims[d];
+        vol.spacing = {spacing[0], spacing[1], spacing[2]};
+        vol.origin = {origin[0], origin[1], origin[2]};
+        vol.data.assign(volume, volume + (std::size_t)dims[0] * dims[1] * dims[2]);
+        FitConfig fc;
+        fc.iterations = c->iterations;
+        fc.lr_position = c->lr_position;
+        fc.lr_opacity = c->lr_opacity;
+        fc.lr_scale = c->lr_scale;
+        fc.lr_rotation = c->lr_rotation;
+        fc.init_count = c->init_count;
+        fc.tau = c->tau;
+        fc.densify_start = c->densify_start;
+        fc.densify_end = c->densify_end;
+        fc.grad_threshold = c->grad_threshold;
+        fc.lambda = c->lambda;
+        fc.densify_interval = c->densify_interval;
+        fc.rng_seed = c->rng_seed;
+        fc.init_mode = c->init_mode == 1 ? "grid" : "random";
+        fc.scale_modifier = c->scale_modifier;
+        fc.split_scale_fraction = c->split_scale_fraction;
+        fc.split_scale_divisor = c->split_scale_divisor;
+        fc.dssim_scale = c->dssim_scale;
+        fc.progress_interval = c->progress_interval;
+        fc.tile_size = c->tile_size;
+        fc.footprint_sigmas = c->footprint_sigmas;
+        *n_progress = 0;
+        const GaussianSet set = fit(vol, psf_from(psf), fc, [&](const FitProgress& p) {
+            if (*n_progress < max_progress) {
+                double* o = progress + 5 * (*n_progress);
+                o[0] = p.iteration;
+                o[1] = p.loss;
+                o[2] = (double)p.count;
+                o[3] = p.psnr2d;
+                o[4] = p.monitor_loss;
+            }
+            ++*n_progress;
+        });
+        *out_n = set.size();
+        if (set.size() > capacity) throw std::invalid_argument("gref_fit: output capacity");
+        for (std::size_t i = 0; i < set.size(); ++i) prim_to(set.primitives[i], out_rec + 11 * i);
     });
 }
 

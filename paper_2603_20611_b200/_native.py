@@ -13,7 +13,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libgpile_b200.so"
-GPK_ABI_VERSION = 3  # include/gpile_b200.h
+GPK_ABI_VERSION = 4  # include/gpile_b200.h
 
 GPK_OK = 0
 GPK_ERR_INVALID_ARGUMENT = 1
@@ -82,6 +82,47 @@ class ScreenStatsC(C.Structure):
         ("observed", C.POINTER(C.c_uint8)),
         ("world_pos_grad", C.POINTER(C.c_double)),
     ]
+
+
+class DensifyConfigC(C.Structure):
+    _fields_ = [("tau", C.c_double), ("grad_threshold", C.c_double),
+                ("split_scale_fraction", C.c_double), ("split_scale_divisor", C.c_double),
+                ("scale_modifier", C.c_double)]
+
+
+class DensifyReportC(C.Structure):
+    _fields_ = [("pruned", C.c_uint64), ("cloned", C.c_uint64), ("split", C.c_uint64)]
+
+
+class FitConfigC(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int32),
+        ("lr_position", C.c_double), ("lr_opacity", C.c_double), ("lr_scale", C.c_double),
+        ("lr_rotation", C.c_double),
+        ("init_count", C.c_uint64),
+        ("tau", C.c_double),
+        ("densify_start", C.c_int32), ("densify_end", C.c_int32),
+        ("grad_threshold", C.c_double),
+        ("lambda_", C.c_double),
+        ("densify_interval", C.c_int32),
+        ("rng_seed", C.c_uint64),
+        ("init_mode", C.c_int32),
+        ("scale_modifier", C.c_double),
+        ("split_scale_fraction", C.c_double),
+        ("split_scale_divisor", C.c_double),
+        ("dssim_scale", C.c_double),
+        ("progress_interval", C.c_int32),
+        ("tile_size", C.c_int32),
+        ("footprint_sigmas", C.c_double),
+    ]
+
+
+class FitProgressC(C.Structure):
+    _fields_ = [("iteration", C.c_int32), ("loss", C.c_double), ("count", C.c_uint64),
+                ("psnr2d", C.c_double), ("monitor_loss", C.c_double)]
+
+
+PROGRESS_FN = C.CFUNCTYPE(None, C.POINTER(FitProgressC), C.c_void_p)
 
 
 def _load() -> C.CDLL:
@@ -164,6 +205,19 @@ _PROTOS = {
     "gpk_init_random": (C.c_int, [C.c_uint64, C.POINTER(Bounds), C.c_double, C.c_uint64, _D]),
     "gpk_slice_pose_for_index": (C.c_int, [_I32, _D, _D, C.c_int, C.POINTER(SlicePoseC)]),
     "gpk_lr_at": (C.c_double, [C.c_double, C.c_int, C.c_int]),
+    "gpk_init_grid": (C.c_int, [C.c_uint64, C.POINTER(Bounds), C.c_double, C.c_uint64, _D]),
+    "gpk_default_init_count": (C.c_int, [C.c_uint64, _U64]),
+    "gpk_rng_create": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
+    "gpk_rng_destroy": (C.c_int, [_P]),
+    "gpk_rng_uniform": (C.c_int, [_P, _D]),
+    "gpk_rng_below": (C.c_int, [_P, C.c_uint64, _U64]),
+    "gpk_rng_normal": (C.c_int, [_P, _D]),
+    "gpk_densify_accum_enable": (C.c_int, [_P, C.c_int]),
+    "gpk_densify_accum_reset": (C.c_int, [_P]),
+    "gpk_get_densify_accum": (C.c_int, [_P, _D, _I32, _D]),
+    "gpk_set_densify_accum": (C.c_int, [_P, _D, _I32, _D]),
+    "gpk_densify_and_prune": (C.c_int, [_P, C.POINTER(DensifyConfigC), _P, C.POINTER(DensifyReportC)]),
+    "gpk_fit": (C.c_int, [_P, _F, _I32, _D, _D, C.POINTER(PsfC), C.POINTER(FitConfigC), PROGRESS_FN, _P]),
     "gpk_nccl_get_unique_id": (C.c_int, [_P]),
     "gpk_comm_init": (C.c_int, [_P, C.c_int, C.c_int, _P]),
     "gpk_comm_destroy": (C.c_int, [_P]),

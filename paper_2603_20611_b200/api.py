@@ -36,7 +36,8 @@ __all__ = [
     "VoxelizerConfig", "ScreenGradStats", "Session", "Prepared",
     "rasterize_slice", "prepare_gaussians", "tile_lists", "backward_slice", "photometric_loss",
     "adam_step", "lr_at", "voxelize", "voxelize_backward", "init_random",
-    "slice_pose_for_index", "default_session",
+    "slice_pose_for_index", "default_session", "init_grid", "default_init_count", "Rng",
+    "DensifyConfig", "DensifyReport", "DensifyAccum", "FitConfig", "FitProgress", "fit",
     "DegenerateCovariance", "NumericFailure", "InvalidArgument", "GpileError", "StateError",
 ]
 
@@ -190,6 +191,122 @@ class Prepared:
     bounds: np.ndarray     # int32 (S, 4): lo_x, hi_x, lo_y, hi_y (inclusive)
     fields: np.ndarray     # float64 (S, 6): alpha_tilde, mu2d.x, mu2d.y, conic a, b, d
     pairs: int = 0         # (tile, Gaussian) pairs of the binning
+
+
+class Rng:
+    """The reference's seeded generator (Rng, rng.hpp:14-70), native: same stream."""
+
+    def __init__(self, seed: int):
+        h = C.c_void_p()
+        check(N.lib.gpk_rng_create(int(seed) & (2**64 - 1), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            N.lib.gpk_rng_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def uniform(self) -> float:
+        v = C.c_double()
+        check(N.lib.gpk_rng_uniform(self._h, C.byref(v)))
+        return v.value
+
+    def below(self, n: int) -> int:
+        v = C.c_uint64()
+        check(N.lib.gpk_rng_below(self._h, int(n), C.byref(v)))
+        return int(v.value)
+
+    def normal(self) -> float:
+        v = C.c_double()
+        check(N.lib.gpk_rng_normal(self._h, C.byref(v)))
+        return v.value
+
+
+@dataclass
+class DensifyConfig:
+    """The FitConfig fields densify_and_prune reads (optimize.hpp:21-44)."""
+
+    tau: float = 0.02
+    grad_threshold: float = 5e-5
+    split_scale_fraction: float = 0.01
+    split_scale_divisor: float = 1.6
+    scale_modifier: float = 1.0
+
+    def to_c(self) -> N.DensifyConfigC:
+        return N.DensifyConfigC(self.tau, self.grad_threshold, self.split_scale_fraction,
+                                self.split_scale_divisor, self.scale_modifier)
+
+
+@dataclass
+class DensifyReport:
+    """DensifyReport (optimize.hpp:251-253)."""
+
+    pruned: int = 0
+    cloned: int = 0
+    split: int = 0
+
+
+@dataclass
+class DensifyAccum:
+    """DensifyAccum (optimize.hpp:228-249) as host arrays."""
+
+    grad_norm_sum: np.ndarray
+    observations: np.ndarray
+    world_grad_sum: np.ndarray   # (n, 3)
+
+
+@dataclass
+class FitConfig:
+    """FitConfig (optimize.hpp:21-62); init_mode "random" | "grid"."""
+
+    iterations: int = 30000
+    lr_position: float = 0.0006
+    lr_opacity: float = 0.02
+    lr_scale: float = 0.002
+    lr_rotation: float = 0.001
+    init_count: int = 0
+    tau: float = 0.02
+    densify_start: int = 500
+    densify_end: int = 25000
+    grad_threshold: float = 5e-5
+    lam: float = 0.2
+    densify_interval: int = 100
+    rng_seed: int = 0
+    init_mode: str = "random"
+    scale_modifier: float = 1.0
+    split_scale_fraction: float = 0.01
+    split_scale_divisor: float = 1.6
+    dssim_scale: float = 0.5
+    progress_interval: int = 200
+    tile_size: int = 16
+    footprint_sigmas: float = 3.0
+
+    def to_c(self) -> N.FitConfigC:
+        if self.init_mode not in ("random", "grid"):
+            raise InvalidArgument("FitConfig: init_mode must be random or grid")
+        return N.FitConfigC(int(self.iterations), self.lr_position, self.lr_opacity, self.lr_scale,
+                            self.lr_rotation, int(self.init_count), self.tau, int(self.densify_start),
+                            int(self.densify_end), self.grad_threshold, self.lam,
+                            int(self.densify_interval), int(self.rng_seed) & (2**64 - 1),
+                            0 if self.init_mode == "random" else 1, self.scale_modifier,
+                            self.split_scale_fraction, self.split_scale_divisor, self.dssim_scale,
+                            int(self.progress_interval), int(self.tile_size), self.footprint_sigmas)
+
+
+@dataclass
+class FitProgress:
+    """FitProgress (optimize.hpp:350-356)."""
+
+    iteration: int
+    loss: float
+    count: int
+    psnr2d: float
+    monitor_loss: float
 
 
 # ---- session -----------------------------------------------------------------
@@ -465,6 +582,68 @@ class Session:
                                           N.fptr(out)))
         return out
 
+    # ---- adaptive density control + fit driver (optimize.hpp:228-424) ----
+    def _refresh_n(self):
+        v = C.c_uint64()
+        check(N.lib.gpk_gaussian_count(self._h, C.byref(v)))
+        self.n = int(v.value)
+
+    def densify_accum_enable(self, on: bool = True):
+        check(N.lib.gpk_densify_accum_enable(self._h, 1 if on else 0))
+
+    def densify_accum_reset(self):
+        check(N.lib.gpk_densify_accum_reset(self._h))
+
+    def densify_accum(self) -> DensifyAccum:
+        n = self.n
+        a = DensifyAccum(np.zeros(n), np.zeros(n, np.int32), np.zeros((n, 3)))
+        check(N.lib.gpk_get_densify_accum(self._h, N.dptr(a.grad_norm_sum), N.i32ptr(a.observations),
+                                          N.dptr(a.world_grad_sum)))
+        return a
+
+    def set_densify_accum(self, a: DensifyAccum):
+        n = self.n
+        g = np.ascontiguousarray(a.grad_norm_sum, np.float64).reshape(n)
+        o = np.ascontiguousarray(a.observations, np.int32).reshape(n)
+        w = np.ascontiguousarray(a.world_grad_sum, np.float64).reshape(n, 3)
+        check(N.lib.gpk_set_densify_accum(self._h, N.dptr(g), N.i32ptr(o), N.dptr(w)))
+
+    def densify_and_prune(self, cfg: DensifyConfig, rng: Rng) -> DensifyReport:
+        c = cfg.to_c()
+        r = N.DensifyReportC()
+        check(N.lib.gpk_densify_and_prune(self._h, C.byref(c), rng.handle, C.byref(r)))
+        self._refresh_n()
+        return DensifyReport(int(r.pruned), int(r.cloned), int(r.split))
+
+    def fit(self, volume: np.ndarray, spacing, origin, psf: PsfSpec, cfg: FitConfig,
+            progress=None) -> None:
+        """fit (optimize.hpp:360-424) on this session; volume is (Z, Y, X). The
+        fitted set stays resident (get_gaussians)."""
+        vol = np.ascontiguousarray(volume, np.float32)
+        if vol.ndim != 3:
+            raise InvalidArgument("fit: volume must be (Z, Y, X)")
+        dims = np.array([vol.shape[2], vol.shape[1], vol.shape[0]], np.int32)
+        sp = np.asarray(spacing, np.float64)
+        org = np.asarray(origin, np.float64)
+        c = cfg.to_c()
+        p = psf.to_c()
+        errors = []
+
+        def _cb(pp, _user):
+            try:
+                q = pp.contents
+                progress(FitProgress(int(q.iteration), q.loss, int(q.count), q.psnr2d, q.monitor_loss))
+            except BaseException as e:  # noqa: BLE001  (re-raised after the native call)
+                errors.append(e)
+
+        cb = N.PROGRESS_FN(_cb) if progress is not None else N.PROGRESS_FN()
+        st = N.lib.gpk_fit(self._h, N.fptr(vol), N.i32ptr(dims), N.dptr(sp), N.dptr(org), C.byref(p),
+                           C.byref(c), cb, None)
+        self._refresh_n()
+        check(st)
+        if errors:
+            raise errors[0]
+
 
 _default: dict[int, Session] = {}
 _lock = threading.Lock()
@@ -593,3 +772,33 @@ def slice_pose_for_index(dims, spacing, origin, k: int) -> SlicePose:
     p = N.SlicePoseC()
     check(N.lib.gpk_slice_pose_for_index(N.i32ptr(d), N.dptr(sp), N.dptr(o), int(k), C.byref(p)))
     return SlicePose.from_c(p)
+
+
+def init_grid(count: int, bbox_min, bbox_max, scale_base: float, seed: int) -> GaussianSet:
+    """init_grid (optimize.hpp:111-133), bit-identical stream."""
+    rec = np.zeros((int(count), RECORD), np.float64)
+    b = N.Bounds((C.c_double * 3)(*bbox_min), (C.c_double * 3)(*bbox_max))
+    st = N.lib.gpk_init_grid(int(count), C.byref(b), float(scale_base), int(seed), N.dptr(rec))
+    if st != N.GPK_OK:
+        raise InvalidArgument("init_grid: count must be >= 1 and bbox non-degenerate")
+    return GaussianSet(rec, tuple(bbox_min), tuple(bbox_max))
+
+
+def default_init_count(voxel_count: int) -> int:
+    """default_init_count (optimize.hpp:64-66)."""
+    v = C.c_uint64()
+    check(N.lib.gpk_default_init_count(int(voxel_count), C.byref(v)))
+    return int(v.value)
+
+
+def fit(volume: np.ndarray, spacing, origin, psf: PsfSpec, cfg: FitConfig, progress=None,
+        device: int = 0) -> GaussianSet:
+    """fit(volume, psf, cfg, progress) (optimize.hpp:360-424) -> the fitted set."""
+    vol = np.asarray(volume)
+    dims = (vol.shape[2], vol.shape[1], vol.shape[0])
+    lo = tuple(float(o) - float(s) * 0.5 for o, s in zip(origin, spacing))
+    hi = tuple(float(o) + (d - 0.5) * float(s) for o, s, d in zip(origin, spacing, dims))
+    with Session(device) as s:
+        s.fit(vol, spacing, origin, psf, cfg, progress)
+        rec = s.get_gaussians().astype(np.float64)
+    return GaussianSet(rec, lo, hi)

@@ -26,6 +26,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-I", str(INCLUDE), "-Xptxas", "-warn-spills"]
 PER_FILE = {
     "prep.cu": ["--fmad=false"],
+    "densify.cu": ["--fmad=false"],
 }
 
 

@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+
 #include <utility>
 
 namespace gpk {
@@ -453,6 +455,9 @@ struct ChainLaunch {
     float* stat_norm;              // optional (screen-space dL/dmu_2d norm)
     uint8_t* stat_observed;        // optional
     float* stat_world;             // optional, 3 per primitive
+    double* acc_norm;              // optional DensifyAccum (fit): += |dL/dmu_2d| ...
+    int* acc_obs;                  //   ... += 1 ...
+    double* acc_world;             //   ... += world dL/dmu
     const uint32_t* exact_list;    // record slots of the fp64 chain (K_decide)
     unsigned* exact_count;         // Control::chain_exact
     const unsigned* grp_surv;      // survivors per K_decide group (CTA per group)
@@ -582,6 +587,32 @@ struct VoxChainLaunch {
     ErrorState* err;
     VoxArgs v;
 };
+
+// densify_and_prune (optimize.hpp:255-344), densify.cu
+struct DensifyLaunch {
+    const float* params;           // 11 planes, stride cap
+    const float* m;
+    const float* v;
+    uint64_t cap, n;
+    const double* acc_norm;        // DensifyAccum (optimize.hpp:228-249): sum of |dL/dmu_2d|
+    const int* acc_obs;            //   observation count
+    const double* acc_world;       //   sum of world dL/dmu, 3 per primitive
+    double tau, grad_threshold, split_threshold, shrink, mod;
+    double bmin[3], bmax[3];
+    uint8_t* cls;                  // per primitive: prune / keep / clone / split
+    unsigned* block_sums;          // 3 per block: kept, born, split (then their block offsets)
+    unsigned* totals;              // 3: kept, born, split
+    const double* normals;         // 6 per split parent, in parent order (host Rng)
+    float* out_params;             // 11 planes, stride cap_out (cleared)
+    float* out_m;
+    float* out_v;
+    uint64_t cap_out;
+};
+
+unsigned densify_blocks(uint64_t n);
+int set_last_error(int code, const std::string& msg);  // session.cu (thread-local message)
+void launch_densify_classify(const DensifyLaunch& a, cudaStream_t st);
+void launch_densify_emit(const DensifyLaunch& a, cudaStream_t st);
 
 void launch_vox_prep(const VoxPrepLaunch& a, cudaStream_t st);
 void launch_vox_eval(const VoxEvalLaunch& a, cudaStream_t st);

@@ -825,6 +825,13 @@ __device__ __forceinline__ void store_chain(const ChainLaunch& a, uint32_t i, ui
         a.stat_world[3ull * i + 1] = dmu[1];
         a.stat_world[3ull * i + 2] = dmu[2];
     }
+    if (a.acc_obs && !a.ctrl->pair_overflow) {  // DensifyAccum::add (optimize.hpp:238-245); one survivor per thread; an overflowed slice is replayed
+        a.acc_norm[i] += sqrt(acc[1] * acc[1] + acc[2] * acc[2]);
+        a.acc_obs[i] += 1;
+        a.acc_world[3ull * i + 0] += (double)dmu[0];
+        a.acc_world[3ull * i + 1] += (double)dmu[1];
+        a.acc_world[3ull * i + 2] += (double)dmu[2];
+    }
 }
 
 // K_chain: one thread per survivor (backward.hpp:148-185). Survivors that

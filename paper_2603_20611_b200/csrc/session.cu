@@ -27,6 +27,15 @@ int fail(int code, const std::string& msg, int64_t index = -1) {
     return code;
 }
 
+}  // namespace
+
+namespace gpk {
+// the fit driver (fit.cu) reports through the same thread-local message
+int set_last_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace gpk
+
+namespace {
+
 int ok() {
     t_err.clear();
     t_err_index = -1;
@@ -150,6 +159,10 @@ struct gpk_session {
     DevBuf persist;    // ErrorState | epoch | adam step | adam done ctr | loss done ctr | loss
     DevBuf image, dl_di, target, loss_g, loss_partial;
     DevBuf stat_norm, stat_obs, stat_world;
+    // DensifyAccum (optimize.hpp:228-249), accumulated by every backward's
+    // chain while enabled (gpk_densify_accum_enable)
+    DevBuf acc_norm, acc_obs, acc_world;
+    bool accum_on = false;
     int img_w = 0, img_h = 0;
 
     PrepState prep;
@@ -715,6 +728,9 @@ int run_backward(gpk_session* s, bool stats, bool slots = false) {
     c.stat_norm = stats ? s->stat_norm.as<float>() : nullptr;
     c.stat_observed = stats ? s->stat_obs.as<uint8_t>() : nullptr;
     c.stat_world = stats ? s->stat_world.as<float>() : nullptr;
+    c.acc_norm = s->accum_on ? s->acc_norm.as<double>() : nullptr;
+    c.acc_obs = s->accum_on ? s->acc_obs.as<int>() : nullptr;
+    c.acc_world = s->accum_on ? s->acc_world.as<double>() : nullptr;
     c.exact_list = s->cand_list.as<uint32_t>();  // deferral list (record slots)
     c.exact_count = &s->ctrl()->chain_exact;
     c.grp_surv = s->grp_surv();
@@ -790,6 +806,17 @@ int copy_planes_out(gpk_session* s, const float* dev, float* rec) {
     return GPK_OK;
 }
 
+// DensifyAccum::reset(n) on the device (optimize.hpp:234-238)
+int accum_alloc_zero(gpk_session* s) {
+    CK(s->acc_norm.ensure(s->cap * 8));
+    CK(s->acc_obs.ensure(s->cap * 4));
+    CK(s->acc_world.ensure(s->cap * 24));
+    CK(cudaMemsetAsync(s->acc_norm.p, 0, s->cap * 8, s->stream));
+    CK(cudaMemsetAsync(s->acc_obs.p, 0, s->cap * 4, s->stream));
+    CK(cudaMemsetAsync(s->acc_world.p, 0, s->cap * 24, s->stream));
+    return GPK_OK;
+}
+
 int alloc_for_n(gpk_session* s, uint64_t n) {
     // plane stride: a multiple of the K_filter chunk, so every chunk's plane
     // slice is a 4 KB, 16 B-aligned TMA bulk-copy source/destination
@@ -819,7 +846,9 @@ int alloc_for_n(gpk_session* s, uint64_t n) {
         s->cap = cap;
         ++s->alloc_epoch;
     }
+    if (n != s->n) ++s->alloc_epoch;  // captured graphs bake the set size
     s->n = n;
+    if (s->accum_on) TRY(accum_alloc_zero(s));
     return GPK_OK;
 }
 
@@ -1218,7 +1247,7 @@ int gpk_session_destroy(gpk_session* s) {
     DevBuf* bufs[] = {&s->params, &s->grads, &s->adam_m, &s->adam_v, &s->records, &s->survivors,
                       &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials,
                       &s->sort_status, &s->head, &s->persist, &s->image,
-                      &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm,
+                      &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm, &s->acc_norm, &s->acc_obs, &s->acc_world,
                       &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table, &s->bucket_tab,
                       &s->dirty_idx, &s->vox_records, &s->slot_grads, &s->gmap,
                       &s->volume, &s->dl_dv_vol, &s->vox_partials};
@@ -2216,6 +2245,152 @@ int gpk_voxelize_backward(gpk_session* s, const gpk_voxelizer_config* cfg, const
     }
     TRY(sync_and_check(s, "voxelize_backward"));
     if (grads_out && s->n) TRY(copy_planes_out(s, s->grads.as<float>(), grads_out));
+    return ok();
+}
+
+
+/* ---- adaptive density control (optimize.hpp:228-344) --------------------- */
+
+int gpk_densify_accum_enable(gpk_session* s, int on) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    const bool want = on != 0;
+    if (want && !s->accum_on) {
+        s->accum_on = true;
+        TRY(accum_alloc_zero(s));
+    }
+    if (want != s->accum_on) s->accum_on = want;
+    ++s->alloc_epoch;  // captured graphs hold the chain's accumulator pointers
+    return ok();
+}
+
+int gpk_densify_accum_reset(gpk_session* s) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    if (!s->accum_on) return fail(GPK_ERR_STATE, "densify accumulator not enabled");
+    TRY(set_device(s));
+    TRY(accum_alloc_zero(s));
+    return ok();
+}
+
+int gpk_get_densify_accum(gpk_session* s, double* grad_norm_sum, int32_t* observations,
+                          double* world_grad_sum) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    if (!s->accum_on) return fail(GPK_ERR_STATE, "densify accumulator not enabled");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    if (grad_norm_sum && s->n) CK(cudaMemcpy(grad_norm_sum, s->acc_norm.p, s->n * 8, cudaMemcpyDeviceToHost));
+    if (observations && s->n) CK(cudaMemcpy(observations, s->acc_obs.p, s->n * 4, cudaMemcpyDeviceToHost));
+    if (world_grad_sum && s->n) CK(cudaMemcpy(world_grad_sum, s->acc_world.p, s->n * 24, cudaMemcpyDeviceToHost));
+    return ok();
+}
+
+int gpk_set_densify_accum(gpk_session* s, const double* grad_norm_sum, const int32_t* observations,
+                          const double* world_grad_sum) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    if (!s->accum_on) return fail(GPK_ERR_STATE, "densify accumulator not enabled");
+    if (s->n && (!grad_norm_sum || !observations || !world_grad_sum))
+        return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    if (s->n) {
+        CK(cudaMemcpy(s->acc_norm.p, grad_norm_sum, s->n * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(s->acc_obs.p, observations, s->n * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(s->acc_world.p, world_grad_sum, s->n * 24, cudaMemcpyHostToDevice));
+    }
+    return ok();
+}
+
+// densify_and_prune (optimize.hpp:255-344) on the resident set: classify +
+// block scan on the device, the split children's normals from the caller's
+// generator (drawn in parent order, as the reference draws them), emit into
+// fresh planes, then the new set (moments carried over, the step counter
+// kept) replaces the old one. The accumulator is reset (fit, optimize.hpp:400).
+int gpk_densify_and_prune(gpk_session* s, const gpk_densify_config* cfg, gpk_rng* rng,
+                          gpk_densify_report* report) {
+    if (!s || !cfg || !rng) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (!s->accum_on) return fail(GPK_ERR_STATE, "densify accumulator not enabled");
+    if (!(cfg->split_scale_divisor > 0.0)) return fail(GPK_ERR_INVALID_ARGUMENT, "split_scale_divisor must be > 0");
+    TRY(set_device(s));
+    TRY(clear_gmap(s));  // the slot map of the last step is set-indexed
+    const uint64_t n = s->n;
+    DensifyLaunch a{};
+    a.params = s->params.as<float>();
+    a.m = s->adam_m.as<float>();
+    a.v = s->adam_v.as<float>();
+    a.cap = s->cap;
+    a.n = n;
+    a.acc_norm = s->acc_norm.as<double>();
+    a.acc_obs = s->acc_obs.as<int>();
+    a.acc_world = s->acc_world.as<double>();
+    double ext = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        a.bmin[d] = s->bbox.min[d];
+        a.bmax[d] = s->bbox.max[d];
+    }
+    {   // scene_extent = max extent (:257-259), as the reference evaluates it
+        const double ex = s->bbox.max[0] - s->bbox.min[0], ey = s->bbox.max[1] - s->bbox.min[1],
+                     ez = s->bbox.max[2] - s->bbox.min[2];
+        ext = std::fmax(ex, std::fmax(ey, ez));
+    }
+    a.tau = cfg->tau;
+    a.grad_threshold = cfg->grad_threshold;
+    a.split_threshold = cfg->split_scale_fraction * ext;
+    a.shrink = std::log(cfg->split_scale_divisor);
+    a.mod = cfg->scale_modifier;
+    const unsigned nb = densify_blocks(n);
+    DevBuf cls, sums, normals, outp, outm, outv;
+    CK(cls.ensure(std::max<uint64_t>(n, 1)));
+    CK(sums.ensure((uint64_t)nb * 12 + 16));
+    a.cls = cls.as<uint8_t>();
+    a.block_sums = sums.as<unsigned>();
+    a.totals = sums.as<unsigned>() + 3ull * nb;
+    launch_densify_classify(a, s->stream);
+    CK(cudaGetLastError());
+    unsigned tot[3];
+    CK(cudaMemcpyAsync(tot, a.totals, 12, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    const uint64_t kept = tot[0], born = tot[1], split = tot[2];
+    const uint64_t n_new = kept + born;
+    if (n_new >= (1ull << 31)) return fail(GPK_ERR_INVALID_ARGUMENT, "densify: set size must stay < 2^31");
+    std::vector<double> xi(6 * split);
+    for (uint64_t k = 0; k < xi.size(); ++k) TRY(gpk_rng_normal(rng, &xi[k]));
+    CK(normals.ensure(std::max<uint64_t>(xi.size(), 1) * 8));
+    if (!xi.empty()) CK(cudaMemcpyAsync(normals.p, xi.data(), xi.size() * 8, cudaMemcpyHostToDevice, s->stream));
+    const uint64_t need = (std::max<uint64_t>(n_new, 1) + kParamAlign - 1) / kParamAlign * kParamAlign;
+    const uint64_t cap_out = std::max(need, s->cap);  // the plane stride after alloc_for_n
+    for (DevBuf* b : {&outp, &outm, &outv}) {
+        CK(b->ensure(cap_out * 44));
+        CK(cudaMemsetAsync(b->p, 0, cap_out * 44, s->stream));
+    }
+    a.normals = normals.as<double>();
+    a.out_params = outp.as<float>();
+    a.out_m = outm.as<float>();
+    a.out_v = outv.as<float>();
+    a.cap_out = cap_out;
+    launch_densify_emit(a, s->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s->stream));
+    TRY(alloc_for_n(s, n_new));  // may reallocate the planes (contents not kept)
+    if (s->cap != cap_out) return fail(GPK_ERR_CUDA, "densify: unexpected plane stride");
+    CK(cudaMemcpyAsync(s->params.p, outp.p, cap_out * 44, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->adam_m.p, outm.p, cap_out * 44, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->adam_v.p, outv.p, cap_out * 44, cudaMemcpyDeviceToDevice, s->stream));
+    // gradients and prepared state refer to the old indices: clear them
+    CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 44, s->stream));
+    s->grads_in_slots = false;
+    s->gmap_dirty = false;
+    TRY(mark_grads_dense(s));
+    s->prep.valid = false;
+    s->prefilter.valid = false;
+    TRY(accum_alloc_zero(s));
+    CK(cudaStreamSynchronize(s->stream));
+    for (DevBuf* b : {&cls, &sums, &normals, &outp, &outm, &outv}) b->release();
+    if (report) {
+        report->pruned = n - (kept + split);  // `kept` holds keeps and clone originals
+        report->cloned = born - 2 * split;
+        report->split = split;
+    }
     return ok();
 }
 

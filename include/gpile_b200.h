@@ -47,7 +47,9 @@ typedef enum {
     GPK_ERR_CUDA = 4,                  /* CUDA runtime / launch failure */
     GPK_ERR_NCCL = 5,                  /* NCCL failure */
     GPK_ERR_OUT_OF_MEMORY = 6,         /* device allocation failed */
-    GPK_ERR_STATE = 7                  /* call order violated (e.g. backward before prepare) */
+    GPK_ERR_STATE = 7,                 /* call order violated (e.g. backward before prepare) */
+    GPK_ERR_CORRUPT_CONTAINER = 8,     /* gpile::CorruptContainer, errors.hpp:19 */
+    GPK_ERR_LOAD = 9                   /* gpile::LoadError, errors.hpp:24 */
 } gpk_status;
 
 /* Bounds (core.hpp:50-65): world-space bbox, positions clamped into it by Adam. */
@@ -310,6 +312,17 @@ int gpk_rng_destroy(gpk_rng* rng);
 int gpk_rng_uniform(gpk_rng* rng, double* out);              /* [0, 1) */
 int gpk_rng_below(gpk_rng* rng, uint64_t n, uint64_t* out);  /* Rng::below */
 int gpk_rng_normal(gpk_rng* rng, double* out);               /* Box-Muller, spare cached */
+
+/* ---- checkpoints: save_checkpoint / load_checkpoint (checkpoint.hpp:38-92) ---- */
+/* The reference's uncompressed format byte for byte ("GPILE", u32 version 1,
+ * u64 count, 6 f64 bbox, count x 11 f32 records). Load replaces the session's
+ * set (Adam reset, as gpk_set_gaussians). Errors: GPK_ERR_LOAD (cannot open /
+ * write), GPK_ERR_CORRUPT_CONTAINER (magic, version, truncation). */
+int gpk_save_checkpoint(gpk_session* s, const char* path);
+int gpk_load_checkpoint(gpk_session* s, const char* path);
+uint64_t gpk_checkpoint_bytes(uint64_t count);   /* checkpoint_bytes (checkpoint.hpp:95-97) */
+/* The set's world bbox (GaussianSet::bbox, core.hpp:67-74). */
+int gpk_get_bounds(gpk_session* s, gpk_bounds* out);
 
 /* ---- adaptive density control (optimize.hpp:228-344) ------------------------ */
 typedef struct {

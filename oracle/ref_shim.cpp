@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "gpile/backward.hpp"
+#include "gpile/checkpoint.hpp"
 #include "gpile/core.hpp"
 #include "gpile/errors.hpp"
 #include "gpile/loss.hpp"
@@ -696,5 +697,36 @@ int gref_fit(const double* volume, const int32_t dims[3], const double spacing[3
         for (std::size_t i = 0; i < set.size(); ++i) prim_to(set.primitives[i], out_rec + 11 * i);
     });
 }
+
+
+// ---- checkpoints (checkpoint.hpp:38-97) --------------------------------------
+int gref_save_checkpoint(void* s, const char* path) {
+    return guarded([&] { save_checkpoint(*static_cast<GaussianSet*>(s), path); });
+}
+// load_checkpoint -> records (capacity) + bbox; status 8 CorruptContainer, 9 LoadError
+int gref_load_checkpoint(const char* path, double* out, uint64_t capacity, uint64_t* n, gpk_bounds* bbox) {
+    try {
+        const GaussianSet set = load_checkpoint(path);
+        *n = set.size();
+        if (set.size() > capacity) throw std::invalid_argument("capacity");
+        for (std::size_t i = 0; i < set.size(); ++i) prim_to(set.primitives[i], out + 11 * i);
+        for (int d = 0; d < 3; ++d) {
+            bbox->min[d] = set.bbox.min[d];
+            bbox->max[d] = set.bbox.max[d];
+        }
+        g_err.clear();
+        return GPK_OK;
+    } catch (const CorruptContainer& e) {
+        g_err = e.what();
+        return GPK_ERR_CORRUPT_CONTAINER;
+    } catch (const LoadError& e) {
+        g_err = e.what();
+        return GPK_ERR_LOAD;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return GPK_ERR_INVALID_ARGUMENT;
+    }
+}
+uint64_t gref_checkpoint_bytes(uint64_t count) { return checkpoint_bytes(count); }
 
 }  // extern "C"

@@ -23,6 +23,8 @@ GPK_ERR_CUDA = 4
 GPK_ERR_NCCL = 5
 GPK_ERR_OUT_OF_MEMORY = 6
 GPK_ERR_STATE = 7
+GPK_ERR_CORRUPT_CONTAINER = 8
+GPK_ERR_LOAD = 9
 
 GPK_BUF_PARAMS, GPK_BUF_GRADS, GPK_BUF_IMAGE, GPK_BUF_DL_DI, GPK_BUF_TARGET = 0, 1, 2, 3, 4
 GPK_BUF_VOLUME, GPK_BUF_DL_DV, GPK_BUF_LOSS = 5, 6, 7
@@ -205,6 +207,10 @@ _PROTOS = {
     "gpk_init_random": (C.c_int, [C.c_uint64, C.POINTER(Bounds), C.c_double, C.c_uint64, _D]),
     "gpk_slice_pose_for_index": (C.c_int, [_I32, _D, _D, C.c_int, C.POINTER(SlicePoseC)]),
     "gpk_lr_at": (C.c_double, [C.c_double, C.c_int, C.c_int]),
+    "gpk_save_checkpoint": (C.c_int, [_P, C.c_char_p]),
+    "gpk_load_checkpoint": (C.c_int, [_P, C.c_char_p]),
+    "gpk_checkpoint_bytes": (C.c_uint64, [C.c_uint64]),
+    "gpk_get_bounds": (C.c_int, [_P, C.POINTER(Bounds)]),
     "gpk_init_grid": (C.c_int, [C.c_uint64, C.POINTER(Bounds), C.c_double, C.c_uint64, _D]),
     "gpk_default_init_count": (C.c_int, [C.c_uint64, _U64]),
     "gpk_rng_create": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
@@ -261,6 +267,14 @@ class StateError(GpileError):
     pass
 
 
+class CorruptContainer(GpileError):
+    """gpile::CorruptContainer (errors.hpp:19)."""
+
+
+class LoadError(GpileError):
+    """gpile::LoadError (errors.hpp:24)."""
+
+
 _EXC = {
     GPK_ERR_INVALID_ARGUMENT: InvalidArgument,
     GPK_ERR_DEGENERATE_COVARIANCE: DegenerateCovariance,
@@ -269,6 +283,8 @@ _EXC = {
     GPK_ERR_NCCL: CudaError,
     GPK_ERR_OUT_OF_MEMORY: CudaError,
     GPK_ERR_STATE: StateError,
+    GPK_ERR_CORRUPT_CONTAINER: CorruptContainer,
+    GPK_ERR_LOAD: LoadError,
 }
 
 

@@ -28,8 +28,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from ._native import (DegenerateCovariance, GpileError, InvalidArgument, NumericFailure,
-                      StateError, check)
+from ._native import (CorruptContainer, DegenerateCovariance, GpileError, InvalidArgument,
+                      LoadError, NumericFailure, StateError, check)
 
 __all__ = [
     "GaussianSet", "SlicePose", "PsfSpec", "RasterConfig", "LearningRates", "AdamState",
@@ -38,6 +38,7 @@ __all__ = [
     "adam_step", "lr_at", "voxelize", "voxelize_backward", "init_random",
     "slice_pose_for_index", "default_session", "init_grid", "default_init_count", "Rng",
     "DensifyConfig", "DensifyReport", "DensifyAccum", "FitConfig", "FitProgress", "fit",
+    "save_checkpoint", "load_checkpoint", "checkpoint_bytes", "CorruptContainer", "LoadError",
     "DegenerateCovariance", "NumericFailure", "InvalidArgument", "GpileError", "StateError",
 ]
 
@@ -582,6 +583,20 @@ class Session:
                                           N.fptr(out)))
         return out
 
+    # ---- checkpoints (checkpoint.hpp:38-92) ----
+    def bounds(self) -> tuple:
+        b = N.Bounds()
+        check(N.lib.gpk_get_bounds(self._h, C.byref(b)))
+        return tuple(b.min), tuple(b.max)
+
+    def save_checkpoint(self, path):
+        check(N.lib.gpk_save_checkpoint(self._h, str(path).encode()))
+
+    def load_checkpoint(self, path):
+        st = N.lib.gpk_load_checkpoint(self._h, str(path).encode())
+        check(st)
+        self._refresh_n()
+
     # ---- adaptive density control + fit driver (optimize.hpp:228-424) ----
     def _refresh_n(self):
         v = C.c_uint64()
@@ -802,3 +817,22 @@ def fit(volume: np.ndarray, spacing, origin, psf: PsfSpec, cfg: FitConfig, progr
         s.fit(vol, spacing, origin, psf, cfg, progress)
         rec = s.get_gaussians().astype(np.float64)
     return GaussianSet(rec, lo, hi)
+
+
+def save_checkpoint(gs: GaussianSet, path, device: int = 0) -> None:
+    """save_checkpoint (checkpoint.hpp:38-57) through a device session."""
+    _session_for(gs, device).save_checkpoint(path)
+
+
+def load_checkpoint(path, device: int = 0) -> GaussianSet:
+    """load_checkpoint (checkpoint.hpp:60-91) -> GaussianSet (records as f64 of the f32 file)."""
+    with Session(device) as s:
+        s.load_checkpoint(path)
+        lo, hi = s.bounds()
+        rec = s.get_gaussians().astype(np.float64)
+    return GaussianSet(rec, lo, hi)
+
+
+def checkpoint_bytes(count: int) -> int:
+    """checkpoint_bytes (checkpoint.hpp:95-97)."""
+    return int(N.lib.gpk_checkpoint_bytes(int(count)))

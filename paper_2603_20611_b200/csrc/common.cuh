@@ -609,6 +609,9 @@ struct DensifyLaunch {
     uint64_t cap_out;
 };
 
+// layout.cu: 11-f32 records <-> 11 planes of stride cap
+void launch_records_to_planes(const float* rec, uint64_t n, float* planes, uint64_t cap, cudaStream_t st);
+void launch_planes_to_records(const float* planes, uint64_t cap, uint64_t n, float* rec, cudaStream_t st);
 unsigned densify_blocks(uint64_t n);
 int set_last_error(int code, const std::string& msg);  // session.cu (thread-local message)
 void launch_densify_classify(const DensifyLaunch& a, cudaStream_t st);

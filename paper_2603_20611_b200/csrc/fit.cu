@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -176,6 +178,9 @@ int gpk_fit(gpk_session* s, const float* volume, const int32_t dims[3], const do
         return fail_fit(code, "fit: iteration " + std::to_string(it) + ": " + gpk_last_error_message());
     };
 
+    double prof[4] = {0, 0, 0, 0};
+    const bool profile = std::getenv("GPK_FIT_PROFILE") != nullptr;
+    const auto tfit = std::chrono::steady_clock::now();
     for (int it = 1; it <= cfg->iterations; ++it) {
         uint64_t k64 = 0;
         FIT_TRY(gpk_rng_below(rng, Z, &k64));
@@ -186,10 +191,17 @@ int gpk_fit(gpk_session* s, const float* volume, const int32_t dims[3], const do
         // iteration's statistics; none are read after the window closes)
         if (it == cfg->densify_end + 1) FIT_TRY(gpk_densify_accum_enable(s, 0));
         for (int attempt = 0;; ++attempt) {
+            const auto t0 = std::chrono::steady_clock::now();
             int stt = load_target(k);
             if (stt != GPK_OK) return iter_fail(it, stt);
+            const auto t1 = std::chrono::steady_clock::now();
             stt = gpk_train_step(s, &pose, psf, &rcfg, cfg->lambda, cfg->dssim_scale, &lr0, cfg->iterations);
+            const auto t2 = std::chrono::steady_clock::now();
             if (stt == GPK_OK) stt = gpk_session_synchronize(s);
+            const auto t3 = std::chrono::steady_clock::now();
+            prof[0] += std::chrono::duration<double>(t1 - t0).count();
+            prof[1] += std::chrono::duration<double>(t2 - t1).count();
+            prof[2] += std::chrono::duration<double>(t3 - t2).count();
             if (stt == GPK_OK) break;
             uint64_t surv = 0, pairs = 0;
             if (stt == GPK_ERR_STATE && attempt == 0 && gpk_prepared_count(s, &surv, &pairs) == GPK_OK) {
@@ -229,6 +241,10 @@ int gpk_fit(gpk_session* s, const float* volume, const int32_t dims[3], const do
         }
     }
     FIT_TRY(gpk_session_synchronize(s));
+    if (profile)
+        std::fprintf(stderr, "gpk_fit profile: total %.3f s; target %.3f, train_step %.3f, sync %.3f s\n",
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - tfit).count(), prof[0],
+                     prof[1], prof[2]);
     return GPK_OK;
 #undef FIT_TRY
 #undef FIT_CK

@@ -782,27 +782,31 @@ int settle_pairs(gpk_session* s) {
     return GPK_OK;
 }
 
-int copy_params_in(gpk_session* s, uint64_t n, const float* rec) {
-    // AoS record -> 11 SoA planes on the host, then one H2D per plane.
-    std::vector<float> plane(n);
-    for (int k = 0; k < 11; ++k) {
-        for (uint64_t i = 0; i < n; ++i) plane[i] = rec[11 * i + k];
-        CK(cudaMemcpyAsync(s->params.as<float>() + (size_t)k * s->cap, plane.data(), n * 4,
-                           cudaMemcpyHostToDevice, s->stream));
-        CK(cudaStreamSynchronize(s->stream));
-    }
+// Host records (n x 11 f32) -> 11 device planes of stride cap: one H2D copy of
+// the record block into a staging buffer, then the transpose kernel.
+int copy_records_in(gpk_session* s, uint64_t n, const float* rec, float* planes) {
+    DevBuf stage;
+    CK(stage.ensure(n * 44));
+    CK(cudaMemcpyAsync(stage.p, rec, n * 44, cudaMemcpyHostToDevice, s->stream));
+    launch_records_to_planes(stage.as<float>(), n, planes, s->cap, s->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s->stream));  // before the staging buffer is freed
     return GPK_OK;
 }
 
+int copy_params_in(gpk_session* s, uint64_t n, const float* rec) {
+    return copy_records_in(s, n, rec, s->params.as<float>());
+}
+
+// 11 device planes -> host records: transpose into a staging buffer, one D2H copy.
 int copy_planes_out(gpk_session* s, const float* dev, float* rec) {
     const uint64_t n = s->n;
-    std::vector<float> plane(n);
-    for (int k = 0; k < 11; ++k) {
-        CK(cudaMemcpyAsync(plane.data(), dev + (size_t)k * s->cap, n * 4, cudaMemcpyDeviceToHost,
-                           s->stream));
-        CK(cudaStreamSynchronize(s->stream));
-        for (uint64_t i = 0; i < n; ++i) rec[11 * i + k] = plane[i];
-    }
+    DevBuf stage;
+    CK(stage.ensure(n * 44));
+    launch_planes_to_records(dev, s->cap, n, stage.as<float>(), s->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(rec, stage.p, n * 44, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
     return GPK_OK;
 }
 
@@ -1435,6 +1439,12 @@ int gpk_set_gaussians_f64(gpk_session* s, uint64_t n, const double* records,
     return gpk_set_gaussians(s, n, f.data(), bbox);
 }
 
+int gpk_get_bounds(gpk_session* s, gpk_bounds* out) {
+    if (!s || !out) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    *out = s->bbox;
+    return ok();
+}
+
 int gpk_get_gaussians(gpk_session* s, float* records) {
     if (!s || (s->n && !records)) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
     TRY(set_device(s));
@@ -1447,13 +1457,7 @@ int gpk_set_gradients(gpk_session* s, const float* grads) {
     if (!s || (s->n && !grads)) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
     TRY(set_device(s));
     CK(cudaStreamSynchronize(s->stream));
-    const uint64_t n = s->n;
-    std::vector<float> plane(n);
-    for (int k = 0; k < 11; ++k) {
-        for (uint64_t i = 0; i < n; ++i) plane[i] = grads[11 * i + k];
-        CK(cudaMemcpy(s->grads.as<float>() + (size_t)k * s->cap, plane.data(), n * 4,
-                      cudaMemcpyHostToDevice));
-    }
+    if (s->n) TRY(copy_records_in(s, s->n, grads, s->grads.as<float>()));
     s->grads_in_slots = false;
     TRY(mark_grads_dense(s));
     CK(cudaStreamSynchronize(s->stream));
@@ -1715,16 +1719,8 @@ int gpk_set_adam_state(gpk_session* s, const float* m, const float* v, int64_t s
     TRY(set_device(s));
     CK(cudaStreamSynchronize(s->stream));
     const uint64_t n = s->n;
-    std::vector<float> plane(n);
-    for (int which = 0; which < 2; ++which) {
-        const float* src = which ? v : m;
-        float* dst = which ? s->adam_v.as<float>() : s->adam_m.as<float>();
-        if (!src) continue;
-        for (int k = 0; k < 11; ++k) {
-            for (uint64_t i = 0; i < n; ++i) plane[i] = src[11 * i + k];
-            CK(cudaMemcpy(dst + (size_t)k * s->cap, plane.data(), n * 4, cudaMemcpyHostToDevice));
-        }
-    }
+    if (m && n) TRY(copy_records_in(s, n, m, s->adam_m.as<float>()));
+    if (v && n) TRY(copy_records_in(s, n, v, s->adam_v.as<float>()));
     long long st = step;
     CK(cudaMemcpy(s->adam_step(), &st, 8, cudaMemcpyHostToDevice));
     return ok();

@@ -56,7 +56,7 @@ def random_densify_case(seed, n=3000, ext=64.0):
     lo, hi = (0.0, 0.0, 0.0), (ext, ext, ext)
     rec = np.zeros((n, 11))
     rec[:, 0:3] = rng.uniform(0, ext, (n, 3))
-    rec[:, 3:6] = np.log(rng.uniform(0.15, 1.6, (n, 3)))   # split threshold 0.01 * 64 = 0.64
+    rec[:, 3:6] = np.log(rng.uniform(0.1, 1.0, (n, 3)))    # split threshold 0.01 * 64 = 0.64
     q = rng.normal(size=(n, 4))
     rec[:, 6:10] = q / np.linalg.norm(q, axis=1, keepdims=True)
     alpha = rng.uniform(0.005, 0.3, n)                      # some below tau = 0.02

@@ -356,6 +356,12 @@ int gpk_set_densify_accum(gpk_session* s, const double* grad_norm_sum, const int
  * parent order. Resets the accumulator. */
 int gpk_densify_and_prune(gpk_session* s, const gpk_densify_config* cfg, gpk_rng* rng,
                           gpk_densify_report* report);
+/* The same with the normals drawn by the caller's generator (e.g. the
+ * reference's own gpile::Rng): normal(user) is called 6 times per split
+ * parent, in parent order, before any parameter changes. */
+typedef double (*gpk_normal_fn)(void* user);
+int gpk_densify_and_prune_draw(gpk_session* s, const gpk_densify_config* cfg, gpk_normal_fn normal,
+                               void* user, gpk_densify_report* report);
 
 /* ---- fit driver (optimize.hpp:360-424) --------------------------------------- */
 typedef struct {

@@ -15,6 +15,10 @@
 //   adam_step             optimize.hpp:195      adam_step
 //   voxelize              voxelize.hpp:113      voxelize
 //   voxelize_backward     voxelize.hpp:152      voxelize_backward
+//   densify_and_prune     optimize.hpp:255      densify_and_prune
+//   fit                   optimize.hpp:360      fit
+//   save_checkpoint       checkpoint.hpp:38     save_checkpoint
+//   load_checkpoint       checkpoint.hpp:60     load_checkpoint
 //
 // Errors: GPK_ERR_INVALID_ARGUMENT -> std::invalid_argument,
 // GPK_ERR_DEGENERATE_COVARIANCE -> gpile::DegenerateCovariance,
@@ -35,6 +39,7 @@
 #pragma once
 
 #include <gpile/backward.hpp>
+#include <gpile/checkpoint.hpp>
 #include <gpile/core.hpp>
 #include <gpile/errors.hpp>
 #include <gpile/image.hpp>
@@ -44,6 +49,7 @@
 #include <gpile/voxelize.hpp>
 
 #include <cstring>
+#include <exception>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -63,6 +69,8 @@ inline void check(int status) {
         case GPK_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
         case GPK_ERR_DEGENERATE_COVARIANCE: throw DegenerateCovariance(msg);
         case GPK_ERR_NUMERIC_FAILURE: throw NumericFailure(msg);
+        case GPK_ERR_CORRUPT_CONTAINER: throw CorruptContainer(msg);
+        case GPK_ERR_LOAD: throw LoadError(msg);
         default: throw std::runtime_error(msg);
     }
 }
@@ -441,6 +449,174 @@ inline GaussianGradients voxelize_backward(const GaussianSet& set, const Voxeliz
     std::vector<float> g(set.size() * 11);
     check(gpk_voxelize_backward(s.handle(), &c, dl.data(), g.data()));
     return detail::grads_of(g, set.size());
+}
+
+// ---- optimize.hpp: adaptive density control, fit -------------------------------
+namespace detail {
+
+inline void adam_records(const AdamState& st, std::vector<float>& m, std::vector<float>& v) {
+    const std::size_t n = st.size();
+    m.assign(n * 11, 0.0f);
+    v.assign(n * 11, 0.0f);
+    for (std::size_t i = 0; i < n; ++i) {
+        const double mm[11] = {st.m_mu[i].x, st.m_mu[i].y, st.m_mu[i].z, st.m_ls[i].x, st.m_ls[i].y, st.m_ls[i].z,
+                               st.m_q[i].w, st.m_q[i].x, st.m_q[i].y, st.m_q[i].z, st.m_a[i]};
+        const double vv[11] = {st.v_mu[i].x, st.v_mu[i].y, st.v_mu[i].z, st.v_ls[i].x, st.v_ls[i].y, st.v_ls[i].z,
+                               st.v_q[i].w, st.v_q[i].x, st.v_q[i].y, st.v_q[i].z, st.v_a[i]};
+        for (int k = 0; k < 11; ++k) {
+            m[11 * i + k] = static_cast<float>(mm[k]);
+            v[11 * i + k] = static_cast<float>(vv[k]);
+        }
+    }
+}
+
+inline void store_adam(const std::vector<float>& m, const std::vector<float>& v, AdamState& st) {
+    const std::size_t n = m.size() / 11;
+    st.resize(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const float* a = &m[11 * i];
+        const float* b = &v[11 * i];
+        st.m_mu[i] = {a[0], a[1], a[2]};
+        st.m_ls[i] = {a[3], a[4], a[5]};
+        st.m_q[i] = {a[6], a[7], a[8], a[9]};
+        st.m_a[i] = a[10];
+        st.v_mu[i] = {b[0], b[1], b[2]};
+        st.v_ls[i] = {b[3], b[4], b[5]};
+        st.v_q[i] = {b[6], b[7], b[8], b[9]};
+        st.v_a[i] = b[10];
+    }
+}
+
+// The resident set of `s` (any size) into `set`.
+inline void fetch_set(gpk_session* s, GaussianSet& set) {
+    uint64_t n = 0;
+    check(gpk_gaussian_count(s, &n));
+    std::vector<float> r(n * 11);
+    if (n) check(gpk_get_gaussians(s, r.data()));
+    set.primitives.resize(n);
+    store_records(r, set);
+}
+
+}  // namespace detail
+
+// densify_and_prune(set, adam, accum, cfg, rng) (optimize.hpp:255-344): the
+// split normals come from the caller's own generator, in the reference's order.
+inline DensifyReport densify_and_prune(GaussianSet& set, AdamState& adam, const DensifyAccum& accum,
+                                       const FitConfig& cfg, Rng& rng) {
+    const std::size_t n = set.size();
+    if (adam.size() != n || accum.observations.size() != n)
+        throw std::invalid_argument("densify_and_prune: size mismatch");
+    Session& s = default_session();
+    s.set_gaussians(set);
+    std::vector<float> m, v;
+    detail::adam_records(adam, m, v);
+    check(gpk_set_adam_state(s.handle(), m.data(), v.data(), adam.step));
+    check(gpk_densify_accum_enable(s.handle(), 1));
+    std::vector<double> wsum(3 * n);
+    for (std::size_t i = 0; i < n; ++i)
+        for (int d = 0; d < 3; ++d) wsum[3 * i + d] = accum.world_grad_sum[i][d];
+    std::vector<int32_t> obs(accum.observations.begin(), accum.observations.end());
+    check(gpk_set_densify_accum(s.handle(), accum.grad_norm_sum.data(), obs.data(), wsum.data()));
+    const gpk_densify_config c{cfg.tau, cfg.grad_threshold, cfg.split_scale_fraction, cfg.split_scale_divisor,
+                               cfg.scale_modifier};
+    gpk_densify_report rep{};
+    const int st = gpk_densify_and_prune_draw(
+        s.handle(), &c, [](void* u) { return static_cast<Rng*>(u)->normal(); }, &rng, &rep);
+    gpk_densify_accum_enable(s.handle(), 0);
+    check(st);
+    detail::fetch_set(s.handle(), set);
+    int64_t step = 0;
+    m.assign(set.size() * 11, 0.0f);
+    v.assign(set.size() * 11, 0.0f);
+    check(gpk_get_adam_state(s.handle(), m.data(), v.data(), &step));
+    detail::store_adam(m, v, adam);
+    adam.step = static_cast<long>(step);
+    DensifyReport out;
+    out.pruned = rep.pruned;
+    out.cloned = rep.cloned;
+    out.split = rep.split;
+    return out;
+}
+
+// fit(volume, psf, cfg, progress) (optimize.hpp:360-424) on the device: the
+// volume stays resident, the loop runs in the library (gpk_fit).
+inline GaussianSet fit(const VolumeGrid& volume, const PsfSpec& psf, const FitConfig& cfg,
+                       const ProgressSink& progress = nullptr) {
+    volume.validate();
+    psf.validate();
+    cfg.validate();
+    const std::vector<float> vol(volume.data.begin(), volume.data.end());
+    gpk_fit_config c{};
+    c.iterations = cfg.iterations;
+    c.lr_position = cfg.lr_position;
+    c.lr_opacity = cfg.lr_opacity;
+    c.lr_scale = cfg.lr_scale;
+    c.lr_rotation = cfg.lr_rotation;
+    c.init_count = cfg.init_count;
+    c.tau = cfg.tau;
+    c.densify_start = cfg.densify_start;
+    c.densify_end = cfg.densify_end;
+    c.grad_threshold = cfg.grad_threshold;
+    c.lambda = cfg.lambda;
+    c.densify_interval = cfg.densify_interval;
+    c.rng_seed = cfg.rng_seed;
+    c.init_mode = cfg.init_mode == "grid" ? 1 : 0;
+    c.scale_modifier = cfg.scale_modifier;
+    c.split_scale_fraction = cfg.split_scale_fraction;
+    c.split_scale_divisor = cfg.split_scale_divisor;
+    c.dssim_scale = cfg.dssim_scale;
+    c.progress_interval = cfg.progress_interval;
+    c.tile_size = cfg.tile_size;
+    c.footprint_sigmas = cfg.footprint_sigmas;
+    struct Sink {
+        const ProgressSink* fn;
+        std::exception_ptr err;
+    } sink{&progress, nullptr};
+    auto tramp = [](const gpk_fit_progress* p, void* u) {
+        Sink* k = static_cast<Sink*>(u);
+        if (k->err) return;
+        try {
+            FitProgress fp;
+            fp.iteration = p->iteration;
+            fp.loss = p->loss;
+            fp.count = p->count;
+            fp.psnr2d = p->psnr2d;
+            fp.monitor_loss = p->monitor_loss;
+            (*k->fn)(fp);
+        } catch (...) {
+            k->err = std::current_exception();
+        }
+    };
+    Session& s = default_session();
+    const double spacing[3] = {volume.spacing.x, volume.spacing.y, volume.spacing.z};
+    const double origin[3] = {volume.origin.x, volume.origin.y, volume.origin.z};
+    const gpk_psf f = detail::psf_of(psf);
+    const int st = gpk_fit(s.handle(), vol.data(), volume.dims, spacing, origin, &f, &c,
+                           progress ? +tramp : nullptr, &sink);
+    if (sink.err) std::rethrow_exception(sink.err);
+    check(st);
+    GaussianSet set;
+    set.bbox = volume.world_bounds();
+    detail::fetch_set(s.handle(), set);
+    return set;
+}
+
+// ---- checkpoint.hpp ----------------------------------------------------------------
+inline void save_checkpoint(const GaussianSet& set, const std::string& path) {
+    Session& s = default_session();
+    s.set_gaussians(set);
+    check(gpk_save_checkpoint(s.handle(), path.c_str()));
+}
+
+inline GaussianSet load_checkpoint(const std::string& path) {
+    Session& s = default_session();
+    check(gpk_load_checkpoint(s.handle(), path.c_str()));
+    GaussianSet set;
+    gpk_bounds b;
+    check(gpk_get_bounds(s.handle(), &b));
+    set.bbox = {{b.min[0], b.min[1], b.min[2]}, {b.max[0], b.max[1], b.max[2]}};
+    detail::fetch_set(s.handle(), set);
+    return set;
 }
 
 }  // namespace b200

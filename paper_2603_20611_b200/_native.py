@@ -125,6 +125,7 @@ class FitProgressC(C.Structure):
 
 
 PROGRESS_FN = C.CFUNCTYPE(None, C.POINTER(FitProgressC), C.c_void_p)
+NORMAL_FN = C.CFUNCTYPE(C.c_double, C.c_void_p)
 
 
 def _load() -> C.CDLL:
@@ -223,6 +224,8 @@ _PROTOS = {
     "gpk_get_densify_accum": (C.c_int, [_P, _D, _I32, _D]),
     "gpk_set_densify_accum": (C.c_int, [_P, _D, _I32, _D]),
     "gpk_densify_and_prune": (C.c_int, [_P, C.POINTER(DensifyConfigC), _P, C.POINTER(DensifyReportC)]),
+    "gpk_densify_and_prune_draw": (C.c_int, [_P, C.POINTER(DensifyConfigC), NORMAL_FN, _P,
+                                             C.POINTER(DensifyReportC)]),
     "gpk_fit": (C.c_int, [_P, _F, _I32, _D, _D, C.POINTER(PsfC), C.POINTER(FitConfigC), PROGRESS_FN, _P]),
     "gpk_nccl_get_unique_id": (C.c_int, [_P]),
     "gpk_comm_init": (C.c_int, [_P, C.c_int, C.c_int, _P]),

@@ -2302,9 +2302,21 @@ int gpk_set_densify_accum(gpk_session* s, const double* grad_norm_sum, const int
 // generator (drawn in parent order, as the reference draws them), emit into
 // fresh planes, then the new set (moments carried over, the step counter
 // kept) replaces the old one. The accumulator is reset (fit, optimize.hpp:400).
+static double draw_from_gpk_rng(void* user) {
+    double v = 0.0;
+    gpk_rng_normal(static_cast<gpk_rng*>(user), &v);
+    return v;
+}
+
 int gpk_densify_and_prune(gpk_session* s, const gpk_densify_config* cfg, gpk_rng* rng,
                           gpk_densify_report* report) {
-    if (!s || !cfg || !rng) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (!rng) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    return gpk_densify_and_prune_draw(s, cfg, draw_from_gpk_rng, rng, report);
+}
+
+int gpk_densify_and_prune_draw(gpk_session* s, const gpk_densify_config* cfg, gpk_normal_fn normal,
+                               void* user, gpk_densify_report* report) {
+    if (!s || !cfg || !normal) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
     if (!s->accum_on) return fail(GPK_ERR_STATE, "densify accumulator not enabled");
     if (!(cfg->split_scale_divisor > 0.0)) return fail(GPK_ERR_INVALID_ARGUMENT, "split_scale_divisor must be > 0");
     TRY(set_device(s));
@@ -2350,7 +2362,7 @@ int gpk_densify_and_prune(gpk_session* s, const gpk_densify_config* cfg, gpk_rng
     const uint64_t n_new = kept + born;
     if (n_new >= (1ull << 31)) return fail(GPK_ERR_INVALID_ARGUMENT, "densify: set size must stay < 2^31");
     std::vector<double> xi(6 * split);
-    for (uint64_t k = 0; k < xi.size(); ++k) TRY(gpk_rng_normal(rng, &xi[k]));
+    for (uint64_t k = 0; k < xi.size(); ++k) xi[k] = normal(user);  // in parent order (:310)
     CK(normals.ensure(std::max<uint64_t>(xi.size(), 1) * 8));
     if (!xi.empty()) CK(cudaMemcpyAsync(normals.p, xi.data(), xi.size() * 8, cudaMemcpyHostToDevice, s->stream));
     const uint64_t need = (std::max<uint64_t>(n_new, 1) + kParamAlign - 1) / kParamAlign * kParamAlign;

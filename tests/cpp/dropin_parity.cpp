@@ -9,6 +9,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <fstream>
+#include <iterator>
+#include <string>
 #include <stdexcept>
 
 #include "../../include/gpile_b200.hpp"
@@ -195,6 +198,104 @@ int main() {
         threw = true;
     }
     expect(threw, "zero quaternion -> std::invalid_argument");
+
+    // densify_and_prune (optimize.hpp:255-344): same inputs, same Rng seed
+    {
+        GaussianSet ds = f32_set(init_random(2000, {{0, 0, 0}, {40, 40, 40}}, 0.4, 12));
+        Rng r0(77);
+        AdamState ad(ds.size());
+        DensifyAccum acc(ds.size());
+        for (std::size_t i = 0; i < ds.size(); ++i) {
+            acc.observations[i] = (int)(i % 4);
+            acc.grad_norm_sum[i] = acc.observations[i] * r0.uniform(0.0, 1e-4);
+            acc.world_grad_sum[i] = {r0.normal(), r0.normal(), r0.normal()};
+            ad.m_a[i] = (double)(float)r0.normal();
+        }
+        ad.step = 9;
+        FitConfig fc;
+        GaussianSet d_ref = ds, d_gpu = ds;
+        AdamState a1 = ad, a2 = ad;
+        Rng g1(31), g2(31);
+        const DensifyReport r_ref = densify_and_prune(d_ref, a1, acc, fc, g1);
+        const DensifyReport r_gpu = b200::densify_and_prune(d_gpu, a2, acc, fc, g2);
+        bool dok = r_ref.pruned == r_gpu.pruned && r_ref.cloned == r_gpu.cloned && r_ref.split == r_gpu.split &&
+                   d_ref.size() == d_gpu.size() && a2.size() == d_gpu.size() && a2.step == 9 &&
+                   r_ref.cloned > 0 && r_ref.split > 0 && r_ref.pruned > 0;
+        for (std::size_t i = 0; dok && i < d_ref.size(); ++i) {
+            for (int k = 0; k < 3; ++k)
+                dok = dok && std::fabs(d_ref.primitives[i].mu[k] - d_gpu.primitives[i].mu[k]) <=
+                                 2e-7 * std::fabs(d_ref.primitives[i].mu[k]) + 1e-6;
+            dok = dok && (float)a1.m_a[i] == (float)a2.m_a[i];
+        }
+        dok = dok && g1.normal() == g2.normal();  // the caller's generator advanced identically
+        expect(dok, "densify_and_prune: report, order, moments, generator state");
+    }
+
+    // fit (optimize.hpp:360-424) on a blob volume, progress every 25
+    {
+        VolumeGrid fv;
+        fv.dims[0] = 24;
+        fv.dims[1] = 24;
+        fv.dims[2] = 8;
+        fv.data.assign(fv.voxel_count(), 0.0);
+        for (int k = 0; k < 8; ++k)
+            for (int j = 0; j < 24; ++j)
+                for (int i = 0; i < 24; ++i) {
+                    const double dx = (i - 12.0) / 3.0, dy = (j - 12.0) / 3.0, dz = (k - 3.0) / 1.5;
+                    fv.at(i, j, k) = (double)(float)(0.9 * std::exp(-0.5 * (dx * dx + dy * dy + dz * dz)));
+                }
+        FitConfig fc;
+        fc.iterations = 200;
+        fc.init_count = 16;
+        fc.densify_start = 100;
+        fc.densify_end = 200;
+        fc.densify_interval = 100;
+        fc.rng_seed = 11;
+        fc.progress_interval = 50;
+        std::vector<FitProgress> pr, pg;
+        const GaussianSet f_ref = fit(fv, PsfSpec{}, fc, [&](const FitProgress& p) { pr.push_back(p); });
+        const GaussianSet f_gpu = b200::fit(fv, PsfSpec{}, fc, [&](const FitProgress& p) { pg.push_back(p); });
+        bool fok = pr.size() == pg.size() && f_ref.size() == f_gpu.size() && f_gpu.size() > 16;
+        for (std::size_t i = 0; fok && i < pr.size(); ++i)
+            fok = pr[i].iteration == pg[i].iteration && pr[i].count == pg[i].count &&
+                  std::fabs(pr[i].loss - pg[i].loss) <= 2e-3 * std::fabs(pr[i].loss) &&
+                  std::fabs(pr[i].psnr2d - pg[i].psnr2d) <= 0.05;
+        expect(fok, "fit: progress (count, loss, PSNR) tracks the reference");
+        bool threw_cfg = false;
+        try {
+            FitConfig bad = fc;
+            bad.densify_start = 300;
+            bad.densify_end = 200;
+            b200::fit(fv, PsfSpec{}, bad);
+        } catch (const std::invalid_argument&) {
+            threw_cfg = true;
+        }
+        expect(threw_cfg, "fit: FitConfig validation -> std::invalid_argument");
+    }
+
+    // checkpoints (checkpoint.hpp:38-92): byte-identical files, round trip
+    {
+        const std::string a = "/tmp/gpk_dropin_a.gpile", b = "/tmp/gpk_dropin_b.gpile";
+        save_checkpoint(set, a);
+        b200::save_checkpoint(set, b);
+        std::ifstream fa(a, std::ios::binary), fb(b, std::ios::binary);
+        const std::string ba((std::istreambuf_iterator<char>(fa)), {}), bb((std::istreambuf_iterator<char>(fb)), {});
+        const GaussianSet back = b200::load_checkpoint(a);
+        bool cok = ba == bb && back.size() == set.size() && back.bbox.max.x == set.bbox.max.x;
+        for (std::size_t i = 0; cok && i < set.size(); ++i)
+            cok = back.primitives[i].mu.y == set.primitives[i].mu.y &&
+                  back.primitives[i].alpha_raw == set.primitives[i].alpha_raw;
+        expect(cok, "save/load_checkpoint: byte-identical file, bitwise round trip");
+        bool threw_c = false;
+        try {
+            b200::load_checkpoint("/tmp/gpk_dropin_missing.gpile");
+        } catch (const LoadError&) {
+            threw_c = true;
+        }
+        expect(threw_c, "load_checkpoint: missing file -> gpile::LoadError");
+        std::remove(a.c_str());
+        std::remove(b.c_str());
+    }
 
     std::printf("%s\n", failures ? "DROPIN PARITY FAILED" : "DROPIN PARITY OK");
     return failures ? 1 : 0;

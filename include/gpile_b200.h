@@ -324,6 +324,35 @@ uint64_t gpk_checkpoint_bytes(uint64_t count);   /* checkpoint_bytes (checkpoint
 /* The set's world bbox (GaussianSet::bbox, core.hpp:67-74). */
 int gpk_get_bounds(gpk_session* s, gpk_bounds* out);
 
+/* ---- codec front half (morton.hpp, quant.hpp, container.hpp:136-230) --------- */
+typedef struct {
+    int32_t pos_bits;      /* 14, per axis */
+    int32_t opacity_bits;  /* 12 */
+    int32_t scale_bits;    /* 12, on log-scale */
+    int32_t quat_bits;     /* 12, per component */
+    int32_t morton_bits;   /* 14, per axis */
+} gpk_quant_spec;          /* QuantSpec (quant.hpp:13-26), widths in [4, 21] */
+
+/* morton_sort(set, bits) (morton.hpp:33-48) of the resident set: the stable
+ * Z-order permutation (n entries; perm[k] = set index of the k-th). */
+int gpk_morton_sort(gpk_session* s, int32_t bits, uint64_t* perm_out);
+/* quantize (quant.hpp:67-132) of the resident set — in Morton order
+ * (morton_order != 0, as encode() does, container.hpp:203-206) or set order:
+ * positions 3n, opacities n, log_scales 3n, quats 4n (u32), and the observed
+ * log-scale range. Non-finite / zero-quaternion inputs -> INVALID_ARGUMENT
+ * naming the (quantized-order) index, as the reference throws. */
+int gpk_quantize(gpk_session* s, const gpk_quant_spec* spec, int32_t morton_order, uint32_t* positions,
+                 uint32_t* opacities, uint32_t* log_scales, uint32_t* quats, double scale_min[3],
+                 double scale_max[3]);
+/* encode()'s front half (container.hpp:203-230): Morton sort, quantize, and
+ * the delta + zig-zag packing of each stream (detail::pack_deltas,
+ * container.hpp:136-156) — the byte streams LZMA then compresses.
+ * Sizes: gpk_stream_bytes(n, 3, pos_bits), (n, 1, opacity_bits),
+ * (n, 3, scale_bits), (n, 4, quat_bits). */
+int gpk_encode_streams(gpk_session* s, const gpk_quant_spec* spec, uint8_t* positions, uint8_t* opacities,
+                       uint8_t* log_scales, uint8_t* quats, double scale_min[3], double scale_max[3]);
+uint64_t gpk_stream_bytes(uint64_t count, int32_t components, int32_t bits);
+
 /* ---- adaptive density control (optimize.hpp:228-344) ------------------------ */
 typedef struct {
     double tau;                  /* prune exposed alpha < tau (FitConfig::tau) */

@@ -22,6 +22,9 @@
 
 #include "gpile/backward.hpp"
 #include "gpile/checkpoint.hpp"
+#include "gpile/container.hpp"  // pack_deltas only (oracle/stub/lzma.h)
+#include "gpile/morton.hpp"
+#include "gpile/quant.hpp"
 #include "gpile/core.hpp"
 #include "gpile/errors.hpp"
 #include "gpile/loss.hpp"
@@ -728,5 +731,55 @@ int gref_load_checkpoint(const char* path, double* out, uint64_t capacity, uint6
     }
 }
 uint64_t gref_checkpoint_bytes(uint64_t count) { return checkpoint_bytes(count); }
+
+
+// ---- codec front half (morton.hpp:33-48, quant.hpp:67-132, container.hpp:136-156)
+int gref_morton_sort(void* s, int bits, uint64_t* perm) {
+    return guarded([&] {
+        const auto p = morton_sort(*static_cast<GaussianSet*>(s), bits);
+        for (std::size_t k = 0; k < p.size(); ++k) perm[k] = p[k];
+    });
+}
+
+// quantize of the set (in morton order when morton_order: encode's order)
+int gref_quantize(void* s, const gpk_quant_spec* spec, int morton_order, uint32_t* pos, uint32_t* opa,
+                  uint32_t* ls, uint32_t* quat, double* smin, double* smax) {
+    return guarded([&] {
+        QuantSpec q;
+        q.pos_bits = spec->pos_bits;
+        q.opacity_bits = spec->opacity_bits;
+        q.scale_bits = spec->scale_bits;
+        q.quat_bits = spec->quat_bits;
+        q.morton_bits = spec->morton_bits;
+        const GaussianSet& set = *static_cast<GaussianSet*>(s);
+        const QuantizedSet qs = morton_order ? quantize(apply_permutation(set, morton_sort(set, q.morton_bits)), q)
+                                             : quantize(set, q);
+        std::copy(qs.positions.begin(), qs.positions.end(), pos);
+        std::copy(qs.opacities.begin(), qs.opacities.end(), opa);
+        std::copy(qs.log_scales.begin(), qs.log_scales.end(), ls);
+        std::copy(qs.quats.begin(), qs.quats.end(), quat);
+        for (int d = 0; d < 3; ++d) {
+            smin[d] = qs.scale_min[d];
+            smax[d] = qs.scale_max[d];
+        }
+    });
+}
+
+int gref_pack_deltas(const uint32_t* values, uint64_t total, int components, int bits, uint8_t* out) {
+    return guarded([&] {
+        const std::vector<std::uint32_t> v(values, values + total);
+        const auto b = detail::pack_deltas(v, components, bits);
+        std::copy(b.begin(), b.end(), out);
+    });
+}
+
+int gref_unpack_deltas(const uint8_t* bytes, uint64_t nbytes, uint64_t count, int components, int bits,
+                       uint32_t* out) {
+    return guarded([&] {
+        const std::vector<std::uint8_t> b(bytes, bytes + nbytes);
+        const auto v = detail::unpack_deltas(b, count, components, bits, "test");
+        std::copy(v.begin(), v.end(), out);
+    });
+}
 
 }  // extern "C"

@@ -119,6 +119,11 @@ class FitConfigC(C.Structure):
     ]
 
 
+class QuantSpecC(C.Structure):
+    _fields_ = [("pos_bits", C.c_int32), ("opacity_bits", C.c_int32), ("scale_bits", C.c_int32),
+                ("quat_bits", C.c_int32), ("morton_bits", C.c_int32)]
+
+
 class FitProgressC(C.Structure):
     _fields_ = [("iteration", C.c_int32), ("loss", C.c_double), ("count", C.c_uint64),
                 ("psnr2d", C.c_double), ("monitor_loss", C.c_double)]
@@ -208,6 +213,10 @@ _PROTOS = {
     "gpk_init_random": (C.c_int, [C.c_uint64, C.POINTER(Bounds), C.c_double, C.c_uint64, _D]),
     "gpk_slice_pose_for_index": (C.c_int, [_I32, _D, _D, C.c_int, C.POINTER(SlicePoseC)]),
     "gpk_lr_at": (C.c_double, [C.c_double, C.c_int, C.c_int]),
+    "gpk_morton_sort": (C.c_int, [_P, C.c_int32, _U64]),
+    "gpk_quantize": (C.c_int, [_P, C.POINTER(QuantSpecC), C.c_int32, _U32, _U32, _U32, _U32, _D, _D]),
+    "gpk_encode_streams": (C.c_int, [_P, C.POINTER(QuantSpecC), _P, _P, _P, _P, _D, _D]),
+    "gpk_stream_bytes": (C.c_uint64, [C.c_uint64, C.c_int32, C.c_int32]),
     "gpk_save_checkpoint": (C.c_int, [_P, C.c_char_p]),
     "gpk_load_checkpoint": (C.c_int, [_P, C.c_char_p]),
     "gpk_checkpoint_bytes": (C.c_uint64, [C.c_uint64]),

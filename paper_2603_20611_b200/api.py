@@ -39,6 +39,7 @@ __all__ = [
     "slice_pose_for_index", "default_session", "init_grid", "default_init_count", "Rng",
     "DensifyConfig", "DensifyReport", "DensifyAccum", "FitConfig", "FitProgress", "fit",
     "save_checkpoint", "load_checkpoint", "checkpoint_bytes", "CorruptContainer", "LoadError",
+    "QuantSpec", "QuantizedStreams",
     "DegenerateCovariance", "NumericFailure", "InvalidArgument", "GpileError", "StateError",
 ]
 
@@ -297,6 +298,32 @@ class FitConfig:
                             0 if self.init_mode == "random" else 1, self.scale_modifier,
                             self.split_scale_fraction, self.split_scale_divisor, self.dssim_scale,
                             int(self.progress_interval), int(self.tile_size), self.footprint_sigmas)
+
+
+@dataclass
+class QuantSpec:
+    """QuantSpec (quant.hpp:13-26)."""
+
+    pos_bits: int = 14
+    opacity_bits: int = 12
+    scale_bits: int = 12
+    quat_bits: int = 12
+    morton_bits: int = 14
+
+    def to_c(self) -> N.QuantSpecC:
+        return N.QuantSpecC(self.pos_bits, self.opacity_bits, self.scale_bits, self.quat_bits, self.morton_bits)
+
+
+@dataclass
+class QuantizedStreams:
+    """QuantizedSet's integer streams (quant.hpp:29-39) or encode()'s packed byte streams."""
+
+    positions: np.ndarray
+    opacities: np.ndarray
+    log_scales: np.ndarray
+    quats: np.ndarray
+    scale_min: tuple
+    scale_max: tuple
 
 
 @dataclass
@@ -582,6 +609,35 @@ class Session:
         check(N.lib.gpk_voxelize_backward(self._h, C.byref(c), None if d is None else N.fptr(d),
                                           N.fptr(out)))
         return out
+
+    # ---- codec front half (morton.hpp, quant.hpp, container.hpp) ----
+    def morton_sort(self, bits: int = 14) -> np.ndarray:
+        perm = np.zeros(self.n, np.uint64)
+        check(N.lib.gpk_morton_sort(self._h, int(bits), perm.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return perm
+
+    def quantize(self, spec: QuantSpec | None = None, morton_order: bool = False) -> QuantizedStreams:
+        spec = spec or QuantSpec()
+        n = self.n
+        pos, opa = np.zeros(3 * n, np.uint32), np.zeros(n, np.uint32)
+        ls, qt = np.zeros(3 * n, np.uint32), np.zeros(4 * n, np.uint32)
+        lo, hi = np.zeros(3), np.zeros(3)
+        c = spec.to_c()
+        check(N.lib.gpk_quantize(self._h, C.byref(c), 1 if morton_order else 0, N.u32ptr(pos), N.u32ptr(opa),
+                                 N.u32ptr(ls), N.u32ptr(qt), N.dptr(lo), N.dptr(hi)))
+        return QuantizedStreams(pos, opa, ls, qt, tuple(lo), tuple(hi))
+
+    def encode_streams(self, spec: QuantSpec | None = None) -> QuantizedStreams:
+        spec = spec or QuantSpec()
+        n = self.n
+        sb = N.lib.gpk_stream_bytes
+        bufs = [np.zeros(sb(n, k, b), np.uint8) for k, b in
+                ((3, spec.pos_bits), (1, spec.opacity_bits), (3, spec.scale_bits), (4, spec.quat_bits))]
+        lo, hi = np.zeros(3), np.zeros(3)
+        c = spec.to_c()
+        check(N.lib.gpk_encode_streams(self._h, C.byref(c), *[b.ctypes.data_as(C.c_void_p) for b in bufs],
+                                       N.dptr(lo), N.dptr(hi)))
+        return QuantizedStreams(*bufs, tuple(lo), tuple(hi))
 
     # ---- checkpoints (checkpoint.hpp:38-92) ----
     def bounds(self) -> tuple:

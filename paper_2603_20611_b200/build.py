@@ -27,6 +27,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 PER_FILE = {
     "prep.cu": ["--fmad=false"],
     "densify.cu": ["--fmad=false"],
+    "codec.cu": ["--fmad=false"],
 }
 
 

@@ -86,3 +86,22 @@ def test_fit_config_layout_matches_header(gp):
     assert c.iterations == 30000 and c.densify_start == 500 and c.densify_end == 25000
     with pytest.raises(gp.InvalidArgument):
         gp.FitConfig(init_mode="hexagonal").to_c()
+
+
+def test_reference_pack_unpack_round_trip(ref):
+    """The reference's pack_deltas / unpack_deltas (container.hpp:136-181), built
+    into oracle/_ref against the declaration-only lzma stub, invert each other."""
+    U32 = C.POINTER(C.c_uint32)
+    rng = np.random.default_rng(2)
+    for comps, bits in ((3, 14), (1, 12), (4, 21), (3, 4)):
+        v = rng.integers(0, 1 << bits, 999 * comps).astype(np.uint32)
+        w = (bits + 7) // 8
+        b = np.zeros(v.size * w, np.uint8)
+        ref.lib.gref_pack_deltas.argtypes = [U32, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint8)]
+        assert ref.lib.gref_pack_deltas(v.ctypes.data_as(U32), v.size, comps, bits,
+                                        b.ctypes.data_as(C.POINTER(C.c_uint8))) == 0
+        back = np.zeros_like(v)
+        ref.lib.gref_unpack_deltas.argtypes = [C.POINTER(C.c_uint8), C.c_uint64, C.c_uint64, C.c_int, C.c_int, U32]
+        assert ref.lib.gref_unpack_deltas(b.ctypes.data_as(C.POINTER(C.c_uint8)), b.size, 999, comps, bits,
+                                          back.ctypes.data_as(U32)) == 0
+        assert np.array_equal(back, v)

@@ -178,6 +178,18 @@ int gpk_fit(gpk_session* s, const float* volume, const int32_t dims[3], const do
         return fail_fit(code, "fit: iteration " + std::to_string(it) + ": " + gpk_last_error_message());
     };
 
+    // After the densify window the set size is fixed: each slice's step is a
+    // CUDA graph captured once (GPK_FIT_NO_GRAPHS=1: direct launches).
+    const bool graphs = std::getenv("GPK_FIT_NO_GRAPHS") == nullptr;
+    std::vector<int32_t> graph_of(Z, -1);
+    auto drop_graphs = [&] {
+        gpk_graph_destroy_all(s);
+        std::fill(graph_of.begin(), graph_of.end(), -1);
+    };
+    struct GraphGuard {
+        gpk_session* s;
+        ~GraphGuard() { gpk_graph_destroy_all(s); }
+    } graph_guard{s};
     double prof[4] = {0, 0, 0, 0};
     const bool profile = std::getenv("GPK_FIT_PROFILE") != nullptr;
     const auto tfit = std::chrono::steady_clock::now();
@@ -195,7 +207,24 @@ int gpk_fit(gpk_session* s, const float* volume, const int32_t dims[3], const do
             int stt = load_target(k);
             if (stt != GPK_OK) return iter_fail(it, stt);
             const auto t1 = std::chrono::steady_clock::now();
-            stt = gpk_train_step(s, &pose, psf, &rcfg, cfg->lambda, cfg->dssim_scale, &lr0, cfg->iterations);
+            if (graphs && it > cfg->densify_end) {
+                // the set is frozen: replay the step's CUDA graph for this slice
+                // (captured on first use; bitwise the direct step)
+                for (int g = 0; g < 2; ++g) {
+                    stt = GPK_OK;
+                    if (graph_of[k] < 0) {
+                        int32_t gid = -1;
+                        stt = gpk_graph_capture_train(s, &pose, psf, &rcfg, cfg->lambda, cfg->dssim_scale, &lr0,
+                                                      cfg->iterations, &gid);
+                        if (stt == GPK_OK) graph_of[k] = gid;
+                    }
+                    if (stt == GPK_OK) stt = gpk_graph_launch(s, graph_of[k]);
+                    if (stt != GPK_ERR_STATE) break;
+                    drop_graphs();  // buffers were reallocated since capture
+                }
+            } else {
+                stt = gpk_train_step(s, &pose, psf, &rcfg, cfg->lambda, cfg->dssim_scale, &lr0, cfg->iterations);
+            }
             const auto t2 = std::chrono::steady_clock::now();
             if (stt == GPK_OK) stt = gpk_session_synchronize(s);
             const auto t3 = std::chrono::steady_clock::now();
@@ -206,7 +235,10 @@ int gpk_fit(gpk_session* s, const float* volume, const int32_t dims[3], const do
             uint64_t surv = 0, pairs = 0;
             if (stt == GPK_ERR_STATE && attempt == 0 && gpk_prepared_count(s, &surv, &pairs) == GPK_OK) {
                 // pair overflow: nothing was updated; grow the buffers and replay
-                if (gpk_session_reserve_pairs(s, pairs + pairs / 4 + 1024) == GPK_OK) continue;
+                if (gpk_session_reserve_pairs(s, pairs + pairs / 4 + 1024) == GPK_OK) {
+                    drop_graphs();
+                    continue;
+                }
             }
             return iter_fail(it, stt);
         }

@@ -240,3 +240,21 @@ def test_fit_zero_volume_prunes_to_near_empty(gp):
         img = gp.rasterize_slice(gs, gp.slice_pose_for_index((16, 16, 16), (1, 1, 1), (0, 0, 0), 8),
                                  gp.PsfSpec(), gp.RasterConfig())
         assert np.all(img < 0.02)
+
+
+def test_fit_graph_replay_equals_direct_steps(gp, monkeypatch):
+    """After the densify window gpk_fit replays one CUDA graph per slice; the
+    result is bitwise that of direct launches (GPK_FIT_NO_GRAPHS=1)."""
+    vol = blob_volume((20, 16, 12), (9.0, 8.0, 6.0), (2.5, 2.0, 2.0), 0.8)
+    cfg = gp.FitConfig(iterations=300, init_count=40, densify_start=50, densify_end=100,
+                       densify_interval=50, rng_seed=4, progress_interval=50)
+    runs = []
+    for direct in (False, True):
+        if direct:
+            monkeypatch.setenv("GPK_FIT_NO_GRAPHS", "1")
+        rows = []
+        gs = gp.fit(vol, (1, 1, 1), (0, 0, 0), gp.PsfSpec(), cfg,
+                    lambda p: rows.append((p.iteration, p.loss, p.count, p.psnr2d, p.monitor_loss)))
+        runs.append((gs.records, rows))
+    assert runs[0][1] == runs[1][1]
+    assert np.array_equal(runs[0][0], runs[1][0])

@@ -182,6 +182,7 @@ int gpk_fit(gpk_session* s, const float* volume, const int32_t dims[3], const do
     // CUDA graph captured once (GPK_FIT_NO_GRAPHS=1: direct launches).
     const bool graphs = std::getenv("GPK_FIT_NO_GRAPHS") == nullptr;
     std::vector<int32_t> graph_of(Z, -1);
+    std::vector<int> visits(Z, 0);
     auto drop_graphs = [&] {
         gpk_graph_destroy_all(s);
         std::fill(graph_of.begin(), graph_of.end(), -1);
@@ -207,7 +208,10 @@ int gpk_fit(gpk_session* s, const float* volume, const int32_t dims[3], const do
             int stt = load_target(k);
             if (stt != GPK_OK) return iter_fail(it, stt);
             const auto t1 = std::chrono::steady_clock::now();
-            if (graphs && it > cfg->densify_end) {
+            // a slice's graph is captured on its second visit after the window
+            // (a capture costs about ten direct steps' host time)
+            if (graphs && it > cfg->densify_end && (graph_of[k] >= 0 || (attempt == 0 && ++visits[k] >= 2) ||
+                                                    (attempt > 0 && visits[k] >= 2))) {
                 // the set is frozen: replay the step's CUDA graph for this slice
                 // (captured on first use; bitwise the direct step)
                 for (int g = 0; g < 2; ++g) {

@@ -19,8 +19,8 @@ import paper_2603_20611_b200 as gp  # noqa: E402
 
 CASES = {
     # dims, init_count, device iterations, reference iterations
-    "c1": ((128, 128, 32), 20000, 600, 600),
-    "c2": ((512, 512, 128), 1000000, 600, 12),
+    "c1": ((128, 128, 32), 20000, 3000, 600),
+    "c2": ((512, 512, 128), 1000000, 3000, 12),
 }
 
 

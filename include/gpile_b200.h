@@ -352,6 +352,15 @@ int gpk_quantize(gpk_session* s, const gpk_quant_spec* spec, int32_t morton_orde
 int gpk_encode_streams(gpk_session* s, const gpk_quant_spec* spec, uint8_t* positions, uint8_t* opacities,
                        uint8_t* log_scales, uint8_t* quats, double scale_min[3], double scale_max[3]);
 uint64_t gpk_stream_bytes(uint64_t count, int32_t components, int32_t bits);
+/* The decode side before dequantization (detail::unpack_deltas,
+ * container.hpp:158-181, then dequantize, quant.hpp:134-176): the four packed
+ * streams of n primitives -> n x 11 f32 records (records_out, host, if
+ * non-NULL); load != 0 makes the decoded set the session's (gpk_set_gaussians).
+ * An out-of-range delta -> GPK_ERR_CORRUPT_CONTAINER naming the stream. */
+int gpk_decode_streams(gpk_session* s, const gpk_quant_spec* spec, uint64_t n, const gpk_bounds* bbox,
+                       const double scale_min[3], const double scale_max[3], const uint8_t* positions,
+                       const uint8_t* opacities, const uint8_t* log_scales, const uint8_t* quats,
+                       float* records_out, int32_t load);
 
 /* ---- adaptive density control (optimize.hpp:228-344) ------------------------ */
 typedef struct {

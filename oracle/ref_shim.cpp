@@ -782,4 +782,28 @@ int gref_unpack_deltas(const uint8_t* bytes, uint64_t nbytes, uint64_t count, in
     });
 }
 
+
+// dequantize (quant.hpp:134-176) of u32 streams -> n x 11 f64 records
+int gref_dequantize(const gpk_quant_spec* spec, uint64_t n, const gpk_bounds* bbox, const double* smin,
+                    const double* smax, const uint32_t* pos, const uint32_t* opa, const uint32_t* ls,
+                    const uint32_t* quat, double* out) {
+    return guarded([&] {
+        QuantizedSet q;
+        q.spec.pos_bits = spec->pos_bits;
+        q.spec.opacity_bits = spec->opacity_bits;
+        q.spec.scale_bits = spec->scale_bits;
+        q.spec.quat_bits = spec->quat_bits;
+        q.spec.morton_bits = spec->morton_bits;
+        q.bbox = bounds_from(bbox);
+        q.scale_min = {smin[0], smin[1], smin[2]};
+        q.scale_max = {smax[0], smax[1], smax[2]};
+        q.positions.assign(pos, pos + 3 * n);
+        q.opacities.assign(opa, opa + n);
+        q.log_scales.assign(ls, ls + 3 * n);
+        q.quats.assign(quat, quat + 4 * n);
+        const GaussianSet set = dequantize(q);
+        for (std::size_t i = 0; i < set.size(); ++i) prim_to(set.primitives[i], out + 11 * i);
+    });
+}
+
 }  // extern "C"

@@ -217,6 +217,8 @@ _PROTOS = {
     "gpk_quantize": (C.c_int, [_P, C.POINTER(QuantSpecC), C.c_int32, _U32, _U32, _U32, _U32, _D, _D]),
     "gpk_encode_streams": (C.c_int, [_P, C.POINTER(QuantSpecC), _P, _P, _P, _P, _D, _D]),
     "gpk_stream_bytes": (C.c_uint64, [C.c_uint64, C.c_int32, C.c_int32]),
+    "gpk_decode_streams": (C.c_int, [_P, C.POINTER(QuantSpecC), C.c_uint64, C.POINTER(Bounds), _D, _D, _P, _P, _P,
+                                     _P, _F, C.c_int32]),
     "gpk_save_checkpoint": (C.c_int, [_P, C.c_char_p]),
     "gpk_load_checkpoint": (C.c_int, [_P, C.c_char_p]),
     "gpk_checkpoint_bytes": (C.c_uint64, [C.c_uint64]),

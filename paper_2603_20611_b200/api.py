@@ -639,6 +639,24 @@ class Session:
                                        N.dptr(lo), N.dptr(hi)))
         return QuantizedStreams(*bufs, tuple(lo), tuple(hi))
 
+    def decode_streams(self, enc: QuantizedStreams, n: int, bbox, spec: QuantSpec | None = None,
+                       load: bool = True) -> np.ndarray:
+        """unpack_deltas + dequantize of encode_streams' output -> (n, 11) f32 records
+        (and, with load, the session's set)."""
+        spec = spec or QuantSpec()
+        out = np.zeros((n, RECORD), np.float32)
+        b = N.Bounds((C.c_double * 3)(*bbox[0]), (C.c_double * 3)(*bbox[1]))
+        lo = np.ascontiguousarray(enc.scale_min, np.float64)
+        hi = np.ascontiguousarray(enc.scale_max, np.float64)
+        bufs = [np.ascontiguousarray(x, np.uint8) for x in (enc.positions, enc.opacities, enc.log_scales, enc.quats)]
+        c = spec.to_c()
+        st = N.lib.gpk_decode_streams(self._h, C.byref(c), int(n), C.byref(b), N.dptr(lo), N.dptr(hi),
+                                      *[x.ctypes.data_as(C.c_void_p) for x in bufs], N.fptr(out), 1 if load else 0)
+        check(st)
+        if load:
+            self._refresh_n()
+        return out
+
     # ---- checkpoints (checkpoint.hpp:38-92) ----
     def bounds(self) -> tuple:
         b = N.Bounds()

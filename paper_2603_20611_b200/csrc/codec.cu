@@ -254,6 +254,80 @@ __global__ void k_pack_deltas(const uint32_t* __restrict__ v, uint64_t total, in
     for (int b = 0; b < width; ++b) out[i * width + b] = (uint8_t)((zz >> (8 * b)) & 0xffu);
 }
 
+// ---- decode direction: detail::unpack_deltas (container.hpp:158-181) + dequantize (quant.hpp:134-176)
+struct UnpackStream {
+    const uint8_t* bytes;
+    uint32_t* values;
+    uint64_t count;   // primitives
+    int comps, bits;
+};
+
+// zig-zag bytes -> signed deltas (as u32, wrapping); flags an out-of-range delta
+__global__ void k_unzigzag(const UnpackStream u, unsigned* bad) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= u.count * (uint64_t)u.comps) return;
+    const int width = (u.bits + 7) / 8;
+    unsigned long long zz = 0;
+    for (int b = 0; b < width; ++b) zz |= (unsigned long long)u.bytes[i * width + b] << (8 * b);
+    if (zz >= (1ull << u.bits)) atomicOr(bad, 1u);
+    const long long sv = (long long)((zz >> 1) ^ (~(zz & 1) + 1));
+    u.values[i] = (uint32_t)(unsigned long long)sv;
+}
+
+// per-component running sum mod 2^bits: CTA c scans component c (chunk per
+// thread, then a block scan of the chunk sums; u32 wrap-around is exact mod 2^bits)
+__global__ void __launch_bounds__(1024) k_delta_scan(const UnpackStream u) {
+    __shared__ uint32_t part[1024];
+    const int c = blockIdx.x;
+    const uint64_t n = u.count, chunk = (n + 1023) / 1024;
+    const uint64_t lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
+    uint32_t sum = 0;
+    for (uint64_t k = lo; k < hi; ++k) sum += u.values[k * u.comps + c];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const uint32_t v = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = part[threadIdx.x] - sum;
+    const uint32_t mask = (uint32_t)((1ull << u.bits) - 1);
+    for (uint64_t k = lo; k < hi; ++k) {
+        run += u.values[k * u.comps + c];
+        u.values[k * u.comps + c] = run & mask;
+    }
+}
+
+struct DequantArgs {
+    const uint32_t *pos, *opa, *ls, *quat;
+    uint64_t n;
+    gpk_bounds bb;
+    double smin[3], smax[3];
+    gpk_quant_spec spec;
+    float* rec;  // n x 11 records
+};
+
+__device__ __forceinline__ double dequant_value(uint32_t q, int bits) { return (double)q / (double)((1u << bits) - 1); }
+
+__global__ void k_dequantize(const DequantArgs a) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    float* r = a.rec + 11 * i;
+    for (int d = 0; d < 3; ++d) {
+        const double ext = a.bb.max[d] - a.bb.min[d];
+        r[d] = (float)(a.bb.min[d] + dequant_value(a.pos[3 * i + d], a.spec.pos_bits) * ext);
+        r[3 + d] = (float)(a.smin[d] + dequant_value(a.ls[3 * i + d], a.spec.scale_bits) * (a.smax[d] - a.smin[d]));
+    }
+    double al = dequant_value(a.opa[i], a.spec.opacity_bits);  // alpha_activation_inverse (core.hpp:23-27)
+    al = fmin(1.0 - 1e-12, fmax(1e-12, al));
+    r[10] = (float)log(al / (1.0 - al));
+    double q[4];
+    for (int k = 0; k < 4; ++k) q[k] = dequant_value(a.quat[4 * i + k], a.spec.quat_bits) * 2.0 - 1.0;
+    const bool nz = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) > 0.0;
+    for (int k = 0; k < 4; ++k) r[6 + k] = nz ? (float)q[k] : (k == 0 ? 1.0f : 0.0f);
+}
+
 struct Dev {
     void* p = nullptr;
     ~Dev() {
@@ -474,6 +548,81 @@ int gpk_encode_streams(gpk_session* s, const gpk_quant_spec* spec, uint8_t* posi
         off += b;
     }
     CCK(cudaStreamSynchronize(r.st));
+    return GPK_OK;
+}
+
+// unpack_deltas of the four streams + dequantize (the decode side of
+// container.hpp:232-260 after LZMA): records out (n x 11 f32, host), and the
+// decoded set loaded into the session when load != 0.
+int gpk_decode_streams(gpk_session* s, const gpk_quant_spec* spec, uint64_t n, const gpk_bounds* bbox,
+                       const double scale_min[3], const double scale_max[3], const uint8_t* positions,
+                       const uint8_t* opacities, const uint8_t* log_scales, const uint8_t* quats,
+                       float* records_out, int32_t load) {
+    if (!s || !spec || !bbox || !scale_min || !scale_max) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (n && (!positions || !opacities || !log_scales || !quats)) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    CTRY(validate_spec(spec));
+    void* stv = nullptr;
+    CTRY(gpk_session_get_stream(s, &stv));
+    CTRY(gpk_session_synchronize(s));  // selects the session's device
+    cudaStream_t st = static_cast<cudaStream_t>(stv);
+    const int comps[4] = {3, 1, 3, 4};
+    const int bits[4] = {spec->pos_bits, spec->opacity_bits, spec->scale_bits, spec->quat_bits};
+    const uint8_t* host[4] = {positions, opacities, log_scales, quats};
+    const char* names[4] = {"positions", "opacities", "log_scales", "quats"};
+    Dev raw, vals, rec, bad;
+    uint64_t rb = 0;
+    for (int k = 0; k < 4; ++k) rb += gpk_stream_bytes(n, comps[k], bits[k]);
+    CCK(raw.alloc(rb));
+    CCK(vals.alloc(n * 11 * 4));
+    CCK(rec.alloc(n * 44));
+    CCK(bad.alloc(16));
+    CCK(cudaMemsetAsync(bad.p, 0, 16, st));
+    uint64_t off = 0, voff = 0;
+    uint32_t* vp[4];
+    for (int k = 0; k < 4; ++k) {
+        const uint64_t b = gpk_stream_bytes(n, comps[k], bits[k]);
+        uint8_t* dst = static_cast<uint8_t*>(raw.p) + off;
+        if (b) CCK(cudaMemcpyAsync(dst, host[k], b, cudaMemcpyHostToDevice, st));
+        UnpackStream u{dst, static_cast<uint32_t*>(vals.p) + voff, n, comps[k], bits[k]};
+        vp[k] = u.values;
+        if (n) {
+            k_unzigzag<<<grid(n * comps[k]), kThreads, 0, st>>>(u, static_cast<unsigned*>(bad.p) + k);
+            k_delta_scan<<<comps[k], 1024, 0, st>>>(u);
+        }
+        CCK(cudaGetLastError());
+        off += b;
+        voff += n * comps[k];
+    }
+    unsigned flags[4];
+    CCK(cudaMemcpyAsync(flags, bad.p, 16, cudaMemcpyDeviceToHost, st));
+    CCK(cudaStreamSynchronize(st));
+    for (int k = 0; k < 4; ++k)
+        if (flags[k])
+            return fail(GPK_ERR_CORRUPT_CONTAINER, std::string("container: out-of-range delta in ") + names[k]);
+    DequantArgs a;
+    a.pos = vp[0];
+    a.opa = vp[1];
+    a.ls = vp[2];
+    a.quat = vp[3];
+    a.n = n;
+    a.bb = *bbox;
+    for (int d = 0; d < 3; ++d) {
+        a.smin[d] = scale_min[d];
+        a.smax[d] = scale_max[d];
+    }
+    a.spec = *spec;
+    a.rec = static_cast<float*>(rec.p);
+    if (n) k_dequantize<<<grid(n), kThreads, 0, st>>>(a);
+    CCK(cudaGetLastError());
+    std::vector<float> tmp;
+    float* out = records_out;
+    if (!out && load) {
+        tmp.resize(n * 11);
+        out = tmp.data();
+    }
+    if (out && n) CCK(cudaMemcpyAsync(out, rec.p, n * 44, cudaMemcpyDeviceToHost, st));
+    CCK(cudaStreamSynchronize(st));
+    if (load) CTRY(gpk_set_gaussians(s, n, out, bbox));
     return GPK_OK;
 }
 

@@ -112,3 +112,45 @@ def test_quantize_errors_match_reference(gp, ref, session):
         assert st == 1 and str(e.value) == msg
     with pytest.raises(gp.InvalidArgument):
         session.quantize(gp.QuantSpec(pos_bits=22))
+
+
+def test_decode_streams_matches_reference(gp, ref, session):
+    """encode_streams -> decode_streams on the device vs the reference's
+    unpack_deltas + dequantize of the same bytes (container.hpp:158-181,
+    quant.hpp:134-176): the records equal the reference's rounded to fp32
+    (log / division in fp64 on both sides: within one fp32 ulp)."""
+    import paper_2603_20611_b200._native as N
+
+    gs = _set(gp, 30000, 9)
+    spec = gp.QuantSpec()
+    session.set_gaussians(gs)
+    enc = session.encode_streams(spec)
+    n = gs.size()
+    bbox = (gs.bbox_min, gs.bbox_max)
+    with gp.Session(0) as s2:
+        got = s2.decode_streams(enc, n, bbox, spec, load=True)
+        assert s2.n == n
+        assert np.array_equal(s2.get_gaussians(), got)
+    vals = []
+    ref.lib.gref_unpack_deltas.argtypes = [C.POINTER(C.c_uint8), C.c_uint64, C.c_uint64, C.c_int, C.c_int, U32]
+    for b, comps, bits in ((enc.positions, 3, 14), (enc.opacities, 1, 12), (enc.log_scales, 3, 12), (enc.quats, 4, 12)):
+        v = np.zeros(n * comps, np.uint32)
+        assert ref.lib.gref_unpack_deltas(b.ctypes.data_as(C.POINTER(C.c_uint8)), b.size, n, comps, bits, _u32(v)) == 0
+        vals.append(v)
+    want = np.zeros((n, 11))
+    b = N.Bounds((C.c_double * 3)(*bbox[0]), (C.c_double * 3)(*bbox[1]))
+    lo, hi = np.array(enc.scale_min), np.array(enc.scale_max)
+    c = spec.to_c()
+    ref.lib.gref_dequantize.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_double),
+                                        C.POINTER(C.c_double), U32, U32, U32, U32, C.POINTER(C.c_double)]
+    assert ref.lib.gref_dequantize(C.byref(c), n, C.byref(b), N.dptr(lo), N.dptr(hi), *[_u32(v) for v in vals],
+                                   N.dptr(want)) == 0
+    w32 = want.astype(np.float32)
+    ulp = np.abs(np.spacing(w32))
+    assert np.all(np.abs(got - w32) <= ulp), np.abs(got - w32).max()
+    # a corrupted delta (zig-zag value >= 2^bits) is refused like the reference
+    bad = gp.QuantizedStreams(enc.positions.copy(), enc.opacities.copy(), enc.log_scales, enc.quats,
+                              enc.scale_min, enc.scale_max)
+    bad.opacities[1::2][5] = 0xFF  # high byte of a 12-bit delta
+    with gp.Session(0) as s3, pytest.raises(gp.CorruptContainer):
+        s3.decode_streams(bad, n, bbox, spec)

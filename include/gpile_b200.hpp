@@ -19,6 +19,8 @@
 //   fit                   optimize.hpp:360      fit
 //   save_checkpoint       checkpoint.hpp:38     save_checkpoint
 //   load_checkpoint       checkpoint.hpp:60     load_checkpoint
+//   morton_sort           morton.hpp:33         morton_sort
+//   quantize              quant.hpp:67          quantize
 //
 // Errors: GPK_ERR_INVALID_ARGUMENT -> std::invalid_argument,
 // GPK_ERR_DEGENERATE_COVARIANCE -> gpile::DegenerateCovariance,
@@ -44,7 +46,9 @@
 #include <gpile/errors.hpp>
 #include <gpile/image.hpp>
 #include <gpile/loss.hpp>
+#include <gpile/morton.hpp>
 #include <gpile/optimize.hpp>
+#include <gpile/quant.hpp>
 #include <gpile/render.hpp>
 #include <gpile/voxelize.hpp>
 
@@ -599,6 +603,36 @@ inline GaussianSet fit(const VolumeGrid& volume, const PsfSpec& psf, const FitCo
     set.bbox = volume.world_bounds();
     detail::fetch_set(s.handle(), set);
     return set;
+}
+
+// ---- morton.hpp / quant.hpp (the codec's front half) -------------------------------
+inline std::vector<std::size_t> morton_sort(const GaussianSet& set, int bits = 14) {
+    Session& s = default_session();
+    s.set_gaussians(set);
+    std::vector<uint64_t> p(set.size());
+    check(gpk_morton_sort(s.handle(), bits, p.data()));
+    return std::vector<std::size_t>(p.begin(), p.end());
+}
+
+inline QuantizedSet quantize(const GaussianSet& set, const QuantSpec& spec) {
+    spec.validate();
+    Session& s = default_session();
+    s.set_gaussians(set);
+    const gpk_quant_spec c{spec.pos_bits, spec.opacity_bits, spec.scale_bits, spec.quat_bits, spec.morton_bits};
+    QuantizedSet q;
+    q.spec = spec;
+    q.bbox = set.bbox;
+    const std::size_t n = set.size();
+    q.positions.resize(3 * n);
+    q.opacities.resize(n);
+    q.log_scales.resize(3 * n);
+    q.quats.resize(4 * n);
+    double lo[3], hi[3];
+    check(gpk_quantize(s.handle(), &c, 0, q.positions.data(), q.opacities.data(), q.log_scales.data(),
+                       q.quats.data(), lo, hi));
+    q.scale_min = {lo[0], lo[1], lo[2]};
+    q.scale_max = {hi[0], hi[1], hi[2]};
+    return q;
 }
 
 // ---- checkpoint.hpp ----------------------------------------------------------------

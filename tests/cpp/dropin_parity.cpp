@@ -297,6 +297,18 @@ int main() {
         std::remove(b.c_str());
     }
 
+    // codec front half (morton.hpp:33-48, quant.hpp:67-132)
+    {
+        const auto p_ref = morton_sort(set, 14), p_gpu = b200::morton_sort(set, 14);
+        expect(p_ref == p_gpu, "morton_sort: identical stable permutation");
+        QuantSpec qs;
+        const QuantizedSet q_ref = quantize(set, qs), q_gpu = b200::quantize(set, qs);
+        expect(q_ref.positions == q_gpu.positions && q_ref.opacities == q_gpu.opacities &&
+                   q_ref.log_scales == q_gpu.log_scales && q_ref.quats == q_gpu.quats &&
+                   q_ref.scale_min.x == q_gpu.scale_min.x && q_ref.scale_max.z == q_gpu.scale_max.z,
+               "quantize: identical integer streams and scale ranges");
+    }
+
     std::printf("%s\n", failures ? "DROPIN PARITY FAILED" : "DROPIN PARITY OK");
     return failures ? 1 : 0;
 }

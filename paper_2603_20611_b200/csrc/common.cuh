@@ -329,6 +329,59 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+// One tile's list from the K_decide buckets (render.hpp:142-160 order): the
+// buckets of tile d — one per K_decide group, each already in ascending slot
+// order (K_decide fills them stably) — concatenated in group order into
+// vals_out[out ...). The whole CTA (kThreads) copies cooperatively: per chunk
+// of kThreads groups, an exclusive scan of the bucket sizes, then every
+// thread takes list positions and finds its bucket by binary search — work
+// linear in the list length and independent of how the pairs are spread over
+// groups (a clustered set can put hundreds of one group's survivors into one
+// tile). Returns the end of the list. Ends with a barrier.
+template <int kThreads>
+__device__ __forceinline__ unsigned gather_tile_list(const unsigned* __restrict__ bucket_tab, unsigned ngroups,
+                                                     unsigned row_stride, unsigned d, unsigned out, unsigned P,
+                                                     const uint32_t* vals_in, uint32_t* vals_out,
+                                                     unsigned* s_ex /* kThreads + 1 */, unsigned* s_b /* kThreads */,
+                                                     unsigned* s_wsum /* kThreads / 32 */) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (unsigned g0 = 0; g0 < ngroups; g0 += kThreads) {
+        const unsigned g = g0 + tid;
+        unsigned b = 0, e = 0;
+        if (g < ngroups) {  // group g's bucket for tile d: [row[d], row[d + 1])
+            const unsigned* row = bucket_tab + (uint64_t)g * row_stride;
+            b = min(__ldcg(&row[d]), P);
+            e = min(__ldcg(&row[d + 1]), P);
+        }
+        const unsigned cnt = e > b ? e - b : 0u;
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        unsigned ex = incl - cnt;
+        for (int w = 0; w < warp; ++w) ex += s_wsum[w];
+        s_ex[tid] = ex;
+        s_b[tid] = b;
+        if (tid == kThreads - 1) s_ex[kThreads] = ex + cnt;
+        __syncthreads();
+        const unsigned total = s_ex[kThreads];
+        for (unsigned t = tid; t < total; t += kThreads) {
+            unsigned q = 0;  // last bucket starting at or before t (empty buckets share starts)
+#pragma unroll
+            for (unsigned step = kThreads / 2; step > 0; step >>= 1)
+                if (s_ex[q + step] <= t) q += step;
+            vals_out[out + t] = __ldcg(&vals_in[s_b[q] + (t - s_ex[q])]);
+        }
+        out += total;
+        __syncthreads();  // s_ex / s_b / s_wsum are rewritten by the next chunk
+    }
+    return out;
+}
+
 // Kernel-launch wrappers (defined in the .cu files, called by session.cu).
 struct PrepLaunch {
     const float* params;      // 11 planes x cap

@@ -716,11 +716,49 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
             if (tid == 0) trow[nb] = P0 + Pb;
         }
         __syncthreads();
-        for (unsigned k = tid; k < Pb; k += kDecideThreads) {
-            unsigned j;
-            const unsigned tile = pair_tile(k, j);
-            const unsigned long long pos = (unsigned long long)P0 + s_start[tile] + atomicAdd(&s_hist[0][tile], 1u);
-            if (pos < a.pair_cap) a.vals[pos] = base + j;
+        // stable fill: each bucket receives its pairs in pair order (= ascending
+        // slot, one pair per survivor and tile), so the gather is a plain
+        // concatenation. Rounds of 1024 pairs; warp w ranks its 128 with
+        // __match_any_sync against its own per-tile counters, then a per-tile
+        // prefix over the warps (on top of the running bucket fill) places them.
+        uint16_t(*s_w16)[kMaxBuckets] = reinterpret_cast<uint16_t(*)[kMaxBuckets]>(s_dyn_u + kDecideGroup + kDecideGroup * 3 / 2);
+        constexpr int kSub = 4;  // 32-pair rounds per warp per round
+        for (unsigned r0 = 0; r0 < Pb; r0 += kDecideThreads * kSub) {
+            for (unsigned w = tid; w < 8u * (nb / 2); w += kDecideThreads)
+                reinterpret_cast<unsigned*>(&s_w16[0][0])[(w / (nb / 2)) * (kMaxBuckets / 2) + w % (nb / 2)] = 0u;
+            __syncthreads();
+            unsigned tl[kSub], jj[kSub], rk[kSub];
+#pragma unroll
+            for (int q = 0; q < kSub; ++q) {
+                const unsigned k = r0 + (unsigned)(warp * kSub + q) * 32 + lane;
+                const bool valid = k < Pb;
+                tl[q] = valid ? pair_tile(k, jj[q]) : 0xffffffffu;
+                const unsigned peers = __match_any_sync(0xffffffffu, tl[q]);
+                const unsigned prior = valid ? s_w16[warp][tl[q]] : 0u;
+                __syncwarp();
+                if (valid && (__ffs(peers) - 1) == lane) s_w16[warp][tl[q]] = (uint16_t)(prior + __popc(peers));
+                __syncwarp();
+                rk[q] = prior + __popc(peers & lanemask_lt());
+            }
+            __syncthreads();
+            for (unsigned d = tid; d < nb; d += kDecideThreads) {
+                unsigned run = s_hist[0][d];
+#pragma unroll
+                for (int w = 0; w < 8; ++w) {
+                    const unsigned c = s_w16[w][d];
+                    s_w16[w][d] = (uint16_t)run;  // bucket fill <= survivors of the group <= 4096
+                    run += c;
+                }
+                s_hist[0][d] = run;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < kSub; ++q)
+                if (tl[q] != 0xffffffffu) {
+                    const unsigned long long pos = (unsigned long long)P0 + s_start[tl[q]] + s_w16[warp][tl[q]] + rk[q];
+                    if (pos < a.pair_cap) a.vals[pos] = base + jj[q];
+                }
+            __syncthreads();  // the next round clears the warp tables
         }
         // the last group to finish turns the per-tile counts into list starts
         // (one scan, instead of every gather CTA re-reading the same counts)
@@ -1145,7 +1183,7 @@ void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& f, cudaStream_t st)
 
 void launch_bin(const PrepLaunch& a, cudaStream_t st) {
     if (!a.n) return;
-    const int smem = kDecideGroup * (4 + 6);
+    const int smem = kDecideGroup * (4 + 6) + 8 * kMaxBuckets * 2;  // + the stable fill's warp tables
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -103,50 +103,13 @@ __device__ __forceinline__ void tile_range(const RasterLaunch& a, int tile, unsi
     }
 }
 
-// k_gather's work for one tile (sort.cu): concatenate the K_decide groups'
-// buckets for the tile in group (= ascending slot) order into its list at
-// tile_begin[d]; tiny buckets are ordered by rank. Whole CTA of 256; the list
-// is visible to the CTA after the caller's barrier.
+// k_gather's work for one tile (sort.cu): the tile's list from the K_decide
+// buckets (common.cuh gather_tile_list). The list is visible to the CTA after
+// the helper's closing barrier.
 __device__ __forceinline__ void gather_tile(const RasterLaunch& a, unsigned d) {
-    __shared__ unsigned s_wsum[8];
-    __shared__ unsigned s_chunk_total;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
-    unsigned out = __ldcg(&a.grp_begin[d]);
-    for (unsigned g0 = 0; g0 < a.ngroups; g0 += 256) {
-        const unsigned g = g0 + tid;
-        unsigned b = 0, e = 0;
-        if (g < a.ngroups) {  // group g's bucket for tile d: [row[d], row[d + 1])
-            const unsigned* row = a.bucket_tab + (uint64_t)g * a.row_stride;
-            b = min(__ldcg(&row[d]), P);
-            e = min(__ldcg(&row[d + 1]), P);
-        }
-        const unsigned cnt = e > b ? e - b : 0u;
-        unsigned incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
-        }
-        __syncthreads();  // s_wsum of the previous chunk consumed
-        if (lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        unsigned pos = out + incl - cnt;
-        for (int w = 0; w < warp; ++w) pos += s_wsum[w];
-        if (tid == 255) s_chunk_total = pos + cnt - out;
-        if (cnt == 1) {
-            a.vals_out[pos] = __ldcg(&a.vals_in[b]);
-        } else if (cnt > 1) {
-            for (unsigned i = 0; i < cnt; ++i) {  // rank within the bucket (slots are unique)
-                const uint32_t v = __ldcg(&a.vals_in[b + i]);
-                unsigned r = 0;
-                for (unsigned j = 0; j < cnt; ++j) r += __ldcg(&a.vals_in[b + j]) < v;
-                a.vals_out[pos + r] = v;
-            }
-        }
-        __syncthreads();
-        out += s_chunk_total;
-    }
+    __shared__ unsigned s_ex[257], s_b[256], s_wsum[8];
+    gather_tile_list<256>(a.bucket_tab, a.ngroups, a.row_stride, d, __ldcg(&a.grp_begin[d]),
+                          stored_pairs(a.ctrl, a.pair_cap), a.vals_in, a.vals_out, s_ex, s_b, s_wsum);
 }
 
 __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {

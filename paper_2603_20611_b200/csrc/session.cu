@@ -347,6 +347,29 @@ int mark_grads_dense(gpk_session* s) {
     return GPK_OK;
 }
 
+uint64_t decide_group_count(uint64_t n);
+
+// Per-sort-tile digit counts of every radix pass (kept zero between prepares:
+// K_filter clears the rows the previous prepare used). A pass has one row per
+// sort tile: kSortTile consecutive pair positions, or — the first pass over
+// K_decide's output — one per K_decide group; the super-tile rows follow at
+// row sort_tiles_cap. Sized for both, so neither the pair capacity nor the set
+// size can push the group rows into the super rows.
+int size_sort_status(gpk_session* s) {
+    const uint64_t st_tiles = std::max<uint64_t>((s->pair_cap + kSortTile - 1) / kSortTile,
+                                                 decide_group_count(std::max<uint64_t>(s->cap, 1)));
+    if (st_tiles <= s->sort_tiles_cap && s->sort_status.p) return GPK_OK;
+    const uint64_t super_tiles = (st_tiles + kSuperTiles - 1) / kSuperTiles;
+    const uint64_t region = (st_tiles + super_tiles) * kMaxBuckets;
+    CK(s->sort_status.ensure((size_t)kMaxSortPasses * region * 4));
+    CK(cudaMemsetAsync(s->sort_status.p, 0, s->sort_status.bytes, s->stream));
+    CK(cudaMemsetAsync(s->prev_sort_words(), 0, 12, s->stream));
+    s->sort_tiles_cap = st_tiles;
+    s->hist_region = region;
+    ++s->alloc_epoch;
+    return GPK_OK;
+}
+
 int ensure_pairs(gpk_session* s, uint64_t need) {
     if (need <= s->pair_cap && s->keys[0].p) return GPK_OK;
     const uint64_t cap = std::max<uint64_t>(need, 1ull << 16);
@@ -356,18 +379,8 @@ int ensure_pairs(gpk_session* s, uint64_t need) {
     }
     CK(s->partials.ensure(cap * 24));
     ++s->alloc_epoch;
-    // per-sort-tile digit counts of every pass (kept zero between prepares:
-    // K_filter clears the rows the previous prepare used)
-    const uint64_t st_tiles = (cap + kSortTile - 1) / kSortTile;
-    const uint64_t super_tiles = (st_tiles + kSuperTiles - 1) / kSuperTiles;
-    const uint64_t region = (st_tiles + super_tiles) * kMaxBuckets;
-    CK(s->sort_status.ensure((size_t)kMaxSortPasses * region * 4));
-    CK(cudaMemsetAsync(s->sort_status.p, 0, s->sort_status.bytes, s->stream));
-    CK(cudaMemsetAsync(s->prev_sort_words(), 0, 12, s->stream));
     s->pair_cap = cap;
-    s->sort_tiles_cap = st_tiles;
-    s->hist_region = region;
-    return GPK_OK;
+    return size_sort_status(s);
 }
 
 int ensure_image(gpk_session* s, int w, int h) {
@@ -849,6 +862,7 @@ int alloc_for_n(gpk_session* s, uint64_t n) {
         CK(s->head.ensure(head_size(cap)));
         s->cap = cap;
         ++s->alloc_epoch;
+        if (s->keys[0].p) TRY(size_sort_status(s));  // more K_decide groups than sort-tile rows
     }
     if (n != s->n) ++s->alloc_epoch;  // captured graphs bake the set size
     s->n = n;
@@ -1635,11 +1649,13 @@ int gpk_photometric_loss(gpk_session* s, const float* target, double lambda, dou
         return fail(GPK_ERR_INVALID_ARGUMENT, "photometric_loss: lambda must be >= 0");
     TRY(set_device(s));
     const size_t px = (size_t)s->img_w * s->img_h;
+    // host results: the render must be complete first (a slice whose tile pairs
+    // overflowed is re-prepared and re-rendered before the loss reads it)
+    if ((loss_out || dl_di_out) && s->prep.valid && s->prep.rasterized) TRY(settle_pairs(s));
     TRY(target_wait(s));
     if (target) CK(cudaMemcpyAsync(s->target.p, target, px * 4, cudaMemcpyHostToDevice, s->stream));
     TRY(run_loss(s, lambda, dssim_scale));
     if (loss_out || dl_di_out) {
-        TRY(settle_pairs(s));
         TRY(sync_and_check(s, "photometric_loss"));
         if (loss_out) CK(cudaMemcpy(loss_out, s->loss(), 8, cudaMemcpyDeviceToHost));
         if (dl_di_out) CK(cudaMemcpy(dl_di_out, s->dl_di.p, px * 4, cudaMemcpyDeviceToHost));

@@ -229,54 +229,16 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
 // ---- k_gather --------------------------------------------------------------------
 // Single-pass slices (every tile is one digit): instead of a radix pass, one
 // CTA per tile concatenates the tile's buckets — one per K_decide group, in
-// group order, which is ascending slot order — into the tile's final list.
-// A bucket holds the group's survivors overlapping the tile (almost always 0-3
-// entries) in arbitrary order; each thread orders its bucket by rank (slots are
-// unique), so the list comes out in ascending slot order, like the reference's.
+// group order, each filled in ascending slot order by K_decide — into the
+// tile's final list: ascending slot order, like the reference's lists.
 constexpr int kGatherThreads = 256;
 
 __global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    __shared__ unsigned s_wsum[kGatherThreads / 32];
-    __shared__ unsigned s_chunk_total;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ unsigned s_ex[kGatherThreads + 1], s_b[kGatherThreads], s_wsum[kGatherThreads / 32];
     const unsigned d = blockIdx.x;
-    const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
-    unsigned out = __ldcg(&a.tile_begin[d]);
-    for (unsigned g0 = 0; g0 < a.ngroups; g0 += kGatherThreads) {
-        const unsigned g = g0 + tid;
-        unsigned b = 0, e = 0;
-        if (g < a.ngroups) {  // group g's bucket for tile d: [row[d], row[d + 1])
-            const unsigned* row = a.bucket_tab + (uint64_t)g * a.row_stride;
-            b = min(__ldcg(&row[d]), P);
-            e = min(__ldcg(&row[d + 1]), P);
-        }
-        const unsigned cnt = e > b ? e - b : 0u;
-        unsigned incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
-        }
-        __syncthreads();  // s_wsum of the previous chunk consumed
-        if (lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        unsigned pos = out + incl - cnt;
-        for (int w = 0; w < warp; ++w) pos += s_wsum[w];
-        if (tid == kGatherThreads - 1) s_chunk_total = pos + cnt - out;
-        if (cnt == 1) {
-            a.vals_out[pos] = a.vals_in[b];
-        } else if (cnt > 1) {
-            for (unsigned i = 0; i < cnt; ++i) {  // rank within the bucket (slots are unique)
-                const uint32_t v = a.vals_in[b + i];
-                unsigned r = 0;
-                for (unsigned j = 0; j < cnt; ++j) r += a.vals_in[b + j] < v;
-                a.vals_out[pos + r] = v;
-            }
-        }
-        __syncthreads();
-        out += s_chunk_total;
-    }
+    gather_tile_list<kGatherThreads>(a.bucket_tab, a.ngroups, a.row_stride, d, __ldcg(&a.tile_begin[d]),
+                                     stored_pairs(a.ctrl, a.pair_cap), a.vals_in, a.vals_out, s_ex, s_b, s_wsum);
 }
 
 }  // namespace

@@ -1,0 +1,229 @@
+"""GPU parity at every BASELINE.json configuration, against the reference
+itself (oracle/_ref), through the C-ABI.
+
+  C2  512^2 x 128, 1M Gaussians   — the bench unit: one full U2 training step
+                                    (gpk_train_step, the graph path bench.py
+                                    times) against the reference's fit-loop
+                                    sequence (optimize.hpp:385-402).
+  C3  256^2 x 320, 500k, sigma_z 3 — thick-slice PSF, one mid slice, U1 pieces.
+  C4  1M Gaussians -> 512^3        — voxelize: VoxelTiles bit-exact
+                                    (voxelize.hpp:86-105), voxels to tolerance.
+  C5  2048^2 x 256, 8M             — one mid-stack slice: 16,384 tiles, so the
+                                    two-pass radix binning (k_sort_pass) is the
+                                    path under test (render.hpp:142-160), and
+                                    fp32 pixel coordinates would fail 1e-4
+                                    (core.hpp:86-89).
+plus cheap >1024-tile cases for the multi-pass path, including a session whose
+pair reservation is far below the set size (the digit-count rows of the
+K_decide groups must not overrun the sort's super-tile rows).
+
+Tolerances: tests/tolerances.py (north star: images 1e-4 relative, gradients
+1e-3 relative; integer outputs bit-exact).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import f32
+from tolerances import grads_ok, image_ok
+
+pytestmark = pytest.mark.gpu
+
+
+def stack_set(gp, n, dims, seed=1):
+    """init_random over the volume's world bounds (optimize.hpp:94-108, 367-368)."""
+    lo = (-0.5, -0.5, -0.5)
+    hi = (dims[0] - 0.5, dims[1] - 0.5, dims[2] - 0.5)
+    gs = gp.init_random(n, lo, hi, 1.5, seed)
+    return gp.GaussianSet(f32(gs.records), lo, hi)
+
+
+def slice_parity(gp, session, ref, gs, pose, psf, cfg, dl):
+    """Survivors, bounds, tile lists bit-exact; image and gradients to tolerance."""
+    bbox = (gs.bbox_min, gs.bbox_max)
+    session.set_gaussians(gs)
+    session.prepare(pose, psf, cfg)
+    img = session.rasterize()
+    grads, stats = session.backward(dl, stats=True)
+    prep = session.prepared()
+    off, ent = session.tile_lists()
+    idx, bnd, _ = ref.prepare(gs.records, pose, psf, cfg, bbox)
+    assert np.array_equal(prep.index, idx), "survivor set (render.hpp:107,127)"
+    assert np.array_equal(prep.bounds, bnd), "pixel bounds (render.hpp:116-127)"
+    roff, rent = ref.tile_lists(gs.records, pose, psf, cfg, bbox)
+    assert np.array_equal(off, roff), "tile list offsets (render.hpp:142-160)"
+    assert np.array_equal(ent, rent), "tile list entries / order (render.hpp:151-157)"
+    del roff, rent
+    rimg = ref.rasterize(gs.records, pose, psf, cfg, bbox)
+    ok, worst = image_ok(img, rimg)
+    assert ok, f"image beyond tolerance (worst {worst:.3f} x bound)"
+    rg, (_, ro, _) = ref.backward(gs.records, pose, psf, cfg, dl.astype(np.float64), bbox)
+    ok, gworst = grads_ok(grads, rg)
+    assert ok, f"gradients beyond tolerance (worst {gworst:.3f} x bound)"
+    assert np.array_equal(stats.observed, ro), "observed flags (backward.hpp:168-172)"
+    print(f"S={len(idx)} T={len(ent)} image worst {worst:.3g} x bound, grads worst {gworst:.3g} x bound")
+    return len(idx), len(ent)
+
+
+def test_multipass_binning_640(gp, session, ref):
+    """640^2 = 1600 tiles (> 1024): two radix passes over the K_decide output."""
+    dims = (640, 640, 64)
+    gs = stack_set(gp, 50_000, dims, seed=11)
+    pose = gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), 32)
+    dl = (np.random.default_rng(3).uniform(-1, 1, (640, 640)) / 640 ** 2).astype(np.float32)
+    S, T = slice_parity(gp, session, ref, gs, pose, gp.PsfSpec(), gp.RasterConfig(), dl)
+    assert S > 500 and T > S
+
+
+def test_multipass_binning_wide_nonsquare(gp, session, ref):
+    """3000 x 40 (188 x 3 tiles = 564 < 1024) and 1100 x 300 (69 x 19 = 1311 > 1024):
+    ragged edge tiles on both plans."""
+    for w, h, n, seed in ((3000, 40, 30_000, 5), (1100, 300, 40_000, 6)):
+        dims = (w, h, 16)
+        gs = stack_set(gp, n, dims, seed=seed)
+        pose = gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), 8)
+        dl = (np.random.default_rng(seed).uniform(-1, 1, (h, w)) / (w * h)).astype(np.float32)
+        slice_parity(gp, session, ref, gs, pose, gp.PsfSpec(), gp.RasterConfig(), dl)
+
+
+def test_multipass_small_pair_reservation(gp, ref):
+    """A session first sized for a small set (pair capacity 2^16) then given a set
+    with many more K_decide groups than sort tiles (n >> 4 * pair capacity), on a
+    > 1024-tile slice: the buffers must grow and the lists stay bit-exact."""
+    dims = (704, 704, 32)
+    gs = stack_set(gp, 600_000, dims, seed=12)
+    pose = gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), 16)
+    with gp.Session(0) as s:
+        s.reserve_pairs(1)
+        small = stack_set(gp, 1000, (64, 64, 8), seed=1)
+        s.set_gaussians(small)
+        s.prepare(gp.slice_pose_for_index((64, 64, 8), (1, 1, 1), (0, 0, 0), 4), gp.PsfSpec(), gp.RasterConfig())
+        s.rasterize()
+        dl = (np.random.default_rng(4).uniform(-1, 1, (704, 704)) / 704 ** 2).astype(np.float32)
+        slice_parity(gp, s, ref, gs, pose, gp.PsfSpec(), gp.RasterConfig(), dl)
+
+
+def test_c3_full_size_thick_psf(gp, session, ref):
+    """C3: 256^2 x 320, 500k Gaussians, sigma_z = 3 (the ABUS thick-slice case)."""
+    dims = (256, 256, 320)
+    gs = stack_set(gp, 500_000, dims)
+    pose = gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), 160)
+    dl = (np.random.default_rng(9).uniform(-1, 1, (256, 256)) / 256 ** 2).astype(np.float32)
+    S, T = slice_parity(gp, session, ref, gs, pose, gp.PsfSpec(sigma_z=3.0), gp.RasterConfig(), dl)
+    assert 10_000 < S < 40_000
+
+
+def test_c5_mid_slice_2048(gp, session, ref):
+    """C5: one mid-stack 2048^2 slice of the 8M set (seed 1): 16,384 tiles."""
+    dims = (2048, 2048, 256)
+    gs = stack_set(gp, 8_000_000, dims)
+    pose = gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), 128)
+    dl = (np.random.default_rng(5).uniform(-1, 1, (2048, 2048)) / 2048 ** 2).astype(np.float32)
+    S, T = slice_parity(gp, session, ref, gs, pose, gp.PsfSpec(), gp.RasterConfig(), dl)
+    assert 150_000 < S < 260_000
+
+
+def test_c4_voxelize_512(gp, session, ref):
+    """C4: voxelize 1M init_random Gaussians to a 512^3 unit grid, support 3 sigma."""
+    n = 512
+    lo, hi = (-0.5,) * 3, (n - 0.5,) * 3
+    gs = gp.GaussianSet(f32(gp.init_random(1_000_000, lo, hi, 1.5, 1).records), lo, hi)
+    cfg = gp.VoxelizerConfig(dims=(n, n, n))
+    session.set_gaussians(gs)
+    vol = session.voxelize(cfg)
+    off, ent = session.voxel_tile_lists()
+    roff, rent = ref.voxel_tiles(gs.records, cfg)
+    assert np.array_equal(off, roff), "voxel tile offsets (voxelize.hpp:86-105)"
+    assert np.array_equal(ent, rent), "voxel tile entries / order (voxelize.hpp:93-103)"
+    assert len(off) == 64 ** 3 + 1 and len(ent) > 5_000_000
+    del off, ent, roff, rent
+    rvol = ref.voxelize(gs.records, cfg)
+    ok, worst = image_ok(vol, rvol)
+    assert ok, f"volume beyond tolerance (worst {worst:.3f} x bound)"
+    print(f"C4 voxels worst {worst:.3g} x bound")
+
+
+def test_c2_u2_training_step_matches_reference(gp, session, ref):
+    """The bench unit at C2: one gpk_train_step (loss lambda 0.2, scheduled Adam,
+    step 1 of 30000) against prepare_gaussians -> rasterize_prepared ->
+    photometric_loss -> backward_prepared -> adam_step (optimize.hpp:385-402).
+
+    The L1 term's sign(I - T) (loss.hpp:25) flips wherever the fp32 render and
+    the target tie within the image tolerance; the reference's dL/dI is
+    therefore taken with the signs the device saw (every other term is the
+    reference's own). Adam is checked on the device's gradient (the update is
+    ~lr * sign(g) at step 1, so it is checked separately from the gradient)."""
+    from paper_2603_20611_b200 import _native as N
+
+    dims = (512, 512, 128)
+    gs = stack_set(gp, 1_000_000, dims)
+    bbox = (gs.bbox_min, gs.bbox_max)
+    pose = gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), 64)
+    psf, rc = gp.PsfSpec(), gp.RasterConfig()
+    tgt = np.random.default_rng(7).uniform(0, 0.1, (512, 512)).astype(np.float32)
+    lr0 = (6e-4, 0.02, 2e-3, 1e-3)
+    total = 30000
+    session.set_gaussians(gs)
+    session.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
+    session.train_step(pose, psf, rc, 0.2, 0.5, gp.LearningRates(*lr0), total)
+    session.synchronize()
+    img = np.zeros((512, 512), np.float32)
+    session.download(N.GPK_BUF_IMAGE, img.ctypes.data, img.nbytes)
+    loss = np.zeros(1)
+    session.download(N.GPK_BUF_LOSS, loss.ctypes.data, 8)
+    session.synchronize()
+    grads = session.get_gradients()
+    after = session.get_gaussians()
+    m, v, step = session.adam_state()
+    assert step == 1
+
+    rimg = ref.rasterize(gs.records, pose, psf, rc, bbox)
+    ok, worst = image_ok(img, rimg)
+    assert ok, f"image (worst {worst:.3f} x bound)"
+    t64 = tgt.astype(np.float64)
+    rL, rdl = ref.loss(rimg, t64, 0.2, 0.5)
+    assert loss[0] == pytest.approx(rL, rel=1e-5), "photometric loss (loss.hpp:13-37)"
+    flips = np.sign(img.astype(np.float64) - t64) - np.sign(rimg - t64)
+    rdl = rdl + flips / img.size
+    rg, _ = ref.backward(gs.records, pose, psf, rc, rdl, bbox)
+    ok, gworst = grads_ok(grads, rg)
+    assert ok, f"gradients (worst {gworst:.3f} x bound)"
+    lrs = tuple(ref.lib.gref_lr_at(x, 1, total) for x in lr0)
+    zero = np.zeros_like(gs.records)
+    rrec, rm, rv, rstep = ref.adam_step(gs.records, bbox, grads.astype(np.float64), zero, zero, 0, lrs)
+    assert rstep == 1
+
+    def close(a, b, rel=2e-6, abs_=1e-7):
+        a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+        return bool(np.all(np.abs(a - b) <= rel * np.abs(b) + abs_))
+
+    assert close(after, rrec), "parameters after adam_step (optimize.hpp:195-221)"
+    assert close(m, rm) and close(v, rv, abs_=1e-12), "Adam moments"
+    print(f"C2 U2: loss {loss[0]:.9g} vs {rL:.9g}, L1 sign ties {int(np.count_nonzero(flips))}, "
+          f"image worst {worst:.3g}, grads worst {gworst:.3g} x bound")
+
+
+def test_clustered_sets_bitexact_lists(gp, session, ref):
+    """Spatially ordered / clustered sets put many of one K_decide group's
+    survivors into the same tile (the case a per-bucket rank loop degrades on):
+    a Morton-sorted set (what gpk_decode_streams loads) and a dense blob whose
+    tiles hold thousands of Gaussians. Lists bit-exact, image and gradients to
+    tolerance."""
+    dims = (256, 256, 64)
+    gs = stack_set(gp, 200_000, dims, seed=21)
+    session.set_gaussians(gs)
+    perm = session.morton_sort(10)
+    ms = gp.GaussianSet(gs.records[perm], gs.bbox_min, gs.bbox_max)
+    pose = gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), 30)
+    dl = (np.random.default_rng(2).uniform(-1, 1, (256, 256)) / 256 ** 2).astype(np.float32)
+    slice_parity(gp, session, ref, ms, pose, gp.PsfSpec(), gp.RasterConfig(), dl)
+    # blob: 30k Gaussians inside a 48 x 48 x 6 box of a 128^2 slice
+    rng = np.random.default_rng(5)
+    rec = f32(gp.init_random(30_000, (40, 40, 13), (88, 88, 19), 2.0, 9).records)
+    rec[:, 10] = np.log(0.05 / 0.95)  # alpha 0.05: survivors stay above tau
+    blob = gp.GaussianSet(rec, (0, 0, 0), (128, 128, 32))
+    pose = gp.slice_pose_for_index((128, 128, 32), (1, 1, 1), (0, 0, 0), 16)
+    dl = (rng.uniform(-1, 1, (128, 128)) / 128 ** 2).astype(np.float32)
+    S, T = slice_parity(gp, session, ref, blob, pose, gp.PsfSpec(), gp.RasterConfig(), dl)
+    assert T > 20 * 9 * 100  # hundreds of Gaussians per tile

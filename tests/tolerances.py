@@ -5,16 +5,18 @@ Images: per pixel |I - I_ref| <= 1e-4 * |I_ref| + 1e-6 * max|I_ref| (the small
 absolute floor covers pixels that are sums of far tails, whose relative error
 is set by fp32 cancellation-free exponent rounding, not by the algorithm).
 
-Gradients: |g - g_ref| <= 1e-3 * |g_ref| + 1e-3 * max|g_ref[:, slot]| per
+Gradients: |g - g_ref| <= 1e-3 * |g_ref| + 1e-5 * max|g_ref[:, slot]| per
 parameter slot: gradients can be ~0 by symmetry, so a pure
-relative bound is ill-posed.
+relative bound is ill-posed. The absolute floor is 1e-5 of the plane's peak
+(round 1 used 1e-3; the device's fp32 sums reach ~2e-6 of the peak, so the
+floor now bites on the small gradients of the many weakly-covered survivors).
 """
 import numpy as np
 
 IMG_REL = 1e-4
 IMG_ABS_OF_PEAK = 1e-6
 GRAD_REL = 1e-3
-GRAD_ABS_OF_PLANE = 1e-3
+GRAD_ABS_OF_PLANE = 1e-5
 
 
 def image_ok(img, ref):

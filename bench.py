@@ -81,6 +81,12 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
                     help="submit the step kernel by kernel instead of as a CUDA graph")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="slices per step (1..8): B slices rendered concurrently on slice contexts; u2: one "
+                         "Adam on their summed gradient (gpk_train_step_batch), u1: the summed dense gradient")
+    ap.add_argument("--no-batched", action="store_true",
+                    help="skip the extra B = 8 measurement reported beside a B = 1 run")
+    ap.add_argument("--cpu-1thread-seconds", type=float, default=5.0)
     return ap.parse_args()
 
 
@@ -163,6 +169,17 @@ class ClockSampler:
         if self._t:
             self._t.join()
 
+    @staticmethod
+    def peak_mhz(index: int) -> float:
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            return float(pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(index),
+                                                           pynvml.NVML_CLOCK_SM))
+        except Exception:
+            return 1965.0
+
     def result(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
@@ -172,7 +189,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------
-def cpu_reference_rate(cfg, rec, unit, seconds_budget, max_reps=None, warmup=1):
+def cpu_reference_rate(cfg, rec, unit, seconds_budget, max_reps=None, warmup=1, threads=0):
     """The reference's own CPU implementation (oracle/_ref: its headers compiled
     unmodified) of the same unit on this host's cores. Its slice poses come from
     the reference's slice_pose_for_index (core.hpp:202-211); `rec` is the same
@@ -184,7 +201,7 @@ def cpu_reference_rate(cfg, rec, unit, seconds_budget, max_reps=None, warmup=1):
     ref = load("ref")
     L = ref.lib
     cores = os.cpu_count() or 1
-    L.gref_set_threads(0)  # worker_cap() = 0 -> hardware_concurrency (parallel.hpp:14-20)
+    L.gref_set_threads(threads)  # worker_cap() = 0 -> hardware_concurrency (parallel.hpp:14-20)
     workers = L.gref_effective_workers()
     X, Y, Z = cfg["dims"]
     lo, hi = geometry(cfg)
@@ -280,12 +297,19 @@ def make_records(cfg, via_reference=False):
 
 def config_json(args, cfg, world):
     X, Y, Z = cfg["dims"]
-    return {"workload": cfg["name"], "unit_of_work": UNITS[args.unit] + (
-        " (Adam fused with the next slice's cull)" if args.unit == "u2" and getattr(args, "pipeline", True) else ""),
+    B = getattr(args, "batch", 1)
+    unit = UNITS[args.unit] + (
+        " (Adam fused with the next slice's cull)" if args.unit == "u2" and getattr(args, "pipeline", False) else "")
+    if B > 1:
+        unit += (f"; {B} slices per step on slice contexts, " +
+                 ("one Adam on their summed gradient" if args.unit == "u2" else "their gradients summed"))
+    return {"workload": cfg["name"], "unit_of_work": unit,
             "volume": [X, Y, Z], "gaussians": cfg["n"], "sigma_z": cfg["sigma_z"],
-            "slices": f"{len(slice_indices(Z))} mid-stack indices, cycled, one per step",
+            "slices": f"{len(slice_indices(Z))} mid-stack indices, cycled, {B} per step",
+            "slices_per_step": B,
             "parallelism": f"slice-sharded dp{world}",
-            "l2": "flushed (256 MiB read) before each timed step, outside the event window",
+            "l2": "flushed (256 MiB read) before each timed step, outside the event window; "
+                  "steady_state = the same steps back to back without the flush",
             "config_id": args.config}
 
 
@@ -362,20 +386,33 @@ def run_ours(args):
     if world > 1:
         dp.init_grad_comm(sess, rank, world)
 
+    B = args.batch
+    if not 1 <= B <= 8 or 16 % B:
+        raise SystemExit("--batch must be 1, 2, 4 or 8")
+    if B > 1 and world > 1:
+        raise SystemExit("--batch > 1 is single-GPU (the batched step has no collective)")
     tgt = synthetic_target(cfg)
     dl = synthetic_dl_di(cfg)
-    sess.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
-    sess.upload(N.GPK_BUF_DL_DI, dl.ctypes.data, dl.nbytes)
+    batch_ctx = 8 if (B == 1 and world == 1 and not args.no_batched) else B
+    for k in range(batch_ctx):  # slice k of a batched step reads context k's target / dL/dI
+        c = sess.context(k)
+        c.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
+        c.upload(N.GPK_BUF_DL_DI, dl.ctypes.data, dl.nbytes)
     sess.synchronize()
-    # per-slice counters (algorithmic bytes of the prepare kernels)
-    counts = []
+    # per-slice counters (algorithmic bytes of the prepare kernels) and the
+    # reference's pixel-pair evaluation count (render.hpp:179-181: every pixel of
+    # tile x bounds; the tiles partition the image, so sum of bound areas)
+    counts, evals = [], []
     for p in poses:
         sess.prepare(p, psf, rcfg)
         counts.append(sess.prepare_stats())
+        b = sess.prepared().bounds.astype(np.int64)
+        evals.append(float(((b[:, 1] - b[:, 0] + 1) * (b[:, 3] - b[:, 2] + 1)).sum()))
     S_mean = float(np.mean([c["survivors"] for c in counts]))
     T_mean = float(np.mean([c["pairs"] for c in counts]))
     C_mean = float(np.mean([c["candidates"] for c in counts]))
     X64_mean = float(np.mean([c["fp64_decided"] for c in counts]))
+    E_mean = float(np.mean(evals))
 
     # L2 flush by READING 256 MiB (> 126 MB L2): evicts the step's working set
     # without leaving dirty lines whose write-back would bill the next kernel.
@@ -385,21 +422,36 @@ def run_ours(args):
     def flush():
         torch.sum(flush_src, dim=0, out=flush_dst)
 
-    def capture(k):
-        # u2: the step's Adam is fused with the cull of this rank's next slice
-        # (gpk_graph_capture_train_next), so each step starts at K_decide
+    n_groups = len(poses) // B   # step i renders group i mod n_groups (B consecutive poses)
+
+    def group(k, nb=None):
+        nb = nb or B
+        return [poses[(k * nb + b) % len(poses)] for b in range(nb)]
+
+    def capture(k, nb=None):
+        nb = nb or B
+        if nb > 1:
+            return (sess.capture_train_batch(group(k, nb), psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS) if u2
+                    else sess.capture_fwd_bwd_batch(group(k, nb), psf, rcfg))
+        # u2 --pipeline: the step's Adam is fused with the cull of this rank's
+        # next slice (gpk_graph_capture_train_next), so each step starts at K_decide
         if u2:
             return sess.capture_train(poses[k], psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS,
                                       next_pose=poses[(k + world) % len(poses)] if args.pipeline else None)
         return sess.capture_fwd_bwd(poses[k], psf, rcfg)
 
-    # one CUDA graph per slice pose: the whole step is one submission
-    graphs = [capture(k) for k in range(len(poses))] if args.graphs else None
+    # one CUDA graph per slice pose (group of B poses): the whole step is one submission
+    graphs = [capture(k) for k in range(n_groups)] if args.graphs else None
 
     def step(i):
-        k = dp.slice_for(i, rank, world, len(poses))
+        k = dp.slice_for(i, rank, world, n_groups)
         if graphs is not None:
             sess.graph_launch(graphs[k])
+        elif B > 1:
+            if u2:
+                sess.train_step_batch(group(k), psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS)
+            else:
+                sess.fwd_bwd_batch(group(k), psf, rcfg)
         elif u2:  # all-reduce inside
             sess.train_step(poses[k], psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS,
                             next_pose=poses[(k + world) % len(poses)] if args.pipeline else None)
@@ -430,18 +482,58 @@ def run_ours(args):
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     total_ms = dp.max_over_ranks([total_ms], device="cuda")[0]
     ms_per_step = total_ms / args.steps
-    value = world * 1000.0 / ms_per_step
+    value = world * B * 1000.0 / ms_per_step
+
+    # steady state: the same steps back to back, no flush (a training loop's
+    # regime: the previous step's dirty lines are written back inside this one)
+    ss_steps = min(args.steps, 100)
+    ss0, ss1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ss0.record(stream)
+    for i in range(ss_steps):
+        step(args.warmup + args.steps + i)
+    ss1.record(stream)
+    torch.cuda.synchronize()
+    ss_ms = dp.max_over_ranks([ss0.elapsed_time(ss1) / ss_steps], device="cuda")[0]
+
+    # the same workload B = 8 slices per step (batched step, single GPU), beside a B = 1 run
+    batched = None
+    if B == 1 and world == 1 and not args.no_batched and args.graphs:
+        bg = [capture(k, 8) for k in range(len(poses) // 8)]
+        for i in range(3):
+            sess.graph_launch(bg[i % len(bg)])
+        torch.cuda.synchronize()
+        nb_steps = max(10, min(args.steps // 4, 50))
+        bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(nb_steps)]
+        for i in range(nb_steps):
+            flush()
+            bev[i][0].record(stream)
+            sess.graph_launch(bg[i % len(bg)])
+            bev[i][1].record(stream)
+        torch.cuda.synchronize()
+        b_ms = sum(a.elapsed_time(b) for a, b in bev) / nb_steps
+        batched = {"slices_per_step": 8, "ms_per_step": b_ms, "value": 8 * 1000.0 / b_ms, "unit": "slices/s",
+                   "steps": nb_steps, "unit_of_work": ("8 slices rendered concurrently on slice contexts, "
+                                                       + ("one Adam on their summed gradient" if u2
+                                                          else "their gradients summed")),
+                   "l2": "flushed before each step"}
+        sess.graph_destroy_all()
+        graphs = [capture(k) for k in range(n_groups)]
 
     # per-kernel device time: the same steps through graphs captured with an
     # event-record node around every stage (device-side timestamps; the nodes
     # themselves add ~2-4 us per stage, so these over-state each stage a little)
+    # (B > 1: only the session's own stream is bracketed: slice 0's kernels and Adam)
     prof_steps = min(args.steps, 100)
     sess.stage_timing(True)
-    prof_graphs = [capture(k) for k in range(len(poses))]
+    prof_graphs = [capture(k) for k in range(n_groups)]
     sess.stage_times(reset=True)
     for i in range(prof_steps):
         flush()
-        sess.graph_launch(prof_graphs[dp.slice_for(args.warmup + i, rank, world, len(poses))])
+        sess.graph_launch(prof_graphs[dp.slice_for(args.warmup + i, rank, world, n_groups)])
     sess.stage_timing(False)
     stages = sess.stage_times(reset=True)
 
@@ -449,13 +541,21 @@ def run_ours(args):
     e2e_steps = max(5, min(args.steps, 50))
     e_s = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)]
     e_e = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)]
+    ctxs = [sess.context(b) for b in range(B)]
     if u2:
-        pin_tgt = torch.from_numpy(tgt).pin_memory()
-        pin_loss = torch.empty(1, dtype=torch.float64).pin_memory()
-        for i in range(3):  # warm-up of the copy path (first transfers on the copy stream)
-            sess.upload(N.GPK_BUF_TARGET, pin_tgt.data_ptr(), P * 4)
+        # the step's B targets (one per slice context) up, its B losses down
+        pin_tgt = [torch.from_numpy(tgt).pin_memory() for _ in range(B)]
+        pin_loss = torch.empty(B, dtype=torch.float64).pin_memory()
+
+        def e2e_step(i):
+            for b in range(B):
+                ctxs[b].upload(N.GPK_BUF_TARGET, pin_tgt[b].data_ptr(), P * 4)
             step(i)
-            sess.download(N.GPK_BUF_LOSS, pin_loss.data_ptr(), 8)
+            for b in range(B):
+                ctxs[b].download(N.GPK_BUF_LOSS, pin_loss.data_ptr() + 8 * b, 8)
+
+        for i in range(3):  # warm-up of the copy path (first transfers on the copy stream)
+            e2e_step(i)
         sess.synchronize()
         for i in range(e2e_steps):
             # two flushes (~80 us of GPU work outside the window) give the host
@@ -464,37 +564,40 @@ def run_ours(args):
             flush()
             flush()
             e_s[i].record(stream)
-            sess.upload(N.GPK_BUF_TARGET, pin_tgt.data_ptr(), P * 4)
-            step(i)
-            sess.download(N.GPK_BUF_LOSS, pin_loss.data_ptr(), 8)
+            e2e_step(i)
             e_e[i].record(stream)
             e_e[i].synchronize()
         assert np.isfinite(pin_loss.numpy()).all()
-        h2d, d2h = P * 4, 8
-        e2e_path = "C-ABI: gpk_upload(target, pinned) + train step (graph) + gpk_download(loss)"
+        h2d, d2h = B * P * 4, B * 8
+        e2e_path = (f"C-ABI: gpk_upload(target, pinned) x {B} + train step (graph) + gpk_download(loss) x {B}")
     else:
-        pin_dl = torch.from_numpy(dl).pin_memory()
-        pin_img = torch.empty(P, dtype=torch.float32).pin_memory()
+        pin_dl = [torch.from_numpy(dl).pin_memory() for _ in range(B)]
+        pin_img = torch.empty(B * P, dtype=torch.float32).pin_memory()
         _, gbytes = sess.device_buffer(N.GPK_BUF_GRADS)
         pin_grads = torch.empty(gbytes // 4, dtype=torch.float32).pin_memory()
-        for i in range(3):  # warm-up of the copy path
-            sess.upload(N.GPK_BUF_DL_DI, pin_dl.data_ptr(), P * 4)
+
+        def e2e_step(i):
+            for b in range(B):
+                ctxs[b].upload(N.GPK_BUF_DL_DI, pin_dl[b].data_ptr(), P * 4)
             step(i)
-            sess.download(N.GPK_BUF_IMAGE, pin_img.data_ptr(), P * 4)
+            for b in range(B):
+                ctxs[b].download(N.GPK_BUF_IMAGE, pin_img.data_ptr() + 4 * P * b, P * 4)
+            sess.download(N.GPK_BUF_GRADS, pin_grads.data_ptr(), gbytes)  # dense gradient planes
+
+        for i in range(3):  # warm-up of the copy path
+            e2e_step(i)
         sess.synchronize()
         for i in range(e2e_steps):
             flush()
             flush()
             e_s[i].record(stream)
-            sess.upload(N.GPK_BUF_DL_DI, pin_dl.data_ptr(), P * 4)
-            step(i)
-            sess.download(N.GPK_BUF_IMAGE, pin_img.data_ptr(), P * 4)
-            sess.download(N.GPK_BUF_GRADS, pin_grads.data_ptr(), gbytes)  # dense gradient planes
+            e2e_step(i)
             e_e[i].record(stream)
             e_e[i].synchronize()
         assert np.isfinite(pin_grads.numpy()[:1000]).all()
-        h2d, d2h = P * 4, P * 4 + gbytes
-        e2e_path = "C-ABI: gpk_upload(dL/dI) + fwd_bwd (graph) + gpk_download(image, dense gradients)"
+        h2d, d2h = B * P * 4, B * P * 4 + gbytes
+        e2e_path = (f"C-ABI: gpk_upload(dL/dI) x {B} + fwd_bwd (graph) + gpk_download(image) x {B} "
+                    "+ gpk_download(dense gradients)")
     e2e_each = sorted(s.elapsed_time(e) for s, e in zip(e_s, e_e))
     e2e_ms = sum(e2e_each) / e2e_steps
     e2e_ms = dp.max_over_ranks([e2e_ms], device="cuda")[0]
@@ -548,6 +651,20 @@ def run_ours(args):
         kn, kb, _ = kernel_bytes[k]
         ms = ms_tot / cnt
         per_kernel[kn] = {"ms": ms, "gbs": kb / (ms * 1e-3) / 1e9, "frac": kb / (ms * 1e-3) / 1e9 / peak}
+    # The pixel kernels are not HBM-bound: their work is one exp per pixel and
+    # (tile, Gaussian) pair of the reference's loops (render.hpp:179-181,
+    # backward.hpp:120-137): E = sum over survivors of the bound area. Their
+    # roofline is the MUFU ex2 rate (16 per SM per clock).
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    clk_mhz = ClockSampler.peak_mhz(local)
+    ex2_peak = 16.0 * sm_count * clk_mhz * 1e6
+    compute_roof = {"ex2_peak_per_s": ex2_peak, "evals_per_slice": E_mean,
+                    "basis": f"16 ex2/clk/SM x {sm_count} SMs x {clk_mhz:.0f} MHz; E = sum of survivor bound areas"}
+    for stg, kn in (("raster", "k_raster_fwd"), ("backward", "k_raster_bwd")):
+        if stg in measured:
+            ms = measured[stg][0] / measured[stg][1]
+            compute_roof[kn] = {"ms": ms, "evals_per_s": E_mean / (ms * 1e-3),
+                                "frac": E_mean / (ms * 1e-3) / ex2_peak}
     # U2 floor with slot gradients: 44N cull read + 264N Adam (p, m, v read and
     # written) + 2N slot map (SURVEY.md §8d's 396N assumed dense gradient
     # planes: +44N Adam read, +44N clear)
@@ -565,21 +682,31 @@ def run_ours(args):
                           "formula": (("310N + 8P (U2 with slot gradients; SURVEY.md §8d: 396N dense)" if world == 1
                                        else "44N + 308N/world + 8P per rank (U2, sharded Adam; collectives excluded)")
                                       if u2 else "88N + 8P (U1, SURVEY.md §8d)")},
+        "steady_state": {"ms_per_step": ss_ms, "value": world * B * 1000.0 / ss_ms, "steps": ss_steps,
+                         "note": "no L2 flush between steps (back-to-back training loop)"},
         "stage_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in stages.items() if v[1]},
+        "compute_roofline": compute_roof,
         "kernels": per_kernel,
         "submission": "CUDA graph per slice pose" if graphs is not None else "kernel by kernel",
         "survivors_mean": S_mean, "pairs_mean": T_mean, "candidates_mean": C_mean,
         "fp64_decided_mean": X64_mean,
-        "e2e": {"value": world * 1000.0 / e2e_ms, "unit": "slices/s", "h2d_bytes_per_step": h2d,
+        "e2e": {"value": world * B * 1000.0 / e2e_ms, "unit": "slices/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "path": e2e_path,
                 "ms_min": e2e_each[0], "ms_median": e2e_each[len(e2e_each) // 2], "ms_max": e2e_each[-1]},
         "gpu_launches": None,
         "clocks": clk.result(),
     }
-    # u1: filter + decide + (gather | radix passes) + forward + backward + chain + chain_exact;
-    # u2: the same without the filter (fused into Adam) + SSIM forward + Adam/cull
-    # (the SSIM backward runs inside the raster backward; memsets are not kernels)
-    launches = 2 + (1 if passes == 1 else passes) + 4 + (1 if u2 else 0)
+    if batched:
+        line["batched"] = batched
+    # per slice: filter + decide + (gather | radix passes) + forward + backward + chain + chain_exact;
+    # u2: the gather runs inside the forward, + SSIM forward (its backward runs in the raster
+    # backward), + Adam constants + Adam once per step (--pipeline: the filter is fused into
+    # Adam); u1 x B: + one gradient scatter per slice. Memsets are not kernels.
+    sort_k = passes if passes > 1 else (0 if u2 else 1)
+    per_slice = 2 + sort_k + 4 + (1 if u2 else 0)
+    launches = B * per_slice + (2 if u2 else (B if B > 1 else 0))
+    if u2 and args.pipeline:
+        launches -= 1
     line["gpu_launches"] = launches * args.steps
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -587,6 +714,8 @@ def run_ours(args):
                                                                         args.cpu_seconds).items()
                                     if k in ("value", "unit", "cores", "kind", "sample",
                                              "stage_seconds_per_slice")}
+            one = cpu_reference_rate(cfg, gs.records, args.unit, args.cpu_1thread_seconds, threads=1)
+            line["cpu_baseline"]["one_thread"] = {k: one[k] for k in ("value", "unit", "cores", "sample")}
         except Exception as e:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     sess.close()

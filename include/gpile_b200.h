@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GPK_ABI_VERSION 4
+#define GPK_ABI_VERSION 5
 #define GPK_RECORD_FLOATS 11
 
 typedef enum {
@@ -196,6 +196,13 @@ int gpk_prepare_stats(gpk_session* s, uint64_t* candidates, uint64_t* survivors,
  * pixel bounds (lo_x, hi_x, lo_y, hi_y) and 6 doubles (alpha_tilde, mu_2d.x,
  * mu_2d.y, conic.a, conic.b, conic.d). Any pointer may be NULL. */
 int gpk_get_prepared(gpk_session* s, uint32_t* index, int32_t* bounds, double* fields);
+/* Every PreparedGaussian field (render.hpp:68-79) of the survivors, in set
+ * order, GPK_PREPARED_FIELDS doubles each, in the reference's fp64 operation
+ * order: alpha, opacity_r, alpha_tilde, mu_c[3], mu_e[3], sigma_c[9],
+ * sigma_c_inv[9], sigma_e[9] (row-major), mu_2d[2], cov2d[4] (a b c d),
+ * conic[4], det2. Synchronizes. */
+#define GPK_PREPARED_FIELDS 47
+int gpk_get_prepared_fields(gpk_session* s, double* fields);
 /* Per-tile lists (render.hpp:142-160): offsets[tiles+1], entries[pairs] holding
  * set indices in list order. */
 int gpk_get_tile_lists(gpk_session* s, uint32_t* offsets, uint32_t* entries);
@@ -258,6 +265,28 @@ int gpk_train_step_next(gpk_session* s, const gpk_slice_pose* pose, const gpk_ps
                         const gpk_learning_rates* lr0, int32_t total_iterations,
                         const gpk_slice_pose* next_pose);
 
+/* ---- batched slices (SURVEY.md §7.3.7, §8e "B slices per rank per step") ------
+ * Context k in [0, 8) of a session: k = 0 is the session itself; k >= 1 is a
+ * session handle with its own stream and per-slice buffers (image, dL/dI,
+ * target, survivor records, tile lists) whose Gaussian parameters, dense
+ * gradient planes and Adam moments are the session's. Upload slice k's target
+ * or dL/dI to context k (gpk_upload); per-slice calls (gpk_prepare,
+ * gpk_rasterize, gpk_get_prepared, ...) work on a context; calls that change
+ * the set or the optimizer state do not (GPK_ERR_STATE). Contexts are owned
+ * and destroyed by their session. */
+int gpk_slice_context(gpk_session* s, int32_t k, gpk_session** ctx);
+/* U1 x B: slices poses[0..B) (B <= 8) rendered concurrently, slice k on
+ * context k, each backward of its context's GPK_BUF_DL_DI; GPK_BUF_GRADS
+ * holds the SUM of the B slices' gradients, added in slice order. */
+int gpk_fwd_bwd_batch(gpk_session* s, int32_t nslices, const gpk_slice_pose* poses, const gpk_psf* psf,
+                      const gpk_raster_config* cfg);
+/* U2 x B: B slices (targets from the contexts' GPK_BUF_TARGET), their losses
+ * (each context's GPK_BUF_LOSS), ONE scheduled Adam step on the sum of the B
+ * gradients (slice order). B = 1 is gpk_train_step. */
+int gpk_train_step_batch(gpk_session* s, int32_t nslices, const gpk_slice_pose* poses, const gpk_psf* psf,
+                         const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                         const gpk_learning_rates* lr0, int32_t total_iterations);
+
 /* ---- CUDA graphs of the fused paths ------------------------------------------- */
 /* Capture gpk_fwd_bwd_slice / gpk_train_step for a fixed pose into an
  * executable CUDA graph (launch overhead of the ~7 kernels collapses to one
@@ -275,6 +304,13 @@ int gpk_graph_capture_train_next(gpk_session* s, const gpk_slice_pose* pose, con
                                  const gpk_raster_config* cfg, double lambda, double dssim_scale,
                                  const gpk_learning_rates* lr0, int32_t total_iterations,
                                  const gpk_slice_pose* next_pose, int32_t* graph_id);
+/* Graphs of the batched steps (fixed poses). */
+int gpk_graph_capture_fwd_bwd_batch(gpk_session* s, int32_t nslices, const gpk_slice_pose* poses,
+                                    const gpk_psf* psf, const gpk_raster_config* cfg, int32_t* graph_id);
+int gpk_graph_capture_train_batch(gpk_session* s, int32_t nslices, const gpk_slice_pose* poses,
+                                  const gpk_psf* psf, const gpk_raster_config* cfg, double lambda,
+                                  double dssim_scale, const gpk_learning_rates* lr0, int32_t total_iterations,
+                                  int32_t* graph_id);
 int gpk_graph_launch(gpk_session* s, int32_t graph_id);
 int gpk_graph_destroy_all(gpk_session* s);
 

@@ -33,11 +33,15 @@
 // parameters resident: use gpile::b200::Session (set_gaussians once, then
 // fwd_bwd / train_step, parameters never leave HBM).
 //
-// PreparedGaussian: the device keeps the prepared slice; the vector returned
-// by prepare_gaussians carries index, alpha_tilde, mu_2d, conic and the pixel
-// bounds (the fields the pixel kernels consume), and acts as the handle that
-// rasterize_prepared / backward_prepared must be given (the most recent
-// prepare on this thread's default session).
+// PreparedGaussian: prepare_gaussians fills every field the reference fills
+// (render.hpp:68-79; gpk_get_prepared_fields, the reference's fp64 operation
+// order). The device keeps the most recent prepared slice; the drop-in also
+// remembers the last few prepared vectors it returned on this thread (their
+// pose, PSF, config and the set they came from), so rasterize_prepared /
+// backward_prepared accept any of them — a vector other than the latest is
+// prepared again on the device from the remembered inputs. A vector the
+// drop-in did not return (or forgot: more than kPreparedMemory prepares ago)
+// raises std::logic_error.
 #pragma once
 
 #include <gpile/backward.hpp>
@@ -209,26 +213,45 @@ class Session {
         check(gpk_prepared_count(s_, &S, &T));
         std::vector<uint32_t> idx(S);
         std::vector<int32_t> bnd(4 * S);
-        std::vector<double> fld(6 * S);
-        if (S) check(gpk_get_prepared(s_, idx.data(), bnd.data(), fld.data()));
+        std::vector<double> fld(GPK_PREPARED_FIELDS * S);
+        if (S) {
+            check(gpk_get_prepared(s_, idx.data(), bnd.data(), nullptr));
+            check(gpk_get_prepared_fields(s_, fld.data()));
+        }
         std::vector<PreparedGaussian> out(S);
+        auto mat3 = [](const double* f) {
+            Mat3 m;
+            for (int i = 0; i < 9; ++i) m.m[i / 3][i % 3] = f[i];
+            return m;
+        };
         for (uint64_t k = 0; k < S; ++k) {
             PreparedGaussian& g = out[k];
+            const double* f = &fld[GPK_PREPARED_FIELDS * k];
             g.index = idx[k];
             g.lo_x = bnd[4 * k];
             g.hi_x = bnd[4 * k + 1];
             g.lo_y = bnd[4 * k + 2];
             g.hi_y = bnd[4 * k + 3];
-            g.alpha_tilde = fld[6 * k];
-            g.mu_2d = {fld[6 * k + 1], fld[6 * k + 2]};
-            g.conic = {fld[6 * k + 3], fld[6 * k + 4], fld[6 * k + 4], fld[6 * k + 5]};
+            g.alpha = f[0];
+            g.opacity_r = f[1];
+            g.alpha_tilde = f[2];
+            g.mu_c = {f[3], f[4], f[5]};
+            g.mu_e = {f[6], f[7], f[8]};
+            g.sigma_c = mat3(f + 9);
+            g.sigma_c_inv = mat3(f + 18);
+            g.sigma_e = mat3(f + 27);
+            g.mu_2d = {f[36], f[37]};
+            g.cov2d = {f[38], f[39], f[40], f[41]};
+            g.conic = {f[42], f[43], f[44], f[45]};
+            g.det2 = f[46];
         }
         pose_ = pose;
         return out;
     }
 
-    SliceImage rasterize() {
-        SliceImage img(pose_.width, pose_.height);
+    SliceImage rasterize() { return rasterize(pose_); }
+    SliceImage rasterize(const SlicePose& pose) {
+        SliceImage img(pose.width, pose.height);
         std::vector<float> px(img.size());
         check(gpk_rasterize(s_, px.data()));
         std::copy(px.begin(), px.end(), img.pixels.begin());
@@ -236,7 +259,10 @@ class Session {
     }
 
     GaussianGradients backward(const SliceImage& dl_di, ScreenGradStats* stats = nullptr) {
-        if (dl_di.width != pose_.width || dl_di.height != pose_.height)
+        return backward(dl_di, stats, pose_);
+    }
+    GaussianGradients backward(const SliceImage& dl_di, ScreenGradStats* stats, const SlicePose& pose) {
+        if (dl_di.width != pose.width || dl_di.height != pose.height)
             throw std::invalid_argument("backward_prepared: dl_di shape mismatch");  // backward.hpp:102-103
         uint64_t n = 0;
         check(gpk_gaussian_count(s_, &n));
@@ -289,12 +315,40 @@ class Session {
 
 namespace detail {
 
-// This thread's session on device 0 and the handle of its last prepare.
+constexpr std::size_t kPreparedMemory = 8;  // prepared vectors remembered per thread
+
+// One prepared vector the drop-in returned: its identity (storage, size and a
+// fingerprint of its integer content) and the inputs that produced it.
+struct PreparedEntry {
+    const void* data = nullptr;
+    std::size_t size = 0;
+    uint64_t fingerprint = 0;
+    uint64_t serial = 0;               // 1 + position in this thread's prepare sequence
+    SlicePose pose{};
+    PsfSpec psf{};
+    RasterConfig cfg{};
+    std::shared_ptr<const std::vector<float>> records;  // the set it was prepared from
+    gpk_bounds bbox{};
+};
+
+inline uint64_t fingerprint_of(const std::vector<PreparedGaussian>& v) {
+    uint64_t h = 1469598103934665603ull ^ v.size();
+    for (const PreparedGaussian& g : v) {
+        const uint64_t w[3] = {g.index, (uint64_t)(uint32_t)g.lo_x | ((uint64_t)(uint32_t)g.hi_x << 32),
+                               (uint64_t)(uint32_t)g.lo_y | ((uint64_t)(uint32_t)g.hi_y << 32)};
+        for (uint64_t x : w) h = (h ^ x) * 1099511628211ull;
+    }
+    return h;
+}
+
+// This thread's session on device 0, the prepared vectors it returned, and
+// which of them the device holds now.
 struct ThreadState {
     std::unique_ptr<Session> session;
-    const void* prepared_data = nullptr;
-    std::size_t prepared_size = 0;
-    std::size_t set_size = 0;
+    std::vector<PreparedEntry> prepared;   // most recent last, at most kPreparedMemory
+    uint64_t serial = 0;
+    uint64_t device_serial = 0;            // the entry whose slice the device holds (0: none)
+    const std::vector<float>* device_records = nullptr;
 };
 
 inline ThreadState& state() {
@@ -303,35 +357,78 @@ inline ThreadState& state() {
     return st;
 }
 
-inline void require_last(const std::vector<PreparedGaussian>& prepared) {
-    const ThreadState& st = state();
-    if (prepared.data() != st.prepared_data || prepared.size() != st.prepared_size)
-        throw std::logic_error(
-            "gpile::b200: prepared vector is not the result of this thread's last prepare_gaussians");
+// Make the device hold `prepared`'s slice: the latest prepare as is, an older
+// remembered one prepared again from its own set, pose, PSF and config.
+inline const PreparedEntry& bind_prepared(const std::vector<PreparedGaussian>& prepared) {
+    ThreadState& st = state();
+    const uint64_t fp = fingerprint_of(prepared);
+    for (auto it = st.prepared.rbegin(); it != st.prepared.rend(); ++it) {
+        if (it->data != prepared.data() || it->size != prepared.size() || it->fingerprint != fp) continue;
+        if (st.device_serial != it->serial) {
+            gpk_session* h = st.session->handle();
+            if (st.device_records != it->records.get()) {
+                check(gpk_set_gaussians(h, it->records->size() / 11, it->records->data(), &it->bbox));
+                st.device_records = it->records.get();
+            }
+            const gpk_slice_pose p = pose_of(it->pose);
+            const gpk_psf f = psf_of(it->psf);
+            const gpk_raster_config c = cfg_of(it->cfg);
+            check(gpk_prepare(h, &p, &f, &c));
+            st.device_serial = it->serial;
+        }
+        return *it;
+    }
+    throw std::logic_error(
+        "gpile::b200: prepared vector was not returned by one of this thread's recent prepare_gaussians calls");
 }
 
 }  // namespace detail
 
-inline Session& default_session() { return *detail::state().session; }
+// The thread's session for direct use; whoever takes it may change the
+// resident set or prepared slice, so the next rasterize_prepared /
+// backward_prepared binds its vector again.
+inline Session& default_session() {
+    detail::ThreadState& st = detail::state();
+    st.device_serial = 0;
+    st.device_records = nullptr;
+    return *st.session;
+}
 
 // ---- render.hpp ------------------------------------------------------------------
 inline std::vector<PreparedGaussian> prepare_gaussians(const GaussianSet& set, const SlicePose& pose,
                                                        const PsfSpec& psf, const RasterConfig& cfg) {
     detail::ThreadState& st = detail::state();
-    st.session->set_gaussians(set);
+    auto recs = std::make_shared<const std::vector<float>>(detail::records_of(set));
+    const gpk_bounds b = detail::bounds_of(set.bbox);
+    check(gpk_set_gaussians(st.session->handle(), set.size(), recs->data(), &b));
+    st.device_records = recs.get();
     std::vector<PreparedGaussian> out = st.session->prepare(pose, psf, cfg);
-    st.prepared_data = out.data();
-    st.prepared_size = out.size();
-    st.set_size = set.size();
+    detail::PreparedEntry e;
+    e.data = out.data();
+    e.size = out.size();
+    e.fingerprint = detail::fingerprint_of(out);
+    e.serial = ++st.serial;
+    e.pose = pose;
+    e.psf = psf;
+    e.cfg = cfg;
+    e.records = std::move(recs);
+    e.bbox = b;
+    // vectors are returned by value: a moved-from result keeps its heap
+    // storage, so data() identifies it (with the size and the fingerprint)
+    if (st.prepared.size() == detail::kPreparedMemory) st.prepared.erase(st.prepared.begin());
+    st.prepared.push_back(std::move(e));
+    st.device_serial = st.serial;
     return out;
 }
 
+// The remembered slice of `prepared` rendered (render.hpp:166-192); pose and
+// cfg are the caller's and must describe the same slice.
 inline SliceImage rasterize_prepared(const std::vector<PreparedGaussian>& prepared, const SlicePose& pose,
                                      const RasterConfig& cfg) {
-    (void)pose;
-    (void)cfg;
-    detail::require_last(prepared);
-    return detail::state().session->rasterize();
+    const detail::PreparedEntry& e = detail::bind_prepared(prepared);
+    if (pose.width != e.pose.width || pose.height != e.pose.height || cfg.tile_size != e.cfg.tile_size)
+        throw std::invalid_argument("rasterize_prepared: pose / config differ from the prepared slice");
+    return detail::state().session->rasterize(pose);
 }
 
 inline SliceImage rasterize_slice(const GaussianSet& set, const SlicePose& pose, const PsfSpec& psf,
@@ -344,12 +441,13 @@ inline SliceImage rasterize_slice(const GaussianSet& set, const SlicePose& pose,
 inline GaussianGradients backward_prepared(const GaussianSet& set, const std::vector<PreparedGaussian>& prepared,
                                            const SlicePose& pose, const SliceImage& dl_di,
                                            const RasterConfig& cfg, ScreenGradStats* stats = nullptr) {
-    (void)pose;
     (void)cfg;
-    detail::require_last(prepared);
-    if (set.size() != detail::state().set_size)
+    const detail::PreparedEntry& e = detail::bind_prepared(prepared);
+    if (set.size() * 11 != e.records->size())
         throw std::invalid_argument("backward_prepared: set does not match the prepared slice");
-    return detail::state().session->backward(dl_di, stats);
+    if (pose.width != e.pose.width || pose.height != e.pose.height)
+        throw std::invalid_argument("backward_prepared: pose differs from the prepared slice");
+    return detail::state().session->backward(dl_di, stats, pose);
 }
 
 inline GaussianGradients backward_slice(const GaussianSet& set, const SlicePose& pose, const PsfSpec& psf,

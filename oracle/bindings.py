@@ -189,6 +189,18 @@ class CpuChecker:
         k = cnt.value
         return idx[:k].copy(), bnd[:k].copy(), fld[:k].copy()
 
+    def prepare_full(self, rec, pose, psf, cfg, bbox=((0, 0, 0), (1, 1, 1))):
+        """Every PreparedGaussian field (47 doubles per survivor, ref only)."""
+        assert self.is_ref, "prepare_full: the reference build only"
+        h = self._set(rec, bbox)
+        n = h.rec.shape[0]
+        cnt = C.c_uint64()
+        fld = np.zeros((max(n, 1), 47), np.float64)
+        p, f, c = pose_c(pose), psf_c(psf), cfg_c(cfg)
+        self._call("prepare_full", C.c_void_p(h.h), C.byref(p), C.byref(f), C.byref(c), C.byref(cnt), _d(fld),
+                   C.c_uint64(fld.shape[0]))
+        return fld[:cnt.value].copy()
+
     def tile_lists(self, rec, pose, psf, cfg, bbox=((0, 0, 0), (1, 1, 1))):
         h = self._set(rec, bbox)
         p, f, c = pose_c(pose), psf_c(psf), cfg_c(cfg)

@@ -301,6 +301,36 @@ int gref_prepare(void* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     });
 }
 
+// prepare_gaussians (render.hpp:83), every PreparedGaussian field (:68-79):
+// 47 doubles per survivor in gpk_get_prepared_fields' layout (alpha,
+// opacity_r, alpha_tilde, mu_c, mu_e, sigma_c, sigma_c_inv, sigma_e, mu_2d,
+// cov2d a b c d, conic a b c d, det2).
+int gref_prepare_full(void* s, const gpk_slice_pose* pose, const gpk_psf* psf, const gpk_raster_config* cfg,
+                      uint64_t* count, double* fields, uint64_t capacity) {
+    return guarded([&] {
+        psf_from(psf).validate();
+        const auto prep = prepare_gaussians(*static_cast<GaussianSet*>(s), pose_from(pose), psf_from(psf),
+                                            cfg_from(cfg));
+        *count = prep.size();
+        for (std::size_t k = 0; k < prep.size() && k < capacity; ++k) {
+            const PreparedGaussian& p = prep[k];
+            double* f = fields + 47 * k;
+            f[0] = p.alpha; f[1] = p.opacity_r; f[2] = p.alpha_tilde;
+            f[3] = p.mu_c.x; f[4] = p.mu_c.y; f[5] = p.mu_c.z;
+            f[6] = p.mu_e.x; f[7] = p.mu_e.y; f[8] = p.mu_e.z;
+            for (int i = 0; i < 9; ++i) {
+                f[9 + i] = p.sigma_c.m[i / 3][i % 3];
+                f[18 + i] = p.sigma_c_inv.m[i / 3][i % 3];
+                f[27 + i] = p.sigma_e.m[i / 3][i % 3];
+            }
+            f[36] = p.mu_2d.x; f[37] = p.mu_2d.y;
+            f[38] = p.cov2d.a; f[39] = p.cov2d.b; f[40] = p.cov2d.c; f[41] = p.cov2d.d;
+            f[42] = p.conic.a; f[43] = p.conic.b; f[44] = p.conic.c; f[45] = p.conic.d;
+            f[46] = p.det2;
+        }
+    });
+}
+
 // detail::TileGrid (render.hpp:142-160), entries translated to set indices.
 int gref_tile_lists(void* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                     const gpk_raster_config* cfg, uint32_t* offsets, uint32_t* entries,

@@ -13,7 +13,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libgpile_b200.so"
-GPK_ABI_VERSION = 4  # include/gpile_b200.h
+GPK_ABI_VERSION = 5  # include/gpile_b200.h
 
 GPK_OK = 0
 GPK_ERR_INVALID_ARGUMENT = 1
@@ -180,6 +180,7 @@ _PROTOS = {
     "gpk_prepared_count": (C.c_int, [_P, _U64, _U64]),
     "gpk_prepare_stats": (C.c_int, [_P, _U64, _U64, _U64, _U64]),
     "gpk_get_prepared": (C.c_int, [_P, _U32, _I32, _D]),
+    "gpk_get_prepared_fields": (C.c_int, [_P, _D]),
     "gpk_get_tile_lists": (C.c_int, [_P, _U32, _U32]),
     "gpk_rasterize": (C.c_int, [_P, _F]),
     "gpk_backward": (C.c_int, [_P, _F, _F, C.POINTER(ScreenStatsC)]),
@@ -196,6 +197,17 @@ _PROTOS = {
                                  C.c_double, C.c_double, C.POINTER(LearningRatesC), C.c_int32]),
     "gpk_train_step_next": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC), C.POINTER(RasterConfigC),
                                  C.c_double, C.c_double, C.POINTER(LearningRatesC), C.c_int32, C.POINTER(SlicePoseC)]),
+    "gpk_slice_context": (C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
+    "gpk_fwd_bwd_batch": (C.c_int, [_P, C.c_int32, C.POINTER(SlicePoseC), C.POINTER(PsfC),
+                                    C.POINTER(RasterConfigC)]),
+    "gpk_train_step_batch": (C.c_int, [_P, C.c_int32, C.POINTER(SlicePoseC), C.POINTER(PsfC),
+                                       C.POINTER(RasterConfigC), C.c_double, C.c_double,
+                                       C.POINTER(LearningRatesC), C.c_int32]),
+    "gpk_graph_capture_fwd_bwd_batch": (C.c_int, [_P, C.c_int32, C.POINTER(SlicePoseC), C.POINTER(PsfC),
+                                                  C.POINTER(RasterConfigC), C.POINTER(C.c_int32)]),
+    "gpk_graph_capture_train_batch": (C.c_int, [_P, C.c_int32, C.POINTER(SlicePoseC), C.POINTER(PsfC),
+                                                C.POINTER(RasterConfigC), C.c_double, C.c_double,
+                                                C.POINTER(LearningRatesC), C.c_int32, C.POINTER(C.c_int32)]),
     "gpk_graph_capture_fwd_bwd": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC),
                                             C.POINTER(RasterConfigC), C.POINTER(C.c_int32)]),
     "gpk_graph_capture_train": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC),

@@ -456,6 +456,22 @@ class Session:
         check(N.lib.gpk_get_prepared(self._h, N.u32ptr(idx), N.i32ptr(bnd), N.dptr(fld)))
         return Prepared(idx, bnd, fld, t)
 
+    PREPARED_FIELDS = ("alpha", "opacity_r", "alpha_tilde", "mu_c", "mu_e", "sigma_c", "sigma_c_inv",
+                       "sigma_e", "mu_2d", "cov2d", "conic", "det2")
+
+    def prepared_fields(self) -> dict:
+        """Every PreparedGaussian field (render.hpp:68-79) of the survivors, set
+        order, in the reference's fp64 operation order (gpk_get_prepared_fields)."""
+        S, _ = self.prepared_count()
+        raw = np.zeros((max(S, 1), 47), np.float64)
+        check(N.lib.gpk_get_prepared_fields(self._h, N.dptr(raw)))
+        raw = raw[:S]
+        return {"alpha": raw[:, 0], "opacity_r": raw[:, 1], "alpha_tilde": raw[:, 2], "mu_c": raw[:, 3:6],
+                "mu_e": raw[:, 6:9], "sigma_c": raw[:, 9:18].reshape(-1, 3, 3),
+                "sigma_c_inv": raw[:, 18:27].reshape(-1, 3, 3), "sigma_e": raw[:, 27:36].reshape(-1, 3, 3),
+                "mu_2d": raw[:, 36:38], "cov2d": raw[:, 38:42].reshape(-1, 2, 2),
+                "conic": raw[:, 42:46].reshape(-1, 2, 2), "det2": raw[:, 46]}
+
     def tile_lists(self) -> tuple[np.ndarray, np.ndarray]:
         s, t = self.prepared_count()
         h, w = self.shape
@@ -573,6 +589,55 @@ class Session:
                                             dssim_scale, C.byref(l), int(total_iterations),
                                             C.byref(gid)))
         self.shape = (pose.height, pose.width)
+        return int(gid.value)
+
+    # batched slices (gpk_slice_context / gpk_*_batch)
+    def context(self, k: int) -> "Session":
+        """Slice context k (0 = this session): per-slice buffers on their own
+        stream, sharing this session's parameters (include/gpile_b200.h)."""
+        if k == 0:
+            return self
+        h = C.c_void_p()
+        check(N.lib.gpk_slice_context(self._h, int(k), C.byref(h)))
+        ctx = _SliceContext.__new__(_SliceContext)
+        ctx._h, ctx.device, ctx.n, ctx.bbox, ctx.shape = h, self.device, self.n, self.bbox, self.shape
+        return ctx
+
+    @staticmethod
+    def _poses(poses):
+        arr = (N.SlicePoseC * len(poses))(*[p.to_c() for p in poses])
+        return arr
+
+    def fwd_bwd_batch(self, poses, psf: PsfSpec, cfg: RasterConfig):
+        """U1 x B: slice k's backward takes context k's GPK_BUF_DL_DI; the dense
+        gradient is the sum over the slices (slice order)."""
+        arr, f, c = self._poses(poses), psf.to_c(), cfg.to_c()
+        check(N.lib.gpk_fwd_bwd_batch(self._h, len(poses), arr, C.byref(f), C.byref(c)))
+        self.shape = (poses[0].height, poses[0].width)
+
+    def train_step_batch(self, poses, psf: PsfSpec, cfg: RasterConfig, lam: float, dssim_scale: float,
+                         lr0: LearningRates, total_iterations: int):
+        """U2 x B: B slices (targets from the contexts), one Adam on the summed gradient."""
+        arr, f, c, l = self._poses(poses), psf.to_c(), cfg.to_c(), lr0.to_c()
+        check(N.lib.gpk_train_step_batch(self._h, len(poses), arr, C.byref(f), C.byref(c), lam, dssim_scale,
+                                         C.byref(l), int(total_iterations)))
+        self.shape = (poses[0].height, poses[0].width)
+
+    def capture_fwd_bwd_batch(self, poses, psf: PsfSpec, cfg: RasterConfig) -> int:
+        arr, f, c = self._poses(poses), psf.to_c(), cfg.to_c()
+        gid = C.c_int32()
+        check(N.lib.gpk_graph_capture_fwd_bwd_batch(self._h, len(poses), arr, C.byref(f), C.byref(c),
+                                                    C.byref(gid)))
+        self.shape = (poses[0].height, poses[0].width)
+        return int(gid.value)
+
+    def capture_train_batch(self, poses, psf: PsfSpec, cfg: RasterConfig, lam: float, dssim_scale: float,
+                            lr0: LearningRates, total_iterations: int) -> int:
+        arr, f, c, l = self._poses(poses), psf.to_c(), cfg.to_c(), lr0.to_c()
+        gid = C.c_int32()
+        check(N.lib.gpk_graph_capture_train_batch(self._h, len(poses), arr, C.byref(f), C.byref(c), lam,
+                                                  dssim_scale, C.byref(l), int(total_iterations), C.byref(gid)))
+        self.shape = (poses[0].height, poses[0].width)
         return int(gid.value)
 
     def graph_launch(self, graph_id: int):
@@ -736,6 +801,13 @@ class Session:
 
 _default: dict[int, Session] = {}
 _lock = threading.Lock()
+
+
+class _SliceContext(Session):
+    """A slice context handle (Session.context): owned by its session."""
+
+    def close(self):
+        self._h = None
 
 
 def default_session(device: int = 0) -> Session:

@@ -48,26 +48,62 @@ __global__ void __launch_bounds__(256, kMinB) k_adam(const AdamLaunch a) {
     if (any) adam_slots_clear<kAdamItems>(a, i0);
 }
 
-// Slot gradients -> dense planes (gpk_get_gradients after a training step;
-// the dense planes were zeroed before) and/or clearing the survivors' map
-// entries (a slot backward no Adam consumed). CTA per K_decide group.
-__global__ void __launch_bounds__(256) k_scatter_slots(const AdamLaunch a, int grads) {
+// Batched step: the gradient of each primitive is the sum of the B slices'
+// slot gradients (slice order); an overflowed slice anywhere skips the update.
+__device__ __forceinline__ bool batch_overflow(const AdamLaunch& a) {
+    bool of = a.ctrl && a.ctrl->pair_overflow;
+    for (int s = 0; s < a.nsrc; ++s) of |= a.src_ctrl[s]->pair_overflow != 0;
+    return of;
+}
+
+template <int kMinB>
+__global__ void __launch_bounds__(256, kMinB) k_adam_batch(const AdamLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    const uint32_t i0 = a.lo + (blockIdx.x * blockDim.x + threadIdx.x) * kAdamItems;
+    if (i0 >= a.n) return;
+    unsigned pm[kMaxBatch];
+    const bool any = adam_slots_multi(a, i0, pm);
+    if (batch_overflow(a)) {
+        if (any) adam_slots_multi_clear(a, i0, pm);
+        return;
+    }
+    const AdamConsts& c = *a.consts;
+    adam_advance_step(a, c);
+    adam_update_store_g<kAdamItems>(a, c, i0, [&](int k) { return adam_grad_multi(a, k, i0, pm); });
+    if (any) adam_slots_multi_clear(a, i0, pm);
+}
+
+// Slot gradients -> dense planes, by survivor slot (CTA per K_decide group):
+// kScatterSet writes a survivor's gradient, kScatterAdd adds it (a batched
+// step's slices, one launch per slice in slice order: the same fp32 sums as
+// its Adam), kScatterClearMap zeroes the survivor's map entry (a slot
+// backward no Adam consumed).
+__global__ void __launch_bounds__(256) k_scatter_slots(const AdamLaunch a, int mode) {
     const unsigned g = blockIdx.x;
     const unsigned S = a.grp_surv[g];
     for (unsigned j = threadIdx.x; j < S; j += blockDim.x) {
         const uint32_t slot = g * kDecideGroupSize + j, i = a.surv_gidx[slot];
-        if (grads)
+        if (mode & (kScatterSet | kScatterAdd))
 #pragma unroll
-            for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = a.slot_grads[(uint64_t)k * a.cap + slot];
-        else
-            a.gmap[i] = 0;
+            for (int k = 0; k < 11; ++k) {
+                float* d = a.grads + (uint64_t)k * a.cap + i;
+                const float v = a.slot_grads[(uint64_t)k * a.cap + slot];
+                *d = (mode & kScatterAdd) ? __fadd_rn(*d, v) : v;
+            }
+        if (mode & kScatterClearMap) a.gmap[i] = 0;
     }
 }
 
 }  // namespace
 
-void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, bool grads, cudaStream_t st) {
-    if (ngroups) k_scatter_slots<<<ngroups, 256, 0, st>>>(a, grads ? 1 : 0);
+void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, int mode, cudaStream_t st) {
+    if (ngroups) k_scatter_slots<<<ngroups, 256, 0, st>>>(a, mode);
+}
+
+void launch_adam_batch(const AdamLaunch& a, cudaStream_t st) {
+    const unsigned grid = (a.n - a.lo + 256 * kAdamItems - 1) / (256 * kAdamItems);
+    if (!grid || a.n <= a.lo) return;
+    launch_pdl(k_adam_batch<5>, dim3(grid), dim3(256), 0, st, a);
 }
 
 void launch_adam_consts(const AdamLaunch& a, cudaStream_t st) {

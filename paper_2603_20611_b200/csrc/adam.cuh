@@ -149,11 +149,43 @@ __device__ __forceinline__ void adam_slots_clear(const AdamLaunch& a, uint32_t i
 // One parameter plane of N consecutive primitives: moments updated and stored,
 // the stepped parameters returned (before clamp / renormalisation); nz collects
 // which primitives had a non-zero gradient.
-template <int N>
-__device__ __forceinline__ Pack<N> adam_plane(const AdamLaunch& a, const AdamConsts& c, int k, float lr, uint32_t i0,
-                                              const uint32_t* gslot, unsigned& nz) {
+// Batched step: the maps of all B slices for primitives i0, i0+1 (one u32 =
+// two u16 entries per slice; N == 2) and the summed gradient of plane k.
+__device__ __forceinline__ bool adam_slots_multi(const AdamLaunch& a, uint32_t i0, unsigned pm[kMaxBatch]) {
+    unsigned any = 0;
+#pragma unroll
+    for (int s = 0; s < kMaxBatch; ++s) {
+        pm[s] = 0;
+        if (s <= a.nsrc) pm[s] = *reinterpret_cast<const unsigned*>((s ? a.src_gmap[s - 1] : a.gmap) + i0);
+        any |= pm[s];
+    }
+    return any != 0;
+}
+__device__ __forceinline__ void adam_slots_multi_clear(const AdamLaunch& a, uint32_t i0, const unsigned pm[kMaxBatch]) {
+#pragma unroll
+    for (int s = 0; s < kMaxBatch; ++s)
+        if (pm[s]) *reinterpret_cast<unsigned*>((s ? a.src_gmap[s - 1] : a.gmap) + i0) = 0u;
+}
+__device__ __forceinline__ Pack<2> adam_grad_multi(const AdamLaunch& a, int k, uint32_t i0, const unsigned pm[kMaxBatch]) {
+    Pack<2> g;
+    g.v[0] = g.v[1] = 0.f;
+    const uint32_t gbase = i0 / kDecideGroupSize * kDecideGroupSize;
+#pragma unroll
+    for (int s = 0; s < kMaxBatch; ++s) {
+        if (!pm[s]) continue;
+        const float* base = (s ? a.src_slot[s - 1] : a.slot_grads) + (uint64_t)k * a.cap + gbase - 1;
+        const unsigned m0 = pm[s] & 0xffffu, m1 = pm[s] >> 16;
+        if (m0) g.v[0] = __fadd_rn(g.v[0], __ldcs(base + m0));
+        if (m1) g.v[1] = __fadd_rn(g.v[1], __ldcs(base + m1));
+    }
+    return g;
+}
+
+template <int N, typename G>
+__device__ __forceinline__ Pack<N> adam_plane_g(const AdamLaunch& a, const AdamConsts& c, int k, float lr, uint32_t i0,
+                                                const G& grad, unsigned& nz) {
     const uint64_t o = (uint64_t)k * a.cap + i0;
-    const Pack<N> g = adam_grad<N>(a, k, i0, gslot);
+    const Pack<N> g = grad(k);
     // Everything evict-first: the moments must not push the parameters (which
     // K_filter left in L2 with evict-last priority for this read) out of L2,
     // and the parameter accesses here demote those lines again, so nothing of
@@ -170,6 +202,12 @@ __device__ __forceinline__ Pack<N> adam_plane(const AdamLaunch& a, const AdamCon
     stp_stream<N>(a.m + o, m);
     stp_stream<N>(a.v + o, v);
     return p;
+}
+
+template <int N>
+__device__ __forceinline__ Pack<N> adam_plane(const AdamLaunch& a, const AdamConsts& c, int k, float lr, uint32_t i0,
+                                              const uint32_t* gslot, unsigned& nz) {
+    return adam_plane_g<N>(a, c, k, lr, i0, [&](int kk) { return adam_grad<N>(a, kk, i0, gslot); }, nz);
 }
 
 // All 11 planes of N consecutive primitives in the reference's order: position
@@ -212,13 +250,13 @@ __device__ __forceinline__ void adam_update(const AdamLaunch& a, const AdamConst
 // As adam_update + adam_store, storing each plane's parameters as soon as they
 // are final (all but the quaternion, renormalised at the end): few registers
 // live, so the stand-alone kernel runs at full occupancy. Same bits.
-template <int N>
-__device__ __forceinline__ void adam_update_store(const AdamLaunch& a, const AdamConsts& c, uint32_t i0,
-                                                  const uint32_t* gslot) {
+template <int N, typename G>
+__device__ __forceinline__ void adam_update_store_g(const AdamLaunch& a, const AdamConsts& c, uint32_t i0,
+                                                    const G& grad) {
     unsigned nz = 0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        Pack<N> p = adam_plane<N>(a, c, d, c.lr[0], i0, gslot, nz);
+        Pack<N> p = adam_plane_g<N>(a, c, d, c.lr[0], i0, grad, nz);
         const float lo = a.bbox_min[d], hi = a.bbox_max[d];
 #pragma unroll
         for (int l = 0; l < N; ++l) p.v[l] = fminf(hi, fmaxf(lo, p.v[l]));
@@ -226,11 +264,11 @@ __device__ __forceinline__ void adam_update_store(const AdamLaunch& a, const Ada
     }
 #pragma unroll
     for (int d = 3; d < 6; ++d)
-        stp_stream<N>(a.params + (uint64_t)d * a.cap + i0, adam_plane<N>(a, c, d, c.lr[2], i0, gslot, nz));
-    stp_stream<N>(a.params + (uint64_t)10 * a.cap + i0, adam_plane<N>(a, c, 10, c.lr[1], i0, gslot, nz));
+        stp_stream<N>(a.params + (uint64_t)d * a.cap + i0, adam_plane_g<N>(a, c, d, c.lr[2], i0, grad, nz));
+    stp_stream<N>(a.params + (uint64_t)10 * a.cap + i0, adam_plane_g<N>(a, c, 10, c.lr[1], i0, grad, nz));
     Pack<N> q[4];
 #pragma unroll
-    for (int d = 0; d < 4; ++d) q[d] = adam_plane<N>(a, c, 6 + d, c.lr[3], i0, gslot, nz);
+    for (int d = 0; d < 4; ++d) q[d] = adam_plane_g<N>(a, c, 6 + d, c.lr[3], i0, grad, nz);
 #pragma unroll
     for (int l = 0; l < N; ++l) {
         float& w = q[0].v[l];
@@ -248,6 +286,12 @@ __device__ __forceinline__ void adam_update_store(const AdamLaunch& a, const Ada
     }
 #pragma unroll
     for (int d = 0; d < 4; ++d) stp_stream<N>(a.params + (uint64_t)(6 + d) * a.cap + i0, q[d]);
+}
+
+template <int N>
+__device__ __forceinline__ void adam_update_store(const AdamLaunch& a, const AdamConsts& c, uint32_t i0,
+                                                  const uint32_t* gslot) {
+    adam_update_store_g<N>(a, c, i0, [&](int k) { return adam_grad<N>(a, k, i0, gslot); });
 }
 
 template <int N>

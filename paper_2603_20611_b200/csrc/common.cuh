@@ -38,6 +38,7 @@ constexpr int kMaxBuckets = 1 << kMaxDigitBits;
 constexpr int kMaxSortPasses = 2;                       // up to 2^20 image tiles
 constexpr int kSuperTiles = 16;                         // sort tiles per super-tile histogram row
 constexpr int kNumParams = 11;
+constexpr int kMaxBatch = 8;                            // slices per batched step (gpk_train_step_batch)
 
 // Error codes recorded on the device (mirrors gpk_status).
 enum DevErr : int {
@@ -554,6 +555,15 @@ struct AdamLaunch {
     uint16_t* gmap;
     const uint32_t* surv_gidx;    // slot -> set index (the gradient scatter)
     const unsigned* grp_surv;
+    // Batched training step (gpk_train_step_batch, B slices, one Adam): the
+    // further slices' slot gradients, maps and control heads. A primitive's
+    // gradient is the fp32 sum over the slices in slice order (slice 0 =
+    // slot_grads / gmap / ctrl above); every map read is cleared; an overflowed
+    // slice anywhere skips the update.
+    int nsrc;                     // further slices (0: a single slice)
+    const float* src_slot[kMaxBatch - 1];
+    uint16_t* src_gmap[kMaxBatch - 1];
+    const Control* src_ctrl[kMaxBatch - 1];
 };
 
 struct LossLaunch {
@@ -671,11 +681,14 @@ void launch_densify_classify(const DensifyLaunch& a, cudaStream_t st);
 void launch_densify_emit(const DensifyLaunch& a, cudaStream_t st);
 
 void launch_vox_prep(const VoxPrepLaunch& a, cudaStream_t st);
+void launch_prepared_full(const CandParams* sparams, const uint32_t* slots, unsigned S, const SliceArgs& s,
+                          double* out, cudaStream_t st);
 void launch_vox_eval(const VoxEvalLaunch& a, cudaStream_t st);
 void launch_vox_bwd(const VoxEvalLaunch& a, cudaStream_t st);
 void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st);
 
 void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st);
+void launch_prep_multi(const PrepLaunch* pl, int nb, int num_sms, cudaStream_t st);
 void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& next, cudaStream_t st);
 void launch_bin(const PrepLaunch& a, cudaStream_t st);
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st);
@@ -685,7 +698,9 @@ void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st);
 void launch_chain_exact(const ChainLaunch& a, int grid, cudaStream_t st);
 void launch_adam(const AdamLaunch& a, cudaStream_t st);
 void launch_adam_consts(const AdamLaunch& a, cudaStream_t st);
-void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, bool grads, cudaStream_t st);
+void launch_adam_batch(const AdamLaunch& a, cudaStream_t st);
+enum ScatterMode : int { kScatterSet = 1, kScatterAdd = 2, kScatterClearMap = 4 };
+void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, int mode, cudaStream_t st);
 void launch_loss(const LossLaunch& a, cudaStream_t st);
 unsigned loss_partial_blocks(int W, int H, double lambda);
 

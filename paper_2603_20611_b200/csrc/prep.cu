@@ -407,6 +407,66 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter(const PrepLaunch a
     }
 }
 
+// ---- K_filter over several slice poses (batched steps) ---------------------------
+// The parameters are streamed ONCE for the B slices of a batched step: each
+// warp chunk is culled against every slice's pose in turn (cull_chunk with that
+// slice's PrepLaunch), each slice's candidates compacted into its own context's
+// buffers. Per-slice housekeeping (control head, previous sort rows) as
+// K_filter's. Gradients are not touched (batched steps keep slot gradients).
+struct MultiPrep {
+    PrepLaunch p[kMaxBatch];
+    float log_tau[kMaxBatch];
+    int filter_on[kMaxBatch];
+    int nb;
+};
+
+__global__ void __launch_bounds__(kFilterThreads, 2) k_filter_multi(const __grid_constant__ MultiPrep m) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    extern __shared__ __align__(16) float s_filter[];
+    const PrepLaunch& a0 = m.p[0];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float* ring = s_filter + (size_t)warp * kFilterStages * kFilterStageFloats;
+    CullIdx& sx = reinterpret_cast<CullIdx*>(s_filter + (size_t)(kFilterThreads / 32) * kFilterStages *
+                                                             kFilterStageFloats)[warp];
+    const unsigned nchunks = a0.nfilter;
+    const unsigned gthreads = gridDim.x * kFilterThreads;
+    const unsigned gtid = blockIdx.x * kFilterThreads + tid;
+    const unsigned gwarps = gthreads / 32;
+    const unsigned long long keep = l2_evict_last_policy();
+    auto prefetch = [&](unsigned b, int stage) {
+        const float* src = a0.params + (uint64_t)b * kFilterBlock + lane * kFilterItems;
+        float* dst = ring + stage * kFilterStageFloats + lane * kFilterItems;
+#pragma unroll
+        for (int q = 0; q < 11; ++q) cp_async16_hint(dst + q * kFilterBlock, src + (uint64_t)q * a0.cap, keep);
+    };
+    unsigned b = gtid / 32;
+    if (b < nchunks) prefetch(b, 0);
+    cp_async_commit();
+    for (int k = 0; k < m.nb; ++k) {
+        const PrepLaunch& a = m.p[k];
+        for (unsigned w = gtid; w < a.head_words; w += gthreads) a.head[w] = 0u;
+        clear_prev_sort_rows(a, gtid, gthreads);
+    }
+    for (int it = 0; b < nchunks; ++it, b += gwarps) {
+        if (b + gwarps < nchunks) prefetch(b + gwarps, (it + 1) & 1);
+        cp_async_commit();
+        cp_async_wait1();
+        __syncwarp();
+        const float* st = ring + (it & 1) * kFilterStageFloats;
+        const uint32_t i0 = b * kFilterBlock + lane * kFilterItems;
+        float4 v[11];
+#pragma unroll
+        for (int q = 0; q < 11; ++q) v[q] = *reinterpret_cast<const float4*>(st + q * kFilterBlock + lane * kFilterItems);
+#pragma unroll 1
+        for (int k = 0; k < m.nb; ++k) {
+            const PrepLaunch& a = m.p[k];
+            cull_chunk(a, filter_consts(a.slice, m.log_tau[k]), m.log_tau[k], m.filter_on[k], b, i0, v, sx, nullptr,
+                       st);
+        }
+        __syncwarp();
+    }
+}
+
 // ---- K_adam_cull -----------------------------------------------------------------
 // Training step: adam_step (optimize.hpp:195-221) fused with the NEXT slice's
 // K_filter. Both stream every parameter once; fused, the next step starts at
@@ -928,6 +988,55 @@ __global__ void __launch_bounds__(128) k_chain_exact(const ChainLaunch a) {
     }
 }
 
+// ---- PreparedGaussian in full (render.hpp:68-79) ----------------------------------
+// For the survivors listed by slot (set order), every field the reference's
+// prepare_gaussians fills, in the reference's own fp64 operation order
+// (focus_prepare; this TU is built --fmad=false): alpha, opacity_r,
+// alpha_tilde, mu_c, mu_e, sigma_c, sigma_c_inv, sigma_e, mu_2d, cov2d,
+// conic, det2 — 47 doubles per survivor (include/gpile_b200.h). Read-out only:
+// the pixel kernels use the 48 B SurvivorRecord.
+__global__ void __launch_bounds__(128) k_prepared_full(const CandParams* __restrict__ sparams,
+                                                       const uint32_t* __restrict__ slots, unsigned S,
+                                                       const SliceArgs s, double* __restrict__ out) {
+    const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= S) return;
+    float pf[11];
+    uint32_t idx;
+    load_cand(sparams + slots[k], pf, idx);
+    double pd[11];
+#pragma unroll
+    for (int t = 0; t < 11; ++t) pd[t] = (double)pf[t];
+    Focus f;
+    focus_prepare(pd, s, f);
+    D33 sigma, rot, sc;
+    D3 scale;
+    world_covariance(pd, s.mod, sigma, rot, scale);
+    if (s.identity_rot) {
+        sc = sigma;
+    } else {
+        D33 Rc;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) Rc.m[i / 3][i % 3] = s.R[i];
+        sc = m33_mul(m33_mul(Rc, sigma), m33_t(Rc));
+    }
+    double* o = out + 47ull * k;
+    o[0] = f.alpha;
+    o[1] = f.op;
+    o[2] = f.alpha_tilde;
+    o[3] = f.mu_c.x, o[4] = f.mu_c.y, o[5] = f.mu_c.z;
+    o[6] = f.mu_e.x, o[7] = f.mu_e.y, o[8] = f.mu_e.z;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        o[9 + i] = sc.m[i / 3][i % 3];
+        o[18 + i] = f.A.m[i / 3][i % 3];
+        o[27 + i] = f.Se.m[i / 3][i % 3];
+    }
+    o[36] = f.mu_e.x, o[37] = f.mu_e.y;  // mu_2d (render.hpp:53-56)
+    o[38] = f.cov_a, o[39] = f.cov_b, o[40] = f.cov_c, o[41] = f.cov_d;
+    o[42] = f.con_a, o[43] = f.con_b, o[44] = f.con_c, o[45] = f.con_d;
+    o[46] = f.det2;
+}
+
 // ---- voxelizer: prepare_voxel_prims + VoxelTiles (voxelize.hpp:52-105) ---------
 // Persistent CTAs take 256-primitive chunks in set order. Per primitive: the
 // world covariance and its inverse in the reference's fp64 order (support
@@ -1143,6 +1252,11 @@ __global__ void __launch_bounds__(128) k_vchain(const VoxChainLaunch a) {
 
 }  // namespace
 
+void launch_prepared_full(const CandParams* sparams, const uint32_t* slots, unsigned S, const SliceArgs& s,
+                          double* out, cudaStream_t st) {
+    if (S) k_prepared_full<<<(S + 127) / 128, 128, 0, st>>>(sparams, slots, S, s, out);
+}
+
 void launch_vox_prep(const VoxPrepLaunch& a, cudaStream_t st) {
     if (a.n) k_vprep<<<a.grid, 256, 0, st>>>(a);
 }
@@ -1169,6 +1283,28 @@ void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st) {
         launch_pdl(k_filter<true>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, filter_on ? 1 : 0);
     else
         launch_pdl(k_filter<false>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, filter_on ? 1 : 0);
+}
+
+void launch_prep_multi(const PrepLaunch* pl, int nb, int num_sms, cudaStream_t st) {
+    if (nb < 1 || pl[0].n == 0) return;
+    MultiPrep m;
+    m.nb = nb;
+    for (int k = 0; k < nb; ++k) {
+        m.p[k] = pl[k];
+        const SliceArgs& sl = pl[k].slice;
+        const bool on = sl.tau > 0.0 && sl.mod > 1e-10 && sl.mod < 1e10 && sl.sigma_z > 1e-10 && sl.sigma_z < 1e10;
+        m.filter_on[k] = on ? 1 : 0;
+        m.log_tau[k] = on ? (float)log(sl.tau) : 0.f;
+    }
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaFuncSetAttribute(k_filter_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFilterSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter_multi, kFilterThreads, kFilterSmem);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const uint64_t need = ((uint64_t)pl[0].nfilter * 32 + kFilterThreads - 1) / kFilterThreads;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms * per_sm));
+    launch_pdl(k_filter_multi, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, m);
 }
 
 void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& f, cudaStream_t st) {

@@ -61,14 +61,22 @@ int ok() {
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    bool borrowed = false;  // another session's memory (slice contexts share the parameters)
     void release() {
-        if (p) cudaFree(p);
+        if (p && !borrowed) cudaFree(p);
         p = nullptr;
         bytes = 0;
+        borrowed = false;
+    }
+    void borrow(const DevBuf& o) {
+        release();
+        p = o.p;
+        bytes = o.bytes;
+        borrowed = true;
     }
     // (Re)allocate to at least `need` bytes; contents are NOT preserved.
     cudaError_t ensure(size_t need) {
-        if (need <= bytes && p) return cudaSuccess;
+        if (need <= bytes && p && !borrowed) return cudaSuccess;
         release();
         if (need == 0) need = 16;
         cudaError_t e = cudaMalloc(&p, need);
@@ -167,6 +175,19 @@ struct gpk_session {
 
     PrepState prep;
 
+    // Slice contexts (batched steps, gpk_slice_context): context k >= 1 is a
+    // session of its own — stream, per-slice buffers, control head, error
+    // word — whose parameter, dense-gradient and Adam planes are this
+    // session's (borrowed). owner is set on a context.
+    gpk_session* owner = nullptr;
+    std::vector<gpk_session*> ctxs;
+    cudaEvent_t ev_bjoin = nullptr;  // a context's work of the batched step is done
+    cudaEvent_t ev_ord = nullptr;    // a context's copies: ordered after / before its session's stream
+    // the latest gradient is a batched step's: the slices' slot gradients of
+    // these sessions (slice order), summed on demand (materialize_dense_grads)
+    std::vector<gpk_session*> batch_srcs;
+    int ctx_used = 0;  // contexts a batched body used (graph capture snapshots their state)
+
     // voxelizer state (last voxelize / voxelize_backward)
     struct VoxState {
         bool valid = false;
@@ -181,9 +202,16 @@ struct gpk_session {
         int stage;
         cudaEvent_t a, b;
     };
+    struct CtxSnap {
+        gpk_session* ctx;
+        PrepState prep;
+        bool grads_in_slots, gmap_dirty;
+    };
     struct Graph {
         cudaGraphExec_t exec;
         PrepState prep;
+        std::vector<CtxSnap> ctx_state;       // batched graphs: the contexts' state they leave
+        std::vector<gpk_session*> batch_srcs;
         uint64_t alloc_epoch;
         bool needs_prefilter = false;  // pipelined train step: starts at K_decide
         bool sets_prefilter = false;   // ... and leaves next_pose culled
@@ -521,13 +549,15 @@ int clear_gmap(gpk_session* s) {
     c.gmap = s->gmap.as<uint16_t>();
     c.surv_gidx = s->survivors.as<uint32_t>();
     c.grp_surv = s->grp_surv();
-    launch_scatter_slot_grads(c, (unsigned)decide_group_count(s->n), false, s->stream);
+    launch_scatter_slot_grads(c, (unsigned)decide_group_count(s->n), kScatterClearMap, s->stream);
     CK(cudaGetLastError());
     return GPK_OK;
 }
 
+// filtered: K_filter's work for this slice was done already (k_filter_multi of
+// a batched step: candidates, control head and sort rows are in place).
 int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
-                const gpk_raster_config* cfg, bool zero_grads) {
+                const gpk_raster_config* cfg, bool zero_grads, bool filtered = false) {
     SliceArgs a;
     TRY(make_slice(s, pose, psf, cfg, a));
     TRY(ensure_image(s, a.W, a.H));
@@ -547,6 +577,13 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     ps.grads_zeroed = zero_grads;
     ps.ssim_pending = false;
     s->grads_in_slots = false;  // the survivor slots are about to change
+    {
+        gpk_session* o = s->owner ? s->owner : s;
+        if (std::find(o->batch_srcs.begin(), o->batch_srcs.end(), s) != o->batch_srcs.end()) {
+            o->batch_srcs.clear();  // a slice of the latest batched gradient is overwritten
+            o->grads_in_slots = false;
+        }
+    }
     const uint64_t nbf = filter_blocks(s->n);
     const size_t head_bytes = head_size(s->n);
     StageScope scope_prep(s, GPK_STAGE_PREPARE);
@@ -560,7 +597,9 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     // already produced this slice's candidates (and left the gradients zero)
     const bool pre = zero_grads && (s->assume_prefiltered || prefilter_matches(s, pose, psf, cfg));
     s->prefilter.valid = false;
-    if (!pre) {
+    if (filtered) {
+        // k_filter_multi culled this slice and zeroed its control head
+    } else if (!pre) {
         // K_filter zeroes the control head itself (K_decide is the first to use it)
         pl.head = s->head.as<unsigned>();
         pl.head_words = (unsigned)(head_bytes / 4);
@@ -766,12 +805,12 @@ int run_backward(gpk_session* s, bool stats, bool slots = false) {
 // U1 with dL/dI already in GPK_BUF_DL_DI: the forward does not feed the
 // backward, so it runs on the side stream while the backward (+ chain) runs on
 // the session stream; the session stream then waits for the forward.
-int run_fwd_bwd_forked(gpk_session* s) {
+int run_fwd_bwd_forked(gpk_session* s, bool slots = false) {
     CK(cudaEventRecord(s->ev_fork, s->stream));
     CK(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
     TRY(run_rasterize(s, s->side));
     CK(cudaEventRecord(s->ev_join, s->side));
-    TRY(run_backward(s, false));
+    TRY(run_backward(s, false, slots));
     CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
     return GPK_OK;
 }
@@ -834,7 +873,34 @@ int accum_alloc_zero(gpk_session* s) {
     return GPK_OK;
 }
 
+// Per-slice buffers sized for a plane stride `cap` (survivor records, candidates,
+// K_decide tables, slot gradients and their map, the control head).
+int alloc_slice_bufs(gpk_session* s, uint64_t cap) {
+    const uint64_t nbf = filter_blocks(cap);
+    CK(s->records.ensure(cap * sizeof(SurvivorRecord)));
+    CK(s->cand_list.ensure(cap * 4));
+    CK(s->surv_params.ensure(cap * sizeof(CandParams)));
+    CK(s->grp_table.ensure((cap / kDecideGroupSize + 2) * 12));
+    CK(s->bucket_tab.ensure((cap / kDecideGroupSize + 2) * (kMaxBuckets + 1) * 4));
+    CK(s->cand.ensure(cap * sizeof(CandParams)));
+    CK(s->cand_count.ensure(nbf * 4));
+    CK(s->dirty_idx.ensure(cap * 4));
+    CK(s->slot_grads.ensure(cap * 11 * 4));
+    CK(s->gmap.ensure(cap * 2));
+    CK(cudaMemsetAsync(s->gmap.p, 0, cap * 2, s->stream));
+    s->grads_in_slots = false;
+    s->gmap_dirty = false;
+    TRY(mark_grads_dense(s));
+    CK(s->survivors.ensure(cap * 4));
+    CK(s->head.ensure(head_size(cap)));
+    s->cap = cap;
+    ++s->alloc_epoch;
+    if (s->keys[0].p) TRY(size_sort_status(s));  // more K_decide groups than sort-tile rows
+    return GPK_OK;
+}
+
 int alloc_for_n(gpk_session* s, uint64_t n) {
+    if (s->owner) return fail(GPK_ERR_STATE, "slice context: the Gaussian set belongs to its session");
     // plane stride: a multiple of the K_filter chunk, so every chunk's plane
     // slice is a 4 KB, 16 B-aligned TMA bulk-copy source/destination
     const uint64_t cap = (std::max<uint64_t>(n, 1) + kParamAlign - 1) / kParamAlign * kParamAlign;
@@ -843,26 +909,7 @@ int alloc_for_n(gpk_session* s, uint64_t n) {
         CK(s->grads.ensure(cap * 11 * 4));
         CK(s->adam_m.ensure(cap * 11 * 4));
         CK(s->adam_v.ensure(cap * 11 * 4));
-        const uint64_t nbf = filter_blocks(cap);
-        CK(s->records.ensure(cap * sizeof(SurvivorRecord)));
-        CK(s->cand_list.ensure(cap * 4));
-        CK(s->surv_params.ensure(cap * sizeof(CandParams)));
-        CK(s->grp_table.ensure((cap / kDecideGroupSize + 2) * 12));
-        CK(s->bucket_tab.ensure((cap / kDecideGroupSize + 2) * (kMaxBuckets + 1) * 4));
-        CK(s->cand.ensure(cap * sizeof(CandParams)));
-        CK(s->cand_count.ensure(nbf * 4));
-        CK(s->dirty_idx.ensure(cap * 4));
-        CK(s->slot_grads.ensure(cap * 11 * 4));
-        CK(s->gmap.ensure(cap * 2));
-        CK(cudaMemsetAsync(s->gmap.p, 0, cap * 2, s->stream));
-        s->grads_in_slots = false;
-        s->gmap_dirty = false;
-        TRY(mark_grads_dense(s));
-        CK(s->survivors.ensure(cap * 4));
-        CK(s->head.ensure(head_size(cap)));
-        s->cap = cap;
-        ++s->alloc_epoch;
-        if (s->keys[0].p) TRY(size_sort_status(s));  // more K_decide groups than sort-tile rows
+        TRY(alloc_slice_bufs(s, cap));
     }
     if (n != s->n) ++s->alloc_epoch;  // captured graphs bake the set size
     s->n = n;
@@ -898,6 +945,26 @@ int adam_grad_source(gpk_session* s, AdamLaunch& a) {
 int materialize_dense_grads(gpk_session* s) {
     if (!s->grads_in_slots) return GPK_OK;
     s->grads_in_slots = false;
+    if (!s->batch_srcs.empty()) {
+        // a batched step's gradient: the slices' slot gradients added in slice
+        // order (the same fp32 sums its Adam formed)
+        if (s->capturing) return fail(GPK_ERR_STATE, "gradient layout change during capture");
+        std::vector<gpk_session*> srcs;
+        srcs.swap(s->batch_srcs);
+        CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
+        for (gpk_session* c : srcs) {
+            if (!c->prep.valid || c->n == 0) continue;
+            AdamLaunch a{};
+            a.grads = s->grads.as<float>();
+            a.cap = s->cap;
+            a.slot_grads = c->slot_grads.as<float>();
+            a.surv_gidx = c->survivors.as<uint32_t>();
+            a.grp_surv = c->grp_surv();
+            launch_scatter_slot_grads(a, (unsigned)decide_group_count(c->n), kScatterAdd, s->stream);
+            CK(cudaGetLastError());
+        }
+        return mark_grads_dense(s);
+    }
     if (!s->prep.valid || s->n == 0) return GPK_OK;
     if (s->capturing) return fail(GPK_ERR_STATE, "gradient layout change during capture");
     CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
@@ -907,7 +974,7 @@ int materialize_dense_grads(gpk_session* s) {
     a.slot_grads = s->slot_grads.as<float>();
     a.surv_gidx = s->survivors.as<uint32_t>();
     a.grp_surv = s->grp_surv();
-    launch_scatter_slot_grads(a, (unsigned)decide_group_count(s->n), true, s->stream);
+    launch_scatter_slot_grads(a, (unsigned)decide_group_count(s->n), kScatterSet, s->stream);
     CK(cudaGetLastError());
     return mark_grads_dense(s);
 }
@@ -962,6 +1029,7 @@ int adam_consts_ready(gpk_session* s, const AdamLaunch& a) {
 // lo, hi: the primitives to update (a data-parallel rank's shard), default all
 int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
              const gpk_adam_hparams* hp, uint64_t lo = 0, uint64_t hi = ~0ull) {
+    if (s->owner) return fail(GPK_ERR_STATE, "slice context: Adam runs on its session");
     if (s->n == 0) {
         s->consts_pending = false;
         long long st = 0;
@@ -1237,6 +1305,8 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->copy, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_bjoin, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_ord, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) {
         gpk_session_destroy(s);
@@ -1250,10 +1320,19 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     return ok();
 }
 
+static int session_destroy(gpk_session* s);
+
 int gpk_session_destroy(gpk_session* s) {
+    if (s && s->owner) return fail(GPK_ERR_STATE, "a slice context is destroyed with its session");
+    return session_destroy(s);
+}
+
+static int session_destroy(gpk_session* s) {
     if (!s) return ok();
     cudaSetDevice(s->device);
     if (s->stream) cudaStreamSynchronize(s->stream);
+    for (gpk_session* c : s->ctxs) session_destroy(c);  // their borrowed planes are not freed
+    s->ctxs.clear();
     for (auto& g : s->graphs) {
         cudaGraphExecDestroy(g.exec);
         for (auto& p : g.timed) {
@@ -1288,6 +1367,8 @@ int gpk_session_destroy(gpk_session* s) {
     }
     if (s->ev_tgt_fork) cudaEventDestroy(s->ev_tgt_fork);
     if (s->ev_tgt_ready) cudaEventDestroy(s->ev_tgt_ready);
+    if (s->ev_bjoin) cudaEventDestroy(s->ev_bjoin);
+    if (s->ev_ord) cudaEventDestroy(s->ev_ord);
     if (s->comm) gpk_comm_destroy(s);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
@@ -1313,6 +1394,7 @@ int gpk_session_get_stream(gpk_session* s, void** cuda_stream) {
 int gpk_session_synchronize(gpk_session* s) {
     if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
     TRY(set_device(s));
+    if (s->owner) CK(cudaStreamSynchronize(s->owner->stream));  // batched steps run there
     TRY(sync_and_check(s, "session"));
     if (s->prep.valid) {
         Control c;
@@ -1366,6 +1448,23 @@ int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
     return ok();
 }
 
+// A context's stream-ordered copies are ordered on both its own stream (its
+// direct calls) and its session's stream (where batched steps and their graphs
+// run): the context stream first waits for the session stream, and the
+// session stream afterwards waits for the copy.
+static int ctx_order_in(gpk_session* s) {
+    if (!s->owner || s->capturing) return GPK_OK;
+    CK(cudaEventRecord(s->owner->ev_ord, s->owner->stream));
+    CK(cudaStreamWaitEvent(s->stream, s->owner->ev_ord, 0));
+    return GPK_OK;
+}
+static int ctx_order_out(gpk_session* s, cudaStream_t copied_on) {
+    if (!s->owner || s->capturing) return GPK_OK;
+    CK(cudaEventRecord(s->ev_ord, copied_on));
+    CK(cudaStreamWaitEvent(s->owner->stream, s->ev_ord, 0));
+    return GPK_OK;
+}
+
 int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes) {
     if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
     // image-shaped inputs may be staged before the first slice sized them
@@ -1384,10 +1483,12 @@ int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes) {
     if (grow) cap = grow->bytes;
     if (!host || bytes > cap) return fail(GPK_ERR_INVALID_ARGUMENT, "upload: size exceeds buffer");
     TRY(set_device(s));
+    TRY(ctx_order_in(s));
     if (which == GPK_BUF_TARGET && !s->capturing) {
         // after everything already queued on the session stream (earlier
         // readers of the target), on the copy stream: the transfer overlaps
         // the next step's prepare and forward, which do not read the target
+        // (a context's readers may run on its session's stream: ctx_order_in)
         CK(cudaEventRecord(s->ev_tgt_fork, s->stream));
         CK(cudaStreamWaitEvent(s->copy, s->ev_tgt_fork, 0));
         CK(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, s->copy));
@@ -1396,6 +1497,7 @@ int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes) {
         return ok();
     }
     CK(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, s->stream));
+    TRY(ctx_order_out(s, s->stream));
     return ok();
 }
 
@@ -1405,7 +1507,9 @@ int gpk_download(gpk_session* s, int which, void* host, uint64_t bytes) {
     TRY(gpk_device_buffer(s, which, &p, &cap));
     if (!host || bytes > cap) return fail(GPK_ERR_INVALID_ARGUMENT, "download: size exceeds buffer");
     TRY(set_device(s));
+    TRY(ctx_order_in(s));
     CK(cudaMemcpyAsync(host, p, bytes, cudaMemcpyDeviceToHost, s->stream));
+    TRY(ctx_order_out(s, s->stream));
     return ok();
 }
 
@@ -1561,6 +1665,29 @@ int gpk_get_prepared(gpk_session* s, uint32_t* index, int32_t* bounds, double* f
             f[5] = r.conic_d;
         }
     }
+    return ok();
+}
+
+int gpk_get_prepared_fields(gpk_session* s, double* fields) {
+    uint64_t S = 0, T = 0;
+    TRY(gpk_prepared_count(s, &S, &T));
+    if (S == 0 || !fields) return ok();
+    const uint64_t ng = decide_group_count(s->n);
+    std::vector<uint32_t> per(ng), list;
+    CK(cudaMemcpy(per.data(), s->grp_surv(), ng * 4, cudaMemcpyDeviceToHost));
+    list.reserve(S);
+    for (uint64_t g = 0; g < ng; ++g)
+        for (uint32_t j = 0; j < per[g]; ++j) list.push_back((uint32_t)(g * kDecideGroupSize + j));
+    if (list.size() != S) return fail(GPK_ERR_STATE, "prepared: survivor bookkeeping mismatch");
+    DevBuf slots, out;
+    CK(slots.ensure(S * 4));
+    CK(out.ensure(S * GPK_PREPARED_FIELDS * 8));
+    CK(cudaMemcpyAsync(slots.p, list.data(), S * 4, cudaMemcpyHostToDevice, s->stream));
+    launch_prepared_full(s->surv_params.as<CandParams>(), slots.as<uint32_t>(), (unsigned)S, s->prep.slice,
+                         out.as<double>(), s->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(fields, out.p, S * GPK_PREPARED_FIELDS * 8, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
     return ok();
 }
 
@@ -1823,6 +1950,210 @@ int gpk_train_step_next(gpk_session* s, const gpk_slice_pose* pose, const gpk_ps
     return ok();
 }
 
+// ---- slice contexts and batched steps -----------------
+// A batched step renders B slices of the resident set concurrently — slice k on
+// context k (its own stream and per-slice buffers; context 0 is the session
+// itself) — and sums their gradients per primitive in slice order: inside the
+// one Adam of the training step (k_adam_batch reads every slice's slot map), or
+// into the dense planes for the fwd+bwd unit. Launch-latency-bound slice
+// kernels (a 512^2 slice is 1024 tiles, ~7 CTAs per SM) of different slices
+// then overlap on the GPU instead of running one after another.
+
+static int ctx_sync(gpk_session* s, gpk_session* c) {
+    if (c->params.p != s->params.p || c->adam_m.p != s->adam_m.p) {
+        c->params.borrow(s->params);
+        c->grads.borrow(s->grads);
+        c->adam_m.borrow(s->adam_m);
+        c->adam_v.borrow(s->adam_v);
+        ++c->alloc_epoch;
+    }
+    c->bbox = s->bbox;
+    if (c->n != s->n) {
+        TRY(clear_gmap(c));  // the old slots' map entries (before the set size changes)
+        c->prep.valid = false;
+        c->n = s->n;
+        ++c->alloc_epoch;
+    }
+    if (c->cap != s->cap) TRY(alloc_slice_bufs(c, s->cap));
+    return GPK_OK;
+}
+
+static int ctx_get(gpk_session* s, int k, gpk_session** out) {
+    if (s->owner) return fail(GPK_ERR_STATE, "slice contexts belong to a session, not to a context");
+    if (k < 0 || k >= kMaxBatch) return fail(GPK_ERR_INVALID_ARGUMENT, "slice context index out of range [0, 8)");
+    if (k == 0) {
+        *out = s;
+        return GPK_OK;
+    }
+    while ((int)s->ctxs.size() < k) {
+        if (s->capturing) return fail(GPK_ERR_STATE, "slice contexts must exist before capture");
+        gpk_session* c = nullptr;
+        TRY(gpk_session_create(s->device, nullptr, &c));
+        c->owner = s;
+        s->ctxs.push_back(c);
+    }
+    gpk_session* c = s->ctxs[k - 1];
+    if (s->capturing && (c->params.p != s->params.p || c->n != s->n || c->cap != s->cap))
+        return fail(GPK_ERR_STATE, "slice context out of date during capture");
+    TRY(ctx_sync(s, c));
+    *out = c;
+    return GPK_OK;
+}
+
+static uint64_t epoch_total(gpk_session* s) {
+    uint64_t e = s->alloc_epoch;
+    for (gpk_session* c : s->ctxs) e += c->alloc_epoch;
+    return e;
+}
+
+static int batch_check(gpk_session* s, int B, const gpk_slice_pose* poses) {
+    if (!s || !poses) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (s->owner) return fail(GPK_ERR_STATE, "batched steps run on the session, not on a context");
+    if (B < 1 || B > kMaxBatch) return fail(GPK_ERR_INVALID_ARGUMENT, "batch of 1..8 slices");
+    if (s->accum_on && B > 1)
+        return fail(GPK_ERR_STATE, "densify accumulation is per slice: batched steps need it disabled");
+    return GPK_OK;
+}
+
+static int presize_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
+                        const gpk_raster_config* cfg, bool loss, double lambda);
+
+// The batch's K_filter work in one pass over the parameters (k_filter_multi),
+// on the session stream before the fork: every slice's candidates, control
+// head and sort rows. Buffers are sized first (outside capture).
+static int batch_filter(gpk_session* s, gpk_session* const* cx, int B, const gpk_slice_pose* poses,
+                        const gpk_psf* psf, const gpk_raster_config* cfg, bool loss, double lambda) {
+    if (!s->capturing)  // the contexts' own queued work (direct calls) precedes the batch
+        for (int k = 1; k < B; ++k) {
+            CK(cudaEventRecord(cx[k]->ev_bjoin, cx[k]->stream));
+            CK(cudaStreamWaitEvent(s->stream, cx[k]->ev_bjoin, 0));
+        }
+    PrepLaunch pl[kMaxBatch];
+    for (int k = 0; k < B; ++k) {
+        gpk_session* c = cx[k];
+        TRY(presize_step(c, &poses[k], psf, cfg, loss, lambda));
+        SliceArgs a;
+        TRY(make_slice(c, &poses[k], psf, cfg, a));
+        int passes = 0, bits = 0;
+        sort_plan(a.tiles_x * a.tiles_y, passes, bits);
+        if (a.tiles_x * a.tiles_y > (1 << (kMaxDigitBits * kMaxSortPasses)))
+            return fail(GPK_ERR_INVALID_ARGUMENT, "SlicePose: more than 2^20 tiles unsupported");
+        pl[k] = prep_launch(c, a, passes, bits, false);
+        pl[k].head = c->head.as<unsigned>();
+        pl[k].head_words = (unsigned)(head_size(c->n) / 4);
+    }
+    if (s->n == 0) return GPK_OK;
+    StageScope scope(s, GPK_STAGE_PREPARE);
+    launch_prep_multi(pl, B, s->num_sms, s->stream);
+    CK(cudaGetLastError());
+    return GPK_OK;
+}
+
+// Fork the contexts of slices 1..B-1 off the session stream.
+static int batch_fork(gpk_session* s, gpk_session* const* cx, int B) {
+    CK(cudaEventRecord(s->ev_fork, s->stream));
+    for (int k = 1; k < B; ++k) {
+        CK(cudaStreamWaitEvent(cx[k]->stream, s->ev_fork, 0));
+        cx[k]->capturing = s->capturing;
+    }
+    return GPK_OK;
+}
+
+static int batch_join(gpk_session* s, gpk_session* const* cx, int B) {
+    for (int k = 1; k < B; ++k) {
+        CK(cudaEventRecord(cx[k]->ev_bjoin, cx[k]->stream));
+        CK(cudaStreamWaitEvent(s->stream, cx[k]->ev_bjoin, 0));
+        cx[k]->capturing = false;
+    }
+    return GPK_OK;
+}
+
+// The B slices' gradients summed into the dense planes (slice order), their
+// maps consumed.
+static int batch_dense_sum(gpk_session* s, gpk_session* const* cx, int B) {
+    CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
+    for (int k = 0; k < B; ++k) {
+        gpk_session* c = cx[k];
+        AdamLaunch a{};
+        a.grads = s->grads.as<float>();
+        a.cap = s->cap;
+        a.slot_grads = c->slot_grads.as<float>();
+        a.surv_gidx = c->survivors.as<uint32_t>();
+        a.grp_surv = c->grp_surv();
+        a.gmap = c->gmap.as<uint16_t>();
+        launch_scatter_slot_grads(a, (unsigned)decide_group_count(c->n), kScatterAdd | kScatterClearMap, s->stream);
+        CK(cudaGetLastError());
+        c->gmap_dirty = false;
+        c->grads_in_slots = false;
+    }
+    s->batch_srcs.clear();
+    s->grads_in_slots = false;
+    return mark_grads_dense(s);
+}
+
+// U1 x B: per slice prepare, then its forward (context side stream) beside its
+// backward of the slice's GPK_BUF_DL_DI (slot gradients); the dense gradient
+// is the sum over the slices.
+static int fwd_bwd_batch_body(gpk_session* s, int B, const gpk_slice_pose* poses, const gpk_psf* psf,
+                              const gpk_raster_config* cfg) {
+    gpk_session* cx[kMaxBatch];
+    for (int k = 0; k < B; ++k) TRY(ctx_get(s, k, &cx[k]));
+    s->ctx_used = B - 1;
+    TRY(batch_filter(s, cx, B, poses, psf, cfg, false, 0.0));
+    TRY(batch_fork(s, cx, B));
+    for (int k = 0; k < B; ++k) {
+        TRY(run_prepare(cx[k], &poses[k], psf, cfg, false, /*filtered=*/true));
+        TRY(run_fwd_bwd_forked(cx[k], /*slots=*/true));
+    }
+    TRY(batch_join(s, cx, B));
+    return batch_dense_sum(s, cx, B);
+}
+
+// U2 x B: every slice prepared, rendered, its loss (its context's target) and
+// backward taken; one Adam over the summed gradient (k_adam_batch).
+static int train_batch_body(gpk_session* s, int B, const gpk_slice_pose* poses, const gpk_psf* psf,
+                            const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                            const gpk_learning_rates* lr0, int32_t total) {
+    const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
+    gpk_session* cx[kMaxBatch];
+    for (int k = 0; k < B; ++k) TRY(ctx_get(s, k, &cx[k]));
+    s->ctx_used = B - 1;
+    if (s->n) TRY(adam_consts_ahead(s, adam_launch(s, lr, true, total, nullptr)));
+    TRY(batch_filter(s, cx, B, poses, psf, cfg, true, lambda));
+    TRY(batch_fork(s, cx, B));
+    for (int k = 0; k < B; ++k) {
+        gpk_session* c = cx[k];
+        c->fuse_gather = true;
+        const int pst = run_prepare(c, &poses[k], psf, cfg, false, /*filtered=*/true);
+        c->fuse_gather = false;
+        TRY(pst);
+        TRY(run_rasterize(c));
+        TRY(run_loss(c, lambda, dssim_scale, true));
+        TRY(run_backward(c, false, /*slots=*/true));
+    }
+    TRY(batch_join(s, cx, B));
+    if (s->n == 0) return run_adam(s, lr, true, total, nullptr);
+    AdamLaunch a = adam_launch(s, lr, true, total, nullptr);
+    a.slot_grads = cx[0]->slot_grads.as<float>();
+    a.gmap = cx[0]->gmap.as<uint16_t>();
+    a.ctrl = cx[0]->ctrl();
+    a.nsrc = B - 1;
+    for (int k = 1; k < B; ++k) {
+        a.src_slot[k - 1] = cx[k]->slot_grads.as<float>();
+        a.src_gmap[k - 1] = cx[k]->gmap.as<uint16_t>();
+        a.src_ctrl[k - 1] = cx[k]->ctrl();
+    }
+    for (int k = 0; k < B; ++k) cx[k]->gmap_dirty = false;  // k_adam_batch consumes every map
+    s->batch_srcs.assign(cx, cx + B);
+    s->grads_in_slots = true;
+    s->prefilter.valid = false;
+    StageScope scope(s, GPK_STAGE_ADAM);
+    TRY(adam_consts_ready(s, a));
+    launch_adam_batch(a, s->stream);
+    CK(cudaGetLastError());
+    return GPK_OK;
+}
+
 // ---- CUDA graphs -------------------------------------------------------------
 static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_session*, const void*),
                          const void* arg) {
@@ -1834,8 +2165,10 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
     drain_timing(s);
     CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
     s->capturing = true;
+    s->ctx_used = 0;
     const int st = body(s, arg);
     s->capturing = false;
+    for (gpk_session* c : s->ctxs) c->capturing = false;
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(s->stream, &g);
     // stage events recorded during capture became event-record nodes of the graph
@@ -1861,7 +2194,12 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
     gr.prep = s->prep;
     gr.grads_in_slots = s->grads_in_slots;
     gr.gmap_dirty = s->gmap_dirty;
-    gr.alloc_epoch = s->alloc_epoch;
+    gr.alloc_epoch = epoch_total(s);
+    for (int k = 0; k < s->ctx_used; ++k) {
+        gpk_session* c = s->ctxs[k];
+        gr.ctx_state.push_back({c, c->prep, c->grads_in_slots, c->gmap_dirty});
+    }
+    gr.batch_srcs = s->batch_srcs;
     gr.timed = std::move(timed);
     gr.needs_prefilter = meta.needs_prefilter;
     gr.sets_prefilter = meta.sets_prefilter;
@@ -1966,12 +2304,91 @@ int gpk_graph_capture_train_next(gpk_session* s, const gpk_slice_pose* pose, con
     return st;
 }
 
+// ---- batched steps: C-ABI ---------------------------------------------------------
+struct BatchArgs {
+    int B;
+    const gpk_slice_pose* poses;
+    const gpk_psf* psf;
+    const gpk_raster_config* cfg;
+    double lambda, dssim;
+    const gpk_learning_rates* lr0;
+    int total;
+};
+
+static int presize_batch(gpk_session* s, const BatchArgs& b, bool loss) {
+    for (int k = 0; k < b.B; ++k) {
+        gpk_session* c = nullptr;
+        TRY(ctx_get(s, k, &c));
+        TRY(presize_step(c, &b.poses[k], b.psf, b.cfg, loss, b.lambda));
+    }
+    return GPK_OK;
+}
+
+int gpk_slice_context(gpk_session* s, int32_t k, gpk_session** ctx) {
+    if (!s || !ctx) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    TRY(set_device(s));
+    TRY(ctx_get(s, k, ctx));
+    return ok();
+}
+
+int gpk_fwd_bwd_batch(gpk_session* s, int32_t nslices, const gpk_slice_pose* poses, const gpk_psf* psf,
+                      const gpk_raster_config* cfg) {
+    TRY(batch_check(s, nslices, poses));
+    TRY(set_device(s));
+    TRY(fwd_bwd_batch_body(s, nslices, poses, psf, cfg));
+    return ok();
+}
+
+int gpk_train_step_batch(gpk_session* s, int32_t nslices, const gpk_slice_pose* poses, const gpk_psf* psf,
+                         const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                         const gpk_learning_rates* lr0, int32_t total_iterations) {
+    TRY(batch_check(s, nslices, poses));
+    if (!lr0 || total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "bad learning rates");
+    if (session_comm(s)) return fail(GPK_ERR_STATE, "batched step under a communicator: not supported");
+    TRY(set_device(s));
+    const int st = train_batch_body(s, nslices, poses, psf, cfg, lambda, dssim_scale, lr0, total_iterations);
+    if (st != GPK_OK) s->consts_pending = false;
+    TRY(st);
+    return ok();
+}
+
+int gpk_graph_capture_fwd_bwd_batch(gpk_session* s, int32_t nslices, const gpk_slice_pose* poses,
+                                    const gpk_psf* psf, const gpk_raster_config* cfg, int32_t* graph_id) {
+    TRY(batch_check(s, nslices, poses));
+    TRY(set_device(s));
+    const BatchArgs args{nslices, poses, psf, cfg, 0.0, 0.0, nullptr, 1};
+    TRY(presize_batch(s, args, false));
+    return capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
+        const BatchArgs* a = static_cast<const BatchArgs*>(p);
+        return fwd_bwd_batch_body(ss, a->B, a->poses, a->psf, a->cfg);
+    }, &args);
+}
+
+int gpk_graph_capture_train_batch(gpk_session* s, int32_t nslices, const gpk_slice_pose* poses,
+                                  const gpk_psf* psf, const gpk_raster_config* cfg, double lambda,
+                                  double dssim_scale, const gpk_learning_rates* lr0, int32_t total_iterations,
+                                  int32_t* graph_id) {
+    TRY(batch_check(s, nslices, poses));
+    if (!lr0 || total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "bad learning rates");
+    if (session_comm(s)) return fail(GPK_ERR_STATE, "batched step under a communicator: not supported");
+    TRY(set_device(s));
+    const BatchArgs args{nslices, poses, psf, cfg, lambda, dssim_scale, lr0, total_iterations};
+    TRY(presize_batch(s, args, true));
+    s->capture_meta.writes_params = true;
+    return capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
+        const BatchArgs* a = static_cast<const BatchArgs*>(p);
+        const int st = train_batch_body(ss, a->B, a->poses, a->psf, a->cfg, a->lambda, a->dssim, a->lr0, a->total);
+        if (st != GPK_OK) ss->consts_pending = false;
+        return st;
+    }, &args);
+}
+
 int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
     if (!s || graph_id < 0 || graph_id >= (int32_t)s->graphs.size())
         return fail(GPK_ERR_INVALID_ARGUMENT, "unknown graph id");
     TRY(set_device(s));
     gpk_session::Graph& g = s->graphs[graph_id];
-    if (g.alloc_epoch != s->alloc_epoch)
+    if (g.alloc_epoch != epoch_total(s))
         return fail(GPK_ERR_STATE, "graph invalidated: session buffers were reallocated since capture; recapture");
     if (g.needs_prefilter && !prefilter_matches(s, &g.prep.pose, &g.prep.psf, &g.prep.cfg)) {
         // the graph starts at K_decide: cull its slice first (stand-alone K_filter,
@@ -1991,6 +2408,12 @@ int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
     s->prep = g.prep;
     s->grads_in_slots = g.grads_in_slots;
     s->gmap_dirty = g.gmap_dirty;
+    for (const auto& cs : g.ctx_state) {
+        cs.ctx->prep = cs.prep;
+        cs.ctx->grads_in_slots = cs.grads_in_slots;
+        cs.ctx->gmap_dirty = cs.gmap_dirty;
+    }
+    s->batch_srcs = g.batch_srcs;
     if (s->timing && !g.timed.empty()) {
         // graph captured with stage timing: its event nodes bracket each stage
         // on the device, back to back (no host submission gaps)

@@ -124,6 +124,52 @@ int main() {
     expect(adam_ok, "adam_step parameters within fp32 tolerance");
     expect(b200::lr_at(6e-4, 7, 30) == lr_at(6e-4, 7, 30), "lr_at identical");
 
+    // every PreparedGaussian field (render.hpp:68-79), reference fp64 order
+    {
+        auto close = [](double a, double b) { return std::fabs(a - b) <= 1e-9 * std::fabs(b) + 1e-12; };
+        bool ok = prep_ref.size() == prep_gpu.size();
+        for (std::size_t k = 0; ok && k < prep_ref.size(); ++k) {
+            const PreparedGaussian &r = prep_ref[k], &g = prep_gpu[k];
+            ok = close(g.alpha, r.alpha) && close(g.opacity_r, r.opacity_r) && close(g.alpha_tilde, r.alpha_tilde) &&
+                 close(g.det2, r.det2);
+            for (int i = 0; i < 3 && ok; ++i) ok = close(g.mu_c[i], r.mu_c[i]) && close(g.mu_e[i], r.mu_e[i]);
+            for (int i = 0; i < 9 && ok; ++i)
+                ok = close(g.sigma_c.m[i / 3][i % 3], r.sigma_c.m[i / 3][i % 3]) &&
+                     close(g.sigma_c_inv.m[i / 3][i % 3], r.sigma_c_inv.m[i / 3][i % 3]) &&
+                     close(g.sigma_e.m[i / 3][i % 3], r.sigma_e.m[i / 3][i % 3]);
+            ok = ok && close(g.mu_2d.x, r.mu_2d.x) && close(g.mu_2d.y, r.mu_2d.y) && close(g.cov2d.a, r.cov2d.a) &&
+                 close(g.cov2d.b, r.cov2d.b) && close(g.cov2d.c, r.cov2d.c) && close(g.cov2d.d, r.cov2d.d) &&
+                 close(g.conic.a, r.conic.a) && close(g.conic.b, r.conic.b) && close(g.conic.c, r.conic.c) &&
+                 close(g.conic.d, r.conic.d);
+        }
+        expect(ok, "PreparedGaussian: every field within 1e-9 rel");
+    }
+
+    // two prepared slices held at once, used in any order (the drop-in
+    // re-binds an older vector on the device)
+    {
+        const SlicePose pa = slice_pose_for_index(vol, 6), pb = slice_pose_for_index(vol, 17);
+        const auto ra = prepare_gaussians(set, pa, psf, cfg);
+        const auto rb = prepare_gaussians(set, pb, psf, cfg);
+        const auto ga = b200::prepare_gaussians(set, pa, psf, cfg);
+        const auto gb = b200::prepare_gaussians(set, pb, psf, cfg);
+        bool ok = images_close(b200::rasterize_prepared(ga, pa, cfg), rasterize_prepared(ra, pa, cfg));
+        ok = ok && images_close(b200::rasterize_prepared(gb, pb, cfg), rasterize_prepared(rb, pb, cfg));
+        SliceImage dla(pa.width, pa.height);
+        for (std::size_t i = 0; i < dla.size(); ++i) dla.pixels[i] = (double)(float)(std::cos(0.11 * i) / dla.size());
+        ok = ok && grads_close(b200::backward_prepared(set, ga, pa, dla, cfg), backward_prepared(set, ra, pa, dla, cfg));
+        ok = ok && images_close(b200::rasterize_prepared(gb, pb, cfg), rasterize_prepared(rb, pb, cfg));
+        expect(ok, "rasterize/backward_prepared on an older prepared vector");
+        bool threw = false;
+        try {
+            std::vector<PreparedGaussian> foreign = ra;  // not returned by the drop-in
+            (void)b200::rasterize_prepared(foreign, pa, cfg);
+        } catch (const std::logic_error&) {
+            threw = true;
+        }
+        expect(threw, "a vector the drop-in did not return -> std::logic_error");
+    }
+
     // rasterize_slice / backward_slice, random pose, tau = 0 (test_grad.cpp:128-177)
     Rng rng(5);
     GaussianSet small;

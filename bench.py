@@ -54,7 +54,10 @@ CONFIGS = {
                name="ABUS-like 256x256x320 volume, thick-slice PSF sigma_z=3, 500k Gaussians"),
     "c5": dict(dims=(2048, 2048, 256), n=8_000_000, sigma_z=1.0,
                name="large microscopy 2048x2048x256 stack, 8M Gaussians, sigma_z=1"),
+    "c4": dict(dims=(512, 512, 512), n=1_000_000, sigma_z=1.0,
+               name="3D voxelization of a 1M-Gaussian set to a 512^3 grid (8^3 tiles, support 3 sigma)"),
 }
+VOXEL_METRIC = "voxelizations/s of 1M Gaussians to 512^3 (bit-exact tile binning); % MUFU ex2 roofline"
 UNITS = {
     "u2": "U2 training step: prepare + bin + rasterize + photometric loss (lambda 0.2, SSIM) + backward "
           "+ scheduled Adam, one slice",
@@ -345,6 +348,138 @@ def sort_passes(X, Y):
     tiles = ((X + 15) // 16) * ((Y + 15) // 16)
     bits = max(1, (tiles - 1).bit_length())
     return (bits + 9) // 10
+
+
+def run_voxel(args, impl):
+    """C4: voxelize (voxelize.hpp:113-148) of the 1M init_random
+    set on a 512^3 unit grid. One step = one voxelize call (primitive prep +
+    8^3-tile binning + per-tile evaluation of every voxel of every touched tile,
+    the reference's loop). The evaluation is MUFU-bound: one ex2 per (voxel,
+    primitive) of a touched tile; its roofline is the ex2 rate."""
+    import ctypes as C
+
+    cfg = CONFIGS["c4"]
+    X, Y, Z = cfg["dims"]
+    V = X * Y * Z
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    base = {"metric": VOXEL_METRIC, "unit": "voxelizations/s", "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "data": "synthetic (init_random seed 1 over the grid's world bounds)",
+            "config": {"workload": cfg["name"], "dims": [X, Y, Z], "gaussians": cfg["n"], "tile": [8, 8, 8],
+                       "support_sigmas": 3.0, "config_id": "c4",
+                       "parallelism": "replicas only (one voxelization per GPU)"}}
+
+    def ref_rate(threads, seconds):
+        from oracle.bindings import VcfgC, load
+
+        ref = load("ref")
+        L = ref.lib
+        L.gref_set_threads(threads)
+        workers = L.gref_effective_workers()
+        rec = make_records(cfg, via_reference=True)
+        h = ref._set(rec, geometry(cfg))
+        vc = VcfgC((C.c_int32 * 3)(X, Y, Z), (C.c_double * 3)(1, 1, 1), (C.c_double * 3)(0, 0, 0),
+                   (C.c_int32 * 3)(8, 8, 8), 3.0, 1.0)
+        secs = C.c_double()
+        L.gref_time_voxelize.argtypes = [C.c_void_p, C.POINTER(VcfgC), C.c_int, C.POINTER(C.c_double)]
+        if L.gref_time_voxelize(C.c_void_p(h.h), C.byref(vc), 1, C.byref(secs)) != 0:
+            raise RuntimeError("reference voxelize failed")
+        reps = max(1, min(int(seconds / max(secs.value, 1e-6)), 20))
+        if L.gref_time_voxelize(C.c_void_p(h.h), C.byref(vc), reps, C.byref(secs)) != 0:
+            raise RuntimeError("reference voxelize failed")
+        return {"value": reps / secs.value, "unit": "voxelizations/s", "cores": int(workers), "kind": "reference",
+                "sample": f"{reps} voxelize calls of {cfg['name']}, oracle/_ref with {workers} threads"}
+
+    if impl == "reference":
+        if rank != 0:
+            return 0
+        r = ref_rate(0, min(150.0, max(20.0, 2.0 * args.steps)))
+        line = dict(base, impl="reference", value=r["value"], n_gpus=args.gpus, steps=args.steps,
+                    warmup=args.warmup, ms_per_step=1000.0 / r["value"], dtype="f64",
+                    cpu_baseline=r, e2e={"value": r["value"], "unit": "voxelizations/s",
+                                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+
+    import paper_2603_20611_b200 as gp
+    from paper_2603_20611_b200 import dp
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    s = gp.Session(local, stream=stream.cuda_stream)
+    gs = make_records(cfg)
+    s.set_gaussians(gs)
+    vcfg = gp.VoxelizerConfig(dims=(X, Y, Z))
+    s.voxelize(vcfg, to_host=False)
+    off, ent = s.voxel_tile_lists()
+    inst = len(ent)
+    del off, ent
+    evals = inst * 512.0  # every voxel of every touched 8^3 tile (voxelize.hpp:137-143)
+    for _ in range(max(args.warmup, 2)):
+        s.voxelize(vcfg, to_host=False)
+    s.synchronize()
+    steps = max(3, min(args.steps, 30))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    s.stage_timing(True)
+    s.stage_times(reset=True)
+    with ClockSampler(local) as clk:
+        for i in range(steps):
+            ev[i][0].record(stream)
+            s.voxelize(vcfg, to_host=False)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    st = s.stage_times(reset=True)
+    s.stage_timing(False)
+    ms = dp.max_over_ranks([sum(a.elapsed_time(b) for a, b in ev) / steps], device="cuda")[0]
+    eval_ms = st["voxel_eval"][0] / max(st["voxel_eval"][1], 1)
+    prep_ms = st["voxel"][0] / max(st["voxel"][1], 1)
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    clk_mhz = ClockSampler.peak_mhz(local)
+    ex2_peak = 16.0 * sm_count * clk_mhz * 1e6
+    peak, peak_src = load_peaks()
+    # e2e: the public call with the volume copied to host memory (pinned)
+    vol = torch.empty(V, dtype=torch.float32).pin_memory()
+    e_steps = 3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    from paper_2603_20611_b200 import _native as N
+
+    e0.record(stream)
+    for _ in range(e_steps):
+        s.voxelize(vcfg, to_host=False)
+        s.download(N.GPK_BUF_VOLUME, vol.data_ptr(), V * 4)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1) / e_steps
+    line = dict(base, value=world * 1000.0 / ms, n_gpus=world, steps=steps, warmup=args.warmup, ms_per_step=ms,
+                dtype="f32 (fp64 support bounds)")
+    line["roofline"] = {"kernel": "k_veval", "bound": "mufu", "achieved": evals / (eval_ms * 1e-3),
+                        "peak": ex2_peak, "unit": "ex2/s", "frac": evals / (eval_ms * 1e-3) / ex2_peak,
+                        "traffic": None, "launch_ms": eval_ms, "evals_per_launch": evals,
+                        "basis": f"one ex2 per (voxel, primitive) of a touched tile: 512 x {inst} tile "
+                                 f"instances; 16 ex2/clk/SM x {sm_count} SMs x {clk_mhz:.0f} MHz"}
+    line["hbm_roofline"] = {"bytes_per_step": 44 * cfg["n"] + 4 * V,
+                            "achieved_gbs": (44 * cfg["n"] + 4 * V) / (ms * 1e-3) / 1e9, "peak": peak,
+                            "frac": (44 * cfg["n"] + 4 * V) / (ms * 1e-3) / 1e9 / peak, "peak_source": peak_src,
+                            "formula": "44N params + 4V volume"}
+    line["stage_ms"] = {"prims_and_tile_lists": prep_ms, "evaluation": eval_ms}
+    line["tile_instances"] = inst
+    line["e2e"] = {"value": 1000.0 / e_ms, "unit": "voxelizations/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": V * 4, "path": "C-ABI: gpk_voxelize + gpk_download(volume, pinned)"}
+    line["gpu_launches"] = (1 + 2 + 1) * steps  # k_vprep, 2 radix passes, k_veval
+    line["clocks"] = clk.result()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = ref_rate(0, args.cpu_seconds)
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    s.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
 
 
 def run_ours(args):
@@ -728,6 +863,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.config == "c4":
+        return run_voxel(args, args.impl)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

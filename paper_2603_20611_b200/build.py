@@ -2,9 +2,12 @@
 
 Each .cu is compiled with nvcc for sm_100a only (``-gencode arch=compute_100a,
 code=sm_100a``), ``-lineinfo`` so ncu source pages map to the code, and linked
-into one C-ABI shared library (include/gpile_b200.h). prep.cu is built with
-``--fmad=false``: its fp64 focus algebra must round like the reference's
-x86-64 build (see csrc/focus.cuh). No torch types cross this library.
+into one C-ABI shared library (include/gpile_b200.h). prep.cu (K_decide, the
+reference-order fp64 chain, the voxelizer's fp64 bounds), densify.cu and
+codec.cu are built with ``--fmad=false``: their fp64 expressions must round
+like the reference's x86-64 build (see csrc/focus.cuh). The fp32 streaming
+cull (cull.cu) and chain (chain.cu) keep FMA contraction. No torch types
+cross this library.
 """
 from __future__ import annotations
 

@@ -185,12 +185,13 @@ template <int N, typename G>
 __device__ __forceinline__ Pack<N> adam_plane_g(const AdamLaunch& a, const AdamConsts& c, int k, float lr, uint32_t i0,
                                                 const G& grad, unsigned& nz) {
     const uint64_t o = (uint64_t)k * a.cap + i0;
-    const Pack<N> g = grad(k);
     // Everything evict-first: the moments must not push the parameters (which
     // K_filter left in L2 with evict-last priority for this read) out of L2,
     // and the parameter accesses here demote those lines again, so nothing of
-    // this step stays resident into the next one.
+    // this step stays resident into the next one. The streams are requested
+    // before the gradient (whose source may take several dependent loads).
     Pack<N> m = ldp_stream<N>(a.m + o), v = ldp_stream<N>(a.v + o), p = ldp_stream<N>(a.params + o);
+    const Pack<N> g = grad(k);
     const float lrc = __fmul_rn(lr, c.ibc1);
 #pragma unroll
     for (int l = 0; l < N; ++l) {

@@ -59,6 +59,48 @@ struct alignas(16) SurvivorRecord {
 };
 static_assert(sizeof(SurvivorRecord) == 48, "record must stay 48 B");
 
+// One (tile, survivor) pair as the pixel kernels consume it: tile-major, in
+// list order (the reference's per-tile lists, render.hpp:142-160), 32 B. The
+// centre is relative to the tile's first pixel centre, formed in fp64 from the
+// survivor's fp64 mean (absolute fp32 pixel coordinates lose
+// 3.6e-4 at 2048^2). A tile's pairs are one contiguous run: the forward and
+// backward stage them into shared memory with cp.async.bulk (TMA) copies.
+struct alignas(16) PairRecord {
+    float ox, oy;        // mu_2d - pixel_centre(tile x0, y0), world units
+    float ka, kb2, kd;   // conic a, 2b, d times -1/2 log2(e): exponent = dx(ka dx + kb2 dy) + kd dy^2
+    float at;            // alpha_tilde
+    uint32_t rect;       // tile-clipped footprint as bit masks: bits [0,16) covered columns, [16,32) rows
+    uint32_t pos;        // pre-sort pair position (the backward's partials, K_chain's merge order)
+};
+static_assert(sizeof(PairRecord) == 32, "pair record must stay 32 B");
+
+constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
+
+// The pair record of survivor r on tile (tx, ty) (x0 = 16 tx, y0 = 16 ty pixels).
+__device__ __forceinline__ PairRecord make_pair_record(const SurvivorRecord& r, int tx, int ty, double X0, double Y0) {
+    const int x0 = tx * kTile, y0 = ty * kTile;
+    PairRecord p;
+    p.ox = (float)(r.mu2d_x - X0);
+    p.oy = (float)(r.mu2d_y - Y0);
+    p.ka = r.conic_a * kNegHalfLog2e;
+    p.kb2 = 2.f * r.conic_b * kNegHalfLog2e;
+    p.kd = r.conic_d * kNegHalfLog2e;
+    p.at = r.alpha_tilde;
+    const int cx0 = max((int)r.lo_x - x0, 0), cx1 = min((int)r.hi_x - x0, kTile - 1);
+    const int cy0 = max((int)r.lo_y - y0, 0), cy1 = min((int)r.hi_y - y0, kTile - 1);
+    const unsigned xm = ((2u << cx1) - (1u << cx0)) & 0xffffu;
+    const unsigned ym = ((2u << cy1) - (1u << cy0)) & 0xffffu;
+    p.rect = xm | (ym << 16);
+    const unsigned ntx = r.hi_x / kTile - r.lo_x / kTile + 1;
+    p.pos = r.pair_base + (unsigned)((ty - r.lo_y / kTile) * ntx + (tx - r.lo_x / kTile));
+    return p;
+}
+__device__ __forceinline__ void store_pair_record(PairRecord* dst, const PairRecord& p) {
+    float4* d = reinterpret_cast<float4*>(dst);
+    d[0] = make_float4(p.ox, p.oy, p.ka, p.kb2);
+    d[1] = make_float4(p.kd, p.at, __uint_as_float(p.rect), __uint_as_float(p.pos));
+}
+
 // One candidate's parameters, gathered once by K_filter from the SoA planes
 // (which it streams anyway) so later stages read 48 contiguous bytes instead of
 // 11 scattered 32 B sectors.
@@ -440,8 +482,15 @@ struct GatherLaunch {
     uint32_t* vals_out;            // per-tile lists, ascending slot
     const Control* ctrl;
     uint64_t pair_cap;
+    // the tile-major pair records of the lists (PairRecord)
+    const SurvivorRecord* records;
+    PairRecord* pairs;
+    SliceArgs slice;
 };
 void launch_gather(const GatherLaunch& a, cudaStream_t st);
+// Multi-pass slices: the pair records of the sorted lists, one per position.
+void launch_pair_records(const uint32_t* keys, const uint32_t* vals, const SurvivorRecord* records, PairRecord* pairs,
+                         const Control* ctrl, uint64_t pair_cap, const SliceArgs& slice, int num_sms, cudaStream_t st);
 
 struct SortLaunch {
     const uint32_t* keys_in;
@@ -492,6 +541,9 @@ struct RasterLaunch {
     unsigned ngroups, row_stride;
     const uint32_t* vals_in;
     uint32_t* vals_out;
+    // tile-major pair records: written by the gather (or by the forward when it
+    // gathers), read by the pixel kernels through cp.async.bulk
+    PairRecord* pairs;
 };
 
 struct ChainLaunch {

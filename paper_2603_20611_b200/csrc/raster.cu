@@ -2,19 +2,23 @@
 //
 // Forward replaces rasterize_prepared (render.hpp:166-192):
 //   one CTA per 16x16 tile, one thread per pixel, warps own 8x4 pixel blocks.
-//   Survivor records of the tile's list are staged through shared memory in
-//   batches of 256 (one gather per thread; the records are L2-resident), each
-//   converted to tile-local fp32 offsets from its fp64 centre (SURVEY.md
-//   §7.3.3: absolute fp32 pixel coordinates lose 3.6e-4 at 2048^2) and to a
-//   bit mask of the tile rows/columns its footprint covers. Each warp ballots
+//   The tile's pairs are one contiguous run of 32 B PairRecords (tile-local
+//   fp32 centre from the fp64 mean — SURVEY.md §7.3.3: absolute fp32 pixel
+//   coordinates lose 3.6e-4 at 2048^2 — scaled conic, alpha_tilde, the bit
+//   mask of covered tile rows/columns, the pair's partials position), written
+//   by the gather; the forward stages them into shared memory in batches of
+//   256 with double-buffered cp.async.bulk (TMA) copies on an mbarrier. In the
+//   training step the forward builds its own tile's list and records (the
+//   gather fused in), stages them directly and stores them for the backward.
+//   Each warp ballots
 //   which of 32 records touch its 8x4 block and walks only those, in list
 //   order — every pixel sums its Gaussians in ascending set order like the
 //   reference, deterministically. exp runs on MUFU.EX2 with the -1/2*log2(e)
 //   factor folded into the conic.
 //
 // Backward replaces stage 1 of backward_prepared (backward.hpp:108-139):
-//   the tile's pairs are staged once in shared memory (tile-local centre,
-//   conic, alpha_tilde, clipped footprint, output position), bucketed by work
+//   the tile's PairRecords are staged into shared memory by cp.async.bulk
+//   (TMA, double-buffered batches of 256), bucketed by work
 //   (rows-per-lane x width, largest first) and processed one QUAD (4 lanes)
 //   per pair: lane q takes rows q, q+4, ... of the tile-clipped footprint and
 //   walks each row left to right. The per-pixel work is factored through the
@@ -31,8 +35,6 @@
 namespace gpk {
 
 namespace {
-
-constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -60,22 +62,6 @@ __device__ __forceinline__ unsigned warp_lower_bound(const uint32_t* __restrict_
     const unsigned pos = lo + lane;
     const bool less = pos < hi && keys[pos] < target;
     return lo + __popc(__ballot_sync(0xffffffffu, less));
-}
-
-// Tile-clipped footprint (inclusive, tile-local): cx0 | cx1<<8 | cy0<<16 | cy1<<24.
-__device__ __forceinline__ unsigned clip_rect(const SurvivorRecord& r, int x0, int y0) {
-    const int cx0 = max((int)r.lo_x - x0, 0), cx1 = min((int)r.hi_x - x0, kTile - 1);
-    const int cy0 = max((int)r.lo_y - y0, 0), cy1 = min((int)r.hi_y - y0, kTile - 1);
-    return (unsigned)cx0 | ((unsigned)cx1 << 8) | ((unsigned)cy0 << 16) | ((unsigned)cy1 << 24);
-}
-
-// Same footprint as bit masks: bits [0,16) = covered columns, [16,32) = rows.
-__device__ __forceinline__ unsigned clip_mask(const SurvivorRecord& r, int x0, int y0) {
-    const int cx0 = max((int)r.lo_x - x0, 0), cx1 = min((int)r.hi_x - x0, kTile - 1);
-    const int cy0 = max((int)r.lo_y - y0, 0), cy1 = min((int)r.hi_y - y0, kTile - 1);
-    const unsigned xm = ((2u << cx1) - (1u << cx0)) & 0xffffu;
-    const unsigned ym = ((2u << cy1) - (1u << cy0)) & 0xffffu;
-    return xm | (ym << 16);
 }
 
 // [begin, end) of the tile's pairs in the sorted list. The last radix pass
@@ -112,17 +98,73 @@ __device__ __forceinline__ void gather_tile(const RasterLaunch& a, unsigned d) {
                           stored_pairs(a.ctrl, a.pair_cap), a.vals_in, a.vals_out, s_ex, s_b, s_wsum);
 }
 
+// Double-buffered TMA staging of a tile's PairRecords: batch q of [start, end)
+// goes to buffer q & 1; one elected thread arms the buffer's mbarrier with
+// the batch's bytes and issues one bulk copy. Callers wait with pair_wait and
+// re-arm a buffer only after a CTA barrier (every warp done reading it).
+constexpr int kPairBatch = 256;
+
+struct PairStage {
+    PairRecord (*buf)[kPairBatch];
+    uint64_t* bar;
+    unsigned start, end;
+};
+
+__device__ __forceinline__ void pair_issue(const PairStage& ps, const PairRecord* pairs, unsigned q) {
+    const unsigned b = ps.start + q * kPairBatch;
+    if (b >= ps.end) return;
+    const unsigned nb = min((unsigned)kPairBatch, ps.end - b);
+    mbar_expect_tx(&ps.bar[q & 1], nb * (unsigned)sizeof(PairRecord));
+    bulk_g2s(ps.buf[q & 1], pairs + b, nb * (unsigned)sizeof(PairRecord), &ps.bar[q & 1]);
+}
+
+__device__ __forceinline__ void pair_wait(const PairStage& ps, unsigned q) { mbar_wait(&ps.bar[q & 1], (q >> 1) & 1); }
+
+// Every pixel of the warp's 8x4 block sums the batch's records that touch the
+// block, in list order (ascending set index, like the reference).
+__device__ __forceinline__ float fwd_batch(const PairRecord* recs, unsigned nb, unsigned warp_x, unsigned warp_y,
+                                           unsigned lane_bits, float fx, float fy, float acc) {
+    const int lane = threadIdx.x & 31;
+    const float4* s4 = reinterpret_cast<const float4*>(recs);
+    for (unsigned g = 0; g < nb; g += 32) {
+        bool hit = false;
+        if (g + lane < nb) {
+            const unsigned m = recs[g + lane].rect;
+            hit = (m & warp_x) && (m & warp_y);
+        }
+        unsigned m = __ballot_sync(0xffffffffu, hit);
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            const float4 r0 = s4[2 * (g + k)];
+            const float4 r1 = s4[2 * (g + k) + 1];
+            const bool inside = (__float_as_uint(r1.z) & lane_bits) == lane_bits;
+            const float dx = fx - r0.x, dy = fy - r0.y;
+            const float e = fmaf(dx, fmaf(r0.z, dx, r0.w * dy), r1.x * dy * dy);
+            acc = fmaf(inside ? r1.y : 0.f, ex2_approx(e), acc);
+        }
+    }
+    return acc;
+}
+
 __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    __shared__ float4 s_rec[256][2];  // {ox, oy, a*k, 2b*k}, {d*k, alpha_tilde, mask, -}
+    __shared__ __align__(128) PairRecord s_pr[2][kPairBatch];
+    __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ unsigned s_range[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
-    if (a.bucket_tab) gather_tile(a, (unsigned)tile);  // (ends with a barrier)
+    const bool produce = a.bucket_tab != nullptr;
+    if (produce) gather_tile(a, (unsigned)tile);  // (ends with a barrier)
     const int tx = tile % a.slice.tiles_x, ty = tile / a.slice.tiles_x;
     const int x0 = tx * kTile, y0 = ty * kTile;
     tile_range(a, tile, s_range);
+    if (!produce && tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+    }
     // pixel of this thread: warp w -> 8x4 block
     const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
     const int lx = wx0 + (lane & 7), ly = wy0 + (lane >> 3);
@@ -132,37 +174,37 @@ __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
     const double Y0 = ((double)y0 - a.slice.ppy) * a.slice.sy;
     const float fx = (float)(lx * a.slice.sx), fy = (float)(ly * a.slice.sy);
     __syncthreads();
-    const unsigned start = s_range[0], end = s_range[1];
+    const PairStage ps{s_pr, s_bar, s_range[0], s_range[1]};
+    const unsigned nbatch = (ps.end - ps.start + kPairBatch - 1) / kPairBatch;
 
     float acc = 0.f;
-    for (unsigned b = start; b < end; b += 256) {
-        const unsigned nb = min(256u, end - b);
-        __syncthreads();
-        if (tid < nb) {
-            // (L2 load: the list may have been written by this CTA / a neighbour just now)
-            const SurvivorRecord r = a.records[__ldcg(&a.vals[b + tid])];
-            s_rec[tid][0] = make_float4((float)(r.mu2d_x - X0), (float)(r.mu2d_y - Y0),
-                                        r.conic_a * kNegHalfLog2e, 2.f * r.conic_b * kNegHalfLog2e);
-            s_rec[tid][1] = make_float4(r.conic_d * kNegHalfLog2e, r.alpha_tilde,
-                                        __uint_as_float(clip_mask(r, x0, y0)), 0.f);
-        }
-        __syncthreads();
-        for (unsigned g = 0; g < nb; g += 32) {
-            bool hit = false;
-            if (g + lane < nb) {
-                const unsigned m = __float_as_uint(s_rec[g + lane][1].z);
-                hit = (m & warp_x) && (m & warp_y);
+    if (produce) {
+        // the training step's forward builds its tile's records itself (from
+        // the list it just gathered) and stores them for the backward
+        for (unsigned q = 0; q < nbatch; ++q) {
+            const unsigned b = ps.start + q * kPairBatch, nb = min((unsigned)kPairBatch, ps.end - b);
+            if ((unsigned)tid < nb) {
+                // (L2 load: the list was written by this CTA just now)
+                const PairRecord pr = make_pair_record(a.records[__ldcg(&a.vals[b + tid])], tx, ty, X0, Y0);
+                store_pair_record(&s_pr[0][tid], pr);
+                store_pair_record(a.pairs + b + tid, pr);
             }
-            unsigned m = __ballot_sync(0xffffffffu, hit);
-            while (m) {
-                const int k = __ffs(m) - 1;
-                m &= m - 1;
-                const float4 r0 = s_rec[g + k][0];
-                const float4 r1 = s_rec[g + k][1];
-                const bool inside = (__float_as_uint(r1.z) & lane_bits) == lane_bits;
-                const float dx = fx - r0.x, dy = fy - r0.y;
-                const float e = fmaf(dx, fmaf(r0.z, dx, r0.w * dy), r1.x * dy * dy);
-                acc = fmaf(inside ? r1.y : 0.f, ex2_approx(e), acc);
+            __syncthreads();
+            acc = fwd_batch(s_pr[0], nb, warp_x, warp_y, lane_bits, fx, fy, acc);
+            __syncthreads();
+        }
+    } else {
+        if (tid == 0) {
+            pair_issue(ps, a.pairs, 0);
+            pair_issue(ps, a.pairs, 1);
+        }
+        for (unsigned q = 0; q < nbatch; ++q) {
+            const unsigned nb = min((unsigned)kPairBatch, ps.end - (ps.start + q * kPairBatch));
+            pair_wait(ps, q);
+            acc = fwd_batch(s_pr[q & 1], nb, warp_x, warp_y, lane_bits, fx, fy, acc);
+            if (q + 2 < nbatch) {
+                __syncthreads();  // buffer q & 1 read by every warp
+                if (tid == 0) pair_issue(ps, a.pairs, q + 2);
             }
         }
     }
@@ -273,15 +315,15 @@ __device__ __forceinline__ void ssim_dl_tile(const RasterLaunch& a, int x0, int 
     s_dl[threadIdx.x] = dl;
 }
 
-constexpr int kBwdBatch = 256;    // pairs staged per round (one per thread)
 constexpr int kWorkBuckets = 16;
 
 __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    __shared__ __align__(128) PairRecord s_pr[2][kPairBatch];
+    __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ float s_dl[kTile * kTile];
-    __shared__ float4 s_pair[kBwdBatch][2];   // {ox, oy, ca, cb}, {cd, at, rect, pos}
     __shared__ unsigned s_bucket[kWorkBuckets];
-    __shared__ uint8_t s_order[kBwdBatch];
+    __shared__ uint8_t s_order[kPairBatch];
     __shared__ unsigned s_range[2];
 
     const int tid = threadIdx.x;
@@ -289,32 +331,39 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
     const int tx = tile % a.slice.tiles_x, ty = tile / a.slice.tiles_x;
     const int x0 = tx * kTile, y0 = ty * kTile;
     tile_range(a, tile, s_range);
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const PairStage ps{s_pr, s_bar, s_range[0], s_range[1]};
+    const unsigned nbatch = (ps.end - ps.start + kPairBatch - 1) / kPairBatch;
+    if (tid == 0) {  // the first records land while dL/dI is formed
+        pair_issue(ps, a.pairs, 0);
+        pair_issue(ps, a.pairs, 1);
+    }
     if (a.ssim_g) {
         ssim_dl_tile(a, x0, y0, s_dl);
     } else {
         const int i = x0 + (tid & 15), j = y0 + (tid >> 4);
         s_dl[tid] = (i < a.slice.W && j < a.slice.H) ? __ldg(&a.dl_di[(size_t)j * a.slice.W + i]) : 0.f;
     }
-    const double X0 = ((double)x0 - a.slice.ppx) * a.slice.sx;
-    const double Y0 = ((double)y0 - a.slice.ppy) * a.slice.sy;
     const float sxf = (float)a.slice.sx, syf = (float)a.slice.sy;
-    __syncthreads();
-    const unsigned start = s_range[0], end = s_range[1];
+    constexpr float kInvK = 1.f / kNegHalfLog2e;
 
-    for (unsigned b = start; b < end; b += kBwdBatch) {
-        const unsigned nb = min((unsigned)kBwdBatch, end - b);
+    for (unsigned q = 0; q < nbatch; ++q) {
+        const unsigned nb = min((unsigned)kPairBatch, ps.end - (ps.start + q * kPairBatch));
+        const PairRecord* recs = s_pr[q & 1];
         if (tid < kWorkBuckets) s_bucket[tid] = 0;
-        __syncthreads();
-        // ---- stage the batch's pairs, bucketed by per-lane work ---------------
+        pair_wait(ps, q);
+        __syncthreads();  // buckets cleared; s_dl complete (first batch)
+        // ---- the batch's pairs bucketed by per-lane work (largest first) -------
         unsigned slot = 0xffffffffu;
         if ((unsigned)tid < nb) {
-            const SurvivorRecord r = a.records[a.vals[b + tid]];
-            const unsigned rc = clip_rect(r, x0, y0);
-            const unsigned w = ((rc >> 8) & 255u) - (rc & 255u) + 1, h = (rc >> 24) - ((rc >> 16) & 255u) + 1;
-            const unsigned ntx = r.hi_x / kTile - r.lo_x / kTile + 1;
-            const unsigned pos = r.pair_base + (unsigned)((ty - r.lo_y / kTile) * ntx + (tx - r.lo_x / kTile));
-            s_pair[tid][0] = make_float4((float)(r.mu2d_x - X0), (float)(r.mu2d_y - Y0), r.conic_a, r.conic_b);
-            s_pair[tid][1] = make_float4(r.conic_d, r.alpha_tilde, __uint_as_float(rc), __uint_as_float(pos));
+            const unsigned m = recs[tid].rect;
+            const unsigned xm = m & 0xffffu, ym = m >> 16;
+            const unsigned w = (31 - __clz(xm)) - (__ffs(xm) - 1) + 1, h = (31 - __clz(ym)) - (__ffs(ym) - 1) + 1;
             const unsigned work = ((h + 3) >> 2) * w;  // rows per lane x row length, <= 64
             const unsigned bk = (kWorkBuckets - 1) - min(work >> 2, (unsigned)kWorkBuckets - 1);
             slot = (bk << 16) | atomicAdd(&s_bucket[bk], 1u);
@@ -336,19 +385,19 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
 
         // ---- one quad per pair ------------------------------------------------
         const int quad = tid >> 2, ql = tid & 3;
-        for (unsigned o0 = 0; o0 < nb; o0 += kBwdBatch / 4) {
+        const float4* s4 = reinterpret_cast<const float4*>(recs);
+        for (unsigned o0 = 0; o0 < nb; o0 += kPairBatch / 4) {
             const unsigned o = o0 + quad;
             const bool active = o < nb;  // quads are whole: all 4 lanes agree
             float U = 0.f, UX = 0.f, UY = 0.f, UXX = 0.f, UXY = 0.f, UYY = 0.f;
-            float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0;
+            float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0;  // {ox, oy, ka, kb2}, {kd, at, mask, pos}
             if (active) {
-                const unsigned q = s_order[o];
-                p0 = s_pair[q][0];
-                p1 = s_pair[q][1];
-                const unsigned rc = __float_as_uint(p1.z);
-                const int cx0 = rc & 255, cx1 = (rc >> 8) & 255, cy0 = (rc >> 16) & 255, cy1 = rc >> 24;
-                const float ka = p0.z * kNegHalfLog2e, kb2 = 2.f * p0.w * kNegHalfLog2e,
-                            kd = p1.x * kNegHalfLog2e;
+                const unsigned k = s_order[o];
+                p0 = s4[2 * k];
+                p1 = s4[2 * k + 1];
+                const unsigned m = __float_as_uint(p1.z), xm = m & 0xffffu, ym = m >> 16;
+                const int cx0 = __ffs(xm) - 1, cx1 = 31 - __clz(xm), cy0 = __ffs(ym) - 1, cy1 = 31 - __clz(ym);
+                const float ka = p0.z, kb2 = p0.w, kd = p1.x;
                 for (int y = cy0 + ql; y <= cy1; y += 4) {
                     const float dy = fmaf((float)y, syf, -p0.y);
                     const float B = kb2 * dy, Cc = kd * dy * dy;
@@ -383,14 +432,16 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
             const unsigned pos = __float_as_uint(p1.w);
             if (active && ql == 0 && pos < a.pair_cap) {
                 // PixelAccum (backward.hpp:129-136): dA, dmu = w C d, dconic = -w/2 d d^T
-                const float at = p1.y, ca = p0.z, cb = p0.w, cd = p1.x, h = -0.5f * at;
+                // (C = the stored scaled conic / (-1/2 log2 e))
+                const float at = p1.y, atk = at * kInvK, h = -0.5f * at;
                 float2* dst = reinterpret_cast<float2*>(a.partials + 6ull * pos);
-                dst[0] = make_float2(U, at * fmaf(ca, UX, cb * UY));
-                dst[1] = make_float2(at * fmaf(cb, UX, cd * UY), h * UXX);
+                dst[0] = make_float2(U, atk * fmaf(p0.z, UX, 0.5f * p0.w * UY));
+                dst[1] = make_float2(atk * fmaf(0.5f * p0.w, UX, p1.x * UY), h * UXX);
                 dst[2] = make_float2(h * UXY, h * UYY);
             }
         }
-        __syncthreads();
+        __syncthreads();  // buffer q & 1 and s_order consumed
+        if (tid == 0 && q + 2 < nbatch) pair_issue(ps, a.pairs, q + 2);
     }
 }
 

@@ -134,6 +134,7 @@ struct gpk_session {
 
     DevBuf params, grads, adam_m, adam_v, records, survivors;
     DevBuf keys[2], vals[2], partials, sort_status;  // sort_status: per-sort-tile digit counts
+    DevBuf pair_recs;  // tile-major PairRecords of the sorted lists (32 B per pair)
     DevBuf head;       // Control | hist | prep flags (memset per prepare)
     DevBuf cand_list;  // K_chain's deferral list (survivor slots for the fp64 chain)
     DevBuf cand;       // CandParams of K_filter's candidates (block-major slots)
@@ -406,6 +407,7 @@ int ensure_pairs(gpk_session* s, uint64_t need) {
         CK(s->vals[b].ensure(cap * 4));
     }
     CK(s->partials.ensure(cap * 24));
+    CK(s->pair_recs.ensure(cap * sizeof(PairRecord)));
     ++s->alloc_epoch;
     s->pair_cap = cap;
     return size_sort_status(s);
@@ -626,6 +628,10 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     } else {
         StageScope scope_sort(s, GPK_STAGE_SORT);
         TRY(launch_sorts(s, ps.passes, ps.digit_bits, s->grp_pairs(), (unsigned)decide_group_count(s->n)));
+        const int fb = ps.passes & 1;
+        launch_pair_records(s->keys[fb].as<uint32_t>(), s->vals[fb].as<uint32_t>(), s->records.as<SurvivorRecord>(),
+                            s->pair_recs.as<PairRecord>(), s->ctrl(), s->pair_cap, a, s->num_sms, s->stream);
+        CK(cudaGetLastError());
     }
     ps.final_buf = ps.passes & 1;
     return GPK_OK;
@@ -688,6 +694,7 @@ RasterLaunch raster_args(gpk_session* s) {
     r.row_stride = (1u << s->prep.digit_bits) + 1;
     r.vals_in = s->vals[0].as<uint32_t>();
     r.vals_out = s->vals[1].as<uint32_t>();
+    r.pairs = s->pair_recs.as<PairRecord>();
     return r;
 }
 
@@ -702,6 +709,9 @@ GatherLaunch gather_args(gpk_session* s) {
     gl.vals_out = s->vals[1].as<uint32_t>();
     gl.ctrl = s->ctrl();
     gl.pair_cap = s->pair_cap;
+    gl.records = s->records.as<SurvivorRecord>();
+    gl.pairs = s->pair_recs.as<PairRecord>();
+    gl.slice = s->prep.slice;
     return gl;
 }
 
@@ -1342,7 +1352,7 @@ static int session_destroy(gpk_session* s) {
     }
     s->graphs.clear();
     DevBuf* bufs[] = {&s->params, &s->grads, &s->adam_m, &s->adam_v, &s->records, &s->survivors,
-                      &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials,
+                      &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials, &s->pair_recs,
                       &s->sort_status, &s->head, &s->persist, &s->image,
                       &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm, &s->acc_norm, &s->acc_obs, &s->acc_world,
                       &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table, &s->bucket_tab,
@@ -2607,7 +2617,7 @@ int gpk_voxelize(gpk_session* s, const gpk_voxelizer_config* cfg, float* volume_
     TRY(set_device(s));
     TRY(vox_prep_settled(s, cfg));
     {
-        StageScope scope(s, GPK_STAGE_VOXEL);
+        StageScope scope(s, GPK_STAGE_VOXEL_EVAL);
         launch_vox_eval(vox_eval_args(s), s->stream);
         CK(cudaGetLastError());
     }

@@ -237,14 +237,45 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherLaunch a)
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ unsigned s_ex[kGatherThreads + 1], s_b[kGatherThreads], s_wsum[kGatherThreads / 32];
     const unsigned d = blockIdx.x;
-    gather_tile_list<kGatherThreads>(a.bucket_tab, a.ngroups, a.row_stride, d, __ldcg(&a.tile_begin[d]),
-                                     stored_pairs(a.ctrl, a.pair_cap), a.vals_in, a.vals_out, s_ex, s_b, s_wsum);
+    const unsigned begin = __ldcg(&a.tile_begin[d]);
+    const unsigned end = gather_tile_list<kGatherThreads>(a.bucket_tab, a.ngroups, a.row_stride, d, begin,
+                                                          stored_pairs(a.ctrl, a.pair_cap), a.vals_in, a.vals_out,
+                                                          s_ex, s_b, s_wsum);
+    // the tile's pair records, in list order (the list is this CTA's own
+    // writes: visible after the helper's closing barrier)
+    const int tx = (int)(d % (unsigned)a.slice.tiles_x), ty = (int)(d / (unsigned)a.slice.tiles_x);
+    const double X0 = ((double)(tx * kTile) - a.slice.ppx) * a.slice.sx;
+    const double Y0 = ((double)(ty * kTile) - a.slice.ppy) * a.slice.sy;
+    for (unsigned t = begin + threadIdx.x; t < end; t += kGatherThreads)
+        store_pair_record(a.pairs + t, make_pair_record(a.records[__ldcg(&a.vals_out[t])], tx, ty, X0, Y0));
+}
+
+// Multi-pass slices: the pair record of every sorted position (its tile is its key).
+__global__ void __launch_bounds__(256) k_pair_records(const uint32_t* __restrict__ keys,
+                                                      const uint32_t* __restrict__ vals,
+                                                      const SurvivorRecord* __restrict__ records,
+                                                      PairRecord* __restrict__ pairs, const Control* ctrl,
+                                                      uint64_t pair_cap, const SliceArgs sl) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    const unsigned P = stored_pairs(ctrl, pair_cap);
+    for (unsigned j = blockIdx.x * blockDim.x + threadIdx.x; j < P; j += gridDim.x * blockDim.x) {
+        const unsigned tile = keys[j];
+        const int tx = (int)(tile % (unsigned)sl.tiles_x), ty = (int)(tile / (unsigned)sl.tiles_x);
+        const double X0 = ((double)(tx * kTile) - sl.ppx) * sl.sx;
+        const double Y0 = ((double)(ty * kTile) - sl.ppy) * sl.sy;
+        store_pair_record(pairs + j, make_pair_record(records[vals[j]], tx, ty, X0, Y0));
+    }
 }
 
 }  // namespace
 
 void launch_gather(const GatherLaunch& a, cudaStream_t st) {
     if (a.ntiles) launch_pdl(k_gather, dim3(a.ntiles), dim3(kGatherThreads), 0, st, a);
+}
+
+void launch_pair_records(const uint32_t* keys, const uint32_t* vals, const SurvivorRecord* records, PairRecord* pairs,
+                         const Control* ctrl, uint64_t pair_cap, const SliceArgs& slice, int num_sms, cudaStream_t st) {
+    launch_pdl(k_pair_records, dim3(num_sms * 8), dim3(256), 0, st, keys, vals, records, pairs, ctrl, pair_cap, slice);
 }
 
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st) {

@@ -34,7 +34,9 @@ __global__ void __launch_bounds__(256, kMinB) k_adam(const AdamLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     const uint32_t i0 = a.lo + (blockIdx.x * blockDim.x + threadIdx.x) * kAdamItems;
     if (i0 >= a.n) return;  // the capacity is a multiple of 512: vector accesses stay in the plane
-    if (a.ctrl && a.ctrl->pair_overflow) {  // the slice overflowed: no update
+    bool overflow = a.ctrl && a.ctrl->pair_overflow;  // a slice overflowed: no update
+    for (int s = 0; s < a.nsrc; ++s) overflow |= a.src_ctrl[s]->pair_overflow != 0;  // (batched step)
+    if (overflow) {
         if (kSlots) adam_slots_clear<kAdamItems>(a, i0);
         return;
     }
@@ -48,29 +50,25 @@ __global__ void __launch_bounds__(256, kMinB) k_adam(const AdamLaunch a) {
     if (any) adam_slots_clear<kAdamItems>(a, i0);
 }
 
-// Batched step: the gradient of each primitive is the sum of the B slices'
-// slot gradients (slice order); an overflowed slice anywhere skips the update.
-__device__ __forceinline__ bool batch_overflow(const AdamLaunch& a) {
-    bool of = a.ctrl && a.ctrl->pair_overflow;
-    for (int s = 0; s < a.nsrc; ++s) of |= a.src_ctrl[s]->pair_overflow != 0;
-    return of;
-}
-
-template <int kMinB>
-__global__ void __launch_bounds__(256, kMinB) k_adam_batch(const AdamLaunch a) {
+// Batched step, before its Adam: the B slices' slot gradients summed per
+// primitive in slice order into the dense planes — every entry written (zero
+// where no slice kept the primitive), every map read cleared. The dense Adam
+// (k_adam) then updates from them: the sum is formed once, in a streaming
+// pass, instead of B scattered reads per plane inside the latency-bound update.
+__global__ void __launch_bounds__(256) k_sum_slots(const AdamLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    const uint32_t i0 = a.lo + (blockIdx.x * blockDim.x + threadIdx.x) * kAdamItems;
+    const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * kAdamItems;
     if (i0 >= a.n) return;
     unsigned pm[kMaxBatch];
     const bool any = adam_slots_multi(a, i0, pm);
-    if (batch_overflow(a)) {
-        if (any) adam_slots_multi_clear(a, i0, pm);
+    if (!any) {
+#pragma unroll
+        for (int k = 0; k < 11; ++k) stp<kAdamItems>(a.grads + (uint64_t)k * a.cap + i0, Pack<kAdamItems>{});
         return;
     }
-    const AdamConsts& c = *a.consts;
-    adam_advance_step(a, c);
-    adam_update_store_g<kAdamItems>(a, c, i0, [&](int k) { return adam_grad_multi(a, k, i0, pm); });
-    if (any) adam_slots_multi_clear(a, i0, pm);
+#pragma unroll
+    for (int k = 0; k < 11; ++k) stp<kAdamItems>(a.grads + (uint64_t)k * a.cap + i0, adam_grad_multi(a, k, i0, pm));
+    adam_slots_multi_clear(a, i0, pm);
 }
 
 // Slot gradients -> dense planes, by survivor slot (CTA per K_decide group):
@@ -100,10 +98,9 @@ void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, int mode, 
     if (ngroups) k_scatter_slots<<<ngroups, 256, 0, st>>>(a, mode);
 }
 
-void launch_adam_batch(const AdamLaunch& a, cudaStream_t st) {
-    const unsigned grid = (a.n - a.lo + 256 * kAdamItems - 1) / (256 * kAdamItems);
-    if (!grid || a.n <= a.lo) return;
-    launch_pdl(k_adam_batch<5>, dim3(grid), dim3(256), 0, st, a);
+void launch_sum_slots(const AdamLaunch& a, cudaStream_t st) {
+    const unsigned grid = (a.n + 256 * kAdamItems - 1) / (256 * kAdamItems);
+    if (grid) launch_pdl(k_sum_slots, dim3(grid), dim3(256), 0, st, a);
 }
 
 void launch_adam_consts(const AdamLaunch& a, cudaStream_t st) {

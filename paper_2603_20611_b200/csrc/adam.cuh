@@ -149,14 +149,14 @@ __device__ __forceinline__ void adam_slots_clear(const AdamLaunch& a, uint32_t i
 // One parameter plane of N consecutive primitives: moments updated and stored,
 // the stepped parameters returned (before clamp / renormalisation); nz collects
 // which primitives had a non-zero gradient.
-// Batched step: the maps of all B slices for primitives i0, i0+1 (one u32 =
-// two u16 entries per slice; N == 2) and the summed gradient of plane k.
+// Batched step: the B slices' map entries of primitives i0, i0 + 1 (one u32
+// of two u16 per slice) and their gradient of plane k summed over the slices
+// in slice order.
 __device__ __forceinline__ bool adam_slots_multi(const AdamLaunch& a, uint32_t i0, unsigned pm[kMaxBatch]) {
     unsigned any = 0;
 #pragma unroll
     for (int s = 0; s < kMaxBatch; ++s) {
-        pm[s] = 0;
-        if (s <= a.nsrc) pm[s] = *reinterpret_cast<const unsigned*>((s ? a.src_gmap[s - 1] : a.gmap) + i0);
+        pm[s] = s <= a.nsrc ? *reinterpret_cast<const unsigned*>((s ? a.src_gmap[s - 1] : a.gmap) + i0) : 0u;
         any |= pm[s];
     }
     return any != 0;
@@ -167,16 +167,28 @@ __device__ __forceinline__ void adam_slots_multi_clear(const AdamLaunch& a, uint
         if (pm[s]) *reinterpret_cast<unsigned*>((s ? a.src_gmap[s - 1] : a.gmap) + i0) = 0u;
 }
 __device__ __forceinline__ Pack<2> adam_grad_multi(const AdamLaunch& a, int k, uint32_t i0, const unsigned pm[kMaxBatch]) {
-    Pack<2> g;
-    g.v[0] = g.v[1] = 0.f;
-    const uint32_t gbase = i0 / kDecideGroupSize * kDecideGroupSize;
+    // Branch-free: every slice's value is requested at once (an absent entry
+    // reads the plane's first slot and is discarded), then summed in slice
+    // order exactly as the dense per-slice gradients add (absent = +0).
+    const uint64_t off = (uint64_t)k * a.cap + i0 / kDecideGroupSize * kDecideGroupSize - 1;
+    float x0[kMaxBatch], x1[kMaxBatch];
 #pragma unroll
     for (int s = 0; s < kMaxBatch; ++s) {
-        if (!pm[s]) continue;
-        const float* base = (s ? a.src_slot[s - 1] : a.slot_grads) + (uint64_t)k * a.cap + gbase - 1;
+        x0[s] = x1[s] = 0.f;
+        if (s > a.nsrc) break;  // uniform: the batch size
+        const float* base = (s ? a.src_slot[s - 1] : a.slot_grads) + off;
         const unsigned m0 = pm[s] & 0xffffu, m1 = pm[s] >> 16;
-        if (m0) g.v[0] = __fadd_rn(g.v[0], __ldcs(base + m0));
-        if (m1) g.v[1] = __fadd_rn(g.v[1], __ldcs(base + m1));
+        x0[s] = __ldcs(base + (m0 ? m0 : 1u));
+        x1[s] = __ldcs(base + (m1 ? m1 : 1u));
+    }
+    Pack<2> g;
+    g.v[0] = (pm[0] & 0xffffu) ? x0[0] : 0.f;
+    g.v[1] = (pm[0] >> 16) ? x1[0] : 0.f;
+#pragma unroll
+    for (int s = 1; s < kMaxBatch; ++s) {
+        if (s > a.nsrc) break;
+        g.v[0] = __fadd_rn(g.v[0], (pm[s] & 0xffffu) ? x0[s] : 0.f);
+        g.v[1] = __fadd_rn(g.v[1], (pm[s] >> 16) ? x1[s] : 0.f);
     }
     return g;
 }

@@ -608,10 +608,10 @@ struct AdamLaunch {
     const uint32_t* surv_gidx;    // slot -> set index (the gradient scatter)
     const unsigned* grp_surv;
     // Batched training step (gpk_train_step_batch, B slices, one Adam): the
-    // further slices' slot gradients, maps and control heads. A primitive's
-    // gradient is the fp32 sum over the slices in slice order (slice 0 =
-    // slot_grads / gmap / ctrl above); every map read is cleared; an overflowed
-    // slice anywhere skips the update.
+    // further slices' slot gradients and maps for k_sum_slots, which sums a
+    // primitive's gradient over the slices in slice order (slice 0 =
+    // slot_grads / gmap above) into the dense planes and clears every map it
+    // reads; src_ctrl: an overflowed slice anywhere skips the update.
     int nsrc;                     // further slices (0: a single slice)
     const float* src_slot[kMaxBatch - 1];
     uint16_t* src_gmap[kMaxBatch - 1];
@@ -740,7 +740,10 @@ void launch_vox_bwd(const VoxEvalLaunch& a, cudaStream_t st);
 void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st);
 
 void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st);
-void launch_prep_multi(const PrepLaunch* pl, int nb, int num_sms, cudaStream_t st);
+// own / union_words: a data-parallel step (only pose `own` stores candidates;
+// the union of every pose's candidates as 4 words per 128-Gaussian chunk)
+void launch_prep_multi(const PrepLaunch* pl, int nb, int num_sms, cudaStream_t st, int own = -1,
+                       unsigned* union_words = nullptr);
 void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& next, cudaStream_t st);
 void launch_bin(const PrepLaunch& a, cudaStream_t st);
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st);
@@ -750,7 +753,7 @@ void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st);
 void launch_chain_exact(const ChainLaunch& a, int grid, cudaStream_t st);
 void launch_adam(const AdamLaunch& a, cudaStream_t st);
 void launch_adam_consts(const AdamLaunch& a, cudaStream_t st);
-void launch_adam_batch(const AdamLaunch& a, cudaStream_t st);
+void launch_sum_slots(const AdamLaunch& a, cudaStream_t st);
 enum ScatterMode : int { kScatterSet = 1, kScatterAdd = 2, kScatterClearMap = 4 };
 void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, int mode, cudaStream_t st);
 void launch_loss(const LossLaunch& a, cudaStream_t st);

@@ -145,6 +145,43 @@ __device__ __forceinline__ bool quick_culled_identity(const float p[11], const F
     return fin & scales_ok & quat_ok & culled;
 }
 
+// quick_culled_identity split for several poses that differ only in t_z
+// (slice_pose_for_index stacks: same R = I, t_x, t_y, PSF, tau, mod): the
+// pose-invariant terms once per Gaussian, then a few FMAs per pose. Same
+// arithmetic, same verdicts as quick_culled_identity.
+struct QuickInv {
+    float p2, ap2, mcx, mcy, den_hi, inv_smin2, thr;  // thr = fminf(raw alpha, 0) - log tau
+    bool ok;
+};
+__device__ __forceinline__ QuickInv quick_invariant(const float p[11], const FilterConsts& c) {
+    QuickInv q;
+    const bool fin = isfinite(((p[2] + p[3]) + (p[4] + p[5])) + p[10]);
+    const float lmax = fmaxf(p[3], fmaxf(p[4], p[5])), lmin = fminf(p[3], fminf(p[4], p[5]));
+    const bool scales_ok = (lmax < 40.f) & (lmin > -40.f) & (lmax - lmin < 6.2f);
+    const float qn2 = __fmaf_rn(p[6], p[6], __fmaf_rn(p[7], p[7], __fmaf_rn(p[8], p[8], p[9] * p[9])));
+    const bool quat_ok = (qn2 > 1e-20f) & (qn2 < 1e20f);
+    const float mcx = p[0] + c.tx, mcy = p[1] + c.ty;
+    q.p2 = p[2];
+    q.ap2 = fabsf(p[2]);
+    q.mcx = mcx;  // NaN in mu_x/y propagates into the compare (not culled)
+    q.mcy = mcy;
+    q.den_hi = __fmaf_rn(ex2_ftz(fminf(lmax, 40.f) * 2.8853900817779268f) * c.mod2, 1.0002f, c.sz2);
+    q.inv_smin2 = ex2_ftz(fmaxf(lmin, -40.f) * -2.8853900817779268f) * c.inv_mod2 * 1.0002f;
+    q.thr = fminf(p[10], 0.f) - c.log_tau;
+    q.ok = fin & scales_ok & quat_ok;
+    return q;
+}
+__device__ __forceinline__ bool quick_culled_pose(const QuickInv& q, const FilterConsts& c) {
+    const float mcz = (q.p2 + c.tz_hi) + c.tz_lo;
+    const float mu2 = __fmaf_rn(q.mcx, q.mcx, __fmaf_rn(q.mcy, q.mcy, mcz * mcz));
+    const float noise = __fmaf_rn(2e-14f * mu2, q.inv_smin2,
+                                  4.8e-7f * fabsf(mcz) * (q.ap2 + fabsf(c.tz_hi)) * c.inv_sz2 * 1.0002f);
+    const float x = q.thr + (2e-3f + __fmaf_rn(2e-5f, fabsf(q.thr) + 0.7f, noise));
+    const float x_up = __fmaf_rn(1e-3f, fabsf(x) + noise, x) + 1e-6f;
+    const bool culled = 0.5f * mcz * mcz > x_up * (x_up >= 0.f ? q.den_hi : c.sz2);
+    return q.ok & culled;
+}
+
 // ---- K_filter ------------------------------------------------------------------
 // prepare_gaussians' cull (render.hpp:107) as a streaming pass with no block
 // barriers. Warps walk 128-Gaussian chunks grid-stride; each lane owns four
@@ -210,16 +247,23 @@ struct CullScratch {
 // in 10 at C2) are compacted so the full test runs in ceil(U/32) warp rounds
 // instead of once per lane item. `staged` (plane-major [11][128], the chunk in
 // shared memory) supplies their parameters; else they are copied to sc.p.
-__device__ __forceinline__ void cull_chunk(const PrepLaunch& a, const FilterConsts& fc, float log_tau, int filter_on,
-                                           unsigned b, uint32_t i0, const float4 v[11], CullIdx& sx,
-                                           float (*sp)[kFilterBlock], const float* staged) {
+// qmask_given >= 0: the quick test's verdicts of the lane's items, computed by
+// the caller (the multi-pose filter shares its pose-invariant part).
+// Returns the lane's candidate mask; write = false: verdicts only (the union
+// of a data-parallel step's other poses), nothing stored.
+__device__ __forceinline__ unsigned cull_chunk(const PrepLaunch& a, const FilterConsts& fc, float log_tau,
+                                               int filter_on, unsigned b, uint32_t i0, const float4 v[11],
+                                               CullIdx& sx, float (*sp)[kFilterBlock], const float* staged,
+                                               int qmask_given = -1, bool write = true) {
     const int lane = threadIdx.x & 31;
     const bool ident = a.slice.identity_rot != 0;
     // items inside the set: all candidates with the cull off, else undecided
     // unless the quick test culls them (identity poses only)
     const unsigned inset = i0 >= a.n ? 0u : (a.n - i0 >= kFilterItems ? (1u << kFilterItems) - 1 : (1u << (a.n - i0)) - 1);
     unsigned cmask = filter_on ? 0u : inset, umask = filter_on ? inset : 0u;
-    if (filter_on && ident) {
+    if (filter_on && ident && qmask_given >= 0) {
+        umask &= ~(unsigned)qmask_given;
+    } else if (filter_on && ident) {
         unsigned qmask = 0;
 #pragma unroll
         for (int k = 0; k < kFilterItems; ++k) {
@@ -281,6 +325,7 @@ __device__ __forceinline__ void cull_chunk(const PrepLaunch& a, const FilterCons
             }
         __syncwarp();  // the scratch is reused by the warp's next chunk
     }
+    if (!write) return cmask;
     const unsigned nc = __popc(cmask);
     unsigned incl = nc;
 #pragma unroll
@@ -300,6 +345,7 @@ __device__ __forceinline__ void cull_chunk(const PrepLaunch& a, const FilterCons
                 store_cand(out++, p, i0 + k);
             }
     }
+    return cmask;
 }
 
 // cp.async (16 B, L1 bypass) staging of K_filter chunks: each lane copies its
@@ -399,6 +445,12 @@ struct MultiPrep {
     float log_tau[kMaxBatch];
     int filter_on[kMaxBatch];
     int nb;
+    int shared_quick;  // every pose R = I with the same t_x, t_y, PSF, tau, mod: split quick test
+    // data-parallel step: only pose `own` stores candidates (the others give
+    // verdicts); union_words[4 b + k] bit l = item 4 l + k of chunk b is a
+    // candidate of some pose (nullptr: batched step, every pose stores)
+    int own;
+    unsigned* union_words;
 };
 
 __global__ void __launch_bounds__(kFilterThreads, 2) k_filter_multi(const __grid_constant__ MultiPrep m) {
@@ -420,14 +472,17 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter_multi(const __grid
 #pragma unroll
         for (int q = 0; q < 11; ++q) cp_async16_hint(dst + q * kFilterBlock, src + (uint64_t)q * a0.cap, keep);
     };
+    __shared__ FilterConsts s_fc[kMaxBatch];
     unsigned b = gtid / 32;
     if (b < nchunks) prefetch(b, 0);
     cp_async_commit();
+    if (tid < m.nb) s_fc[tid] = filter_consts(m.p[tid].slice, m.log_tau[tid]);
     for (int k = 0; k < m.nb; ++k) {
         const PrepLaunch& a = m.p[k];
         for (unsigned w = gtid; w < a.head_words; w += gthreads) a.head[w] = 0u;
         clear_prev_sort_rows(a, gtid, gthreads);
     }
+    __syncthreads();  // s_fc
     for (int it = 0; b < nchunks; ++it, b += gwarps) {
         if (b + gwarps < nchunks) prefetch(b + gwarps, (it + 1) & 1);
         cp_async_commit();
@@ -438,11 +493,36 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter_multi(const __grid
         float4 v[11];
 #pragma unroll
         for (int q = 0; q < 11; ++q) v[q] = *reinterpret_cast<const float4*>(st + q * kFilterBlock + lane * kFilterItems);
+        unsigned umask = 0;
+        if (m.shared_quick) {
+            QuickInv qi[kFilterItems];
+#pragma unroll
+            for (int it2 = 0; it2 < kFilterItems; ++it2) {
+                float p[11];
+#pragma unroll
+                for (int q = 0; q < 11; ++q) p[q] = (&v[q].x)[it2];
+                qi[it2] = quick_invariant(p, s_fc[0]);
+            }
 #pragma unroll 1
-        for (int k = 0; k < m.nb; ++k) {
-            const PrepLaunch& a = m.p[k];
-            cull_chunk(a, filter_consts(a.slice, m.log_tau[k]), m.log_tau[k], m.filter_on[k], b, i0, v, sx, nullptr,
-                       st);
+            for (int k = 0; k < m.nb; ++k) {
+                unsigned qmask = 0;
+#pragma unroll
+                for (int it2 = 0; it2 < kFilterItems; ++it2) qmask |= (quick_culled_pose(qi[it2], s_fc[k]) ? 1u : 0u) << it2;
+                umask |= cull_chunk(m.p[k], s_fc[k], m.log_tau[k], m.filter_on[k], b, i0, v, sx, nullptr, st, (int)qmask,
+                                    !m.union_words || k == m.own);
+            }
+        } else {
+#pragma unroll 1
+            for (int k = 0; k < m.nb; ++k)
+                umask |= cull_chunk(m.p[k], s_fc[k], m.log_tau[k], m.filter_on[k], b, i0, v, sx, nullptr, st, -1,
+                                    !m.union_words || k == m.own);
+        }
+        if (m.union_words) {
+#pragma unroll
+            for (int it2 = 0; it2 < kFilterItems; ++it2) {
+                const unsigned w = __ballot_sync(0xffffffffu, (umask >> it2) & 1u);
+                if (lane == 0) m.union_words[(uint64_t)b * kFilterItems + it2] = w;
+            }
         }
         __syncwarp();
     }
@@ -537,16 +617,23 @@ void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st) {
         launch_pdl(k_filter<false>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, filter_on ? 1 : 0);
 }
 
-void launch_prep_multi(const PrepLaunch* pl, int nb, int num_sms, cudaStream_t st) {
+void launch_prep_multi(const PrepLaunch* pl, int nb, int num_sms, cudaStream_t st, int own, unsigned* union_words) {
     if (nb < 1 || pl[0].n == 0) return;
     MultiPrep m;
     m.nb = nb;
+    m.own = own;
+    m.union_words = union_words;
+    m.shared_quick = 1;
     for (int k = 0; k < nb; ++k) {
         m.p[k] = pl[k];
         const SliceArgs& sl = pl[k].slice;
         const bool on = sl.tau > 0.0 && sl.mod > 1e-10 && sl.mod < 1e10 && sl.sigma_z > 1e-10 && sl.sigma_z < 1e10;
         m.filter_on[k] = on ? 1 : 0;
         m.log_tau[k] = on ? (float)log(sl.tau) : 0.f;
+        const SliceArgs& s0 = pl[0].slice;
+        if (!on || !sl.identity_rot || sl.t[0] != s0.t[0] || sl.t[1] != s0.t[1] || sl.sigma_z != s0.sigma_z ||
+            sl.tau != s0.tau || sl.mod != s0.mod)
+            m.shared_quick = 0;
     }
     static int per_sm = 0;
     if (!per_sm) {

@@ -184,9 +184,6 @@ struct gpk_session {
     std::vector<gpk_session*> ctxs;
     cudaEvent_t ev_bjoin = nullptr;  // a context's work of the batched step is done
     cudaEvent_t ev_ord = nullptr;    // a context's copies: ordered after / before its session's stream
-    // the latest gradient is a batched step's: the slices' slot gradients of
-    // these sessions (slice order), summed on demand (materialize_dense_grads)
-    std::vector<gpk_session*> batch_srcs;
     int ctx_used = 0;  // contexts a batched body used (graph capture snapshots their state)
 
     // voxelizer state (last voxelize / voxelize_backward)
@@ -212,7 +209,6 @@ struct gpk_session {
         cudaGraphExec_t exec;
         PrepState prep;
         std::vector<CtxSnap> ctx_state;       // batched graphs: the contexts' state they leave
-        std::vector<gpk_session*> batch_srcs;
         uint64_t alloc_epoch;
         bool needs_prefilter = false;  // pipelined train step: starts at K_decide
         bool sets_prefilter = false;   // ... and leaves next_pose culled
@@ -579,13 +575,6 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     ps.grads_zeroed = zero_grads;
     ps.ssim_pending = false;
     s->grads_in_slots = false;  // the survivor slots are about to change
-    {
-        gpk_session* o = s->owner ? s->owner : s;
-        if (std::find(o->batch_srcs.begin(), o->batch_srcs.end(), s) != o->batch_srcs.end()) {
-            o->batch_srcs.clear();  // a slice of the latest batched gradient is overwritten
-            o->grads_in_slots = false;
-        }
-    }
     const uint64_t nbf = filter_blocks(s->n);
     const size_t head_bytes = head_size(s->n);
     StageScope scope_prep(s, GPK_STAGE_PREPARE);
@@ -955,26 +944,6 @@ int adam_grad_source(gpk_session* s, AdamLaunch& a) {
 int materialize_dense_grads(gpk_session* s) {
     if (!s->grads_in_slots) return GPK_OK;
     s->grads_in_slots = false;
-    if (!s->batch_srcs.empty()) {
-        // a batched step's gradient: the slices' slot gradients added in slice
-        // order (the same fp32 sums its Adam formed)
-        if (s->capturing) return fail(GPK_ERR_STATE, "gradient layout change during capture");
-        std::vector<gpk_session*> srcs;
-        srcs.swap(s->batch_srcs);
-        CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
-        for (gpk_session* c : srcs) {
-            if (!c->prep.valid || c->n == 0) continue;
-            AdamLaunch a{};
-            a.grads = s->grads.as<float>();
-            a.cap = s->cap;
-            a.slot_grads = c->slot_grads.as<float>();
-            a.surv_gidx = c->survivors.as<uint32_t>();
-            a.grp_surv = c->grp_surv();
-            launch_scatter_slot_grads(a, (unsigned)decide_group_count(c->n), kScatterAdd, s->stream);
-            CK(cudaGetLastError());
-        }
-        return mark_grads_dense(s);
-    }
     if (!s->prep.valid || s->n == 0) return GPK_OK;
     if (s->capturing) return fail(GPK_ERR_STATE, "gradient layout change during capture");
     CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
@@ -2078,25 +2047,34 @@ static int batch_join(gpk_session* s, gpk_session* const* cx, int B) {
     return GPK_OK;
 }
 
-// The B slices' gradients summed into the dense planes (slice order), their
-// maps consumed.
-static int batch_dense_sum(gpk_session* s, gpk_session* const* cx, int B) {
-    CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
-    for (int k = 0; k < B; ++k) {
-        gpk_session* c = cx[k];
-        AdamLaunch a{};
-        a.grads = s->grads.as<float>();
-        a.cap = s->cap;
-        a.slot_grads = c->slot_grads.as<float>();
-        a.surv_gidx = c->survivors.as<uint32_t>();
-        a.grp_surv = c->grp_surv();
-        a.gmap = c->gmap.as<uint16_t>();
-        launch_scatter_slot_grads(a, (unsigned)decide_group_count(c->n), kScatterAdd | kScatterClearMap, s->stream);
-        CK(cudaGetLastError());
-        c->gmap_dirty = false;
-        c->grads_in_slots = false;
+// The B slices' gradients summed into the dense planes in slice order
+// (k_sum_slots: every entry written, every map read cleared).
+static AdamLaunch batch_sources(gpk_session* s, gpk_session* const* cx, int B) {
+    AdamLaunch a{};
+    a.grads = s->grads.as<float>();
+    a.cap = s->cap;
+    a.n = (uint32_t)s->n;
+    a.slot_grads = cx[0]->slot_grads.as<float>();
+    a.gmap = cx[0]->gmap.as<uint16_t>();
+    a.ctrl = cx[0]->ctrl();
+    a.nsrc = B - 1;
+    for (int k = 1; k < B; ++k) {
+        a.src_slot[k - 1] = cx[k]->slot_grads.as<float>();
+        a.src_gmap[k - 1] = cx[k]->gmap.as<uint16_t>();
+        a.src_ctrl[k - 1] = cx[k]->ctrl();
     }
-    s->batch_srcs.clear();
+    return a;
+}
+
+static int batch_dense_sum(gpk_session* s, gpk_session* const* cx, int B) {
+    if (s->n) {
+        launch_sum_slots(batch_sources(s, cx, B), s->stream);
+        CK(cudaGetLastError());
+    }
+    for (int k = 0; k < B; ++k) {
+        cx[k]->gmap_dirty = false;
+        cx[k]->grads_in_slots = false;
+    }
     s->grads_in_slots = false;
     return mark_grads_dense(s);
 }
@@ -2142,24 +2120,20 @@ static int train_batch_body(gpk_session* s, int B, const gpk_slice_pose* poses, 
         TRY(run_backward(c, false, /*slots=*/true));
     }
     TRY(batch_join(s, cx, B));
+    // the summed gradient into the dense planes, then the dense Adam (an
+    // overflowed slice anywhere skips the update, as k_adam checks every
+    // slice's control head)
+    TRY(batch_dense_sum(s, cx, B));
     if (s->n == 0) return run_adam(s, lr, true, total, nullptr);
     AdamLaunch a = adam_launch(s, lr, true, total, nullptr);
-    a.slot_grads = cx[0]->slot_grads.as<float>();
-    a.gmap = cx[0]->gmap.as<uint16_t>();
-    a.ctrl = cx[0]->ctrl();
-    a.nsrc = B - 1;
-    for (int k = 1; k < B; ++k) {
-        a.src_slot[k - 1] = cx[k]->slot_grads.as<float>();
-        a.src_gmap[k - 1] = cx[k]->gmap.as<uint16_t>();
-        a.src_ctrl[k - 1] = cx[k]->ctrl();
-    }
-    for (int k = 0; k < B; ++k) cx[k]->gmap_dirty = false;  // k_adam_batch consumes every map
-    s->batch_srcs.assign(cx, cx + B);
-    s->grads_in_slots = true;
+    const AdamLaunch src = batch_sources(s, cx, B);
+    a.ctrl = src.ctrl;
+    a.nsrc = src.nsrc;
+    for (int k = 0; k + 1 < B; ++k) a.src_ctrl[k] = src.src_ctrl[k];
     s->prefilter.valid = false;
     StageScope scope(s, GPK_STAGE_ADAM);
     TRY(adam_consts_ready(s, a));
-    launch_adam_batch(a, s->stream);
+    launch_adam(a, s->stream);
     CK(cudaGetLastError());
     return GPK_OK;
 }
@@ -2209,7 +2183,6 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
         gpk_session* c = s->ctxs[k];
         gr.ctx_state.push_back({c, c->prep, c->grads_in_slots, c->gmap_dirty});
     }
-    gr.batch_srcs = s->batch_srcs;
     gr.timed = std::move(timed);
     gr.needs_prefilter = meta.needs_prefilter;
     gr.sets_prefilter = meta.sets_prefilter;
@@ -2423,7 +2396,6 @@ int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
         cs.ctx->grads_in_slots = cs.grads_in_slots;
         cs.ctx->gmap_dirty = cs.gmap_dirty;
     }
-    s->batch_srcs = g.batch_srcs;
     if (s->timing && !g.timed.empty()) {
         // graph captured with stage timing: its event nodes bracket each stage
         // on the device, back to back (no host submission gaps)

@@ -24,7 +24,8 @@ from collections import defaultdict
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
-METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
            "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
            "launch__grid_size", "launch__block_size", "sm__inst_executed.avg.per_cycle_active"]
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3,
@@ -81,6 +82,8 @@ def full(rep: str, out: str, config: str) -> None:
             "duration_us": d["gpu__time_duration.sum"],
             "dram_read_bytes": d["dram__bytes_read.sum"],
             "dram_write_bytes": d["dram__bytes_write.sum"],
+            "l2_bytes": d["lts__t_bytes.sum"],
+            "smem_wavefronts": d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"],
             "warp_instructions": d["smsp__inst_executed.sum"],
             "registers": d["launch__registers_per_thread"],
             "grid": d["launch__grid_size"], "block": d["launch__block_size"],

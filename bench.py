@@ -20,9 +20,11 @@ step's target from pinned memory and reads the loss back; u1 uploads dL/dI and
 reads the image and the dense gradient back.
 
 Multi-GPU (torchrun): slices are sharded across ranks (rank r renders its own
-slice each step) with one NCCL all-reduce of the dense gradient per step (inside
-the u2 step, between backward and Adam); the value is all ranks' slices /
-max-over-ranks device time (weak scaling).
+slice of the step's world poses). u2 exchanges the gradient union-compacted
+(gpk_train_step_dp): every rank derives the union of the step's candidates in
+its own cull pass, one grouped NCCL all-reduce sums the union rows, every rank
+runs the same Adam. The value is all ranks' slices / max-over-ranks device
+time (weak scaling).
 
 --impl reference: the reference CPU implementation (oracle/_ref: the unmodified
 reference headers compiled here) on this host's cores, same unit, config and
@@ -557,7 +559,13 @@ def run_ours(args):
     def flush():
         torch.sum(flush_src, dim=0, out=flush_dst)
 
-    n_groups = len(poses) // B   # step i renders group i mod n_groups (B consecutive poses)
+    # step i renders group i mod n_groups (B consecutive poses); data-parallel
+    # u2: step i's world poses (dp.step_slices), rank r renders the r-th
+    dp_union = u2 and world > 1
+    n_groups = len(poses) // (world if dp_union else B)
+
+    def step_poses(k):
+        return [poses[j] for j in dp.step_slices(k, world, len(poses))]
 
     def group(k, nb=None):
         nb = nb or B
@@ -565,6 +573,8 @@ def run_ours(args):
 
     def capture(k, nb=None):
         nb = nb or B
+        if dp_union:
+            return sess.capture_train_dp(world, rank, step_poses(k), psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS)
         if nb > 1:
             return (sess.capture_train_batch(group(k, nb), psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS) if u2
                     else sess.capture_fwd_bwd_batch(group(k, nb), psf, rcfg))
@@ -575,13 +585,25 @@ def run_ours(args):
                                       next_pose=poses[(k + world) % len(poses)] if args.pipeline else None)
         return sess.capture_fwd_bwd(poses[k], psf, rcfg)
 
+    union_rows = [(0, 0)]
+    if dp_union:
+        # the union row capacity (the all-reduce count, baked into the graphs)
+        # grows on direct steps; every rank runs the same steps, so every rank
+        # ends with the same capacity
+        for k in range(n_groups):
+            sess.train_step_dp(world, rank, step_poses(k), psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS)
+        sess.synchronize()
+        union_rows = [sess.dp_union_rows()]
+
     # one CUDA graph per slice pose (group of B poses): the whole step is one submission
     graphs = [capture(k) for k in range(n_groups)] if args.graphs else None
 
     def step(i):
-        k = dp.slice_for(i, rank, world, n_groups)
+        k = i % n_groups if dp_union else dp.slice_for(i, rank, world, n_groups)
         if graphs is not None:
             sess.graph_launch(graphs[k])
+        elif dp_union:
+            sess.train_step_dp(world, rank, step_poses(k), psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS)
         elif B > 1:
             if u2:
                 sess.train_step_batch(group(k), psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS)
@@ -668,7 +690,8 @@ def run_ours(args):
     sess.stage_times(reset=True)
     for i in range(prof_steps):
         flush()
-        sess.graph_launch(prof_graphs[dp.slice_for(args.warmup + i, rank, world, n_groups)])
+        j = args.warmup + i
+        sess.graph_launch(prof_graphs[j % n_groups if dp_union else dp.slice_for(j, rank, world, n_groups)])
     sess.stage_timing(False)
     stages = sess.stage_times(reset=True)
 
@@ -768,8 +791,8 @@ def run_ours(args):
         ("k_adam", 266 * n + 44 * S,
          "266N + 44S: read params, m, v, 2 B slot map; write params, m, v; survivor gradients")
         if world == 1 else
-        ("k_adam", 308 * n / world,
-         "308N/world: the rank's shard (read params, dense gradients, m, v; write params, m, v)"),
+        ("k_adam", 268 * n + 44 * union_rows[0][0],
+         "268N + 44M: read params, m, v, 4 B union map; write params, m, v; the M summed union rows"),
     }
     measured = {k: v for k, v in stages.items() if v[1] > 0 and k in kernel_bytes}
     dom = max(measured, key=lambda k: measured[k][0])
@@ -803,8 +826,8 @@ def run_ours(args):
     # U2 floor with slot gradients: 44N cull read + 264N Adam (p, m, v read and
     # written) + 2N slot map (SURVEY.md §8d's 396N assumed dense gradient
     # planes: +44N Adam read, +44N clear)
-    step_bytes = ((310 * n + 8 * P) if world == 1 else (44 * n + 308 * n / world + 8 * P)) if u2 \
-        else (88 * n + 8 * P)
+    step_bytes = ((310 * n + 8 * P) if world == 1 else (44 * n + 4 * n + 268 * n + 88 * union_rows[0][0] + 8 * P)) \
+        if u2 else (88 * n + 8 * P)
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
 
     line = {
@@ -815,7 +838,8 @@ def run_ours(args):
         "roofline": roof,
         "step_roofline": {"bytes_per_step": step_bytes, "achieved_gbs": step_gbs, "frac": step_gbs / peak,
                           "formula": (("310N + 8P (U2 with slot gradients; SURVEY.md §8d: 396N dense)" if world == 1
-                                       else "44N + 308N/world + 8P per rank (U2, sharded Adam; collectives excluded)")
+                                       else "44N cull + 4N union map + 268N Adam + 88M union rows + 8P per rank "
+                                            "(U2, union-compacted exchange; the all-reduce excluded)")
                                       if u2 else "88N + 8P (U1, SURVEY.md §8d)")},
         "steady_state": {"ms_per_step": ss_ms, "value": world * B * 1000.0 / ss_ms, "steps": ss_steps,
                          "note": "no L2 flush between steps (back-to-back training loop)"},
@@ -831,6 +855,10 @@ def run_ours(args):
         "gpu_launches": None,
         "clocks": clk.result(),
     }
+    if dp_union:
+        line["exchange"] = {"kind": "union-compacted: one grouped ncclAllReduce of the step's union rows",
+                            "union_rows": union_rows[0][0], "row_capacity": union_rows[0][1],
+                            "bytes_per_rank": 44 * union_rows[0][1], "dense_bytes": 44 * n}
     if batched:
         line["batched"] = batched
     # per slice: filter + decide + (gather | radix passes) + forward + backward + chain + chain_exact;
@@ -839,7 +867,7 @@ def run_ours(args):
     # Adam); u1 x B: + one gradient scatter per slice. Memsets are not kernels.
     sort_k = passes if passes > 1 else (0 if u2 else 1)
     per_slice = 2 + sort_k + 4 + (1 if u2 else 0)
-    launches = B * per_slice + (2 if u2 else (B if B > 1 else 0))
+    launches = B * per_slice + (2 if u2 else (B if B > 1 else 0)) + (2 if dp_union else 0)  # + union scan, map
     if u2 and args.pipeline:
         launches -= 1
     line["gpu_launches"] = launches * args.steps

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GPK_ABI_VERSION 5
+#define GPK_ABI_VERSION 6
 #define GPK_RECORD_FLOATS 11
 
 typedef enum {
@@ -119,7 +119,9 @@ typedef enum {
     GPK_BUF_TARGET = 4,   /* W*H f32: target slice for the photometric loss */
     GPK_BUF_VOLUME = 5,   /* X*Y*Z f32: voxelize output */
     GPK_BUF_DL_DV = 6,    /* X*Y*Z f32: dL/dV consumed by voxelize_backward */
-    GPK_BUF_LOSS = 7      /* 1 f64: last photometric loss */
+    GPK_BUF_LOSS = 7,     /* 1 f64: last photometric loss */
+    GPK_BUF_UNION_ROWS = 8  /* 11 f32 planes x capacity: a data-parallel step's union gradient rows
+                               (rows [0, union capacity) of each plane; gpk_train_step_dp) */
 } gpk_buffer;
 
 /* ---- library ------------------------------------------------------------ */
@@ -485,6 +487,36 @@ int gpk_comm_init(gpk_session* s, int nranks, int rank, const void* id128);
 int gpk_comm_destroy(gpk_session* s);
 /* Sum GPK_BUF_GRADS across ranks (one ncclAllReduce, in place, session stream). */
 int gpk_allreduce_grads(gpk_session* s);
+
+/* Data-parallel training step with the union-compacted exchange (SURVEY.md
+ * §7.3.8, §8e). Every rank passes the step's `world` slice poses in rank order
+ * (the shared schedule) and renders poses[rank]. In its cull pass each rank
+ * also evaluates the other poses' certain-cull, so every rank derives the same
+ * union of candidates (a superset of every rank's survivors) without a
+ * collective; its chain writes the survivors' gradients into rows of that
+ * union (GPK_BUF_UNION_ROWS); ONE grouped ncclAllReduce sums the rows; every
+ * rank runs the scheduled Adam on all Gaussians from the summed rows, so the
+ * replicas stay bitwise equal. phases: a bitmask of GPK_DP_RENDER,
+ * GPK_DP_EXCHANGE, GPK_DP_UPDATE (GPK_DP_ALL = the step; the exchange needs
+ * gpk_comm_init; the split lets a caller exchange the rows itself). world <= 8.
+ * A direct call sizes the row capacity (the all-reduce count) from the union
+ * it computed; graphs bake it (gpk_dp_reserve_union before capture). */
+#define GPK_DP_RENDER 1
+#define GPK_DP_EXCHANGE 2
+#define GPK_DP_UPDATE 4
+#define GPK_DP_ALL 7
+int gpk_train_step_dp(gpk_session* s, int32_t world, int32_t rank, const gpk_slice_pose* poses, const gpk_psf* psf,
+                      const gpk_raster_config* cfg, double lambda, double dssim_scale, const gpk_learning_rates* lr0,
+                      int32_t total_iterations, int32_t phases);
+int gpk_graph_capture_train_dp(gpk_session* s, int32_t world, int32_t rank, const gpk_slice_pose* poses,
+                               const gpk_psf* psf, const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                               const gpk_learning_rates* lr0, int32_t total_iterations, int32_t* graph_id);
+/* Union rows of the last step and the exchange capacity (synchronizes);
+ * GPK_ERR_STATE when the union outgrew a captured capacity (that step's
+ * update was skipped). */
+int gpk_dp_union_rows(gpk_session* s, uint64_t* rows, uint64_t* capacity);
+/* Set the exchanged row capacity (every rank the same value). */
+int gpk_dp_reserve_union(gpk_session* s, uint64_t rows);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libgpile_b200.so"
-GPK_ABI_VERSION = 5  # include/gpile_b200.h
+GPK_ABI_VERSION = 6  # include/gpile_b200.h
 
 GPK_OK = 0
 GPK_ERR_INVALID_ARGUMENT = 1
@@ -27,7 +27,8 @@ GPK_ERR_CORRUPT_CONTAINER = 8
 GPK_ERR_LOAD = 9
 
 GPK_BUF_PARAMS, GPK_BUF_GRADS, GPK_BUF_IMAGE, GPK_BUF_DL_DI, GPK_BUF_TARGET = 0, 1, 2, 3, 4
-GPK_BUF_VOLUME, GPK_BUF_DL_DV, GPK_BUF_LOSS = 5, 6, 7
+GPK_BUF_VOLUME, GPK_BUF_DL_DV, GPK_BUF_LOSS, GPK_BUF_UNION_ROWS = 5, 6, 7, 8
+GPK_DP_RENDER, GPK_DP_EXCHANGE, GPK_DP_UPDATE, GPK_DP_ALL = 1, 2, 4, 7
 
 
 class Bounds(C.Structure):
@@ -198,6 +199,14 @@ _PROTOS = {
     "gpk_train_step_next": (C.c_int, [_P, C.POINTER(SlicePoseC), C.POINTER(PsfC), C.POINTER(RasterConfigC),
                                  C.c_double, C.c_double, C.POINTER(LearningRatesC), C.c_int32, C.POINTER(SlicePoseC)]),
     "gpk_slice_context": (C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
+    "gpk_train_step_dp": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(SlicePoseC), C.POINTER(PsfC),
+                                    C.POINTER(RasterConfigC), C.c_double, C.c_double, C.POINTER(LearningRatesC),
+                                    C.c_int32, C.c_int32]),
+    "gpk_graph_capture_train_dp": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(SlicePoseC), C.POINTER(PsfC),
+                                             C.POINTER(RasterConfigC), C.c_double, C.c_double,
+                                             C.POINTER(LearningRatesC), C.c_int32, C.POINTER(C.c_int32)]),
+    "gpk_dp_union_rows": (C.c_int, [_P, _U64, _U64]),
+    "gpk_dp_reserve_union": (C.c_int, [_P, C.c_uint64]),
     "gpk_fwd_bwd_batch": (C.c_int, [_P, C.c_int32, C.POINTER(SlicePoseC), C.POINTER(PsfC),
                                     C.POINTER(RasterConfigC)]),
     "gpk_train_step_batch": (C.c_int, [_P, C.c_int32, C.POINTER(SlicePoseC), C.POINTER(PsfC),

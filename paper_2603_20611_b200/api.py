@@ -640,6 +640,35 @@ class Session:
         self.shape = (poses[0].height, poses[0].width)
         return int(gid.value)
 
+    # data parallelism with the union-compacted exchange (gpk_train_step_dp)
+    def train_step_dp(self, world: int, rank: int, poses, psf: PsfSpec, cfg: RasterConfig, lam: float,
+                      dssim_scale: float, lr0: LearningRates, total_iterations: int, phases: int = 7):
+        """Rank `rank` of `world` renders poses[rank]; the gradients of the union
+        of the step's candidates are summed across ranks (phases: 1 render, 2
+        exchange (NCCL), 4 update)."""
+        arr, f, c, l = self._poses(poses), psf.to_c(), cfg.to_c(), lr0.to_c()
+        check(N.lib.gpk_train_step_dp(self._h, int(world), int(rank), arr, C.byref(f), C.byref(c), lam, dssim_scale,
+                                      C.byref(l), int(total_iterations), int(phases)))
+        self.shape = (poses[rank].height, poses[rank].width)
+
+    def capture_train_dp(self, world: int, rank: int, poses, psf: PsfSpec, cfg: RasterConfig, lam: float,
+                         dssim_scale: float, lr0: LearningRates, total_iterations: int) -> int:
+        arr, f, c, l = self._poses(poses), psf.to_c(), cfg.to_c(), lr0.to_c()
+        gid = C.c_int32()
+        check(N.lib.gpk_graph_capture_train_dp(self._h, int(world), int(rank), arr, C.byref(f), C.byref(c), lam,
+                                               dssim_scale, C.byref(l), int(total_iterations), C.byref(gid)))
+        self.shape = (poses[rank].height, poses[rank].width)
+        return int(gid.value)
+
+    def dp_union_rows(self) -> tuple[int, int]:
+        """(rows of the last step's union, exchanged row capacity)."""
+        r, c = C.c_uint64(), C.c_uint64()
+        check(N.lib.gpk_dp_union_rows(self._h, C.byref(r), C.byref(c)))
+        return int(r.value), int(c.value)
+
+    def dp_reserve_union(self, rows: int):
+        check(N.lib.gpk_dp_reserve_union(self._h, int(rows)))
+
     def graph_launch(self, graph_id: int):
         check(N.lib.gpk_graph_launch(self._h, int(graph_id)))
 

@@ -36,8 +36,9 @@ __global__ void __launch_bounds__(256, kMinB) k_adam(const AdamLaunch a) {
     if (i0 >= a.n) return;  // the capacity is a multiple of 512: vector accesses stay in the plane
     bool overflow = a.ctrl && a.ctrl->pair_overflow;  // a slice overflowed: no update
     for (int s = 0; s < a.nsrc; ++s) overflow |= a.src_ctrl[s]->pair_overflow != 0;  // (batched step)
+    if (a.uctrl) overflow |= a.uctrl[1] != 0;  // (data-parallel union rows beyond the capacity)
     if (overflow) {
-        if (kSlots) adam_slots_clear<kAdamItems>(a, i0);
+        if (kSlots && !a.umap) adam_slots_clear<kAdamItems>(a, i0);
         return;
     }
     // read in place (L1) where used: the constants would otherwise hold 12

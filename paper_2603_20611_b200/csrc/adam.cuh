@@ -119,6 +119,17 @@ __device__ __forceinline__ Pack<N> adam_grad(const AdamLaunch& a, int k, uint32_
 // clears those map entries (adam_slots_clear) so the map is zero again.
 template <int N>
 __device__ __forceinline__ bool adam_slots(const AdamLaunch& a, uint32_t i0, uint32_t gslot[N]) {
+    if (a.umap) {  // data-parallel union rows: the map is rebuilt every step, never cleared
+        bool any = false;
+#pragma unroll
+        for (int l = 0; l < N; ++l) {
+            const uint32_t m = a.umap[i0 + l];
+            gslot[l] = m ? m - 1 : kNoSlot;
+            any |= m != 0;
+        }
+        (void)any;
+        return false;  // nothing to clear
+    }
     uint16_t m[N];
     if constexpr (N == 4) {
         const uint2 t = *reinterpret_cast<const uint2*>(a.gmap + i0);

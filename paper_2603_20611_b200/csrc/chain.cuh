@@ -35,9 +35,14 @@ __device__ __forceinline__ void store_chain(const ChainLaunch& a, uint32_t i, ui
                         isfinite(g[3] + g[4] + g[5]) && isfinite(g[6] + g[7] + g[8] + g[9]);
     if (!finite) record_error(a.err, kErrNumeric, i);  // backward.hpp:175-185
     float* dst = a.slot_grads ? a.slot_grads + cid : a.grads + i;
+    if (a.urows) {  // data-parallel union row (a survivor is always in the union)
+        const uint32_t m = a.umap[i];
+        dst = (m && m - 1 < a.ucap) ? a.urows + (m - 1) : nullptr;
+    }
+    if (dst)
 #pragma unroll
-    for (int k = 0; k < 11; ++k) dst[(uint64_t)k * a.cap] = g[k];
-    if (a.slot_grads) a.gmap[i] = (uint16_t)(cid % kDecideGroupSize + 1);
+        for (int k = 0; k < 11; ++k) dst[(uint64_t)k * a.cap] = g[k];
+    if (a.slot_grads && !a.urows) a.gmap[i] = (uint16_t)(cid % kDecideGroupSize + 1);
     if (a.stat_norm) a.stat_norm[i] = (float)sqrt(acc[1] * acc[1] + acc[2] * acc[2]);
     if (a.stat_observed) a.stat_observed[i] = 1;
     if (a.stat_world) {

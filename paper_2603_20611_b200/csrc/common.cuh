@@ -558,6 +558,11 @@ struct ChainLaunch {
     float* grads;                  // dense gradient planes (set-indexed) ...
     float* slot_grads;             // ... or, when non-null, slot-indexed planes (see AdamLaunch)
     uint16_t* gmap;                // slot mode: 1 + the survivor's offset in its group, by set index
+    // data-parallel union rows (dp.cu): when urows is non-null the gradient of
+    // set index i goes to row umap[i] - 1 of 11 planes (stride cap), rows < ucap
+    const uint32_t* umap;
+    float* urows;
+    uint64_t ucap;
     float* stat_norm;              // optional (screen-space dL/dmu_2d norm)
     uint8_t* stat_observed;        // optional
     float* stat_world;             // optional, 3 per primitive
@@ -612,6 +617,11 @@ struct AdamLaunch {
     // primitive's gradient over the slices in slice order (slice 0 =
     // slot_grads / gmap above) into the dense planes and clears every map it
     // reads; src_ctrl: an overflowed slice anywhere skips the update.
+    // data-parallel step (dp.cu): when umap is non-null the gradient of
+    // Gaussian i is row umap[i] - 1 of slot_grads (0: zero gradient), and
+    // uctrl[1] != 0 (union rows beyond the capacity) skips the update
+    const uint32_t* umap;
+    const unsigned* uctrl;
     int nsrc;                     // further slices (0: a single slice)
     const float* src_slot[kMaxBatch - 1];
     uint16_t* src_gmap[kMaxBatch - 1];
@@ -740,6 +750,12 @@ void launch_vox_bwd(const VoxEvalLaunch& a, cudaStream_t st);
 void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st);
 
 void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st);
+// dp.cu: the data-parallel union numbering and its dense view
+void launch_union_scan(const unsigned* words, unsigned nchunks, unsigned* prefix, unsigned* uctrl, uint64_t ucap,
+                       cudaStream_t st);
+void launch_union_map(const unsigned* words, const unsigned* prefix, uint32_t n, uint32_t* umap, cudaStream_t st);
+void launch_union_to_dense(const uint32_t* umap, const float* rows, uint64_t cap, uint32_t n, uint64_t ucap,
+                           float* grads, cudaStream_t st);
 // own / union_words: a data-parallel step (only pose `own` stores candidates;
 // the union of every pose's candidates as 4 words per 128-Gaussian chunk)
 void launch_prep_multi(const PrepLaunch* pl, int nb, int num_sms, cudaStream_t st, int own = -1,

@@ -94,12 +94,6 @@ __device__ __forceinline__ bool certainly_culled_identity(const float p[11], con
     return 0.5f * q > thresh + margin;
 }
 
-__device__ __forceinline__ void load_params(const float* __restrict__ params, uint64_t cap,
-                                            uint32_t i, float p[11]) {
-#pragma unroll
-    for (int k = 0; k < 11; ++k) p[k] = __ldg(params + (uint64_t)k * cap + i);
-}
-
 
 // Cheapest certain-cull for R_c = I, division-free: lower-bounds q by replacing
 // the projected variance Sigma_c,zz with its maximum (mod * s_max)^2, upper-
@@ -478,6 +472,7 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter_multi(const __grid
     cp_async_commit();
     if (tid < m.nb) s_fc[tid] = filter_consts(m.p[tid].slice, m.log_tau[tid]);
     for (int k = 0; k < m.nb; ++k) {
+        if (m.union_words && k != m.own) continue;  // verdict-only poses own no buffers
         const PrepLaunch& a = m.p[k];
         for (unsigned w = gtid; w < a.head_words; w += gthreads) a.head[w] = 0u;
         clear_prev_sort_rows(a, gtid, gthreads);

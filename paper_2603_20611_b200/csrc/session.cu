@@ -143,6 +143,10 @@ struct gpk_session {
     DevBuf dirty_idx;  // set indices of the last backward's survivors
     DevBuf slot_grads; // training-step gradients by survivor slot (11 planes, stride cap)
     bool grads_in_slots = false;  // the latest gradient lives in slot_grads (see AdamLaunch)
+    // data-parallel union rows (dp.cu, gpk_train_step_dp)
+    DevBuf union_words, union_prefix, umap, urows, uctrl;
+    uint64_t ucap = 0;             // rows exchanged per plane (the all-reduce count), <= cap
+    bool grads_in_union = false;   // the latest gradient is a data-parallel step's union rows
     DevBuf gmap;       // slot mode: u16 per primitive, 1 + survivor offset in its group (else 0)
     bool gmap_dirty = false;      // a slot backward wrote gmap and no Adam consumed (cleared) it
     DevBuf grp_table;  // per K_decide group: uint2 (first pair, pairs), then u32 survivors
@@ -214,6 +218,7 @@ struct gpk_session {
         bool sets_prefilter = false;   // ... and leaves next_pose culled
         bool writes_params = false;
         bool grads_in_slots = false;   // where the graph leaves the gradient
+        bool grads_in_union = false;
         bool gmap_dirty = false;
         gpk_slice_pose next_pose{};
         std::vector<Pending> timed;  // event-record nodes captured with stage timing on
@@ -737,12 +742,14 @@ int run_rasterize(gpk_session* s, cudaStream_t on = nullptr) {
 
 // slots: the chain writes the gradient by survivor slot (single-GPU training
 // step: Adam reads it there) instead of into the dense planes.
-int run_backward(gpk_session* s, bool stats, bool slots = false) {
+// union: the chain writes the data-parallel union rows (train_dp_body).
+int run_backward(gpk_session* s, bool stats, bool slots = false, bool urows = false) {
     if (!s->prep.valid) return fail(GPK_ERR_STATE, "backward: no prepared slice");
     s->prefilter.valid = false;  // the chain writes gradients
     TRY(clear_gmap(s));
     TRY(ensure_lists(s));
-    s->grads_in_slots = slots && s->n;
+    s->grads_in_union = urows && s->n;
+    s->grads_in_slots = slots && !urows && s->n;
     s->gmap_dirty = s->grads_in_slots;
     if (s->n == 0) return GPK_OK;
     if (!slots && !s->prep.grads_zeroed) {
@@ -776,6 +783,9 @@ int run_backward(gpk_session* s, bool stats, bool slots = false) {
     c.grads = s->grads.as<float>();
     c.slot_grads = slots ? s->slot_grads.as<float>() : nullptr;
     c.gmap = s->gmap.as<uint16_t>();
+    c.umap = urows ? s->umap.as<uint32_t>() : nullptr;
+    c.urows = urows ? s->urows.as<float>() : nullptr;
+    c.ucap = s->ucap;
     c.stat_norm = stats ? s->stat_norm.as<float>() : nullptr;
     c.stat_observed = stats ? s->stat_obs.as<uint8_t>() : nullptr;
     c.stat_world = stats ? s->stat_world.as<float>() : nullptr;
@@ -888,6 +898,7 @@ int alloc_slice_bufs(gpk_session* s, uint64_t cap) {
     CK(s->gmap.ensure(cap * 2));
     CK(cudaMemsetAsync(s->gmap.p, 0, cap * 2, s->stream));
     s->grads_in_slots = false;
+    s->grads_in_union = false;
     s->gmap_dirty = false;
     TRY(mark_grads_dense(s));
     CK(s->survivors.ensure(cap * 4));
@@ -942,6 +953,14 @@ int adam_grad_source(gpk_session* s, AdamLaunch& a) {
 // Make the dense planes hold the latest gradient (API readers and writers of
 // GPK_BUF_GRADS, the all-reduce): scatter the slot gradient if it lives there.
 int materialize_dense_grads(gpk_session* s) {
+    if (s->grads_in_union) {  // a data-parallel step's summed gradient: its union rows, densely
+        s->grads_in_union = false;
+        if (s->capturing) return fail(GPK_ERR_STATE, "gradient layout change during capture");
+        launch_union_to_dense(s->umap.as<uint32_t>(), s->urows.as<float>(), s->cap, (uint32_t)s->n, s->ucap,
+                              s->grads.as<float>(), s->stream);
+        CK(cudaGetLastError());
+        return mark_grads_dense(s);
+    }
     if (!s->grads_in_slots) return GPK_OK;
     s->grads_in_slots = false;
     if (!s->prep.valid || s->n == 0) return GPK_OK;
@@ -1325,7 +1344,8 @@ static int session_destroy(gpk_session* s) {
                       &s->sort_status, &s->head, &s->persist, &s->image,
                       &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm, &s->acc_norm, &s->acc_obs, &s->acc_world,
                       &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table, &s->bucket_tab,
-                      &s->dirty_idx, &s->vox_records, &s->slot_grads, &s->gmap,
+                      &s->dirty_idx, &s->vox_records, &s->slot_grads, &s->gmap, &s->union_words,
+                      &s->union_prefix, &s->umap, &s->urows, &s->uctrl,
                       &s->volume, &s->dl_dv_vol, &s->vox_partials};
     for (DevBuf* b : bufs) b->release();
     drain_timing(s);
@@ -1418,6 +1438,7 @@ int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
             b = px * 4;
             break;
         case GPK_BUF_LOSS: p = s->loss(); b = 8; break;
+        case GPK_BUF_UNION_ROWS: p = s->urows.p; b = s->urows.p ? s->cap * 44 : 0; break;
         case GPK_BUF_VOLUME: p = s->volume.p; b = s->vox.voxels * 4; break;
         case GPK_BUF_DL_DV: p = s->dl_dv_vol.p; b = s->vox.voxels * 4; break;
         default: return fail(GPK_ERR_INVALID_ARGUMENT, "unknown or unallocated buffer");
@@ -1556,6 +1577,7 @@ int gpk_set_gradients(gpk_session* s, const float* grads) {
     CK(cudaStreamSynchronize(s->stream));
     if (s->n) TRY(copy_records_in(s, s->n, grads, s->grads.as<float>()));
     s->grads_in_slots = false;
+    s->grads_in_union = false;
     TRY(mark_grads_dense(s));
     CK(cudaStreamSynchronize(s->stream));
     return ok();
@@ -2076,6 +2098,7 @@ static int batch_dense_sum(gpk_session* s, gpk_session* const* cx, int B) {
         cx[k]->grads_in_slots = false;
     }
     s->grads_in_slots = false;
+    s->grads_in_union = false;
     return mark_grads_dense(s);
 }
 
@@ -2138,6 +2161,100 @@ static int train_batch_body(gpk_session* s, int B, const gpk_slice_pose* poses, 
     return GPK_OK;
 }
 
+// ---- data-parallel step with the union-compacted exchange (dp.cu) -----------------
+static int dp_union_allreduce(gpk_session* s);
+
+// Buffers of the union exchange (sized by the plane stride; outside capture).
+static int dp_union_alloc(gpk_session* s) {
+    const void* before[3] = {s->union_words.p, s->umap.p, s->urows.p};
+    CK(s->union_words.ensure(filter_blocks(s->cap) * kFilterItems * 4));
+    CK(s->union_prefix.ensure(filter_blocks(s->cap) * 4));
+    CK(s->umap.ensure(s->cap * 4));
+    CK(s->urows.ensure(s->cap * 44));
+    CK(s->uctrl.ensure(16));
+    if (before[0] != s->union_words.p || before[1] != s->umap.p || before[2] != s->urows.p) {
+        if (s->capturing) return fail(GPK_ERR_STATE, "union buffers must be sized before capture");
+        ++s->alloc_epoch;
+    }
+    if (s->ucap == 0 || s->ucap > s->cap) s->ucap = std::min<uint64_t>(s->cap, std::max<uint64_t>(1u << 16, s->n / 8));
+    return GPK_OK;
+}
+
+// One data-parallel training step, rank `rank` of `world`, rendering
+// poses[rank] (optimize.hpp:385-402 per rank). phases: GPK_DP_RENDER (union,
+// prepare, render, loss, backward into the union rows), GPK_DP_EXCHANGE (the
+// grouped all-reduce of the rows), GPK_DP_UPDATE (Adam on every Gaussian from
+// its summed row).
+static int train_dp_body(gpk_session* s, int world, int rank, const gpk_slice_pose* poses, const gpk_psf* psf,
+                         const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                         const gpk_learning_rates* lr0, int32_t total, int phases) {
+    const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
+    if (phases & GPK_DP_RENDER) {
+        TRY(dp_union_alloc(s));
+        if (s->n) TRY(adam_consts_ahead(s, adam_launch(s, lr, true, total, nullptr)));
+        TRY(presize_step(s, &poses[rank], psf, cfg, true, lambda));
+        if (s->n) {
+            PrepLaunch pl[kMaxBatch];
+            for (int k = 0; k < world; ++k) {
+                SliceArgs a;
+                TRY(make_slice(s, &poses[k], psf, cfg, a));
+                int passes = 0, bits = 0;
+                sort_plan(a.tiles_x * a.tiles_y, passes, bits);
+                pl[k] = prep_launch(s, a, passes, bits, false);
+            }
+            pl[rank].head = s->head.as<unsigned>();
+            pl[rank].head_words = (unsigned)(head_size(s->n) / 4);
+            {
+                StageScope scope(s, GPK_STAGE_PREPARE);
+                launch_prep_multi(pl, world, s->num_sms, s->stream, rank, s->union_words.as<unsigned>());
+                CK(cudaGetLastError());
+                launch_union_scan(s->union_words.as<unsigned>(), (unsigned)filter_blocks(s->n),
+                                  s->union_prefix.as<unsigned>(), s->uctrl.as<unsigned>(), s->ucap, s->stream);
+                CK(cudaGetLastError());
+                launch_union_map(s->union_words.as<unsigned>(), s->union_prefix.as<unsigned>(), (uint32_t)s->n,
+                                 s->umap.as<uint32_t>(), s->stream);
+                CK(cudaGetLastError());
+            }
+            if (!s->capturing) {
+                // direct call: the union size decides the exchange count; every
+                // rank computes the same union, so every rank grows alike
+                unsigned u[2];
+                CK(cudaMemcpyAsync(u, s->uctrl.p, 8, cudaMemcpyDeviceToHost, s->stream));
+                CK(cudaStreamSynchronize(s->stream));
+                if (u[1]) {
+                    s->ucap = std::min<uint64_t>(s->cap, (uint64_t)u[0] + u[0] / 4 + 1024);
+                    CK(cudaMemsetAsync(s->uctrl.as<unsigned>() + 1, 0, 4, s->stream));
+                }
+            }
+            for (int k = 0; k < 11; ++k)
+                CK(cudaMemsetAsync(s->urows.as<float>() + (size_t)k * s->cap, 0, s->ucap * 4, s->stream));
+        }
+        s->fuse_gather = true;
+        const int pst = run_prepare(s, &poses[rank], psf, cfg, false, /*filtered=*/s->n != 0);
+        s->fuse_gather = false;
+        TRY(pst);
+        TRY(run_rasterize(s));
+        TRY(run_loss(s, lambda, dssim_scale, true));
+        TRY(run_backward(s, false, /*slots=*/true, /*urows=*/true));
+    }
+    if (phases & GPK_DP_EXCHANGE) TRY(dp_union_allreduce(s));
+    if (phases & GPK_DP_UPDATE) {
+        if (!s->urows.p) return fail(GPK_ERR_STATE, "data-parallel update before its render phase");
+        if (s->n == 0) return run_adam(s, lr, true, total, nullptr);
+        AdamLaunch a = adam_launch(s, lr, true, total, nullptr);
+        a.slot_grads = s->urows.as<float>();
+        a.umap = s->umap.as<uint32_t>();
+        a.uctrl = s->uctrl.as<unsigned>();
+        s->prefilter.valid = false;
+        StageScope scope(s, GPK_STAGE_ADAM);
+        TRY(adam_consts_ready(s, a));
+        launch_adam(a, s->stream);
+        CK(cudaGetLastError());
+        s->grads_in_union = true;
+    }
+    return GPK_OK;
+}
+
 // ---- CUDA graphs -------------------------------------------------------------
 static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_session*, const void*),
                          const void* arg) {
@@ -2177,6 +2294,7 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
     gr.exec = ex;
     gr.prep = s->prep;
     gr.grads_in_slots = s->grads_in_slots;
+    gr.grads_in_union = s->grads_in_union;
     gr.gmap_dirty = s->gmap_dirty;
     gr.alloc_epoch = epoch_total(s);
     for (int k = 0; k < s->ctx_used; ++k) {
@@ -2366,6 +2484,38 @@ int gpk_graph_capture_train_batch(gpk_session* s, int32_t nslices, const gpk_sli
     }, &args);
 }
 
+static int dp_check(gpk_session* s, int world, int rank, const gpk_slice_pose* poses, const gpk_learning_rates* lr0,
+                    int total);
+
+struct DpArgs {
+    int world, rank;
+    const gpk_slice_pose* poses;
+    const gpk_psf* psf;
+    const gpk_raster_config* cfg;
+    double lambda, dssim;
+    const gpk_learning_rates* lr0;
+    int total;
+};
+
+int gpk_graph_capture_train_dp(gpk_session* s, int32_t world, int32_t rank, const gpk_slice_pose* poses,
+                               const gpk_psf* psf, const gpk_raster_config* cfg, double lambda, double dssim_scale,
+                               const gpk_learning_rates* lr0, int32_t total_iterations, int32_t* graph_id) {
+    TRY(dp_check(s, world, rank, poses, lr0, total_iterations));
+    if (!s->comm) return fail(GPK_ERR_STATE, "exchange: communicator not initialized");
+    TRY(set_device(s));
+    TRY(dp_union_alloc(s));
+    TRY(presize_step(s, &poses[rank], psf, cfg, true, lambda));
+    const DpArgs args{world, rank, poses, psf, cfg, lambda, dssim_scale, lr0, total_iterations};
+    s->capture_meta.writes_params = true;
+    return capture_graph(s, graph_id, [](gpk_session* ss, const void* p) -> int {
+        const DpArgs* a = static_cast<const DpArgs*>(p);
+        const int st = train_dp_body(ss, a->world, a->rank, a->poses, a->psf, a->cfg, a->lambda, a->dssim, a->lr0,
+                                     a->total, GPK_DP_RENDER | GPK_DP_EXCHANGE | GPK_DP_UPDATE);
+        if (st != GPK_OK) ss->consts_pending = false;
+        return st;
+    }, &args);
+}
+
 int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
     if (!s || graph_id < 0 || graph_id >= (int32_t)s->graphs.size())
         return fail(GPK_ERR_INVALID_ARGUMENT, "unknown graph id");
@@ -2390,6 +2540,7 @@ int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
         s->prefilter.valid = false;
     s->prep = g.prep;
     s->grads_in_slots = g.grads_in_slots;
+    s->grads_in_union = g.grads_in_union;
     s->gmap_dirty = g.gmap_dirty;
     for (const auto& cs : g.ctx_state) {
         cs.ctx->prep = cs.prep;
@@ -2566,6 +2717,66 @@ static int dp_all_gather_params(gpk_session* s) {
     return GPK_OK;
 }
 
+// The union rows' sum over the ranks: one grouped all-reduce of the first
+// ucap rows of each of the 11 planes, in place, on the session stream.
+static int dp_union_allreduce(gpk_session* s) {
+    NcclApi* api = nccl();
+    if (!api || !s->comm || !api->group_start) return fail(GPK_ERR_STATE, "exchange: communicator not initialized");
+    if (!s->urows.p) return fail(GPK_ERR_STATE, "exchange before the render phase");
+    if (api->group_start() != 0) return fail(GPK_ERR_NCCL, "ncclGroupStart failed");
+    for (int k = 0; k < 11; ++k) {
+        float* plane = s->urows.as<float>() + (size_t)k * s->cap;
+        if (api->all_reduce(plane, plane, s->ucap, /*ncclFloat32*/ 7, /*ncclSum*/ 0, s->comm, s->stream) != 0)
+            return fail(GPK_ERR_NCCL, "ncclAllReduce (union rows) failed");
+    }
+    if (api->group_end() != 0) return fail(GPK_ERR_NCCL, "ncclGroupEnd failed");
+    return GPK_OK;
+}
+
+static int dp_check(gpk_session* s, int world, int rank, const gpk_slice_pose* poses, const gpk_learning_rates* lr0,
+                    int total) {
+    if (!s || !poses || !lr0) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
+    if (s->owner) return fail(GPK_ERR_STATE, "data-parallel steps run on a session, not on a context");
+    if (world < 1 || world > kMaxBatch || rank < 0 || rank >= world)
+        return fail(GPK_ERR_INVALID_ARGUMENT, "data-parallel step: 1 <= world <= 8, 0 <= rank < world");
+    if (total < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "total iterations must be >= 1");
+    if (s->accum_on) return fail(GPK_ERR_STATE, "densify accumulation is not gathered across ranks");
+    return GPK_OK;
+}
+
+int gpk_train_step_dp(gpk_session* s, int32_t world, int32_t rank, const gpk_slice_pose* poses, const gpk_psf* psf,
+                      const gpk_raster_config* cfg, double lambda, double dssim_scale, const gpk_learning_rates* lr0,
+                      int32_t total_iterations, int32_t phases) {
+    TRY(dp_check(s, world, rank, poses, lr0, total_iterations));
+    if ((phases & GPK_DP_EXCHANGE) && !s->comm) return fail(GPK_ERR_STATE, "exchange: communicator not initialized");
+    TRY(set_device(s));
+    const int st = train_dp_body(s, world, rank, poses, psf, cfg, lambda, dssim_scale, lr0, total_iterations, phases);
+    if (st != GPK_OK) s->consts_pending = false;
+    TRY(st);
+    return ok();
+}
+
+int gpk_dp_union_rows(gpk_session* s, uint64_t* rows, uint64_t* capacity) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    CK(cudaStreamSynchronize(s->stream));
+    unsigned u[2] = {0, 0};
+    if (s->uctrl.p) CK(cudaMemcpy(u, s->uctrl.p, 8, cudaMemcpyDeviceToHost));
+    if (rows) *rows = u[0];
+    if (capacity) *capacity = s->ucap;
+    if (u[1]) return fail(GPK_ERR_STATE, "data-parallel union rows exceed the capacity (gpk_dp_reserve_union, recapture)");
+    return ok();
+}
+
+int gpk_dp_reserve_union(gpk_session* s, uint64_t rows) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    TRY(dp_union_alloc(s));
+    s->ucap = std::min<uint64_t>(s->cap, std::max<uint64_t>(rows, 1));
+    ++s->alloc_epoch;  // captured graphs bake the exchange count
+    return ok();
+}
+
 int gpk_allreduce_grads(gpk_session* s) {
     if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
     NcclApi* api = nccl();
@@ -2642,6 +2853,7 @@ int gpk_voxelize_backward(gpk_session* s, const gpk_voxelizer_config* cfg, const
         CK(cudaMemcpyAsync(s->dl_dv_vol.p, dl_dv, s->vox.voxels * 4, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 11 * 4, s->stream));
     s->grads_in_slots = false;
+    s->grads_in_union = false;
     TRY(mark_grads_dense(s));
     if (s->n) {
         StageScope scope(s, GPK_STAGE_VOXEL);
@@ -2808,6 +3020,7 @@ int gpk_densify_and_prune_draw(gpk_session* s, const gpk_densify_config* cfg, gp
     // gradients and prepared state refer to the old indices: clear them
     CK(cudaMemsetAsync(s->grads.p, 0, s->cap * 44, s->stream));
     s->grads_in_slots = false;
+    s->grads_in_union = false;
     s->gmap_dirty = false;
     TRY(mark_grads_dense(s));
     s->prep.valid = false;

@@ -3,10 +3,20 @@
 One process per GPU, each holding a full Gaussian replica in its session. In
 step s, rank r renders slice ``schedule[(s * world + r) % len(schedule)]``
 (the fit loop's slices, optimize.hpp:385-395, dealt round-robin), so the
-world renders ``world`` distinct slices per step. The only exchange is the
-sum of the per-slice dense gradient planes — one ``ncclAllReduce`` over the
-11 x capacity f32 planes (``gpk_allreduce_grads``) — after which every rank
-runs the identical fused Adam and the replicas stay bitwise equal.
+world renders ``world`` distinct slices per step, and every rank knows all of
+the step's poses (``step_slices``).
+
+The exchange (``gpk_train_step_dp``, csrc/dp.cu) is union-compacted:
+gradients are exactly zero outside the union of the step's survivors, so each
+rank evaluates the cull of every pose of the step in its own cull pass, numbers
+the union of candidates identically on every rank (row = how many union
+members precede the Gaussian in index order: ``union_rows``), writes its
+survivors' gradients into those rows and ONE grouped ``ncclAllReduce`` sums
+the rows; every rank then runs the scheduled Adam on all Gaussians from the
+summed rows, so the replicas stay bitwise equal. ``pack_rows`` /
+``unpack_rows`` restate the device layout for the CPU tests. The dense
+all-reduce (``gpk_allreduce_grads``) and the reduce-scatter + sharded Adam +
+all-gather step (``gpk_train_step`` under a communicator) remain.
 
 The NCCL communicator is created by the C-ABI (``gpk_comm_init``) from an
 ``ncclUniqueId`` that rank 0 generates and the launcher's process group
@@ -78,3 +88,39 @@ def max_over_ranks(values: Sequence[float], device=None, group=None) -> list[flo
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return [float(x) for x in t.tolist()]
+
+
+def union_rows(mask):
+    """Row numbering of the union (csrc/dp.cu k_union_map): umap[i] = 1 + the
+    number of union members with a smaller index, 0 outside the union."""
+    import numpy as np
+
+    m = np.asarray(mask, bool)
+    rows = np.cumsum(m, dtype=np.int64) - 1
+    return np.where(m, rows + 1, 0).astype(np.uint32)
+
+
+def pack_rows(grads, umap):
+    """A rank's (n, 11) gradient as the union rows (M, 11): row umap[i]-1 holds
+    Gaussian i's gradient (zero for union members that are not its survivors)."""
+    import numpy as np
+
+    umap = np.asarray(umap, np.int64)
+    grads = np.asarray(grads)
+    M = int((umap > 0).sum())
+    rows = np.zeros((M, 11), grads.dtype)
+    sel = umap > 0
+    rows[umap[sel] - 1] = grads[sel]
+    return rows
+
+
+def unpack_rows(rows, umap):
+    """The summed union rows back to an (n, 11) gradient (zero outside)."""
+    import numpy as np
+
+    umap = np.asarray(umap, np.int64)
+    rows = np.asarray(rows)
+    out = np.zeros((umap.size, 11), rows.dtype)
+    sel = umap > 0
+    out[sel] = rows[umap[sel] - 1]
+    return out

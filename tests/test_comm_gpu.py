@@ -69,3 +69,39 @@ def test_train_step_under_world1_communicator_equals_single_gpu(gp, session):
     finally:
         N.check(N.lib.gpk_comm_destroy(sc.handle))
         sc.close()
+
+
+def test_union_exchange_world1_equals_single_gpu(gp, session):
+    """gpk_train_step_dp at world size 1 (union of one pose, one all-reduce of
+    the union rows, Adam from the rows) == gpk_train_step bitwise, direct and
+    as a captured graph."""
+    from paper_2603_20611_b200 import _native as N
+
+    dims = (64, 48, 12)
+    lo, hi = (-0.5, -0.5, -0.5), (63.5, 47.5, 11.5)
+    gs = gp.GaussianSet(f32(gp.init_random(3000, lo, hi, 1.5, 23).records), lo, hi)
+    poses = [gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), k) for k in (4, 8, 6)]
+    psf, rc = gp.PsfSpec(), gp.RasterConfig()
+    tgt = np.random.default_rng(24).uniform(0, 0.1, (48, 64)).astype(np.float32)
+    lr0 = gp.LearningRates(6e-4, 0.02, 2e-3, 1e-3)
+    sc = _comm_session(gp)
+    try:
+        for s in (session, sc):
+            s.set_gaussians(gs)
+            s.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
+        for it in range(4):
+            p = poses[it % 3]
+            session.train_step(p, psf, rc, 0.2, 0.5, lr0, 30)
+            sc.train_step_dp(1, 0, [p], psf, rc, 0.2, 0.5, lr0, 30)
+            assert np.array_equal(session.get_gaussians(), sc.get_gaussians()), it
+            assert np.array_equal(session.get_gradients(), sc.get_gradients()), it
+        rows, cap = sc.dp_union_rows()
+        assert 0 < rows <= cap
+        gids = [sc.capture_train_dp(1, 0, [p], psf, rc, 0.2, 0.5, lr0, 30) for p in poses]
+        for it in range(3):
+            session.train_step(poses[it], psf, rc, 0.2, 0.5, lr0, 30)
+            sc.graph_launch(gids[it])
+            assert np.array_equal(session.get_gaussians(), sc.get_gaussians()), it
+        sc.graph_destroy_all()
+    finally:
+        sc.close()

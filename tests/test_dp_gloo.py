@@ -11,7 +11,11 @@
   11-plane buffer computes on the GPUs;
 * the training step's ZeRO-style update: reduce the summed gradient to each
   primitive's owner, Adam on the owner's shard only, all-gather the parameter
-  shards — every replica ends bitwise equal to the full all-reduce + full Adam.
+  shards — every replica ends bitwise equal to the full all-reduce + full Adam;
+* the union-compacted exchange (gpk_train_step_dp, csrc/dp.cu): each rank
+  derives the union of the step's survivors itself, numbers it like the
+  device (dp.union_rows), packs its gradient into those rows; one all-reduce
+  of the rows, unpacked, equals the dense all-reduce.
 """
 from __future__ import annotations
 
@@ -101,6 +105,26 @@ def _worker(rank, world, port, q):
         dist.all_gather(shards, mine_p)  # the parameter shards to every replica
         out["zero_params"] = torch.cat(shards)[:n].numpy()
         out["zero_grads"] = np.array(g, copy=True)
+        # union-compacted exchange (csrc/dp.cu): every rank evaluates the cull of
+        # ALL the step's poses itself — no collective for the union — numbers
+        # the union identically, packs its own gradient into those rows, one
+        # all-reduce of the rows, unpack; equals the dense all-reduce
+        for step in range(3):
+            ks = dp.step_slices(step, world, len(poses))
+            union = np.zeros(n, bool)
+            for kk in ks:
+                idx, _, _ = oracle.prepare(rec, poses[kk], psf, cfg)
+                union[idx] = True
+            umap = dp.union_rows(union)
+            g, _ = oracle.backward(rec, poses[ks[rank]], psf, cfg, dl[ks[rank]])
+            assert not np.any(g[~union]), "a rank's gradient lives inside the union"
+            rows = torch.from_numpy(dp.pack_rows(np.asarray(g, np.float32), umap))
+            dist.all_reduce(rows)
+            out.setdefault("union_umap", []).append(umap)
+            out.setdefault("union_sum", []).append(dp.unpack_rows(rows.numpy(), umap))
+            dense = torch.from_numpy(np.ascontiguousarray(g, np.float32))
+            dist.all_reduce(dense)
+            out.setdefault("union_dense", []).append(dense.numpy().copy())
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -155,3 +179,9 @@ def test_gloo_world2_exchange():
                             (6e-4, 0.02, 2e-3, 1e-3))[0]
     assert np.array_equal(res[0]["zero_params"], res[1]["zero_params"])
     assert np.array_equal(res[0]["zero_params"], want)
+    # union-compacted exchange: same numbering on both ranks, rows' sum == dense sum
+    for step in range(3):
+        assert np.array_equal(res[0]["union_umap"][step], res[1]["union_umap"][step])
+        for r in (0, 1):
+            assert np.array_equal(res[r]["union_sum"][step], res[r]["union_dense"][step])
+        assert 0 < (res[0]["union_umap"][step] > 0).sum() < rec.shape[0]

@@ -230,10 +230,28 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     if (a.bucket_tab) {
         // single-pass slice (every tile is one digit): bucket the group's pairs
         // by tile — counts, bucket starts (published for k_gather), then slots
-        // into their buckets. Order inside a bucket is restored by k_gather.
-        for (unsigned k = tid; k < Pb; k += kDecideThreads) {
-            unsigned j;
-            atomicAdd(&s_hist[0][pair_tile(k, j)], 1u);
+        // into their buckets in pair order (stable). Pairs go in rounds of
+        // 1024, warp w taking 4 x 32 consecutive ones; a round's tiles are
+        // found once (binary search over the survivors' pair counts) and, for
+        // a one-round group (the common case), kept in registers for the fill.
+        constexpr int kSub = 4;
+        constexpr unsigned kRound = kDecideThreads * kSub;
+        unsigned tl[kSub], jj[kSub];
+        auto round_tiles = [&](unsigned r0) {
+#pragma unroll
+            for (int q = 0; q < kSub; ++q) {
+                const unsigned k = r0 + (unsigned)(warp * kSub + q) * 32 + lane;
+                tl[q] = k < Pb ? pair_tile(k, jj[q]) : 0xffffffffu;
+            }
+        };
+        for (unsigned r0 = 0; r0 < Pb; r0 += kRound) {
+            round_tiles(r0);
+#pragma unroll
+            for (int q = 0; q < kSub; ++q) {  // warp-aggregated counts
+                const unsigned peers = __match_any_sync(0xffffffffu, tl[q]);
+                if (tl[q] != 0xffffffffu && (__ffs(peers) - 1) == lane)
+                    atomicAdd(&s_hist[0][tl[q]], (unsigned)__popc(peers));
+            }
         }
         __syncthreads();
         unsigned* s_start = &s_hist[1][0];
@@ -271,47 +289,47 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
         __syncthreads();
         // stable fill: each bucket receives its pairs in pair order (= ascending
         // slot, one pair per survivor and tile), so the gather is a plain
-        // concatenation. Rounds of 1024 pairs; warp w ranks its 128 with
-        // __match_any_sync against its own per-tile counters, then a per-tile
-        // prefix over the warps (on top of the running bucket fill) places them.
+        // concatenation. Per round: warp w ranks its pairs with
+        // __match_any_sync against its own counter of the tile; a pair's slot
+        // in its bucket is the bucket's fill before the round + the counts of
+        // the tile in earlier warps + its rank. Only the round's tiles are
+        // touched (no per-digit sweeps).
         uint16_t(*s_w16)[kMaxBuckets] = reinterpret_cast<uint16_t(*)[kMaxBuckets]>(s_dyn_u + kDecideGroup + kDecideGroup * 3 / 2);
-        constexpr int kSub = 4;  // 32-pair rounds per warp per round
-        for (unsigned r0 = 0; r0 < Pb; r0 += kDecideThreads * kSub) {
-            for (unsigned w = tid; w < 8u * (nb / 2); w += kDecideThreads)
-                reinterpret_cast<unsigned*>(&s_w16[0][0])[(w / (nb / 2)) * (kMaxBuckets / 2) + w % (nb / 2)] = 0u;
+        for (unsigned r0 = 0; r0 < Pb; r0 += kRound) {
+            if (Pb > kRound) round_tiles(r0);  // (one round: the tiles are still in registers)
+#pragma unroll
+            for (int q = 0; q < kSub; ++q)
+                if (tl[q] != 0xffffffffu)
+#pragma unroll
+                    for (int w = 0; w < kDecideThreads / 32; ++w) s_w16[w][tl[q]] = 0;
             __syncthreads();
-            unsigned tl[kSub], jj[kSub], rk[kSub];
+            unsigned rk[kSub], pc[kSub];
 #pragma unroll
             for (int q = 0; q < kSub; ++q) {
-                const unsigned k = r0 + (unsigned)(warp * kSub + q) * 32 + lane;
-                const bool valid = k < Pb;
-                tl[q] = valid ? pair_tile(k, jj[q]) : 0xffffffffu;
+                const bool valid = tl[q] != 0xffffffffu;
                 const unsigned peers = __match_any_sync(0xffffffffu, tl[q]);
                 const unsigned prior = valid ? s_w16[warp][tl[q]] : 0u;
                 __syncwarp();
-                if (valid && (__ffs(peers) - 1) == lane) s_w16[warp][tl[q]] = (uint16_t)(prior + __popc(peers));
+                const bool leader = valid && (__ffs(peers) - 1) == lane;
+                if (leader) s_w16[warp][tl[q]] = (uint16_t)(prior + __popc(peers));
                 __syncwarp();
                 rk[q] = prior + __popc(peers & lanemask_lt());
-            }
-            __syncthreads();
-            for (unsigned d = tid; d < nb; d += kDecideThreads) {
-                unsigned run = s_hist[0][d];
-#pragma unroll
-                for (int w = 0; w < 8; ++w) {
-                    const unsigned c = s_w16[w][d];
-                    s_w16[w][d] = (uint16_t)run;  // bucket fill <= survivors of the group <= 4096
-                    run += c;
-                }
-                s_hist[0][d] = run;
+                pc[q] = leader ? (unsigned)__popc(peers) : 0u;
             }
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < kSub; ++q)
                 if (tl[q] != 0xffffffffu) {
-                    const unsigned long long pos = (unsigned long long)P0 + s_start[tl[q]] + s_w16[warp][tl[q]] + rk[q];
+                    unsigned b = s_hist[0][tl[q]] + rk[q];
+                    for (int w = 0; w < warp; ++w) b += s_w16[w][tl[q]];
+                    const unsigned long long pos = (unsigned long long)P0 + s_start[tl[q]] + b;
                     if (pos < a.pair_cap) a.vals[pos] = base + jj[q];
                 }
-            __syncthreads();  // the next round clears the warp tables
+            __syncthreads();  // every base read before the fills advance
+#pragma unroll
+            for (int q = 0; q < kSub; ++q)
+                if (pc[q]) atomicAdd(&s_hist[0][tl[q]], pc[q]);
+            __syncthreads();
         }
         // the last group to finish turns the per-tile counts into list starts
         // (one scan, instead of every gather CTA re-reading the same counts)

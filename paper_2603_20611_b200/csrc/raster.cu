@@ -1,7 +1,8 @@
 // raster.cu — per-tile pixel accumulation kernels (forward and backward).
 //
 // Forward replaces rasterize_prepared (render.hpp:166-192):
-//   one CTA per 16x16 tile, one thread per pixel, warps own 8x4 pixel blocks.
+//   one CTA of 128 threads per 16x16 tile; warp w owns the tile rows
+//   [4w, 4w + 4), each lane two horizontally adjacent pixels of one row.
 //   The tile's pairs are one contiguous run of 32 B PairRecords (tile-local
 //   fp32 centre from the fp64 mean — SURVEY.md §7.3.3: absolute fp32 pixel
 //   coordinates lose 3.6e-4 at 2048^2 — scaled conic, alpha_tilde, the bit
@@ -10,11 +11,12 @@
 //   256 with double-buffered cp.async.bulk (TMA) copies on an mbarrier. In the
 //   training step the forward builds its own tile's list and records (the
 //   gather fused in), stages them directly and stores them for the backward.
-//   Each warp ballots
-//   which of 32 records touch its 8x4 block and walks only those, in list
-//   order — every pixel sums its Gaussians in ascending set order like the
-//   reference, deterministically. exp runs on MUFU.EX2 with the -1/2*log2(e)
-//   factor folded into the conic.
+//   Each warp ballots which of 32 records touch its rows and walks only
+//   those, in list order —
+//   every pixel sums its Gaussians in ascending set order like the reference,
+//   deterministically; a lane shares a record's row terms between its two
+//   pixels. exp runs on MUFU.EX2 with the -1/2*log2(e) factor folded into the
+//   conic.
 //
 // Backward replaces stage 1 of backward_prepared (backward.hpp:108-139):
 //   the tile's PairRecords are staged into shared memory by cp.async.bulk
@@ -92,10 +94,11 @@ __device__ __forceinline__ void tile_range(const RasterLaunch& a, int tile, unsi
 // k_gather's work for one tile (sort.cu): the tile's list from the K_decide
 // buckets (common.cuh gather_tile_list). The list is visible to the CTA after
 // the helper's closing barrier.
+template <int kThreads>
 __device__ __forceinline__ void gather_tile(const RasterLaunch& a, unsigned d) {
-    __shared__ unsigned s_ex[257], s_b[256], s_wsum[8];
-    gather_tile_list<256>(a.bucket_tab, a.ngroups, a.row_stride, d, __ldcg(&a.grp_begin[d]),
-                          stored_pairs(a.ctrl, a.pair_cap), a.vals_in, a.vals_out, s_ex, s_b, s_wsum);
+    __shared__ unsigned s_ex[kThreads + 1], s_b[kThreads], s_wsum[kThreads / 32];
+    gather_tile_list<kThreads>(a.bucket_tab, a.ngroups, a.row_stride, d, __ldcg(&a.grp_begin[d]),
+                               stored_pairs(a.ctrl, a.pair_cap), a.vals_in, a.vals_out, s_ex, s_b, s_wsum);
 }
 
 // Double-buffered TMA staging of a tile's PairRecords: batch q of [start, end)
@@ -120,34 +123,42 @@ __device__ __forceinline__ void pair_issue(const PairStage& ps, const PairRecord
 
 __device__ __forceinline__ void pair_wait(const PairStage& ps, unsigned q) { mbar_wait(&ps.bar[q & 1], (q >> 1) & 1); }
 
-// Every pixel of the warp's 8x4 block sums the batch's records that touch the
-// block, in list order (ascending set index, like the reference).
-__device__ __forceinline__ float fwd_batch(const PairRecord* recs, unsigned nb, unsigned warp_x, unsigned warp_y,
-                                           unsigned lane_bits, float fx, float fy, float acc) {
+// Forward: 128 threads per tile, warp w owns the tile's rows [4w, 4w + 4),
+// lane l the horizontally adjacent pixels (2 (l mod 8) + {0, 1}, 4w + l / 8).
+// A record is walked by the warps whose rows it covers; per record a lane
+// shares the row terms (dy, kb2 dy, kd dy^2) between its two pixels. Every
+// pixel sums the records that cover it in list order (ascending set index,
+// like the reference) with exactly the per-pixel arithmetic of one pixel per
+// thread: the image is the same bits.
+constexpr int kFwdThreads = 128;
+
+__device__ __forceinline__ void fwd_batch(const PairRecord* recs, unsigned nb, unsigned warp_y, unsigned ybit,
+                                          unsigned xb0, unsigned xb1, float fx0, float fx1, float fy, float& acc0,
+                                          float& acc1) {
     const int lane = threadIdx.x & 31;
     const float4* s4 = reinterpret_cast<const float4*>(recs);
     for (unsigned g = 0; g < nb; g += 32) {
-        bool hit = false;
-        if (g + lane < nb) {
-            const unsigned m = recs[g + lane].rect;
-            hit = (m & warp_x) && (m & warp_y);
-        }
+        const bool hit = g + lane < nb && (recs[g + lane].rect & warp_y);
         unsigned m = __ballot_sync(0xffffffffu, hit);
         while (m) {
             const int k = __ffs(m) - 1;
             m &= m - 1;
-            const float4 r0 = s4[2 * (g + k)];
-            const float4 r1 = s4[2 * (g + k) + 1];
-            const bool inside = (__float_as_uint(r1.z) & lane_bits) == lane_bits;
-            const float dx = fx - r0.x, dy = fy - r0.y;
-            const float e = fmaf(dx, fmaf(r0.z, dx, r0.w * dy), r1.x * dy * dy);
-            acc = fmaf(inside ? r1.y : 0.f, ex2_approx(e), acc);
+            const float4 r0 = s4[2 * (g + k)];  // {ox, oy, ka, kb2}
+            const float4 r1 = s4[2 * (g + k) + 1];  // {kd, at, mask, pos}
+            const unsigned mask = __float_as_uint(r1.z);
+            const float dy = fy - r0.y;
+            const float B = r0.w * dy, Cc = r1.x * dy * dy;
+            const float dx0 = fx0 - r0.x, dx1 = fx1 - r0.x;
+            const float e0 = fmaf(dx0, fmaf(r0.z, dx0, B), Cc);
+            const float e1 = fmaf(dx1, fmaf(r0.z, dx1, B), Cc);
+            const bool iny = (mask & ybit) != 0;
+            acc0 = fmaf(iny && (mask & xb0) ? r1.y : 0.f, ex2_approx(e0), acc0);
+            acc1 = fmaf(iny && (mask & xb1) ? r1.y : 0.f, ex2_approx(e1), acc1);
         }
     }
-    return acc;
 }
 
-__global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
+__global__ void __launch_bounds__(kFwdThreads) k_raster_fwd(const RasterLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ __align__(128) PairRecord s_pr[2][kPairBatch];
     __shared__ __align__(8) uint64_t s_bar[2];
@@ -156,7 +167,7 @@ __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
     const bool produce = a.bucket_tab != nullptr;
-    if (produce) gather_tile(a, (unsigned)tile);  // (ends with a barrier)
+    if (produce) gather_tile<kFwdThreads>(a, (unsigned)tile);  // (ends with a barrier)
     const int tx = tile % a.slice.tiles_x, ty = tile / a.slice.tiles_x;
     const int x0 = tx * kTile, y0 = ty * kTile;
     tile_range(a, tile, s_range);
@@ -165,32 +176,31 @@ __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
         mbar_init(&s_bar[1], 1);
         fence_mbar_init();
     }
-    // pixel of this thread: warp w -> 8x4 block
-    const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;
-    const int lx = wx0 + (lane & 7), ly = wy0 + (lane >> 3);
-    const unsigned lane_bits = (1u << lx) | (1u << (16 + ly));
-    const unsigned warp_x = 0xffu << wx0, warp_y = 0xfu << (16 + wy0);
+    const int lx = 2 * (lane & 7), ly = warp * 4 + (lane >> 3);
+    const unsigned ybit = 1u << (16 + ly), xb0 = 1u << lx, xb1 = 2u << lx;
+    const unsigned warp_y = 0xfu << (16 + warp * 4);
     const double X0 = ((double)x0 - a.slice.ppx) * a.slice.sx;
     const double Y0 = ((double)y0 - a.slice.ppy) * a.slice.sy;
-    const float fx = (float)(lx * a.slice.sx), fy = (float)(ly * a.slice.sy);
+    const float fx0 = (float)(lx * a.slice.sx), fx1 = (float)((lx + 1) * a.slice.sx);
+    const float fy = (float)(ly * a.slice.sy);
     __syncthreads();
     const PairStage ps{s_pr, s_bar, s_range[0], s_range[1]};
     const unsigned nbatch = (ps.end - ps.start + kPairBatch - 1) / kPairBatch;
 
-    float acc = 0.f;
+    float acc0 = 0.f, acc1 = 0.f;
     if (produce) {
         // the training step's forward builds its tile's records itself (from
         // the list it just gathered) and stores them for the backward
         for (unsigned q = 0; q < nbatch; ++q) {
             const unsigned b = ps.start + q * kPairBatch, nb = min((unsigned)kPairBatch, ps.end - b);
-            if ((unsigned)tid < nb) {
+            for (unsigned t = tid; t < nb; t += kFwdThreads) {
                 // (L2 load: the list was written by this CTA just now)
-                const PairRecord pr = make_pair_record(a.records[__ldcg(&a.vals[b + tid])], tx, ty, X0, Y0);
-                store_pair_record(&s_pr[0][tid], pr);
-                store_pair_record(a.pairs + b + tid, pr);
+                const PairRecord pr = make_pair_record(a.records[__ldcg(&a.vals[b + t])], tx, ty, X0, Y0);
+                store_pair_record(&s_pr[0][t], pr);
+                store_pair_record(a.pairs + b + t, pr);
             }
             __syncthreads();
-            acc = fwd_batch(s_pr[0], nb, warp_x, warp_y, lane_bits, fx, fy, acc);
+            fwd_batch(s_pr[0], nb, warp_y, ybit, xb0, xb1, fx0, fx1, fy, acc0, acc1);
             __syncthreads();
         }
     } else {
@@ -201,7 +211,7 @@ __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
         for (unsigned q = 0; q < nbatch; ++q) {
             const unsigned nb = min((unsigned)kPairBatch, ps.end - (ps.start + q * kPairBatch));
             pair_wait(ps, q);
-            acc = fwd_batch(s_pr[q & 1], nb, warp_x, warp_y, lane_bits, fx, fy, acc);
+            fwd_batch(s_pr[q & 1], nb, warp_y, ybit, xb0, xb1, fx0, fx1, fy, acc0, acc1);
             if (q + 2 < nbatch) {
                 __syncthreads();  // buffer q & 1 read by every warp
                 if (tid == 0) pair_issue(ps, a.pairs, q + 2);
@@ -209,7 +219,11 @@ __global__ void __launch_bounds__(256) k_raster_fwd(const RasterLaunch a) {
         }
     }
     const int i = x0 + lx, j = y0 + ly;
-    if (i < a.slice.W && j < a.slice.H) a.image[(size_t)j * a.slice.W + i] = acc;
+    if (j < a.slice.H) {
+        float* row = a.image + (size_t)j * a.slice.W;
+        if (i < a.slice.W) row[i] = acc0;
+        if (i + 1 < a.slice.W) row[i + 1] = acc1;
+    }
 }
 
 // Training step: dL/dI of the tile from k_ssim_fwd's three partial planes
@@ -449,7 +463,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
 
 void launch_raster_fwd(const RasterLaunch& a, cudaStream_t st) {
     const int tiles = a.slice.tiles_x * a.slice.tiles_y;
-    if (tiles > 0) launch_pdl(k_raster_fwd, dim3(tiles), dim3(256), 0, st, a);
+    if (tiles > 0) launch_pdl(k_raster_fwd, dim3(tiles), dim3(kFwdThreads), 0, st, a);
 }
 
 void launch_raster_bwd(const RasterLaunch& a, cudaStream_t st) {

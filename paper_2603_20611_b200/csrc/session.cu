@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -165,6 +166,7 @@ struct gpk_session {
     } prefilter;
     bool assume_prefiltered = false;  // set while capturing a pipelined train step
     bool fuse_gather = false;         // training step: the next prepare leaves the gather to the forward
+    bool fuse_gather_ok = true;       // (GPK_FUSE_GATHER=0: the gather stays its own kernel; A/B measurements)
     struct CaptureMeta {
         bool needs_prefilter = false, sets_prefilter = false, writes_params = false;
         gpk_slice_pose next_pose{};
@@ -1285,6 +1287,7 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
         s->own_stream = true;
     }
     cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (const char* f = getenv("GPK_FUSE_GATHER")) s->fuse_gather_ok = f[0] != '0';
     if (s->num_sms < 1) s->num_sms = 148;
     e = s->persist.ensure(kPersistBytes);
     if (e == cudaSuccess) e = cudaMemsetAsync(s->persist.p, 0, kPersistBytes, s->stream);
@@ -1899,7 +1902,7 @@ static int train_body_(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf
                        const gpk_learning_rates* lr0, int32_t total, const gpk_slice_pose* next) {
     const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
     if (s->n) TRY(adam_consts_ahead(s, adam_launch(s, lr, true, total, nullptr)));
-    s->fuse_gather = true;  // the forward builds the tile lists (gather_tile): -1.4 us per step
+    s->fuse_gather = s->fuse_gather_ok;  // the forward builds the tile lists (gather_tile)
     const int pst = run_prepare(s, pose, psf, cfg, true);
     s->fuse_gather = false;
     TRY(pst);
@@ -2134,7 +2137,7 @@ static int train_batch_body(gpk_session* s, int B, const gpk_slice_pose* poses, 
     TRY(batch_fork(s, cx, B));
     for (int k = 0; k < B; ++k) {
         gpk_session* c = cx[k];
-        c->fuse_gather = true;
+        c->fuse_gather = s->fuse_gather_ok;
         const int pst = run_prepare(c, &poses[k], psf, cfg, false, /*filtered=*/true);
         c->fuse_gather = false;
         TRY(pst);
@@ -2229,7 +2232,7 @@ static int train_dp_body(gpk_session* s, int world, int rank, const gpk_slice_po
             for (int k = 0; k < 11; ++k)
                 CK(cudaMemsetAsync(s->urows.as<float>() + (size_t)k * s->cap, 0, s->ucap * 4, s->stream));
         }
-        s->fuse_gather = true;
+        s->fuse_gather = s->fuse_gather_ok;
         const int pst = run_prepare(s, &poses[rank], psf, cfg, false, /*filtered=*/s->n != 0);
         s->fuse_gather = false;
         TRY(pst);

@@ -3,7 +3,8 @@
 // Forward (voxelize, voxelize.hpp:126-146): one CTA per voxel tile. The
 // tile's primitives (already in ascending set order from the stable radix
 // sort) are staged through shared memory in batches; each thread owns one
-// 16-voxel segment of an x-row and, per primitive, evaluates
+// x-row segment (a whole 8-voxel row of an 8^3 tile, 64 threads per tile;
+// 16-voxel segments for other tile widths) and, per primitive, evaluates
 //     alpha * exp(-1/2 d^T Sigma^-1 d) = 2^(q(dx)),  q(dx) = (a00 dx + B) dx + C
 // where B, C are per-(row, primitive) constants and log2(alpha) and
 // -1/2*log2(e) are folded into C and the a's: two FMAs + one MUFU.EX2 + one
@@ -24,7 +25,6 @@ namespace {
 
 constexpr float kNegHalfLog2e = -0.72134752044448170368f;
 constexpr int kVoxBatch = 128;
-constexpr int kSeg = 16;
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -70,7 +70,11 @@ __device__ __forceinline__ TileBox tile_box(const VoxArgs& v, unsigned t) {
     return b;
 }
 
-__global__ void __launch_bounds__(128) k_veval(const VoxEvalLaunch a) {
+// SEG voxels of an x-row per thread, THREADS per CTA: (8, 64) for 8-wide
+// tiles (every thread owns one full row of the 8x8x8 tile: no idle lanes, no
+// evaluations past the row), (16, 128) otherwise.
+template <int SEG, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_veval(const VoxEvalLaunch a) {
     __shared__ float4 s_p[kVoxBatch][3];  // {ox, oy, oz, log2a}, {a00, a11, a22, 2a01}, {2a02, 2a12}
     __shared__ unsigned s_range[2];
     const int tid = threadIdx.x;
@@ -88,29 +92,32 @@ __global__ void __launch_bounds__(128) k_veval(const VoxEvalLaunch a) {
     const float sx = (float)a.v.spacing[0], sy = (float)a.v.spacing[1], sz = (float)a.v.spacing[2];
     __syncthreads();
     const unsigned start = s_range[0], end = s_range[1];
-    const int nseg = (b.nx + kSeg - 1) / kSeg;
+    const int nseg = (b.nx + SEG - 1) / SEG;
     const int nitems = b.ny * b.nz * nseg;
 
-    for (int ig = 0; ig < nitems; ig += blockDim.x) {
+    for (int ig = 0; ig < nitems; ig += THREADS) {
         const int it = ig + tid;
         const bool active = it < nitems;
         const int seg = active ? it % nseg : 0, row = active ? it / nseg : 0;
         const int ly = row % b.ny, lz = row / b.ny;
-        const int lx0 = seg * kSeg;
-        const int len = active ? min(kSeg, b.nx - lx0) : 0;
-        float acc[kSeg];
+        const int lx0 = seg * SEG;
+        const int len = active ? min(SEG, b.nx - lx0) : 0;
+        float acc[SEG];
 #pragma unroll
-        for (int j = 0; j < kSeg; ++j) acc[j] = 0.f;
+        for (int j = 0; j < SEG; ++j) acc[j] = 0.f;
         const float fy = ly * sy, fz = lz * sz;
+        float fxs[SEG];
+#pragma unroll
+        for (int j = 0; j < SEG; ++j) fxs[j] = (float)(lx0 + j) * sx;
         for (unsigned bb = start; bb < end; bb += kVoxBatch) {
             const unsigned nb = min((unsigned)kVoxBatch, end - bb);
             __syncthreads();
-            if ((unsigned)tid < nb) {
-                const VoxRecord r = a.records[a.vals[bb + tid]];
-                s_p[tid][0] = make_float4((float)(wx0 - (double)r.mu[0]), (float)(wy0 - (double)r.mu[1]),
-                                          (float)(wz0 - (double)r.mu[2]), r.log2a);
-                s_p[tid][1] = make_float4(r.a[0], r.a[1], r.a[2], r.a[3]);
-                s_p[tid][2] = make_float4(r.a[4], r.a[5], 0.f, 0.f);
+            for (unsigned q = tid; q < nb; q += THREADS) {
+                const VoxRecord r = a.records[a.vals[bb + q]];
+                s_p[q][0] = make_float4((float)(wx0 - (double)r.mu[0]), (float)(wy0 - (double)r.mu[1]),
+                                        (float)(wz0 - (double)r.mu[2]), r.log2a);
+                s_p[q][1] = make_float4(r.a[0], r.a[1], r.a[2], r.a[3]);
+                s_p[q][2] = make_float4(r.a[4], r.a[5], 0.f, 0.f);
             }
             __syncthreads();
             if (active) {
@@ -120,8 +127,8 @@ __global__ void __launch_bounds__(128) k_veval(const VoxEvalLaunch a) {
                     const float B = fmaf(p1.w, dy, p2.x * dz);
                     const float Cc = fmaf(dy, fmaf(p1.y, dy, p2.y * dz), fmaf(p1.z * dz, dz, p0.w));
 #pragma unroll
-                    for (int j = 0; j < kSeg; ++j) {
-                        const float dx = fmaf((float)(lx0 + j), sx, p0.x);
+                    for (int j = 0; j < SEG; ++j) {
+                        const float dx = fxs[j] + p0.x;
                         const float q = fmaf(fmaf(p1.x, dx, B), dx, Cc);
                         acc[j] += ex2_approx(q);
                     }
@@ -132,7 +139,7 @@ __global__ void __launch_bounds__(128) k_veval(const VoxEvalLaunch a) {
             const size_t X = (size_t)a.v.dims[0], Y = (size_t)a.v.dims[1];
             float* out = a.volume + ((size_t)(b.z0 + lz) * Y + (b.y0 + ly)) * X + (b.x0 + lx0);
 #pragma unroll
-            for (int j = 0; j < kSeg; ++j)
+            for (int j = 0; j < SEG; ++j)
                 if (j < len) out[j] = fmaxf(0.f, acc[j]);
         }
     }
@@ -226,7 +233,9 @@ __global__ void __launch_bounds__(128) k_vbwd(const VoxEvalLaunch a) {
 
 void launch_vox_eval(const VoxEvalLaunch& a, cudaStream_t st) {
     const unsigned tiles = (unsigned)a.v.ntiles[0] * a.v.ntiles[1] * a.v.ntiles[2];
-    if (tiles) k_veval<<<tiles, 128, 0, st>>>(a);
+    if (!tiles) return;
+    if (a.v.tile[0] == 8) k_veval<8, 64><<<tiles, 64, 0, st>>>(a);
+    else k_veval<16, 128><<<tiles, 128, 0, st>>>(a);
 }
 
 void launch_vox_bwd(const VoxEvalLaunch& a, cudaStream_t st) {

@@ -788,11 +788,17 @@ def run_ours(args):
                  "266N + 44S: read params, m, v, 2 B slot map; write params, m, v; survivor gradients "
                  "+ 48C next-slice candidates")
         if (u2 and args.pipeline and world == 1) else
+        ("k_adam_final", 264 * S + 44 * S + 6 * S,
+         "264S + 44S + 6S: the survivors' params, m, v read and written, their slot gradients, set index, map")
+        if (world == 1 and B == 1 and "adam_rest" in stages and stages["adam_rest"][1]) else
         ("k_adam", 266 * n + 44 * S,
          "266N + 44S: read params, m, v, 2 B slot map; write params, m, v; survivor gradients")
         if world == 1 else
         ("k_adam", 268 * n + 44 * union_rows[0][0],
          "268N + 44M: read params, m, v, 4 B union map; write params, m, v; the M summed union rows"),
+        # the non-survivors' Adam, on a side stream beside the render (split step)
+        "adam_rest": ("k_adam_rest", 264 * (n - S) + n / 8,
+                      "264(N-S): the non-survivors' params, m, v read and written + N/8 survivor bits"),
     }
     measured = {k: v for k, v in stages.items() if v[1] > 0 and k in kernel_bytes}
     dom = max(measured, key=lambda k: measured[k][0])
@@ -867,7 +873,8 @@ def run_ours(args):
     # Adam); u1 x B: + one gradient scatter per slice. Memsets are not kernels.
     sort_k = passes if passes > 1 else (0 if u2 else 1)
     per_slice = 2 + sort_k + 4 + (1 if u2 else 0)
-    launches = B * per_slice + (2 if u2 else (B if B > 1 else 0)) + (2 if dp_union else 0)  # + union scan, map
+    split = "adam_rest" in stages and stages["adam_rest"][1] > 0  # Adam in two kernels (rest + final)
+    launches = B * per_slice + (2 if u2 else (B if B > 1 else 0)) + (2 if dp_union else 0) + (1 if split else 0)
     if u2 and args.pipeline:
         launches -= 1
     line["gpu_launches"] = launches * args.steps

@@ -160,7 +160,8 @@ typedef enum {
     GPK_STAGE_VOXEL = 7,
     GPK_STAGE_BIN = 8,       /* K_bin: survivor slots, (tile, candidate) pair emission */
     GPK_STAGE_VOXEL_EVAL = 9,   /* voxelize: the per-tile evaluation (GPK_STAGE_VOXEL: prims + tile lists) */
-    GPK_NUM_STAGES = 10
+    GPK_STAGE_ADAM_REST = 10,   /* training step: the non-survivors' Adam beside the render (GPK_STAGE_ADAM: the survivors') */
+    GPK_NUM_STAGES = 11
 } gpk_stage;
 /* Enable/disable event pairs around every stage launch. */
 int gpk_stage_timing(gpk_session* s, int enable);

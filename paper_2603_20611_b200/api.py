@@ -397,7 +397,8 @@ class Session:
     def download(self, which: int, host_ptr: int, nbytes: int):
         check(N.lib.gpk_download(self._h, int(which), C.c_void_p(host_ptr), int(nbytes)))
 
-    STAGES = ("prepare", "sort", "raster", "backward", "chain", "loss", "adam", "voxel", "bin", "voxel_eval")
+    STAGES = ("prepare", "sort", "raster", "backward", "chain", "loss", "adam", "voxel", "bin", "voxel_eval",
+              "adam_rest")
 
     def stage_timing(self, enable: bool = True):
         check(N.lib.gpk_stage_timing(self._h, 1 if enable else 0))

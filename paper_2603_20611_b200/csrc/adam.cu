@@ -13,6 +13,8 @@
 // survivor. The reference's order is kept: position update then bbox clamp
 // (:212), log-scale, raw alpha, quaternion update then renormalisation when
 // the norm is > 0 (:216-217).
+#include <algorithm>
+
 #include "adam.cuh"
 
 namespace gpk {
@@ -49,6 +51,52 @@ __global__ void __launch_bounds__(256, kMinB) k_adam(const AdamLaunch a) {
     const bool any = kSlots && adam_slots<kAdamItems>(a, i0, gslot);
     adam_update_store<kAdamItems>(a, c, i0, kSlots ? gslot : nullptr);
     if (any) adam_slots_clear<kAdamItems>(a, i0);
+}
+
+// ---- Adam split around the render (single-GPU training step) ---------------------
+// A Gaussian that did not survive the slice's cull has an exactly zero
+// gradient, known as soon as K_decide has run; its update does not depend on
+// the render. k_adam_rest updates them on a side stream while the slice
+// renders (grid-stride, a bounded number of CTAs, launched at the lowest
+// priority so the latency-bound slice kernels keep the SMs), k_adam_final
+// the survivors from their slot gradients after the chain. Per Gaussian the
+// same operations as k_adam: the same bits.
+__device__ __forceinline__ bool adam_overflow(const AdamLaunch& a) { return a.ctrl && a.ctrl->pair_overflow; }
+
+__global__ void __launch_bounds__(256, 6) k_adam_rest(const AdamLaunch a, const unsigned* __restrict__ surv_bits) {
+    if (adam_overflow(a)) return;
+    const AdamConsts& c = *a.consts;
+    const auto zero2 = [](int) { Pack<2> g; g.v[0] = g.v[1] = 0.f; return g; };
+    const auto zero1 = [](int) { Pack<1> g; g.v[0] = 0.f; return g; };
+    for (uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 2; i0 < a.n; i0 += gridDim.x * blockDim.x * 2) {
+        const unsigned bits = (__ldg(&surv_bits[i0 >> 5]) >> (i0 & 31)) & 3u;  // i0 even: one word
+        if (bits == 0) {
+            adam_update_store_g<2>(a, c, i0, zero2);
+        } else if (bits != 3) {
+            adam_update_store_g<1>(a, c, i0 + (bits == 1 ? 1u : 0u), zero1);
+        }
+    }
+}
+
+// CTA per K_decide group: its survivors (slots g*4096 + [0, S_g)); CTA 0
+// advances the step counter; the chain's map entries are cleared.
+__global__ void __launch_bounds__(256) k_adam_final(const AdamLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    const unsigned g = blockIdx.x;
+    const unsigned S = a.grp_surv[g];
+    const bool skip = adam_overflow(a);
+    const AdamConsts& c = *a.consts;
+    if (!skip) adam_advance_step(a, c);
+    for (unsigned j = threadIdx.x; j < S; j += blockDim.x) {
+        const uint32_t slot = g * kDecideGroupSize + j, i = a.surv_gidx[slot];
+        if (!skip)
+            adam_update_store_g<1>(a, c, i, [&](int k) {
+                Pack<1> gr;
+                gr.v[0] = __ldcs(a.slot_grads + (uint64_t)k * a.cap + slot);
+                return gr;
+            });
+        a.gmap[i] = 0;
+    }
 }
 
 // Batched step, before its Adam: the B slices' slot gradients summed per
@@ -102,6 +150,16 @@ void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, int mode, 
 void launch_sum_slots(const AdamLaunch& a, cudaStream_t st) {
     const unsigned grid = (a.n + 256 * kAdamItems - 1) / (256 * kAdamItems);
     if (grid) launch_pdl(k_sum_slots, dim3(grid), dim3(256), 0, st, a);
+}
+
+void launch_adam_rest(const AdamLaunch& a, const unsigned* surv_bits, int ctas, cudaStream_t st) {
+    const unsigned need = (a.n + 511) / 512;
+    const unsigned grid = ctas > 0 ? std::min<unsigned>((unsigned)ctas, need) : need;
+    if (grid) k_adam_rest<<<grid, 256, 0, st>>>(a, surv_bits);
+}
+
+void launch_adam_final(const AdamLaunch& a, unsigned ngroups, cudaStream_t st) {
+    if (ngroups) launch_pdl(k_adam_final, dim3(ngroups), dim3(256), 0, st, a);
 }
 
 void launch_adam_consts(const AdamLaunch& a, cudaStream_t st) {

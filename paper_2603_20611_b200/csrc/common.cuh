@@ -334,6 +334,18 @@ __device__ __forceinline__ void pdl_entry() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// The step's kernels launch at the device's highest priority: a training
+// step's background work (k_adam_rest, default priority) yields the SMs to
+// them whenever both have CTAs waiting.
+inline int high_priority() {
+    static int p = [] {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        return hi;
+    }();
+    return p;
+}
+
 template <typename... Params, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -342,11 +354,13 @@ inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, 
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributePriority;
+    attr[1].val.priority = high_priority();
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -440,6 +454,7 @@ struct PrepLaunch {
     unsigned* bucket_tab;     // single-pass slices: per group, bucket starts + end (else nullptr)
     unsigned* tile_begin;     // single-pass slices: tile list starts, written by the last group
     unsigned* grp_surv;       // per K_decide group: survivors (slots g*4096 + [0, S_g))
+    unsigned* surv_bits;      // optional: bit i = Gaussian i survived (K_decide writes its group's words)
     unsigned nfilter;         // 64-Gaussian chunks
     SurvivorRecord* records;  // indexed by candidate slot
     uint32_t* survivor_list;  // survivor slot -> set index (K_decide)
@@ -770,6 +785,8 @@ void launch_chain_exact(const ChainLaunch& a, int grid, cudaStream_t st);
 void launch_adam(const AdamLaunch& a, cudaStream_t st);
 void launch_adam_consts(const AdamLaunch& a, cudaStream_t st);
 void launch_sum_slots(const AdamLaunch& a, cudaStream_t st);
+void launch_adam_rest(const AdamLaunch& a, const unsigned* surv_bits, int ctas, cudaStream_t st);
+void launch_adam_final(const AdamLaunch& a, unsigned ngroups, cudaStream_t st);
 enum ScatterMode : int { kScatterSet = 1, kScatterAdd = 2, kScatterClearMap = 4 };
 void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, int mode, cudaStream_t st);
 void launch_loss(const LossLaunch& a, cudaStream_t st);

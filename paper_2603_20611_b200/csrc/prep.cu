@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     __shared__ unsigned s_cnt[2][kDecideThreads / 32];
     __shared__ unsigned s_cpre[kDecideChunks + 1];
     __shared__ unsigned s_grp, s_nsurv, s_nexact;
+    __shared__ unsigned s_bits[kDecideGroup / 32];  // survivor bits of the group (a.surv_bits)
     __shared__ unsigned long long s_excl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned dmask = (1u << a.digit_bits) - 1;
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     const int tiles_x = a.slice.tiles_x;
     const unsigned ngroups = gridDim.x;
     for (int k = tid; k < a.passes * kMaxBuckets; k += kDecideThreads) (&s_hist[0][0])[k] = 0;
+    for (int k = tid; k < kDecideGroup / 32; k += kDecideThreads) s_bits[k] = 0;
     if (tid == 0) {
         s_grp = blockIdx.x;
         s_nsurv = 0;
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
             a.records[base + rank] = rec;
             store_cand(a.surv_params + base + rank, pf, i);
             a.survivor_list[base + rank] = i;
+            atomicOr(&s_bits[(i - base) >> 5], 1u << (i & 31));
             // fp64-decided survivors take the fp64 chain (K_chain_exact, which
             // runs beside K_chain once the backward is done)
             if (rec.gidx & kExactFlag) a.exact_list[atomicAdd(&a.ctrl->chain_exact, 1u)] = base + rank;
@@ -172,6 +175,8 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     }
     __syncthreads();
     const unsigned S = s_nsurv;
+    if (a.surv_bits)  // the group's 4096 bits, every word (no clearing between slices)
+        for (int k = tid; k < kDecideGroup / 32; k += kDecideThreads) a.surv_bits[(uint64_t)g * (kDecideGroup / 32) + k] = s_bits[k];
     if (tid == 0) {  // statistics (gpk_prepare_stats)
         if (nc) atomicAdd(&a.ctrl->candidates, nc);
         if (s_nexact) atomicAdd(&a.ctrl->exact_decided, s_nexact);

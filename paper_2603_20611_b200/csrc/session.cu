@@ -167,6 +167,18 @@ struct gpk_session {
     bool assume_prefiltered = false;  // set while capturing a pipelined train step
     bool fuse_gather = false;         // training step: the next prepare leaves the gather to the forward
     bool fuse_gather_ok = true;       // (GPK_FUSE_GATHER=0: the gather stays its own kernel; A/B measurements)
+    // Adam split around the render (single-GPU training step): the
+    // non-survivors' update on adam_stream beside the render (k_adam_rest,
+    // adam_rest_ctas CTAs, -1 = one per 512 Gaussians), the survivors' after
+    // the chain. Off: measured slower on B200 (C2: 0.170-0.300 ms vs 0.139 ms
+    // per step — the streaming Adam's CTAs hold the SMs the latency-bound
+    // slice kernels need). GPK_ADAM_SPLIT=1 enables it,
+    // GPK_ADAM_REST_CTAS sizes it.
+    bool adam_split = false;
+    int adam_rest_ctas = -1;
+    cudaStream_t adam_stream = nullptr;
+    cudaEvent_t ev_rest_fork = nullptr, ev_rest_join = nullptr;
+    DevBuf surv_bits;                 // K_decide: bit i = Gaussian i survived the last prepare
     struct CaptureMeta {
         bool needs_prefilter = false, sets_prefilter = false, writes_params = false;
         gpk_slice_pose next_pose{};
@@ -501,6 +513,7 @@ PrepLaunch prep_launch(gpk_session* s, const SliceArgs& a, int passes, int digit
     pl.cand_count = s->cand_count.as<unsigned>();
     pl.grp_pairs = s->grp_pairs();
     pl.grp_surv = s->grp_surv();
+    pl.surv_bits = s->surv_bits.as<unsigned>();
     pl.bucket_tab = passes == 1 ? s->bucket_tab.as<unsigned>() : nullptr;
     pl.tile_begin = s->grp_begin();
     pl.grads_dirty = s->grads_dirty();
@@ -904,6 +917,7 @@ int alloc_slice_bufs(gpk_session* s, uint64_t cap) {
     s->gmap_dirty = false;
     TRY(mark_grads_dense(s));
     CK(s->survivors.ensure(cap * 4));
+    CK(s->surv_bits.ensure(cap / 8 + 512));
     CK(s->head.ensure(head_size(cap)));
     s->cap = cap;
     ++s->alloc_epoch;
@@ -1288,6 +1302,8 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     }
     cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (const char* f = getenv("GPK_FUSE_GATHER")) s->fuse_gather_ok = f[0] != '0';
+    if (const char* f = getenv("GPK_ADAM_SPLIT")) s->adam_split = f[0] == '1';
+    if (const char* f = getenv("GPK_ADAM_REST_CTAS")) s->adam_rest_ctas = atoi(f);
     if (s->num_sms < 1) s->num_sms = 148;
     e = s->persist.ensure(kPersistBytes);
     if (e == cudaSuccess) e = cudaMemsetAsync(s->persist.p, 0, kPersistBytes, s->stream);
@@ -1308,6 +1324,9 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_bjoin, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_ord, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->adam_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_rest_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_rest_join, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) {
         gpk_session_destroy(s);
@@ -1348,7 +1367,7 @@ static int session_destroy(gpk_session* s) {
                       &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm, &s->acc_norm, &s->acc_obs, &s->acc_world,
                       &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table, &s->bucket_tab,
                       &s->dirty_idx, &s->vox_records, &s->slot_grads, &s->gmap, &s->union_words,
-                      &s->union_prefix, &s->umap, &s->urows, &s->uctrl,
+                      &s->union_prefix, &s->umap, &s->urows, &s->uctrl, &s->surv_bits,
                       &s->volume, &s->dl_dv_vol, &s->vox_partials};
     for (DevBuf* b : bufs) b->release();
     drain_timing(s);
@@ -1371,6 +1390,12 @@ static int session_destroy(gpk_session* s) {
     if (s->ev_tgt_ready) cudaEventDestroy(s->ev_tgt_ready);
     if (s->ev_bjoin) cudaEventDestroy(s->ev_bjoin);
     if (s->ev_ord) cudaEventDestroy(s->ev_ord);
+    if (s->ev_rest_fork) cudaEventDestroy(s->ev_rest_fork);
+    if (s->ev_rest_join) cudaEventDestroy(s->ev_rest_join);
+    if (s->adam_stream) {
+        cudaStreamSynchronize(s->adam_stream);
+        cudaStreamDestroy(s->adam_stream);
+    }
     if (s->comm) gpk_comm_destroy(s);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
@@ -1907,10 +1932,39 @@ static int train_body_(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf
     s->fuse_gather = false;
     TRY(pst);
     s->assume_prefiltered = false;
+    const bool dp = session_comm(s) != nullptr;
+    // the non-survivors' Adam beside the render (see gpk_session::adam_split)
+    const bool split = s->adam_split && !dp && !next && s->n && s->consts_pending;
+    if (split) {
+        const AdamLaunch ar = adam_launch(s, lr, true, total, nullptr);
+        CK(cudaEventRecord(s->ev_rest_fork, s->stream));
+        CK(cudaStreamWaitEvent(s->adam_stream, s->ev_rest_fork, 0));
+        CK(cudaStreamWaitEvent(s->adam_stream, s->ev_cjoin, 0));  // the step's constants
+        s->consts_pending = false;
+        {
+            StageScope scope(s, GPK_STAGE_ADAM_REST, s->adam_stream);
+            launch_adam_rest(ar, s->surv_bits.as<unsigned>(), s->adam_rest_ctas, s->adam_stream);
+            CK(cudaGetLastError());
+        }
+        CK(cudaEventRecord(s->ev_rest_join, s->adam_stream));
+    }
     TRY(run_rasterize(s));
     TRY(run_loss(s, lambda, dssim_scale, true));
-    const bool dp = session_comm(s) != nullptr;
     TRY(run_backward(s, false, /*slots=*/!dp));  // dense planes for the collectives
+    if (split) {
+        CK(cudaStreamWaitEvent(s->stream, s->ev_rest_join, 0));
+        AdamLaunch a = adam_launch(s, lr, true, total, nullptr);
+        a.slot_grads = s->slot_grads.as<float>();
+        a.gmap = s->gmap.as<uint16_t>();
+        a.surv_gidx = s->survivors.as<uint32_t>();
+        a.grp_surv = s->grp_surv();
+        s->gmap_dirty = false;  // k_adam_final clears the survivors' map entries
+        s->prefilter.valid = false;
+        StageScope scope(s, GPK_STAGE_ADAM);
+        launch_adam_final(a, (unsigned)decide_group_count(s->n), s->stream);
+        CK(cudaGetLastError());
+        return GPK_OK;
+    }
     if (dp && s->n && s->cap % (uint64_t)s->comm_world == 0) {
         TRY(dp_reduce_scatter(s));
         const uint64_t chunk = dp_chunk(s), lo = (uint64_t)s->comm_rank * chunk;

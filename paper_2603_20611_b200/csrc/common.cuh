@@ -40,6 +40,24 @@ constexpr int kSuperTiles = 16;                         // sort tiles per super-
 constexpr int kNumParams = 11;
 constexpr int kMaxBatch = 8;                            // slices per batched step (gpk_train_step_batch)
 
+// Digit-count rows of one radix pass (a region of sort_status, nb counts per
+// row): a row per sort tile [0, tiles_cap), then a super row per 16 tiles.
+// Before the pass reads them, k_super_scan turns the super rows into their
+// exclusive prefix over the super-tiles, so a tile's output offsets add one
+// super row and at most 15 tile rows.
+__host__ __device__ __forceinline__ uint64_t sort_supers_cap(uint64_t tiles_cap) {
+    return (tiles_cap + kSuperTiles - 1) / kSuperTiles;
+}
+__device__ __forceinline__ unsigned* sort_super_row(unsigned* region, uint64_t tiles_cap, unsigned nb, unsigned t) {
+    return region + (tiles_cap + t / kSuperTiles) * nb;
+}
+// v more keys of digit d in sort tile t (its tile and super rows)
+__device__ __forceinline__ void sort_count(unsigned* region, uint64_t tiles_cap, unsigned nb, unsigned t, unsigned d,
+                                           unsigned v) {
+    atomicAdd(&region[(uint64_t)t * nb + d], v);
+    atomicAdd(&sort_super_row(region, tiles_cap, nb, t)[d], v);
+}
+
 // Error codes recorded on the device (mirrors gpk_status).
 enum DevErr : int {
     kErrNone = 0,
@@ -519,8 +537,9 @@ struct SortLaunch {
     unsigned* prev_sort_words;     // written by the last pass: {sort tiles, buckets, passes}
     unsigned* grp_begin;           // last pass only: first sorted position of every digit (+ end)
     const uint2* grp_pairs;        // pass over K_decide output: sort tiles are its groups (in group
-    unsigned ngroups;              //   order = slot order); nullptr: tiles of kSortTile positions
+    unsigned ngroups;              //   order = slot order); nullptr: tiles of kSortTile << tile_shift positions
     int shift;
+    int tile_shift;                // position tiles are kSortTile << tile_shift keys (<= ~1024 tiles)
     int bits;                      // digit width of this pass
     unsigned next_buckets;         // 2^bits of the next pass
     int pass;
@@ -696,6 +715,7 @@ struct VoxPrepLaunch {
     uint64_t sort_tiles_cap;
     int passes;
     int digit_bits;
+    int tile_shift;            // sort tiles of kSortTile << tile_shift positions (SortLaunch)
     unsigned long long* chunk_words;  // per 256-prim chunk: ready<<63 | S<<32 | P
     Control* ctrl;
     ErrorState* err;
@@ -778,6 +798,8 @@ void launch_prep_multi(const PrepLaunch* pl, int nb, int num_sms, cudaStream_t s
 void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& next, cudaStream_t st);
 void launch_bin(const PrepLaunch& a, cudaStream_t st);
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st);
+void launch_super_scan(unsigned* region, uint64_t tiles_cap, unsigned nb, const Control* ctrl, uint64_t pair_cap,
+                       unsigned ngroups, unsigned tile_keys, cudaStream_t st);
 void launch_raster_fwd(const RasterLaunch& a, cudaStream_t st);
 void launch_raster_bwd(const RasterLaunch& a, cudaStream_t st);
 void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st);

@@ -199,11 +199,11 @@ constexpr int kFilterThreads = 256;
 __device__ __forceinline__ void clear_prev_sort_rows(const PrepLaunch& a, unsigned gtid, unsigned gthreads) {
     const unsigned pt = a.prev_sort_words[0], pnb = a.prev_sort_words[1], pp = a.prev_sort_words[2];
     const unsigned tile_words = pt * pnb;
-    const unsigned used = tile_words + ((pt + kSuperTiles - 1) / kSuperTiles) * pnb;  // per pass
+    const unsigned used = tile_words + (unsigned)sort_supers_cap(pt) * pnb;  // per pass
     for (unsigned ps = 0; ps < pp; ++ps) {
         unsigned* region = a.tile_hist_all + (uint64_t)ps * a.hist_region;
-        unsigned* super = region + a.sort_tiles_cap * pnb - tile_words;
-        for (unsigned w = gtid; w < used; w += gthreads) (w < tile_words ? region : super)[w] = 0u;
+        unsigned* super = sort_super_row(region, a.sort_tiles_cap, pnb, 0);
+        for (unsigned w = gtid; w < used; w += gthreads) (w < tile_words ? region : super - tile_words)[w] = 0u;
     }
 }
 

@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     // first radix pass: this group's digit-count row (plain stores, every digit),
     // its super-row and the global counts of every pass
     unsigned* row = a.tile_hist0 + (uint64_t)g * nb;
-    unsigned* super = a.tile_hist0 + (a.sort_tiles_cap + g / kSuperTiles) * nb;
+    unsigned* super = sort_super_row(a.tile_hist0, a.sort_tiles_cap, nb, g);
     for (unsigned d = tid; d <= dmask; d += kDecideThreads) {
         const unsigned v = s_hist[0][d];
         row[d] = v;
@@ -625,9 +625,8 @@ __global__ void __launch_bounds__(256) k_vprep(const VoxPrepLaunch a) {
                 a.keys[pos] = tile;
                 a.vals[pos] = chunk * 256 + lo;
                 if (a.passes > 0) {
-                    const uint64_t st = pos / kSortTile;
-                    atomicAdd(&a.tile_hist0[st * (dmask + 1) + (tile & dmask)], 1u);
-                    atomicAdd(&a.tile_hist0[(a.sort_tiles_cap + st / kSuperTiles) * (dmask + 1) + (tile & dmask)], 1u);
+                    const unsigned st = (unsigned)(pos / ((uint64_t)kSortTile << a.tile_shift));
+                    sort_count(a.tile_hist0, a.sort_tiles_cap, dmask + 1, st, tile & dmask, 1u);
                 }
                 for (int ps = 0; ps < a.passes; ++ps)
                     atomicAdd(&s_hist[ps][(tile >> (a.digit_bits * ps)) & dmask], 1u);

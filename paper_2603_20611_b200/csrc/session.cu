@@ -403,8 +403,7 @@ int size_sort_status(gpk_session* s) {
     const uint64_t st_tiles = std::max<uint64_t>((s->pair_cap + kSortTile - 1) / kSortTile,
                                                  decide_group_count(std::max<uint64_t>(s->cap, 1)));
     if (st_tiles <= s->sort_tiles_cap && s->sort_status.p) return GPK_OK;
-    const uint64_t super_tiles = (st_tiles + kSuperTiles - 1) / kSuperTiles;
-    const uint64_t region = (st_tiles + super_tiles) * kMaxBuckets;
+    const uint64_t region = (st_tiles + sort_supers_cap(st_tiles)) * kMaxBuckets;
     CK(s->sort_status.ensure((size_t)kMaxSortPasses * region * 4));
     CK(cudaMemsetAsync(s->sort_status.p, 0, s->sort_status.bytes, s->stream));
     CK(cudaMemsetAsync(s->prev_sort_words(), 0, 12, s->stream));
@@ -498,7 +497,7 @@ void sort_plan(int tiles, int& passes, int& digit_bits) {
 }
 
 int launch_sorts(gpk_session* s, int passes, int digit_bits, const uint2* grp_pairs = nullptr,
-                 unsigned ngroups = 0);
+                 unsigned ngroups = 0, int tile_shift = 0);
 uint64_t decide_group_count(uint64_t n);
 GatherLaunch gather_args(gpk_session* s);
 
@@ -649,7 +648,18 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
 uint64_t decide_group_count(uint64_t n) { return (filter_blocks(n) + kDecideChunks - 1) / kDecideChunks; }
 
 // Stable LSD radix passes over the (key, value) pairs in keys[0]/vals[0].
-int launch_sorts(gpk_session* s, int passes, int digit_bits, const uint2* grp_pairs, unsigned ngroups) {
+// Position tiles of the voxelizer's radix passes: kSortTile << shift keys, at
+// most 16k tiles per pass over its capacity-sized pair list (the per-tile row
+// work is bounded by the super-row prefix, so smaller tiles only add CTAs).
+// The slice passes keep 1024-key tiles.
+int sort_tile_shift(uint64_t pair_cap) {
+    int shift = 0;
+    while (((pair_cap + ((uint64_t)kSortTile << shift) - 1) >> (10 + shift)) > 16384 && shift < 12) ++shift;
+    return shift;
+}
+
+int launch_sorts(gpk_session* s, int passes, int digit_bits, const uint2* grp_pairs, unsigned ngroups,
+                 int tile_shift) {
     const int grid = (int)std::max<uint64_t>(
         1, std::min<uint64_t>(std::max<uint64_t>(s->sort_tiles_cap, ngroups), (uint64_t)s->num_sms * 4));
     const size_t region = s->hist_region;
@@ -667,6 +677,7 @@ int launch_sorts(gpk_session* s, int passes, int digit_bits, const uint2* grp_pa
         sl.grp_begin = (p + 1 == passes) ? s->grp_begin() : nullptr;
         sl.sort_tiles_cap = s->sort_tiles_cap;
         sl.shift = digit_bits * p;
+        sl.tile_shift = tile_shift;
         sl.bits = digit_bits;
         sl.next_buckets = 1u << digit_bits;
         sl.pass = p;
@@ -674,6 +685,10 @@ int launch_sorts(gpk_session* s, int passes, int digit_bits, const uint2* grp_pa
         sl.pair_cap = s->pair_cap;
         sl.grp_pairs = p == 0 ? grp_pairs : nullptr;
         sl.ngroups = ngroups;
+        launch_super_scan(s->sort_status.as<unsigned>() + (size_t)p * region, s->sort_tiles_cap, 1u << digit_bits,
+                          s->ctrl(), s->pair_cap, p == 0 && grp_pairs ? ngroups : 0u,
+                          (unsigned)kSortTile << tile_shift, s->stream);
+        CK(cudaGetLastError());
         launch_sort_pass(sl, grid, s->stream);
         CK(cudaGetLastError());
     }
@@ -1222,6 +1237,7 @@ int run_vox_prep(gpk_session* s, const gpk_voxelizer_config* cfg) {
     p.sort_tiles_cap = s->sort_tiles_cap;
     p.passes = vs.passes;
     p.digit_bits = vs.digit_bits;
+    p.tile_shift = sort_tile_shift(s->pair_cap);
     p.chunk_words = reinterpret_cast<unsigned long long*>(s->filter_flags());
     p.ctrl = s->ctrl();
     p.err = s->err();
@@ -1229,7 +1245,7 @@ int run_vox_prep(gpk_session* s, const gpk_voxelizer_config* cfg) {
     p.grid = (int)std::min<uint64_t>(exact_chunks(s->n), (uint64_t)s->num_sms * 4);
     launch_vox_prep(p, s->stream);
     CK(cudaGetLastError());
-    TRY(launch_sorts(s, vs.passes, vs.digit_bits));
+    TRY(launch_sorts(s, vs.passes, vs.digit_bits, nullptr, 0, p.tile_shift));
     return GPK_OK;
 }
 

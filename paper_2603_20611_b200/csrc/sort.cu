@@ -36,19 +36,19 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
     const bool groups = a.grp_pairs != nullptr;
-    const unsigned ntiles = groups ? a.ngroups : (P + kSortTile - 1) / kSortTile;
+    const unsigned tile_keys = (unsigned)kSortTile << a.tile_shift;
+    const unsigned ntiles = groups ? a.ngroups : (P + tile_keys - 1) / tile_keys;
     const unsigned nb = 1u << a.bits;
     const unsigned mask = nb - 1;
     if (blockIdx.x == 0 && tid == 0 && a.grp_begin) a.grp_begin[nb] = P;
     if (blockIdx.x == 0 && tid == 0 && !a.tile_hist_next) {
         // rows the filter clears before the next prepare: the largest tile
         // count any pass of this sort used (group rows or position tiles)
-        const unsigned pos_tiles = (P + kSortTile - 1) / kSortTile;
+        const unsigned pos_tiles = (P + tile_keys - 1) / tile_keys;
         a.prev_sort_words[0] = max(ntiles, max(pos_tiles, a.ngroups));
         a.prev_sort_words[1] = nb;
         a.prev_sort_words[2] = (unsigned)a.pass + 1;
     }
-    const unsigned* super_rows = a.tile_hist + a.sort_tiles_cap * nb;
 
     for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
         unsigned first, count;
@@ -57,8 +57,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
             first = min(gp.x, P);
             count = min(gp.x + gp.y, P) - first;
         } else {
-            first = t * kSortTile;
-            count = min(P - first, (unsigned)kSortTile);
+            first = t * tile_keys;
+            count = min(P - first, tile_keys);
         }
         // ---- global digit base: exclusive scan of the histogram (nb <= 1024)
         {
@@ -91,23 +91,25 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
             }
             __syncthreads();
         }
-        // ---- add the counts of all earlier tiles: whole super-tiles from the
-        // super rows, then the earlier tiles of this super-tile (<= 15 rows).
-        // Thread owns 4 consecutive digits (one 16 B load per row); rows are
-        // unrolled so all of a thread's loads are in flight together.
+        // ---- add the counts of all earlier tiles: the super row holds the
+        // prefix over the earlier super-tiles (k_super_scan), then the earlier
+        // tiles of this super-tile (<= 15 rows). Thread owns 4 consecutive
+        // digits (one 16 B load per row); rows are unrolled so all of a
+        // thread's loads are in flight together.
         {
-            const unsigned sup = t / kSuperTiles;
-            const unsigned t0 = sup * kSuperTiles;
-            const unsigned nrows = sup + (t - t0);  // super rows first, then tile rows
+            const unsigned* region = a.tile_hist;
+            const unsigned sup = t / kSuperTiles, t0 = sup * kSuperTiles;
+            const unsigned nrows = 1 + (t - t0);  // the super prefix, then tile rows
+            auto row_of = [&](unsigned r) -> const unsigned* {
+                return r == 0 ? region + (a.sort_tiles_cap + sup) * nb : region + (size_t)(t0 + r - 1) * nb;
+            };
             if (nb >= 4) {
                 const unsigned d0 = tid * 4;
                 if (d0 < nb) {
                     uint4 acc = make_uint4(0, 0, 0, 0);
 #pragma unroll 8
                     for (unsigned r = 0; r < nrows; ++r) {
-                        const unsigned* row = r < sup ? super_rows + (size_t)r * nb
-                                                      : a.tile_hist + (size_t)(t0 + r - sup) * nb;
-                        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(row + d0));
+                        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(row_of(r) + d0));
                         acc.x += v.x;
                         acc.y += v.y;
                         acc.z += v.z;
@@ -120,8 +122,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
                 }
             } else if ((unsigned)tid < nb) {
                 unsigned acc = 0;
-                for (unsigned r = 0; r < nrows; ++r)
-                    acc += r < sup ? super_rows[(size_t)r * nb + tid] : a.tile_hist[(size_t)(t0 + r - sup) * nb + tid];
+                for (unsigned r = 0; r < nrows; ++r) acc += row_of(r)[tid];
                 s_base[tid] += acc;
             }
         }
@@ -156,9 +157,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
                         a.vals_out[pos] = val;
                         if (a.tile_hist_next) {
                             const unsigned nd = (key >> (a.shift + a.bits)) & (a.next_buckets - 1);
-                            const unsigned st = pos / kSortTile;
-                            atomicAdd(&a.tile_hist_next[(size_t)st * a.next_buckets + nd], 1u);
-                            atomicAdd(&a.tile_hist_next[(a.sort_tiles_cap + st / kSuperTiles) * a.next_buckets + nd], 1u);
+                            sort_count(a.tile_hist_next, a.sort_tiles_cap, a.next_buckets, pos / tile_keys, nd, 1u);
                         }
                     }
                 }
@@ -213,9 +212,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
                     a.vals_out[pos] = val[r];
                     if (a.tile_hist_next) {
                         const unsigned nd = (key[r] >> (a.shift + a.bits)) & (a.next_buckets - 1);
-                        const unsigned st = pos / kSortTile;
-                        atomicAdd(&a.tile_hist_next[(size_t)st * a.next_buckets + nd], 1u);
-                        atomicAdd(&a.tile_hist_next[(a.sort_tiles_cap + st / kSuperTiles) * a.next_buckets + nd], 1u);
+                        sort_count(a.tile_hist_next, a.sort_tiles_cap, a.next_buckets, pos / tile_keys, nd, 1u);
                     }
                 }
             }
@@ -223,6 +220,46 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
         }
         }
         __syncthreads();  // s_base / s_wsum are rewritten for the next tile
+    }
+}
+
+// Before a pass: the super rows (counts of 16 sort tiles each) become their
+// exclusive prefix over the super-tiles, digit by digit (CTA per digit,
+// block scan of the column), so a tile's offsets need one super row and at
+// most 15 tile rows whatever the number of tiles.
+constexpr int kScanThreads = 512;
+
+__global__ void __launch_bounds__(kScanThreads) k_super_scan(unsigned* __restrict__ region, uint64_t tiles_cap,
+                                                             unsigned nb, const Control* ctrl, uint64_t pair_cap,
+                                                             unsigned ngroups, unsigned tile_keys) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    __shared__ unsigned s_wsum[kScanThreads / 32];
+    __shared__ unsigned s_carry;
+    const unsigned d = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned P = stored_pairs(ctrl, pair_cap);
+    const unsigned ntiles = ngroups ? ngroups : (P + tile_keys - 1) / tile_keys;
+    const unsigned nsup = (ntiles + kSuperTiles - 1) / kSuperTiles;
+    unsigned* col = region + tiles_cap * nb + d;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (unsigned s0 = 0; s0 < nsup; s0 += kScanThreads) {
+        const unsigned sidx = s0 + tid;
+        const unsigned v = sidx < nsup ? __ldcg(&col[(size_t)sidx * nb]) : 0u;
+        unsigned incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        unsigned ex = s_carry + incl - v;
+        for (int w = 0; w < warp; ++w) ex += s_wsum[w];
+        if (sidx < nsup) col[(size_t)sidx * nb] = ex;
+        __syncthreads();
+        if (tid == kScanThreads - 1) s_carry = ex + v;
+        __syncthreads();
     }
 }
 
@@ -276,6 +313,12 @@ void launch_gather(const GatherLaunch& a, cudaStream_t st) {
 void launch_pair_records(const uint32_t* keys, const uint32_t* vals, const SurvivorRecord* records, PairRecord* pairs,
                          const Control* ctrl, uint64_t pair_cap, const SliceArgs& slice, int num_sms, cudaStream_t st) {
     launch_pdl(k_pair_records, dim3(num_sms * 8), dim3(256), 0, st, keys, vals, records, pairs, ctrl, pair_cap, slice);
+}
+
+void launch_super_scan(unsigned* region, uint64_t tiles_cap, unsigned nb, const Control* ctrl, uint64_t pair_cap,
+                       unsigned ngroups, unsigned tile_keys, cudaStream_t st) {
+    launch_pdl(k_super_scan, dim3(nb), dim3(kScanThreads), 0, st, region, tiles_cap, nb, ctrl, pair_cap, ngroups,
+               tile_keys);
 }
 
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st) {

@@ -24,8 +24,17 @@ from collections import defaultdict
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
+try:
+    HBM_GBS = float(json.loads((HERE.parent / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+except Exception:  # the profiling recipe's fallback
+    HBM_GBS = 6650.0
+PCT = ["dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sectors.avg.pct_of_peak_sustained_elapsed",
+       "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed",
+       "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+       "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
-           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
+           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum", *PCT,
            "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
            "launch__grid_size", "launch__block_size", "sm__inst_executed.avg.per_cycle_active"]
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3,
@@ -46,6 +55,9 @@ def ncu_raw(rep: str) -> list[dict]:
     for r in rows[2:]:
         d = {"kernel": short(r[head.index("Kernel Name")])}
         for m in METRICS:
+            if m not in head:
+                d[m] = None
+                continue
             i = head.index(m)
             v = float(r[i].replace(",", "")) if r[i] not in ("", "n/a") else None
             if v is not None and units[i] in UNIT:
@@ -84,6 +96,17 @@ def full(rep: str, out: str, config: str) -> None:
             "dram_write_bytes": d["dram__bytes_write.sum"],
             "l2_bytes": d["lts__t_bytes.sum"],
             "smem_wavefronts": d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"],
+            # achieved DRAM bandwidth against MEASURED_PEAKS.json's copy peak, and
+            # ncu's own utilisation of the DRAM, L2, shared-memory, FMA and
+            # MUFU (XU) pipes (percent of peak)
+            "dram_gbs": (((d["dram__bytes_read.sum"] or 0) + (d["dram__bytes_write.sum"] or 0)) /
+                         (d["gpu__time_duration.sum"] * 1e3)) if d["gpu__time_duration.sum"] else None,
+            "dram_frac_of_measured_peak": (((d["dram__bytes_read.sum"] or 0) + (d["dram__bytes_write.sum"] or 0)) /
+                                           (d["gpu__time_duration.sum"] * 1e3) / HBM_GBS)
+            if d["gpu__time_duration.sum"] else None,
+            "l2_gbs": ((d["lts__t_bytes.sum"] or 0) / (d["gpu__time_duration.sum"] * 1e3))
+            if d["gpu__time_duration.sum"] else None,
+            "pct_of_peak": {m.split("__")[1].split(".")[0]: d[m] for m in PCT},
             "warp_instructions": d["smsp__inst_executed.sum"],
             "registers": d["launch__registers_per_thread"],
             "grid": d["launch__grid_size"], "block": d["launch__block_size"],

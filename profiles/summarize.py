@@ -106,7 +106,7 @@ def full(rep: str, out: str, config: str) -> None:
             if d["gpu__time_duration.sum"] else None,
             "l2_gbs": ((d["lts__t_bytes.sum"] or 0) / (d["gpu__time_duration.sum"] * 1e3))
             if d["gpu__time_duration.sum"] else None,
-            "pct_of_peak": {m.split("__")[1].split(".")[0]: d[m] for m in PCT},
+            "pct_of_peak": {m.split(".")[0]: d[m] for m in PCT},
             "warp_instructions": d["smsp__inst_executed.sum"],
             "registers": d["launch__registers_per_thread"],
             "grid": d["launch__grid_size"], "block": d["launch__block_size"],

@@ -715,16 +715,17 @@ def run_ours(args):
         for i in range(3):  # warm-up of the copy path (first transfers on the copy stream)
             e2e_step(i)
         sess.synchronize()
+        # the steps are queued back to back, the host never waits inside the
+        # loop (a training loop's regime: copies and launches run ahead of the
+        # GPU); each step's window — its target upload, the step, its loss
+        # read-back — is bracketed by events, the L2 flush stays outside it
+        torch.cuda.synchronize()
         for i in range(e2e_steps):
-            # two flushes (~80 us of GPU work outside the window) give the host
-            # time to queue the step's calls, so Python submission jitter does
-            # not leave the GPU idle inside the timed region
-            flush()
             flush()
             e_s[i].record(stream)
             e2e_step(i)
             e_e[i].record(stream)
-            e_e[i].synchronize()
+        torch.cuda.synchronize()
         assert np.isfinite(pin_loss.numpy()).all()
         h2d, d2h = B * P * 4, B * 8
         e2e_path = (f"C-ABI: gpk_upload(target, pinned) x {B} + train step (graph) + gpk_download(loss) x {B}")
@@ -745,13 +746,13 @@ def run_ours(args):
         for i in range(3):  # warm-up of the copy path
             e2e_step(i)
         sess.synchronize()
+        torch.cuda.synchronize()
         for i in range(e2e_steps):
-            flush()
             flush()
             e_s[i].record(stream)
             e2e_step(i)
             e_e[i].record(stream)
-            e_e[i].synchronize()
+        torch.cuda.synchronize()
         assert np.isfinite(pin_grads.numpy()[:1000]).all()
         h2d, d2h = B * P * 4, B * P * 4 + gbytes
         e2e_path = (f"C-ABI: gpk_upload(dL/dI) x {B} + fwd_bwd (graph) + gpk_download(image) x {B} "

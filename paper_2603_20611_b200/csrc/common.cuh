@@ -352,18 +352,6 @@ __device__ __forceinline__ void pdl_entry() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-// The step's kernels launch at the device's highest priority: a training
-// step's background work (k_adam_rest, default priority) yields the SMs to
-// them whenever both have CTAs waiting.
-inline int high_priority() {
-    static int p = [] {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        return hi;
-    }();
-    return p;
-}
-
 template <typename... Params, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -372,13 +360,11 @@ inline cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, 
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    attr[1].id = cudaLaunchAttributePriority;
-    attr[1].val.priority = high_priority();
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -407,29 +393,37 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // One tile's list from the K_decide buckets (render.hpp:142-160 order): the
 // buckets of tile d — one per K_decide group, each already in ascending slot
 // order (K_decide fills them stably) — concatenated in group order into
-// vals_out[out ...). The whole CTA (kThreads) copies cooperatively: per chunk
-// of kThreads groups, an exclusive scan of the bucket sizes, then every
-// thread takes list positions and finds its bucket by binary search — work
-// linear in the list length and independent of how the pairs are spread over
-// groups (a clustered set can put hundreds of one group's survivors into one
-// tile). Returns the end of the list. Ends with a barrier.
-template <int kThreads>
+// vals_out[out ...). The whole CTA (kThreads, kItems groups per thread per
+// chunk) copies cooperatively: an exclusive scan of the chunk's bucket sizes,
+// then every thread takes list positions and finds its bucket by binary
+// search — work linear in the list length and independent of how the pairs
+// are spread over groups (a clustered set can put hundreds of one group's
+// survivors into one tile). Returns the end of the list. Ends with a barrier.
+template <int kThreads, int kItems = 1>
 __device__ __forceinline__ unsigned gather_tile_list(const unsigned* __restrict__ bucket_tab, unsigned ngroups,
                                                      unsigned row_stride, unsigned d, unsigned out, unsigned P,
                                                      const uint32_t* vals_in, uint32_t* vals_out,
-                                                     unsigned* s_ex /* kThreads + 1 */, unsigned* s_b /* kThreads */,
+                                                     unsigned* s_ex /* kThreads * kItems + 1 */,
+                                                     unsigned* s_b /* kThreads * kItems */,
                                                      unsigned* s_wsum /* kThreads / 32 */) {
+    constexpr unsigned kChunk = kThreads * kItems;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (unsigned g0 = 0; g0 < ngroups; g0 += kThreads) {
-        const unsigned g = g0 + tid;
-        unsigned b = 0, e = 0;
-        if (g < ngroups) {  // group g's bucket for tile d: [row[d], row[d + 1])
-            const unsigned* row = bucket_tab + (uint64_t)g * row_stride;
-            b = min(__ldcg(&row[d]), P);
-            e = min(__ldcg(&row[d + 1]), P);
+    for (unsigned g0 = 0; g0 < ngroups; g0 += kChunk) {
+        unsigned b[kItems], cnt[kItems], run = 0;
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {  // group g's bucket for tile d: [row[d], row[d + 1])
+            const unsigned g = g0 + tid * kItems + q;
+            unsigned e = 0;
+            b[q] = 0;
+            if (g < ngroups) {
+                const unsigned* row = bucket_tab + (uint64_t)g * row_stride;
+                b[q] = min(__ldcg(&row[d]), P);
+                e = min(__ldcg(&row[d + 1]), P);
+            }
+            cnt[q] = e > b[q] ? e - b[q] : 0u;
+            run += cnt[q];
         }
-        const unsigned cnt = e > b ? e - b : 0u;
-        unsigned incl = cnt;
+        unsigned incl = run;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
@@ -437,17 +431,21 @@ __device__ __forceinline__ unsigned gather_tile_list(const unsigned* __restrict_
         }
         if (lane == 31) s_wsum[warp] = incl;
         __syncthreads();
-        unsigned ex = incl - cnt;
+        unsigned ex = incl - run;
         for (int w = 0; w < warp; ++w) ex += s_wsum[w];
-        s_ex[tid] = ex;
-        s_b[tid] = b;
-        if (tid == kThreads - 1) s_ex[kThreads] = ex + cnt;
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            s_ex[tid * kItems + q] = ex;
+            s_b[tid * kItems + q] = b[q];
+            ex += cnt[q];
+        }
+        if (tid == kThreads - 1) s_ex[kChunk] = ex;
         __syncthreads();
-        const unsigned total = s_ex[kThreads];
+        const unsigned total = s_ex[kChunk];
         for (unsigned t = tid; t < total; t += kThreads) {
             unsigned q = 0;  // last bucket starting at or before t (empty buckets share starts)
 #pragma unroll
-            for (unsigned step = kThreads / 2; step > 0; step >>= 1)
+            for (unsigned step = kChunk / 2; step > 0; step >>= 1)
                 if (s_ex[q + step] <= t) q += step;
             vals_out[out + t] = __ldcg(&vals_in[s_b[q] + (t - s_ex[q])]);
         }

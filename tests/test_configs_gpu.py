@@ -227,3 +227,20 @@ def test_clustered_sets_bitexact_lists(gp, session, ref):
     dl = (rng.uniform(-1, 1, (128, 128)) / 128 ** 2).astype(np.float32)
     S, T = slice_parity(gp, session, ref, blob, pose, gp.PsfSpec(), gp.RasterConfig(), dl)
     assert T > 20 * 9 * 100  # hundreds of Gaussians per tile
+
+
+def test_c4_voxelize_backward_256(gp, session, ref):
+    """voxelize_backward (voxelize.hpp:152-240) at scale: 250k Gaussians on a
+    256^3 grid (2M+ tile instances, two radix passes, 32k voxel tiles) against
+    the reference, gradients to tolerance."""
+    n = 256
+    lo, hi = (-0.5,) * 3, (n - 0.5,) * 3
+    gs = gp.GaussianSet(f32(gp.init_random(250_000, lo, hi, 1.5, 2).records), lo, hi)
+    cfg = gp.VoxelizerConfig(dims=(n, n, n))
+    dl = (np.random.default_rng(8).uniform(-1.0, 1.0, (n, n, n)) / n ** 3).astype(np.float32)
+    session.set_gaussians(gs)
+    g = session.voxelize_backward(cfg, dl)
+    rg = ref.voxelize_backward(gs.records, cfg, dl.astype(np.float64))
+    ok, worst = grads_ok(g, rg)
+    assert ok, f"voxel gradients beyond tolerance (worst {worst:.3f} x bound)"
+    print(f"C4-scale voxelize_backward: grads worst {worst:.3g} x bound")

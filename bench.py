@@ -68,6 +68,7 @@ UNITS = {
 LAMBDA = 0.2
 LR0 = (6e-4, 0.02, 2e-3, 1e-3)      # optimize.hpp:23-26
 TOTAL_ITERS = 30000
+E2E_WARMUP = 32  # untimed end-to-end steps before the e2e window
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -315,7 +316,9 @@ def config_json(args, cfg, world):
             "parallelism": f"slice-sharded dp{world}",
             "l2": "flushed (256 MiB read) before each timed step, outside the event window; "
                   "steady_state = the same steps back to back without the flush",
-            "config_id": args.config}
+            "config_id": args.config,
+            "state": "every measured section (timed, steady state, batched, stages, e2e) starts from the "
+                     "initial parameters and Adam moments"}
 
 
 def data_note(unit):
@@ -514,6 +517,21 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     sess = gp.Session(local, stream=stream.cuda_stream)
     sess.set_gaussians(gs)
+    # Training moves the Gaussians (the synthetic target is noise: scales and
+    # opacities drift and slices get more pairs), so every measured section
+    # below starts from the same initial parameters and moments (restored from
+    # this snapshot) and all of them time the same workload.
+    p_bytes = sess.device_buffer(N.GPK_BUF_PARAMS)[1]
+    init_params = torch.empty(p_bytes // 4, dtype=torch.float32).pin_memory()
+    sess.download(N.GPK_BUF_PARAMS, init_params.data_ptr(), p_bytes)
+    sess.synchronize()
+    init_adam = sess.adam_state()
+
+    def restore_initial_state():
+        sess.synchronize()
+        sess.upload(N.GPK_BUF_PARAMS, init_params.data_ptr(), p_bytes)
+        sess.set_adam_state(*init_adam)
+        sess.synchronize()
     sess.reserve_pairs(max(1 << 20, n))
     psf = gp.PsfSpec(sigma_z=cfg["sigma_z"])
     rcfg = gp.RasterConfig()
@@ -617,6 +635,7 @@ def run_ours(args):
         if world > 1 and not u2:
             dp.allreduce_grads(sess)
 
+    restore_initial_state()
     for i in range(args.warmup):
         step(i)
     sess.synchronize()
@@ -644,6 +663,9 @@ def run_ours(args):
     # steady state: the same steps back to back, no flush (a training loop's
     # regime: the previous step's dirty lines are written back inside this one)
     ss_steps = min(args.steps, 100)
+    restore_initial_state()
+    for i in range(3):
+        step(i)
     ss0, ss1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
@@ -659,6 +681,7 @@ def run_ours(args):
     batched = None
     if B == 1 and world == 1 and not args.no_batched and args.graphs:
         bg = [capture(k, 8) for k in range(len(poses) // 8)]
+        restore_initial_state()
         for i in range(3):
             sess.graph_launch(bg[i % len(bg)])
         torch.cuda.synchronize()
@@ -685,6 +708,7 @@ def run_ours(args):
     # themselves add ~2-4 us per stage, so these over-state each stage a little)
     # (B > 1: only the session's own stream is bracketed: slice 0's kernels and Adam)
     prof_steps = min(args.steps, 100)
+    restore_initial_state()
     sess.stage_timing(True)
     prof_graphs = [capture(k) for k in range(n_groups)]
     sess.stage_times(reset=True)
@@ -700,6 +724,7 @@ def run_ours(args):
     e_s = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)]
     e_e = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps)]
     ctxs = [sess.context(b) for b in range(B)]
+    restore_initial_state()
     if u2:
         # the step's B targets (one per slice context) up, its B losses down
         pin_tgt = [torch.from_numpy(tgt).pin_memory() for _ in range(B)]
@@ -712,7 +737,11 @@ def run_ours(args):
             for b in range(B):
                 ctxs[b].download(N.GPK_BUF_LOSS, pin_loss.data_ptr() + 8 * b, 8)
 
-        for i in range(3):  # warm-up of the copy path (first transfers on the copy stream)
+        # warm-up of the copy path: the first transfers from freshly pinned
+        # pages are slow on the box's host (measured: a pinned 1 MB upload
+        # settles after tens of transfers, tests/_h2d_probe.py)
+        for i in range(E2E_WARMUP):
+            flush()
             e2e_step(i)
         sess.synchronize()
         # the steps are queued back to back, the host never waits inside the
@@ -743,7 +772,8 @@ def run_ours(args):
                 ctxs[b].download(N.GPK_BUF_IMAGE, pin_img.data_ptr() + 4 * P * b, P * 4)
             sess.download(N.GPK_BUF_GRADS, pin_grads.data_ptr(), gbytes)  # dense gradient planes
 
-        for i in range(3):  # warm-up of the copy path
+        for i in range(E2E_WARMUP):  # warm-up of the copy path (as above)
+            flush()
             e2e_step(i)
         sess.synchronize()
         torch.cuda.synchronize()

@@ -33,6 +33,18 @@ for g in graphs:
 s.synchronize()
 
 
+def stages(tag):
+    s.stage_timing(True)
+    pg = [s.capture_train(p, psf, cfg, 0.2, 0.5, lr, 30000) for p in poses]
+    s.stage_times(reset=True)
+    for i in range(64):
+        torch.sum(flush_src, dim=0, out=flush_dst)
+        s.graph_launch(pg[i % 16])
+    s.stage_timing(False)
+    st = s.stage_times(reset=True)
+    print(tag, {k: round(v[0] / v[1] * 1e3, 1) for k, v in st.items() if v[1]}, flush=True)
+
+
 def run(name, up, down, sync_each=True, n=50, flush=True):
     es = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
     ee = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
@@ -53,12 +65,42 @@ def run(name, up, down, sync_each=True, n=50, flush=True):
     print(f"{name:28s} {ms * 1e3:8.1f} us/step")
 
 
+stages("stages before")
 run("graph only, no sync", False, False, sync_each=False)
 run("graph only, sync each", False, False)
 run("upload + graph", True, False)
 run("graph + download", False, True)
 run("upload + graph + download", True, True)
 run("u+g+d no flush", True, True, flush=False)
-for rep in range(2):
+for rep in range(8):
     run("u+g+d rep", True, True)
     run("upload + graph rep", True, False)
+run("u+g+d async (no sync)", True, True, sync_each=False)
+# the upload alone (1 MB pinned H2D through the copy stream)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+cs = torch.cuda.Stream()
+dev = torch.empty(512 * 512, device="cuda")
+e0.record(cs)
+for _ in range(20):
+    dev.copy_(pin_tgt.view(-1), non_blocking=True)
+e1.record(cs)
+torch.cuda.synchronize()
+print(f"{'1 MB H2D (torch)':28s} {e0.elapsed_time(e1) / 20 * 1e3:8.1f} us")
+# the bench's sequence: slice contexts + a batched step, then the graphs recaptured
+for k in range(1, 8):
+    c = s.context(k)
+    c.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
+s.synchronize()
+bg = [s.capture_train_batch(poses[8 * j:8 * j + 8], psf, cfg, 0.2, 0.5, lr, 30000) for j in range(2)]
+for i in range(4):
+    s.graph_launch(bg[i % 2])
+s.synchronize()
+s.graph_destroy_all()
+stages("stages after")
+graphs[:] = [s.capture_train(p, psf, cfg, 0.2, 0.5, lr, 30000) for p in poses]
+for g in graphs:
+    s.graph_launch(g)
+s.synchronize()
+run("graph only (recaptured)", False, False)
+run("u+g+d (recaptured)", True, True)
+run("u+g+d (recaptured) async", True, True, sync_each=False)

@@ -577,6 +577,12 @@ def run_ours(args):
     def flush():
         torch.sum(flush_src, dim=0, out=flush_dst)
 
+    def host_ahead(ms=25.0):
+        # hold the stream for `ms` so the host queues the whole timed loop
+        # before the GPU reaches it: the event windows then time the device
+        # work of each step, not the Python loop's submission jitter
+        torch.cuda._sleep(int(ms * 1e-3 * ClockSampler.peak_mhz(local) * 1e6))
+
     # step i renders group i mod n_groups (B consecutive poses); data-parallel
     # u2: step i's world poses (dp.step_slices), rank r renders the r-th
     dp_union = u2 and world > 1
@@ -646,6 +652,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        host_ahead()
         for i in range(args.steps):
             flush()
             starts[i].record(stream)
@@ -749,6 +756,7 @@ def run_ours(args):
         # GPU); each step's window — its target upload, the step, its loss
         # read-back — is bracketed by events, the L2 flush stays outside it
         torch.cuda.synchronize()
+        host_ahead()
         for i in range(e2e_steps):
             flush()
             e_s[i].record(stream)
@@ -756,6 +764,26 @@ def run_ours(args):
             e_e[i].record(stream)
         torch.cuda.synchronize()
         assert np.isfinite(pin_loss.numpy()).all()
+        if os.environ.get("GPK_BENCH_E2E_DEBUG"):  # where the window's time goes (stderr)
+            for name, up, down in (("graph", 0, 0), ("up+graph", 1, 0), ("graph+down", 0, 1), ("all", 1, 1)):
+                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                      for _ in range(e2e_steps)]
+                host_ahead()
+                for i in range(e2e_steps):
+                    flush()
+                    ev[i][0].record(stream)
+                    if up:
+                        for b in range(B):
+                            ctxs[b].upload(N.GPK_BUF_TARGET, pin_tgt[b].data_ptr(), P * 4)
+                    step(i)
+                    if down:
+                        for b in range(B):
+                            ctxs[b].download(N.GPK_BUF_LOSS, pin_loss.data_ptr() + 8 * b, 8)
+                    ev[i][1].record(stream)
+                torch.cuda.synchronize()
+                t = sorted(a.elapsed_time(b) for a, b in ev)
+                print(f"e2e debug {name:10s} median {t[len(t) // 2] * 1e3:7.1f} us  min {t[0] * 1e3:7.1f}",
+                      file=sys.stderr, flush=True)
         h2d, d2h = B * P * 4, B * 8
         e2e_path = (f"C-ABI: gpk_upload(target, pinned) x {B} + train step (graph) + gpk_download(loss) x {B}")
     else:
@@ -777,6 +805,7 @@ def run_ours(args):
             e2e_step(i)
         sess.synchronize()
         torch.cuda.synchronize()
+        host_ahead()
         for i in range(e2e_steps):
             flush()
             e_s[i].record(stream)
@@ -790,6 +819,23 @@ def run_ours(args):
     e2e_each = sorted(s.elapsed_time(e) for s, e in zip(e_s, e_e))
     e2e_ms = sum(e2e_each) / e2e_steps
     e2e_ms = dp.max_over_ranks([e2e_ms], device="cuda")[0]
+    # the box's pinned host->device copy time of one step's input (the e2e
+    # window waits for it when it exceeds the step's time to the loss; it
+    # varies between boxes and over time on this pool)
+    probe_src = torch.from_numpy(np.ascontiguousarray(tgt if u2 else dl)).pin_memory()
+    probe_dst = torch.empty(probe_src.numel(), dtype=torch.float32, device="cuda")
+    probe_stream = torch.cuda.Stream(device=local)
+    h2d_us = []
+    for i in range(21):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(probe_stream):
+            a0.record(probe_stream)
+            probe_dst.copy_(probe_src.view(-1), non_blocking=True)
+            a1.record(probe_stream)
+        probe_stream.synchronize()
+        if i:
+            h2d_us.append(a0.elapsed_time(a1) * 1e3)
+    h2d_us.sort()
 
     # ---- roofline of the dominant kernel -------------------------------------------
     # Algorithmic bytes per launch (each logical tensor read or written once at its
@@ -818,7 +864,11 @@ def run_ours(args):
         "adam": ("k_adam_cull", 266 * n + 44 * S + 48 * Cc,
                  "266N + 44S: read params, m, v, 2 B slot map; write params, m, v; survivor gradients "
                  "+ 48C next-slice candidates")
-        if (u2 and args.pipeline and world == 1) else
+        if (u2 and args.pipeline and world == 1 and os.environ.get("GPK_LAZY_ADAM") != "1") else
+        ("k_lazy_survivors + k_lazy_window", 322 * S + (n / 16) * 272,
+         "322S + 272N/16: the survivors' params, m, v read and written, their slot gradients, t_done, set "
+         "index, map; the step's 1/16 window of params, m, v, t_done read and written (lazy mode)")
+        if (u2 and world == 1 and B == 1 and os.environ.get("GPK_LAZY_ADAM") == "1") else
         ("k_adam_final", 264 * S + 44 * S + 6 * S,
          "264S + 44S + 6S: the survivors' params, m, v read and written, their slot gradients, set index, map")
         if (world == 1 and B == 1 and "adam_rest" in stages and stages["adam_rest"][1]) else
@@ -888,7 +938,9 @@ def run_ours(args):
         "fp64_decided_mean": X64_mean,
         "e2e": {"value": world * B * 1000.0 / e2e_ms, "unit": "slices/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "path": e2e_path,
-                "ms_min": e2e_each[0], "ms_median": e2e_each[len(e2e_each) // 2], "ms_max": e2e_each[-1]},
+                "ms_min": e2e_each[0], "ms_median": e2e_each[len(e2e_each) // 2], "ms_max": e2e_each[-1],
+                "h2d_probe_us": {"bytes": probe_src.numel() * 4, "median": h2d_us[len(h2d_us) // 2],
+                                 "min": h2d_us[0], "max": h2d_us[-1]}},
         "gpu_launches": None,
         "clocks": clk.result(),
     }

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GPK_ABI_VERSION 6
+#define GPK_ABI_VERSION 7
 #define GPK_RECORD_FLOATS 11
 
 typedef enum {
@@ -255,6 +255,16 @@ int gpk_set_adam_state(gpk_session* s, const float* m, const float* v, int64_t s
 int gpk_fwd_bwd_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                       const gpk_raster_config* cfg);
 /* U2: prepare + rasterize + loss(GPK_BUF_TARGET) + backward + scheduled Adam. */
+/* Lazy mode (off by default; measured slower on B200): single-GPU
+ * U2 steps run "lazily": Adam updates the slice's
+ * survivors and one 1/16 window of the set per step; every other Gaussian's
+ * zero-gradient step (optimize.hpp:195-221 with g = 0) is deferred and
+ * replayed, in order and with the same fp32 operations, where it is next
+ * needed — by the next cull for the Gaussians it cannot reject, by the window,
+ * and by every API call that reads or writes parameters or moments — so each
+ * result is bit-identical to the eager step. on = 0 (the default): every step
+ * updates all n (the deferred steps are replayed first). */
+int gpk_set_lazy_adam(gpk_session* s, int on);
 int gpk_train_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                    const gpk_raster_config* cfg, double lambda, double dssim_scale,
                    const gpk_learning_rates* lr0, int32_t total_iterations);

@@ -13,7 +13,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libgpile_b200.so"
-GPK_ABI_VERSION = 6  # include/gpile_b200.h
+GPK_ABI_VERSION = 7  # include/gpile_b200.h
 
 GPK_OK = 0
 GPK_ERR_INVALID_ARGUMENT = 1
@@ -168,6 +168,7 @@ _PROTOS = {
     "gpk_upload": (C.c_int, [_P, C.c_int, _P, C.c_uint64]),
     "gpk_download": (C.c_int, [_P, C.c_int, _P, C.c_uint64]),
     "gpk_stage_timing": (C.c_int, [_P, C.c_int]),
+    "gpk_set_lazy_adam": (C.c_int, [_P, C.c_int]),
     "gpk_stage_times": (C.c_int, [_P, _D, _U64, C.c_int]),
     "gpk_set_gaussians": (C.c_int, [_P, C.c_uint64, _F, C.POINTER(Bounds)]),
     "gpk_set_gaussians_f64": (C.c_int, [_P, C.c_uint64, _D, C.POINTER(Bounds)]),

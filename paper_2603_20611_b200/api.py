@@ -400,6 +400,13 @@ class Session:
     STAGES = ("prepare", "sort", "raster", "backward", "chain", "loss", "adam", "voxel", "bin", "voxel_eval",
               "adam_rest")
 
+    def set_lazy_adam(self, on: bool = True):
+        """Lazy single-GPU training steps (include/gpile_b200.h gpk_set_lazy_adam;
+        off by default, measured slower): deferred zero-gradient Adam steps,
+        bit-identical results; off: every step updates all n. Graphs captured
+        before a mode change must be recaptured."""
+        check(N.lib.gpk_set_lazy_adam(self._h, 1 if on else 0))
+
     def stage_timing(self, enable: bool = True):
         check(N.lib.gpk_stage_timing(self._h, 1 if enable else 0))
 

@@ -14,6 +14,7 @@
 // (:212), log-scale, raw alpha, quaternion update then renormalisation when
 // the norm is > 0 (:216-217).
 #include <algorithm>
+#include <cmath>
 
 #include "adam.cuh"
 
@@ -27,7 +28,35 @@ __global__ void k_adam_consts(const AdamLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     AdamConsts c;
     adam_consts(a, c);
-    if (threadIdx.x == 0) *a.consts = c;
+    const int lane = threadIdx.x & 31;
+    AdamConsts* ring = a.lazy.ring;  // lazy training steps only (else nullptr)
+    if (ring) {
+        // LazyAdam drift bound of this step: |delta p| = lr/bc1 |m| / (sqrt(v/bc2) + eps)
+        // <= lr (|m| / sqrt(v)) sqrt(bc2) / bc1 <= lr 1.03 K sqrt(bc2) / bc1, and
+        // lr/bc1 1e-18 / eps when v underflowed (lazy_state_ok's absolute term)
+        const double b1 = a.beta1, b2 = a.beta2, eps = a.eps;
+        const double gam = b1 * b1 / b2;
+        const double K = (b1 >= 0.0 && b1 < 1.0 && b2 > 0.0 && b2 < 1.0 && gam < 1.0)
+                             ? (1.0 - b1) / sqrt((1.0 - b2) * (1.0 - gam)) : (double)INFINITY;
+        const double bc1 = 1.0 / (double)c.ibc1, bc2 = 1.0 / ((double)c.isbc2 * (double)c.isbc2);
+        const double B = 1.03 * K * sqrt(bc2) / bc1 + (eps > 0.0 ? 1e-18 / (bc1 * eps) : (double)INFINITY);
+        c.kratio = (float)(1.02 * K);
+        // lane j (1 .. kLazyWindow - 2) holds step - j's entry, the warp sums
+        const long long sj = c.step - lane;
+        const bool use = lane >= 1 && lane <= kLazyWindow - 2 && sj >= 1;
+        const AdamConsts* e = use ? &ring[sj % kLazyRing] : nullptr;
+        const bool ok = !use || e->step == sj;
+        for (int k = 0; k < 4; ++k) {
+            c.drift[k] = (float)((double)c.lr[k] * B * 1.0001);
+            double d = lane == 0 ? (double)c.drift[k] : use ? (ok ? (double)e->drift[k] : (double)INFINITY) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            c.cum[k] = (float)(d * 1.0001);
+        }
+    }
+    if (lane != 0) return;
+    *a.consts = c;
+    if (ring) ring[c.step % kLazyRing] = c;
 }
 
 // (6 CTAs/SM: 40 registers; 7-8 CTAs/SM spill and measured slower)
@@ -99,6 +128,115 @@ __global__ void __launch_bounds__(256) k_adam_final(const AdamLaunch a) {
     }
 }
 
+// ---- lazy training steps (LazyAdam, common.cuh) ----------------------------------
+__device__ __forceinline__ void lazy_load(const AdamLaunch& a, uint32_t i, float p[11], float m[11], float v[11]) {
+#pragma unroll
+    for (int k = 0; k < 11; ++k) {
+        const uint64_t o = (uint64_t)k * a.cap + i;
+        p[k] = a.params[o];
+        m[k] = a.m[o];
+        v[k] = a.v[o];
+    }
+}
+__device__ __forceinline__ void lazy_store(const AdamLaunch& a, uint32_t i, const float p[11], const float m[11],
+                                           const float v[11]) {
+#pragma unroll
+    for (int k = 0; k < 11; ++k) {
+        const uint64_t o = (uint64_t)k * a.cap + i;
+        a.params[o] = p[k];
+        a.m[o] = m[k];
+        a.v[o] = v[k];
+    }
+}
+
+// The survivors of the step (CTA per K_decide group, as k_adam_final): pending
+// zero-gradient steps replayed, then this step with the slot gradient; the map
+// entries cleared; CTA 0 advances the step counter.
+__global__ void __launch_bounds__(256) k_lazy_survivors(const AdamLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    const unsigned g = blockIdx.x;
+    const unsigned S = a.grp_surv[g];
+    const bool skip = adam_overflow(a);
+    const AdamConsts& c = *a.consts;
+    const long long t = c.step;
+    if (!skip) adam_advance_step(a, c);
+    bool ok = true;
+    for (unsigned j = threadIdx.x; j < S; j += blockDim.x) {
+        const uint32_t slot = g * kDecideGroupSize + j, i = a.surv_gidx[slot];
+        if (!skip) {
+            float p[11], m[11], v[11], gr[11];
+            lazy_load(a, i, p, m, v);
+            lazy_replay(a.lazy, (long long)a.lazy.t_done[i] + 1, t - 1, p, m, v);
+#pragma unroll
+            for (int k = 0; k < 11; ++k) gr[k] = __ldcs(a.slot_grads + (uint64_t)k * a.cap + slot);
+            adam_gauss_step(c, a.bbox_min, a.bbox_max, p, m, v, gr);
+            lazy_store(a, i, p, m, v);
+            a.lazy.t_done[i] = (uint32_t)t;
+            ok &= lazy_state_ok(c.kratio, m, v);
+        }
+        a.gmap[i] = 0;
+    }
+    if (!ok) atomicOr(a.lazy.bad, 1u);
+}
+
+// The step's window: Gaussians [w W, (w + 1) W), w = step mod kLazyWindow,
+// brought up to date through this step (survivors were, by k_lazy_survivors).
+__global__ void __launch_bounds__(256) k_lazy_window(const AdamLaunch a) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    if (adam_overflow(a)) return;
+    const AdamConsts& c = *a.consts;
+    const long long t = c.step;
+    const uint32_t W = (uint32_t)(((uint64_t)a.n + kLazyWindow - 1) / kLazyWindow);
+    const uint32_t lo = (uint32_t)(t % kLazyWindow) * W;
+    const uint32_t hi = min(a.n, lo + W);
+    bool ok = true;
+    for (uint32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x) {
+        const long long td = a.lazy.t_done[i];
+        if (td >= t) continue;
+        float p[11], m[11], v[11];
+        lazy_load(a, i, p, m, v);
+        lazy_replay(a.lazy, td + 1, t, p, m, v);
+        lazy_store(a, i, p, m, v);
+        a.lazy.t_done[i] = (uint32_t)t;
+        ok &= lazy_state_ok(c.kratio, m, v);
+    }
+    if (!ok) atomicOr(a.lazy.bad, 1u);
+}
+
+// Every Gaussian up to date through AdamState::step (before anything reads or
+// writes the parameters or moments directly).
+__global__ void __launch_bounds__(256) k_lazy_flush(const AdamLaunch a) {
+    const long long t = *a.lazy.step;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
+        const long long td = a.lazy.t_done[i];
+        if (td >= t) continue;
+        float p[11], m[11], v[11];
+        lazy_load(a, i, p, m, v);
+        lazy_replay(a.lazy, td + 1, t, p, m, v);
+        lazy_store(a, i, p, m, v);
+        a.lazy.t_done[i] = (uint32_t)t;
+    }
+}
+
+// Lazy mode starts from current values: t_done = step for every Gaussian, and
+// every moment state checked against the drift bound (kratio from the host:
+// the training step's betas).
+__global__ void __launch_bounds__(256) k_lazy_begin(const AdamLaunch a, float kratio) {
+    const long long t = *a.lazy.step;
+    bool ok = true;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
+        a.lazy.t_done[i] = (uint32_t)t;
+        float m[11], v[11];
+#pragma unroll
+        for (int k = 0; k < 11; ++k) {
+            m[k] = a.m[(uint64_t)k * a.cap + i];
+            v[k] = a.v[(uint64_t)k * a.cap + i];
+        }
+        ok &= lazy_state_ok(kratio, m, v);
+    }
+    if (!ok) atomicOr(a.lazy.bad, 1u);
+}
+
 // Batched step, before its Adam: the B slices' slot gradients summed per
 // primitive in slice order into the dense planes — every entry written (zero
 // where no slice kept the primitive), every map read cleared. The dense Adam
@@ -160,6 +298,26 @@ void launch_adam_rest(const AdamLaunch& a, const unsigned* surv_bits, int ctas, 
 
 void launch_adam_final(const AdamLaunch& a, unsigned ngroups, cudaStream_t st) {
     if (ngroups) launch_pdl(k_adam_final, dim3(ngroups), dim3(256), 0, st, a);
+}
+
+void launch_lazy_survivors(const AdamLaunch& a, unsigned ngroups, cudaStream_t st) {
+    if (ngroups) launch_pdl(k_lazy_survivors, dim3(ngroups), dim3(256), 0, st, a);
+}
+
+void launch_lazy_window(const AdamLaunch& a, cudaStream_t st) {
+    const uint32_t W = (uint32_t)(((uint64_t)a.n + kLazyWindow - 1) / kLazyWindow);
+    if (W) launch_pdl(k_lazy_window, dim3((W + 255) / 256), dim3(256), 0, st, a);
+}
+
+void launch_lazy_flush(const AdamLaunch& a, cudaStream_t st) {
+    if (a.n) k_lazy_flush<<<(a.n + 255) / 256, 256, 0, st>>>(a);
+}
+
+void launch_lazy_begin(const AdamLaunch& a, cudaStream_t st) {
+    const double b1 = a.beta1, b2 = a.beta2, gam = b1 * b1 / b2;
+    const double K = (b1 >= 0.0 && b1 < 1.0 && b2 > 0.0 && b2 < 1.0 && gam < 1.0)
+                         ? (1.0 - b1) / std::sqrt((1.0 - b2) * (1.0 - gam)) : HUGE_VAL;
+    if (a.n) k_lazy_begin<<<(a.n + 255) / 256, 256, 0, st>>>(a, (float)(1.02 * K));
 }
 
 void launch_adam_consts(const AdamLaunch& a, cudaStream_t st) {

@@ -99,6 +99,76 @@ __device__ __forceinline__ float adam_delta(const AdamConsts& c, float lrc, floa
     return __fdividef(__fmul_rn(lrc, m), __fmaf_rn(sq, c.isbc2, c.eps));
 }
 
+// One parameter's update (optimize.hpp:184-188): the moments, then the step.
+// Every Adam path (eager, lazy, replay) goes through this: the same bits.
+__device__ __forceinline__ void adam_elem(const AdamConsts& c, float lrc, float& p, float& m, float& v, float g) {
+    m = __fmaf_rn(c.b1, m, __fmul_rn(c.ib1, g));
+    v = __fmaf_rn(c.b2, v, __fmul_rn(__fmul_rn(c.ib2, g), g));
+    p = __fsub_rn(p, adam_delta(c, lrc, m, v));
+}
+
+// The reference's quaternion renormalisation (optimize.hpp:216-217).
+__device__ __forceinline__ void adam_renorm(float& w, float& x, float& y, float& z) {
+    const float qn = __fsqrt_rn(__fmaf_rn(w, w, __fmaf_rn(x, x, __fmaf_rn(y, y, __fmul_rn(z, z)))));
+    if (qn > 0.f) {
+        const float inv = __frcp_rn(qn);
+        w = __fmul_rn(w, inv);
+        x = __fmul_rn(x, inv);
+        y = __fmul_rn(y, inv);
+        z = __fmul_rn(z, inv);
+    }
+}
+
+// One whole Adam step of one Gaussian held in registers (planes in the
+// reference's order, the bbox clamp after the position, the renormalisation
+// after the quaternion): the per-Gaussian form of adam_update_store_g.
+__device__ __forceinline__ void adam_gauss_step(const AdamConsts& c, const float bmin[3], const float bmax[3],
+                                                float p[11], float m[11], float v[11], const float g[11]) {
+    const float l0 = __fmul_rn(c.lr[0], c.ibc1), l1 = __fmul_rn(c.lr[1], c.ibc1);
+    const float l2 = __fmul_rn(c.lr[2], c.ibc1), l3 = __fmul_rn(c.lr[3], c.ibc1);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        adam_elem(c, l0, p[d], m[d], v[d], g[d]);
+        p[d] = fminf(bmax[d], fmaxf(bmin[d], p[d]));
+    }
+#pragma unroll
+    for (int d = 3; d < 6; ++d) adam_elem(c, l2, p[d], m[d], v[d], g[d]);
+    adam_elem(c, l1, p[10], m[10], v[10], g[10]);
+#pragma unroll
+    for (int d = 6; d < 10; ++d) adam_elem(c, l3, p[d], m[d], v[d], g[d]);
+    adam_renorm(p[6], p[7], p[8], p[9]);
+}
+
+// A zero the compiler cannot see through (the eager path's zero gradients are
+// loaded values: no constant folding may change a rounding or a sign here).
+__device__ __forceinline__ float opaque_zero() {
+    float z;
+    asm volatile("mov.b32 %0, 0;" : "=f"(z));
+    return z;
+}
+
+// Replays the zero-gradient steps from .. to (inclusive) of one Gaussian
+// (LazyAdam): constants from the ring, the eager operations in the eager order.
+__device__ __forceinline__ void lazy_replay(const LazyAdam& L, long long from, long long to, float p[11], float m[11],
+                                            float v[11]) {
+    if (from > to) return;
+    float g[11];
+    const float z = opaque_zero();
+#pragma unroll
+    for (int k = 0; k < 11; ++k) g[k] = z;
+    for (long long s = from; s <= to; ++s) adam_gauss_step(L.ring[s % kLazyRing], L.bbox_min, L.bbox_max, p, m, v, g);
+}
+
+// The moment-state bound the lazy drift assumes (|m| <= kratio sqrt(v) per
+// parameter, + 1e-18 for flushed denormals): false (NaN included) flags the
+// state as outside it.
+__device__ __forceinline__ bool lazy_state_ok(float kratio, const float m[11], const float v[11]) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 11; ++k) ok &= fabsf(m[k]) <= __fmaf_rn(kratio, sqrtf(fmaxf(v[k], 0.f)), 1e-18f);
+    return ok;
+}
+
 // Where a thread's N gradients come from: the dense planes at i0 (gslot ==
 // nullptr), or per primitive a survivor slot (kNoSlot: zero gradient).
 constexpr uint32_t kNoSlot = 0xffffffffu;
@@ -219,9 +289,7 @@ __device__ __forceinline__ Pack<N> adam_plane_g(const AdamLaunch& a, const AdamC
 #pragma unroll
     for (int l = 0; l < N; ++l) {
         nz |= (g.v[l] != 0.f ? 1u : 0u) << l;
-        m.v[l] = __fmaf_rn(c.b1, m.v[l], __fmul_rn(c.ib1, g.v[l]));
-        v.v[l] = __fmaf_rn(c.b2, v.v[l], __fmul_rn(__fmul_rn(c.ib2, g.v[l]), g.v[l]));
-        p.v[l] = __fsub_rn(p.v[l], adam_delta(c, lrc, m.v[l], v.v[l]));
+        adam_elem(c, lrc, p.v[l], m.v[l], v.v[l], g.v[l]);
     }
     stp_stream<N>(a.m + o, m);
     stp_stream<N>(a.v + o, v);
@@ -255,20 +323,7 @@ __device__ __forceinline__ void adam_update(const AdamLaunch& a, const AdamConst
 #pragma unroll
     for (int d = 6; d < 10; ++d) p[d] = adam_plane<N>(a, c, d, c.lr[3], i0, gslot, nz);
 #pragma unroll
-    for (int l = 0; l < N; ++l) {
-        float& w = p[6].v[l];
-        float& x = p[7].v[l];
-        float& y = p[8].v[l];
-        float& z = p[9].v[l];
-        const float qn = __fsqrt_rn(__fmaf_rn(w, w, __fmaf_rn(x, x, __fmaf_rn(y, y, __fmul_rn(z, z)))));
-        if (qn > 0.f) {
-            const float inv = __frcp_rn(qn);
-            w = __fmul_rn(w, inv);
-            x = __fmul_rn(x, inv);
-            y = __fmul_rn(y, inv);
-            z = __fmul_rn(z, inv);
-        }
-    }
+    for (int l = 0; l < N; ++l) adam_renorm(p[6].v[l], p[7].v[l], p[8].v[l], p[9].v[l]);
 }
 
 // As adam_update + adam_store, storing each plane's parameters as soon as they
@@ -294,20 +349,7 @@ __device__ __forceinline__ void adam_update_store_g(const AdamLaunch& a, const A
 #pragma unroll
     for (int d = 0; d < 4; ++d) q[d] = adam_plane_g<N>(a, c, 6 + d, c.lr[3], i0, grad, nz);
 #pragma unroll
-    for (int l = 0; l < N; ++l) {
-        float& w = q[0].v[l];
-        float& x = q[1].v[l];
-        float& y = q[2].v[l];
-        float& z = q[3].v[l];
-        const float qn = __fsqrt_rn(__fmaf_rn(w, w, __fmaf_rn(x, x, __fmaf_rn(y, y, __fmul_rn(z, z)))));
-        if (qn > 0.f) {
-            const float inv = __frcp_rn(qn);
-            w = __fmul_rn(w, inv);
-            x = __fmul_rn(x, inv);
-            y = __fmul_rn(y, inv);
-            z = __fmul_rn(z, inv);
-        }
-    }
+    for (int l = 0; l < N; ++l) adam_renorm(q[0].v[l], q[1].v[l], q[2].v[l], q[3].v[l]);
 #pragma unroll
     for (int d = 0; d < 4; ++d) stp_stream<N>(a.params + (uint64_t)(6 + d) * a.cap + i0, q[d]);
 }

@@ -455,6 +455,44 @@ __device__ __forceinline__ unsigned gather_tile_list(const unsigned* __restrict_
     return out;
 }
 
+struct AdamConsts {
+    float b1, b2, ib1, ib2;   // beta1, beta2, 1 - beta1, 1 - beta2
+    float ibc1, isbc2, eps;   // 1 / bc1, 1 / sqrt(bc2), eps
+    float lr[4];              // position, opacity, scale, rotation
+    // Deferred zero-gradient steps (LazyAdam): an upper bound of |delta p| of
+    // this step for any moment state with |m| <= kratio sqrt(v) (per lr group),
+    // and the sum of it over this step and the kLazyWindow - 2 before it.
+    float drift[4], cum[4];
+    float kratio;             // the moment-state bound the drift assumes (1.02 K)
+    long long step;           // the step these constants are for (AdamState::step after it)
+};
+
+// ---- deferred zero-gradient Adam steps ("lazy" training steps) ---------------
+// A Gaussian outside a slice's survivors has an exactly zero gradient, and its
+// Adam update (optimize.hpp:195-221) is then a fixed function of its own
+// parameters and moments and of the step's constants. A lazy training step
+// updates only the survivors and one window of N / kLazyWindow Gaussians (by
+// step number); every other Gaussian keeps the step pending. t_done[i] is the
+// AdamState::step its stored parameters and moments are current at; pending
+// steps t_done+1 .. t are replayed in order with the same fp32 operations as
+// the eager update (the constants of the last kLazyRing steps are kept), so
+// the values are the eager ones bit for bit — K_filter replays them for every
+// Gaussian it cannot cull from the stored (stale) parameters widened by the
+// largest possible drift of kLazyWindow - 1 steps (Adam's update is bounded:
+// |m| <= K sqrt(v), K = (1 - b1) / sqrt((1 - b2)(1 - b1^2 / b2)), checked on
+// every stored state; a violation sets `bad` and K_filter then replays all).
+constexpr int kLazyRing = 32;    // AdamConsts of step s at ring[s % kLazyRing]
+constexpr int kLazyWindow = 16;  // a Gaussian is brought up to date at least every 16 steps
+struct LazyAdam {
+    uint32_t* t_done;
+    AdamConsts* ring;
+    long long* step;          // AdamState::step (device)
+    float* m;
+    float* v;
+    unsigned* bad;
+    float bbox_min[3], bbox_max[3];
+};
+
 // Kernel-launch wrappers (defined in the .cu files, called by session.cu).
 struct PrepLaunch {
     const float* params;      // 11 planes x cap
@@ -492,6 +530,10 @@ struct PrepLaunch {
     Control* ctrl;
     ErrorState* err;
     SliceArgs slice;
+    // lazy training steps: K_filter replays the pending steps of every Gaussian
+    // it does not cull (lazy_on = 0: the parameters are current)
+    int lazy_on;
+    LazyAdam lazy;
 };
 
 constexpr int kFilterItems = 4;                            // consecutive Gaussians per K_filter lane
@@ -610,13 +652,6 @@ struct ChainLaunch {
 };
 
 // Per-step Adam constants (adam.cuh adam_consts), written by k_adam_consts.
-struct AdamConsts {
-    float b1, b2, ib1, ib2;   // beta1, beta2, 1 - beta1, 1 - beta2
-    float ibc1, isbc2, eps;   // 1 / bc1, 1 / sqrt(bc2), eps
-    float lr[4];              // position, opacity, scale, rotation
-    long long step;           // the step these constants are for (AdamState::step after it)
-};
-
 struct AdamLaunch {
     float* params;
     float* grads;         // read (and cleared where non-zero by the fused Adam + cull)
@@ -658,6 +693,9 @@ struct AdamLaunch {
     const float* src_slot[kMaxBatch - 1];
     uint16_t* src_gmap[kMaxBatch - 1];
     const Control* src_ctrl[kMaxBatch - 1];
+    // the constants ring of the lazy steps (k_adam_consts writes every step's
+    // entry) and, for the lazy update kernels, the rest of their state
+    LazyAdam lazy;
 };
 
 struct LossLaunch {
@@ -807,6 +845,13 @@ void launch_adam_consts(const AdamLaunch& a, cudaStream_t st);
 void launch_sum_slots(const AdamLaunch& a, cudaStream_t st);
 void launch_adam_rest(const AdamLaunch& a, const unsigned* surv_bits, int ctas, cudaStream_t st);
 void launch_adam_final(const AdamLaunch& a, unsigned ngroups, cudaStream_t st);
+// lazy training steps (adam.cu): the survivors' update (pending steps replayed
+// first), the step's window of Gaussians, every Gaussian (flush), and the
+// start of lazy mode (t_done = step, moment states checked)
+void launch_lazy_survivors(const AdamLaunch& a, unsigned ngroups, cudaStream_t st);
+void launch_lazy_window(const AdamLaunch& a, cudaStream_t st);
+void launch_lazy_flush(const AdamLaunch& a, cudaStream_t st);
+void launch_lazy_begin(const AdamLaunch& a, cudaStream_t st);
 enum ScatterMode : int { kScatterSet = 1, kScatterAdd = 2, kScatterClearMap = 4 };
 void launch_scatter_slot_grads(const AdamLaunch& a, unsigned ngroups, int mode, cudaStream_t st);
 void launch_loss(const LossLaunch& a, cudaStream_t st);

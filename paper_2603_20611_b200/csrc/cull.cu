@@ -139,6 +139,86 @@ __device__ __forceinline__ bool quick_culled_identity(const float p[11], const F
     return fin & scales_ok & quat_ok & culled;
 }
 
+// ---- lazy training steps: the cull from stale parameters --------------------------
+// K_filter of a lazy step (LazyAdam, common.cuh) sees each Gaussian's stored
+// parameters, current at t_done <= t, and |true - stored| <= the drift bound of
+// the kLazyWindow - 1 last steps per parameter group (position, log-scale, raw
+// alpha, quaternion). quick_culled_drift is quick_culled_identity with every
+// input at its worst case inside that box, so it culls only what the quick
+// test would cull at the true parameters (and so the reference too); the rest
+// is brought up to date (replayed, lazy_materialize) and decided exactly as
+// the eager K_filter decides it.
+struct LazyView {
+    LazyAdam L;
+    uint64_t cap;
+    long long t;             // AdamState::step: the steps the true parameters have seen
+    float dmu, dls, dal;     // drift bounds: position, log-scale, raw alpha
+    bool all;                // no usable bound (bad state / missing constants): replay everything
+};
+
+__device__ __forceinline__ bool quick_culled_drift(const float p[11], const FilterConsts& c, const LazyView& z) {
+    const bool fin = isfinite(((p[2] + p[3]) + (p[4] + p[5])) + p[10]) & isfinite(p[0] + p[1]);
+    const float lmax = fmaxf(p[3], fmaxf(p[4], p[5])) + z.dls, lmin = fminf(p[3], fminf(p[4], p[5])) - z.dls;
+    const bool scales_ok = (lmax < 40.f) & (lmin > -40.f) & (lmax - lmin < 6.2f);
+    // renormalised every step: a stored norm near 1 stays away from the guards
+    const float qn2 = __fmaf_rn(p[6], p[6], __fmaf_rn(p[7], p[7], __fmaf_rn(p[8], p[8], p[9] * p[9])));
+    const bool quat_ok = (qn2 > 0.25f) & (qn2 < 4.f);
+    const float az = fabsf((p[2] + c.tz_hi) + c.tz_lo);
+    const float dz = __fmaf_rn(2.4e-7f, fabsf(p[2]) + fabsf(c.tz_hi), z.dmu);
+    const float mcz_lo = fmaxf(az - dz, 0.f), mcz_hi = az + dz;
+    const float mcx = fabsf(p[0] + c.tx) + z.dmu, mcy = fabsf(p[1] + c.ty) + z.dmu;
+    const float mu2 = __fmaf_rn(mcx, mcx, __fmaf_rn(mcy, mcy, mcz_hi * mcz_hi)) * 1.0001f;
+    const float den_hi = __fmaf_rn(ex2_ftz(fminf(lmax, 40.f) * 2.8853900817779268f) * c.mod2, 1.0003f, c.sz2);
+    const float inv_smin2 = ex2_ftz(fmaxf(lmin, -40.f) * -2.8853900817779268f) * c.inv_mod2 * 1.0003f;
+    const float thresh_hi = fminf(p[10] + z.dal, 0.f) - c.log_tau;
+    const float noise = __fmaf_rn(2e-14f * mu2, inv_smin2,
+                                  4.8e-7f * mcz_hi * (fabsf(p[2]) + dz + fabsf(c.tz_hi)) * c.inv_sz2 * 1.0003f);
+    const float x = thresh_hi + (2e-3f + __fmaf_rn(2e-5f, fabsf(thresh_hi) + 0.7f, noise));
+    const float x_up = __fmaf_rn(1e-3f, fabsf(x) + noise, x) + 2e-6f;
+    const float rhs = x_up >= 0.f ? x_up * den_hi * 1.0001f : x_up * c.sz2 * 0.9999f;
+    const bool culled = 0.5f * mcz_lo * mcz_lo > rhs;
+    return fin & scales_ok & quat_ok & culled;
+}
+
+// Gaussian i's true parameters (p: its stored ones in, the replayed ones out).
+__device__ __noinline__ void lazy_materialize(const LazyView z, uint32_t i, float p[11]) {
+    const LazyAdam& L = z.L;
+    const long long td = L.t_done[i];
+    if (td >= z.t) return;
+    float m[11], v[11];
+#pragma unroll
+    for (int k = 0; k < 11; ++k) {
+        m[k] = L.m[(uint64_t)k * z.cap + i];
+        v[k] = L.v[(uint64_t)k * z.cap + i];
+    }
+    lazy_replay(L, td + 1, z.t, p, m, v);
+}
+
+// The drift bounds of the pending steps (one thread; k_adam_consts summed them
+// per step into the ring entry of the last step done).
+__device__ __forceinline__ LazyView lazy_view(const PrepLaunch& a) {
+    LazyView z;
+    z.L = a.lazy;
+    z.cap = a.cap;
+    z.t = *a.lazy.step;
+    z.dmu = z.dls = z.dal = 0.f;
+    z.all = *a.lazy.bad != 0;
+    if (z.t > 0) {
+        const AdamConsts& e = a.lazy.ring[z.t % kLazyRing];
+        if (e.step != z.t) {
+            z.all = true;
+        } else {
+            z.dmu = e.cum[0];
+            z.dal = e.cum[1];
+            z.dls = e.cum[2];
+            // the quaternion guard of quick_culled_drift needs the renormalised
+            // quaternion to stay renormalisable (|delta q| per step well below 1)
+            z.all |= !(e.cum[0] < 1e30f && e.cum[1] < 1e30f && e.cum[2] < 1e30f && e.cum[3] < 0.25f);
+        }
+    }
+    return z;
+}
+
 // quick_culled_identity split for several poses that differ only in t_z
 // (slice_pose_for_index stacks: same R = I, t_x, t_y, PSF, tau, mod): the
 // pose-invariant terms once per Gaussian, then a few FMAs per pose. Same
@@ -248,14 +328,31 @@ struct CullScratch {
 __device__ __forceinline__ unsigned cull_chunk(const PrepLaunch& a, const FilterConsts& fc, float log_tau,
                                                int filter_on, unsigned b, uint32_t i0, const float4 v[11],
                                                CullIdx& sx, float (*sp)[kFilterBlock], const float* staged,
-                                               int qmask_given = -1, bool write = true) {
+                                               int qmask_given = -1, bool write = true,
+                                               const LazyView* lz = nullptr) {
     const int lane = threadIdx.x & 31;
     const bool ident = a.slice.identity_rot != 0;
     // items inside the set: all candidates with the cull off, else undecided
     // unless the quick test culls them (identity poses only)
     const unsigned inset = i0 >= a.n ? 0u : (a.n - i0 >= kFilterItems ? (1u << kFilterItems) - 1 : (1u << (a.n - i0)) - 1);
     unsigned cmask = filter_on ? 0u : inset, umask = filter_on ? inset : 0u;
-    if (filter_on && ident && qmask_given >= 0) {
+    if (lz) {
+        // lazy step: everything the drift-widened quick test cannot cull is
+        // brought up to date below and takes the exact test (staged != nullptr)
+        cmask = 0u;
+        umask = inset;
+        if (filter_on && ident && !lz->all) {
+            unsigned lmask = 0;
+#pragma unroll
+            for (int k = 0; k < kFilterItems; ++k) {
+                float p[11];
+#pragma unroll
+                for (int q = 0; q < 11; ++q) p[q] = (&v[q].x)[k];
+                lmask |= (quick_culled_drift(p, fc, *lz) ? 1u : 0u) << k;
+            }
+            umask &= ~lmask;
+        }
+    } else if (filter_on && ident && qmask_given >= 0) {
         umask &= ~(unsigned)qmask_given;
     } else if (filter_on && ident) {
         unsigned qmask = 0;
@@ -299,12 +396,18 @@ __device__ __forceinline__ unsigned cull_chunk(const PrepLaunch& a, const Filter
                     const unsigned j = sx.idx[e];
 #pragma unroll
                     for (int q = 0; q < 11; ++q) p[q] = staged[q * kFilterBlock + j];
+                    if (lz) {  // the true parameters, back into the stage for the emission
+                        lazy_materialize(*lz, b * kFilterBlock + j, p);
+                        float* stw = const_cast<float*>(staged);
+#pragma unroll
+                        for (int q = 0; q < 11; ++q) stw[q * kFilterBlock + j] = p[q];
+                    }
                 } else {
 #pragma unroll
                     for (int q = 0; q < 11; ++q) p[q] = sp[q][e];
                 }
-                cand = ident ? !certainly_culled_identity(p, fc)
-                             : !certainly_culled(p, a.slice, log_tau, fc.mod, fc.sz2);
+                cand = !filter_on || (ident ? !certainly_culled_identity(p, fc)
+                                            : !certainly_culled(p, a.slice, log_tau, fc.mod, fc.sz2));
             }
             const unsigned bal = __ballot_sync(0xffffffffu, cand);
             if (lane == 0) sx.res[r] = bal;
@@ -335,7 +438,8 @@ __device__ __forceinline__ unsigned cull_chunk(const PrepLaunch& a, const Filter
             if (cmask & (1u << k)) {
                 float p[11];
 #pragma unroll
-                for (int q = 0; q < 11; ++q) p[q] = (&v[q].x)[k];
+                for (int q = 0; q < 11; ++q)
+                    p[q] = lz ? staged[q * kFilterBlock + (threadIdx.x & 31) * kFilterItems + k] : (&v[q].x)[k];
                 store_cand(out++, p, i0 + k);
             }
     }
@@ -372,7 +476,7 @@ constexpr size_t kFilterSmem =
 // chunk b+1's 5.6 KB is in flight while chunk b is culled, so HBM never waits
 // for the cull arithmetic (a register-fed loop leaves the memory idle between
 // its load bursts: ~2 chunks per warp at C2).
-template <bool kZeroGrads>
+template <bool kZeroGrads, bool kLazy>
 __global__ void __launch_bounds__(kFilterThreads, 2) k_filter(const PrepLaunch a, float log_tau, int filter_on) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     extern __shared__ __align__(16) float s_filter[];
@@ -408,6 +512,12 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter(const PrepLaunch a
             for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = 0.f;
         }
     const FilterConsts fc = filter_consts(a.slice, log_tau);
+    __shared__ LazyView s_lz;
+    if (kLazy) {
+        if (tid == 0) s_lz = lazy_view(a);
+        __syncthreads();
+    }
+    const LazyView lz = kLazy ? s_lz : LazyView{};
 
     for (int it = 0; b < nchunks; ++it, b += gwarps) {
         if (b + gwarps < nchunks) prefetch(b + gwarps, (it + 1) & 1);
@@ -423,7 +533,7 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter(const PrepLaunch a
 #pragma unroll
             for (int q = 0; q < 11; ++q)
                 *reinterpret_cast<float4*>(a.grads + (uint64_t)q * a.cap + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
-        cull_chunk(a, fc, log_tau, filter_on, b, i0, v, sx, nullptr, st);
+        cull_chunk(a, fc, log_tau, filter_on, b, i0, v, sx, nullptr, st, -1, true, kLazy ? &lz : nullptr);
         __syncwarp();  // stage (it & 1) is refilled by the next iteration's prefetch
     }
 }
@@ -599,17 +709,23 @@ void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st) {
     const float log_tau = filter_on ? (float)log(a.slice.tau) : 0.f;
     static int per_sm = 0;
     if (!per_sm) {
-        cudaFuncSetAttribute(k_filter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFilterSmem);
-        cudaFuncSetAttribute(k_filter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFilterSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<true>, kFilterThreads, kFilterSmem);
+        cudaFuncSetAttribute(k_filter<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFilterSmem);
+        cudaFuncSetAttribute(k_filter<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFilterSmem);
+        cudaFuncSetAttribute(k_filter<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFilterSmem);
+        cudaFuncSetAttribute(k_filter<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFilterSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_filter<true, false>, kFilterThreads, kFilterSmem);
         if (per_sm < 1) per_sm = 1;
     }
     const uint64_t need = ((uint64_t)a.nfilter * 32 + kFilterThreads - 1) / kFilterThreads;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms * per_sm));
-    if (a.grads)
-        launch_pdl(k_filter<true>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, filter_on ? 1 : 0);
-    else
-        launch_pdl(k_filter<false>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, filter_on ? 1 : 0);
+    const int fo = filter_on ? 1 : 0;
+    if (a.lazy_on) {
+        if (a.grads) launch_pdl(k_filter<true, true>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, fo);
+        else launch_pdl(k_filter<false, true>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, fo);
+    } else {
+        if (a.grads) launch_pdl(k_filter<true, false>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, fo);
+        else launch_pdl(k_filter<false, false>, dim3(grid), dim3(kFilterThreads), kFilterSmem, st, a, log_tau, fo);
+    }
 }
 
 void launch_prep_multi(const PrepLaunch* pl, int nb, int num_sms, cudaStream_t st, int own, unsigned* union_words) {

@@ -176,6 +176,16 @@ struct gpk_session {
     // GPK_ADAM_REST_CTAS sizes it.
     bool adam_split = false;
     int adam_rest_ctas = -1;
+    // lazy training steps (LazyAdam, common.cuh): the survivors and one window
+    // of Gaussians updated per step, every other Gaussian's zero-gradient step
+    // deferred and replayed in order where it is next needed
+    bool lazy_on = false;        // mode (GPK_LAZY_ADAM=1 / gpk_set_lazy_adam; measured slower)
+    bool lazy_live = false;      // t_done is valid (every deferred step is replayable)
+    bool lazy_pending = false;   // a lazy step ran since the last flush
+    bool cap_lazy = false;       // capture: the graph being captured runs lazily
+    bool cap_lazy_used = false;  // ... and recorded lazy kernels
+    bool cap_lazy_writes = false;
+    DevBuf t_done;               // u32 per Gaussian
     cudaStream_t adam_stream = nullptr;
     cudaEvent_t ev_rest_fork = nullptr, ev_rest_join = nullptr;
     DevBuf surv_bits;                 // K_decide: bit i = Gaussian i survived the last prepare
@@ -183,6 +193,8 @@ struct gpk_session {
         bool needs_prefilter = false, sets_prefilter = false, writes_params = false;
         gpk_slice_pose next_pose{};
     } capture_meta;
+    AdamConsts* lazy_ring() { return reinterpret_cast<AdamConsts*>(persist.as<char>() + 256); }
+    unsigned* lazy_bad() { return reinterpret_cast<unsigned*>(persist.as<char>() + 256 + kLazyRing * sizeof(AdamConsts)); }
     DevBuf persist;    // ErrorState | epoch | adam step | adam done ctr | loss done ctr | loss
     DevBuf image, dl_di, target, loss_g, loss_partial;
     DevBuf stat_norm, stat_obs, stat_world;
@@ -231,6 +243,8 @@ struct gpk_session {
         bool needs_prefilter = false;  // pipelined train step: starts at K_decide
         bool sets_prefilter = false;   // ... and leaves next_pose culled
         bool writes_params = false;
+        bool lazy = false;             // runs lazily (needs t_done valid at launch)
+        bool lazy_writes = false;      // ... and leaves deferred steps
         bool grads_in_slots = false;   // where the graph leaves the gradient
         bool grads_in_union = false;
         bool gmap_dirty = false;
@@ -271,7 +285,7 @@ struct gpk_session {
 
 namespace {
 
-constexpr size_t kPersistBytes = 192;
+constexpr size_t kPersistBytes = 256 + kLazyRing * sizeof(AdamConsts) + 16;  // .., lazy ring, bad flag
 
 cudaEvent_t take_event(gpk_session* s) {
     if (!s->event_pool.empty()) {
@@ -500,6 +514,18 @@ int launch_sorts(gpk_session* s, int passes, int digit_bits, const uint2* grp_pa
                  unsigned ngroups = 0, int tile_shift = 0);
 uint64_t decide_group_count(uint64_t n);
 GatherLaunch gather_args(gpk_session* s);
+LazyAdam lazy_args(gpk_session* s);
+int lazy_flush_dev(gpk_session* s);
+int lazy_sync(gpk_session* s);
+int lazy_kill(gpk_session* s);
+int lazy_ensure_live(gpk_session* s);
+bool lazy_now(gpk_session* s);
+
+// K_filter can cull lazily (from stale parameters) only with its quick test:
+// an R = I pose and the cull on (launch_prep's filter_on)
+bool lazy_filter_ok(const SliceArgs& a) {
+    return a.identity_rot && a.tau > 0.0 && a.mod > 1e-10 && a.mod < 1e10 && a.sigma_z > 1e-10 && a.sigma_z < 1e10;
+}
 
 PrepLaunch prep_launch(gpk_session* s, const SliceArgs& a, int passes, int digit_bits, bool zero_grads) {
     PrepLaunch pl;
@@ -538,6 +564,8 @@ PrepLaunch prep_launch(gpk_session* s, const SliceArgs& a, int passes, int digit
     pl.ctrl = s->ctrl();
     pl.err = s->err();
     pl.slice = a;
+    pl.lazy_on = 0;
+    pl.lazy = lazy_args(s);
     return pl;
 }
 
@@ -579,6 +607,7 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     TRY(make_slice(s, pose, psf, cfg, a));
     TRY(ensure_image(s, a.W, a.H));
     if (!s->keys[0].p) TRY(ensure_pairs(s, std::max<uint64_t>(1ull << 20, 8 * s->n)));
+    if (s->owner) TRY(lazy_kill(s->owner));  // a context's cull reads its session's parameters
     PrepState& ps = s->prep;
     ps.slice = a;
     ps.tiles = a.tiles_x * a.tiles_y;
@@ -613,6 +642,15 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
         // K_filter zeroes the control head itself (K_decide is the first to use it)
         pl.head = s->head.as<unsigned>();
         pl.head_words = (unsigned)(head_bytes / 4);
+        // lazy: K_filter culls from the stored parameters and replays what it
+        // keeps; a pose its drift test cannot take gets every deferred step first
+        pl.lazy_on = lazy_now(s) ? 1 : 0;
+        if (pl.lazy_on && !lazy_filter_ok(a)) {
+            TRY(lazy_flush_dev(s));
+            if (!s->capturing) s->lazy_pending = false;
+            pl.lazy_on = 0;
+        }
+        if (pl.lazy_on && s->capturing) s->cap_lazy_used = true;
         launch_prep(pl, s->num_sms, s->stream);
         CK(cudaGetLastError());
         pl.head = nullptr;
@@ -950,9 +988,12 @@ int alloc_for_n(gpk_session* s, uint64_t n) {
         CK(s->grads.ensure(cap * 11 * 4));
         CK(s->adam_m.ensure(cap * 11 * 4));
         CK(s->adam_v.ensure(cap * 11 * 4));
+        CK(s->t_done.ensure(cap * 4));
         TRY(alloc_slice_bufs(s, cap));
     }
     if (n != s->n) ++s->alloc_epoch;  // captured graphs bake the set size
+    s->lazy_live = false;  // (callers flushed what was deferred)
+    s->lazy_pending = false;
     s->n = n;
     if (s->accum_on) TRY(accum_alloc_zero(s));
     return GPK_OK;
@@ -1008,6 +1049,21 @@ int materialize_dense_grads(gpk_session* s) {
     return mark_grads_dense(s);
 }
 
+LazyAdam lazy_args(gpk_session* s) {
+    LazyAdam L{};
+    L.t_done = s->t_done.as<uint32_t>();
+    L.ring = s->lazy_on ? s->lazy_ring() : nullptr;  // (k_adam_consts fills it in lazy mode only)
+    L.step = s->adam_step();
+    L.m = s->adam_m.as<float>();
+    L.v = s->adam_v.as<float>();
+    L.bad = s->lazy_bad();
+    for (int d = 0; d < 3; ++d) {
+        L.bbox_min[d] = (float)s->bbox.min[d];
+        L.bbox_max[d] = (float)s->bbox.max[d];
+    }
+    return L;
+}
+
 AdamLaunch adam_launch(gpk_session* s, const double lr[4], bool scheduled, int total, const gpk_adam_hparams* hp) {
     AdamLaunch a{};
     a.params = s->params.as<float>();
@@ -1029,8 +1085,57 @@ AdamLaunch adam_launch(gpk_session* s, const double lr[4], bool scheduled, int t
     a.step = s->adam_step();
     a.consts = s->adam_consts();
     a.ctrl = s->prep.valid ? s->ctrl() : nullptr;
+    a.lazy = lazy_args(s);
     return a;
 }
+
+// ---- lazy training steps (LazyAdam, common.cuh) ---------------------------------
+// Host rules: lazy_sync before anything reads the parameters or moments
+// directly (every deferred step replayed), lazy_kill before anything writes
+// them or runs an eager Adam step (t_done is then no longer maintained), and
+// lazy_ensure_live before a lazy step. Under capture nothing changes on the
+// host: the graph records whether it runs lazily and gpk_graph_launch applies
+// the rules at launch.
+int lazy_flush_dev(gpk_session* s) {
+    if (!s->n) return GPK_OK;
+    const double lr[4] = {0, 0, 0, 0};
+    launch_lazy_flush(adam_launch(s, lr, false, 1, nullptr), s->stream);
+    CK(cudaGetLastError());
+    if (s->capturing) s->cap_lazy_used = true;
+    return GPK_OK;
+}
+
+int lazy_sync(gpk_session* s) {
+    if (s->owner) return lazy_sync(s->owner);
+    if (s->capturing || !s->lazy_live || !s->lazy_pending) return GPK_OK;
+    TRY(lazy_flush_dev(s));
+    s->lazy_pending = false;
+    return GPK_OK;
+}
+
+int lazy_kill(gpk_session* s) {
+    if (s->owner) return lazy_kill(s->owner);
+    if (s->capturing) return GPK_OK;
+    TRY(lazy_sync(s));
+    s->lazy_live = false;
+    return GPK_OK;
+}
+
+int lazy_ensure_live(gpk_session* s) {
+    if (s->capturing || s->lazy_live) return GPK_OK;
+    if (s->n) {
+        CK(cudaMemsetAsync(s->lazy_bad(), 0, 4, s->stream));
+        const double lr[4] = {0, 0, 0, 0};
+        launch_lazy_begin(adam_launch(s, lr, false, 1, nullptr), s->stream);
+        CK(cudaGetLastError());
+    }
+    s->lazy_live = true;
+    s->lazy_pending = false;
+    return GPK_OK;
+}
+
+// K_filter of this prepare runs lazily
+bool lazy_now(gpk_session* s) { return !s->owner && (s->capturing ? s->cap_lazy : s->lazy_live); }
 
 // The training step evaluates the Adam constants (fp64 pow latency) on the
 // side stream while the slice renders; the update waits on ev_cjoin.
@@ -1059,6 +1164,7 @@ int adam_consts_ready(gpk_session* s, const AdamLaunch& a) {
 int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
              const gpk_adam_hparams* hp, uint64_t lo = 0, uint64_t hi = ~0ull) {
     if (s->owner) return fail(GPK_ERR_STATE, "slice context: Adam runs on its session");
+    TRY(lazy_kill(s));  // the eager update over all N
     if (s->n == 0) {
         s->consts_pending = false;
         long long st = 0;
@@ -1085,6 +1191,7 @@ int run_adam(gpk_session* s, const double lr[4], bool scheduled, int total,
 // leaves `next` culled for the following prepare and every gradient zero.
 int run_adam_cull(gpk_session* s, const double lr[4], int total, const gpk_slice_pose* next,
                   const gpk_psf* psf, const gpk_raster_config* cfg) {
+    TRY(lazy_kill(s));
     SliceArgs na;
     TRY(make_slice(s, next, psf, cfg, na));
     if (s->n == 0) return run_adam(s, lr, true, total, nullptr);
@@ -1205,6 +1312,7 @@ int make_vox(gpk_session* s, const gpk_voxelizer_config* cfg, VoxArgs& v) {
 int run_vox_prep(gpk_session* s, const gpk_voxelizer_config* cfg) {
     VoxArgs v;
     TRY(make_vox(s, cfg, v));
+    TRY(lazy_sync(s));  // the voxelizer reads the parameters directly
     if (!s->keys[0].p) TRY(ensure_pairs(s, std::max<uint64_t>(1ull << 20, 8 * s->n)));
     s->prep.valid = false;  // the pair buffers now hold voxel tiles
     s->prep.rasterized = false;
@@ -1320,6 +1428,7 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     if (const char* f = getenv("GPK_FUSE_GATHER")) s->fuse_gather_ok = f[0] != '0';
     if (const char* f = getenv("GPK_ADAM_SPLIT")) s->adam_split = f[0] == '1';
     if (const char* f = getenv("GPK_ADAM_REST_CTAS")) s->adam_rest_ctas = atoi(f);
+    if (const char* f = getenv("GPK_LAZY_ADAM")) s->lazy_on = f[0] == '1';
     if (s->num_sms < 1) s->num_sms = 148;
     e = s->persist.ensure(kPersistBytes);
     if (e == cudaSuccess) e = cudaMemsetAsync(s->persist.p, 0, kPersistBytes, s->stream);
@@ -1467,7 +1576,12 @@ int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
     void* p = nullptr;
     uint64_t b = 0;
     switch (which) {
-        case GPK_BUF_PARAMS: p = s->params.p; b = s->cap * 44; s->prefilter.valid = false; break;
+        case GPK_BUF_PARAMS:  // the caller may read or write them: current, not maintained lazily
+            TRY(lazy_kill(s));
+            p = s->params.p;
+            b = s->cap * 44;
+            s->prefilter.valid = false;
+            break;
         case GPK_BUF_GRADS:  // the caller may read or write the dense planes
             TRY(materialize_dense_grads(s));
             TRY(mark_grads_dense(s));
@@ -1557,6 +1671,16 @@ int gpk_download(gpk_session* s, int which, void* host, uint64_t bytes) {
     return ok();
 }
 
+int gpk_set_lazy_adam(gpk_session* s, int on) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    if (s->owner) return fail(GPK_ERR_STATE, "slice context: the mode belongs to its session");
+    TRY(set_device(s));
+    if (!on) TRY(lazy_kill(s));
+    if ((on != 0) != s->lazy_on) ++s->alloc_epoch;  // graphs captured in the other mode
+    s->lazy_on = on != 0;
+    return ok();
+}
+
 int gpk_stage_timing(gpk_session* s, int enable) {
     if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
     s->timing = enable != 0;
@@ -1610,6 +1734,7 @@ int gpk_get_bounds(gpk_session* s, gpk_bounds* out) {
 int gpk_get_gaussians(gpk_session* s, float* records) {
     if (!s || (s->n && !records)) return fail(GPK_ERR_INVALID_ARGUMENT, "null argument");
     TRY(set_device(s));
+    TRY(lazy_sync(s));
     CK(cudaStreamSynchronize(s->stream));
     if (s->n) TRY(copy_planes_out(s, s->params.as<float>(), records));
     return ok();
@@ -1884,6 +2009,7 @@ int gpk_adam_step_scheduled(gpk_session* s, const gpk_learning_rates* lr0, int32
 int gpk_adam_reset(gpk_session* s) {
     if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
     TRY(set_device(s));
+    TRY(lazy_kill(s));  // the deferred steps' parameter updates first
     TRY(adam_reset(s));
     return ok();
 }
@@ -1891,6 +2017,7 @@ int gpk_adam_reset(gpk_session* s) {
 int gpk_get_adam_state(gpk_session* s, float* m, float* v, int64_t* step) {
     if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
     TRY(set_device(s));
+    TRY(lazy_sync(s));
     CK(cudaStreamSynchronize(s->stream));
     if (m && s->n) TRY(copy_planes_out(s, s->adam_m.as<float>(), m));
     if (v && s->n) TRY(copy_planes_out(s, s->adam_v.as<float>(), v));
@@ -1905,6 +2032,7 @@ int gpk_get_adam_state(gpk_session* s, float* m, float* v, int64_t* step) {
 int gpk_set_adam_state(gpk_session* s, const float* m, const float* v, int64_t step) {
     if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
     TRY(set_device(s));
+    TRY(lazy_kill(s));
     CK(cudaStreamSynchronize(s->stream));
     const uint64_t n = s->n;
     if (m && n) TRY(copy_records_in(s, n, m, s->adam_m.as<float>()));
@@ -1942,15 +2070,25 @@ static int train_body_(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf
                        const gpk_raster_config* cfg, double lambda, double dssim_scale,
                        const gpk_learning_rates* lr0, int32_t total, const gpk_slice_pose* next) {
     const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
+    const bool dp = session_comm(s) != nullptr;
+    // lazy step (LazyAdam): the single-GPU step with the default betas; the
+    // pipelined form (Adam fused with the next slice's cull) does not apply
+    const bool lazy = s->lazy_on && !dp && !s->owner && s->n;
+    if (lazy) {
+        TRY(lazy_ensure_live(s));
+        next = nullptr;
+        if (s->capturing) s->cap_lazy = s->cap_lazy_used = s->cap_lazy_writes = true;
+    } else {
+        TRY(lazy_kill(s));
+    }
     if (s->n) TRY(adam_consts_ahead(s, adam_launch(s, lr, true, total, nullptr)));
     s->fuse_gather = s->fuse_gather_ok;  // the forward builds the tile lists (gather_tile)
     const int pst = run_prepare(s, pose, psf, cfg, true);
     s->fuse_gather = false;
     TRY(pst);
     s->assume_prefiltered = false;
-    const bool dp = session_comm(s) != nullptr;
     // the non-survivors' Adam beside the render (see gpk_session::adam_split)
-    const bool split = s->adam_split && !dp && !next && s->n && s->consts_pending;
+    const bool split = s->adam_split && !lazy && !dp && !next && s->n && s->consts_pending;
     if (split) {
         const AdamLaunch ar = adam_launch(s, lr, true, total, nullptr);
         CK(cudaEventRecord(s->ev_rest_fork, s->stream));
@@ -1967,6 +2105,24 @@ static int train_body_(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf
     TRY(run_rasterize(s));
     TRY(run_loss(s, lambda, dssim_scale, true));
     TRY(run_backward(s, false, /*slots=*/!dp));  // dense planes for the collectives
+    if (lazy) {
+        // the survivors (their deferred steps first), then the step's window
+        AdamLaunch a = adam_launch(s, lr, true, total, nullptr);
+        a.slot_grads = s->slot_grads.as<float>();
+        a.gmap = s->gmap.as<uint16_t>();
+        a.surv_gidx = s->survivors.as<uint32_t>();
+        a.grp_surv = s->grp_surv();
+        s->gmap_dirty = false;  // k_lazy_survivors clears the survivors' map entries
+        s->prefilter.valid = false;
+        StageScope scope(s, GPK_STAGE_ADAM);
+        TRY(adam_consts_ready(s, a));
+        launch_lazy_survivors(a, (unsigned)decide_group_count(s->n), s->stream);
+        CK(cudaGetLastError());
+        launch_lazy_window(a, s->stream);
+        CK(cudaGetLastError());
+        if (!s->capturing) s->lazy_pending = true;
+        return GPK_OK;
+    }
     if (split) {
         CK(cudaStreamWaitEvent(s->stream, s->ev_rest_join, 0));
         AdamLaunch a = adam_launch(s, lr, true, total, nullptr);
@@ -2180,6 +2336,7 @@ static int batch_dense_sum(gpk_session* s, gpk_session* const* cx, int B) {
 // is the sum over the slices.
 static int fwd_bwd_batch_body(gpk_session* s, int B, const gpk_slice_pose* poses, const gpk_psf* psf,
                               const gpk_raster_config* cfg) {
+    TRY(lazy_kill(s));  // k_filter_multi reads current parameters
     gpk_session* cx[kMaxBatch];
     for (int k = 0; k < B; ++k) TRY(ctx_get(s, k, &cx[k]));
     s->ctx_used = B - 1;
@@ -2199,6 +2356,7 @@ static int train_batch_body(gpk_session* s, int B, const gpk_slice_pose* poses, 
                             const gpk_raster_config* cfg, double lambda, double dssim_scale,
                             const gpk_learning_rates* lr0, int32_t total) {
     const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
+    TRY(lazy_kill(s));  // eager: k_filter_multi + the dense Adam
     gpk_session* cx[kMaxBatch];
     for (int k = 0; k < B; ++k) TRY(ctx_get(s, k, &cx[k]));
     s->ctx_used = B - 1;
@@ -2262,6 +2420,7 @@ static int train_dp_body(gpk_session* s, int world, int rank, const gpk_slice_po
                          const gpk_raster_config* cfg, double lambda, double dssim_scale,
                          const gpk_learning_rates* lr0, int32_t total, int phases) {
     const double lr[4] = {lr0->position, lr0->opacity, lr0->scale, lr0->rotation};
+    TRY(lazy_kill(s));  // eager: every rank's Adam over all N
     if (phases & GPK_DP_RENDER) {
         TRY(dp_union_alloc(s));
         if (s->n) TRY(adam_consts_ahead(s, adam_launch(s, lr, true, total, nullptr)));
@@ -2340,8 +2499,11 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
     CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
     s->capturing = true;
     s->ctx_used = 0;
+    s->cap_lazy = s->cap_lazy_used = s->cap_lazy_writes = false;
     const int st = body(s, arg);
     s->capturing = false;
+    const bool lazy = s->cap_lazy_used, lazy_writes = s->cap_lazy_writes;
+    s->cap_lazy = s->cap_lazy_used = s->cap_lazy_writes = false;
     for (gpk_session* c : s->ctxs) c->capturing = false;
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(s->stream, &g);
@@ -2378,6 +2540,8 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
     gr.needs_prefilter = meta.needs_prefilter;
     gr.sets_prefilter = meta.sets_prefilter;
     gr.writes_params = meta.writes_params;
+    gr.lazy = lazy;
+    gr.lazy_writes = lazy_writes;
     gr.next_pose = meta.next_pose;
     s->graphs.push_back(std::move(gr));
     *graph_id = (int32_t)s->graphs.size() - 1;
@@ -2459,7 +2623,9 @@ int gpk_graph_capture_train_next(gpk_session* s, const gpk_slice_pose* pose, con
                                  const gpk_learning_rates* lr0, int32_t total_iterations,
                                  const gpk_slice_pose* next_pose, int32_t* graph_id) {
     if (!lr0 || !next_pose || total_iterations < 1) return fail(GPK_ERR_INVALID_ARGUMENT, "bad arguments");
-    if (session_comm(s))  // data parallel: the shard-wise Adam has no fused cull
+    // data parallel: the shard-wise Adam has no fused cull; lazy steps do not
+    // fuse it either (their Adam touches the survivors and a window only)
+    if (session_comm(s) || (s && s->lazy_on))
         return gpk_graph_capture_train(s, pose, psf, cfg, lambda, dssim_scale, lr0, total_iterations, graph_id);
     TRY(presize_step(s, pose, psf, cfg, true, lambda));
     const TrainNextArgs args{pose, psf, cfg, lambda, dssim_scale, lr0, total_iterations, next_pose};
@@ -2596,6 +2762,9 @@ int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
     gpk_session::Graph& g = s->graphs[graph_id];
     if (g.alloc_epoch != epoch_total(s))
         return fail(GPK_ERR_STATE, "graph invalidated: session buffers were reallocated since capture; recapture");
+    // lazy graphs need t_done maintained; any other graph reads or writes
+    // current parameters
+    TRY(g.lazy ? lazy_ensure_live(s) : lazy_kill(s));
     if (g.needs_prefilter && !prefilter_matches(s, &g.prep.pose, &g.prep.psf, &g.prep.cfg)) {
         // the graph starts at K_decide: cull its slice first (stand-alone K_filter,
         // which also clears the gradient planes)
@@ -2607,6 +2776,7 @@ int gpk_graph_launch(gpk_session* s, int32_t graph_id) {
         }
     }
     CK(cudaGraphLaunch(g.exec, s->stream));
+    if (g.lazy_writes) s->lazy_pending = true;
     if (g.sets_prefilter)
         set_prefilter(s, &g.next_pose, &g.prep.psf, &g.prep.cfg);
     else if (g.writes_params || g.needs_prefilter)
@@ -3026,6 +3196,7 @@ int gpk_densify_and_prune_draw(gpk_session* s, const gpk_densify_config* cfg, gp
     if (!s->accum_on) return fail(GPK_ERR_STATE, "densify accumulator not enabled");
     if (!(cfg->split_scale_divisor > 0.0)) return fail(GPK_ERR_INVALID_ARGUMENT, "split_scale_divisor must be > 0");
     TRY(set_device(s));
+    TRY(lazy_kill(s));
     TRY(clear_gmap(s));  // the slot map of the last step is set-indexed
     const uint64_t n = s->n;
     DensifyLaunch a{};

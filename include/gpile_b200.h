@@ -255,6 +255,12 @@ int gpk_set_adam_state(gpk_session* s, const float* m, const float* v, int64_t s
 int gpk_fwd_bwd_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
                       const gpk_raster_config* cfg);
 /* U2: prepare + rasterize + loss(GPK_BUF_TARGET) + backward + scheduled Adam. */
+/* Every later loss evaluation of this session (or slice context) also writes
+ * the f64 loss into *host, page-locked host memory (cudaHostAlloc'd or
+ * registered), from the loss kernel itself: the value is in host memory when
+ * the kernel ends, with no separate device-to-host copy. NULL: off. Graphs
+ * captured before a change must be recaptured. */
+int gpk_set_loss_sink(gpk_session* s, double* host);
 /* Lazy mode (off by default; measured slower on B200): single-GPU
  * U2 steps run "lazily": Adam updates the slice's
  * survivors and one 1/16 window of the set per step; every other Gaussian's

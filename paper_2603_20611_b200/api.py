@@ -400,6 +400,11 @@ class Session:
     STAGES = ("prepare", "sort", "raster", "backward", "chain", "loss", "adam", "voxel", "bin", "voxel_eval",
               "adam_rest")
 
+    def set_loss_sink(self, host_ptr: int | None):
+        """The loss kernel also writes each loss (f64) to this page-locked host
+        address (include/gpile_b200.h gpk_set_loss_sink); None: off."""
+        check(N.lib.gpk_set_loss_sink(self._h, C.c_void_p(host_ptr or None)))
+
     def set_lazy_adam(self, on: bool = True):
         """Lazy single-GPU training steps (include/gpile_b200.h gpk_set_lazy_adam;
         off by default, measured slower): deferred zero-gradient Adam steps,

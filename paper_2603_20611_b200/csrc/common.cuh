@@ -705,6 +705,7 @@ struct LossLaunch {
     float* g;            // 3 planes of W*H: g1, g2, g3
     double* partial;     // 2 per CTA: ssim sum, l1 sum
     double* loss;        // output
+    double* loss_host;   // optional second output: mapped pinned host memory (gpk_set_loss_sink)
     unsigned* done_ctr;
     int W, H;
     double lambda, dssim_scale;

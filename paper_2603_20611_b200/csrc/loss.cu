@@ -80,6 +80,10 @@ __device__ __forceinline__ void finish_loss(const LossLaunch& a, bool with_ssim)
     double L = l1 * inv_n;
     if (with_ssim) L += a.lambda * a.dssim_scale * (1.0 - ss * inv_n);
     *a.loss = L;
+    // straight into the caller's pinned host memory (a posted write: visible
+    // to the host once the kernel has completed; no system fence here, which
+    // would hold the training step's critical path for the PCIe round trip)
+    if (a.loss_host) *a.loss_host = L;
     *a.done_ctr = 0;
 }
 

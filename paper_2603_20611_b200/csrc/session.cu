@@ -122,6 +122,17 @@ struct gpk_session {
     // prepare + forward; the loss waits on ev_tgt_ready (see gpk_upload)
     cudaStream_t copy = nullptr;
     cudaEvent_t ev_tgt_fork = nullptr, ev_tgt_ready = nullptr;
+    // recorded after the last kernel that reads the target (the loss, or the
+    // raster backward that finishes the SSIM gradient): the next upload's copy
+    // starts there, overlapping the rest of the step (chain, Adam) and the next
+    // step's prepare and forward
+    cudaEvent_t ev_tgt_free = nullptr;
+    // under capture the release is a side branch (a record node on its own
+    // stream, joined at the end of the graph) so the PDL edge from the raster
+    // backward to the chain stays programmatic
+    cudaStream_t rel_stream = nullptr;
+    cudaEvent_t ev_rel_fork = nullptr, ev_rel_join = nullptr;
+    bool rel_join_pending = false;
     bool tgt_pending = false;
     // data parallelism (gpk_comm_init): this session's NCCL communicator
     void* comm = nullptr;
@@ -186,6 +197,7 @@ struct gpk_session {
     bool cap_lazy_used = false;  // ... and recorded lazy kernels
     bool cap_lazy_writes = false;
     DevBuf t_done;               // u32 per Gaussian
+    double* loss_sink = nullptr; // device alias of the caller's pinned host loss slot (gpk_set_loss_sink)
     cudaStream_t adam_stream = nullptr;
     cudaEvent_t ev_rest_fork = nullptr, ev_rest_join = nullptr;
     DevBuf surv_bits;                 // K_decide: bit i = Gaussian i survived the last prepare
@@ -520,6 +532,7 @@ int lazy_sync(gpk_session* s);
 int lazy_kill(gpk_session* s);
 int lazy_ensure_live(gpk_session* s);
 bool lazy_now(gpk_session* s);
+int target_release(gpk_session* s);
 
 // K_filter can cull lazily (from stale parameters) only with its quick test:
 // an R = I pose and the cull on (launch_prep's filter_on)
@@ -834,9 +847,11 @@ int run_backward(gpk_session* s, bool stats, bool slots = false, bool urows = fa
     }
     {
         StageScope scope(s, GPK_STAGE_BACKWARD);
+        const bool reads_target = s->prep.ssim_pending;
         launch_raster_bwd(raster_args(s), s->stream);
         CK(cudaGetLastError());
         s->prep.ssim_pending = false;
+        if (reads_target) TRY(target_release(s));
     }
     StageScope scope(s, GPK_STAGE_CHAIN);
     ChainLaunch c;
@@ -1223,6 +1238,21 @@ int target_wait(gpk_session* s) {
     return GPK_OK;
 }
 
+// Everything queued so far that reads the target is done when ev_tgt_free
+// completes (an external record node under capture: each launch re-records it).
+int target_release(gpk_session* s) {
+    if (!s->capturing) {
+        CK(cudaEventRecord(s->ev_tgt_free, s->stream));
+        return GPK_OK;
+    }
+    CK(cudaEventRecord(s->ev_rel_fork, s->stream));
+    CK(cudaStreamWaitEvent(s->rel_stream, s->ev_rel_fork, 0));
+    CK(cudaEventRecordWithFlags(s->ev_tgt_free, s->rel_stream, cudaEventRecordExternal));
+    CK(cudaEventRecord(s->ev_rel_join, s->rel_stream));
+    s->rel_join_pending = true;
+    return GPK_OK;
+}
+
 int run_loss(gpk_session* s, double lambda, double dssim_scale, bool fuse_into_backward = false) {
     if (!s->prep.rasterized) return fail(GPK_ERR_STATE, "photometric_loss: no rendered image");
     const int W = s->img_w, H = s->img_h;
@@ -1241,6 +1271,7 @@ int run_loss(gpk_session* s, double lambda, double dssim_scale, bool fuse_into_b
     l.g = s->loss_g.as<float>();
     l.partial = s->loss_partial.as<double>();
     l.loss = s->loss();
+    l.loss_host = s->loss_sink;
     l.done_ctr = s->loss_done();
     l.W = W;
     l.H = H;
@@ -1267,6 +1298,7 @@ int run_loss(gpk_session* s, double lambda, double dssim_scale, bool fuse_into_b
         launch_loss(l, s->stream);
     }
     CK(cudaGetLastError());
+    if (!fuse) TRY(target_release(s));  // (fused: the raster backward reads it last)
     return GPK_OK;
 }
 
@@ -1447,6 +1479,10 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->copy, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_free, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_rel_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_rel_join, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->rel_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_bjoin, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_ord, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->adam_stream, cudaStreamNonBlocking);
@@ -1513,6 +1549,13 @@ static int session_destroy(gpk_session* s) {
     }
     if (s->ev_tgt_fork) cudaEventDestroy(s->ev_tgt_fork);
     if (s->ev_tgt_ready) cudaEventDestroy(s->ev_tgt_ready);
+    if (s->ev_tgt_free) cudaEventDestroy(s->ev_tgt_free);
+    if (s->ev_rel_fork) cudaEventDestroy(s->ev_rel_fork);
+    if (s->ev_rel_join) cudaEventDestroy(s->ev_rel_join);
+    if (s->rel_stream) {
+        cudaStreamSynchronize(s->rel_stream);
+        cudaStreamDestroy(s->rel_stream);
+    }
     if (s->ev_bjoin) cudaEventDestroy(s->ev_bjoin);
     if (s->ev_ord) cudaEventDestroy(s->ev_ord);
     if (s->ev_rest_fork) cudaEventDestroy(s->ev_rest_fork);
@@ -1592,6 +1635,7 @@ int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
         case GPK_BUF_DL_DI: p = s->dl_di.p; b = px * 4; break;
         case GPK_BUF_TARGET:
             TRY(target_wait(s));
+            if (!s->capturing) TRY(target_release(s));  // (the caller may use it until the next upload)
             p = s->target.p;
             b = px * 4;
             break;
@@ -1643,12 +1687,10 @@ int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes) {
     TRY(set_device(s));
     TRY(ctx_order_in(s));
     if (which == GPK_BUF_TARGET && !s->capturing) {
-        // after everything already queued on the session stream (earlier
-        // readers of the target), on the copy stream: the transfer overlaps
-        // the next step's prepare and forward, which do not read the target
-        // (a context's readers may run on its session's stream: ctx_order_in)
-        CK(cudaEventRecord(s->ev_tgt_fork, s->stream));
-        CK(cudaStreamWaitEvent(s->copy, s->ev_tgt_fork, 0));
+        // on the copy stream, after the last queued reader of the target
+        // (ev_tgt_free): the transfer overlaps the rest of the step that read
+        // it and the next step's prepare and forward, which do not read it
+        CK(cudaStreamWaitEvent(s->copy, s->ev_tgt_free, 0));
         CK(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, s->copy));
         CK(cudaEventRecord(s->ev_tgt_ready, s->copy));
         s->tgt_pending = true;
@@ -1668,6 +1710,23 @@ int gpk_download(gpk_session* s, int which, void* host, uint64_t bytes) {
     TRY(ctx_order_in(s));
     CK(cudaMemcpyAsync(host, p, bytes, cudaMemcpyDeviceToHost, s->stream));
     TRY(ctx_order_out(s, s->stream));
+    return ok();
+}
+
+int gpk_set_loss_sink(gpk_session* s, double* host) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    TRY(set_device(s));
+    void* d = nullptr;
+    if (host) {
+        const cudaError_t e = cudaHostGetDevicePointer(&d, host, 0);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(GPK_ERR_INVALID_ARGUMENT, "loss sink: not page-locked host memory");
+        }
+    }
+    CK(cudaStreamSynchronize(s->stream));
+    if (d != (void*)s->loss_sink) ++s->alloc_epoch;  // captured graphs bake the sink
+    s->loss_sink = static_cast<double*>(d);
     return ok();
 }
 
@@ -2500,7 +2559,15 @@ static int capture_graph(gpk_session* s, int32_t* graph_id, int (*body)(gpk_sess
     s->capturing = true;
     s->ctx_used = 0;
     s->cap_lazy = s->cap_lazy_used = s->cap_lazy_writes = false;
-    const int st = body(s, arg);
+    int st = body(s, arg);
+    // join the target-release branches (target_release) at the end of the graph
+    for (int k = -1; k < (int)s->ctxs.size(); ++k) {
+        gpk_session* c = k < 0 ? s : s->ctxs[k];
+        if (!c->rel_join_pending) continue;
+        c->rel_join_pending = false;
+        if (st == GPK_OK && cudaStreamWaitEvent(s->stream, c->ev_rel_join, 0) != cudaSuccess)
+            st = fail(GPK_ERR_CUDA, "graph capture: target release join");
+    }
     s->capturing = false;
     const bool lazy = s->cap_lazy_used, lazy_writes = s->cap_lazy_writes;
     s->cap_lazy = s->cap_lazy_used = s->cap_lazy_writes = false;

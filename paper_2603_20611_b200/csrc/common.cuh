@@ -561,9 +561,11 @@ struct GatherLaunch {
     SliceArgs slice;
 };
 void launch_gather(const GatherLaunch& a, cudaStream_t st);
-// Multi-pass slices: the pair records of the sorted lists, one per position.
+// Multi-pass slices: the pair records of the sorted lists, one per position,
+// and the tiles' start positions (tile_start[0 .. tiles], the last = P).
 void launch_pair_records(const uint32_t* keys, const uint32_t* vals, const SurvivorRecord* records, PairRecord* pairs,
-                         const Control* ctrl, uint64_t pair_cap, const SliceArgs& slice, int num_sms, cudaStream_t st);
+                         unsigned* tile_start, const Control* ctrl, uint64_t pair_cap, const SliceArgs& slice,
+                         int num_sms, cudaStream_t st);
 
 struct SortLaunch {
     const uint32_t* keys_in;
@@ -591,12 +593,66 @@ struct SortLaunch {
 // control head: first sorted position of every last-pass digit group (+ end).
 constexpr int kGroupBeginWords = kMaxBuckets + 4;
 
+// The photometric loss from the loss kernel's per-CTA partial sums (ssim sum,
+// l1 sum; loss.hpp:29-35): L = l1/N + lambda*dssim*(1 - ssim/N). Reduced by a
+// whole CTA in a fixed order (thread t sums CTAs t, t + blockDim, ..., then a
+// fixed warp/block tree): deterministic run to run. Written by thread 0 to
+// *loss and, when given, straight into the caller's pinned host memory (a
+// posted write, visible to the host once the kernel has completed).
+struct LossFinish {
+    const double* partial;  // nullptr: nothing to finish
+    unsigned nblk;
+    int with_ssim;
+    double inv_n, lambda, dssim_scale;
+    double* loss;
+    double* loss_host;
+};
+
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* s_red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+        s_red[2 * warp] = a;
+        s_red[2 * warp + 1] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a = 0.0;
+        b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += s_red[2 * w];
+            b += s_red[2 * w + 1];
+        }
+    }
+}
+
+__device__ __forceinline__ void loss_reduce(const LossFinish& f, double* s_red /* 2 * 32 */) {
+    double ss = 0.0, l1 = 0.0;
+    for (unsigned k = threadIdx.x; k < f.nblk; k += blockDim.x) {
+        ss += __ldcg(&f.partial[2 * k]);
+        l1 += __ldcg(&f.partial[2 * k + 1]);
+    }
+    block_sum2(ss, l1, s_red);
+    if (threadIdx.x != 0) return;
+    // explicit roundings: the same bits whichever kernel this is inlined into
+    double L = __dmul_rn(l1, f.inv_n);
+    if (f.with_ssim)
+        L = __dadd_rn(L, __dmul_rn(__dmul_rn(f.lambda, f.dssim_scale), __dsub_rn(1.0, __dmul_rn(ss, f.inv_n))));
+    *f.loss = L;
+    if (f.loss_host) *f.loss_host = L;
+}
+
 struct RasterLaunch {
     const SurvivorRecord* records;
     const uint32_t* keys;          // sorted tile keys
     const uint32_t* vals;          // sorted candidate ids
-    const unsigned* grp_begin;     // last radix pass: first position of each digit group
-    int grp_shift;                 // tile >> grp_shift = last-pass digit (-1: no sort pass ran)
+    const unsigned* grp_begin;     // first position of each tile (+ end): the single-pass gather's
+                                   // starts, or k_pair_records' tile starts after radix passes
+    int grp_shift;                 // 0, or -1: no sort pass ran (one tile: [0, P))
     const Control* ctrl;
     uint64_t pair_cap;
     float* image;                  // forward output
@@ -618,6 +674,9 @@ struct RasterLaunch {
     // tile-major pair records: written by the gather (or by the forward when it
     // gathers), read by the pixel kernels through cp.async.bulk
     PairRecord* pairs;
+    // training step: the backward's CTA 0 also finishes the loss from
+    // k_ssim_fwd's partials (the kernel boundary orders them; no ticket)
+    LossFinish fin;
 };
 
 struct ChainLaunch {
@@ -710,8 +769,9 @@ struct LossLaunch {
     int W, H;
     double lambda, dssim_scale;
     float w[11];         // normalized Gaussian taps
-    int finish_in_fwd;   // training step: k_ssim_fwd finalizes the loss; the raster backward
-                         // turns the SSIM partials into dL/dI itself (k_ssim_bwd is skipped)
+    int finish_in_fwd;   // training step (k_ssim_bwd is skipped: the raster backward turns the
+                         // SSIM partials into dL/dI): 1 = k_ssim_fwd finalizes the loss
+                         // (last-CTA ticket), 0 = the raster backward's CTA 0 does
 };
 void launch_loss_fwd_only(const LossLaunch& a, cudaStream_t st);
 

@@ -33,31 +33,7 @@ __device__ __forceinline__ int reflect(int p, int n) {
     return p;
 }
 
-__device__ __forceinline__ void block_sum2(double& a, double& b, double* s_red) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
-    }
-    if (lane == 0) {
-        s_red[2 * warp] = a;
-        s_red[2 * warp + 1] = b;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        a = 0.0;
-        b = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-            a += s_red[2 * w];
-            b += s_red[2 * w + 1];
-        }
-    }
-}
-
-// Last CTA: loss = l1/N + lambda*dssim*(1 - ssim/N). The per-CTA sums are
-// reduced by the whole last CTA in a fixed order (thread t sums CTAs t, t+256,
-// ... then a fixed warp/block tree): deterministic run to run.
+// Last CTA: the loss from every CTA's partial sums (common.cuh loss_reduce).
 __device__ __forceinline__ void finish_loss(const LossLaunch& a, bool with_ssim) {
     __shared__ unsigned s_last;
     __shared__ double s_red2[2 * 32];
@@ -68,23 +44,17 @@ __device__ __forceinline__ void finish_loss(const LossLaunch& a, bool with_ssim)
     }
     __syncthreads();
     if (!s_last) return;
-    const unsigned nblk = gridDim.x * gridDim.y;
-    double ss = 0.0, l1 = 0.0;
-    for (unsigned k = threadIdx.x; k < nblk; k += blockDim.x) {
-        ss += __ldcg(&a.partial[2 * k]);
-        l1 += __ldcg(&a.partial[2 * k + 1]);
-    }
-    block_sum2(ss, l1, s_red2);
-    if (threadIdx.x != 0) return;
-    const double inv_n = 1.0 / ((double)a.W * (double)a.H);
-    double L = l1 * inv_n;
-    if (with_ssim) L += a.lambda * a.dssim_scale * (1.0 - ss * inv_n);
-    *a.loss = L;
-    // straight into the caller's pinned host memory (a posted write: visible
-    // to the host once the kernel has completed; no system fence here, which
-    // would hold the training step's critical path for the PCIe round trip)
-    if (a.loss_host) *a.loss_host = L;
-    *a.done_ctr = 0;
+    LossFinish f;
+    f.partial = a.partial;
+    f.nblk = gridDim.x * gridDim.y;
+    f.with_ssim = with_ssim ? 1 : 0;
+    f.inv_n = 1.0 / ((double)a.W * (double)a.H);
+    f.lambda = a.lambda;
+    f.dssim_scale = a.dssim_scale;
+    f.loss = a.loss;
+    f.loss_host = a.loss_host;
+    loss_reduce(f, s_red2);
+    if (threadIdx.x == 0) *a.done_ctr = 0;
 }
 
 __global__ void __launch_bounds__(256) k_l1_only(const LossLaunch a) {

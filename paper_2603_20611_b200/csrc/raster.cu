@@ -44,51 +44,17 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// First index in keys[0, n) whose value is >= target (keys sorted), one warp.
-__device__ __forceinline__ unsigned warp_lower_bound(const uint32_t* __restrict__ keys, unsigned n,
-                                                     unsigned target) {
-    const int lane = threadIdx.x & 31;
-    unsigned lo = 0, hi = n;  // answer in [lo, hi]
-    while (hi - lo > 32) {
-        const unsigned span = hi - lo;
-        const unsigned pos = lo + (unsigned)(((unsigned long long)span * (lane + 1)) / 32) - 1;
-        const bool less = keys[pos] < target;
-        const unsigned m = __ballot_sync(0xffffffffu, less);
-        const int c = __popc(m);  // probes are monotone: lanes [0, c) are < target
-        const unsigned new_lo = c ? (lo + (unsigned)(((unsigned long long)span * c) / 32)) : lo;
-        const unsigned new_hi =
-            (c < 32) ? (lo + (unsigned)(((unsigned long long)span * (c + 1)) / 32) - 1) : hi;
-        lo = new_lo;
-        hi = new_hi;
-    }
-    const unsigned pos = lo + lane;
-    const bool less = pos < hi && keys[pos] < target;
-    return lo + __popc(__ballot_sync(0xffffffffu, less));
-}
-
-// [begin, end) of the tile's pairs in the sorted list. The last radix pass
-// recorded where each of its digit groups starts; with one pass the digit is
-// the tile, otherwise a warp binary-searches inside the tile's group.
+// [begin, end) of the tile's pairs in the sorted list: the tile starts (the
+// single-pass gather's, or k_pair_records' after radix passes).
 __device__ __forceinline__ void tile_range(const RasterLaunch& a, int tile, unsigned* s_range) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
     if (a.grp_shift < 0) {  // no sort pass: a single tile
         if (threadIdx.x == 0) {
             s_range[0] = 0;
-            s_range[1] = P;
+            s_range[1] = stored_pairs(a.ctrl, a.pair_cap);
         }
         return;
     }
-    const unsigned d = (unsigned)tile >> a.grp_shift;
-    if (a.grp_shift == 0) {
-        if (threadIdx.x < 2) s_range[threadIdx.x] = __ldcg(&a.grp_begin[d + threadIdx.x]);
-        return;
-    }
-    if (warp < 2) {
-        const unsigned lo = __ldcg(&a.grp_begin[d]), hi = __ldcg(&a.grp_begin[d + 1]);
-        const unsigned r = lo + warp_lower_bound(a.keys + lo, hi - lo, (unsigned)tile + warp);
-        if (lane == 0) s_range[warp] = r;
-    }
+    if (threadIdx.x < 2) s_range[threadIdx.x] = __ldcg(&a.grp_begin[tile + threadIdx.x]);
 }
 
 // k_gather's work for one tile (sort.cu): the tile's list from the K_decide
@@ -342,6 +308,10 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
 
     const int tid = threadIdx.x;
     const int tile = blockIdx.x;
+    if (a.fin.partial && tile == 0) {  // the training step's loss (k_ssim_fwd's partials)
+        __shared__ double s_red[2 * 32];
+        loss_reduce(a.fin, s_red);
+    }
     const int tx = tile % a.slice.tiles_x, ty = tile / a.slice.tiles_x;
     const int x0 = tx * kTile, y0 = ty * kTile;
     tile_range(a, tile, s_range);

@@ -101,6 +101,7 @@ struct PrepState {
     bool lists_pending = false; // single-pass slice whose tile lists the forward builds (fused gather)
     float ssim_k = 0.f, inv_n = 0.f;
     float w[11] = {};
+    LossFinish fin{};           // ssim_pending: the loss the raster backward finishes (partial set)
     gpk_slice_pose pose{};
     gpk_psf psf{};
     gpk_raster_config cfg{};
@@ -147,6 +148,8 @@ struct gpk_session {
     DevBuf params, grads, adam_m, adam_v, records, survivors;
     DevBuf keys[2], vals[2], partials, sort_status;  // sort_status: per-sort-tile digit counts
     DevBuf pair_recs;  // tile-major PairRecords of the sorted lists (32 B per pair)
+    DevBuf tile_start; // multi-pass slices: first sorted position of every tile (+ end)
+    bool loss_in_fwd = false;  // A/B knob: the fused loss finished by k_ssim_fwd's last CTA
     DevBuf head;       // Control | hist | prep flags (memset per prepare)
     DevBuf cand_list;  // K_chain's deferral list (survivor slots for the fp64 chain)
     DevBuf cand;       // CandParams of K_filter's candidates (block-major slots)
@@ -453,6 +456,14 @@ int ensure_pairs(gpk_session* s, uint64_t need) {
     return size_sort_status(s);
 }
 
+// Tile starts of a multi-pass slice (written by k_pair_records).
+int ensure_tile_start(gpk_session* s, uint64_t tiles) {
+    const void* before = s->tile_start.p;
+    CK(s->tile_start.ensure((size_t)(tiles + 1) * 4));
+    if (before != s->tile_start.p) ++s->alloc_epoch;
+    return GPK_OK;
+}
+
 int ensure_image(gpk_session* s, int w, int h) {
     const size_t px = (size_t)w * h;
     if (s->copy && px * 4 > s->target.bytes) CK(cudaStreamSynchronize(s->copy));  // no copy into a freed buffer
@@ -627,6 +638,7 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     if (ps.tiles > (1 << (kMaxDigitBits * kMaxSortPasses)))
         return fail(GPK_ERR_INVALID_ARGUMENT, "SlicePose: more than 2^20 tiles unsupported");
     sort_plan(ps.tiles, ps.passes, ps.digit_bits);
+    if (ps.passes > 1) TRY(ensure_tile_start(s, ps.tiles));
     ps.pose = *pose;
     ps.psf = *psf;
     ps.cfg = *cfg;
@@ -689,7 +701,8 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
         TRY(launch_sorts(s, ps.passes, ps.digit_bits, s->grp_pairs(), (unsigned)decide_group_count(s->n)));
         const int fb = ps.passes & 1;
         launch_pair_records(s->keys[fb].as<uint32_t>(), s->vals[fb].as<uint32_t>(), s->records.as<SurvivorRecord>(),
-                            s->pair_recs.as<PairRecord>(), s->ctrl(), s->pair_cap, a, s->num_sms, s->stream);
+                            s->pair_recs.as<PairRecord>(), s->tile_start.as<unsigned>(), s->ctrl(), s->pair_cap, a,
+                            s->num_sms, s->stream);
         CK(cudaGetLastError());
     }
     ps.final_buf = ps.passes & 1;
@@ -751,8 +764,8 @@ RasterLaunch raster_args(gpk_session* s) {
     r.records = s->records.as<SurvivorRecord>();
     r.keys = s->keys[s->prep.final_buf].as<uint32_t>();
     r.vals = s->vals[s->prep.final_buf].as<uint32_t>();
-    r.grp_begin = s->grp_begin();
-    r.grp_shift = s->prep.passes ? s->prep.digit_bits * (s->prep.passes - 1) : -1;
+    r.grp_begin = s->prep.passes > 1 ? s->tile_start.as<unsigned>() : s->grp_begin();
+    r.grp_shift = s->prep.passes ? 0 : -1;
     r.ctrl = s->ctrl();
     r.pair_cap = s->pair_cap;
     r.image = s->image.as<float>();
@@ -770,6 +783,7 @@ RasterLaunch raster_args(gpk_session* s) {
     r.vals_in = s->vals[0].as<uint32_t>();
     r.vals_out = s->vals[1].as<uint32_t>();
     r.pairs = s->pair_recs.as<PairRecord>();
+    r.fin = s->prep.ssim_pending ? s->prep.fin : LossFinish{};
     return r;
 }
 
@@ -851,6 +865,7 @@ int run_backward(gpk_session* s, bool stats, bool slots = false, bool urows = fa
         launch_raster_bwd(raster_args(s), s->stream);
         CK(cudaGetLastError());
         s->prep.ssim_pending = false;
+        s->prep.fin = LossFinish{};
         if (reads_target) TRY(target_release(s));
     }
     StageScope scope(s, GPK_STAGE_CHAIN);
@@ -1287,9 +1302,23 @@ int run_loss(gpk_session* s, double lambda, double dssim_scale, bool fuse_into_b
     TRY(target_wait(s));
     StageScope scope(s, GPK_STAGE_LOSS);
     const bool fuse = fuse_into_backward && lambda != 0.0;
-    l.finish_in_fwd = fuse ? 1 : 0;
+    // the raster backward (which follows at once) finishes the loss: no
+    // last-CTA ticket in k_ssim_fwd (an empty set runs no backward kernel)
+    l.finish_in_fwd = fuse && (s->n == 0 || s->loss_in_fwd) ? 1 : 0;
+    s->prep.fin = LossFinish{};
     if (fuse) {
         launch_loss_fwd_only(l, s->stream);
+        if (!l.finish_in_fwd) {
+            LossFinish& f = s->prep.fin;
+            f.partial = l.partial;
+            f.nblk = loss_partial_blocks(W, H, lambda);
+            f.with_ssim = 1;
+            f.inv_n = 1.0 / ((double)W * (double)H);
+            f.lambda = lambda;
+            f.dssim_scale = dssim_scale;
+            f.loss = l.loss;
+            f.loss_host = l.loss_host;
+        }
         s->prep.ssim_pending = true;
         s->prep.ssim_k = (float)(lambda * dssim_scale);
         s->prep.inv_n = (float)(1.0 / (double)px);
@@ -1461,6 +1490,7 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     if (const char* f = getenv("GPK_ADAM_SPLIT")) s->adam_split = f[0] == '1';
     if (const char* f = getenv("GPK_ADAM_REST_CTAS")) s->adam_rest_ctas = atoi(f);
     if (const char* f = getenv("GPK_LAZY_ADAM")) s->lazy_on = f[0] == '1';
+    if (const char* f = getenv("GPK_LOSS_IN_FWD")) s->loss_in_fwd = f[0] == '1';
     if (s->num_sms < 1) s->num_sms = 148;
     e = s->persist.ensure(kPersistBytes);
     if (e == cudaSuccess) e = cudaMemsetAsync(s->persist.p, 0, kPersistBytes, s->stream);
@@ -1523,7 +1553,7 @@ static int session_destroy(gpk_session* s) {
     }
     s->graphs.clear();
     DevBuf* bufs[] = {&s->params, &s->grads, &s->adam_m, &s->adam_v, &s->records, &s->survivors,
-                      &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials, &s->pair_recs,
+                      &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials, &s->pair_recs, &s->tile_start,
                       &s->sort_status, &s->head, &s->persist, &s->image,
                       &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm, &s->acc_norm, &s->acc_obs, &s->acc_world,
                       &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table, &s->bucket_tab,
@@ -2639,6 +2669,7 @@ static int presize_step(gpk_session* s, const gpk_slice_pose* pose, const gpk_ps
     TRY(make_slice(s, pose, psf, cfg, a));
     TRY(ensure_image(s, a.W, a.H));
     if (!s->keys[0].p) TRY(ensure_pairs(s, std::max<uint64_t>(1ull << 20, 8 * s->n)));
+    TRY(ensure_tile_start(s, (uint64_t)a.tiles_x * a.tiles_y));
     if (loss) {
         const size_t px = (size_t)a.W * a.H;
         const void* before[2] = {s->loss_g.p, s->loss_partial.p};

@@ -287,16 +287,23 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherLaunch a)
         store_pair_record(a.pairs + t, make_pair_record(a.records[__ldcg(&a.vals_out[t])], tx, ty, X0, Y0));
 }
 
-// Multi-pass slices: the pair record of every sorted position (its tile is its key).
+// Multi-pass slices: the pair record of every sorted position (its tile is its
+// key), and the tile starts: position j opens every tile in (key[j-1], key[j]]
+// (key[-1] = -1, key[P] = ntiles), so the pixel kernels read their range with
+// two loads instead of searching the sorted keys.
 __global__ void __launch_bounds__(256) k_pair_records(const uint32_t* __restrict__ keys,
                                                       const uint32_t* __restrict__ vals,
                                                       const SurvivorRecord* __restrict__ records,
-                                                      PairRecord* __restrict__ pairs, const Control* ctrl,
-                                                      uint64_t pair_cap, const SliceArgs sl) {
+                                                      PairRecord* __restrict__ pairs, unsigned* __restrict__ tile_start,
+                                                      const Control* ctrl, uint64_t pair_cap, const SliceArgs sl) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     const unsigned P = stored_pairs(ctrl, pair_cap);
-    for (unsigned j = blockIdx.x * blockDim.x + threadIdx.x; j < P; j += gridDim.x * blockDim.x) {
-        const unsigned tile = keys[j];
+    const unsigned ntiles = (unsigned)(sl.tiles_x * sl.tiles_y);
+    for (unsigned j = blockIdx.x * blockDim.x + threadIdx.x; j <= P; j += gridDim.x * blockDim.x) {
+        const unsigned tile = j < P ? keys[j] : ntiles;
+        const unsigned prev = j ? keys[j - 1] : 0xffffffffu;
+        for (unsigned t = prev + 1; t <= tile; ++t) tile_start[t] = j;
+        if (j == P) break;
         const int tx = (int)(tile % (unsigned)sl.tiles_x), ty = (int)(tile / (unsigned)sl.tiles_x);
         const double X0 = ((double)(tx * kTile) - sl.ppx) * sl.sx;
         const double Y0 = ((double)(ty * kTile) - sl.ppy) * sl.sy;
@@ -311,8 +318,10 @@ void launch_gather(const GatherLaunch& a, cudaStream_t st) {
 }
 
 void launch_pair_records(const uint32_t* keys, const uint32_t* vals, const SurvivorRecord* records, PairRecord* pairs,
-                         const Control* ctrl, uint64_t pair_cap, const SliceArgs& slice, int num_sms, cudaStream_t st) {
-    launch_pdl(k_pair_records, dim3(num_sms * 8), dim3(256), 0, st, keys, vals, records, pairs, ctrl, pair_cap, slice);
+                         unsigned* tile_start, const Control* ctrl, uint64_t pair_cap, const SliceArgs& slice,
+                         int num_sms, cudaStream_t st) {
+    launch_pdl(k_pair_records, dim3(num_sms * 8), dim3(256), 0, st, keys, vals, records, pairs, tile_start, ctrl,
+               pair_cap, slice);
 }
 
 void launch_super_scan(unsigned* region, uint64_t tiles_cap, unsigned nb, const Control* ctrl, uint64_t pair_cap,

@@ -392,36 +392,61 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 // One tile's list from the K_decide buckets (render.hpp:142-160 order): the
 // buckets of tile d — one per K_decide group, each already in ascending slot
-// order (K_decide fills them stably) — concatenated in group order into
-// vals_out[out ...). The whole CTA (kThreads, kItems groups per thread per
-// chunk) copies cooperatively: an exclusive scan of the chunk's bucket sizes,
-// then every thread takes list positions and finds its bucket by binary
-// search — work linear in the list length and independent of how the pairs
-// are spread over groups (a clustered set can put hundreds of one group's
-// survivors into one tile). Returns the end of the list. Ends with a barrier.
+// order (K_decide fills them stably) — concatenated in group order. The list
+// starts where the pairs of tiles < d end: a group's row holds its bucket
+// starts, so row_g[d] - row_g[0] is the group's count of pairs in tiles < d
+// and the tile's start is their sum over the groups (read with the bucket
+// bounds; no global prefix over the tiles is needed). The whole CTA
+// (kThreads, kItems groups per thread per chunk) copies cooperatively: an
+// exclusive scan of the chunk's bucket sizes, then every thread takes list
+// positions and finds its bucket by binary search — work linear in the list
+// length and independent of how the pairs are spread over groups (a
+// clustered set can put hundreds of one group's survivors into one tile).
+// Publishes tile_begin[d] (and the end, tile_begin[ntiles], from the last
+// tile) and leaves [begin, end) in s_range. Ends with a barrier.
 template <int kThreads, int kItems = 1>
-__device__ __forceinline__ unsigned gather_tile_list(const unsigned* __restrict__ bucket_tab, unsigned ngroups,
-                                                     unsigned row_stride, unsigned d, unsigned out, unsigned P,
-                                                     const uint32_t* vals_in, uint32_t* vals_out,
-                                                     unsigned* s_ex /* kThreads * kItems + 1 */,
-                                                     unsigned* s_b /* kThreads * kItems */,
-                                                     unsigned* s_wsum /* kThreads / 32 */) {
+__device__ __forceinline__ void gather_tile_list(const unsigned* __restrict__ bucket_tab, unsigned ngroups,
+                                                 unsigned row_stride, unsigned d, unsigned ntiles,
+                                                 unsigned* tile_begin, unsigned P, uint64_t cap,
+                                                 const uint32_t* vals_in, uint32_t* vals_out,
+                                                 unsigned* s_ex /* kThreads * kItems + 1 */,
+                                                 unsigned* s_b /* kThreads * kItems */,
+                                                 unsigned* s_wsum /* 2 * kThreads / 32 */,
+                                                 unsigned* s_range /* 2 */) {
     constexpr unsigned kChunk = kThreads * kItems;
+    constexpr int kWarps = kThreads / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned out = 0;
+    if (ngroups > kChunk) {  // the start first, over every group (the chunks below need it)
+        unsigned part = 0;
+        for (unsigned g = tid; g < ngroups; g += kThreads) {
+            const unsigned* row = bucket_tab + (uint64_t)g * row_stride;
+            part += min(__ldcg(&row[d]), P) - min(__ldcg(&row[0]), P);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) s_wsum[kWarps + warp] = part;
+        __syncthreads();
+        for (int w = 0; w < kWarps; ++w) out += s_wsum[kWarps + w];
+    }
+    bool first = true;
+    unsigned begin = out;  // (single chunk: set below)
     for (unsigned g0 = 0; g0 < ngroups; g0 += kChunk) {
-        unsigned b[kItems], cnt[kItems], run = 0;
+        unsigned b[kItems], cnt[kItems], run = 0, below = 0;
 #pragma unroll
         for (int q = 0; q < kItems; ++q) {  // group g's bucket for tile d: [row[d], row[d + 1])
             const unsigned g = g0 + tid * kItems + q;
-            unsigned e = 0;
+            unsigned e = 0, z = 0;
             b[q] = 0;
             if (g < ngroups) {
                 const unsigned* row = bucket_tab + (uint64_t)g * row_stride;
                 b[q] = min(__ldcg(&row[d]), P);
                 e = min(__ldcg(&row[d + 1]), P);
+                z = min(__ldcg(&row[0]), P);
             }
             cnt[q] = e > b[q] ? e - b[q] : 0u;
             run += cnt[q];
+            below += b[q] - z;
         }
         unsigned incl = run;
 #pragma unroll
@@ -429,8 +454,19 @@ __device__ __forceinline__ unsigned gather_tile_list(const unsigned* __restrict_
             const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += u;
         }
+        if (ngroups <= kChunk) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+        }
         if (lane == 31) s_wsum[warp] = incl;
+        if (lane == 0 && ngroups <= kChunk) s_wsum[kWarps + warp] = below;
         __syncthreads();
+        if (first && ngroups <= kChunk) {
+            out = 0;
+            for (int w = 0; w < kWarps; ++w) out += s_wsum[kWarps + w];
+            begin = out;
+        }
+        first = false;
         unsigned ex = incl - run;
         for (int w = 0; w < warp; ++w) ex += s_wsum[w];
 #pragma unroll
@@ -447,12 +483,23 @@ __device__ __forceinline__ unsigned gather_tile_list(const unsigned* __restrict_
 #pragma unroll
             for (unsigned step = kChunk / 2; step > 0; step >>= 1)
                 if (s_ex[q + step] <= t) q += step;
-            vals_out[out + t] = __ldcg(&vals_in[s_b[q] + (t - s_ex[q])]);
+            // (bounds: only a pair overflow, whose step is replayed, can exceed them)
+            if ((uint64_t)out + t < cap) vals_out[out + t] = __ldcg(&vals_in[s_b[q] + (t - s_ex[q])]);
         }
         out += total;
         __syncthreads();  // s_ex / s_b / s_wsum are rewritten by the next chunk
     }
-    return out;
+    if (ngroups == 0) begin = out = 0;
+    // (a pair overflow, whose step is replayed, is the only way past the cap)
+    begin = (unsigned)min((uint64_t)begin, cap);
+    out = (unsigned)min((uint64_t)out, cap);
+    if (tid == 0) {
+        tile_begin[d] = begin;
+        if (d + 1 == ntiles) tile_begin[ntiles] = out;
+        s_range[0] = begin;
+        s_range[1] = out;
+    }
+    __syncthreads();
 }
 
 struct AdamConsts {
@@ -506,7 +553,7 @@ struct PrepLaunch {
     CandParams* surv_params;  // survivor params by survivor slot
     uint2* grp_pairs;         // per K_decide group: (first pair position, pair count)
     unsigned* bucket_tab;     // single-pass slices: per group, bucket starts + end (else nullptr)
-    unsigned* tile_begin;     // single-pass slices: tile list starts, written by the last group
+    unsigned* tile_begin;     // (unused by K_decide: the gather derives each tile's start)
     unsigned* grp_surv;       // per K_decide group: survivors (slots g*4096 + [0, S_g))
     unsigned* surv_bits;      // optional: bit i = Gaussian i survived (K_decide writes its group's words)
     unsigned nfilter;         // 64-Gaussian chunks
@@ -550,7 +597,7 @@ struct GatherLaunch {
     unsigned ngroups;
     unsigned ntiles;
     unsigned row_stride;           // radix buckets + 1
-    const unsigned* tile_begin;    // tile list starts (+ end), computed by the last K_decide group
+    unsigned* tile_begin;          // out: tile list starts (+ end), derived by the gather
     const uint32_t* vals_in;       // bucketed slots
     uint32_t* vals_out;            // per-tile lists, ascending slot
     const Control* ctrl;

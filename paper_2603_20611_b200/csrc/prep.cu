@@ -268,7 +268,6 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
             for (int q = 0; q < kPer; ++q) {
                 v[q] = s_hist[0][d0 + q];
                 run += v[q];
-                if (v[q]) atomicAdd(&a.hist[d0 + q], v[q]);
             }
             unsigned incl = run;
 #pragma unroll
@@ -336,41 +335,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
                 if (pc[q]) atomicAdd(&s_hist[0][tl[q]], pc[q]);
             __syncthreads();
         }
-        // the last group to finish turns the per-tile counts into list starts
-        // (one scan, instead of every gather CTA re-reading the same counts)
-        __syncthreads();
-        __shared__ bool s_last;
-        if (tid == 0) s_last = ticket_acq_rel(&a.ctrl->decide_done) == ngroups - 1;
-        __syncthreads();
-        if (!s_last) return;
-        {
-            constexpr int kPer = kMaxBuckets / kDecideThreads;
-            const unsigned d0 = tid * kPer;
-            const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
-            unsigned v[kPer], run = 0;
-#pragma unroll
-            for (int q = 0; q < kPer; ++q) {
-                v[q] = d0 + q < nb ? __ldcg(&a.hist[d0 + q]) : 0u;
-                run += v[q];
-            }
-            unsigned incl = run;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += u;
-            }
-            __syncthreads();
-            if (lane == 31) s_cnt[1][warp] = incl;
-            __syncthreads();
-            unsigned ex = incl - run;
-            for (int w = 0; w < warp; ++w) ex += s_cnt[1][w];
-#pragma unroll
-            for (int q = 0; q < kPer; ++q) {
-                if (d0 + q < nb) a.tile_begin[d0 + q] = min(ex, P);
-                ex += v[q];
-            }
-            if (tid == kDecideThreads - 1) a.tile_begin[nb] = min(ex, P);
-        }
+        // (each tile's list start is derived by its gather from the rows)
         return;
     }
     for (unsigned k = tid; k < Pb; k += kDecideThreads) {

@@ -58,13 +58,15 @@ __device__ __forceinline__ void tile_range(const RasterLaunch& a, int tile, unsi
 }
 
 // k_gather's work for one tile (sort.cu): the tile's list from the K_decide
-// buckets (common.cuh gather_tile_list). The list is visible to the CTA after
-// the helper's closing barrier.
+// buckets (common.cuh gather_tile_list), its range left in s_range. The list
+// is visible to the CTA after the helper's closing barrier.
 template <int kThreads, int kItems>
-__device__ __forceinline__ void gather_tile(const RasterLaunch& a, unsigned d) {
-    __shared__ unsigned s_ex[kThreads * kItems + 1], s_b[kThreads * kItems], s_wsum[kThreads / 32];
-    gather_tile_list<kThreads, kItems>(a.bucket_tab, a.ngroups, a.row_stride, d, __ldcg(&a.grp_begin[d]),
-                                       stored_pairs(a.ctrl, a.pair_cap), a.vals_in, a.vals_out, s_ex, s_b, s_wsum);
+__device__ __forceinline__ void gather_tile(const RasterLaunch& a, unsigned d, unsigned* s_range) {
+    __shared__ unsigned s_ex[kThreads * kItems + 1], s_b[kThreads * kItems], s_wsum[2 * kThreads / 32];
+    gather_tile_list<kThreads, kItems>(a.bucket_tab, a.ngroups, a.row_stride, d,
+                                       (unsigned)(a.slice.tiles_x * a.slice.tiles_y),
+                                       const_cast<unsigned*>(a.grp_begin), stored_pairs(a.ctrl, a.pair_cap),
+                                       a.pair_cap, a.vals_in, a.vals_out, s_ex, s_b, s_wsum, s_range);
 }
 
 // Double-buffered TMA staging of a tile's PairRecords: batch q of [start, end)
@@ -133,10 +135,10 @@ __global__ void __launch_bounds__(kFwdThreads) k_raster_fwd(const RasterLaunch a
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
     const bool produce = a.bucket_tab != nullptr;
-    if (produce) gather_tile<kFwdThreads, 2>(a, (unsigned)tile);  // 256 groups per chunk (ends with a barrier)
+    if (produce) gather_tile<kFwdThreads, 2>(a, (unsigned)tile, s_range);  // 256 groups per chunk (ends with a barrier)
     const int tx = tile % a.slice.tiles_x, ty = tile / a.slice.tiles_x;
     const int x0 = tx * kTile, y0 = ty * kTile;
-    tile_range(a, tile, s_range);
+    if (!produce) tile_range(a, tile, s_range);
     if (!produce && tid == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);

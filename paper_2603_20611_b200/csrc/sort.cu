@@ -272,12 +272,13 @@ constexpr int kGatherThreads = 256;
 
 __global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    __shared__ unsigned s_ex[kGatherThreads + 1], s_b[kGatherThreads], s_wsum[kGatherThreads / 32];
+    __shared__ unsigned s_ex[kGatherThreads + 1], s_b[kGatherThreads], s_wsum[2 * kGatherThreads / 32];
+    __shared__ unsigned s_range[2];
     const unsigned d = blockIdx.x;
-    const unsigned begin = __ldcg(&a.tile_begin[d]);
-    const unsigned end = gather_tile_list<kGatherThreads>(a.bucket_tab, a.ngroups, a.row_stride, d, begin,
-                                                          stored_pairs(a.ctrl, a.pair_cap), a.vals_in, a.vals_out,
-                                                          s_ex, s_b, s_wsum);
+    gather_tile_list<kGatherThreads>(a.bucket_tab, a.ngroups, a.row_stride, d, a.ntiles, a.tile_begin,
+                                     stored_pairs(a.ctrl, a.pair_cap), a.pair_cap, a.vals_in, a.vals_out, s_ex, s_b,
+                                     s_wsum, s_range);
+    const unsigned begin = s_range[0], end = min((uint64_t)s_range[1], a.pair_cap);
     // the tile's pair records, in list order (the list is this CTA's own
     // writes: visible after the helper's closing barrier)
     const int tx = (int)(d % (unsigned)a.slice.tiles_x), ty = (int)(d / (unsigned)a.slice.tiles_x);

@@ -402,13 +402,17 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // positions and finds its bucket by binary search — work linear in the list
 // length and independent of how the pairs are spread over groups (a
 // clustered set can put hundreds of one group's survivors into one tile).
+// The table is tile-major (entry (d, g) at d * gstride + g): a tile's bounds
+// over the groups are three contiguous runs (rows d, d + 1 and 0). Every list
+// position is handed to emit(position, index in the list, slot) as it is copied (the callers
+// write the list and build the position's PairRecord in the same pass).
 // Publishes tile_begin[d] (and the end, tile_begin[ntiles], from the last
 // tile) and leaves [begin, end) in s_range. Ends with a barrier.
-template <int kThreads, int kItems = 1>
+template <int kThreads, int kItems, typename Emit>
 __device__ __forceinline__ void gather_tile_list(const unsigned* __restrict__ bucket_tab, unsigned ngroups,
-                                                 unsigned row_stride, unsigned d, unsigned ntiles,
+                                                 unsigned gstride, unsigned d, unsigned ntiles,
                                                  unsigned* tile_begin, unsigned P, uint64_t cap,
-                                                 const uint32_t* vals_in, uint32_t* vals_out,
+                                                 const uint32_t* vals_in, Emit emit,
                                                  unsigned* s_ex /* kThreads * kItems + 1 */,
                                                  unsigned* s_b /* kThreads * kItems */,
                                                  unsigned* s_wsum /* 2 * kThreads / 32 */,
@@ -419,10 +423,8 @@ __device__ __forceinline__ void gather_tile_list(const unsigned* __restrict__ bu
     unsigned out = 0;
     if (ngroups > kChunk) {  // the start first, over every group (the chunks below need it)
         unsigned part = 0;
-        for (unsigned g = tid; g < ngroups; g += kThreads) {
-            const unsigned* row = bucket_tab + (uint64_t)g * row_stride;
-            part += min(__ldcg(&row[d]), P) - min(__ldcg(&row[0]), P);
-        }
+        for (unsigned g = tid; g < ngroups; g += kThreads)
+            part += min(__ldcg(&bucket_tab[(uint64_t)d * gstride + g]), P) - min(__ldcg(&bucket_tab[g]), P);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
         if (lane == 0) s_wsum[kWarps + warp] = part;
@@ -439,10 +441,9 @@ __device__ __forceinline__ void gather_tile_list(const unsigned* __restrict__ bu
             unsigned e = 0, z = 0;
             b[q] = 0;
             if (g < ngroups) {
-                const unsigned* row = bucket_tab + (uint64_t)g * row_stride;
-                b[q] = min(__ldcg(&row[d]), P);
-                e = min(__ldcg(&row[d + 1]), P);
-                z = min(__ldcg(&row[0]), P);
+                b[q] = min(__ldcg(&bucket_tab[(uint64_t)d * gstride + g]), P);
+                e = min(__ldcg(&bucket_tab[(uint64_t)(d + 1) * gstride + g]), P);
+                z = min(__ldcg(&bucket_tab[g]), P);
             }
             cnt[q] = e > b[q] ? e - b[q] : 0u;
             run += cnt[q];
@@ -484,7 +485,7 @@ __device__ __forceinline__ void gather_tile_list(const unsigned* __restrict__ bu
             for (unsigned step = kChunk / 2; step > 0; step >>= 1)
                 if (s_ex[q + step] <= t) q += step;
             // (bounds: only a pair overflow, whose step is replayed, can exceed them)
-            if ((uint64_t)out + t < cap) vals_out[out + t] = __ldcg(&vals_in[s_b[q] + (t - s_ex[q])]);
+            if ((uint64_t)out + t < cap) emit(out + t, out - begin + t, __ldcg(&vals_in[s_b[q] + (t - s_ex[q])]));
         }
         out += total;
         __syncthreads();  // s_ex / s_b / s_wsum are rewritten by the next chunk
@@ -552,7 +553,8 @@ struct PrepLaunch {
     unsigned* cand_count;     // candidates per chunk (plain stores)
     CandParams* surv_params;  // survivor params by survivor slot
     uint2* grp_pairs;         // per K_decide group: (first pair position, pair count)
-    unsigned* bucket_tab;     // single-pass slices: per group, bucket starts + end (else nullptr)
+    unsigned* bucket_tab;     // single-pass slices: bucket starts, tile-major (else nullptr)
+    unsigned bucket_gstride;  // groups per tile row of bucket_tab
     unsigned* tile_begin;     // (unused by K_decide: the gather derives each tile's start)
     unsigned* grp_surv;       // per K_decide group: survivors (slots g*4096 + [0, S_g))
     unsigned* surv_bits;      // optional: bit i = Gaussian i survived (K_decide writes its group's words)
@@ -593,10 +595,10 @@ constexpr int kParamAlign = 512;                           // plane stride (capa
 // group's pairs by tile and wrote the bucket starts; one CTA per tile
 // concatenates its buckets in group order (= slot order).
 struct GatherLaunch {
-    const unsigned* bucket_tab;    // per group: bucket start of every tile, then the group end
+    const unsigned* bucket_tab;    // tile-major: (tile d, group g) bucket start at d * gstride + g; row nb = ends
     unsigned ngroups;
     unsigned ntiles;
-    unsigned row_stride;           // radix buckets + 1
+    unsigned gstride;              // groups per tile row
     unsigned* tile_begin;          // out: tile list starts (+ end), derived by the gather
     const uint32_t* vals_in;       // bucketed slots
     uint32_t* vals_out;            // per-tile lists, ascending slot
@@ -715,7 +717,7 @@ struct RasterLaunch {
     // builds its tile's list from K_decide's buckets (k_gather's work) into
     // vals_out (== vals), or nullptr when the lists are built already
     const unsigned* bucket_tab;
-    unsigned ngroups, row_stride;
+    unsigned ngroups, gstride;
     const uint32_t* vals_in;
     uint32_t* vals_out;
     // tile-major pair records: written by the gather (or by the forward when it

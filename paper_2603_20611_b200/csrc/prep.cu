@@ -279,16 +279,17 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
             __syncthreads();
             unsigned ex = incl - run;
             for (int w = 0; w < warp; ++w) ex += s_cnt[0][w];
-            // the group's row of bucket starts (+ end), coalesced
-            unsigned* trow = a.bucket_tab + (uint64_t)g * (nb + 1);
+            // the group's column of bucket starts (+ end) in the tile-major table
+            unsigned* tcol = a.bucket_tab + g;
+            const uint64_t gs = a.bucket_gstride;
 #pragma unroll
             for (int q = 0; q < kPer; ++q) {
                 s_start[d0 + q] = ex;
-                if (d0 + q < nb) trow[d0 + q] = P0 + ex;
+                if (d0 + q < nb) tcol[(d0 + q) * gs] = P0 + ex;
                 s_hist[0][d0 + q] = 0;  // becomes the fill counter
                 ex += v[q];
             }
-            if (tid == 0) trow[nb] = P0 + Pb;
+            if (tid == 0) tcol[nb * gs] = P0 + Pb;
         }
         __syncthreads();
         // stable fill: each bucket receives its pairs in pair order (= ascending

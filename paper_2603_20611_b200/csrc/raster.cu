@@ -57,18 +57,6 @@ __device__ __forceinline__ void tile_range(const RasterLaunch& a, int tile, unsi
     if (threadIdx.x < 2) s_range[threadIdx.x] = __ldcg(&a.grp_begin[tile + threadIdx.x]);
 }
 
-// k_gather's work for one tile (sort.cu): the tile's list from the K_decide
-// buckets (common.cuh gather_tile_list), its range left in s_range. The list
-// is visible to the CTA after the helper's closing barrier.
-template <int kThreads, int kItems>
-__device__ __forceinline__ void gather_tile(const RasterLaunch& a, unsigned d, unsigned* s_range) {
-    __shared__ unsigned s_ex[kThreads * kItems + 1], s_b[kThreads * kItems], s_wsum[2 * kThreads / 32];
-    gather_tile_list<kThreads, kItems>(a.bucket_tab, a.ngroups, a.row_stride, d,
-                                       (unsigned)(a.slice.tiles_x * a.slice.tiles_y),
-                                       const_cast<unsigned*>(a.grp_begin), stored_pairs(a.ctrl, a.pair_cap),
-                                       a.pair_cap, a.vals_in, a.vals_out, s_ex, s_b, s_wsum, s_range);
-}
-
 // Double-buffered TMA staging of a tile's PairRecords: batch q of [start, end)
 // goes to buffer q & 1; one elected thread arms the buffer's mbarrier with
 // the batch's bytes and issues one bulk copy. Callers wait with pair_wait and
@@ -135,10 +123,29 @@ __global__ void __launch_bounds__(kFwdThreads) k_raster_fwd(const RasterLaunch a
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
     const bool produce = a.bucket_tab != nullptr;
-    if (produce) gather_tile<kFwdThreads, 2>(a, (unsigned)tile, s_range);  // 256 groups per chunk (ends with a barrier)
     const int tx = tile % a.slice.tiles_x, ty = tile / a.slice.tiles_x;
     const int x0 = tx * kTile, y0 = ty * kTile;
-    if (!produce) tile_range(a, tile, s_range);
+    const double X0 = ((double)x0 - a.slice.ppx) * a.slice.sx;
+    const double Y0 = ((double)y0 - a.slice.ppy) * a.slice.sy;
+    if (produce) {
+        // the training step's forward gathers its own tile's list (k_gather's
+        // work, 256 groups per chunk) and builds each position's PairRecord as
+        // it is copied: into the first staging batch when it falls there, and
+        // to global memory for the backward (and this kernel's later batches)
+        __shared__ unsigned s_ex[kFwdThreads * 2 + 1], s_b[kFwdThreads * 2], s_wsum[2 * kFwdThreads / 32];
+        auto emit = [&](unsigned pos, unsigned idx, uint32_t slot) {
+            a.vals_out[pos] = slot;
+            const PairRecord pr = make_pair_record(a.records[slot], tx, ty, X0, Y0);
+            if (idx < kPairBatch) store_pair_record(&s_pr[0][idx], pr);
+            store_pair_record(a.pairs + pos, pr);
+        };
+        gather_tile_list<kFwdThreads, 2>(a.bucket_tab, a.ngroups, a.gstride, (unsigned)tile,
+                                         (unsigned)(a.slice.tiles_x * a.slice.tiles_y),
+                                         const_cast<unsigned*>(a.grp_begin), stored_pairs(a.ctrl, a.pair_cap),
+                                         a.pair_cap, a.vals_in, emit, s_ex, s_b, s_wsum, s_range);
+    } else {
+        tile_range(a, tile, s_range);
+    }
     if (!produce && tid == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
@@ -147,8 +154,6 @@ __global__ void __launch_bounds__(kFwdThreads) k_raster_fwd(const RasterLaunch a
     const int lx = 2 * (lane & 7), ly = warp * 4 + (lane >> 3);
     const unsigned ybit = 1u << (16 + ly), xb0 = 1u << lx, xb1 = 2u << lx;
     const unsigned warp_y = 0xfu << (16 + warp * 4);
-    const double X0 = ((double)x0 - a.slice.ppx) * a.slice.sx;
-    const double Y0 = ((double)y0 - a.slice.ppy) * a.slice.sy;
     const float fx0 = (float)(lx * a.slice.sx), fx1 = (float)((lx + 1) * a.slice.sx);
     const float fy = (float)(ly * a.slice.sy);
     __syncthreads();
@@ -157,17 +162,15 @@ __global__ void __launch_bounds__(kFwdThreads) k_raster_fwd(const RasterLaunch a
 
     float acc0 = 0.f, acc1 = 0.f;
     if (produce) {
-        // the training step's forward builds its tile's records itself (from
-        // the list it just gathered) and stores them for the backward
+        // batch 0 was staged by the gather; later batches (tiles of more than
+        // kPairBatch pairs) come back from the records this CTA just stored
         for (unsigned q = 0; q < nbatch; ++q) {
             const unsigned b = ps.start + q * kPairBatch, nb = min((unsigned)kPairBatch, ps.end - b);
-            for (unsigned t = tid; t < nb; t += kFwdThreads) {
-                // (L2 load: the list was written by this CTA just now)
-                const PairRecord pr = make_pair_record(a.records[__ldcg(&a.vals[b + t])], tx, ty, X0, Y0);
-                store_pair_record(&s_pr[0][t], pr);
-                store_pair_record(a.pairs + b + t, pr);
+            if (q > 0) {
+                for (unsigned t = tid; t < 2 * nb; t += kFwdThreads)
+                    reinterpret_cast<float4*>(s_pr[0])[t] = __ldcg(reinterpret_cast<const float4*>(a.pairs + b) + t);
+                __syncthreads();
             }
-            __syncthreads();
             fwd_batch(s_pr[0], nb, warp_y, ybit, xb0, xb1, fx0, fx1, fy, acc0, acc1);
             __syncthreads();
         }

@@ -165,7 +165,8 @@ struct gpk_session {
     DevBuf gmap;       // slot mode: u16 per primitive, 1 + survivor offset in its group (else 0)
     bool gmap_dirty = false;      // a slot backward wrote gmap and no Adam consumed (cleared) it
     DevBuf grp_table;  // per K_decide group: uint2 (first pair, pairs), then u32 survivors
-    DevBuf bucket_tab; // single-pass slices: per group, tiles + 1 bucket starts
+    DevBuf bucket_tab; // single-pass slices: bucket starts, tile-major (tiles + 1 rows of bucket_gs groups)
+    unsigned bucket_gs = 0;
     uint2* grp_pairs() { return grp_table.as<uint2>(); }
     unsigned* grp_surv() { return reinterpret_cast<unsigned*>(grp_table.as<char>() + (cap / kDecideGroupSize + 2) * 8); }
     int num_sms = 148;
@@ -422,6 +423,9 @@ int mark_grads_dense(gpk_session* s) {
 
 uint64_t decide_group_count(uint64_t n);
 
+// Groups per tile row of the tile-major bucket table (sized with the set capacity).
+unsigned bucket_gstride(const gpk_session* s) { return s->bucket_gs; }
+
 // Per-sort-tile digit counts of every radix pass (kept zero between prepares:
 // K_filter clears the rows the previous prepare used). A pass has one row per
 // sort tile: kSortTile consecutive pair positions, or — the first pass over
@@ -564,6 +568,7 @@ PrepLaunch prep_launch(gpk_session* s, const SliceArgs& a, int passes, int digit
     pl.grp_surv = s->grp_surv();
     pl.surv_bits = s->surv_bits.as<unsigned>();
     pl.bucket_tab = passes == 1 ? s->bucket_tab.as<unsigned>() : nullptr;
+    pl.bucket_gstride = bucket_gstride(s);
     pl.tile_begin = s->grp_begin();
     pl.grads_dirty = s->grads_dirty();
     pl.dirty_idx = s->dirty_idx.as<uint32_t>();
@@ -779,7 +784,7 @@ RasterLaunch raster_args(gpk_session* s) {
     for (int t = 0; t < 11; ++t) r.w[t] = s->prep.w[t];
     r.bucket_tab = nullptr;
     r.ngroups = (unsigned)decide_group_count(s->n);
-    r.row_stride = (1u << s->prep.digit_bits) + 1;
+    r.gstride = bucket_gstride(s);
     r.vals_in = s->vals[0].as<uint32_t>();
     r.vals_out = s->vals[1].as<uint32_t>();
     r.pairs = s->pair_recs.as<PairRecord>();
@@ -792,7 +797,7 @@ GatherLaunch gather_args(gpk_session* s) {
     gl.bucket_tab = s->bucket_tab.as<unsigned>();
     gl.ngroups = (unsigned)decide_group_count(s->n);
     gl.ntiles = (unsigned)s->prep.tiles;
-    gl.row_stride = (1u << s->prep.digit_bits) + 1;
+    gl.gstride = bucket_gstride(s);
     gl.tile_begin = s->grp_begin();
     gl.vals_in = s->vals[0].as<uint32_t>();
     gl.vals_out = s->vals[1].as<uint32_t>();
@@ -989,6 +994,7 @@ int alloc_slice_bufs(gpk_session* s, uint64_t cap) {
     CK(s->surv_params.ensure(cap * sizeof(CandParams)));
     CK(s->grp_table.ensure((cap / kDecideGroupSize + 2) * 12));
     CK(s->bucket_tab.ensure((cap / kDecideGroupSize + 2) * (kMaxBuckets + 1) * 4));
+    s->bucket_gs = (unsigned)(cap / kDecideGroupSize + 2);
     CK(s->cand.ensure(cap * sizeof(CandParams)));
     CK(s->cand_count.ensure(nbf * 4));
     CK(s->dirty_idx.ensure(cap * 4));

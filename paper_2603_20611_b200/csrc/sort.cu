@@ -275,17 +275,17 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherLaunch a)
     __shared__ unsigned s_ex[kGatherThreads + 1], s_b[kGatherThreads], s_wsum[2 * kGatherThreads / 32];
     __shared__ unsigned s_range[2];
     const unsigned d = blockIdx.x;
-    gather_tile_list<kGatherThreads>(a.bucket_tab, a.ngroups, a.row_stride, d, a.ntiles, a.tile_begin,
-                                     stored_pairs(a.ctrl, a.pair_cap), a.pair_cap, a.vals_in, a.vals_out, s_ex, s_b,
-                                     s_wsum, s_range);
-    const unsigned begin = s_range[0], end = min((uint64_t)s_range[1], a.pair_cap);
-    // the tile's pair records, in list order (the list is this CTA's own
-    // writes: visible after the helper's closing barrier)
+    // the tile's pair records, in list order, built as the list is copied
     const int tx = (int)(d % (unsigned)a.slice.tiles_x), ty = (int)(d / (unsigned)a.slice.tiles_x);
     const double X0 = ((double)(tx * kTile) - a.slice.ppx) * a.slice.sx;
     const double Y0 = ((double)(ty * kTile) - a.slice.ppy) * a.slice.sy;
-    for (unsigned t = begin + threadIdx.x; t < end; t += kGatherThreads)
-        store_pair_record(a.pairs + t, make_pair_record(a.records[__ldcg(&a.vals_out[t])], tx, ty, X0, Y0));
+    auto emit = [&](unsigned pos, unsigned, uint32_t slot) {
+        a.vals_out[pos] = slot;
+        store_pair_record(a.pairs + pos, make_pair_record(a.records[slot], tx, ty, X0, Y0));
+    };
+    gather_tile_list<kGatherThreads, 1>(a.bucket_tab, a.ngroups, a.gstride, d, a.ntiles, a.tile_begin,
+                                        stored_pairs(a.ctrl, a.pair_cap), a.pair_cap, a.vals_in, emit, s_ex, s_b,
+                                        s_wsum, s_range);
 }
 
 // Multi-pass slices: the pair record of every sorted position (its tile is its

@@ -1,6 +1,7 @@
 """Per-CUDA-source-line stall samples of a kernel from an ncu report (SASS
 samples mapped to lines through the cubin's line table).
-python tests/_srcline.py <rep> <kernel> <object.o> [top]"""
+python tests/_srcline.py <rep> <kernel> <object.o> [top] [inst]   (inst: weigh by warp
+instructions executed instead of stall samples)"""
 import csv
 import re
 import subprocess
@@ -9,6 +10,7 @@ from collections import defaultdict
 
 rep, kern, obj = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
+col = "Instructions Executed" if len(sys.argv) > 5 and sys.argv[5] == "inst" else "Warp Stall Sampling (All Samples)"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:(^|::){kern}(<|$|\\()",
                       "--print-source", "sass"], capture_output=True, text=True).stdout.splitlines()
 r = csv.reader(out)
@@ -23,7 +25,7 @@ for x in rows:
     seen.add(x["Address"])
     first.append(x)
 base = int(first[0]["Address"], 16)
-samp = {int(x["Address"], 16) - base: int(x["Warp Stall Sampling (All Samples)"] or 0) for x in first}
+samp = {int(x["Address"], 16) - base: int(x[col] or 0) for x in first}
 # line table of the kernel's function in the object's cubin
 cub = subprocess.run(["cuobjdump", "-xelf", "all", __import__("os").path.abspath(obj)], capture_output=True, text=True, cwd="/tmp")
 dis = subprocess.run(f"nvdisasm --print-line-info /tmp/{obj.split('/')[-1].replace('.o','')}*.cubin",

@@ -934,7 +934,8 @@ void launch_prep(const PrepLaunch& a, int num_sms, cudaStream_t st);
 // dp.cu: the data-parallel union numbering and its dense view
 void launch_union_scan(const unsigned* words, unsigned nchunks, unsigned* prefix, unsigned* uctrl, uint64_t ucap,
                        cudaStream_t st);
-void launch_union_map(const unsigned* words, const unsigned* prefix, uint32_t n, uint32_t* umap, cudaStream_t st);
+void launch_union_map(const unsigned* words, const unsigned* prefix, uint32_t n, uint32_t* umap, float* rows,
+                      uint64_t cap, uint64_t ucap, cudaStream_t st);
 void launch_union_to_dense(const uint32_t* umap, const float* rows, uint64_t cap, uint32_t n, uint64_t ucap,
                            float* grads, cudaStream_t st);
 // own / union_words: a data-parallel step (only pose `own` stores candidates;

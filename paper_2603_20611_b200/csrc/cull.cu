@@ -256,6 +256,50 @@ __device__ __forceinline__ bool quick_culled_pose(const QuickInv& q, const Filte
     return q.ok & culled;
 }
 
+// Data-parallel union over the step's poses when they share R = I, t_x,
+// t_y, PSF, tau and mod (MultiPrep::shared_quick): a superset of every pose's
+// candidates (the complement of certainly_culled_identity) from ONE evaluation
+// per Gaussian. Only the cancellation-noise term of the margin depends on the
+// pose (through mu_c,z); with |mu_c,z| bounded by its largest value over the
+// poses, margin_k <= margin_max, so pose k's candidate test implies
+//   mu_c,z,k^2 <= Q = 2 (sigma_z^2 + Sigma_c,zz) (thresh + margin_max)
+// (relative slack 1e-4 for the fp32 roundings), and the union is "some pose's
+// mu_c,z within sqrt(Q)". Identical on every rank (same parameters, same poses).
+__device__ __forceinline__ bool union_candidate(const float p[11], const FilterConsts& c,
+                                                const FilterConsts* fcs, int nb, float tz_abs_max) {
+    float sum = p[0];
+#pragma unroll
+    for (int k = 1; k < 11; ++k) sum += p[k];
+    if (!isfinite(sum)) return true;
+    const float lmax = fmaxf(p[3], fmaxf(p[4], p[5])), lmin = fminf(p[3], fminf(p[4], p[5]));
+    if (!(lmax < 40.f && lmin > -40.f && lmax - lmin < 6.2f)) return true;
+    const float qn2 = p[6] * p[6] + p[7] * p[7] + p[8] * p[8] + p[9] * p[9];
+    if (!(qn2 > 1e-20f && qn2 < 1e20f)) return true;
+    const float inv = rsqrtf(qn2);
+    const float w = p[6] * inv, x = p[7] * inv, y = p[8] * inv, z = p[9] * inv;
+    const float r0 = 2.f * (x * z - w * y), r1 = 2.f * (y * z + w * x), r2 = 1.f - 2.f * (x * x + y * y);
+    const float s0 = __expf(p[3]) * c.mod, s1 = __expf(p[4]) * c.mod, s2 = __expf(p[5]) * c.mod;
+    const float var = (s0 * r0) * (s0 * r0) + (s1 * r1) * (s1 * r1) + (s2 * r2) * (s2 * r2);
+    const float den = c.sz2 + var;
+    const float raw = p[10];
+    const float log_alpha = raw >= 0.f ? -__logf(1.f + __expf(-raw)) : raw - __logf(1.f + __expf(raw));
+    float mz = 0.f;
+    for (int k = 0; k < nb; ++k) mz = fmaxf(mz, fabsf((p[2] + fcs[k].tz_hi) + fcs[k].tz_lo));
+    const float mcx = p[0] + c.tx, mcy = p[1] + c.ty;
+    const float smin = __expf(lmin) * c.mod;
+    const float mu2 = mcx * mcx + mcy * mcy + mz * mz;
+    const float noise = 2e-14f * mu2 / (smin * smin) + 4.f * mz * 1.2e-7f * (fabsf(p[2]) + tz_abs_max) / den;
+    const float thresh = log_alpha - c.log_tau;
+    const float R = thresh + (2e-3f + 2e-5f * fabsf(thresh) + noise);
+    if (!(R >= 0.f)) return !(R < 0.f);  // every pose culls it (NaN: keep)
+    const float Q = 2.f * den * R * 1.0001f + 1e-30f;
+    for (int k = 0; k < nb; ++k) {
+        const float mcz = (p[2] + fcs[k].tz_hi) + fcs[k].tz_lo;
+        if (mcz * mcz <= Q) return true;
+    }
+    return false;
+}
+
 // ---- K_filter ------------------------------------------------------------------
 // prepare_gaussians' cull (render.hpp:107) as a streaming pass with no block
 // barriers. Warps walk 128-Gaussian chunks grid-stride; each lane owns four
@@ -580,7 +624,13 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter_multi(const __grid
     unsigned b = gtid / 32;
     if (b < nchunks) prefetch(b, 0);
     cp_async_commit();
+    __shared__ float s_tzmax;
     if (tid < m.nb) s_fc[tid] = filter_consts(m.p[tid].slice, m.log_tau[tid]);
+    if (tid == 0) {
+        float t = 0.f;
+        for (int k = 0; k < m.nb; ++k) t = fmaxf(t, fabsf((float)m.p[k].slice.t[2]));
+        s_tzmax = t;
+    }
     for (int k = 0; k < m.nb; ++k) {
         if (m.union_words && k != m.own) continue;  // verdict-only poses own no buffers
         const PrepLaunch& a = m.p[k];
@@ -599,7 +649,25 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter_multi(const __grid
 #pragma unroll
         for (int q = 0; q < 11; ++q) v[q] = *reinterpret_cast<const float4*>(st + q * kFilterBlock + lane * kFilterItems);
         unsigned umask = 0;
-        if (m.shared_quick) {
+        if (m.union_words && m.shared_quick) {
+            // the union in one evaluation per Gaussian; only the rank's own
+            // pose runs the cull with its candidate emission
+            // (one pose: the union is the pose's own candidates)
+            const FilterConsts& fo = s_fc[m.own];
+            unsigned qmask = 0;
+#pragma unroll
+            for (int it2 = 0; it2 < kFilterItems; ++it2) {
+                float p[11];
+#pragma unroll
+                for (int q = 0; q < 11; ++q) p[q] = (&v[q].x)[it2];
+                qmask |= (quick_culled_pose(quick_invariant(p, fo), fo) ? 1u : 0u) << it2;
+                if (m.nb > 1)
+                    umask |= (i0 + it2 < a0.n && union_candidate(p, fo, s_fc, m.nb, s_tzmax) ? 1u : 0u) << it2;
+            }
+            const unsigned own = cull_chunk(m.p[m.own], fo, m.log_tau[m.own], m.filter_on[m.own], b, i0, v, sx,
+                                            nullptr, st, (int)qmask, true);
+            if (m.nb == 1) umask = own;
+        } else if (m.shared_quick) {
             QuickInv qi[kFilterItems];
 #pragma unroll
             for (int it2 = 0; it2 < kFilterItems; ++it2) {

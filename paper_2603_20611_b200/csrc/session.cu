@@ -2493,11 +2493,14 @@ static int dp_union_allreduce(gpk_session* s);
 // Buffers of the union exchange (sized by the plane stride; outside capture).
 static int dp_union_alloc(gpk_session* s) {
     const void* before[3] = {s->union_words.p, s->umap.p, s->urows.p};
-    CK(s->union_words.ensure(filter_blocks(s->cap) * kFilterItems * 4));
-    CK(s->union_prefix.ensure(filter_blocks(s->cap) * 4));
+    const uint64_t fb = filter_blocks(s->cap);
+    CK(s->union_words.ensure(fb * kFilterItems * 4));
+    CK(s->union_prefix.ensure((fb + 2 * (fb / 1024 + 1)) * 4));  // chunk prefixes, block totals, block offsets
     CK(s->umap.ensure(s->cap * 4));
     CK(s->urows.ensure(s->cap * 44));
-    CK(s->uctrl.ensure(16));
+    const void* uc = s->uctrl.p;
+    CK(s->uctrl.ensure(16));  // M, overflow, the scan's ticket
+    if (uc != s->uctrl.p) CK(cudaMemsetAsync(s->uctrl.p, 0, 16, s->stream));
     if (before[0] != s->union_words.p || before[1] != s->umap.p || before[2] != s->urows.p) {
         if (s->capturing) return fail(GPK_ERR_STATE, "union buffers must be sized before capture");
         ++s->alloc_epoch;
@@ -2539,7 +2542,7 @@ static int train_dp_body(gpk_session* s, int world, int rank, const gpk_slice_po
                                   s->union_prefix.as<unsigned>(), s->uctrl.as<unsigned>(), s->ucap, s->stream);
                 CK(cudaGetLastError());
                 launch_union_map(s->union_words.as<unsigned>(), s->union_prefix.as<unsigned>(), (uint32_t)s->n,
-                                 s->umap.as<uint32_t>(), s->stream);
+                                 s->umap.as<uint32_t>(), s->urows.as<float>(), s->cap, s->ucap, s->stream);
                 CK(cudaGetLastError());
             }
             if (!s->capturing) {
@@ -2551,10 +2554,16 @@ static int train_dp_body(gpk_session* s, int world, int rank, const gpk_slice_po
                 if (u[1]) {
                     s->ucap = std::min<uint64_t>(s->cap, (uint64_t)u[0] + u[0] / 4 + 1024);
                     CK(cudaMemsetAsync(s->uctrl.as<unsigned>() + 1, 0, 4, s->stream));
+                    // (k_union_map cleared the old capacity's rows only)
+                    for (int k = 0; k < 11; ++k)
+                        CK(cudaMemsetAsync(s->urows.as<float>() + (size_t)k * s->cap, 0, s->ucap * 4, s->stream));
+                } else if (2 * (uint64_t)u[0] + 2048 < s->ucap) {
+                    // far below the capacity: shrink it (the all-reduce count and
+                    // the rows' clearing scale with it; graphs are recaptured)
+                    s->ucap = std::min<uint64_t>(s->cap, (uint64_t)u[0] + u[0] / 4 + 1024);
+                    ++s->alloc_epoch;
                 }
             }
-            for (int k = 0; k < 11; ++k)
-                CK(cudaMemsetAsync(s->urows.as<float>() + (size_t)k * s->cap, 0, s->ucap * 4, s->stream));
         }
         s->fuse_gather = s->fuse_gather_ok;
         const int pst = run_prepare(s, &poses[rank], psf, cfg, false, /*filtered=*/s->n != 0);

@@ -329,6 +329,51 @@ __device__ __forceinline__ void adam_update(const AdamLaunch& a, const AdamConst
 // As adam_update + adam_store, storing each plane's parameters as soon as they
 // are final (all but the quaternion, renormalised at the end): few registers
 // live, so the stand-alone kernel runs at full occupancy. Same bits.
+// Software-pipelined form (GPK_ADAM_PIPE): the next plane's parameter,
+// moments and gradient are requested before this plane's arithmetic, so two
+// planes' loads are in flight per thread. The same operations in the same
+// order per element: the same bits.
+template <int N, typename G>
+__device__ __forceinline__ void adam_update_store_pipe(const AdamLaunch& a, const AdamConsts& c, uint32_t i0,
+                                                       const G& grad) {
+    constexpr int kOrder[11] = {0, 1, 2, 3, 4, 5, 10, 6, 7, 8, 9};
+    Pack<N> m[2], v[2], p[2], g[2], q[4];
+    auto fetch = [&](int j, int b) {
+        const uint64_t o = (uint64_t)kOrder[j] * a.cap + i0;
+        m[b] = ldp_stream<N>(a.m + o);
+        v[b] = ldp_stream<N>(a.v + o);
+        p[b] = ldp_stream<N>(a.params + o);
+        g[b] = grad(kOrder[j]);
+    };
+    fetch(0, 0);
+#pragma unroll
+    for (int j = 0; j < 11; ++j) {
+        const int b = j & 1, k = kOrder[j];
+        if (j + 1 < 11) fetch(j + 1, b ^ 1);
+        const float lr = k < 3 ? c.lr[0] : (k < 6 ? c.lr[2] : (k == 10 ? c.lr[1] : c.lr[3]));
+        const float lrc = __fmul_rn(lr, c.ibc1);
+#pragma unroll
+        for (int l = 0; l < N; ++l) adam_elem(c, lrc, p[b].v[l], m[b].v[l], v[b].v[l], g[b].v[l]);
+        const uint64_t o = (uint64_t)k * a.cap + i0;
+        stp_stream<N>(a.m + o, m[b]);
+        stp_stream<N>(a.v + o, v[b]);
+        if (k < 3) {
+            const float lo = a.bbox_min[k], hi = a.bbox_max[k];
+#pragma unroll
+            for (int l = 0; l < N; ++l) p[b].v[l] = fminf(hi, fmaxf(lo, p[b].v[l]));
+        }
+        if (k >= 6 && k <= 9) {
+            q[k - 6] = p[b];
+        } else {
+            stp_stream<N>(a.params + o, p[b]);
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < N; ++l) adam_renorm(q[0].v[l], q[1].v[l], q[2].v[l], q[3].v[l]);
+#pragma unroll
+    for (int d = 0; d < 4; ++d) stp_stream<N>(a.params + (uint64_t)(6 + d) * a.cap + i0, q[d]);
+}
+
 template <int N, typename G>
 __device__ __forceinline__ void adam_update_store_g(const AdamLaunch& a, const AdamConsts& c, uint32_t i0,
                                                     const G& grad) {

@@ -89,12 +89,17 @@ def main():
         s.synchronize()
         return s
 
-    # t_1: the single-GPU U2 step (bench.py's path: one graph per pose)
-    s = new_session(False)
-    graphs = [s.capture_train(p, psf, rcfg, bench.LAMBDA, 0.5, lr0, bench.TOTAL_ITERS) for p in poses]
-    t1, t1_med = timed(s, lambda k: s.graph_launch(graphs[k]), len(poses))
-    s.graph_destroy_all()
-    s.close()
+    # t_1: the single-GPU U2 step (bench.py's path: one graph per pose);
+    # measured twice (the first run also warms the GPU up), the faster kept
+    def single():
+        s = new_session(False)
+        graphs = [s.capture_train(p, psf, rcfg, bench.LAMBDA, 0.5, lr0, bench.TOTAL_ITERS) for p in poses]
+        t, _ = timed(s, lambda k: s.graph_launch(graphs[k]), len(poses))
+        s.graph_destroy_all()
+        s.close()
+        return t
+
+    t1 = min(single(), single())
     out["single_gpu_u2_ms"] = t1
     for W in [int(w) for w in args.worlds.split(",")]:
         s = new_session(True)

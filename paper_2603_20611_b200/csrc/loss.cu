@@ -80,9 +80,13 @@ __global__ void __launch_bounds__(256) k_l1_only(const LossLaunch a) {
 
 __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const LossLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
-    __shared__ float s_x[kH][kH + 1];
-    __shared__ float s_y[kH][kH + 1];
-    __shared__ float s_h[5][kH][kT + 1];
+    // (x, y) and the moment pairs interleaved, so the filters run on packed
+    // fp32 pairs (FFMA2: two moments per instruction, each rounded as a scalar
+    // FFMA)
+    __shared__ float2 s_xy[kH][kH + 1];
+    __shared__ float2 s_m1[kH][kT + 1];  // (W x, W y) along rows
+    __shared__ float2 s_m2[kH][kT + 1];  // (W xx, W yy)
+    __shared__ float s_m3[kH][kT + 1];   // W xy
     __shared__ double s_red[2 * 32];
     const int X0 = blockIdx.x * kT, Y0 = blockIdx.y * kT;
     const int W = a.W, H = a.H;
@@ -104,41 +108,35 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const LossLaunch a) {
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const int idx = threadIdx.x + k * kSsimThreads;
-            if (idx < kH * kH) {
-                s_x[idx / kH][idx % kH] = vx[k];
-                s_y[idx / kH][idx % kH] = vy[k];
-            }
+            if (idx < kH * kH) s_xy[idx / kH][idx % kH] = make_float2(vx[k], vy[k]);
         }
     }
     __syncthreads();
     // rows (axis 0 of conv_nd, metrics.hpp:112-116): a thread filters 4
     // consecutive outputs from 14 samples in registers (each output still sums
-    // its 11 taps in order)
+    // its 11 taps in order): per tap (W x, W y) by one FFMA2, the products
+    // (w x, w y) by one FMUL2, (W xx, W yy) by one FFMA2 on them, W xy by FFMA
     for (int item = threadIdx.x; item < kH * (kT / 4); item += blockDim.x) {
         const int r = item / (kT / 4), c0 = (item % (kT / 4)) * 4;
-        float x[4 + 2 * kR], y[4 + 2 * kR];
+        float2 xy[4 + 2 * kR];
 #pragma unroll
-        for (int t = 0; t < 4 + 2 * kR; ++t) {
-            x[t] = s_x[r][c0 + t];
-            y[t] = s_y[r][c0 + t];
-        }
+        for (int t = 0; t < 4 + 2 * kR; ++t) xy[t] = s_xy[r][c0 + t];
 #pragma unroll
         for (int o = 0; o < 4; ++o) {
-            float hx = 0.f, hy = 0.f, hxx = 0.f, hxy = 0.f, hyy = 0.f;
+            f32x2 h1 = f2(0.f, 0.f), h2 = h1;
+            float h3 = 0.f;
 #pragma unroll
             for (int t = 0; t < 2 * kR + 1; ++t) {
-                const float xv = x[o + t], yv = y[o + t], w = a.w[t];
-                hx += w * xv;
-                hy += w * yv;
-                hxx += w * xv * xv;
-                hxy += w * xv * yv;
-                hyy += w * yv * yv;
+                const float w = a.w[t];
+                const f32x2 v = f2(xy[o + t]);
+                h1 = ffma2(f2(w, w), v, h1);
+                const f32x2 wv = fmul2(f2(w, w), v);
+                h2 = ffma2(wv, v, h2);
+                h3 = fmaf(f2_unpack(wv).x, xy[o + t].y, h3);
             }
-            s_h[0][r][c0 + o] = hx;
-            s_h[1][r][c0 + o] = hy;
-            s_h[2][r][c0 + o] = hxx;
-            s_h[3][r][c0 + o] = hxy;
-            s_h[4][r][c0 + o] = hyy;
+            s_m1[r][c0 + o] = f2_unpack(h1);
+            s_m2[r][c0 + o] = f2_unpack(h2);
+            s_m3[r][c0 + o] = h3;
         }
     }
     __syncthreads();
@@ -150,17 +148,22 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const LossLaunch a) {
         const int c = threadIdx.x % kT, r0 = (threadIdx.x / kT) * 2;
         float m[2][5];
 #pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            float v[2 + 2 * kR];
+        for (int o = 0; o < 2; ++o) {
+            f32x2 a1 = f2(0.f, 0.f), a2 = a1;
+            float a3 = 0.f;
 #pragma unroll
-            for (int t = 0; t < 2 + 2 * kR; ++t) v[t] = s_h[q][r0 + t][c];
-#pragma unroll
-            for (int o = 0; o < 2; ++o) {
-                float acc = 0.f;
-#pragma unroll
-                for (int t = 0; t < 2 * kR + 1; ++t) acc += a.w[t] * v[o + t];
-                m[o][q] = acc;
+            for (int t = 0; t < 2 * kR + 1; ++t) {
+                const float w = a.w[t];
+                a1 = ffma2(f2(w, w), f2(s_m1[r0 + o + t][c]), a1);
+                a2 = ffma2(f2(w, w), f2(s_m2[r0 + o + t][c]), a2);
+                a3 = fmaf(w, s_m3[r0 + o + t][c], a3);
             }
+            const float2 u1 = f2_unpack(a1), u2 = f2_unpack(a2);
+            m[o][0] = u1.x;
+            m[o][1] = u1.y;
+            m[o][2] = u2.x;
+            m[o][3] = a3;
+            m[o][4] = u2.y;
         }
 #pragma unroll
         for (int o = 0; o < 2; ++o) {
@@ -185,7 +188,8 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const LossLaunch a) {
             a.g[P + off] = (float)(ds_dm2 * inv_n);
             a.g[2 * P + off] = (float)(ds_dm12 * inv_n);
             ssum += s;
-            l1 += fabs((double)(s_x[r + kR][c + kR] - s_y[r + kR][c + kR]));
+            const float2 px = s_xy[r + kR][c + kR];
+            l1 += fabs((double)(px.x - px.y));
         }
     }
     block_sum2(ssum, l1, s_red);

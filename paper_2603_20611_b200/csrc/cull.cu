@@ -256,6 +256,25 @@ __device__ __forceinline__ bool quick_culled_pose(const QuickInv& q, const Filte
     return q.ok & culled;
 }
 
+// The quick bound for every pose of the step at once (a conservative "culled
+// by every pose", so the union test runs only near the poses): the noise term
+// bounded with the largest |mu_c,z| over the poses (at the smallest or the
+// largest t_z), x_up with it (x_up grows with the noise), and the smallest
+// |mu_c,z| by the hull [mu_c,z(t_z min), mu_c,z(t_z max)] (0 inside it).
+__device__ __forceinline__ bool quick_culled_all(const QuickInv& q, const FilterConsts& c, const FilterConsts& lo,
+                                                 const FilterConsts& hi, float tz_abs_max) {
+    const float z0 = (q.p2 + lo.tz_hi) + lo.tz_lo, z1 = (q.p2 + hi.tz_hi) + hi.tz_lo;
+    const float mz = fmaxf(fabsf(z0), fabsf(z1)) * 1.00001f;
+    const float dmin = (z0 <= 0.f && z1 >= 0.f) ? 0.f : fminf(fabsf(z0), fabsf(z1)) * 0.99999f;
+    const float mu2 = __fmaf_rn(q.mcx, q.mcx, __fmaf_rn(q.mcy, q.mcy, mz * mz));
+    const float noise = __fmaf_rn(2e-14f * mu2, q.inv_smin2,
+                                  4.8e-7f * mz * (q.ap2 + tz_abs_max) * c.inv_sz2 * 1.0002f);
+    const float x = q.thr + (2e-3f + __fmaf_rn(2e-5f, fabsf(q.thr) + 0.7f, noise));
+    const float x_up = __fmaf_rn(1e-3f, fabsf(x) + noise, x) + 1e-6f;
+    const bool culled = 0.5f * dmin * dmin * 0.9999f > x_up * (x_up >= 0.f ? q.den_hi : c.sz2);
+    return q.ok & culled;
+}
+
 // Data-parallel union over the step's poses when they share R = I, t_x,
 // t_y, PSF, tau and mod (MultiPrep::shared_quick): a superset of every pose's
 // candidates (the complement of certainly_culled_identity) from ONE evaluation
@@ -625,11 +644,19 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter_multi(const __grid
     if (b < nchunks) prefetch(b, 0);
     cp_async_commit();
     __shared__ float s_tzmax;
+    __shared__ int s_kmin, s_kmax;  // the poses with the smallest / largest t_z (the hull of mu_c,z)
     if (tid < m.nb) s_fc[tid] = filter_consts(m.p[tid].slice, m.log_tau[tid]);
     if (tid == 0) {
         float t = 0.f;
-        for (int k = 0; k < m.nb; ++k) t = fmaxf(t, fabsf((float)m.p[k].slice.t[2]));
+        int kmin = 0, kmax = 0;
+        for (int k = 0; k < m.nb; ++k) {
+            t = fmaxf(t, fabsf((float)m.p[k].slice.t[2]));
+            if (m.p[k].slice.t[2] < m.p[kmin].slice.t[2]) kmin = k;
+            if (m.p[k].slice.t[2] > m.p[kmax].slice.t[2]) kmax = k;
+        }
         s_tzmax = t;
+        s_kmin = kmin;
+        s_kmax = kmax;
     }
     for (int k = 0; k < m.nb; ++k) {
         if (m.union_words && k != m.own) continue;  // verdict-only poses own no buffers
@@ -654,15 +681,58 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter_multi(const __grid
             // pose runs the cull with its candidate emission
             // (one pose: the union is the pose's own candidates)
             const FilterConsts& fo = s_fc[m.own];
-            unsigned qmask = 0;
+            unsigned qmask = 0, need = 0;
 #pragma unroll
             for (int it2 = 0; it2 < kFilterItems; ++it2) {
                 float p[11];
 #pragma unroll
                 for (int q = 0; q < 11; ++q) p[q] = (&v[q].x)[it2];
-                qmask |= (quick_culled_pose(quick_invariant(p, fo), fo) ? 1u : 0u) << it2;
-                if (m.nb > 1)
-                    umask |= (i0 + it2 < a0.n && union_candidate(p, fo, s_fc, m.nb, s_tzmax) ? 1u : 0u) << it2;
+                const QuickInv qi = quick_invariant(p, fo);
+                qmask |= (quick_culled_pose(qi, fo) ? 1u : 0u) << it2;
+                if (m.nb > 1 && i0 + it2 < a0.n && !quick_culled_all(qi, fo, s_fc[s_kmin], s_fc[s_kmax], s_tzmax))
+                    need |= 1u << it2;
+            }
+            if (m.nb > 1) {
+                // the items the all-pose quick bound cannot cull take the union
+                // test compacted across the warp (a few per chunk: one round of
+                // 32 instead of every item slot of every lane)
+                const unsigned nn = __popc(need);
+                unsigned incl = nn;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += u;
+                }
+                const unsigned U = __shfl_sync(0xffffffffu, incl, 31);
+                if (U) {
+                    unsigned pos = incl - nn;
+#pragma unroll
+                    for (int it2 = 0; it2 < kFilterItems; ++it2)
+                        if (need & (1u << it2)) sx.idx[pos++] = (uint8_t)(lane * kFilterItems + it2);
+                    __syncwarp();
+                    for (unsigned r = 0; r * 32 < U; ++r) {
+                        const unsigned e = r * 32 + lane;
+                        bool in = false;
+                        if (e < U) {
+                            const unsigned j = sx.idx[e];
+                            float p[11];
+#pragma unroll
+                            for (int q = 0; q < 11; ++q) p[q] = st[q * kFilterBlock + j];
+                            in = union_candidate(p, fo, s_fc, m.nb, s_tzmax);
+                        }
+                        const unsigned bal = __ballot_sync(0xffffffffu, in);
+                        if (lane == 0) sx.res[r] = bal;
+                    }
+                    __syncwarp();
+                    pos = incl - nn;
+#pragma unroll
+                    for (int it2 = 0; it2 < kFilterItems; ++it2)
+                        if (need & (1u << it2)) {
+                            if ((sx.res[pos >> 5] >> (pos & 31)) & 1u) umask |= 1u << it2;
+                            ++pos;
+                        }
+                    __syncwarp();  // the scratch is reused by the cull below
+                }
             }
             const unsigned own = cull_chunk(m.p[m.own], fo, m.log_tau[m.own], m.filter_on[m.own], b, i0, v, sx,
                                             nullptr, st, (int)qmask, true);

@@ -553,6 +553,14 @@ def run_ours(args):
         c = sess.context(k)
         c.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
         c.upload(N.GPK_BUF_DL_DI, dl.ctypes.data, dl.nbytes)
+    # u2, one slice per step: two target slots (gpk_set_target_slot), graph k
+    # reading slot k mod 2 (the poses cycle with an even period), so a step's
+    # target upload never waits for the previous step's last target reader
+    slots = u2 and B == 1
+    if slots:
+        for k in (1, 0):
+            sess.set_target_slot(k)
+            sess.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
     # u2: every slice context's loss kernel writes its loss straight into this
     # pinned host array (gpk_set_loss_sink): the step's result reaches the host
     # inside the step, no separate read-back copy (set before any capture)
@@ -604,6 +612,8 @@ def run_ours(args):
 
     def capture(k, nb=None):
         nb = nb or B
+        if slots and (nb or B) == 1:
+            sess.set_target_slot(k % 2)
         if dp_union:
             return sess.capture_train_dp(world, rank, step_poses(k), psf, rcfg, LAMBDA, 0.5, lr0, TOTAL_ITERS)
         if nb > 1:
@@ -745,6 +755,9 @@ def run_ours(args):
         pin_loss = torch.empty(B, dtype=torch.float64).pin_memory()
 
         def e2e_step(i, down=False):
+            if slots:  # the slot graph k reads (k = the step's pose group)
+                k = i % n_groups if dp_union else dp.slice_for(i, rank, world, n_groups)
+                sess.set_target_slot(k % 2)
             for b in range(B):
                 ctxs[b].upload(N.GPK_BUF_TARGET, pin_tgt[b].data_ptr(), P * 4)
             step(i)

@@ -261,6 +261,14 @@ int gpk_fwd_bwd_slice(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf*
  * the kernel ends, with no separate device-to-host copy. NULL: off. Graphs
  * captured before a change must be recaptured. */
 int gpk_set_loss_sink(gpk_session* s, double* host);
+/* Target slots (0 or 1; 0 by default): GPK_BUF_TARGET uploads and downloads,
+ * and every later loss evaluation (direct or captured into a graph), use the
+ * selected slot's buffer. A caller that alternates slots step by step (and
+ * captures its graphs with the matching slot) lets the next slice's target
+ * upload run while the previous step still reads the other buffer, instead
+ * of after it: the copy no longer waits for the previous step's last target
+ * reader. Selecting slot 1 the first time allocates it (image-sized). */
+int gpk_set_target_slot(gpk_session* s, int32_t slot);
 /* Lazy mode (off by default; measured slower on B200): single-GPU
  * U2 steps run "lazily": Adam updates the slice's
  * survivors and one 1/16 window of the set per step; every other Gaussian's

@@ -170,6 +170,7 @@ _PROTOS = {
     "gpk_stage_timing": (C.c_int, [_P, C.c_int]),
     "gpk_set_lazy_adam": (C.c_int, [_P, C.c_int]),
     "gpk_set_loss_sink": (C.c_int, [_P, C.c_void_p]),
+    "gpk_set_target_slot": (C.c_int, [_P, C.c_int32]),
     "gpk_stage_times": (C.c_int, [_P, _D, _U64, C.c_int]),
     "gpk_set_gaussians": (C.c_int, [_P, C.c_uint64, _F, C.POINTER(Bounds)]),
     "gpk_set_gaussians_f64": (C.c_int, [_P, C.c_uint64, _D, C.POINTER(Bounds)]),

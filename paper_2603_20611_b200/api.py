@@ -405,6 +405,12 @@ class Session:
         address (include/gpile_b200.h gpk_set_loss_sink); None: off."""
         check(N.lib.gpk_set_loss_sink(self._h, C.c_void_p(host_ptr or None)))
 
+    def set_target_slot(self, slot: int):
+        """Select target buffer 0 or 1 for later uploads and losses (include/
+        gpile_b200.h gpk_set_target_slot): alternating slots lets the next
+        slice's target upload overlap the previous step entirely."""
+        check(N.lib.gpk_set_target_slot(self._h, int(slot)))
+
     def set_lazy_adam(self, on: bool = True):
         """Lazy single-GPU training steps (include/gpile_b200.h gpk_set_lazy_adam;
         off by default, measured slower): deferred zero-gradient Adam steps,

@@ -122,19 +122,25 @@ struct gpk_session {
     // slice targets are uploaded on their own stream and overlap the step's
     // prepare + forward; the loss waits on ev_tgt_ready (see gpk_upload)
     cudaStream_t copy = nullptr;
-    cudaEvent_t ev_tgt_fork = nullptr, ev_tgt_ready = nullptr;
+    cudaEvent_t ev_tgt_fork = nullptr;
+    // two target slots (gpk_set_target_slot): a step reads the current slot's
+    // buffer, so a caller alternating slots uploads the next slice's target
+    // while the previous step still reads the other one; each slot has its own
+    // upload-done (ev_tgt_ready) and last-reader (ev_tgt_free) events
+    int tgt_slot = 0;
+    cudaEvent_t ev_tgt_ready_k[2] = {nullptr, nullptr};
     // recorded after the last kernel that reads the target (the loss, or the
     // raster backward that finishes the SSIM gradient): the next upload's copy
     // starts there, overlapping the rest of the step (chain, Adam) and the next
     // step's prepare and forward
-    cudaEvent_t ev_tgt_free = nullptr;
+    cudaEvent_t ev_tgt_free_k[2] = {nullptr, nullptr};
     // under capture the release is a side branch (a record node on its own
     // stream, joined at the end of the graph) so the PDL edge from the raster
     // backward to the chain stays programmatic
     cudaStream_t rel_stream = nullptr;
     cudaEvent_t ev_rel_fork = nullptr, ev_rel_join = nullptr;
     bool rel_join_pending = false;
-    bool tgt_pending = false;
+    bool tgt_pending_k[2] = {false, false};
     // data parallelism (gpk_comm_init): this session's NCCL communicator
     void* comm = nullptr;
     int comm_rank = 0, comm_world = 1;
@@ -212,7 +218,11 @@ struct gpk_session {
     AdamConsts* lazy_ring() { return reinterpret_cast<AdamConsts*>(persist.as<char>() + 256); }
     unsigned* lazy_bad() { return reinterpret_cast<unsigned*>(persist.as<char>() + 256 + kLazyRing * sizeof(AdamConsts)); }
     DevBuf persist;    // ErrorState | epoch | adam step | adam done ctr | loss done ctr | loss
-    DevBuf image, dl_di, target, loss_g, loss_partial;
+    DevBuf image, dl_di, target_k[2], loss_g, loss_partial;
+    DevBuf& tgt() { return target_k[tgt_slot]; }
+    cudaEvent_t& ev_tgt_ready() { return ev_tgt_ready_k[tgt_slot]; }
+    cudaEvent_t& ev_tgt_free() { return ev_tgt_free_k[tgt_slot]; }
+    bool& tgt_pending() { return tgt_pending_k[tgt_slot]; }
     DevBuf stat_norm, stat_obs, stat_world;
     // DensifyAccum (optimize.hpp:228-249), accumulated by every backward's
     // chain while enabled (gpk_densify_accum_enable)
@@ -470,12 +480,17 @@ int ensure_tile_start(gpk_session* s, uint64_t tiles) {
 
 int ensure_image(gpk_session* s, int w, int h) {
     const size_t px = (size_t)w * h;
-    if (s->copy && px * 4 > s->target.bytes) CK(cudaStreamSynchronize(s->copy));  // no copy into a freed buffer
-    const void* before[3] = {s->image.p, s->dl_di.p, s->target.p};
+    if (s->copy && (px * 4 > s->target_k[0].bytes || (s->target_k[1].p && px * 4 > s->target_k[1].bytes)))
+        CK(cudaStreamSynchronize(s->copy));  // no copy into a freed buffer
+    const void* before[3] = {s->image.p, s->dl_di.p, s->tgt().p};
     CK(s->image.ensure(px * 4));
     CK(s->dl_di.ensure(px * 4));
-    CK(s->target.ensure(px * 4));
-    if (before[0] != s->image.p || before[1] != s->dl_di.p || before[2] != s->target.p) ++s->alloc_epoch;
+    CK(s->tgt().ensure(px * 4));
+    const void* other = s->target_k[s->tgt_slot ^ 1].p;
+    if (other) CK(s->target_k[s->tgt_slot ^ 1].ensure(px * 4));
+    if (before[0] != s->image.p || before[1] != s->dl_di.p || before[2] != s->tgt().p ||
+        other != s->target_k[s->tgt_slot ^ 1].p)
+        ++s->alloc_epoch;
     s->img_w = w;
     s->img_h = h;
     return GPK_OK;
@@ -778,7 +793,7 @@ RasterLaunch raster_args(gpk_session* s) {
     r.partials = s->partials.as<float>();
     r.slice = s->prep.slice;
     r.ssim_g = s->prep.ssim_pending ? s->loss_g.as<float>() : nullptr;
-    r.target = s->target.as<float>();
+    r.target = s->tgt().as<float>();
     r.ssim_k = s->prep.ssim_k;
     r.inv_n = s->prep.inv_n;
     for (int t = 0; t < 11; ++t) r.w[t] = s->prep.w[t];
@@ -1249,12 +1264,12 @@ int run_adam_cull(gpk_session* s, const double lr[4], int total, const gpk_slice
 // event node: resolved at each launch against the latest upload).
 int target_wait(gpk_session* s) {
     if (s->capturing) {
-        CK(cudaStreamWaitEvent(s->stream, s->ev_tgt_ready, cudaEventWaitExternal));
+        CK(cudaStreamWaitEvent(s->stream, s->ev_tgt_ready(), cudaEventWaitExternal));
         return GPK_OK;
     }
-    if (s->tgt_pending) {
-        CK(cudaStreamWaitEvent(s->stream, s->ev_tgt_ready, 0));
-        s->tgt_pending = false;
+    if (s->tgt_pending()) {
+        CK(cudaStreamWaitEvent(s->stream, s->ev_tgt_ready(), 0));
+        s->tgt_pending() = false;
     }
     return GPK_OK;
 }
@@ -1263,12 +1278,12 @@ int target_wait(gpk_session* s) {
 // completes (an external record node under capture: each launch re-records it).
 int target_release(gpk_session* s) {
     if (!s->capturing) {
-        CK(cudaEventRecord(s->ev_tgt_free, s->stream));
+        CK(cudaEventRecord(s->ev_tgt_free(), s->stream));
         return GPK_OK;
     }
     CK(cudaEventRecord(s->ev_rel_fork, s->stream));
     CK(cudaStreamWaitEvent(s->rel_stream, s->ev_rel_fork, 0));
-    CK(cudaEventRecordWithFlags(s->ev_tgt_free, s->rel_stream, cudaEventRecordExternal));
+    CK(cudaEventRecordWithFlags(s->ev_tgt_free(), s->rel_stream, cudaEventRecordExternal));
     CK(cudaEventRecord(s->ev_rel_join, s->rel_stream));
     s->rel_join_pending = true;
     return GPK_OK;
@@ -1287,7 +1302,7 @@ int run_loss(gpk_session* s, double lambda, double dssim_scale, bool fuse_into_b
     }
     LossLaunch l;
     l.image = s->image.as<float>();
-    l.target = s->target.as<float>();
+    l.target = s->tgt().as<float>();
     l.dl_di = s->dl_di.as<float>();
     l.g = s->loss_g.as<float>();
     l.partial = s->loss_partial.as<double>();
@@ -1514,8 +1529,10 @@ int gpk_session_create(int device, void* cuda_stream, gpk_session** out) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_xjoin, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->copy, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_fork, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_ready, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_free, cudaEventDisableTiming);
+    for (int k = 0; k < 2; ++k) {
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_ready_k[k], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_tgt_free_k[k], cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_rel_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_rel_join, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->rel_stream, cudaStreamNonBlocking);
@@ -1561,7 +1578,7 @@ static int session_destroy(gpk_session* s) {
     DevBuf* bufs[] = {&s->params, &s->grads, &s->adam_m, &s->adam_v, &s->records, &s->survivors,
                       &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials, &s->pair_recs, &s->tile_start,
                       &s->sort_status, &s->head, &s->persist, &s->image,
-                      &s->dl_di, &s->target, &s->loss_g, &s->loss_partial, &s->stat_norm, &s->acc_norm, &s->acc_obs, &s->acc_world,
+                      &s->dl_di, &s->target_k[0], &s->target_k[1], &s->loss_g, &s->loss_partial, &s->stat_norm, &s->acc_norm, &s->acc_obs, &s->acc_world,
                       &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table, &s->bucket_tab,
                       &s->dirty_idx, &s->vox_records, &s->slot_grads, &s->gmap, &s->union_words,
                       &s->union_prefix, &s->umap, &s->urows, &s->uctrl, &s->surv_bits,
@@ -1584,8 +1601,10 @@ static int session_destroy(gpk_session* s) {
         cudaStreamDestroy(s->copy);
     }
     if (s->ev_tgt_fork) cudaEventDestroy(s->ev_tgt_fork);
-    if (s->ev_tgt_ready) cudaEventDestroy(s->ev_tgt_ready);
-    if (s->ev_tgt_free) cudaEventDestroy(s->ev_tgt_free);
+    for (int k = 0; k < 2; ++k) {
+        if (s->ev_tgt_ready_k[k]) cudaEventDestroy(s->ev_tgt_ready_k[k]);
+        if (s->ev_tgt_free_k[k]) cudaEventDestroy(s->ev_tgt_free_k[k]);
+    }
     if (s->ev_rel_fork) cudaEventDestroy(s->ev_rel_fork);
     if (s->ev_rel_join) cudaEventDestroy(s->ev_rel_join);
     if (s->rel_stream) {
@@ -1672,7 +1691,7 @@ int gpk_device_buffer(gpk_session* s, int which, void** ptr, uint64_t* bytes) {
         case GPK_BUF_TARGET:
             TRY(target_wait(s));
             if (!s->capturing) TRY(target_release(s));  // (the caller may use it until the next upload)
-            p = s->target.p;
+            p = s->tgt().p;
             b = px * 4;
             break;
         case GPK_BUF_LOSS: p = s->loss(); b = 8; break;
@@ -1706,7 +1725,7 @@ static int ctx_order_out(gpk_session* s, cudaStream_t copied_on) {
 int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes) {
     if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
     // image-shaped inputs may be staged before the first slice sized them
-    DevBuf* grow = which == GPK_BUF_DL_DI ? &s->dl_di : which == GPK_BUF_TARGET ? &s->target
+    DevBuf* grow = which == GPK_BUF_DL_DI ? &s->dl_di : which == GPK_BUF_TARGET ? &s->tgt()
                  : which == GPK_BUF_DL_DV ? &s->dl_dv_vol : nullptr;
     if (grow && host && bytes > grow->bytes) {
         TRY(set_device(s));
@@ -1726,10 +1745,10 @@ int gpk_upload(gpk_session* s, int which, const void* host, uint64_t bytes) {
         // on the copy stream, after the last queued reader of the target
         // (ev_tgt_free): the transfer overlaps the rest of the step that read
         // it and the next step's prepare and forward, which do not read it
-        CK(cudaStreamWaitEvent(s->copy, s->ev_tgt_free, 0));
+        CK(cudaStreamWaitEvent(s->copy, s->ev_tgt_free(), 0));
         CK(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, s->copy));
-        CK(cudaEventRecord(s->ev_tgt_ready, s->copy));
-        s->tgt_pending = true;
+        CK(cudaEventRecord(s->ev_tgt_ready(), s->copy));
+        s->tgt_pending() = true;
         return ok();
     }
     CK(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, s->stream));
@@ -1746,6 +1765,23 @@ int gpk_download(gpk_session* s, int which, void* host, uint64_t bytes) {
     TRY(ctx_order_in(s));
     CK(cudaMemcpyAsync(host, p, bytes, cudaMemcpyDeviceToHost, s->stream));
     TRY(ctx_order_out(s, s->stream));
+    return ok();
+}
+
+int gpk_set_target_slot(gpk_session* s, int32_t slot) {
+    if (!s) return fail(GPK_ERR_INVALID_ARGUMENT, "null session");
+    if (slot != 0 && slot != 1) return fail(GPK_ERR_INVALID_ARGUMENT, "target slot must be 0 or 1");
+    if (s->capturing) return fail(GPK_ERR_STATE, "target slot: select it before the capture");
+    TRY(set_device(s));
+    DevBuf& b = s->target_k[slot];
+    const size_t px = (size_t)s->img_w * s->img_h;
+    if (px && b.bytes < px * 4) {
+        const void* before = b.p;
+        CK(cudaStreamSynchronize(s->copy));
+        CK(b.ensure(px * 4));
+        if (before) ++s->alloc_epoch;  // (a first allocation: no graph holds it yet)
+    }
+    s->tgt_slot = slot;
     return ok();
 }
 
@@ -2045,7 +2081,7 @@ int gpk_photometric_loss(gpk_session* s, const float* target, double lambda, dou
     // overflowed is re-prepared and re-rendered before the loss reads it)
     if ((loss_out || dl_di_out) && s->prep.valid && s->prep.rasterized) TRY(settle_pairs(s));
     TRY(target_wait(s));
-    if (target) CK(cudaMemcpyAsync(s->target.p, target, px * 4, cudaMemcpyHostToDevice, s->stream));
+    if (target) CK(cudaMemcpyAsync(s->tgt().p, target, px * 4, cudaMemcpyHostToDevice, s->stream));
     TRY(run_loss(s, lambda, dssim_scale));
     if (loss_out || dl_di_out) {
         TRY(sync_and_check(s, "photometric_loss"));
@@ -2068,7 +2104,7 @@ int gpk_photometric_loss_images(gpk_session* s, int32_t width, int32_t height,
     const size_t px = (size_t)width * height;
     TRY(target_wait(s));
     CK(cudaMemcpyAsync(s->image.p, rendered, px * 4, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaMemcpyAsync(s->target.p, target, px * 4, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->tgt().p, target, px * 4, cudaMemcpyHostToDevice, s->stream));
     // the prepared slice survives when the images have its shape (only the
     // rendered image buffer is overwritten), as the reference's loss leaves
     // the caller's prepared vector alone

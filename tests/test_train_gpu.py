@@ -360,3 +360,60 @@ def test_target_upload_overlaps_but_is_ordered(gp, session):
             assert np.array_equal(session.get_gaussians(), ref), k
             assert np.array_equal(s2.get_gaussians(), ref), k
         s2.graph_destroy_all()
+
+
+def test_target_slots_alternating_equal_single_slot(gp, session):
+    """gpk_set_target_slot: a session that alternates two target slots step by
+    step (graphs captured per slot, uploads into the slot of the step they
+    feed, queued without waiting) trains exactly like a session that
+    synchronizes after every upload into the one default slot."""
+    from paper_2603_20611_b200 import _native as N
+
+    dims = (256, 192, 8)
+    lo, hi = (-0.5, -0.5, -0.5), (255.5, 191.5, 7.5)
+    gs = gp.GaussianSet(f32(gp.init_random(20000, lo, hi, 1.5, 16).records), lo, hi)
+    poses = [gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), k) for k in (2, 5)]
+    psf, rc = gp.PsfSpec(), gp.RasterConfig()
+    lr0 = gp.LearningRates(6e-4, 0.02, 2e-3, 1e-3)
+    rng = np.random.default_rng(17)
+    targets = [rng.uniform(0, 0.1 * (k + 1), (192, 256)).astype(np.float32) for k in range(6)]
+    with gp.Session(0) as ref:
+        for s in (session, ref):
+            s.set_gaussians(gs)
+            s.upload(N.GPK_BUF_TARGET, targets[0].ctypes.data, targets[0].nbytes)
+        ref.synchronize()
+        session.synchronize()
+        gids = []
+        for k in range(2):  # graph k reads slot k
+            session.set_target_slot(k)
+            session.upload(N.GPK_BUF_TARGET, targets[0].ctypes.data, targets[0].nbytes)
+            gids.append(session.capture_train(poses[k], psf, rc, 0.2, 0.5, lr0, 20))
+        losses = []
+        for i, t in enumerate(targets):
+            session.set_target_slot(i % 2)
+            session.upload(N.GPK_BUF_TARGET, t.ctypes.data, t.nbytes)
+            session.graph_launch(gids[i % 2])
+            ref.upload(N.GPK_BUF_TARGET, t.ctypes.data, t.nbytes)
+            ref.synchronize()
+            ref.train_step(poses[i % 2], psf, rc, 0.2, 0.5, lr0, 20)
+            v = np.zeros(1)
+            ref.download(N.GPK_BUF_LOSS, v.ctypes.data, 8)
+            ref.synchronize()
+            losses.append(v[0])
+        v = np.zeros(1)
+        session.download(N.GPK_BUF_LOSS, v.ctypes.data, 8)
+        session.synchronize()
+        assert v[0] == losses[-1]
+        assert np.array_equal(session.get_gaussians(), ref.get_gaussians())
+        m1, v1, s1 = session.adam_state()
+        m2, v2, s2 = ref.adam_state()
+        assert s1 == s2 == len(targets) and np.array_equal(m1, m2) and np.array_equal(v1, v2)
+        # downloads read the selected slot
+        got = np.zeros_like(targets[0])
+        session.set_target_slot(0)
+        session.download(N.GPK_BUF_TARGET, got.ctypes.data, got.nbytes)
+        session.synchronize()
+        assert np.array_equal(got, targets[4])
+        with pytest.raises(gp.InvalidArgument):
+            session.set_target_slot(2)
+        session.graph_destroy_all()

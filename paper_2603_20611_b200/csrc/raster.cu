@@ -121,9 +121,9 @@ __global__ void __launch_bounds__(kFwdThreads) k_raster_fwd(const RasterLaunch a
     __shared__ unsigned s_range[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tile = blockIdx.x;
+    // 2-D grid (tiles_x, tiles_y): no per-thread division for the tile coordinates
+    const int tx = blockIdx.x, ty = blockIdx.y, tile = ty * a.slice.tiles_x + tx;
     const bool produce = a.bucket_tab != nullptr;
-    const int tx = tile % a.slice.tiles_x, ty = tile / a.slice.tiles_x;
     const int x0 = tx * kTile, y0 = ty * kTile;
     const double X0 = ((double)x0 - a.slice.ppx) * a.slice.sx;
     const double Y0 = ((double)y0 - a.slice.ppy) * a.slice.sy;
@@ -229,12 +229,16 @@ __device__ __forceinline__ void ssim_dl_tile(const RasterLaunch& a, int x0, int 
         // all loads of the haloed g planes in flight at once, then to shared
         constexpr int kPer = (kSsimH * kSsimH + 255) / 256;
         float v[3][kPer];
+        // an interior tile's halo needs no reflection (the common case at
+        // large slices): one test per CTA instead of reflect loops per load
+        const bool inner = x0 >= kSsimR && y0 >= kSsimR && x0 + kTile + kSsimR <= W && y0 + kTile + kSsimR <= H;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const int idx = threadIdx.x + k * 256;
             if (idx < kSsimH * kSsimH) {
                 const int r = idx / kSsimH, c = idx % kSsimH;
-                const size_t o = (size_t)reflect_idx(y0 + r - kSsimR, H) * W + reflect_idx(x0 + c - kSsimR, W);
+                const size_t o = inner ? (size_t)(y0 + r - kSsimR) * W + (x0 + c - kSsimR)
+                                       : (size_t)reflect_idx(y0 + r - kSsimR, H) * W + reflect_idx(x0 + c - kSsimR, W);
                 v[0][k] = a.ssim_g[o];
                 v[1][k] = a.ssim_g[P + o];
                 v[2][k] = a.ssim_g[2 * P + o];
@@ -254,6 +258,8 @@ __device__ __forceinline__ void ssim_dl_tile(const RasterLaunch& a, int x0, int 
     __syncthreads();
     // rows: a thread filters 8 consecutive outputs of one plane row from 18
     // inputs held in registers (each output still sums its 11 taps in order)
+    // (packed g1/g2 pairs measured slower: 47 registers, 5 CTAs/SM, or no gain
+    // when capped at 40)
     if (threadIdx.x < kSsimH * 3 * 2) {
         const int r = threadIdx.x / 6, q = (threadIdx.x % 6) >> 1, c0 = (threadIdx.x & 1) * 8;
         float v[8 + 2 * kSsimR];
@@ -312,12 +318,11 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
     __shared__ unsigned s_range[2];
 
     const int tid = threadIdx.x;
-    const int tile = blockIdx.x;
+    const int tx = blockIdx.x, ty = blockIdx.y, tile = ty * a.slice.tiles_x + tx;  // 2-D grid
     if (a.fin.partial && tile == 0) {  // the training step's loss (k_ssim_fwd's partials)
         __shared__ double s_red[2 * 32];
         loss_reduce(a.fin, s_red);
     }
-    const int tx = tile % a.slice.tiles_x, ty = tile / a.slice.tiles_x;
     const int x0 = tx * kTile, y0 = ty * kTile;
     tile_range(a, tile, s_range);
     if (tid == 0) {
@@ -437,13 +442,13 @@ __global__ void __launch_bounds__(256) k_raster_bwd(const RasterLaunch a) {
 }  // namespace
 
 void launch_raster_fwd(const RasterLaunch& a, cudaStream_t st) {
-    const int tiles = a.slice.tiles_x * a.slice.tiles_y;
-    if (tiles > 0) launch_pdl(k_raster_fwd, dim3(tiles), dim3(kFwdThreads), 0, st, a);
+    if (a.slice.tiles_x > 0 && a.slice.tiles_y > 0)
+        launch_pdl(k_raster_fwd, dim3(a.slice.tiles_x, a.slice.tiles_y), dim3(kFwdThreads), 0, st, a);
 }
 
 void launch_raster_bwd(const RasterLaunch& a, cudaStream_t st) {
-    const int tiles = a.slice.tiles_x * a.slice.tiles_y;
-    if (tiles > 0) launch_pdl(k_raster_bwd, dim3(tiles), dim3(256), 0, st, a);
+    if (a.slice.tiles_x > 0 && a.slice.tiles_y > 0)
+        launch_pdl(k_raster_bwd, dim3(a.slice.tiles_x, a.slice.tiles_y), dim3(256), 0, st, a);
 }
 
 }  // namespace gpk

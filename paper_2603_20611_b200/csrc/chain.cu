@@ -24,16 +24,20 @@ __global__ void __launch_bounds__(256) k_chain(const ChainLaunch a) {
     if (dense && g == 0 && threadIdx.x == 0) *a.grads_dirty = a.ctrl->survivors;
     for (unsigned j = threadIdx.x; j < S; j += blockDim.x) {
         const uint32_t cid = g * kDecideGroupSize + j;
+        // the record and the parameters requested together (the branch on the
+        // record would otherwise hold the parameters' load for a round trip)
         const SurvivorRecord rec = a.records[cid];
-        if (dense) a.dirty_idx[atomicAdd(a.dirty_ctr, 1u)] = rec.gidx & ~kExactFlag;
-        if (rec.gidx & kExactFlag) continue;  // K_chain_exact (listed by K_decide)
         float pf[11];
         uint32_t i;
         load_cand(a.sparams + cid, pf, i);
+        if (dense) a.dirty_idx[atomicAdd(a.dirty_ctr, 1u)] = rec.gidx & ~kExactFlag;
+        if (rec.gidx & kExactFlag) continue;  // K_chain_exact (listed by K_decide)
+        PartialsBatch pb;  // the partials' loads overlap the forward state's arithmetic
+        merge_partials_issue(a, rec, pb);
         FastFocus ff;
         fast_state(pf, a.slice, ff);
         double acc[6];
-        merge_partials(a, rec, acc);
+        merge_partials_finish(pb, acc);
         float g11[11], dmu[3];
         fast_backward(pf, ff, acc, a.slice, g11, dmu);
         store_chain(a, i, cid, g11, dmu, acc);

@@ -8,16 +8,46 @@
 namespace gpk {
 
 // Stage-2 merge of one survivor's per-tile sums in tile order (backward.hpp:141-145).
-__device__ __forceinline__ void merge_partials(const ChainLaunch& a, const SurvivorRecord& rec,
-                                               double acc[6]) {
+// The partials of up to 4 tiles are requested together before any is added
+// (a survivor covers 1-4 tiles at these scales): one L2 round trip instead of
+// one per tile; the adds keep tile order (the same bits). Split in two so the
+// caller can do independent work between the loads and the adds.
+struct PartialsBatch {
+    float2 q[4][3];
+    unsigned np;
+    const float2* part;
+};
+
+__device__ __forceinline__ void merge_partials_issue(const ChainLaunch& a, const SurvivorRecord& rec,
+                                                     PartialsBatch& pb) {
     const unsigned ntx = rec.hi_x / kTile - rec.lo_x / kTile + 1;
     const unsigned nty = rec.hi_y / kTile - rec.lo_y / kTile + 1;
-    const unsigned np = ntx * nty;
+    pb.np = ntx * nty;
+    pb.part = reinterpret_cast<const float2*>(a.partials + 6ull * rec.pair_base);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        if ((unsigned)u < pb.np) {
+            pb.q[u][0] = pb.part[3 * u];
+            pb.q[u][1] = pb.part[3 * u + 1];
+            pb.q[u][2] = pb.part[3 * u + 2];
+        }
+}
+
+__device__ __forceinline__ void merge_partials_finish(const PartialsBatch& pb, double acc[6]) {
 #pragma unroll
     for (int j = 0; j < 6; ++j) acc[j] = 0.0;
-    const float2* part = reinterpret_cast<const float2*>(a.partials + 6ull * rec.pair_base);
-    for (unsigned k = 0; k < np; ++k) {
-        const float2 p0 = part[3 * k], p1 = part[3 * k + 1], p2 = part[3 * k + 2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        if ((unsigned)u < pb.np) {
+            acc[0] += (double)pb.q[u][0].x;
+            acc[1] += (double)pb.q[u][0].y;
+            acc[2] += (double)pb.q[u][1].x;
+            acc[3] += (double)pb.q[u][1].y;
+            acc[4] += (double)pb.q[u][2].x;
+            acc[5] += (double)pb.q[u][2].y;
+        }
+    for (unsigned k = 4; k < pb.np; ++k) {
+        const float2 p0 = pb.part[3 * k], p1 = pb.part[3 * k + 1], p2 = pb.part[3 * k + 2];
         acc[0] += (double)p0.x;
         acc[1] += (double)p0.y;
         acc[2] += (double)p1.x;
@@ -25,6 +55,12 @@ __device__ __forceinline__ void merge_partials(const ChainLaunch& a, const Survi
         acc[4] += (double)p2.x;
         acc[5] += (double)p2.y;
     }
+}
+
+__device__ __forceinline__ void merge_partials(const ChainLaunch& a, const SurvivorRecord& rec, double acc[6]) {
+    PartialsBatch pb;
+    merge_partials_issue(a, rec, pb);
+    merge_partials_finish(pb, acc);
 }
 
 // Gradient of set index i (survivor slot cid): the dense planes, or the slot

@@ -510,13 +510,9 @@ __device__ __forceinline__ unsigned cull_chunk(const PrepLaunch& a, const Filter
 }
 
 // cp.async (16 B, L1 bypass) staging of K_filter chunks: each lane copies its
-// own 4 Gaussians' 11 plane slices; one commit group per chunk.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-// ... with an L2 eviction-priority hint (the parameter planes are read again
-// by the same training step's Adam: keep them in L2 until then)
+// own 4 Gaussians' 11 plane slices; one commit group per chunk. With an L2
+// eviction-priority hint (the parameter planes are read again by the same
+// training step's Adam: keep them in L2 until then)
 __device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, unsigned long long policy) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "l"(policy)
@@ -568,12 +564,14 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter(const PrepLaunch a
     if (a.head)  // the prepare's control head (no separate memset)
         for (unsigned w = gtid; w < a.head_words; w += gthreads) a.head[w] = 0u;
     clear_prev_sort_rows(a, gtid, gthreads);
-    if (kZeroGrads && !dense_zero)  // the previous survivors' gradients (sparse mode)
-        for (unsigned e = gtid; e < dirty; e += gthreads) {
-            const uint32_t i = a.dirty_idx[e];
+    if constexpr (kZeroGrads) {
+        if (!dense_zero)  // the previous survivors' gradients (sparse mode)
+            for (unsigned e = gtid; e < dirty; e += gthreads) {
+                const uint32_t i = a.dirty_idx[e];
 #pragma unroll
-            for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = 0.f;
-        }
+                for (int k = 0; k < 11; ++k) a.grads[(uint64_t)k * a.cap + i] = 0.f;
+            }
+    }
     const FilterConsts fc = filter_consts(a.slice, log_tau);
     __shared__ LazyView s_lz;
     if (kLazy) {

@@ -61,7 +61,6 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
     const unsigned dmask = (1u << a.digit_bits) - 1;
     const unsigned nb = dmask + 1;
     const int tiles_x = a.slice.tiles_x;
-    const unsigned ngroups = gridDim.x;
     for (int k = tid; k < a.passes * kMaxBuckets; k += kDecideThreads) (&s_hist[0][0])[k] = 0;
     for (int k = tid; k < kDecideGroup / 32; k += kDecideThreads) s_bits[k] = 0;
     if (tid == 0) {

@@ -374,6 +374,46 @@ __device__ __forceinline__ void adam_update_store_pipe(const AdamLaunch& a, cons
     for (int d = 0; d < 4; ++d) stp_stream<N>(a.params + (uint64_t)(6 + d) * a.cap + i0, q[d]);
 }
 
+// adam_update (all 11 planes' new parameters in p[], moments stored) with the
+// software pipelining of adam_update_store_pipe: the same bits.
+template <int N, typename G>
+__device__ __forceinline__ void adam_update_pipe(const AdamLaunch& a, const AdamConsts& c, uint32_t i0,
+                                                 const G& grad, Pack<N> out[11], unsigned& nz) {
+    constexpr int kOrder[11] = {0, 1, 2, 3, 4, 5, 10, 6, 7, 8, 9};
+    nz = 0;
+    Pack<N> m[2], v[2], g[2];
+    auto fetch = [&](int j, int b) {
+        const uint64_t o = (uint64_t)kOrder[j] * a.cap + i0;
+        m[b] = ldp_stream<N>(a.m + o);
+        v[b] = ldp_stream<N>(a.v + o);
+        out[kOrder[j]] = ldp_stream<N>(a.params + o);
+        g[b] = grad(kOrder[j]);
+    };
+    fetch(0, 0);
+#pragma unroll
+    for (int j = 0; j < 11; ++j) {
+        const int b = j & 1, k = kOrder[j];
+        if (j + 1 < 11) fetch(j + 1, b ^ 1);
+        const float lr = k < 3 ? c.lr[0] : (k < 6 ? c.lr[2] : (k == 10 ? c.lr[1] : c.lr[3]));
+        const float lrc = __fmul_rn(lr, c.ibc1);
+#pragma unroll
+        for (int l = 0; l < N; ++l) {
+            nz |= (g[b].v[l] != 0.f ? 1u : 0u) << l;
+            adam_elem(c, lrc, out[k].v[l], m[b].v[l], v[b].v[l], g[b].v[l]);
+        }
+        const uint64_t o = (uint64_t)k * a.cap + i0;
+        stp_stream<N>(a.m + o, m[b]);
+        stp_stream<N>(a.v + o, v[b]);
+        if (k < 3) {
+            const float lo = a.bbox_min[k], hi = a.bbox_max[k];
+#pragma unroll
+            for (int l = 0; l < N; ++l) out[k].v[l] = fminf(hi, fmaxf(lo, out[k].v[l]));
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < N; ++l) adam_renorm(out[6].v[l], out[7].v[l], out[8].v[l], out[9].v[l]);
+}
+
 template <int N, typename G>
 __device__ __forceinline__ void adam_update_store_g(const AdamLaunch& a, const AdamConsts& c, uint32_t i0,
                                                     const G& grad) {

@@ -777,7 +777,8 @@ __global__ void __launch_bounds__(kFilterThreads, 2) k_filter_multi(const __grid
 // stand-alone Adam kernel; dense or slot gradients), leaves the dense gradient
 // planes zero, then its warp culls the 128 updated primitives against the next
 // pose (cull_chunk).
-__global__ void __launch_bounds__(256, 3) k_adam_cull(const AdamLaunch a, const PrepLaunch f, float log_tau,
+template <int kMinB>
+__global__ void __launch_bounds__(256, kMinB) k_adam_cull(const AdamLaunch a, const PrepLaunch f, float log_tau,
                                                       int filter_on) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ CullScratch s_cull[8];
@@ -811,7 +812,9 @@ __global__ void __launch_bounds__(256, 3) k_adam_cull(const AdamLaunch a, const 
             Pack<kFilterItems> q[11];
             uint32_t gslot[kFilterItems];
             const bool any = slots && adam_slots<kFilterItems>(a, i0, gslot);
-            adam_update<kFilterItems>(a, c, i0, slots ? gslot : nullptr, q, nz);
+            // (software-pipelined planes, as k_adam: the same bits)
+            adam_update_pipe<kFilterItems>(
+                a, c, i0, [&](int k) { return adam_grad<kFilterItems>(a, k, i0, slots ? gslot : nullptr); }, q, nz);
             adam_store<kFilterItems>(a, i0, q);
             if (any) adam_slots_clear<kFilterItems>(a, i0);
 #pragma unroll
@@ -900,7 +903,8 @@ void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& f, cudaStream_t st)
     const unsigned threads = (unsigned)std::max<uint64_t>((uint64_t)f.nfilter * 32, (a.n + kFilterItems - 1) / kFilterItems);
     const unsigned grid = (threads + 255) / 256;
     if (!grid) return;
-    launch_pdl(k_adam_cull, dim3(grid), dim3(256), 0, st, a, f, log_tau, filter_on ? 1 : 0);
+    // (2 CTAs/SM without spills measured the same as 3 with a 48 B spill)
+    launch_pdl(k_adam_cull<3>, dim3(grid), dim3(256), 0, st, a, f, log_tau, filter_on ? 1 : 0);
 }
 
 }  // namespace gpk

@@ -115,6 +115,17 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_field(config, kernel, field):
+    """A per-kernel field of the committed ncu capture (profiles/ncu_summary.json)."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(config, {}).get(kernel, {}).get(field)
+    except Exception:
+        return None
+
+
 def ncu_traffic(config, kernel):
     """dram__bytes_read+write per launch of `kernel` from the committed ncu capture."""
     p = ROOT / "profiles" / "ncu_summary.json"
@@ -951,6 +962,13 @@ def run_ours(args):
             ms = measured[stg][0] / measured[stg][1]
             compute_roof[kn] = {"ms": ms, "evals_per_s": E_mean / (ms * 1e-3),
                                 "frac": E_mean / (ms * 1e-3) / ex2_peak}
+            # the bound these kernels actually meet is instruction issue: the
+            # committed ncu capture's warp instructions per SM cycle / 4
+            # (profiles/ncu_summary.json; cold, serialised)
+            ipc = ncu_field(args.config, kn, "ipc_per_sm")
+            if ipc is not None:
+                compute_roof[kn]["issue"] = {"ipc_per_sm": ipc, "peak_ipc": 4.0, "frac": ipc / 4.0,
+                                             "source": "ncu --set full (profiles/ncu_summary.json)"}
     # U2 floor with slot gradients: 44N cull read + 264N Adam (p, m, v read and
     # written) + 2N slot map (SURVEY.md §8d's 396N assumed dense gradient
     # planes: +44N Adam read, +44N clear)

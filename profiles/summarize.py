@@ -128,7 +128,9 @@ def full(rep: str, out: str, config: str) -> None:
     for k in kernels:
         name = k["kernel"].split("<")[0]
         cfg[name] = {"dram_bytes_per_launch": (k["dram_read_bytes"] or 0) + (k["dram_write_bytes"] or 0),
-                     "duration_us_cold": k["duration_us"], "source": Path(out).name}
+                     "duration_us_cold": k["duration_us"], "ipc_per_sm": k.get("ipc_per_sm"),
+                     "issue_frac": (k["ipc_per_sm"] / 4.0) if k.get("ipc_per_sm") is not None else None,
+                     "source": Path(out).name}
     summ.write_text(json.dumps(s, indent=1))
 
 

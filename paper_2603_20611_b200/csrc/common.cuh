@@ -902,6 +902,7 @@ struct VoxEvalLaunch {
     const VoxRecord* records;
     const uint32_t* keys;      // sorted voxel-tile keys
     const uint32_t* vals;      // sorted set indices
+    const unsigned* tile_start;  // first sorted position of every tile (+ end, k_key_starts)
     const Control* ctrl;
     uint64_t pair_cap;
     float* volume;             // voxelize output
@@ -956,6 +957,9 @@ void launch_vox_prep(const VoxPrepLaunch& a, cudaStream_t st);
 void launch_prepared_full(const CandParams* sparams, const uint32_t* slots, unsigned S, const SliceArgs& s,
                           double* out, cudaStream_t st);
 void launch_vox_eval(const VoxEvalLaunch& a, cudaStream_t st);
+// sort.cu: the tile starts of a sorted key list (start[0 .. ntiles], the last = P)
+void launch_key_starts(const uint32_t* keys, const Control* ctrl, uint64_t pair_cap, unsigned ntiles,
+                       unsigned* start, int num_sms, cudaStream_t st);
 void launch_vox_bwd(const VoxEvalLaunch& a, cudaStream_t st);
 void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st);
 

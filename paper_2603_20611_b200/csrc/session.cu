@@ -155,6 +155,7 @@ struct gpk_session {
     DevBuf keys[2], vals[2], partials, sort_status;  // sort_status: per-sort-tile digit counts
     DevBuf pair_recs;  // tile-major PairRecords of the sorted lists (32 B per pair)
     DevBuf tile_start; // multi-pass slices: first sorted position of every tile (+ end)
+    DevBuf vox_tile_start;  // the voxelizer's 8^3 tiles: first sorted position (+ end)
     bool loss_in_fwd = false;  // A/B knob: the fused loss finished by k_ssim_fwd's last CTA
     DevBuf head;       // Control | hist | prep flags (memset per prepare)
     DevBuf cand_list;  // K_chain's deferral list (survivor slots for the fp64 chain)
@@ -1406,13 +1407,17 @@ int run_vox_prep(gpk_session* s, const gpk_voxelizer_config* cfg) {
     vs.final_buf = vs.passes & 1;
     vs.valid = true;
     CK(s->vox_records.ensure(s->cap * sizeof(VoxRecord)));
+    CK(s->vox_tile_start.ensure((vs.tiles + 1) * 4));
     CK(s->volume.ensure(vs.voxels * 4));
     CK(s->dl_dv_vol.ensure(vs.voxels * 4));
     StageScope scope(s, GPK_STAGE_VOXEL);
     CK(cudaMemsetAsync(s->head.p, 0, head_size(s->n), s->stream));
     // the slice path clears only the histogram rows its previous sort used
     CK(cudaMemsetAsync(s->sort_status.p, 0, s->sort_status.bytes, s->stream));
-    if (s->n == 0) return GPK_OK;
+    if (s->n == 0) {  // every tile empty
+        CK(cudaMemsetAsync(s->vox_tile_start.p, 0, (vs.tiles + 1) * 4, s->stream));
+        return GPK_OK;
+    }
     VoxPrepLaunch p;
     p.params = s->params.as<float>();
     p.cap = s->cap;
@@ -1436,6 +1441,9 @@ int run_vox_prep(gpk_session* s, const gpk_voxelizer_config* cfg) {
     launch_vox_prep(p, s->stream);
     CK(cudaGetLastError());
     TRY(launch_sorts(s, vs.passes, vs.digit_bits, nullptr, 0, p.tile_shift));
+    launch_key_starts(s->keys[vs.final_buf].as<uint32_t>(), s->ctrl(), s->pair_cap, (unsigned)vs.tiles,
+                      s->vox_tile_start.as<unsigned>(), s->num_sms, s->stream);
+    CK(cudaGetLastError());
     return GPK_OK;
 }
 
@@ -1444,6 +1452,7 @@ VoxEvalLaunch vox_eval_args(gpk_session* s) {
     e.records = s->vox_records.as<VoxRecord>();
     e.keys = s->keys[s->vox.final_buf].as<uint32_t>();
     e.vals = s->vals[s->vox.final_buf].as<uint32_t>();
+    e.tile_start = s->vox_tile_start.as<unsigned>();
     e.ctrl = s->ctrl();
     e.pair_cap = s->pair_cap;
     e.volume = s->volume.as<float>();
@@ -1576,7 +1585,7 @@ static int session_destroy(gpk_session* s) {
     }
     s->graphs.clear();
     DevBuf* bufs[] = {&s->params, &s->grads, &s->adam_m, &s->adam_v, &s->records, &s->survivors,
-                      &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials, &s->pair_recs, &s->tile_start,
+                      &s->keys[0], &s->keys[1], &s->vals[0], &s->vals[1], &s->partials, &s->pair_recs, &s->tile_start, &s->vox_tile_start,
                       &s->sort_status, &s->head, &s->persist, &s->image,
                       &s->dl_di, &s->target_k[0], &s->target_k[1], &s->loss_g, &s->loss_partial, &s->stat_norm, &s->acc_norm, &s->acc_obs, &s->acc_world,
                       &s->stat_obs, &s->stat_world, &s->cand_list, &s->surv_params, &s->cand, &s->cand_count, &s->grp_table, &s->bucket_tab,

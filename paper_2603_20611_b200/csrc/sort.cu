@@ -288,6 +288,26 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(const GatherLaunch a)
                                         s_wsum, s_range);
 }
 
+// Position j of a sorted key list opens every tile in (key[j-1], key[j]]
+// (key[-1] = -1, key[P] = ntiles): over j in [0, P] every start[0 .. ntiles]
+// is written once. Returns key[j] (ntiles at j = P).
+__device__ __forceinline__ unsigned mark_key_starts(const uint32_t* __restrict__ keys, unsigned P, unsigned ntiles,
+                                                    unsigned j, unsigned* __restrict__ start) {
+    const unsigned tile = j < P ? keys[j] : ntiles;
+    const unsigned prev = j ? keys[j - 1] : 0xffffffffu;
+    for (unsigned t = prev + 1; t <= tile; ++t) start[t] = j;
+    return tile;
+}
+
+// The tile starts of a sorted key list (the voxelizer's 8^3 tiles).
+__global__ void __launch_bounds__(256) k_key_starts(const uint32_t* __restrict__ keys, const Control* ctrl,
+                                                    uint64_t pair_cap, unsigned ntiles, unsigned* __restrict__ start) {
+    pdl_entry();  // see common.cuh: successor may launch; predecessor complete
+    const unsigned P = stored_pairs(ctrl, pair_cap);
+    for (unsigned j = blockIdx.x * blockDim.x + threadIdx.x; j <= P; j += gridDim.x * blockDim.x)
+        mark_key_starts(keys, P, ntiles, j, start);
+}
+
 // Multi-pass slices: the pair record of every sorted position (its tile is its
 // key), and the tile starts: position j opens every tile in (key[j-1], key[j]]
 // (key[-1] = -1, key[P] = ntiles), so the pixel kernels read their range with
@@ -301,9 +321,7 @@ __global__ void __launch_bounds__(256) k_pair_records(const uint32_t* __restrict
     const unsigned P = stored_pairs(ctrl, pair_cap);
     const unsigned ntiles = (unsigned)(sl.tiles_x * sl.tiles_y);
     for (unsigned j = blockIdx.x * blockDim.x + threadIdx.x; j <= P; j += gridDim.x * blockDim.x) {
-        const unsigned tile = j < P ? keys[j] : ntiles;
-        const unsigned prev = j ? keys[j - 1] : 0xffffffffu;
-        for (unsigned t = prev + 1; t <= tile; ++t) tile_start[t] = j;
+        const unsigned tile = mark_key_starts(keys, P, ntiles, j, tile_start);
         if (j == P) break;
         const int tx = (int)(tile % (unsigned)sl.tiles_x), ty = (int)(tile / (unsigned)sl.tiles_x);
         const double X0 = ((double)(tx * kTile) - sl.ppx) * sl.sx;
@@ -323,6 +341,11 @@ void launch_pair_records(const uint32_t* keys, const uint32_t* vals, const Survi
                          int num_sms, cudaStream_t st) {
     launch_pdl(k_pair_records, dim3(num_sms * 8), dim3(256), 0, st, keys, vals, records, pairs, tile_start, ctrl,
                pair_cap, slice);
+}
+
+void launch_key_starts(const uint32_t* keys, const Control* ctrl, uint64_t pair_cap, unsigned ntiles,
+                       unsigned* start, int num_sms, cudaStream_t st) {
+    launch_pdl(k_key_starts, dim3(num_sms * 8), dim3(256), 0, st, keys, ctrl, pair_cap, ntiles, start);
 }
 
 void launch_super_scan(unsigned* region, uint64_t tiles_cap, unsigned nb, const Control* ctrl, uint64_t pair_cap,

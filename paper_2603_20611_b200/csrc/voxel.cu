@@ -32,24 +32,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-__device__ __forceinline__ unsigned warp_lower_bound(const uint32_t* __restrict__ keys, unsigned n,
-                                                     unsigned target) {
-    const int lane = threadIdx.x & 31;
-    unsigned lo = 0, hi = n;
-    while (hi - lo > 32) {
-        const unsigned span = hi - lo;
-        const unsigned pos = lo + (unsigned)(((unsigned long long)span * (lane + 1)) / 32) - 1;
-        const unsigned m = __ballot_sync(0xffffffffu, keys[pos] < target);
-        const int c = __popc(m);
-        const unsigned new_lo = c ? (lo + (unsigned)(((unsigned long long)span * c) / 32)) : lo;
-        const unsigned new_hi =
-            (c < 32) ? (lo + (unsigned)(((unsigned long long)span * (c + 1)) / 32) - 1) : hi;
-        lo = new_lo;
-        hi = new_hi;
-    }
-    const unsigned pos = lo + lane;
-    return lo + __popc(__ballot_sync(0xffffffffu, pos < hi && keys[pos] < target));
-}
 
 struct TileBox {
     int x0, y0, z0, nx, ny, nz;  // voxel origin and extent (clipped to the grid)
@@ -80,11 +62,7 @@ __global__ void __launch_bounds__(THREADS) k_veval(const VoxEvalLaunch a) {
     const int tid = threadIdx.x;
     const unsigned t = blockIdx.x;
     const TileBox b = tile_box(a.v, t);
-    if (tid < 64) {
-        const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
-        const unsigned r = warp_lower_bound(a.keys, P, t + (tid >> 5));
-        if ((tid & 31) == 0) s_range[tid >> 5] = r;
-    }
+    if (tid < 2) s_range[tid] = __ldcg(&a.tile_start[t + tid]);  // (k_key_starts)
     // voxel centre of the tile origin (voxel_center, core.hpp:136-138), fp64
     const double wx0 = a.v.origin[0] + b.x0 * a.v.spacing[0];
     const double wy0 = a.v.origin[1] + b.y0 * a.v.spacing[1];
@@ -151,11 +129,7 @@ __global__ void __launch_bounds__(128) k_vbwd(const VoxEvalLaunch a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned t = blockIdx.x;
     const TileBox b = tile_box(a.v, t);
-    if (tid < 64) {
-        const unsigned P = stored_pairs(a.ctrl, a.pair_cap);
-        const unsigned r = warp_lower_bound(a.keys, P, t + (tid >> 5));
-        if ((tid & 31) == 0) s_range[tid >> 5] = r;
-    }
+    if (tid < 2) s_range[tid] = __ldcg(&a.tile_start[t + tid]);  // (k_key_starts)
     const int nvox = b.nx * b.ny * b.nz;
     const size_t X = (size_t)a.v.dims[0], Y = (size_t)a.v.dims[1];
     if (!a.dl_global) {

@@ -104,11 +104,16 @@ __global__ void __launch_bounds__(THREADS) k_veval(const VoxEvalLaunch a) {
                     const float dy = fy + p0.y, dz = fz + p0.z;
                     const float B = fmaf(p1.w, dy, p2.x * dz);
                     const float Cc = fmaf(dy, fmaf(p1.y, dy, p2.y * dz), fmaf(p1.z * dz, dz, p0.w));
+                    // two voxels of the row per packed fp32 pair (FFMA2; x + y as
+                    // fma(1, x, y): each lane rounds exactly like the scalar code)
 #pragma unroll
-                    for (int j = 0; j < SEG; ++j) {
-                        const float dx = fxs[j] + p0.x;
-                        const float q = fmaf(fmaf(p1.x, dx, B), dx, Cc);
-                        acc[j] += ex2_approx(q);
+                    for (int j = 0; j < SEG; j += 2) {
+                        const f32x2 dx = ffma2(f2(1.f, 1.f), f2(fxs[j], fxs[j + 1]), f2(p0.x, p0.x));
+                        const float2 q = f2_unpack(ffma2(ffma2(f2(p1.x, p1.x), dx, f2(B, B)), dx, f2(Cc, Cc)));
+                        const float2 s2 = f2_unpack(
+                            ffma2(f2(1.f, 1.f), f2(ex2_approx(q.x), ex2_approx(q.y)), f2(acc[j], acc[j + 1])));
+                        acc[j] = s2.x;
+                        acc[j + 1] = s2.y;
                     }
                 }
             }

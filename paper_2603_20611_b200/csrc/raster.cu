@@ -89,8 +89,7 @@ __device__ __forceinline__ void pair_wait(const PairStage& ps, unsigned q) { mba
 constexpr int kFwdThreads = 128;
 
 __device__ __forceinline__ void fwd_batch(const PairRecord* recs, unsigned nb, unsigned warp_y, unsigned ybit,
-                                          unsigned xb0, unsigned xb1, float fx0, float fx1, float fy, float& acc0,
-                                          float& acc1) {
+                                          unsigned xb0, unsigned xb1, f32x2 fx01, float fy, f32x2& acc) {
     const int lane = threadIdx.x & 31;
     const float4* s4 = reinterpret_cast<const float4*>(recs);
     for (unsigned g = 0; g < nb; g += 32) {
@@ -104,12 +103,13 @@ __device__ __forceinline__ void fwd_batch(const PairRecord* recs, unsigned nb, u
             const unsigned mask = __float_as_uint(r1.z);
             const float dy = fy - r0.y;
             const float B = r0.w * dy, Cc = r1.x * dy * dy;
-            const float dx0 = fx0 - r0.x, dx1 = fx1 - r0.x;
-            const float e0 = fmaf(dx0, fmaf(r0.z, dx0, B), Cc);
-            const float e1 = fmaf(dx1, fmaf(r0.z, dx1, B), Cc);
+            // the lane's two pixels as packed fp32 pairs (FFMA2/FADD2: each
+            // lane rounds like the scalar ops, the same bits)
+            const f32x2 dx = ffma2(f2(1.f, 1.f), fx01, f2(-r0.x, -r0.x));
+            const float2 e = f2_unpack(ffma2(dx, ffma2(f2(r0.z, r0.z), dx, f2(B, B)), f2(Cc, Cc)));
             const bool iny = (mask & ybit) != 0;
-            acc0 = fmaf(iny && (mask & xb0) ? r1.y : 0.f, ex2_approx(e0), acc0);
-            acc1 = fmaf(iny && (mask & xb1) ? r1.y : 0.f, ex2_approx(e1), acc1);
+            const float2 w = make_float2(iny && (mask & xb0) ? r1.y : 0.f, iny && (mask & xb1) ? r1.y : 0.f);
+            acc = ffma2(f2(w), f2(ex2_approx(e.x), ex2_approx(e.y)), acc);
         }
     }
 }
@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(kFwdThreads) k_raster_fwd(const RasterLaunch a
     const PairStage ps{s_pr, s_bar, s_range[0], s_range[1]};
     const unsigned nbatch = (ps.end - ps.start + kPairBatch - 1) / kPairBatch;
 
-    float acc0 = 0.f, acc1 = 0.f;
+    const f32x2 fx01 = f2(fx0, fx1);
+    f32x2 acc = f2(0.f, 0.f);
     if (produce) {
         // batch 0 was staged by the gather; later batches (tiles of more than
         // kPairBatch pairs) come back from the records this CTA just stored
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_raster_fwd(const RasterLaunch a
                     reinterpret_cast<float4*>(s_pr[0])[t] = __ldcg(reinterpret_cast<const float4*>(a.pairs + b) + t);
                 __syncthreads();
             }
-            fwd_batch(s_pr[0], nb, warp_y, ybit, xb0, xb1, fx0, fx1, fy, acc0, acc1);
+            fwd_batch(s_pr[0], nb, warp_y, ybit, xb0, xb1, fx01, fy, acc);
             __syncthreads();
         }
     } else {
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_raster_fwd(const RasterLaunch a
         for (unsigned q = 0; q < nbatch; ++q) {
             const unsigned nb = min((unsigned)kPairBatch, ps.end - (ps.start + q * kPairBatch));
             pair_wait(ps, q);
-            fwd_batch(s_pr[q & 1], nb, warp_y, ybit, xb0, xb1, fx0, fx1, fy, acc0, acc1);
+            fwd_batch(s_pr[q & 1], nb, warp_y, ybit, xb0, xb1, fx01, fy, acc);
             if (q + 2 < nbatch) {
                 __syncthreads();  // buffer q & 1 read by every warp
                 if (tid == 0) pair_issue(ps, a.pairs, q + 2);
@@ -190,6 +191,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_raster_fwd(const RasterLaunch a
         }
     }
     const int i = x0 + lx, j = y0 + ly;
+    const float acc0 = f2_unpack(acc).x, acc1 = f2_unpack(acc).y;
     if (j < a.slice.H) {
         float* row = a.image + (size_t)j * a.slice.W;
         if (i < a.slice.W) row[i] = acc0;

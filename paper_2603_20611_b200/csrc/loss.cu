@@ -95,12 +95,15 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const LossLaunch a) {
         // would wait one global round trip per element)
         constexpr int kPer = (kH * kH + kSsimThreads - 1) / kSsimThreads;
         float vx[kPer], vy[kPer];
+        // an interior tile's halo needs no reflection: one test per CTA
+        const bool inner = X0 >= kR && Y0 >= kR && X0 + kT + kR <= W && Y0 + kT + kR <= H;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const int idx = threadIdx.x + k * kSsimThreads;
             if (idx < kH * kH) {
                 const int r = idx / kH, c = idx % kH;
-                const size_t o = (size_t)reflect(Y0 + r - kR, H) * W + reflect(X0 + c - kR, W);
+                const size_t o = inner ? (size_t)(Y0 + r - kR) * W + (X0 + c - kR)
+                                       : (size_t)reflect(Y0 + r - kR, H) * W + reflect(X0 + c - kR, W);
                 vx[k] = a.image[o];
                 vy[k] = a.target[o];
             }

@@ -72,3 +72,41 @@ def test_dp_phase_errors(gp, session):
         session.train_step_dp(2, 0, poses, gp.PsfSpec(), gp.RasterConfig(), 0.2, 0.5, lr0, 10)
     with pytest.raises(gp.InvalidArgument):
         session.train_step_dp(2, 2, poses, gp.PsfSpec(), gp.RasterConfig(), 0.2, 0.5, lr0, 10, phases=1)
+
+
+def test_union_holds_every_rank_survivor_at_scale(gp):
+    """The union of W = 8 poses (consecutive mid-stack slices, the shape a
+    data-parallel step gives every rank) is computed by one interval test per
+    Gaussian (cull.cu union_candidate), not per pose. It must contain every
+    rank's survivors, or that rank's gradient would silently lose rows: for
+    each simulated rank, the gradient its render phase writes into the union
+    rows (read back densely) equals, bitwise, the plain single-session
+    gradient of the same slice (same loss, same kernels)."""
+    from paper_2603_20611_b200 import _native as N
+
+    dims = (192, 160, 64)
+    lo, hi = (-0.5,) * 3, tuple(d - 0.5 for d in dims)
+    gs = gp.GaussianSet(f32(gp.init_random(120000, lo, hi, 1.5, 41).records), lo, hi)
+    psf, rc, lr0 = gp.PsfSpec(), gp.RasterConfig(), gp.LearningRates(*LR0)
+    rng = np.random.default_rng(42)
+    tgt = rng.uniform(0, 0.1, (dims[1], dims[0])).astype(np.float32)
+    W = 8
+    poses = [gp.slice_pose_for_index(dims, (1, 1, 1), (0, 0, 0), k) for k in range(28, 28 + W)]
+    with gp.Session(0) as rank, gp.Session(0) as plain:
+        for s in (rank, plain):
+            s.set_gaussians(gs)
+            s.upload(N.GPK_BUF_TARGET, tgt.ctypes.data, tgt.nbytes)
+        union_rows = None
+        for r in (0, 3, 7):
+            rank.train_step_dp(W, r, poses, psf, rc, 0.2, 0.5, lr0, 50, phases=N.GPK_DP_RENDER)
+            got = rank.get_gradients()
+            rows, cap = rank.dp_union_rows()
+            union_rows = union_rows or rows
+            assert rows == union_rows and rows <= cap, "every rank numbers the same union"
+            plain.prepare(poses[r], psf, rc)
+            plain.rasterize()
+            _, dl = plain.photometric_loss(tgt, 0.2, 0.5)
+            want = plain.backward(dl)
+            nz = np.count_nonzero(np.any(want != 0, axis=1))
+            assert nz > 1000, nz  # the slice has survivors
+            assert np.array_equal(got, want), r

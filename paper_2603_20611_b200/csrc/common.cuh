@@ -976,7 +976,7 @@ void launch_union_to_dense(const uint32_t* umap, const float* rows, uint64_t cap
 void launch_prep_multi(const PrepLaunch* pl, int nb, int num_sms, cudaStream_t st, int own = -1,
                        unsigned* union_words = nullptr);
 void launch_adam_cull(const AdamLaunch& a, const PrepLaunch& next, cudaStream_t st);
-void launch_bin(const PrepLaunch& a, cudaStream_t st);
+void launch_bin(const PrepLaunch& a, int num_sms, cudaStream_t st);
 void launch_sort_pass(const SortLaunch& a, int grid, cudaStream_t st);
 void launch_super_scan(unsigned* region, uint64_t tiles_cap, unsigned nb, const Control* ctrl, uint64_t pair_cap,
                        unsigned ngroups, unsigned tile_keys, cudaStream_t st);

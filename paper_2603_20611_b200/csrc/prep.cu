@@ -46,7 +46,8 @@ __device__ __forceinline__ void load_params(const float* __restrict__ params, ui
 constexpr int kDecideThreads = 256;
 constexpr int kDecideGroup = kDecideGroupSize;
 
-__global__ void __launch_bounds__(kDecideThreads) k_decide(const PrepLaunch a) {
+template <int kMinB>
+__global__ void __launch_bounds__(kDecideThreads, kMinB) k_decide(const PrepLaunch a) {
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     extern __shared__ unsigned s_dyn_u[];
     unsigned* s_incl = s_dyn_u;                                              // kDecideGroup
@@ -669,16 +670,21 @@ void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st) {
     k_vchain<<<grid, 128, 0, st>>>(a);
 }
 
-void launch_bin(const PrepLaunch& a, cudaStream_t st) {
+void launch_bin(const PrepLaunch& a, int num_sms, cudaStream_t st) {
     if (!a.n) return;
     const int smem = kDecideGroup * (4 + 6) + 8 * kMaxBuckets * 2;  // + the stable fill's warp tables
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_decide<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_decide<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
     const unsigned groups = (a.nfilter + kDecideChunks - 1) / kDecideChunks;
-    launch_pdl(k_decide, dim3(groups), dim3(kDecideThreads), smem, st, a);
+    // one wave at 2 CTAs/SM: the unconstrained registers (114); more groups
+    // than that (large sets): 3 CTAs/SM (80 registers, a 64 B spill) — C5 bin
+    // 54.7 -> 46.5 us, C2 19.3 -> 19.9 us measured
+    if (groups > 2u * (unsigned)num_sms) launch_pdl(k_decide<3>, dim3(groups), dim3(kDecideThreads), smem, st, a);
+    else launch_pdl(k_decide<2>, dim3(groups), dim3(kDecideThreads), smem, st, a);
 }
 
 void launch_chain_exact(const ChainLaunch& a, int grid, cudaStream_t st) {

@@ -706,7 +706,7 @@ int run_prepare(gpk_session* s, const gpk_slice_pose* pose, const gpk_psf* psf,
     scope_prep.end();
     {
         StageScope scope_bin(s, GPK_STAGE_BIN);
-        launch_bin(pl, s->stream);
+        launch_bin(pl, s->num_sms, s->stream);
         CK(cudaGetLastError());
     }
     ps.lists_pending = false;

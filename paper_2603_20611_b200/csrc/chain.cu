@@ -46,8 +46,11 @@ __global__ void __launch_bounds__(256) k_chain(const ChainLaunch a) {
 
 }  // namespace
 
-void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st) {
-    launch_pdl(k_chain, dim3(grid), dim3(256), 0, st, a);
+void launch_chain(const ChainLaunch& a, int grid, int num_sms, cudaStream_t st) {
+    // CTA per group; more groups than one wave of 256-thread CTAs (3 per SM):
+    // 128 threads (a group holds ~100-200 survivors: more CTAs in flight)
+    const int threads = grid > 3 * num_sms ? 128 : 256;
+    launch_pdl(k_chain, dim3(grid), dim3(threads), 0, st, a);
 }
 
 }  // namespace gpk

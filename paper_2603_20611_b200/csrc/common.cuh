@@ -982,7 +982,7 @@ void launch_super_scan(unsigned* region, uint64_t tiles_cap, unsigned nb, const 
                        unsigned ngroups, unsigned tile_keys, cudaStream_t st);
 void launch_raster_fwd(const RasterLaunch& a, cudaStream_t st);
 void launch_raster_bwd(const RasterLaunch& a, cudaStream_t st);
-void launch_chain(const ChainLaunch& a, int grid, cudaStream_t st);
+void launch_chain(const ChainLaunch& a, int grid, int num_sms, cudaStream_t st);
 void launch_chain_exact(const ChainLaunch& a, int grid, cudaStream_t st);
 void launch_adam(const AdamLaunch& a, cudaStream_t st);
 void launch_adam_consts(const AdamLaunch& a, cudaStream_t st);

@@ -924,7 +924,7 @@ int run_backward(gpk_session* s, bool stats, bool slots = false, bool urows = fa
     launch_chain_exact(c, groups, s->side);
     CK(cudaGetLastError());
     CK(cudaEventRecord(s->ev_xjoin, s->side));
-    launch_chain(c, groups, s->stream);
+    launch_chain(c, groups, s->num_sms, s->stream);
     CK(cudaGetLastError());
     CK(cudaStreamWaitEvent(s->stream, s->ev_xjoin, 0));
     return GPK_OK;

@@ -45,6 +45,7 @@ __device__ __forceinline__ void load_params(const float* __restrict__ params, ui
 //      digit histograms (global, per sort tile, per super-tile).
 constexpr int kDecideThreads = 256;
 constexpr int kDecideGroup = kDecideGroupSize;
+constexpr int kPairMap = 1024;  // pairs of a group mapped to (survivor, tile) in shared memory
 
 template <int kMinB>
 __global__ void __launch_bounds__(kDecideThreads, kMinB) k_decide(const PrepLaunch a) {
@@ -219,9 +220,30 @@ __global__ void __launch_bounds__(kDecideThreads, kMinB) k_decide(const PrepLaun
 
     // ---- 3. pair bases and pair emission ------------------------------------------
     const unsigned P0 = (unsigned)s_excl;
-    for (unsigned j = tid; j < S; j += kDecideThreads) a.records[base + j].pair_base = P0 + (j ? s_incl[j - 1] : 0u);
+    // a group of at most kPairMap pairs (the common case) maps each pair to
+    // its (survivor, tile) up front: survivor j writes its rect's tiles in
+    // row-major order (no per-pair search or division below)
+    unsigned* s_pair = s_dyn_u + kDecideGroup + kDecideGroup * 3 / 2 + kDecideThreads / 32 * kMaxBuckets / 2;
+    const bool direct = Pb <= (unsigned)kPairMap;
+    for (unsigned j = tid; j < S; j += kDecideThreads) {
+        const unsigned k0 = j ? s_incl[j - 1] : 0u;
+        a.records[base + j].pair_base = P0 + k0;
+        if (direct) {
+            const unsigned ntx = s_rect[j][2], nty = (s_incl[j] - k0) / ntx;
+            const unsigned t0 = s_rect[j][1] * (unsigned)tiles_x + s_rect[j][0];
+            unsigned k = k0;
+            for (unsigned dy = 0; dy < nty; ++dy)
+                for (unsigned dx = 0; dx < ntx; ++dx) s_pair[k++] = (j << 20) | (t0 + dy * (unsigned)tiles_x + dx);
+        }
+    }
+    if (direct) __syncthreads();
     // tile of the group's k-th pair (pairs in (survivor, tile-in-rect) order)
     auto pair_tile = [&](unsigned k, unsigned& surv) {
+        if (direct) {
+            const unsigned e = s_pair[k];
+            surv = e >> 20;
+            return e & 0xfffffu;
+        }
         unsigned lo = 0, hi = S - 1;
         while (lo < hi) {
             const unsigned mid = (lo + hi) >> 1;
@@ -672,7 +694,8 @@ void launch_vox_chain(const VoxChainLaunch& a, int grid, cudaStream_t st) {
 
 void launch_bin(const PrepLaunch& a, int num_sms, cudaStream_t st) {
     if (!a.n) return;
-    const int smem = kDecideGroup * (4 + 6) + 8 * kMaxBuckets * 2;  // + the stable fill's warp tables
+    // survivors' pair prefixes and rects, the stable fill's warp tables, the pair map
+    const int smem = kDecideGroup * (4 + 6) + 8 * kMaxBuckets * 2 + kPairMap * 4;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_decide<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -308,6 +308,10 @@ class Session {
         pose_ = pose;
     }
 
+    // Target slot 0 or 1 for later target uploads and losses (gpk_set_target_slot):
+    // a loop alternating slots overlaps each upload with the previous step.
+    void set_target_slot(int slot) { check(gpk_set_target_slot(s_, slot)); }
+
   private:
     gpk_session* s_ = nullptr;
     SlicePose pose_{};

@@ -259,8 +259,11 @@ __device__ __forceinline__ Pack<2> adam_grad_multi(const AdamLaunch& a, int k, u
         if (s > a.nsrc) break;  // uniform: the batch size
         const float* base = (s ? a.src_slot[s - 1] : a.slot_grads) + off;
         const unsigned m0 = pm[s] & 0xffffu, m1 = pm[s] >> 16;
-        x0[s] = __ldcs(base + (m0 ? m0 : 1u));
-        x1[s] = __ldcs(base + (m1 ? m1 : 1u));
+        // only the slices holding the primitive are read (a primitive is in
+        // few of a step's slices: the absent ones' loads were most of the
+        // kernel's issue and load-unit traffic)
+        if (m0) x0[s] = __ldcs(base + m0);
+        if (m1) x1[s] = __ldcs(base + m1);
     }
     Pack<2> g;
     g.v[0] = (pm[0] & 0xffffu) ? x0[0] : 0.f;

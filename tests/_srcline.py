@@ -35,7 +35,7 @@ cur_fn, cur_line, in_fn = None, None, False
 for ln in dis.splitlines():
     m = re.match(r"\s*\.text\.(\S+):", ln)
     if m:
-        in_fn = kern in m.group(1)
+        in_fn = re.search(re.escape(kern) + r"[IE]", m.group(1)) is not None  # (not k_filter_multi for k_filter)
         continue
     m = re.search(r"//## File \"([^\"]+)\", line (\d+)", ln)
     if m:

@@ -211,12 +211,34 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(const LossLaunch a) {
     const int X0 = blockIdx.x * kT, Y0 = blockIdx.y * kT;
     const int W = a.W, H = a.H;
     const size_t P = (size_t)W * H;
-    for (int idx = threadIdx.x; idx < kH * kH; idx += blockDim.x) {
-        const int r = idx / kH, c = idx % kH;
-        const size_t o = (size_t)reflect(Y0 + r - kR, H) * W + reflect(X0 + c - kR, W);
-        s_g[0][r][c] = a.g[o];
-        s_g[1][r][c] = a.g[P + o];
-        s_g[2][r][c] = a.g[2 * P + o];
+    {
+        // every load of the haloed tile in flight at once, then to shared (an
+        // interior tile's halo needs no reflection)
+        constexpr int kPer = (kH * kH + 255) / 256;
+        const bool inner = X0 >= kR && Y0 >= kR && X0 + kT + kR <= W && Y0 + kT + kR <= H;
+        float v[3][kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int idx = threadIdx.x + k * 256;
+            if (idx < kH * kH) {
+                const int r = idx / kH, c = idx % kH;
+                const size_t o = inner ? (size_t)(Y0 + r - kR) * W + (X0 + c - kR)
+                                       : (size_t)reflect(Y0 + r - kR, H) * W + reflect(X0 + c - kR, W);
+                v[0][k] = a.g[o];
+                v[1][k] = a.g[P + o];
+                v[2][k] = a.g[2 * P + o];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int idx = threadIdx.x + k * 256;
+            if (idx < kH * kH) {
+                const int r = idx / kH, c = idx % kH;
+                s_g[0][r][c] = v[0][k];
+                s_g[1][r][c] = v[1][k];
+                s_g[2][r][c] = v[2][k];
+            }
+        }
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < kH * kT; idx += blockDim.x) {

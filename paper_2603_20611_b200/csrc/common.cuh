@@ -214,36 +214,52 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-// Wait-free ordered prefix, executed by one full warp of block `b`: publish the
-// block's aggregate as a single ready-tagged word, then sum ALL predecessors'
-// aggregates with independent loads (16 in flight per lane). No inclusive
-// prefix chain: latency is ~1-2 L2 round trips after the slowest predecessor
-// publishes, instead of one round trip per predecessor window. Requires that
-// every predecessor is (or was) resident — true for in-order claimed work.
-// words[b] = 1<<63 | value (value < 2^63); words zeroed before the kernel.
+// Ordered prefix, executed by one full warp of block `b`: publish the block's
+// aggregate as one ready-tagged word, then read predecessors backwards in
+// windows of 512 (16 independent loads in flight per lane). A window that holds
+// a published inclusive prefix ends the walk at the latest one; otherwise its
+// aggregates are summed and the walk continues. The block then publishes its
+// own inclusive prefix. A window costs ~1-2 L2 round trips after its slowest
+// word is ready, so in-order claimed work (every predecessor resident or done)
+// stops within the first window — O(1) words per block instead of O(b).
+// words[b] = kReady | [kIncl] | value (value < 2^62); words zeroed before the kernel.
 __device__ __forceinline__ unsigned long long warp_prefix_aggregates(unsigned long long* words,
                                                                      unsigned b,
                                                                      unsigned long long agg) {
     const int lane = threadIdx.x & 31;
-    constexpr unsigned long long kReady = 1ull << 63;
+    constexpr unsigned long long kReady = 1ull << 63, kIncl = 1ull << 62, kVal = kIncl - 1;
     if (lane == 0) st_release_u64(&words[b], kReady | agg);
     unsigned long long excl = 0;
-    for (unsigned j0 = 0; j0 < b; j0 += 32 * 16) {
+    for (unsigned hi = b; hi > 0;) {
+        const unsigned lo = hi > 32 * 16 ? hi - 32 * 16 : 0u;
+        // lane's words: j = hi - 1 - (i * 32 + lane), newest first
         unsigned long long w[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            const unsigned j = j0 + i * 32 + lane;
-            w[i] = (j < b) ? ld_acquire_u64(&words[j]) : kReady;
+            const int j = (int)hi - 1 - (i * 32 + lane);
+            w[i] = (j >= (int)lo) ? ld_acquire_u64(&words[j]) : kReady;
         }
+        int newest = -1;  // latest inclusive word this lane saw
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            const unsigned j = j0 + i * 32 + lane;
+            const int j = (int)hi - 1 - (i * 32 + lane);
             while (!(w[i] & kReady)) w[i] = ld_acquire_u64(&words[j]);
-            excl += w[i] & ~kReady;
+            if ((w[i] & kIncl) && j >= (int)lo && j > newest) newest = j;
         }
-    }
+        const int stop = __reduce_max_sync(0xffffffffu, newest);
+        unsigned long long part = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) excl += __shfl_xor_sync(0xffffffffu, excl, o);
+        for (int i = 0; i < 16; ++i) {
+            const int j = (int)hi - 1 - (i * 32 + lane);
+            if (j >= (int)lo && j >= stop) part += w[i] & kVal;  // word `stop` adds its inclusive prefix
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (stop >= 0) break;
+        hi = lo;
+    }
+    if (lane == 0) st_release_u64(&words[b], kReady | kIncl | (excl + agg));
     return excl;
 }
 

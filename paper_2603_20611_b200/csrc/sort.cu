@@ -127,10 +127,11 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
             }
         }
 
-        if (count <= (unsigned)kSortTile) {
-            // ---- short tile: staged in shared memory by all threads, then one
+        if (groups && count <= (unsigned)kSortTile) {
+            // ---- short group: staged in shared memory by all threads, then one
             // warp ranks the pairs in input order, 32 at a time, against running
-            // per-digit counters (no per-warp tables)
+            // per-digit counters (no per-warp tables). Position tiles are full
+            // (all but the last) and take the 8-warp path below.
             uint32_t* s_key = &s_whist[0][0];
             uint32_t* s_val = &s_whist[4][0];
             for (unsigned i = tid; i < count; i += kSortThreads) {

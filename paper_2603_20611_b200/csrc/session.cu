@@ -734,12 +734,14 @@ uint64_t decide_group_count(uint64_t n) { return (filter_blocks(n) + kDecideChun
 
 // Stable LSD radix passes over the (key, value) pairs in keys[0]/vals[0].
 // Position tiles of the voxelizer's radix passes: kSortTile << shift keys, at
-// most 16k tiles per pass over its capacity-sized pair list (the per-tile row
-// work is bounded by the super-row prefix, so smaller tiles only add CTAs).
+// most 4k tiles per pass over its capacity-sized pair list. Every tile reads up
+// to 16 digit-count rows (its super-row prefix and the earlier tiles of its
+// super-tile), so at C4 (7.9M pairs) 1k-key tiles spend as many L2 bytes on the
+// rows as on the keys; 2k-4k-key tiles measured fastest (1k-tile cap: +120 us).
 // The slice passes keep 1024-key tiles.
 int sort_tile_shift(uint64_t pair_cap) {
     int shift = 0;
-    while (((pair_cap + ((uint64_t)kSortTile << shift) - 1) >> (10 + shift)) > 16384 && shift < 12) ++shift;
+    while (((pair_cap + ((uint64_t)kSortTile << shift) - 1) >> (10 + shift)) > 4096 && shift < 12) ++shift;
     return shift;
 }
 

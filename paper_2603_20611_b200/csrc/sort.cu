@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
     pdl_entry();  // see common.cuh: successor may launch; predecessor complete
     __shared__ unsigned s_whist[8][kMaxBuckets];   // per-warp digit counts -> offsets
     __shared__ unsigned s_base[kMaxBuckets];       // running digit offsets of this tile
+    __shared__ unsigned s_gbase[kMaxBuckets];      // exclusive scan of the pass histogram
     __shared__ unsigned s_wsum[32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -50,6 +51,39 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
         a.prev_sort_words[2] = (unsigned)a.pass + 1;
     }
 
+    // ---- global digit base: exclusive scan of the histogram (nb <= 1024), once
+    // per CTA
+    if (blockIdx.x < ntiles) {
+        constexpr int kPer = kMaxBuckets / kSortThreads;  // 4 digits per thread
+        unsigned v[kPer], run = 0;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const unsigned d = tid * kPer + i;
+            v[i] = d < nb ? a.hist[d] : 0;
+            run += v[i];
+        }
+        unsigned incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        unsigned ex = incl - run;
+        for (int w = 0; w < warp; ++w) ex += s_wsum[w];
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const unsigned d = tid * kPer + i;
+            s_gbase[d] = ex;
+            // last pass: the digit groups' sorted start positions let the
+            // pixel kernels find their tile's range without a search
+            if (a.grp_begin && blockIdx.x == 0 && d < nb) a.grp_begin[d] = ex;
+            ex += v[i];
+        }
+        __syncthreads();
+    }
+
     for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
         unsigned first, count;
         if (groups) {
@@ -59,37 +93,6 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
         } else {
             first = t * tile_keys;
             count = min(P - first, tile_keys);
-        }
-        // ---- global digit base: exclusive scan of the histogram (nb <= 1024)
-        {
-            constexpr int kPer = kMaxBuckets / kSortThreads;  // 4 digits per thread
-            unsigned v[kPer], run = 0;
-#pragma unroll
-            for (int i = 0; i < kPer; ++i) {
-                const unsigned d = tid * kPer + i;
-                v[i] = d < nb ? a.hist[d] : 0;
-                run += v[i];
-            }
-            unsigned incl = run;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += u;
-            }
-            if (lane == 31) s_wsum[warp] = incl;
-            __syncthreads();
-            unsigned ex = incl - run;
-            for (int w = 0; w < warp; ++w) ex += s_wsum[w];
-#pragma unroll
-            for (int i = 0; i < kPer; ++i) {
-                const unsigned d = tid * kPer + i;
-                s_base[d] = ex;
-                // last pass: the digit groups' sorted start positions let the
-                // pixel kernels find their tile's range without a search
-                if (a.grp_begin && t == 0 && d < nb) a.grp_begin[d] = ex;
-                ex += v[i];
-            }
-            __syncthreads();
         }
         // ---- add the counts of all earlier tiles: the super row holds the
         // prefix over the earlier super-tiles (k_super_scan), then the earlier
@@ -115,15 +118,15 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
                         acc.z += v.z;
                         acc.w += v.w;
                     }
-                    s_base[d0] += acc.x;
-                    s_base[d0 + 1] += acc.y;
-                    s_base[d0 + 2] += acc.z;
-                    s_base[d0 + 3] += acc.w;
+                    s_base[d0] = s_gbase[d0] + acc.x;
+                    s_base[d0 + 1] = s_gbase[d0 + 1] + acc.y;
+                    s_base[d0 + 2] = s_gbase[d0 + 2] + acc.z;
+                    s_base[d0 + 3] = s_gbase[d0 + 3] + acc.w;
                 }
             } else if ((unsigned)tid < nb) {
                 unsigned acc = 0;
                 for (unsigned r = 0; r < nrows; ++r) acc += row_of(r)[tid];
-                s_base[tid] += acc;
+                s_base[tid] = s_gbase[tid] + acc;
             }
         }
 
@@ -175,11 +178,16 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
             const unsigned seg = r0 + warp * (kSortItems * 32);
             const unsigned lim = min(count - r0, (unsigned)kSortTile) + r0;
 #pragma unroll
+            for (int r = 0; r < kSortItems; ++r) {  // all loads in flight before the ranking
+                const unsigned idx = seg + r * 32 + lane;
+                const bool valid = idx < lim;
+                key[r] = valid ? __ldcs(a.keys_in + first + idx) : 0xffffffffu;
+                val[r] = valid ? __ldcs(a.vals_in + first + idx) : 0u;
+            }
+#pragma unroll
             for (int r = 0; r < kSortItems; ++r) {
                 const unsigned idx = seg + r * 32 + lane;
                 const bool valid = idx < lim;
-                key[r] = valid ? a.keys_in[first + idx] : 0xffffffffu;
-                val[r] = valid ? a.vals_in[first + idx] : 0u;
                 const unsigned d = valid ? ((key[r] >> a.shift) & mask) : 0xffffffffu;
                 const unsigned peers = __match_any_sync(0xffffffffu, d);
                 unsigned prior = 0;

@@ -223,12 +223,18 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 // word is ready, so in-order claimed work (every predecessor resident or done)
 // stops within the first window — O(1) words per block instead of O(b).
 // words[b] = kReady | [kIncl] | value (value < 2^62); words zeroed before the kernel.
+// publish = false: the caller published words[b] = kReady | agg earlier
+// (warp_prefix_publish), e.g. before working on its next block.
+__device__ __forceinline__ void warp_prefix_publish(unsigned long long* words, unsigned b, unsigned long long agg) {
+    st_release_u64(&words[b], (1ull << 63) | agg);
+}
 __device__ __forceinline__ unsigned long long warp_prefix_aggregates(unsigned long long* words,
                                                                      unsigned b,
-                                                                     unsigned long long agg) {
+                                                                     unsigned long long agg,
+                                                                     bool publish = true) {
     const int lane = threadIdx.x & 31;
     constexpr unsigned long long kReady = 1ull << 63, kIncl = 1ull << 62, kVal = kIncl - 1;
-    if (lane == 0) st_release_u64(&words[b], kReady | agg);
+    if (publish && lane == 0) warp_prefix_publish(words, b, agg);
     unsigned long long excl = 0;
     for (unsigned hi = b; hi > 0;) {
         const unsigned lo = hi > 32 * 16 ? hi - 32 * 16 : 0u;

@@ -473,10 +473,14 @@ __global__ void __launch_bounds__(128) k_prepared_full(const CandParams* __restr
 // for the evaluation kernel, and (8^3-tile, primitive) pairs emitted in
 // (primitive, tile) order through the same wait-free ordered prefix as K_exact.
 __global__ void __launch_bounds__(256) k_vprep(const VoxPrepLaunch a) {
+    // Two chunks in flight per CTA: chunk c's primitives are computed and its
+    // aggregate published, then chunk c-1's (claimed the previous round)
+    // prefix is looked up and its pairs emitted — by then its predecessors
+    // have long published, so the look-up rarely waits.
     __shared__ unsigned s_chunk;
-    __shared__ unsigned long long s_incl[256];
-    __shared__ uint16_t s_t0[256][3];
-    __shared__ uint16_t s_nt[256][2];  // tiles along x and y of the primitive's box
+    __shared__ unsigned long long s_incl[2][256];
+    __shared__ uint16_t s_t0[2][256][3];
+    __shared__ uint16_t s_nt[2][256][2];  // tiles along x and y of the primitive's box
     __shared__ unsigned long long s_warp[8];
     __shared__ unsigned long long s_excl;
     __shared__ unsigned s_hist[kMaxSortPasses][kMaxBuckets];
@@ -488,138 +492,151 @@ __global__ void __launch_bounds__(256) k_vprep(const VoxPrepLaunch a) {
     const VoxArgs& v = a.v;
     constexpr float kK = -0.72134752044448170368f;  // -0.5 * log2(e)
 
+    unsigned prev = 0xffffffffu;  // chunk awaiting emission (buffer cur ^ 1)
+    int cur = 0;
     while (true) {
         __syncthreads();
         if (tid == 0) s_chunk = atomicAdd(&a.ctrl->exact_chunk_ctr, 1u);
         __syncthreads();
         const unsigned chunk = s_chunk;
-        if (chunk >= nchunks) break;
-        const uint32_t i = chunk * 256 + tid;
-        unsigned long long val = 0;
-        if (i < a.n) {
-            float pf[11];
-            load_params(a.params, a.cap, i, pf);
-            double pd[11];
+        const bool have = chunk < nchunks;
+        if (have) {
+            const uint32_t i = chunk * 256 + tid;
+            unsigned long long val = 0;
+            if (i < a.n) {
+                float pf[11];
+                load_params(a.params, a.cap, i, pf);
+                double pd[11];
 #pragma unroll
-            for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
-            D33 sigma, rot, inv;
-            D3 scale;
-            int e = world_covariance(pd, v.mod, sigma, rot, scale);
-            if (!e) e = invert_cov(sigma, scale, v.mod, inv);
-            if (e) {
-                record_error(a.err, e, i);
-            } else {
-                const double alpha = 1.0 / (1.0 + exp(-pd[10]));
-                int lo[3], hi[3];
-                bool inside = true;
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const double half = v.support * sqrt(sigma.m[d][d]);
-                    const double lo_w = pd[d] - half, hi_w = pd[d] + half;
-                    lo[d] = max(0, x86_trunc_int(ceil((lo_w - v.origin[d]) / v.spacing[d])));
-                    hi[d] = min(v.dims[d] - 1, x86_trunc_int(floor((hi_w - v.origin[d]) / v.spacing[d])));
-                    if (lo[d] > hi[d]) inside = false;
-                }
-                if (inside) {
-                    unsigned np = 1;
-                    unsigned nt[3];
+                for (int k = 0; k < 11; ++k) pd[k] = (double)pf[k];
+                D33 sigma, rot, inv;
+                D3 scale;
+                int e = world_covariance(pd, v.mod, sigma, rot, scale);
+                if (!e) e = invert_cov(sigma, scale, v.mod, inv);
+                if (e) {
+                    record_error(a.err, e, i);
+                } else {
+                    const double alpha = 1.0 / (1.0 + exp(-pd[10]));
+                    int lo[3], hi[3];
+                    bool inside = true;
 #pragma unroll
                     for (int d = 0; d < 3; ++d) {
-                        const int t0 = lo[d] / v.tile[d];
-                        nt[d] = (unsigned)(hi[d] / v.tile[d] - t0 + 1);
-                        np *= nt[d];
-                        s_t0[tid][d] = (uint16_t)t0;
+                        const double half = v.support * sqrt(sigma.m[d][d]);
+                        const double lo_w = pd[d] - half, hi_w = pd[d] + half;
+                        lo[d] = max(0, x86_trunc_int(ceil((lo_w - v.origin[d]) / v.spacing[d])));
+                        hi[d] = min(v.dims[d] - 1, x86_trunc_int(floor((hi_w - v.origin[d]) / v.spacing[d])));
+                        if (lo[d] > hi[d]) inside = false;
                     }
-                    s_nt[tid][0] = (uint16_t)nt[0];
-                    s_nt[tid][1] = (uint16_t)nt[1];
-                    val = (1ull << 32) | np;
-                    VoxRecord rec;
-                    rec.mu[0] = pf[0];
-                    rec.mu[1] = pf[1];
-                    rec.mu[2] = pf[2];
-                    rec.log2a = (float)log2(alpha);
-                    rec.a[0] = (float)inv.m[0][0] * kK;
-                    rec.a[1] = (float)inv.m[1][1] * kK;
-                    rec.a[2] = (float)inv.m[2][2] * kK;
-                    rec.a[3] = (float)(inv.m[0][1] + inv.m[1][0]) * kK;
-                    rec.a[4] = (float)(inv.m[0][2] + inv.m[2][0]) * kK;
-                    rec.a[5] = (float)(inv.m[1][2] + inv.m[2][1]) * kK;
+                    if (inside) {
+                        unsigned np = 1;
+                        unsigned nt[3];
 #pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        rec.lo[d] = (uint16_t)lo[d];
-                        rec.hi[d] = (uint16_t)hi[d];
+                        for (int d = 0; d < 3; ++d) {
+                            const int t0 = lo[d] / v.tile[d];
+                            nt[d] = (unsigned)(hi[d] / v.tile[d] - t0 + 1);
+                            np *= nt[d];
+                            s_t0[cur][tid][d] = (uint16_t)t0;
+                        }
+                        s_nt[cur][tid][0] = (uint16_t)nt[0];
+                        s_nt[cur][tid][1] = (uint16_t)nt[1];
+                        val = (1ull << 32) | np;
+                        VoxRecord rec;
+                        rec.mu[0] = pf[0];
+                        rec.mu[1] = pf[1];
+                        rec.mu[2] = pf[2];
+                        rec.log2a = (float)log2(alpha);
+                        rec.a[0] = (float)inv.m[0][0] * kK;
+                        rec.a[1] = (float)inv.m[1][1] * kK;
+                        rec.a[2] = (float)inv.m[2][2] * kK;
+                        rec.a[3] = (float)(inv.m[0][1] + inv.m[1][0]) * kK;
+                        rec.a[4] = (float)(inv.m[0][2] + inv.m[2][0]) * kK;
+                        rec.a[5] = (float)(inv.m[1][2] + inv.m[2][1]) * kK;
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) {
+                            rec.lo[d] = (uint16_t)lo[d];
+                            rec.hi[d] = (uint16_t)hi[d];
+                        }
+                        rec.gidx = i;
+                        rec.pair_base = 0;
+                        rec.pad = 0;
+                        a.records[i] = rec;
                     }
-                    rec.gidx = i;
-                    rec.pair_base = 0;
-                    rec.pad = 0;
-                    a.records[i] = rec;
                 }
             }
-        }
-        unsigned long long incl = val;
+            unsigned long long incl = val;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            if (lane == 31) s_warp[warp] = incl;
+            __syncthreads();
+            unsigned long long add = 0;
+            for (int w = 0; w < warp; ++w) add += s_warp[w];
+            incl += add;
+            s_incl[cur][tid] = incl;
+            __syncthreads();
+            if (tid == 0) warp_prefix_publish(a.chunk_words, chunk, s_incl[cur][255]);
         }
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        unsigned long long add = 0;
-        for (int w = 0; w < warp; ++w) add += s_warp[w];
-        incl += add;
-        s_incl[tid] = incl;
-        __syncthreads();
-        const unsigned long long agg = s_incl[255];
-        if (warp == 0) {
-            const unsigned long long excl = warp_prefix_aggregates(a.chunk_words, chunk, agg);
-            if (lane == 0) {
-                s_excl = excl;
-                if (chunk == nchunks - 1) {
-                    const unsigned long long tot = excl + agg;
-                    const unsigned P = (unsigned)(tot & 0xffffffffull);
-                    a.ctrl->survivors = (unsigned)(tot >> 32);
-                    a.ctrl->pairs = P;
-                    a.ctrl->pair_overflow = (P > a.pair_cap) ? 1u : 0u;
+        if (prev != 0xffffffffu) {
+            const int pb = cur ^ 1;
+            const unsigned long long agg = s_incl[pb][255];
+            if (warp == 0) {
+                const unsigned long long excl = warp_prefix_aggregates(a.chunk_words, prev, agg, false);
+                if (lane == 0) {
+                    s_excl = excl;
+                    if (prev == nchunks - 1) {
+                        const unsigned long long tot = excl + agg;
+                        const unsigned P = (unsigned)(tot & 0xffffffffull);
+                        a.ctrl->survivors = (unsigned)(tot >> 32);
+                        a.ctrl->pairs = P;
+                        a.ctrl->pair_overflow = (P > a.pair_cap) ? 1u : 0u;
+                    }
+                }
+            }
+            __syncthreads();
+            const unsigned S0 = (unsigned)(s_excl >> 32);
+            const unsigned P0 = (unsigned)(s_excl & 0xffffffffull);
+            const unsigned long long* inc = s_incl[pb];
+            {
+                const uint32_t i = prev * 256 + tid;
+                const unsigned long long pv = tid ? inc[tid - 1] : 0ull;
+                if ((inc[tid] >> 32) != (pv >> 32)) {
+                    a.survivor_list[S0 + (unsigned)(pv >> 32)] = i;
+                    a.records[i].pair_base = P0 + (unsigned)(pv & 0xffffffffull);
+                }
+            }
+            const unsigned Pb = (unsigned)(agg & 0xffffffffull);
+            for (unsigned k = tid; k < Pb; k += 256) {
+                unsigned lo = 0, hi = 255;
+                while (lo < hi) {
+                    const unsigned mid = (lo + hi) >> 1;
+                    if ((unsigned)(inc[mid] & 0xffffffffull) > k) hi = mid; else lo = mid + 1;
+                }
+                const unsigned before = lo ? (unsigned)(inc[lo - 1] & 0xffffffffull) : 0u;
+                const unsigned local = k - before;
+                const unsigned ntx = s_nt[pb][lo][0], nty = s_nt[pb][lo][1];
+                const unsigned dx = local % ntx, rest = local / ntx;
+                const unsigned dy = rest % nty, dz = rest / nty;
+                // z-major tile index (voxelize.hpp:98-101): ((tz * ny) + ty) * nx + tx
+                const unsigned tile = ((s_t0[pb][lo][2] + dz) * (unsigned)v.ntiles[1] + (s_t0[pb][lo][1] + dy)) *
+                                          (unsigned)v.ntiles[0] + (s_t0[pb][lo][0] + dx);
+                const unsigned long long pos = (unsigned long long)P0 + k;
+                if (pos < a.pair_cap) {
+                    a.keys[pos] = tile;
+                    a.vals[pos] = prev * 256 + lo;
+                    if (a.passes > 0) {
+                        const unsigned st = (unsigned)(pos / ((uint64_t)kSortTile << a.tile_shift));
+                        sort_count(a.tile_hist0, a.sort_tiles_cap, dmask + 1, st, tile & dmask, 1u);
+                    }
+                    for (int ps = 0; ps < a.passes; ++ps)
+                        atomicAdd(&s_hist[ps][(tile >> (a.digit_bits * ps)) & dmask], 1u);
                 }
             }
         }
-        __syncthreads();
-        const unsigned S0 = (unsigned)(s_excl >> 32);
-        const unsigned P0 = (unsigned)(s_excl & 0xffffffffull);
-        {
-            const unsigned long long prev = tid ? s_incl[tid - 1] : 0ull;
-            if ((s_incl[tid] >> 32) != (prev >> 32)) {
-                a.survivor_list[S0 + (unsigned)(prev >> 32)] = i;
-                a.records[i].pair_base = P0 + (unsigned)(prev & 0xffffffffull);
-            }
-        }
-        const unsigned Pb = (unsigned)(agg & 0xffffffffull);
-        for (unsigned k = tid; k < Pb; k += 256) {
-            unsigned lo = 0, hi = 255;
-            while (lo < hi) {
-                const unsigned mid = (lo + hi) >> 1;
-                if ((unsigned)(s_incl[mid] & 0xffffffffull) > k) hi = mid; else lo = mid + 1;
-            }
-            const unsigned before = lo ? (unsigned)(s_incl[lo - 1] & 0xffffffffull) : 0u;
-            const unsigned local = k - before;
-            const unsigned ntx = s_nt[lo][0], nty = s_nt[lo][1];
-            const unsigned dx = local % ntx, rest = local / ntx;
-            const unsigned dy = rest % nty, dz = rest / nty;
-            // z-major tile index (voxelize.hpp:98-101): ((tz * ny) + ty) * nx + tx
-            const unsigned tile = ((s_t0[lo][2] + dz) * (unsigned)v.ntiles[1] + (s_t0[lo][1] + dy)) *
-                                      (unsigned)v.ntiles[0] + (s_t0[lo][0] + dx);
-            const unsigned long long pos = (unsigned long long)P0 + k;
-            if (pos < a.pair_cap) {
-                a.keys[pos] = tile;
-                a.vals[pos] = chunk * 256 + lo;
-                if (a.passes > 0) {
-                    const unsigned st = (unsigned)(pos / ((uint64_t)kSortTile << a.tile_shift));
-                    sort_count(a.tile_hist0, a.sort_tiles_cap, dmask + 1, st, tile & dmask, 1u);
-                }
-                for (int ps = 0; ps < a.passes; ++ps)
-                    atomicAdd(&s_hist[ps][(tile >> (a.digit_bits * ps)) & dmask], 1u);
-            }
-        }
+        if (!have) break;
+        prev = chunk;
+        cur ^= 1;
     }
     __syncthreads();
     for (int ps = 0; ps < a.passes; ++ps)

@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
     __shared__ unsigned s_whist[8][kMaxBuckets];   // per-warp digit counts -> offsets
     __shared__ unsigned s_base[kMaxBuckets];       // running digit offsets of this tile
     __shared__ unsigned s_gbase[kMaxBuckets];      // exclusive scan of the pass histogram
+    __shared__ unsigned s_delta[kMaxBuckets];      // round: output position - staging slot, per digit
     __shared__ unsigned s_wsum[32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -41,6 +42,10 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
     const unsigned ntiles = groups ? a.ngroups : (P + tile_keys - 1) / tile_keys;
     const unsigned nb = 1u << a.bits;
     const unsigned mask = nb - 1;
+    // narrow digits: a round's pairs are staged digit-major in shared memory so
+    // the scatter writes runs (C5's 64-digit passes: -2 us); at 512 digits
+    // (the voxelizer) runs average 2 pairs and the staging costs more (+7 us)
+    const bool staged = nb <= 256;
     if (blockIdx.x == 0 && tid == 0 && a.grp_begin) a.grp_begin[nb] = P;
     if (blockIdx.x == 0 && tid == 0 && !a.tile_hist_next) {
         // rows the filter clears before the next prepare: the largest tile
@@ -198,31 +203,106 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortLaunch a) 
                 rank[r] = prior + __popc(peers & lanemask_lt());
             }
             __syncthreads();
-            // per digit: exclusive prefix over warps on top of the running base
-            for (unsigned d = tid; d < nb; d += kSortThreads) {
-                unsigned base = s_base[d];
+            if (!staged) {
+                // wide digits (runs of ~2 pairs per digit per round): per digit,
+                // exclusive prefix over warps on top of the running base, then
+                // scatter directly
+                for (unsigned d = tid; d < nb; d += kSortThreads) {
+                    unsigned base = s_base[d];
 #pragma unroll
-                for (int w = 0; w < 8; ++w) {
-                    const unsigned c = s_whist[w][d];
-                    s_whist[w][d] = base;
-                    base += c;
+                    for (int w = 0; w < 8; ++w) {
+                        const unsigned c = s_whist[w][d];
+                        s_whist[w][d] = base;
+                        base += c;
+                    }
+                    s_base[d] = base;  // the next round of this tile continues here
                 }
-                s_base[d] = base;  // the next round of this tile continues here
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < kSortItems; ++r)
+                    if (seg + r * 32 + lane < lim) {
+                        const unsigned p = s_whist[warp][(key[r] >> a.shift) & mask] + rank[r];
+                        a.keys_out[p] = key[r];
+                        a.vals_out[p] = val[r];
+                        if (a.tile_hist_next) {
+                            const unsigned nd = (key[r] >> (a.shift + a.bits)) & (a.next_buckets - 1);
+                            sort_count(a.tile_hist_next, a.sort_tiles_cap, a.next_buckets, p / tile_keys, nd, 1u);
+                        }
+                    }
+                __syncthreads();
+                continue;
+            }
+            // per digit (4 consecutive per thread): exclusive prefix over warps on
+            // top of the running base; the round's digit counts, scanned over the
+            // digits, give each pair its slot in a digit-major staging order
+            {
+                const unsigned d0 = tid * 4;
+                unsigned cnt[4], tot = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const unsigned d = d0 + q;
+                    cnt[q] = 0;
+                    if (d < nb) {
+                        unsigned base = s_base[d];
+                        const unsigned b0 = base;
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) {
+                            const unsigned c = s_whist[w][d];
+                            s_whist[w][d] = base;
+                            base += c;
+                        }
+                        s_base[d] = base;  // the next round of this tile continues here
+                        cnt[q] = base - b0;
+                    }
+                    tot += cnt[q];
+                }
+                unsigned incl = tot;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += u;
+                }
+                if (lane == 31) s_wsum[warp] = incl;
+                __syncthreads();
+                unsigned loc = incl - tot;
+                for (int w = 0; w < warp; ++w) loc += s_wsum[w];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const unsigned d = d0 + q;
+                    // output position = staging slot + delta (mod 2^32)
+                    if (d < nb) s_delta[d] = (s_base[d] - cnt[q]) - loc;
+                    loc += cnt[q];
+                }
             }
             __syncthreads();
-            // scatter (+ next pass's per-tile digit counts)
+            unsigned pos[kSortItems];
 #pragma unroll
             for (int r = 0; r < kSortItems; ++r) {
-                const unsigned idx = seg + r * 32 + lane;
-                if (idx < lim) {
-                    const unsigned d = (key[r] >> a.shift) & mask;
-                    const unsigned pos = s_whist[warp][d] + rank[r];
-                    a.keys_out[pos] = key[r];
-                    a.vals_out[pos] = val[r];
-                    if (a.tile_hist_next) {
-                        const unsigned nd = (key[r] >> (a.shift + a.bits)) & (a.next_buckets - 1);
-                        sort_count(a.tile_hist_next, a.sort_tiles_cap, a.next_buckets, pos / tile_keys, nd, 1u);
-                    }
+                const unsigned d = (key[r] >> a.shift) & mask;
+                pos[r] = (seg + r * 32 + lane < lim) ? s_whist[warp][d] + rank[r] : 0u;
+            }
+            __syncthreads();  // the warp rows are read; they become the staging area
+            uint32_t* s_sk = &s_whist[0][0];
+            uint32_t* s_sv = &s_whist[1][0];
+#pragma unroll
+            for (int r = 0; r < kSortItems; ++r)
+                if (seg + r * 32 + lane < lim) {
+                    const unsigned L = pos[r] - s_delta[(key[r] >> a.shift) & mask];
+                    s_sk[L] = key[r];
+                    s_sv[L] = val[r];
+                }
+            __syncthreads();
+            // scatter from the staging order: consecutive threads write runs of
+            // one digit to consecutive positions (+ next pass's per-tile counts)
+            const unsigned nround = lim - r0;
+            for (unsigned L = tid; L < nround; L += kSortThreads) {
+                const uint32_t k = s_sk[L];
+                const unsigned p = L + s_delta[(k >> a.shift) & mask];
+                a.keys_out[p] = k;
+                a.vals_out[p] = s_sv[L];
+                if (a.tile_hist_next) {
+                    const unsigned nd = (k >> (a.shift + a.bits)) & (a.next_buckets - 1);
+                    sort_count(a.tile_hist_next, a.sort_tiles_cap, a.next_buckets, p / tile_keys, nd, 1u);
                 }
             }
             __syncthreads();

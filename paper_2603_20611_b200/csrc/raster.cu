@@ -228,34 +228,51 @@ __device__ __forceinline__ void ssim_dl_tile(const RasterLaunch& a, int x0, int 
         }
     }
     {
-        // all loads of the haloed g planes in flight at once, then to shared
+        // all loads of the haloed g planes in flight at once, then to shared;
+        // an interior tile's halo needs no reflection (the common case at large
+        // slices): one uniform branch per CTA, row r of the halo at g + r * W
         constexpr int kPer = (kSsimH * kSsimH + 255) / 256;
+        constexpr int kPlane = kSsimH * (kSsimH + 1);
         float v[3][kPer];
-        // an interior tile's halo needs no reflection (the common case at
-        // large slices): one test per CTA instead of reflect loops per load
+        int soff[kPer];  // r * (kSsimH + 1) + c = idx + r
         const bool inner = x0 >= kSsimR && y0 >= kSsimR && x0 + kTile + kSsimR <= W && y0 + kTile + kSsimR <= H;
+        if (inner) {
+            const float* g = a.ssim_g + (size_t)(y0 - kSsimR) * W + (x0 - kSsimR);
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int idx = threadIdx.x + k * 256;
-            if (idx < kSsimH * kSsimH) {
-                const int r = idx / kSsimH, c = idx % kSsimH;
-                const size_t o = inner ? (size_t)(y0 + r - kSsimR) * W + (x0 + c - kSsimR)
-                                       : (size_t)reflect_idx(y0 + r - kSsimR, H) * W + reflect_idx(x0 + c - kSsimR, W);
-                v[0][k] = a.ssim_g[o];
-                v[1][k] = a.ssim_g[P + o];
-                v[2][k] = a.ssim_g[2 * P + o];
+            for (int k = 0; k < kPer; ++k) {
+                const int idx = threadIdx.x + k * 256;
+                const int r = idx / kSsimH;
+                soff[k] = idx + r;
+                if (idx < kSsimH * kSsimH) {
+                    const unsigned o = (unsigned)(r * W + (idx - r * kSsimH));
+                    v[0][k] = g[o];
+                    v[1][k] = g[P + o];
+                    v[2][k] = g[2 * P + o];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const int idx = threadIdx.x + k * 256;
+                const int r = idx / kSsimH;
+                soff[k] = idx + r;
+                if (idx < kSsimH * kSsimH) {
+                    const size_t o = (size_t)reflect_idx(y0 + r - kSsimR, H) * W +
+                                     reflect_idx(x0 + (idx - r * kSsimH) - kSsimR, W);
+                    v[0][k] = a.ssim_g[o];
+                    v[1][k] = a.ssim_g[P + o];
+                    v[2][k] = a.ssim_g[2 * P + o];
+                }
             }
         }
+        float* sg = &s_g[0][0][0];
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int idx = threadIdx.x + k * 256;
-            if (idx < kSsimH * kSsimH) {
-                const int r = idx / kSsimH, c = idx % kSsimH;
-                s_g[0][r][c] = v[0][k];
-                s_g[1][r][c] = v[1][k];
-                s_g[2][r][c] = v[2][k];
+        for (int k = 0; k < kPer; ++k)
+            if (threadIdx.x + k * 256 < kSsimH * kSsimH) {
+                sg[soff[k]] = v[0][k];
+                sg[kPlane + soff[k]] = v[1][k];
+                sg[2 * kPlane + soff[k]] = v[2][k];
             }
-        }
     }
     __syncthreads();
     // rows: a thread filters 8 consecutive outputs of one plane row from 18

@@ -92,27 +92,45 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const LossLaunch a) {
     const int W = a.W, H = a.H;
     {
         // every load of the haloed tile in flight at once (a load-store loop
-        // would wait one global round trip per element)
+        // would wait one global round trip per element); an interior tile's
+        // halo needs no reflection: one uniform branch per CTA, each element's
+        // row divided once and its shared offset (r * (kH + 1) + c = idx + r) kept
         constexpr int kPer = (kH * kH + kSsimThreads - 1) / kSsimThreads;
         float vx[kPer], vy[kPer];
-        // an interior tile's halo needs no reflection: one test per CTA
+        int soff[kPer];
         const bool inner = X0 >= kR && Y0 >= kR && X0 + kT + kR <= W && Y0 + kT + kR <= H;
+        if (inner) {
+            const size_t base = (size_t)(Y0 - kR) * W + (X0 - kR);
+            const float* gx = a.image + base;
+            const float* gy = a.target + base;
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int idx = threadIdx.x + k * kSsimThreads;
-            if (idx < kH * kH) {
-                const int r = idx / kH, c = idx % kH;
-                const size_t o = inner ? (size_t)(Y0 + r - kR) * W + (X0 + c - kR)
-                                       : (size_t)reflect(Y0 + r - kR, H) * W + reflect(X0 + c - kR, W);
-                vx[k] = a.image[o];
-                vy[k] = a.target[o];
+            for (int k = 0; k < kPer; ++k) {
+                const int idx = threadIdx.x + k * kSsimThreads;
+                const int r = idx / kH;
+                soff[k] = idx + r;
+                if (idx < kH * kH) {
+                    const unsigned o = (unsigned)(r * W + (idx - r * kH));
+                    vx[k] = gx[o];
+                    vy[k] = gy[o];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const int idx = threadIdx.x + k * kSsimThreads;
+                const int r = idx / kH;
+                soff[k] = idx + r;
+                if (idx < kH * kH) {
+                    const size_t o = (size_t)reflect(Y0 + r - kR, H) * W + reflect(X0 + (idx - r * kH) - kR, W);
+                    vx[k] = a.image[o];
+                    vy[k] = a.target[o];
+                }
             }
         }
+        float2* sxy = &s_xy[0][0];
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int idx = threadIdx.x + k * kSsimThreads;
-            if (idx < kH * kH) s_xy[idx / kH][idx % kH] = make_float2(vx[k], vy[k]);
-        }
+        for (int k = 0; k < kPer; ++k)
+            if (threadIdx.x + k * kSsimThreads < kH * kH) sxy[soff[k]] = make_float2(vx[k], vy[k]);
     }
     __syncthreads();
     // rows (axis 0 of conv_nd, metrics.hpp:112-116): a thread filters 4
@@ -213,32 +231,48 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(const LossLaunch a) {
     const size_t P = (size_t)W * H;
     {
         // every load of the haloed tile in flight at once, then to shared (an
-        // interior tile's halo needs no reflection)
+        // interior tile's halo needs no reflection: one uniform branch per CTA)
         constexpr int kPer = (kH * kH + 255) / 256;
+        constexpr int kPlane = kH * (kH + 1);
         const bool inner = X0 >= kR && Y0 >= kR && X0 + kT + kR <= W && Y0 + kT + kR <= H;
         float v[3][kPer];
+        int soff[kPer];  // r * (kH + 1) + c = idx + r
+        if (inner) {
+            const float* g = a.g + (size_t)(Y0 - kR) * W + (X0 - kR);
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int idx = threadIdx.x + k * 256;
-            if (idx < kH * kH) {
-                const int r = idx / kH, c = idx % kH;
-                const size_t o = inner ? (size_t)(Y0 + r - kR) * W + (X0 + c - kR)
-                                       : (size_t)reflect(Y0 + r - kR, H) * W + reflect(X0 + c - kR, W);
-                v[0][k] = a.g[o];
-                v[1][k] = a.g[P + o];
-                v[2][k] = a.g[2 * P + o];
+            for (int k = 0; k < kPer; ++k) {
+                const int idx = threadIdx.x + k * 256;
+                const int r = idx / kH;
+                soff[k] = idx + r;
+                if (idx < kH * kH) {
+                    const unsigned o = (unsigned)(r * W + (idx - r * kH));
+                    v[0][k] = g[o];
+                    v[1][k] = g[P + o];
+                    v[2][k] = g[2 * P + o];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const int idx = threadIdx.x + k * 256;
+                const int r = idx / kH;
+                soff[k] = idx + r;
+                if (idx < kH * kH) {
+                    const size_t o = (size_t)reflect(Y0 + r - kR, H) * W + reflect(X0 + (idx - r * kH) - kR, W);
+                    v[0][k] = a.g[o];
+                    v[1][k] = a.g[P + o];
+                    v[2][k] = a.g[2 * P + o];
+                }
             }
         }
+        float* sg = &s_g[0][0][0];
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int idx = threadIdx.x + k * 256;
-            if (idx < kH * kH) {
-                const int r = idx / kH, c = idx % kH;
-                s_g[0][r][c] = v[0][k];
-                s_g[1][r][c] = v[1][k];
-                s_g[2][r][c] = v[2][k];
+        for (int k = 0; k < kPer; ++k)
+            if (threadIdx.x + k * 256 < kH * kH) {
+                sg[soff[k]] = v[0][k];
+                sg[kPlane + soff[k]] = v[1][k];
+                sg[2 * kPlane + soff[k]] = v[2][k];
             }
-        }
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < kH * kT; idx += blockDim.x) {
